@@ -1,0 +1,132 @@
+/*
+ * mmm_cu.h -- C ABI of the B200 (sm_100a) polynomial-arithmetic hot path.
+ *
+ * Drop-in boundary for the reference's arithmetic entry points
+ * (/root/reference/proj/include/mmm/, namespace mmm):
+ *
+ *   mmm_cu_mul      <- Poly oracle_mul(const Poly&, const Poly&, const Field&)      oracle.hpp:14
+ *                      MulResult run_multiplication(mp, F, a, b, s, l)             multiplication.hpp:29
+ *   mmm_cu_divmod   <- pair<Poly,Poly> oracle_divmod(a, b, F)                       oracle.hpp:25
+ *                      DivisionResult run_division(variant, mp, F, a, b, s)         division.hpp:18
+ *   mmm_cu_gcd      <- Poly oracle_gcd(a, b, F)                                     oracle.hpp:29
+ *                      GcdResult run_gcd(variant, mp, F, a, b, s)                   gcd.hpp:19
+ *   mmm_cu_ntt_mul  <- (no reference symbol: FFT product is new scope, SURVEY §0;
+ *                      its result is the unique product, == oracle_mul)
+ *   mmm_field_check <- Field::Field(int64) validation                               field.cpp:20-25
+ *   mmm_random_poly <- Poly random_poly(std::mt19937_64&, int64 terms, const Field&) poly.hpp:40
+ *
+ * Conventions (mirroring mmm::Poly, poly.hpp:16-30): a polynomial is a pointer
+ * to ascending uint32 coefficients and a length; length 0 is the zero
+ * polynomial.  Coefficients must be canonical residues in [0, p) of a prime
+ * p with 2 <= p < 2^31.  Host-buffer entry points return TRIMMED results
+ * (no leading zero words) with the length in *n_out, exactly like the
+ * reference's Poly results; batched and device entry points write fixed,
+ * untrimmed lengths.
+ *
+ * Errors: every entry point returns an mmm_status; the message of the last
+ * failure on the calling thread is mmm_last_error().  MMM_INVALID_ARGUMENT
+ * maps to std::invalid_argument (non-prime p, non-canonical coefficients,
+ * output capacity), MMM_DOMAIN_ERROR to std::domain_error (division by the
+ * zero polynomial, gcd of two zeros, inverse of zero), as the oracle throws
+ * them (oracle.cpp:52,71; field.cpp:28).
+ *
+ * Threading: pure functions without global state; host entry points run on a
+ * per-thread CUDA stream of the current device and are safe to call
+ * concurrently.  Device entry points are asynchronous on the
+ * caller's stream (a cudaStream_t passed as void*; NULL = legacy default).
+ */
+#ifndef MMM_CU_H
+#define MMM_CU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum mmm_status {
+    MMM_OK = 0,
+    MMM_INVALID_ARGUMENT = 1, /* std::invalid_argument */
+    MMM_DOMAIN_ERROR = 2,     /* std::domain_error */
+    MMM_CUDA_ERROR = 3,
+    MMM_NCCL_ERROR = 4,
+    MMM_SIM_ERROR = 5 /* mmm::SimError (machine.hpp:20-22): internal invariant */
+} mmm_status;
+
+const char* mmm_last_error(void);
+int mmm_version(void);
+/* Number of CUDA kernels this library has launched in this process. */
+uint64_t mmm_cu_launch_count(void);
+
+/* ---- field and inputs (host) ------------------------------------------- */
+int mmm_field_check(int64_t p);
+/* a^-1 mod p in *out; MMM_DOMAIN_ERROR for a == 0 (Field::inv, field.cpp:27-42). */
+int mmm_field_inv(int64_t a, int64_t p, int64_t* out);
+
+typedef struct mmm_rng mmm_rng; /* std::mt19937_64 */
+mmm_rng* mmm_rng_create(uint64_t seed);
+void mmm_rng_destroy(mmm_rng* g);
+uint64_t mmm_rng_next(mmm_rng* g);
+/* random_poly (poly.cpp:20-29): `terms` coefficients uniform in [0, p),
+ * leading one uniform in [1, p); same draws as the reference. */
+int mmm_random_poly(mmm_rng* g, int64_t terms, int64_t p, uint32_t* out);
+
+/* ---- host-buffer entry points (synchronous, trimmed results) ------------ */
+/* f = a*b; f_cap >= na+nb-1.  s = per-thread register tile (the paper's
+ * program parameter s), l = threads-per-block hint (ignored on B200). */
+int mmm_cu_mul(int64_t p, const uint32_t* a, int64_t na, const uint32_t* b, int64_t nb, int64_t s,
+               int64_t l, uint32_t* f, int64_t f_cap, int64_t* nf);
+/* (q, r) = divmod(a, b); q_cap >= na-nb+1, r_cap >= nb-1 (when na >= nb),
+ * else q = 0 and r = trimmed a (r_cap >= na).  s = heads retired per step. */
+int mmm_cu_divmod(int64_t p, const uint32_t* a, int64_t na, const uint32_t* b, int64_t nb,
+                  int64_t s, uint32_t* q, int64_t q_cap, int64_t* nq, uint32_t* r, int64_t r_cap,
+                  int64_t* nr);
+/* g = monic gcd(a, b); g_cap >= max(na, nb).  s = steps per matrix batch. */
+int mmm_cu_gcd(int64_t p, const uint32_t* a, int64_t na, const uint32_t* b, int64_t nb, int64_t s,
+               uint32_t* g, int64_t g_cap, int64_t* ng);
+/* f = a*b through a Stockham NTT; needs p - 1 divisible by the transform
+ * length (next power of two >= na+nb-1), else MMM_INVALID_ARGUMENT. */
+int mmm_cu_ntt_mul(int64_t p, const uint32_t* a, int64_t na, const uint32_t* b, int64_t nb,
+                   uint32_t* f, int64_t f_cap, int64_t* nf);
+
+/* ---- batched host entry points: `count` equal-shape instances, row-major
+ *      with leading dimensions; outputs untrimmed (fixed lengths). -------- */
+int mmm_cu_mul_batched(int64_t p, const uint32_t* A, int64_t lda, int64_t na, const uint32_t* B,
+                       int64_t ldb, int64_t nb, int64_t count, int64_t s, uint32_t* F, int64_t ldf);
+/* every B row must have a nonzero word at index nb-1; na >= nb.
+ * Q rows hold na-nb+1 words, R rows nb-1 words. */
+int mmm_cu_divmod_batched(int64_t p, const uint32_t* A, int64_t lda, int64_t na,
+                          const uint32_t* B, int64_t ldb, int64_t nb, int64_t count, int64_t s,
+                          uint32_t* Q, int64_t ldq, uint32_t* R, int64_t ldr);
+int mmm_cu_ntt_mul_batched(int64_t p, const uint32_t* A, int64_t lda, int64_t na,
+                           const uint32_t* B, int64_t ldb, int64_t nb, int64_t count, uint32_t* F,
+                           int64_t ldf);
+
+/* ---- device-pointer entry points (asynchronous on `stream`) -------------
+ * Inputs: canonical, na, nb >= 1, leading words as for the host versions.
+ * Outputs: fixed lengths (f: na+nb-1; q: na-nb+1; r: nb-1), untrimmed. */
+int mmm_cu_mul_dev(int64_t p, const uint32_t* d_a, int64_t na, const uint32_t* d_b, int64_t nb,
+                   int64_t s, uint32_t* d_f, void* stream);
+int mmm_cu_divmod_dev(int64_t p, const uint32_t* d_a, int64_t na, const uint32_t* d_b, int64_t nb,
+                      int64_t s, uint32_t* d_q, uint32_t* d_r, void* stream);
+/* d_g capacity max(na, nb); *d_ng (device int64) receives the gcd length. */
+int mmm_cu_gcd_dev(int64_t p, const uint32_t* d_a, int64_t na, const uint32_t* d_b, int64_t nb,
+                   int64_t s, uint32_t* d_g, int64_t* d_ng, void* stream);
+int mmm_cu_ntt_mul_dev(int64_t p, const uint32_t* d_a, int64_t na, const uint32_t* d_b,
+                       int64_t nb, uint32_t* d_f, void* stream);
+int mmm_cu_mul_batched_dev(int64_t p, const uint32_t* d_A, int64_t lda, int64_t na,
+                           const uint32_t* d_B, int64_t ldb, int64_t nb, int64_t count, int64_t s,
+                           uint32_t* d_F, int64_t ldf, void* stream);
+int mmm_cu_divmod_batched_dev(int64_t p, const uint32_t* d_A, int64_t lda, int64_t na,
+                              const uint32_t* d_B, int64_t ldb, int64_t nb, int64_t count,
+                              int64_t s, uint32_t* d_Q, int64_t ldq, uint32_t* d_R, int64_t ldr,
+                              void* stream);
+int mmm_cu_ntt_mul_batched_dev(int64_t p, const uint32_t* d_A, int64_t lda, int64_t na,
+                               const uint32_t* d_B, int64_t ldb, int64_t nb, int64_t count,
+                               uint32_t* d_F, int64_t ldf, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MMM_CU_H */

@@ -1,0 +1,482 @@
+// capi.cu -- the extern "C" boundary (include/mmm_cu.h).
+//
+// Validation and error mapping follow the reference entry points
+// (proj/src/oracle.cpp:8-78, proj/src/field.cpp:20-42, run_util.hpp:24-29);
+// all arithmetic runs in the sm_100a kernels behind the launch_* functions.
+// There is no CPU arithmetic fallback: if the CUDA path fails, the call
+// returns MMM_CUDA_ERROR.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <random>
+#include <string>
+
+#include "../../include/mmm_cu.h"
+#include "common.cuh"
+
+namespace mmm_cu {
+
+std::atomic<uint64_t> g_launches{0};
+
+Scratch::Scratch(cudaStream_t s) : stream(s) {
+    static std::once_flag once[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::call_once(once[dev & 63], [dev] {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    });
+}
+
+Scratch::~Scratch() {
+    for (void* p : blocks) cudaFreeAsync(p, stream);
+}
+
+}  // namespace mmm_cu
+
+using namespace mmm_cu;
+
+namespace {
+
+thread_local std::string t_err;
+
+template <class Fn>
+int guarded(Fn&& fn) {
+    try {
+        fn();
+        return MMM_OK;
+    } catch (const Error& e) {
+        t_err = e.what();
+        return e.status;
+    } catch (const std::bad_alloc&) {
+        t_err = "host allocation failed";
+        return MMM_INVALID_ARGUMENT;
+    } catch (const std::exception& e) {
+        t_err = e.what();
+        return MMM_SIM_ERROR;
+    }
+}
+
+// Field::Field (field.cpp:10-25).
+FieldParams field_or_throw(int64_t p) {
+    if (p < 2 || p >= (int64_t(1) << 31))
+        throw Error(ST_INVALID, "field: p must satisfy 2 <= p < 2^31, got " + std::to_string(p));
+    bool prime = p == 2 || (p % 2 != 0);
+    for (int64_t d = 3; prime && d * d <= p; d += 2)
+        if (p % d == 0) prime = false;
+    if (!prime) throw Error(ST_INVALID, "field: p must be prime, got " + std::to_string(p));
+    return make_field(uint32_t(p));
+}
+
+// validate_coeffs (run_util.hpp:24-29).
+void check_canonical(const uint32_t* c, int64_t n, uint32_t p, const char* who) {
+    if (n < 0) throw Error(ST_INVALID, std::string(who) + ": negative length");
+    if (n > 0 && c == nullptr) throw Error(ST_INVALID, std::string(who) + ": null pointer");
+    for (int64_t i = 0; i < n; ++i)
+        if (c[i] >= p)
+            throw Error(ST_INVALID,
+                        std::string(who) + ": coefficients must be canonical field elements");
+}
+
+int64_t trimmed_len(const uint32_t* c, int64_t n) {
+    while (n > 0 && c[n - 1] == 0) --n;
+    return n;
+}
+
+cudaStream_t thread_stream() {
+    thread_local cudaStream_t s = [] {
+        cudaStream_t st = nullptr;
+        MMM_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        return st;
+    }();
+    return s;
+}
+
+void need_cap(int64_t cap, int64_t need, const char* what) {
+    if (cap < need)
+        throw Error(ST_INVALID, std::string(what) + ": output capacity " + std::to_string(cap) +
+                                    " < " + std::to_string(need));
+}
+
+uint32_t* to_device(Scratch& s, const uint32_t* h, int64_t n) {
+    uint32_t* d = s.get<uint32_t>(size_t(n));
+    if (n) MMM_CUDA(cudaMemcpyAsync(d, h, size_t(n) * 4, cudaMemcpyHostToDevice, s.stream));
+    return d;
+}
+
+void to_host(uint32_t* h, const uint32_t* d, int64_t n, cudaStream_t st) {
+    if (n) MMM_CUDA(cudaMemcpyAsync(h, d, size_t(n) * 4, cudaMemcpyDeviceToHost, st));
+}
+
+void sync(cudaStream_t st) { MMM_CUDA(cudaStreamSynchronize(st)); }
+
+cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+}  // namespace
+
+struct mmm_rng {
+    std::mt19937_64 eng;
+};
+
+extern "C" {
+
+const char* mmm_last_error(void) { return t_err.c_str(); }
+int mmm_version(void) { return 1; }
+uint64_t mmm_cu_launch_count(void) { return g_launches.load(); }
+
+int mmm_field_check(int64_t p) {
+    return guarded([&] { field_or_throw(p); });
+}
+
+int mmm_field_inv(int64_t a, int64_t p, int64_t* out) {
+    return guarded([&] {
+        field_or_throw(p);
+        if (a < 0 || a >= p) throw Error(ST_INVALID, "field: non-canonical element");
+        if (a == 0) throw Error(ST_DOMAIN, "field: inverse of zero");
+        // extended Euclid, as Field::inv
+        int64_t old_r = a, r = p, old_t = 1, t = 0;
+        while (r != 0) {
+            int64_t q = old_r / r, tmp = old_r - q * r;
+            old_r = r;
+            r = tmp;
+            tmp = old_t - q * t;
+            old_t = t;
+            t = tmp;
+        }
+        old_t %= p;
+        *out = old_t < 0 ? old_t + p : old_t;
+    });
+}
+
+mmm_rng* mmm_rng_create(uint64_t seed) {
+    try {
+        return new mmm_rng{std::mt19937_64(seed)};
+    } catch (...) {
+        return nullptr;
+    }
+}
+void mmm_rng_destroy(mmm_rng* g) { delete g; }
+uint64_t mmm_rng_next(mmm_rng* g) { return g->eng(); }
+
+int mmm_random_poly(mmm_rng* g, int64_t terms, int64_t p, uint32_t* out) {
+    return guarded([&] {
+        field_or_throw(p);
+        if (terms < 1) throw Error(ST_INVALID, "random_poly: terms must be >= 1");
+        std::uniform_int_distribution<std::int64_t> any(0, p - 1);
+        std::uniform_int_distribution<std::int64_t> nonzero(1, p - 1);
+        for (int64_t i = 0; i + 1 < terms; ++i) out[i] = uint32_t(any(g->eng));
+        out[terms - 1] = uint32_t(nonzero(g->eng));
+    });
+}
+
+// ------------------------------------------------------------ multiply ----
+int mmm_cu_mul(int64_t p, const uint32_t* a, int64_t na, const uint32_t* b, int64_t nb, int64_t s,
+               int64_t l, uint32_t* f, int64_t f_cap, int64_t* nf) {
+    return guarded([&] {
+        const FieldParams F = field_or_throw(p);
+        check_canonical(a, na, F.p, "multiplication first operand");
+        check_canonical(b, nb, F.p, "multiplication second operand");
+        na = trimmed_len(a, na);
+        nb = trimmed_len(b, nb);
+        *nf = 0;
+        if (na == 0 || nb == 0) return;  // oracle.cpp:9
+        need_cap(f_cap, na + nb - 1, "multiplication");
+        cudaStream_t st = thread_stream();
+        {
+            Scratch sc(st);
+            const uint32_t* da = to_device(sc, a, na);
+            const uint32_t* db = to_device(sc, b, nb);
+            uint32_t* df = sc.get<uint32_t>(size_t(na + nb - 1));
+            launch_mul(F, da, na, db, nb, df, s, l, st);
+            to_host(f, df, na + nb - 1, st);
+        }
+        sync(st);
+        *nf = trimmed_len(f, na + nb - 1);
+    });
+}
+
+int mmm_cu_mul_dev(int64_t p, const uint32_t* d_a, int64_t na, const uint32_t* d_b, int64_t nb,
+                   int64_t s, uint32_t* d_f, void* stream) {
+    return guarded([&] {
+        const FieldParams F = field_or_throw(p);
+        if (na < 1 || nb < 1) throw Error(ST_INVALID, "multiplication: operands must be nonzero");
+        launch_mul(F, d_a, na, d_b, nb, d_f, s, 0, as_stream(stream));
+    });
+}
+
+int mmm_cu_mul_batched(int64_t p, const uint32_t* A, int64_t lda, int64_t na, const uint32_t* B,
+                       int64_t ldb, int64_t nb, int64_t count, int64_t s, uint32_t* Fo,
+                       int64_t ldf) {
+    return guarded([&] {
+        const FieldParams F = field_or_throw(p);
+        if (na < 1 || nb < 1 || count < 0 || lda < na || ldb < nb || ldf < na + nb - 1)
+            throw Error(ST_INVALID, "multiplication batch: bad shape");
+        for (int64_t i = 0; i < count; ++i) {
+            check_canonical(A + i * lda, na, F.p, "multiplication batch first operand");
+            check_canonical(B + i * ldb, nb, F.p, "multiplication batch second operand");
+        }
+        if (count == 0) return;
+        cudaStream_t st = thread_stream();
+        {
+            Scratch sc(st);
+            uint32_t* dA = sc.get<uint32_t>(size_t(count * na));
+            uint32_t* dB = sc.get<uint32_t>(size_t(count * nb));
+            uint32_t* dF = sc.get<uint32_t>(size_t(count * (na + nb - 1)));
+            MMM_CUDA(cudaMemcpy2DAsync(dA, na * 4, A, lda * 4, na * 4, count,
+                                       cudaMemcpyHostToDevice, st));
+            MMM_CUDA(cudaMemcpy2DAsync(dB, nb * 4, B, ldb * 4, nb * 4, count,
+                                       cudaMemcpyHostToDevice, st));
+            launch_mul_batched(F, dA, na, na, dB, nb, nb, count, dF, na + nb - 1, s, st);
+            MMM_CUDA(cudaMemcpy2DAsync(Fo, ldf * 4, dF, (na + nb - 1) * 4, (na + nb - 1) * 4,
+                                       count, cudaMemcpyDeviceToHost, st));
+        }
+        sync(st);
+    });
+}
+
+int mmm_cu_mul_batched_dev(int64_t p, const uint32_t* d_A, int64_t lda, int64_t na,
+                           const uint32_t* d_B, int64_t ldb, int64_t nb, int64_t count, int64_t s,
+                           uint32_t* d_F, int64_t ldf, void* stream) {
+    return guarded([&] {
+        const FieldParams F = field_or_throw(p);
+        if (na < 1 || nb < 1 || count < 0 || lda < na || ldb < nb || ldf < na + nb - 1)
+            throw Error(ST_INVALID, "multiplication batch: bad shape");
+        if (count) launch_mul_batched(F, d_A, lda, na, d_B, ldb, nb, count, d_F, ldf, s,
+                                      as_stream(stream));
+    });
+}
+
+// ------------------------------------------------------------- divmod -----
+int mmm_cu_divmod(int64_t p, const uint32_t* a, int64_t na, const uint32_t* b, int64_t nb,
+                  int64_t s, uint32_t* q, int64_t q_cap, int64_t* nq, uint32_t* r, int64_t r_cap,
+                  int64_t* nr) {
+    return guarded([&] {
+        const FieldParams F = field_or_throw(p);
+        check_canonical(a, na, F.p, "division dividend");
+        check_canonical(b, nb, F.p, "division divisor");
+        *nq = *nr = 0;
+        // oracle.cpp:52-55: b is used as given; a is trimmed.
+        if (nb == 0) throw Error(ST_DOMAIN, "divmod: division by the zero polynomial");
+        na = trimmed_len(a, na);
+        if (na < nb) {
+            need_cap(r_cap, na, "division remainder");
+            if (na) std::memcpy(r, a, size_t(na) * 4);
+            *nr = na;
+            return;
+        }
+        if (b[nb - 1] == 0) throw Error(ST_DOMAIN, "field: inverse of zero");
+        need_cap(q_cap, na - nb + 1, "division quotient");
+        need_cap(r_cap, nb - 1, "division remainder");
+        cudaStream_t st = thread_stream();
+        {
+            Scratch sc(st);
+            const uint32_t* da = to_device(sc, a, na);
+            const uint32_t* db = to_device(sc, b, nb);
+            uint32_t* dq = sc.get<uint32_t>(size_t(na - nb + 1));
+            uint32_t* dr = sc.get<uint32_t>(size_t(nb));
+            launch_divmod(F, da, na, db, nb, dq, dr, s, st);
+            to_host(q, dq, na - nb + 1, st);
+            to_host(r, dr, nb - 1, st);
+        }
+        sync(st);
+        *nq = trimmed_len(q, na - nb + 1);
+        *nr = trimmed_len(r, nb - 1);
+    });
+}
+
+int mmm_cu_divmod_dev(int64_t p, const uint32_t* d_a, int64_t na, const uint32_t* d_b, int64_t nb,
+                      int64_t s, uint32_t* d_q, uint32_t* d_r, void* stream) {
+    return guarded([&] {
+        const FieldParams F = field_or_throw(p);
+        if (nb < 1 || na < nb) throw Error(ST_INVALID, "division: requires deg a >= deg b >= 0");
+        launch_divmod(F, d_a, na, d_b, nb, d_q, d_r, s, as_stream(stream));
+    });
+}
+
+int mmm_cu_divmod_batched(int64_t p, const uint32_t* A, int64_t lda, int64_t na,
+                          const uint32_t* B, int64_t ldb, int64_t nb, int64_t count, int64_t s,
+                          uint32_t* Q, int64_t ldq, uint32_t* R, int64_t ldr) {
+    return guarded([&] {
+        const FieldParams F = field_or_throw(p);
+        if (nb < 1 || na < nb || count < 0 || lda < na || ldb < nb || ldq < na - nb + 1 ||
+            ldr < nb - 1)
+            throw Error(ST_INVALID, "division batch: bad shape");
+        for (int64_t i = 0; i < count; ++i) {
+            check_canonical(A + i * lda, na, F.p, "division batch dividend");
+            check_canonical(B + i * ldb, nb, F.p, "division batch divisor");
+            if (B[i * ldb + nb - 1] == 0) throw Error(ST_DOMAIN, "field: inverse of zero");
+        }
+        if (count == 0) return;
+        const int64_t lq = na - nb + 1, lr = nb - 1;
+        cudaStream_t st = thread_stream();
+        {
+            Scratch sc(st);
+            uint32_t* dA = sc.get<uint32_t>(size_t(count * na));
+            uint32_t* dB = sc.get<uint32_t>(size_t(count * nb));
+            uint32_t* dQ = sc.get<uint32_t>(size_t(count * lq));
+            uint32_t* dR = sc.get<uint32_t>(size_t(count * std::max<int64_t>(lr, 1)));
+            MMM_CUDA(cudaMemcpy2DAsync(dA, na * 4, A, lda * 4, na * 4, count,
+                                       cudaMemcpyHostToDevice, st));
+            MMM_CUDA(cudaMemcpy2DAsync(dB, nb * 4, B, ldb * 4, nb * 4, count,
+                                       cudaMemcpyHostToDevice, st));
+            launch_divmod_batched(F, dA, na, na, dB, nb, nb, count, dQ, lq, dR, lr, s, st);
+            MMM_CUDA(cudaMemcpy2DAsync(Q, ldq * 4, dQ, lq * 4, lq * 4, count,
+                                       cudaMemcpyDeviceToHost, st));
+            if (lr)
+                MMM_CUDA(cudaMemcpy2DAsync(R, ldr * 4, dR, lr * 4, lr * 4, count,
+                                           cudaMemcpyDeviceToHost, st));
+        }
+        sync(st);
+    });
+}
+
+int mmm_cu_divmod_batched_dev(int64_t p, const uint32_t* d_A, int64_t lda, int64_t na,
+                              const uint32_t* d_B, int64_t ldb, int64_t nb, int64_t count,
+                              int64_t s, uint32_t* d_Q, int64_t ldq, uint32_t* d_R, int64_t ldr,
+                              void* stream) {
+    return guarded([&] {
+        const FieldParams F = field_or_throw(p);
+        if (nb < 1 || na < nb || count < 0 || lda < na || ldb < nb || ldq < na - nb + 1 ||
+            ldr < nb - 1)
+            throw Error(ST_INVALID, "division batch: bad shape");
+        if (count)
+            launch_divmod_batched(F, d_A, lda, na, d_B, ldb, nb, count, d_Q, ldq, d_R, ldr, s,
+                                  as_stream(stream));
+    });
+}
+
+// ---------------------------------------------------------------- gcd -----
+int mmm_cu_gcd(int64_t p, const uint32_t* a, int64_t na, const uint32_t* b, int64_t nb, int64_t s,
+               uint32_t* g, int64_t g_cap, int64_t* ng) {
+    return guarded([&] {
+        const FieldParams F = field_or_throw(p);
+        check_canonical(a, na, F.p, "gcd first operand");
+        check_canonical(b, nb, F.p, "gcd second operand");
+        na = trimmed_len(a, na);
+        nb = trimmed_len(b, nb);
+        *ng = 0;
+        if (na == 0 && nb == 0) throw Error(ST_DOMAIN, "gcd: both inputs are zero");
+        need_cap(g_cap, std::max(na, nb), "gcd");
+        cudaStream_t st = thread_stream();
+        int64_t len = 0;
+        {
+            Scratch sc(st);
+            const uint32_t* da = to_device(sc, a, na);
+            const uint32_t* db = to_device(sc, b, nb);
+            uint32_t* dg = sc.get<uint32_t>(size_t(std::max(na, nb)));
+            int64_t* dng = sc.get<int64_t>(1);
+            launch_gcd(F, da, na, db, nb, dg, dng, s, st);
+            MMM_CUDA(cudaMemcpyAsync(&len, dng, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+            sync(st);
+            if (len < 0 || len > std::max(na, nb)) throw Error(ST_SIM, "gcd: bad result length");
+            to_host(g, dg, len, st);
+        }
+        sync(st);
+        *ng = len;
+    });
+}
+
+int mmm_cu_gcd_dev(int64_t p, const uint32_t* d_a, int64_t na, const uint32_t* d_b, int64_t nb,
+                   int64_t s, uint32_t* d_g, int64_t* d_ng, void* stream) {
+    return guarded([&] {
+        const FieldParams F = field_or_throw(p);
+        if (na < 0 || nb < 0 || (na == 0 && nb == 0))
+            throw Error(ST_DOMAIN, "gcd: both inputs are zero");
+        launch_gcd(F, d_a, na, d_b, nb, d_g, d_ng, s, as_stream(stream));
+    });
+}
+
+// ---------------------------------------------------------------- NTT -----
+int mmm_cu_ntt_mul(int64_t p, const uint32_t* a, int64_t na, const uint32_t* b, int64_t nb,
+                   uint32_t* f, int64_t f_cap, int64_t* nf) {
+    return guarded([&] {
+        const FieldParams F = field_or_throw(p);
+        check_canonical(a, na, F.p, "ntt first operand");
+        check_canonical(b, nb, F.p, "ntt second operand");
+        na = trimmed_len(a, na);
+        nb = trimmed_len(b, nb);
+        *nf = 0;
+        if (na == 0 || nb == 0) return;
+        if (!ntt_supported(F.p, na + nb - 1))
+            throw Error(ST_INVALID, "ntt: p has no 2-adic root of unity of the needed order");
+        need_cap(f_cap, na + nb - 1, "ntt");
+        cudaStream_t st = thread_stream();
+        {
+            Scratch sc(st);
+            const uint32_t* da = to_device(sc, a, na);
+            const uint32_t* db = to_device(sc, b, nb);
+            uint32_t* df = sc.get<uint32_t>(size_t(na + nb - 1));
+            launch_ntt_mul(F, da, na, db, nb, df, st);
+            to_host(f, df, na + nb - 1, st);
+        }
+        sync(st);
+        *nf = trimmed_len(f, na + nb - 1);
+    });
+}
+
+int mmm_cu_ntt_mul_dev(int64_t p, const uint32_t* d_a, int64_t na, const uint32_t* d_b,
+                       int64_t nb, uint32_t* d_f, void* stream) {
+    return guarded([&] {
+        const FieldParams F = field_or_throw(p);
+        if (na < 1 || nb < 1) throw Error(ST_INVALID, "ntt: operands must be nonzero");
+        if (!ntt_supported(F.p, na + nb - 1))
+            throw Error(ST_INVALID, "ntt: p has no 2-adic root of unity of the needed order");
+        launch_ntt_mul(F, d_a, na, d_b, nb, d_f, as_stream(stream));
+    });
+}
+
+int mmm_cu_ntt_mul_batched(int64_t p, const uint32_t* A, int64_t lda, int64_t na,
+                           const uint32_t* B, int64_t ldb, int64_t nb, int64_t count, uint32_t* Fo,
+                           int64_t ldf) {
+    return guarded([&] {
+        const FieldParams F = field_or_throw(p);
+        if (na < 1 || nb < 1 || count < 0 || lda < na || ldb < nb || ldf < na + nb - 1)
+            throw Error(ST_INVALID, "ntt batch: bad shape");
+        if (!ntt_supported(F.p, na + nb - 1))
+            throw Error(ST_INVALID, "ntt: p has no 2-adic root of unity of the needed order");
+        for (int64_t i = 0; i < count; ++i) {
+            check_canonical(A + i * lda, na, F.p, "ntt batch first operand");
+            check_canonical(B + i * ldb, nb, F.p, "ntt batch second operand");
+        }
+        if (count == 0) return;
+        const int64_t nf = na + nb - 1;
+        cudaStream_t st = thread_stream();
+        {
+            Scratch sc(st);
+            uint32_t* dA = sc.get<uint32_t>(size_t(count * na));
+            uint32_t* dB = sc.get<uint32_t>(size_t(count * nb));
+            uint32_t* dF = sc.get<uint32_t>(size_t(count * nf));
+            MMM_CUDA(cudaMemcpy2DAsync(dA, na * 4, A, lda * 4, na * 4, count,
+                                       cudaMemcpyHostToDevice, st));
+            MMM_CUDA(cudaMemcpy2DAsync(dB, nb * 4, B, ldb * 4, nb * 4, count,
+                                       cudaMemcpyHostToDevice, st));
+            launch_ntt_mul_batched(F, dA, na, na, dB, nb, nb, count, dF, nf, st);
+            MMM_CUDA(cudaMemcpy2DAsync(Fo, ldf * 4, dF, nf * 4, nf * 4, count,
+                                       cudaMemcpyDeviceToHost, st));
+        }
+        sync(st);
+    });
+}
+
+int mmm_cu_ntt_mul_batched_dev(int64_t p, const uint32_t* d_A, int64_t lda, int64_t na,
+                               const uint32_t* d_B, int64_t ldb, int64_t nb, int64_t count,
+                               uint32_t* d_F, int64_t ldf, void* stream) {
+    return guarded([&] {
+        const FieldParams F = field_or_throw(p);
+        if (na < 1 || nb < 1 || count < 0 || lda < na || ldb < nb || ldf < na + nb - 1)
+            throw Error(ST_INVALID, "ntt batch: bad shape");
+        if (!ntt_supported(F.p, na + nb - 1))
+            throw Error(ST_INVALID, "ntt: p has no 2-adic root of unity of the needed order");
+        if (count)
+            launch_ntt_mul_batched(F, d_A, lda, na, d_B, ldb, nb, count, d_F, ldf,
+                                   as_stream(stream));
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,94 @@
+// common.cuh -- host-side plumbing shared by the kernel translation units:
+// status propagation, the launch counter behind mmm_cu_launch_count(), and
+// stream-ordered scratch memory.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "field.cuh"
+
+namespace mmm_cu {
+
+// Maps 1:1 onto mmm_status (include/mmm_cu.h).
+struct Error : std::runtime_error {
+    int status;
+    Error(int st, const std::string& m) : std::runtime_error(m), status(st) {}
+};
+constexpr int ST_INVALID = 1, ST_DOMAIN = 2, ST_CUDA = 3, ST_NCCL = 4, ST_SIM = 5;
+
+inline void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        throw Error(ST_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define MMM_CUDA(x) ::mmm_cu::cuda_check((x), #x)
+#define MMM_LAUNCHED(n) ::mmm_cu::note_launch(n)
+
+// Every kernel launch of this library bumps this counter (bench.py reports
+// the number inside its timed region as gpu_launches).
+extern std::atomic<uint64_t> g_launches;
+inline void note_launch(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+inline void check_launch(const char* what) {
+    note_launch();
+    cuda_check(cudaGetLastError(), what);
+}
+
+// Stream-ordered scratch: cudaMallocAsync from the device's default pool
+// (its release threshold is raised once so blocks stay cached across calls).
+struct Scratch {
+    cudaStream_t stream;
+    std::vector<void*> blocks;
+    explicit Scratch(cudaStream_t s);
+    ~Scratch();
+    template <class T>
+    T* get(size_t count) {
+        void* p = nullptr;
+        if (count == 0) count = 1;
+        MMM_CUDA(cudaMallocAsync(&p, count * sizeof(T), stream));
+        blocks.push_back(p);
+        return static_cast<T*>(p);
+    }
+    Scratch(const Scratch&) = delete;
+    Scratch& operator=(const Scratch&) = delete;
+};
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+inline int sm_count() {
+    static int n = [] {
+        int dev = 0, v = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return v > 0 ? v : 148;
+    }();
+    return n;
+}
+
+// ---- launchers (device pointers, async on `st`; outputs untrimmed) --------
+// multiplication: f[0 .. na+nb-1) = a * b.  s/l are tile hints (mul.cu).
+void launch_mul(const FieldParams& F, const uint32_t* a, int64_t na, const uint32_t* b, int64_t nb,
+                uint32_t* f, int64_t s, int64_t l, cudaStream_t st);
+void launch_mul_batched(const FieldParams& F, const uint32_t* A, int64_t lda, int64_t na,
+                        const uint32_t* B, int64_t ldb, int64_t nb, int64_t count, uint32_t* Fo,
+                        int64_t ldf, int64_t s, cudaStream_t st);
+// division: q[0 .. na-nb+1), r[0 .. nb-1).  b[nb-1] != 0, na >= nb >= 1.
+void launch_divmod(const FieldParams& F, const uint32_t* a, int64_t na, const uint32_t* b,
+                   int64_t nb, uint32_t* q, uint32_t* r, int64_t s, cudaStream_t st);
+void launch_divmod_batched(const FieldParams& F, const uint32_t* A, int64_t lda, int64_t na,
+                           const uint32_t* B, int64_t ldb, int64_t nb, int64_t count, uint32_t* Q,
+                           int64_t ldq, uint32_t* R, int64_t ldr, int64_t s, cudaStream_t st);
+// gcd: g (capacity max(na,nb)) = monic gcd, *d_ng = its length.
+void launch_gcd(const FieldParams& F, const uint32_t* a, int64_t na, const uint32_t* b, int64_t nb,
+                uint32_t* g, int64_t* d_ng, int64_t s, cudaStream_t st);
+// NTT product: f[0 .. na+nb-1).  Requires 2-adic roots of the needed length.
+bool ntt_supported(uint32_t p, int64_t out_len);
+void launch_ntt_mul(const FieldParams& F, const uint32_t* a, int64_t na, const uint32_t* b,
+                    int64_t nb, uint32_t* f, cudaStream_t st);
+void launch_ntt_mul_batched(const FieldParams& F, const uint32_t* A, int64_t lda, int64_t na,
+                            const uint32_t* B, int64_t ldb, int64_t nb, int64_t count,
+                            uint32_t* Fo, int64_t ldf, cudaStream_t st);
+
+}  // namespace mmm_cu

@@ -1,0 +1,72 @@
+// conv.cuh -- the register-tiled modular convolution engine shared by the
+// plain-multiplication, division-update and GCD matrix-apply kernels.
+//
+// One thread owns R consecutive outputs and walks the terms in blocks of R:
+// per block it loads R term words (warp-uniform, LDS.128 broadcast) and R new
+// window words (its own, LDS.128), then issues R*R IMAD.WIDE.U32 into 64-bit
+// accumulators.  This is the paper's "each thread computes s x s partial
+// products from locally staged coefficients" (Alg. 5-7;
+// proj/src/multiplication.cpp:85-103 simulates it with s = R), re-expressed
+// for registers: the 2R-1 window words slide down by R per block so only R
+// are reloaded.  Accumulators are folded (fold(), field.cuh) every
+// F.fold_terms products, so a block of R terms costs R*R IMAD.WIDE plus an
+// amortised fold.
+#pragma once
+#include <cstdint>
+
+#include "field.cuh"
+
+namespace mmm_cu {
+
+// acc[r] += sum_{u < nblk*R} sw[u] * sv[base + r - u]
+// Requirements: R in {1,2,4,8,16}; for R % 4 == 0: sw 16-byte aligned and
+// base % 4 == 3 (so every window reload is one aligned uint4 per 4 words).
+// `since` counts products added since the last fold (carried across calls).
+template <int R>
+__device__ __forceinline__ void conv_accumulate(uint64_t (&acc)[R], const uint32_t* __restrict__ sw,
+                                                int nblk, const uint32_t* __restrict__ sv, int base,
+                                                uint32_t& since, const FieldParams& F) {
+    uint32_t W[2 * R - 1];
+#pragma unroll
+    for (int j = 0; j < R - 1; ++j) W[R + j] = sv[base + 1 + j];
+    for (int blk = 0; blk < nblk; ++blk) {
+        const int u0 = blk * R;
+        if (since + R > F.fold_terms) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) acc[r] = fold(acc[r], F);
+            since = 0;
+        }
+        since += R;
+        uint32_t X[R];
+        const int lo = base - u0 - (R - 1);
+        if constexpr (R % 4 == 0) {
+#pragma unroll
+            for (int q = 0; q < R / 4; ++q) {
+                const uint4 w = *reinterpret_cast<const uint4*>(sv + lo + 4 * q);
+                W[4 * q + 0] = w.x;
+                W[4 * q + 1] = w.y;
+                W[4 * q + 2] = w.z;
+                W[4 * q + 3] = w.w;
+                const uint4 x = *reinterpret_cast<const uint4*>(sw + u0 + 4 * q);
+                X[4 * q + 0] = x.x;
+                X[4 * q + 1] = x.y;
+                X[4 * q + 2] = x.z;
+                X[4 * q + 3] = x.w;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < R; ++j) {
+                W[j] = sv[lo + j];
+                X[j] = sw[u0 + j];
+            }
+        }
+#pragma unroll
+        for (int t = 0; t < R; ++t)
+#pragma unroll
+            for (int r = 0; r < R; ++r) acc[r] = mad_wide(X[t], W[(R - 1) + r - t], acc[r]);
+#pragma unroll
+        for (int j = R - 2; j >= 0; --j) W[j + R] = W[j];
+    }
+}
+
+}  // namespace mmm_cu

@@ -1,0 +1,195 @@
+// mul.cu -- plain (schoolbook) multiplication over Z/pZ on sm_100a.
+//
+// Replaces the MUL + ADD kernel program of run_multiplication
+// (proj/src/multiplication.cpp:23-164; Alg. 5-7) and computes the
+// same product as oracle_mul (proj/src/oracle.cpp:8-15).
+//
+// Output-stationary 2-D tiling of the (k, i) parallelogram {0 <= i < na,
+// 0 <= k - i < nb}: a CTA of MUL_T threads owns TK = MUL_T*R consecutive
+// outputs ("k-tile") and one contiguous range of input indices i ("item"),
+// staged through shared memory MUL_TI terms at a time; each thread keeps R
+// outputs in 64-bit registers (conv.cuh).  The reference's M array of
+// (x-1)*y partial rows and its log2 ADD rounds disappear: when a k-tile's
+// i-range is split over several items, the items' reduced partial sums
+// (< p each) meet in a 64-bit global accumulator through RED.ADD.64 and one
+// finalize pass reduces them -- the segmented add of the paper, done by
+// atomics in L2 instead of log-round launches.  Batched products give each
+// instance whole k-tiles (no split, direct stores).
+#include "common.cuh"
+#include "conv.cuh"
+
+namespace mmm_cu {
+
+constexpr int MUL_T = 128;   // threads per CTA
+constexpr int MUL_TI = 512;  // terms per shared-memory chunk
+
+struct MulArgs {
+    const uint32_t* a;
+    const uint32_t* b;
+    uint32_t* f;
+    unsigned long long* acc;  // split k-tiles accumulate here (single instance)
+    int64_t na, nb, lda, ldb, ldf;
+    int64_t chunk;  // i-range per item
+    FieldParams F;
+};
+
+template <int R>
+__global__ void __launch_bounds__(MUL_T) mul_kernel(MulArgs g) {
+    constexpr int TK = MUL_T * R;
+    constexpr int ORIGIN = MUL_TI + 3;  // == 3 (mod 4): aligned window reloads
+    __shared__ __align__(16) uint32_t sw[MUL_TI];
+    __shared__ __align__(16) uint32_t sv[MUL_TI + TK + 4];
+
+    const int64_t inst = blockIdx.z;
+    const uint32_t* __restrict__ a = g.a + inst * g.lda;
+    const uint32_t* __restrict__ b = g.b + inst * g.ldb;
+    const int64_t na = g.na, nb = g.nb, nf = na + nb - 1;
+    const int64_t k0 = int64_t(blockIdx.y) * TK;
+    if (k0 >= nf) return;
+    const int64_t ilo = k0 - (nb - 1) > 0 ? k0 - (nb - 1) : 0;
+    const int64_t ihi = k0 + TK < na ? k0 + TK : na;
+    const int64_t i_begin = ilo + int64_t(blockIdx.x) * g.chunk;
+    if (i_begin >= ihi) return;
+    const int64_t i_end = i_begin + g.chunk < ihi ? i_begin + g.chunk : ihi;
+    const bool split = g.acc != nullptr && (ihi - ilo) > g.chunk;
+
+    uint64_t acc[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[r] = 0;
+    uint32_t since = 0;
+    const int base = ORIGIN + int(threadIdx.x) * R;
+
+    for (int64_t ic = i_begin; ic < i_end; ic += MUL_TI) {
+        const int cnt = int(i_end - ic < MUL_TI ? i_end - ic : MUL_TI);
+        __syncthreads();
+        for (int u = threadIdx.x; u < MUL_TI; u += MUL_T) sw[u] = u < cnt ? a[ic + u] : 0u;
+        const int64_t off = k0 - ic - ORIGIN;  // sv[x] = b[x + off]
+        for (int x = threadIdx.x; x < MUL_TI + TK + 4; x += MUL_T) {
+            const int64_t j = x + off;
+            sv[x] = (j >= 0 && j < nb) ? b[j] : 0u;
+        }
+        __syncthreads();
+        conv_accumulate<R>(acc, sw, (cnt + R - 1) / R, sv, base, since, g.F);
+    }
+
+    uint32_t* __restrict__ f = g.f + inst * g.ldf;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int64_t k = k0 + int64_t(threadIdx.x) * R + r;
+        if (k < nf) {
+            const uint32_t v = reduce(acc[r], g.F);
+            if (split)
+                atomicAdd(g.acc + k, (unsigned long long)v);
+            else
+                f[k] = v;
+        }
+    }
+}
+
+// f[k] = acc[k] mod p for the k-tiles that were split across items.
+__global__ void mul_finalize_kernel(const unsigned long long* __restrict__ acc, uint32_t* f,
+                                    int64_t nf, int64_t nb, int64_t na, int tk, int64_t chunk,
+                                    FieldParams F) {
+    const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= nf) return;
+    const int64_t k0 = (k / tk) * tk;
+    const int64_t ilo = k0 - (nb - 1) > 0 ? k0 - (nb - 1) : 0;
+    const int64_t ihi = k0 + tk < na ? k0 + tk : na;
+    if (ihi - ilo > chunk) f[k] = reduce(acc[k], F);
+}
+
+namespace {
+
+int pick_tile(int64_t s, const FieldParams& F) {
+    int R = 1;
+    for (int c : {2, 4, 8, 16})
+        if (c <= s) R = c;
+    while (R > 1 && uint32_t(R) > F.fold_terms) R /= 2;
+    return R;
+}
+
+template <int R>
+void launch_tile(const MulArgs& g, dim3 grid, cudaStream_t st) {
+    mul_kernel<R><<<grid, MUL_T, 0, st>>>(g);
+    check_launch("mul_kernel");
+}
+
+void dispatch(int R, const MulArgs& g, dim3 grid, cudaStream_t st) {
+    switch (R) {
+        case 16: launch_tile<16>(g, grid, st); break;
+        case 8: launch_tile<8>(g, grid, st); break;
+        case 4: launch_tile<4>(g, grid, st); break;
+        case 2: launch_tile<2>(g, grid, st); break;
+        default: launch_tile<1>(g, grid, st); break;
+    }
+}
+
+}  // namespace
+
+void launch_mul(const FieldParams& F, const uint32_t* a, int64_t na, const uint32_t* b, int64_t nb,
+                uint32_t* f, int64_t s, int64_t /*l*/, cudaStream_t st) {
+    const int R = pick_tile(s, F);
+    const int64_t TK = int64_t(MUL_T) * R;
+    const int64_t nf = na + nb - 1;
+    const int64_t nkt = ceil_div(nf, TK);
+    if (nkt > 65535) throw Error(ST_INVALID, "multiplication: product too long for plain kernel");
+    // Total staged terms over all k-tiles; aim for ~8 items per SM.
+    int64_t total = 0, longest = 0;
+    for (int64_t kt = 0; kt < nkt; ++kt) {
+        const int64_t k0 = kt * TK;
+        const int64_t lo = std::max<int64_t>(0, k0 - (nb - 1)), hi = std::min<int64_t>(na, k0 + TK);
+        total += hi - lo;
+        longest = std::max(longest, hi - lo);
+    }
+    const int64_t target = 8LL * sm_count();
+    int64_t chunk = ceil_div(ceil_div(total, target), MUL_TI) * MUL_TI;
+    if (chunk < MUL_TI) chunk = MUL_TI;
+    const int64_t items = ceil_div(longest, chunk);
+
+    Scratch scratch(st);
+    MulArgs g{};
+    g.a = a;
+    g.b = b;
+    g.f = f;
+    g.na = na;
+    g.nb = nb;
+    g.chunk = chunk;
+    g.F = F;
+    if (items > 1) {
+        g.acc = scratch.get<unsigned long long>(size_t(nf));
+        MMM_CUDA(cudaMemsetAsync(g.acc, 0, size_t(nf) * sizeof(unsigned long long), st));
+    }
+    dispatch(R, g, dim3(unsigned(items), unsigned(nkt), 1), st);
+    if (items > 1) {
+        mul_finalize_kernel<<<unsigned(ceil_div(nf, 256)), 256, 0, st>>>(g.acc, f, nf, nb, na,
+                                                                         int(TK), chunk, F);
+        check_launch("mul_finalize_kernel");
+    }
+}
+
+void launch_mul_batched(const FieldParams& F, const uint32_t* A, int64_t lda, int64_t na,
+                        const uint32_t* B, int64_t ldb, int64_t nb, int64_t count, uint32_t* Fo,
+                        int64_t ldf, int64_t s, cudaStream_t st) {
+    const int R = pick_tile(s, F);
+    const int64_t TK = int64_t(MUL_T) * R;
+    const int64_t nf = na + nb - 1;
+    const int64_t nkt = ceil_div(nf, TK);
+    if (nkt > 65535) throw Error(ST_INVALID, "multiplication: product too long for plain kernel");
+    MulArgs g{};
+    g.na = na;
+    g.nb = nb;
+    g.lda = lda;
+    g.ldb = ldb;
+    g.ldf = ldf;
+    g.chunk = na + nb;  // one item per k-tile: no split, direct stores
+    g.F = F;
+    for (int64_t c0 = 0; c0 < count; c0 += 65535) {
+        const int64_t c = std::min<int64_t>(65535, count - c0);
+        g.a = A + c0 * lda;
+        g.b = B + c0 * ldb;
+        g.f = Fo + c0 * ldf;
+        dispatch(R, g, dim3(1, unsigned(nkt), unsigned(c)), st);
+    }
+}
+
+}  // namespace mmm_cu

@@ -1,0 +1,231 @@
+"""GPU parity: every CUDA entry point, called through the C ABI, against the
+reference's golden vectors (tests/golden) and the CPU oracle, bit-exact.
+
+Small suites replay the reference's own seeded tests (suites.py) and compare
+digests of the GPU results with the digests the unmodified reference
+produced; config-scale cases compare with the reference's digests of the
+BASELINE configs; size-independent properties cover the rest."""
+import numpy as np
+import pytest
+
+from helpers import ProductRng, digest, replay
+import suites
+
+pytestmark = pytest.mark.gpu
+
+P = suites.P_BENCH
+NTT_PRIMES = [469762049, 998244353, 7340033, 12289, 257, 17]
+
+
+def _mul_cpu(port):
+    return port.mul
+
+
+# --------------------------------------------------------- frozen cases --
+def test_frozen(cuda_lib, golden_small):
+    mmm = cuda_lib
+    for c in golden_small["frozen"]:
+        p, a, b = c["p"], c["a"], c["b"]
+        if c["op"] == "mul":
+            for s in (1, 2, 4, 8, 16):
+                assert mmm.mul(a, b, p, s=s).tolist() == c["f"]
+        elif c["op"] == "divmod":
+            for s in (1, 2, 3, 4, 8, 64):
+                q, r = mmm.divmod(a, b, p, s=s)
+                assert (q.tolist(), r.tolist()) == (c["q"], c["r"]), (c, s)
+        else:
+            for s in (1, 2, 4, 64):
+                assert mmm.gcd(a, b, p, s=s).tolist() == c["g"], (c, s)
+
+
+# ------------------------------------------------------- seeded suites --
+@pytest.mark.parametrize("suite", ["mutual_oracle", "divmod_roundtrip", "planted_gcd",
+                                   "division_sweep", "multiplication_sweep", "gcd_sweep",
+                                   "acceptance", "verify_p7", "verify_p101",
+                                   "verify_p469762049"])
+def test_suite(cuda_lib, port, golden_small, suite):
+    mmm = cuda_lib
+    cases = golden_small["suites"][suite]["cases"]
+    for c, g in zip(replay(suite, ProductRng, port.mul), cases):
+        p, a, b, op = c["p"], c["a"], c["b"], c["op"]
+        assert (digest(a), digest(b)) == (g["a"], g["b"])
+        if op == "all":      # acceptance_test.cpp:127-209
+            s_mul, s_div, s_gcd = c["s_mul"], [c["s_div"]], c["s_gcd"]
+        elif op == "verify":  # mmm_cli.cpp:478-520
+            s_mul, s_div, s_gcd = [1, 2, 4], [c["s_div"]], [c["s_gcd"]]
+        else:
+            s_mul = s_div = s_gcd = c.get("s") or [1, 7, 64]
+        if "f" in g:
+            src = c["am"] if op == "verify" else a
+            for s in s_mul:
+                assert digest(mmm.mul(src, b, p, s=s)) == g["f"], (suite, s)
+        if "q" in g:
+            for s in list(s_div) + [64]:
+                q, r = mmm.divmod(a, b, p, s=s)
+                assert (digest(q), digest(r)) == (g["q"], g["r"]), (suite, s)
+        if "g" in g:
+            for s in list(s_gcd) + [64]:
+                assert digest(mmm.gcd(a, b, p, s=s)) == g["g"], (suite, s)
+
+
+# ------------------------------------------------------------ edge cases --
+def test_edge_shapes(cuda_lib, port):
+    mmm = cuda_lib
+    rng = np.random.default_rng(11)
+    for p in (2, 3, 7, 101, 469762049, 2147483647):
+        for na in (1, 2, 3, 31, 32, 33, 129, 1000):
+            for nb in (1, 2, 5, 64, 257):
+                a = rng.integers(0, p, na)
+                b = rng.integers(0, p, nb)
+                a[-1] = max(a[-1], 1)
+                b[-1] = max(b[-1], 1)
+                assert np.array_equal(mmm.mul(a, b, p), port.mul(a, b, p)), (p, na, nb)
+                q, r = mmm.divmod(a, b, p, s=16)
+                wq, wr = port.divmod(a, b, p)
+                assert np.array_equal(q, wq) and np.array_equal(r, wr), (p, na, nb)
+                assert np.array_equal(mmm.gcd(a, b, p, s=8), port.gcd(a, b, p)), (p, na, nb)
+
+
+def test_untrimmed_and_zero_inputs(cuda_lib, port):
+    mmm = cuda_lib
+    assert mmm.mul([0, 0], [1, 2], 7).size == 0
+    assert mmm.mul([1, 2, 0, 0], [3, 0], 7).tolist() == port.mul([1, 2], [3], 7).tolist()
+    assert mmm.gcd([3, 0, 2, 5], [], 7).tolist() == port.monic([3, 0, 2, 5], 7).tolist()
+    assert mmm.gcd([], [3, 0, 2, 5], 7).tolist() == port.monic([3, 0, 2, 5], 7).tolist()
+    q, r = mmm.divmod([1, 2, 0, 1, 0, 0], [1, 1], 7)
+    assert (q.tolist(), r.tolist()) == ([3, 6, 1], [5])
+
+
+def test_degree_drops_small_field(cuda_lib, port):
+    """GF(2)/GF(3)/GF(7): many zero heads and multi-step degree drops."""
+    mmm = cuda_lib
+    rng = np.random.default_rng(5)
+    for t in range(300):
+        p = (2, 3, 7)[t % 3]
+        g = rng.integers(0, p, rng.integers(1, 12))
+        g[-1] = 1
+        u = rng.integers(0, p, rng.integers(1, 80))
+        v = rng.integers(0, p, rng.integers(1, 80))
+        a, b = port.mul(g, u, p), port.mul(g, v, p)
+        want = port.gcd(a, b, p) if (len(a) or len(b)) else None
+        if want is None:
+            continue
+        for s in (1, 3, 16, 100):
+            assert np.array_equal(mmm.gcd(a, b, p, s=s), want), (t, s)
+        if len(b):
+            wq, wr = port.divmod(a, b, p)
+            for s in (1, 5, 32):
+                q, r = mmm.divmod(a, b, p, s=s)
+                assert np.array_equal(q, wq) and np.array_equal(r, wr)
+
+
+# --------------------------------------------------------------- NTT ----
+def test_ntt_matches_plain(cuda_lib, port):
+    mmm = cuda_lib
+    rng = np.random.default_rng(3)
+    for p in NTT_PRIMES:
+        for na, nb in ((1, 1), (2, 3), (5, 1), (100, 28), (1000, 1000), (2048, 2049)):
+            if not (p - 1) % (1 << max(2, (na + nb - 2).bit_length())) == 0:
+                continue
+            a = rng.integers(0, p, na)
+            b = rng.integers(0, p, nb)
+            assert np.array_equal(mmm.ntt_mul(a, b, p), port.mul(a, b, p)), (p, na, nb)
+
+
+def test_ntt_rejects_unsupported_prime(cuda_lib):
+    with pytest.raises(cuda_lib.InvalidArgument):
+        cuda_lib.ntt_mul([1, 2, 3], [4, 5], 7)
+
+
+# ----------------------------------------------------------- batches ----
+def test_batched_equal_single(cuda_lib, port):
+    mmm = cuda_lib
+    rng = np.random.default_rng(9)
+    A = rng.integers(0, P, (17, 300)).astype(np.uint32)
+    B = rng.integers(1, P, (17, 120)).astype(np.uint32)
+    F = mmm.mul_batched(A, B, P)
+    Q, R = mmm.divmod_batched(A, B, P, s=32)
+    Fn = mmm.ntt_mul_batched(A, B, P)
+    for i in range(17):
+        want = port.mul(A[i], B[i], P)
+        assert np.array_equal(np.trim_zeros(F[i].astype(np.int64), "b"), want)
+        assert np.array_equal(np.trim_zeros(Fn[i].astype(np.int64), "b"), want)
+        wq, wr = port.divmod(A[i], B[i], P)
+        assert np.array_equal(np.trim_zeros(Q[i].astype(np.int64), "b"), wq)
+        assert np.array_equal(np.trim_zeros(R[i].astype(np.int64), "b"), wr)
+
+
+# --------------------------------------------------------- config scale --
+def test_cfg1_plain_mult(cuda_lib, golden_configs):
+    c = suites.cfg1(ProductRng(42))
+    for s in (1, 2, 4, 8, 16):
+        assert digest(cuda_lib.mul(c["a"], c["b"], P, s=s)) == golden_configs["cfg1"]["f"], s
+
+
+def test_cfg1_via_ntt(cuda_lib, golden_configs):
+    c = suites.cfg1(ProductRng(42))
+    assert digest(cuda_lib.ntt_mul(c["a"], c["b"], P)) == golden_configs["cfg1"]["f"]
+
+
+def test_cfg2_gcd(cuda_lib, port, golden_configs):
+    c = suites.cfg2(ProductRng(42), port.mul, port.monic)
+    assert (digest(c["a"]), digest(c["b"])) == (golden_configs["cfg2"]["a"],
+                                                golden_configs["cfg2"]["b"])
+    for s in (8, 32, 64, 128, 256):
+        g = cuda_lib.gcd(c["a"], c["b"], P, s=s)
+        assert digest(g) == golden_configs["cfg2"]["g"], s
+        assert np.array_equal(g, c["g"])
+
+
+@pytest.mark.parametrize("s", [1, 2, 4, 8, 16, 32, 64, 128, 256, 512])
+def test_cfg3_division_sweep(cuda_lib, golden_configs, s):
+    c = suites.cfg3(ProductRng(42))
+    q, r = cuda_lib.divmod(c["a"], c["b"], P, s=s)
+    assert (digest(q), digest(r)) == (golden_configs["cfg3"]["q"], golden_configs["cfg3"]["r"])
+
+
+def test_cfg3_roundtrip_property(cuda_lib):
+    """Size-independent check: q*b + r == a with the GPU's own product."""
+    c = suites.cfg3(ProductRng(42))
+    q, r = cuda_lib.divmod(c["a"], c["b"], P, s=128)
+    qb = cuda_lib.ntt_mul(q, c["b"], P).astype(np.int64)
+    qb[: len(r)] = (qb[: len(r)] + r) % P
+    assert np.array_equal(qb, np.asarray(c["a"], dtype=np.int64))
+
+
+def test_cfg4_big_ntt(cuda_lib, golden_configs):
+    rng = ProductRng(42)
+    c = suites.cfg4_big(rng)
+    assert (digest(c["a"]), digest(c["b"])) == (golden_configs["cfg4_big"]["a"],
+                                                golden_configs["cfg4_big"]["b"])
+    f = cuda_lib.ntt_mul(c["a"], c["b"], P)
+    if "f" in golden_configs["cfg4_big"]:
+        assert digest(f) == golden_configs["cfg4_big"]["f"]
+    # evaluation at random points (Schwartz-Zippel): f(x) == a(x) b(x)
+    for x in (3, 123456789, 469762000):
+        def ev(poly):
+            acc = 0
+            for coef in np.asarray(poly, dtype=object)[::-1]:
+                acc = (acc * x + int(coef)) % P
+            return acc
+        assert ev(f) == ev(c["a"]) * ev(c["b"]) % P
+
+
+def test_cfg4_batch_ntt(cuda_lib, golden_configs):
+    rng = ProductRng(42)
+    suites.cfg4_big(rng)
+    cb = suites.cfg4_batch(rng)
+    F = cuda_lib.ntt_mul_batched(cb["A"], cb["B"], P)
+    fs = [digest(np.trim_zeros(F[i].astype(np.int64), "b")) for i in range(F.shape[0])]
+    assert fs == golden_configs["cfg4_batch"]["f"]
+
+
+def test_cfg5_batches(cuda_lib, golden_configs):
+    c5 = suites.cfg5(ProductRng(42))
+    F = cuda_lib.mul_batched(c5["A"], c5["B"], P)
+    fs = [digest(np.trim_zeros(F[i].astype(np.int64), "b")) for i in range(F.shape[0])]
+    assert fs == golden_configs["cfg5"]["f"]
+    Q, R = cuda_lib.divmod_batched(c5["C"], c5["D"], P)
+    qs = [digest(np.trim_zeros(Q[i].astype(np.int64), "b")) for i in range(Q.shape[0])]
+    rs = [digest(np.trim_zeros(R[i].astype(np.int64), "b")) for i in range(R.shape[0])]
+    assert qs == golden_configs["cfg5"]["q"] and rs == golden_configs["cfg5"]["r"]
