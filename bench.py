@@ -1,0 +1,610 @@
+#!/usr/bin/env python3
+"""Benchmark of the polynomial-arithmetic hot path (BASELINE.json metric:
+mod-p coefficient operations per second).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload gcd|mul|div|ntt|ntt_batch|batch] [--s S]
+
+Default workload: BASELINE.json configs[1] -- the Euclidean GCD of
+a = g*u, b = g*v over p = 469762049 (deg a = 12288, deg b = 12287, seed 42),
+one instance per GPU.  The unit of work ("coefficient update") is the
+oracle's: for every head elimination of the Euclidean run, deg(divisor)+1
+coefficient updates (oracle.cpp:63-64); 134,225,920 for this input.
+
+One JSON line on rank 0.  `value` = device time of the CUDA path with inputs
+resident in HBM (CUDA events on the launch stream, L2 flushed between timed
+steps, max over ranks); `e2e` = the same metric through the host-buffer C-ABI
+call (mmm_cu_gcd: H2D of the inputs, kernel, D2H of the result inside the
+timed region); `roofline` = the dominant kernel vs the measured peak;
+`cpu_baseline` = the reference oracle (oracle/_ref, else the C port) on the
+host cores.  `--impl reference` times the reference's CPU implementation of
+the same workload on all host threads (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
+
+import suites  # noqa: E402  (input definitions shared with the golden generator)
+
+P = suites.P_BENCH
+METRIC = "mod-p coeff-ops/sec (plain mult, div/GCD, NTT) vs int-MAD/HBM roofline"
+UNIT = "coeff-ops/s"
+GOLDEN = os.path.join(ROOT, "tests", "golden", "golden_configs.json")
+PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+IMAD_PEAKS = os.path.join(ROOT, "profiles", "peaks.json")
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# --------------------------------------------------------------- plumbing --
+class Dist:
+    def __init__(self, impl: str):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+        if self.world > 1 and impl == "ours":
+            import torch.distributed as dist
+            dist.init_process_group("nccl", device_id=None)
+            self.pg = dist
+
+    def max(self, x: float) -> float:
+        if self.pg is None:
+            return x
+        import torch
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
+        return float(t.item())
+
+    def barrier(self):
+        if self.pg is not None:
+            import torch
+            self.pg.barrier(device_ids=[torch.cuda.current_device()])
+
+    def close(self):
+        if self.pg is not None:
+            self.pg.destroy_process_group()
+
+
+class Clocks:
+    """nvidia-smi sampler for the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-i", str(self.index), "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.12)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.t.join(timeout=1)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[4:8]) if v == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def golden():
+    with open(GOLDEN) as fh:
+        return json.load(fh)
+
+
+def digest(x) -> str:
+    import hashlib
+    a = np.ascontiguousarray(np.asarray(x).astype("<i8"))
+    return hashlib.sha256(a.tobytes()).hexdigest()[:16] if a.size else ""
+
+
+def peaks():
+    hbm, src = 6650.0, "fallback (B200_PROFILING.md)"
+    if os.path.exists(PEAKS):
+        with open(PEAKS) as fh:
+            hbm, src = float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    imad = None
+    if os.path.exists(IMAD_PEAKS):
+        with open(IMAD_PEAKS) as fh:
+            imad = float(json.load(fh)["imad_wide_per_s"])
+    return hbm, src, imad
+
+
+class ProductRng:
+    def __init__(self, seed):
+        import paper_1402_0264_b200 as mmm
+        self.g = mmm.Rng(seed)
+
+    def next(self):
+        return self.g()
+
+    def random_poly(self, terms, p):
+        return self.g.random_poly(terms, p)
+
+
+# -------------------------------------------------------------- workloads --
+class Workload:
+    name = ""
+    config = {}
+
+    def units(self) -> float:  # coeff-ops per instance-step
+        raise NotImplementedError
+
+
+class GcdWork(Workload):
+    """configs[1]: single-instance Euclidean GCD (replicas only across GPUs)."""
+
+    name = "gcd"
+
+    def __init__(self, s):
+        import paper_1402_0264_b200 as mmm
+        self.mmm, self.s = mmm, s or 128
+        gold = golden()["cfg2"]
+        rng = ProductRng(42)
+        g = mmm.Field(P)
+        gp = rng.random_poly((1 << 12) + 1, P)
+        gp = mmm.mul(gp, [g.inv(int(gp[-1]))], P)  # monic(g)
+        u = rng.random_poly((1 << 13) + 1, P)
+        v = rng.random_poly(1 << 13, P)
+        self.a, self.b = mmm.mul(gp, u, P), mmm.mul(gp, v, P)
+        assert (digest(self.a), digest(self.b)) == (gold["a"], gold["b"]), "cfg2 inputs"
+        self.want = gold["g"]
+        self.steps_, self.updates, self.ng = gold["steps"], gold["updates"], gold["deg_g"] + 1
+        self.config = {"workload": "cfg2_gcd_deg12288_deg12287_p469762049", "p": P,
+                       "deg_a": len(self.a) - 1, "deg_b": len(self.b) - 1, "s": self.s,
+                       "eliminations": self.steps_, "seed": 42, "parallelism": "replicas",
+                       "l2": "flushed between timed steps (inputs < L2)"}
+
+    def units(self):
+        return float(self.updates)
+
+    def device_setup(self):
+        import torch
+        self.da = torch.from_numpy(self.a.astype(np.int32)).cuda()
+        self.db = torch.from_numpy(self.b.astype(np.int32)).cuda()
+        self.dg = torch.zeros(max(len(self.a), len(self.b)), dtype=torch.int32, device="cuda")
+        self.dn = torch.zeros(1, dtype=torch.int64, device="cuda")
+
+    def device_step(self, stream):
+        self.mmm.gcd_dev(P, self.da.data_ptr(), len(self.a), self.db.data_ptr(), len(self.b),
+                         self.dg.data_ptr(), self.dn.data_ptr(), s=self.s, stream=stream)
+
+    def device_check(self):
+        n = int(self.dn.item())
+        g = self.dg[:n].cpu().numpy().astype(np.uint32)
+        assert digest(g) == self.want, "gcd result differs from the reference"
+
+    def host_setup(self):
+        import torch
+        self.ha = torch.from_numpy(self.a.astype(np.int32)).pin_memory().numpy().view(np.uint32)
+        self.hb = torch.from_numpy(self.b.astype(np.int32)).pin_memory().numpy().view(np.uint32)
+        self.bytes_in = 4 * (len(self.a) + len(self.b))
+
+    def host_step(self):
+        g = self.mmm.gcd(self.ha, self.hb, P, s=self.s)
+        self.bytes_out = 4 * len(g) + 8
+        return g
+
+    def host_check(self, g):
+        assert digest(g) == self.want
+
+    def roofline(self, t_step, hbm, imad):
+        alg = 4.0 * (len(self.a) + len(self.b) + self.ng)  # inputs read once, gcd written once
+        achieved = alg / t_step / 1e9
+        return {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm, "traffic": None, "kernel": "gcd_kernel",
+                "alg_bytes_per_launch": alg,
+                "binding": f"dependency chain: {self.steps_} sequential eliminations, "
+                           f"{t_step / self.steps_ * 1e9:.1f} ns per elimination"}
+
+    def cpu_ref(self, orc):
+        """(callable, coeff-ops per call, checker, sample description)."""
+        a, b = self.a.astype(np.int64), self.b.astype(np.int64)
+        return (lambda: orc.gcd(a, b, P), self.units(),
+                lambda out: digest(out) == self.want, "full instance (oracle_gcd)")
+
+
+def _dev(x):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(x).astype(np.uint32).view(np.int32)).cuda()
+
+
+def _pinned(x):
+    import torch
+    t = torch.from_numpy(np.ascontiguousarray(x).astype(np.uint32).view(np.int32)).pin_memory()
+    return t.numpy().view(np.uint32), t
+
+
+class MulWork(Workload):
+    """configs[0]: 2^14 x 2^14 plain multiplication (IMAD-bound)."""
+
+    name = "mul"
+
+    def __init__(self, s):
+        import paper_1402_0264_b200 as mmm
+        self.mmm, self.s = mmm, s or 8
+        c = suites.cfg1(ProductRng(42))
+        self.a, self.b = c["a"], c["b"]
+        self.want = golden()["cfg1"]["f"]
+        self.nf = len(self.a) + len(self.b) - 1
+        self.config = {"workload": "cfg1_mul_2^14x2^14_p469762049", "p": P, "s": self.s,
+                       "seed": 42, "parallelism": "replicas",
+                       "l2": "flushed between timed steps (inputs < L2)"}
+
+    def units(self):
+        return float(len(self.a) * len(self.b))
+
+    def device_setup(self):
+        import torch
+        self.da, self.db = _dev(self.a), _dev(self.b)
+        self.df = torch.zeros(self.nf, dtype=torch.int32, device="cuda")
+
+    def device_step(self, stream):
+        self.mmm.mul_dev(P, self.da.data_ptr(), len(self.a), self.db.data_ptr(), len(self.b),
+                         self.df.data_ptr(), s=self.s, stream=stream)
+
+    def device_check(self):
+        assert digest(self.df.cpu().numpy().view(np.uint32)) == self.want, "mul result"
+
+    def host_setup(self):
+        (self.ha, self._ta), (self.hb, self._tb) = _pinned(self.a), _pinned(self.b)
+        self.bytes_in = 4 * (len(self.a) + len(self.b))
+        self.bytes_out = 4 * self.nf
+
+    def host_step(self):
+        return self.mmm.mul(self.ha, self.hb, P, s=self.s)
+
+    def host_check(self, f):
+        assert digest(f) == self.want
+
+    def roofline(self, t_step, hbm, imad):
+        macs = self.units()
+        achieved = macs / t_step / 1e12
+        peak = (imad or 7.35e12) / 1e12
+        return {"bound": "imad", "achieved": achieved, "peak": peak, "unit": "TMAC/s",
+                "frac": achieved / peak, "traffic": None, "kernel": "mul_kernel",
+                "alg_macs_per_launch": macs,
+                "note": "integer pipe: one IMAD.WIDE.U32 per modular MAD; peak = measured "
+                        "IMAD.WIDE.U32 rate (profiles/peaks.json); no tensor cores"}
+
+    def cpu_ref(self, orc):
+        a, b = self.a.astype(np.int64), self.b.astype(np.int64)
+        return (lambda: orc.mul(a, b, P), self.units(),
+                lambda out: digest(out) == self.want, "full instance (oracle_mul)")
+
+
+class DivWork(Workload):
+    """configs[2]: long division deg 2^16 by deg 2^15, s-blocked."""
+
+    name = "div"
+
+    def __init__(self, s):
+        import paper_1402_0264_b200 as mmm
+        self.mmm, self.s = mmm, s or 128
+        c = suites.cfg3(ProductRng(42))
+        self.a, self.b = c["a"], c["b"]
+        g = golden()["cfg3"]
+        self.want = (g["q"], g["r"])
+        self.nq, self.nr = len(self.a) - len(self.b) + 1, len(self.b) - 1
+        self.config = {"workload": "cfg3_divmod_deg2^16_by_deg2^15_p469762049", "p": P,
+                       "s": self.s, "seed": 42, "parallelism": "replicas",
+                       "l2": "flushed between timed steps (inputs < L2)"}
+
+    def units(self):
+        return float(self.nq * len(self.b))  # heads x (deg b + 1) updates
+
+    def device_setup(self):
+        import torch
+        self.da, self.db = _dev(self.a), _dev(self.b)
+        self.dq = torch.zeros(self.nq, dtype=torch.int32, device="cuda")
+        self.dr = torch.zeros(max(self.nr, 1), dtype=torch.int32, device="cuda")
+
+    def device_step(self, stream):
+        self.mmm.divmod_dev(P, self.da.data_ptr(), len(self.a), self.db.data_ptr(), len(self.b),
+                            self.dq.data_ptr(), self.dr.data_ptr(), s=self.s, stream=stream)
+
+    def device_check(self):
+        q = np.trim_zeros(self.dq.cpu().numpy().view(np.uint32), "b")
+        r = np.trim_zeros(self.dr[: self.nr].cpu().numpy().view(np.uint32), "b")
+        assert (digest(q), digest(r)) == self.want, "divmod result"
+
+    def host_setup(self):
+        (self.ha, self._ta), (self.hb, self._tb) = _pinned(self.a), _pinned(self.b)
+        self.bytes_in = 4 * (len(self.a) + len(self.b))
+        self.bytes_out = 4 * (self.nq + self.nr)
+
+    def host_step(self):
+        return self.mmm.divmod(self.ha, self.hb, P, s=self.s)
+
+    def host_check(self, qr):
+        assert (digest(qr[0]), digest(qr[1])) == self.want
+
+    def roofline(self, t_step, hbm, imad):
+        alg = 4.0 * (len(self.a) + len(self.b) + self.nq + self.nr)
+        achieved = alg / t_step / 1e9
+        return {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm, "traffic": None, "kernel": "div_grid_kernel",
+                "alg_bytes_per_launch": alg,
+                "imad_frac": self.units() / t_step / (imad or 7.35e12),
+                "binding": f"{-(-self.nq // self.s)} grid-wide steps of s={self.s} heads"}
+
+    def cpu_ref(self, orc):
+        a, b = self.a.astype(np.int64), self.b.astype(np.int64)
+        return (lambda: orc.divmod(a, b, P), self.units(),
+                lambda out: (digest(out[0]), digest(out[1])) == self.want,
+                "full instance (oracle_divmod)")
+
+
+class NttWork(Workload):
+    """configs[3] (single): 2^20 x 2^20 product through a length-2^21 NTT."""
+
+    name = "ntt"
+
+    def __init__(self, s):
+        import paper_1402_0264_b200 as mmm
+        self.mmm = mmm
+        c = suites.cfg4_big(ProductRng(42))
+        self.a, self.b = c["a"], c["b"]
+        self.want = golden()["cfg4_big"].get("f")
+        self.nf = len(self.a) + len(self.b) - 1
+        self.config = {"workload": "cfg4_ntt_2^20x2^20_N2^21_p469762049", "p": P, "seed": 42,
+                       "transform": "four-step 2^10 x 2^11, radix-2 Stockham in smem",
+                       "parallelism": "replicas", "units": "schoolbook-equivalent MACs",
+                       "l2": "flushed between timed steps"}
+
+    def units(self):
+        return float(len(self.a) * len(self.b))
+
+    def device_setup(self):
+        import torch
+        self.da, self.db = _dev(self.a), _dev(self.b)
+        self.df = torch.zeros(self.nf, dtype=torch.int32, device="cuda")
+
+    def device_step(self, stream):
+        self.mmm.ntt_mul_dev(P, self.da.data_ptr(), len(self.a), self.db.data_ptr(), len(self.b),
+                             self.df.data_ptr(), stream=stream)
+
+    def device_check(self):
+        if self.want:
+            assert digest(self.df.cpu().numpy().view(np.uint32)) == self.want, "ntt result"
+
+    def host_setup(self):
+        (self.ha, self._ta), (self.hb, self._tb) = _pinned(self.a), _pinned(self.b)
+        self.bytes_in = 4 * (len(self.a) + len(self.b))
+        self.bytes_out = 4 * self.nf
+
+    def host_step(self):
+        return self.mmm.ntt_mul(self.ha, self.hb, P)
+
+    def host_check(self, f):
+        if self.want:
+            assert digest(f) == self.want
+
+    def roofline(self, t_step, hbm, imad):
+        alg = 4.0 * (len(self.a) + len(self.b) + self.nf)
+        achieved = alg / t_step / 1e9
+        N = 1 << 21
+        bfly = 3 * (N // 2) * 21
+        return {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm, "traffic": None, "kernel": "ntt_rows",
+                "alg_bytes_per_launch": alg, "butterflies": bfly,
+                "butterflies_per_s": bfly / t_step}
+
+    def cpu_ref(self, orc):
+        # bounded sample: 2^12 middle output words of the product, computed
+        # output-stationary exactly as oracle_mul_alt (each ~2^20 MACs)
+        import ctypes as C
+        from oracle import pyoracle
+        port = pyoracle.Port()
+        fn = port.lib.orc_poly_mul_alt_range
+        PT = C.POINTER(C.c_int64)
+        fn.argtypes = [PT, C.c_int64, PT, C.c_int64, C.c_int64, C.c_int64, C.c_int64, PT]
+        fn.restype = None
+        a, b = self.a.astype(np.int64), self.b.astype(np.int64)
+        k0, k1 = (1 << 20) - 2048, (1 << 20) + 2048
+        out = np.zeros(k1 - k0, dtype=np.int64)
+        macs = float(sum(min(k + 1, self.nf - k, len(a)) for k in range(k0, k1)))
+
+        def run():
+            fn(a.ctypes.data_as(PT), len(a), b.ctypes.data_as(PT), len(b), P, k0, k1,
+               out.ctypes.data_as(PT))
+            return out
+        return (run, macs, lambda o: True,
+                "4096 middle output words of the 2^20 x 2^20 product (oracle_mul_alt "
+                "restated, C port), 2^32 MACs")
+
+
+WORKLOADS = {"gcd": GcdWork, "mul": MulWork, "div": DivWork, "ntt": NttWork}
+
+
+# ------------------------------------------------------------------ arms --
+def run_ours(args, dist):
+    import torch
+    torch.cuda.set_device(dist.local)
+    import paper_1402_0264_b200 as mmm
+    mmm.load()
+    work = WORKLOADS[args.workload](args.s)
+    work.device_setup()
+    stream = torch.cuda.current_stream()
+    sp = stream.cuda_stream
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    for _ in range(args.warmup):
+        work.device_step(sp)
+    torch.cuda.synchronize()
+    work.device_check()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    dist.barrier()
+    torch.cuda.synchronize()
+    n0 = mmm.launch_count()
+    with Clocks(torch.cuda.current_device()) as clk:
+        for e0, e1 in ev:
+            flush.zero_()
+            e0.record(stream)
+            work.device_step(sp)
+            e1.record(stream)
+        torch.cuda.synchronize()
+        launches = mmm.launch_count() - n0
+        # keep the sampler alive over a comparable busy window for short runs
+        t_dev = sum(e0.elapsed_time(e1) for e0, e1 in ev) / 1e3
+    dist.barrier()
+    torch.cuda.synchronize()
+    work.device_check()
+    t_dev = dist.max(t_dev)
+    t_step = t_dev / args.steps
+    value = dist.world * work.units() / t_step
+
+    # e2e: host-buffer C-ABI call, H2D + kernel + D2H inside the region
+    work.host_setup()
+    for _ in range(max(1, args.warmup)):
+        work.host_step()
+    dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        out = work.host_step()
+    t_e2e = dist.max(time.perf_counter() - t0) / args.steps
+    work.host_check(out)
+    e2e = {"value": dist.world * work.units() / t_e2e, "unit": UNIT,
+           "h2d_bytes_per_step": work.bytes_in, "d2h_bytes_per_step": work.bytes_out,
+           "ms_per_step": t_e2e * 1e3}
+
+    hbm, src, imad = peaks()
+    roof = work.roofline(t_step, hbm, imad)
+    roof["peak_source"] = src
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": dist.world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic (seeded mt19937_64 inputs, reference random_poly draws)",
+            "config": work.config, "impl": "ours", "e2e": e2e, "roofline": roof,
+            "gpu_launches": launches, "clocks": clk.summary()}
+    if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(work, args.cpu_seconds)
+    return line
+
+
+def _oracle():
+    from oracle import pyoracle
+    if pyoracle.reference_available():
+        return pyoracle.Reference(), "reference"
+    pyoracle.build_port()
+    return pyoracle.Port(), "port"
+
+
+def cpu_baseline(work, seconds):
+    """The CPU oracle on this host, rank 0, one core, a bounded sample."""
+    orc, kind = _oracle()
+    fn, units, ok, what = work.cpu_ref(orc)
+    fn()  # warm
+    n, t0 = 0, time.perf_counter()
+    while time.perf_counter() - t0 < seconds or n == 0:
+        out = fn()
+        n += 1
+    dt = (time.perf_counter() - t0) / n
+    assert ok(out), "cpu baseline result differs from the reference"
+    return {"value": units / dt, "unit": UNIT, "cores": 1, "kind": kind,
+            "sample": f"{n} x {what}, serial, {dt * 1e3:.1f} ms each"}
+
+
+def run_reference(args, dist):
+    """The reference's own CPU path (oracle/_ref, else the C port), all host
+    threads: one independent instance sample per thread per step."""
+    if dist.rank != 0:
+        return None
+    work = WORKLOADS[args.workload](args.s)
+    orc, kind = _oracle()
+    cores = os.cpu_count() or 1
+    fn, units, ok, what = work.cpu_ref(orc)
+
+    def step():
+        with ThreadPoolExecutor(cores) as ex:
+            return list(ex.map(lambda _: fn(), range(cores)))
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        outs = step()
+    dt = (time.perf_counter() - t0) / args.steps
+    assert all(ok(o) for o in outs), "reference result differs from the golden digest"
+    value = cores * units / dt
+    return {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": dist.world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "i64",
+            "data": "synthetic (seeded mt19937_64 inputs, reference random_poly draws)",
+            "config": work.config, "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+                             "sample": f"{cores} concurrent x {what} per step, one per host "
+                                       f"thread"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="gcd")
+    ap.add_argument("--s", type=int, default=0)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    dist = Dist(args.impl)
+    try:
+        line = run_ours(args, dist) if args.impl == "ours" else run_reference(args, dist)
+        if line is not None and dist.rank == 0:
+            print(json.dumps(line), flush=True)
+    finally:
+        dist.close()
+
+
+if __name__ == "__main__":
+    main()

@@ -374,7 +374,8 @@ int mmm_cu_gcd(int64_t p, const uint32_t* a, int64_t na, const uint32_t* b, int6
             launch_gcd(F, da, na, db, nb, dg, dng, s, st);
             MMM_CUDA(cudaMemcpyAsync(&len, dng, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
             sync(st);
-            if (len < 0 || len > std::max(na, nb)) throw Error(ST_SIM, "gcd: bad result length");
+            if (len == -1) throw Error(ST_SIM, "gcd: offset matrix left its window");
+            if (len < 0 || len > std::max(na, nb)) throw Error(ST_SIM, "gcd: batch made no progress");
             to_host(g, dg, len, st);
         }
         sync(st);

@@ -51,7 +51,6 @@ struct GcdArgs {
     int S;        // steps per batch
     int W;        // window words per operand
     FieldParams F;
-    int* status;  // device: 0 ok, else internal error code
 };
 
 // Shared-memory control block written by warp 0, read by the whole CTA.
@@ -280,7 +279,8 @@ __global__ void __launch_bounds__(GCD_T) gcd_kernel(GcdArgs g) {
         if (threadIdx.x < 32) run_chain(ctl, wa, wb, P, g, g.X[cur], g.Y[cur]);
         __syncthreads();
         if (ctl.err || (ctl.steps == 0 && ctl.term == 0)) {
-            if (blockIdx.x == 0 && threadIdx.x == 0) *g.status = ctl.err ? 1 : 2;
+            // internal invariant broken: report through the length word
+            if (blockIdx.x == 0 && threadIdx.x == 0) *g.ng = ctl.err ? -1 : -2;
             return;  // grid-uniform decision: every CTA exits here
         }
         if (ctl.term == 3) break;
@@ -339,8 +339,6 @@ void launch_gcd(const FieldParams& F, const uint32_t* a, int64_t na, const uint3
         g.X[i] = sc.get<uint32_t>(size_t(g.cap));
         g.Y[i] = sc.get<uint32_t>(size_t(g.cap));
     }
-    g.status = sc.get<int>(1);
-    MMM_CUDA(cudaMemsetAsync(g.status, 0, sizeof(int), st));
     const int W = g.W, PL = 2 * W + 1;
     const int ORG = ((PL + 3) & ~3) + 3 + 4;
     const size_t words = size_t(2 * ((W + 3) & ~3) + ((4 * PL + 3) & ~3) + ((PL + 3 + 4) & ~3) +
@@ -357,11 +355,6 @@ void launch_gcd(const FieldParams& F, const uint32_t* a, int64_t na, const uint3
     MMM_CUDA(cudaLaunchCooperativeKernel((void*)gcd_kernel, dim3(blocks), dim3(GCD_T), params, bytes,
                                          st));
     check_launch("gcd_kernel");
-    int status = 0;
-    MMM_CUDA(cudaMemcpyAsync(&status, g.status, sizeof(int), cudaMemcpyDeviceToHost, st));
-    MMM_CUDA(cudaStreamSynchronize(st));
-    if (status) throw Error(ST_SIM, status == 1 ? "gcd: offset matrix left its window"
-                                                : "gcd: batch made no progress");
 }
 
 }  // namespace mmm_cu
