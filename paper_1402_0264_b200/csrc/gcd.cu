@@ -1,244 +1,423 @@
-// gcd.cu -- Euclidean GCD over Z/pZ on sm_100a, s elimination steps per batch.
+// gcd.cu -- Euclidean GCD over Z/pZ on sm_100a.
 //
 // Result: exactly oracle_gcd (proj/src/oracle.cpp:69-78), the monic gcd.
-// Structure: the paper's optimized GCD (Alg. 9-10) as simulated by
-// run_gcd's optimized variant (proj/src/gcd.cpp:116-330): up to s head
-// eliminations are folded into a 2x2 matrix of offset polynomials
-// (UpdateMatrix, gcd.cpp:124-157) that is then applied to both operands by
-// every block.  Differences, B200-first:
+// Structure: the paper's blocked GCD (Alg. 9-10), simulated by
+// run_gcd's optimized variant (proj/src/gcd.cpp:116-330): a run of head
+// eliminations is folded into a 2x2 matrix of offset polynomials
+// (UpdateMatrix, gcd.cpp:124-157) which every block then applies to its part
+// of both operands.  B200-first re-design:
 //
-//  * The matrix is staged ON DEVICE (the reference stages it on the host,
-//    reading device memory per launch, gcd.cpp:203-272).  Warp 0 of every CTA
-//    runs the step chain redundantly on the operands' top windows in shared
-//    memory -- the paper's redundant s-head computation -- so there is no
-//    host round trip and no extra grid barrier to broadcast the matrix.
-//  * Steps are fraction-free:  A <- y*A - x*X^k*B  (x, y the two leads),
-//    evaluated as one Montgomery reduction of y*a + (p-x)*b, i.e. up to the
-//    unit 2^-32.  No per-step field inverse; the operands stay associates of
-//    the oracle's remainders, so the final monic result is bit-identical.
-//  * The role rule is the oracle's: the dividend keeps being reduced while
-//    deg(dividend) >= deg(divisor) (divmod's i-loop, oracle.cpp:58-66), then
-//    the roles swap (oracle.cpp:74-75); a zero dividend ends the run with the
-//    divisor as gcd, a degree-0 divisor with gcd 1 (gcd.cpp:191-199).
-//  * One persistent cooperative grid; a batch = chain, matrix apply
-//    (conv.cuh convolutions over L2-resident ping-pong buffers), grid barrier.
-//
-// Offset convention (as OffPoly): wa[j] = A[da0 - j], wb[j] = B[db0 - j] for
-// the batch-start degree bounds da0, db0.  New operands are
-//   A1[da0-j] = sum_d P11[d] wa0[j-d] + sum_d P12[d] wb0[j-d]   (same for B)
-// with every P support inside [-W, W].
+//  * Fraction-free steps.  U <- y*U - x*X^k*V (x, y the leads) evaluated as
+//    one Montgomery reduction of y*u + (p-x)*v: no field inverse per step;
+//    the operands stay associates of the oracle's remainders, so the final
+//    monic gcd is bit-identical.  For p < 2^29 the reduction is lazy
+//    (values in [0, 2p), no correction), which keeps a step at 5 integer ops.
+//  * Top-aligned windows in registers.  With u[t] = U[deg U - t] the update
+//    is u[t] <- y*u[t] - x*v[t]: lane-aligned, no shuffles; only the
+//    renormalisation after a degree drop (u[t] <- u[t+z]) moves data.  Warp 0
+//    of CTA 0 runs the whole step chain on 128-word windows of both operands
+//    held 4 words per lane, and logs each step (x, y, z, which operand).
+//  * The matrix in the same top-aligned form.  Pu[t] satisfies
+//    u[t] = sum_e Pu1[e] a0[t+e] + sum_e Pu2[e] b0[t+e]; it obeys the same
+//    recurrence as the window (Pu <- y*Pu - x*Pv) and shifts right by z when
+//    the window shifts left.  Warps 1 and 2 replay the step log, one matrix
+//    column each, concurrently with the chain.
+//  * Grid-wide apply.  The matrix is published to global memory and every
+//    CTA applies it to its slice of both operands with the register-tiled
+//    convolution of conv.cuh (L2-resident ping-pong buffers); one grid
+//    barrier before and one after.  The role rule is the oracle's: the
+//    dividend is reduced while deg(dividend) >= deg(divisor)
+//    (oracle.cpp:58-66), then roles swap (oracle.cpp:74-75); a zero dividend
+//    ends the run with the divisor as gcd, a degree-0 divisor with gcd 1
+//    (gcd.cpp:191-199).
 #include <cooperative_groups.h>
 
 #include "common.cuh"
 #include "conv.cuh"
 
+#include <cstdio>
+#include <cstdlib>
+
 namespace cg = cooperative_groups;
 
 namespace mmm_cu {
 
-constexpr int GCD_T = 256;
-constexpr int GCD_R = 2;
+constexpr int GCD_T = 256;         // threads per CTA
+constexpr int GE = 4;              // window words per lane
+constexpr int W1 = 32 * GE;        // window words per operand (128)
+constexpr int PE = 8;              // matrix words per lane per polynomial
+constexpr int PL = 32 * PE;        // matrix capacity (support < 256)
+constexpr int LOGCAP = 2048;       // steps per matrix batch, hard cap
+constexpr int BIG = 1 << 30;       // "validity unbounded": window covers the operand
+constexpr int GCD_R = 1;           // outputs per thread in the apply
+
+struct StepLog {
+    uint32_t x, y;
+    int z;       // renormalisation shift of the reduced operand
+    int u_is_a;  // 1: A was reduced by B, 0: B by A
+};
+
+// Published per batch by CTA 0 (global), read by every CTA after the barrier.
+struct BatchMeta {
+    long long da0, db0;  // exact degrees at batch start (-1: zero operand)
+    long long da1, db1;  // degree bounds after the batch (-1: vanished)
+    int steps, term, dividend_a, err;
+    int sa, sb;          // total shifts of A and B (top moves)
+    int hi[4];           // highest nonzero index of Pa1, Pa2, Pb1, Pb2
+};
 
 struct GcdArgs {
     const uint32_t* a;
     const uint32_t* b;
-    int64_t na, nb;
+    long long na, nb;
     uint32_t* X[2];
     uint32_t* Y[2];
+    uint32_t* Pg;     // 4 * PL words: Pa1, Pa2, Pb1, Pb2 (canonical)
+    BatchMeta* meta;  // global copy
     uint32_t* g;
     int64_t* ng;
-    int64_t cap;  // words per buffer
-    int S;        // steps per batch
-    int W;        // window words per operand
+    int M;            // steps per batch (the program parameter s)
     FieldParams F;
-};
-
-// Shared-memory control block written by warp 0, read by the whole CTA.
-struct GcdCtl {
-    int64_t da0, db0;   // batch-start degree bounds (offset origins)
-    int64_t da1, db1;   // bounds after the batch (-1: operand vanished)
-    int lo[4], hi[4];   // P supports (d), lo > hi = empty
-    int steps;
-    int term;           // 0 running, 1 A vanished, 2 B vanished, 3 unit gcd
-    int dividend_a;
-    int err;
+    long long* stats; // optional (MMM_GCD_STATS): batches, steps, chain/apply cycles
 };
 
 namespace {
 
-__device__ __forceinline__ int64_t i64min(int64_t a, int64_t b) { return a < b ? a : b; }
-__device__ __forceinline__ int64_t i64max(int64_t a, int64_t b) { return a > b ? a : b; }
+// Field flavour of the chain, fixed at compile time so the hot loops carry
+// no fallback branch: MODE 0 = odd p < 2^29, lazy residues in [0, 2p);
+// MODE 1 = odd p, canonical; MODE 2 = p = 2.
+struct Fld {
+    uint32_t p, pinv;
+};
 
-// Warp-wide: first j in [from, to) with w[j] != 0, else -1.
-__device__ int first_nonzero(const uint32_t* w, int from, int to) {
-    const int lane = threadIdx.x & 31;
-    for (int base = from; base < to; base += 32) {
-        const int j = base + lane;
-        const unsigned m = __ballot_sync(0xffffffffu, j < to && w[j] != 0);
-        if (m) return base + __ffs(m) - 1;
+template <int MODE>
+struct Arith {
+    // y*a - x*b (negx = -x) times 2^-32 (odd p); canonical unless MODE 0.
+    static __device__ __forceinline__ uint32_t comb(uint32_t y, uint32_t a, uint32_t negx,
+                                                     uint32_t b, Fld f) {
+        const uint64_t t = uint64_t(y) * a + uint64_t(negx) * b;
+        if (MODE == 2) return uint32_t(t & 1u);
+        const uint32_t m = uint32_t(t) * f.pinv;
+        const uint32_t hi = uint32_t(t >> 32), mp = __umulhi(m, f.p);
+        if (MODE == 0) return hi - mp + f.p;  // t < 8p^2 < p*2^32 for p < 2^29: in (0, 2p)
+        const uint32_t r = hi - mp;
+        return hi < mp ? r + f.p : r;
     }
-    return -1;
+    static __device__ __forceinline__ bool nz(uint32_t v, uint32_t p) {
+        return MODE == 0 ? (v != 0u && v != p) : v != 0u;
+    }
+    static __device__ __forceinline__ uint32_t neg(uint32_t x, uint32_t p) {
+        return MODE == 0 ? 2u * p - x : (x ? p - x : 0u);
+    }
+    static __device__ __forceinline__ uint32_t canon(uint32_t v, uint32_t p) {
+        return MODE == 0 ? (v >= p ? v - p : v) : v;
+    }
+};
+
+// Release/acquire on a shared-memory flag (no full sequentially-consistent
+// fence per step: MEMBAR.SC would stall the chain warp every elimination).
+__device__ __forceinline__ void st_release_cta(volatile int* p, int v) {
+    const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(const_cast<int*>(p)));
+    asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_acquire_cta(volatile int* p) {
+    const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(const_cast<int*>(p)));
+    int v;
+    asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
 }
 
-// Load the top W words below `bound` of buffer Z into w (zero below index 0),
-// lowering the bound past all-zero windows.  Returns the head offset, or -1
-// if the operand is zero.  `bound` is updated (warp-uniform).
-__device__ int load_window(uint32_t* w, const uint32_t* Z, int64_t& bound, int W) {
+__device__ __forceinline__ uint32_t bcast(uint32_t v) { return __shfl_sync(0xffffffffu, v, 0); }
+__device__ __forceinline__ uint32_t from_lane(uint32_t v, int l) {
+    return __shfl_sync(0xffffffffu, v, l);
+}
+
+// w[t] <- w[t + z] (top-aligned left shift), t = slot*32 + lane; z uniform.
+template <int N>
+__device__ __forceinline__ void shift_left(uint32_t (&w)[N], int z) {
     const int lane = threadIdx.x & 31;
-    while (bound >= 0) {
-        for (int j = lane; j < W; j += 32) {
-            const int64_t x = bound - j;
-            w[j] = x >= 0 ? __ldcg(Z + x) : 0u;
+    for (; z >= 32; z -= 32) {
+#pragma unroll
+        for (int e = 0; e < N - 1; ++e) w[e] = w[e + 1];
+        w[N - 1] = 0u;
+    }
+    const int src = (lane + z) & 31;
+    const bool carry = lane + z >= 32;
+    uint32_t r[N];
+#pragma unroll
+    for (int e = 0; e < N; ++e) r[e] = __shfl_sync(0xffffffffu, w[e], src);
+#pragma unroll
+    for (int e = 0; e < N; ++e) w[e] = carry ? (e + 1 < N ? r[e + 1] : 0u) : r[e];
+}
+
+// w[t] <- w[t - z] (right shift, zeros enter at t < z); z uniform.
+template <int N>
+__device__ __forceinline__ void shift_right(uint32_t (&w)[N], int z) {
+    const int lane = threadIdx.x & 31;
+    for (; z >= 32; z -= 32) {
+#pragma unroll
+        for (int e = N - 1; e > 0; --e) w[e] = w[e - 1];
+        w[0] = 0u;
+    }
+    const int src = (lane - z) & 31;
+    const bool borrow = lane < z;
+    uint32_t r[N];
+#pragma unroll
+    for (int e = 0; e < N; ++e) r[e] = __shfl_sync(0xffffffffu, w[e], src);
+#pragma unroll
+    for (int e = N - 1; e >= 0; --e) w[e] = borrow ? (e > 0 ? r[e - 1] : 0u) : r[e];
+}
+
+// First t >= from with w[t] != 0 (warp-uniform), or -1.
+template <int MODE, int N>
+__device__ __forceinline__ int first_nz(const uint32_t (&w)[N], int from, uint32_t p) {
+    const int lane = threadIdx.x & 31;
+    int z = -1;
+#pragma unroll
+    for (int e = 0; e < N; ++e) {
+        const unsigned m = __ballot_sync(0xffffffffu, Arith<MODE>::nz(w[e], p) && e * 32 + lane >= from);
+        if (z < 0 && m) z = e * 32 + __ffs(m) - 1;
+    }
+    return z;
+}
+
+// Load the top W1 words of Z below `deg` into w; lower `deg` past zero words
+// until w[0] is the nonzero lead (or deg = -1: zero operand).  Warp-uniform.
+template <int MODE>
+__device__ void load_top(uint32_t (&w)[GE], const uint32_t* Z, long long& deg, uint32_t p) {
+    const int lane = threadIdx.x & 31;
+    while (deg >= 0) {
+#pragma unroll
+        for (int e = 0; e < GE; ++e) {
+            const long long x = deg - (e * 32 + lane);
+            w[e] = x >= 0 ? __ldcg(Z + x) : 0u;
         }
-        __syncwarp();
-        const int u = first_nonzero(w, 0, W);
-        if (u >= 0) return u;
-        bound -= W;
-        __syncwarp();
+        const int z = first_nz<MODE>(w, 0, p);
+        if (z == 0) return;
+        deg -= z < 0 ? W1 : z;
     }
-    return -1;
 }
 
-// dst[d] <- y*dst[d] - x*src[d - delta]  over the union support (fraction-free).
-__device__ void p_update(uint32_t* dst, int& dlo, int& dhi, const uint32_t* src, int slo, int shi,
-                         int delta, uint32_t y, uint32_t negx, int W, const FieldParams& F,
-                         int& err) {
+// Warp 0 of CTA 0: the elimination chain of one batch.  Windows are kept
+// oriented: u = current dividend, v = divisor (roles swap with MOVs only, so
+// every shuffle sits in straight-line, warp-uniform code).  Fast path: the
+// new lead is u[1] (z = 1), fetched by one shuffle while the window shifts
+// by one -- no ballot on the critical path.
+template <int MODE>
+__device__ void run_chain(BatchMeta& c, StepLog* log, volatile int* logged, volatile int* done,
+                          int M, Fld f, const uint32_t* X, const uint32_t* Y) {
+    using A = Arith<MODE>;
+    const uint32_t p = f.p;
     const int lane = threadIdx.x & 31;
-    int lo = dlo, hi = dhi;
-    if (slo <= shi) {
-        lo = min(lo, slo + delta);
-        hi = max(hi, shi + delta);
-    }
-    if (lo < -W || hi > W) {
-        err = 1;
-        return;
-    }
-    for (int d = lo + lane; d <= hi; d += 32) {
-        const int e = d - delta;
-        const uint32_t sv = (e >= slo && e <= shi) ? src[e + W] : 0u;
-        const uint32_t dv = (d >= dlo && d <= dhi) ? dst[d + W] : 0u;
-        dst[d + W] = ff_comb(y, dv, negx, sv, F);
-    }
-    dlo = lo;
-    dhi = hi;
-    __syncwarp();
-}
-
-// The step chain of one batch, run by warp 0 (all lanes active).
-__device__ void run_chain(GcdCtl& c, uint32_t* wa, uint32_t* wb, uint32_t* P, const GcdArgs& g,
-                          const uint32_t* X, const uint32_t* Y) {
-    const int W = g.W;
-    const int PL = 2 * W + 1;
-    const FieldParams F = g.F;
-    const int lane = threadIdx.x & 31;
-    int64_t da0 = c.da1, db0 = c.db1;
-    int ua = load_window(wa, X, da0, W);
-    int ub = load_window(wb, Y, db0, W);
-    for (int i = lane; i < 4 * PL; i += 32) P[i] = 0u;
-    __syncwarp();
-    if (lane == 0) {
-        P[0 * PL + W] = 1u;  // P11 = 1
-        P[3 * PL + W] = 1u;  // P22 = 1
-    }
-    __syncwarp();
-    int lo[4] = {0, 1, 1, 0}, hi[4] = {0, 0, 0, 0};
-    int limA = W, limB = W, steps = 0, term = 0, err = 0;
+    long long da = c.da1, db = c.db1;
+    uint32_t u[GE], v[GE];
+    load_top<MODE>(u, X, da, p);
+    load_top<MODE>(v, Y, db, p);
+    const long long da0 = da, db0 = db;
+    // orient: u holds A, v holds B initially
+    bool u_is_a = true;
+    long long du = da, dv = db;
+    int vu = da < W1 ? BIG : W1, vv = db < W1 ? BIG : W1;
+    int su = 0, sv = 0;      // shifts of the operand held in u / v
+    int hu_sup = 0, hv_sup = 0;  // matrix-row support bounds (max index), as the replay tracks
+    uint32_t hu = bcast(u[0]), hv = bcast(v[0]);
     int dividend_a = c.dividend_a;
-    int64_t da = ua < 0 ? -1 : da0 - ua;
-    int64_t db = ub < 0 ? -1 : db0 - ub;
-    bool unknown = false;
-    while (steps < g.S && !unknown) {
-        if (da < 0) { term = 1; break; }
-        if (db < 0) { term = 2; break; }
-        if (dividend_a && da < db) dividend_a = 0;
-        else if (!dividend_a && db < da) dividend_a = 1;
-        if ((dividend_a ? db : da) == 0) { term = 3; break; }
-        // orient: reduce "u" (dividend) by "v" (divisor)
-        uint32_t* wu = dividend_a ? wa : wb;
-        const uint32_t* wv = dividend_a ? wb : wa;
-        int& uu = dividend_a ? ua : ub;
-        const int uv = dividend_a ? ub : ua;
-        int& limu = dividend_a ? limA : limB;
-        const int limv = dividend_a ? limB : limA;
-        const int delta = uu - uv;
-        const uint32_t x = wu[uu], y = wv[uv], negx = negmod(x, F);
-        const int nlim = min(limu, limv + delta);
-        for (int j = uu + lane; j < nlim; j += 32) wu[j] = ff_comb(y, wu[j], negx, wv[j - delta], F);
-        // matrix rows: u-row (P11,P12 or P21,P22) -= shift(v-row, delta)
-        const int ru = dividend_a ? 0 : 2, rv = dividend_a ? 2 : 0;
-        __syncwarp();
-        p_update(P + (ru + 0) * PL, lo[ru + 0], hi[ru + 0], P + (rv + 0) * PL, lo[rv + 0],
-                 hi[rv + 0], delta, y, negx, W, F, err);
-        p_update(P + (ru + 1) * PL, lo[ru + 1], hi[ru + 1], P + (rv + 1) * PL, lo[rv + 1],
-                 hi[rv + 1], delta, y, negx, W, F, err);
-        if (err) break;
-        ++steps;
-        limu = nlim;
-        const int nu = first_nonzero(wu, uu + 1, nlim);
-        int64_t& du = dividend_a ? da : db;
-        const int64_t d0 = dividend_a ? da0 : db0;
-        if (nu >= 0) {
-            uu = nu;
-            du = d0 - nu;
-        } else if (d0 - (nlim - 1) <= 0) {
-            uu = nlim;  // every word down to index 0 is zero: the operand vanished
-            du = -1;
-        } else {
-            uu = nlim;  // the valid window ran out before a nonzero word
-            du = d0 - nlim;
-            unknown = true;
+    if (!dividend_a) {  // orient u = dividend
+#pragma unroll
+        for (int e = 0; e < GE; ++e) {
+            const uint32_t t = u[e];
+            u[e] = v[e];
+            v[e] = t;
         }
+        u_is_a = false;
+        long long t1 = du; du = dv; dv = t1;
+        int t2 = vu; vu = vv; vv = t2;
+        uint32_t t3 = hu; hu = hv; hv = t3;
+    }
+    int steps = 0, term = 0;
+    const int cap = min(M, LOGCAP);
+    for (;;) {
+        // role rule (oracle.cpp:58-66, 74-75): swap when deg(dividend) < deg(divisor)
+        if (du >= 0 && dv >= 0 && du < dv) {
+#pragma unroll
+            for (int e = 0; e < GE; ++e) {
+                const uint32_t t = u[e];
+                u[e] = v[e];
+                v[e] = t;
+            }
+            u_is_a = !u_is_a;
+            long long t1 = du; du = dv; dv = t1;
+            int t2 = vu; vu = vv; vv = t2;
+            int t4 = su; su = sv; sv = t4;
+            int t5 = hu_sup; hu_sup = hv_sup; hv_sup = t5;
+            uint32_t t3 = hu; hu = hv; hv = t3;
+        }
+        if (du < 0) { term = u_is_a ? 1 : 2; break; }  // dividend vanished: gcd = divisor
+        if (dv < 0) { term = u_is_a ? 2 : 1; break; }  // zero divisor (zero input)
+        if (dv == 0) { term = 3; break; }                // unit gcd
+        if (steps >= cap || min(vu, vv) < 2) break;      // batch length / window exhausted
+        const int room = PL - 1 - max(hu_sup, hv_sup);   // matrix capacity for this step's shift
+        if (room < 2) break;
+        const uint32_t x = hu, y = hv, nx = A::neg(x, p);
+#pragma unroll
+        for (int e = 0; e < GE; ++e) u[e] = A::comb(y, u[e], nx, v[e], f);
+        vu = min(vu, vv);
+        // speculate z = 1
+        const uint32_t h1 = from_lane(u[0], 1);
+        int z = 1;
+        bool stop = false;
+        if (A::nz(h1, p) && vu > 1) {
+            shift_left(u, 1);
+            hu = h1;
+        } else {
+            z = first_nz<MODE>(u, 1, p);
+            if (z < 0 || z >= vu) {
+                if (vu >= BIG) {  // window held the whole operand: it vanished
+                    du = -1;
+                    z = 0;
+                } else {
+                    z = vu;       // lead not determined inside the valid words
+                    stop = true;
+                }
+            }
+            if (z > room) {       // matrix capacity: shift only as far as it holds
+                z = room;
+                stop = true;
+            }
+            if (du >= 0) {
+                shift_left(u, z);
+                hu = bcast(u[0]);
+            }
+        }
+        if (du >= 0) {
+            du -= z;
+            if (vu < BIG) vu -= z;
+        }
+        su += z;
+        hu_sup = max(hu_sup, hv_sup) + z;
+        if (lane == 0) {
+            log[steps] = StepLog{x, y, z, u_is_a ? 1 : 0};
+            st_release_cta(logged, steps + 1);
+        }
+        ++steps;
+        if (stop) break;
     }
     if (lane == 0) {
         c.da0 = da0;
         c.db0 = db0;
-        c.da1 = da;
-        c.db1 = db;
-        for (int i = 0; i < 4; ++i) {
-            c.lo[i] = lo[i];
-            c.hi[i] = hi[i];
-        }
+        c.da1 = u_is_a ? du : dv;
+        c.db1 = u_is_a ? dv : du;
         c.steps = steps;
         c.term = term;
-        c.dividend_a = dividend_a;
-        c.err = err;
+        c.dividend_a = u_is_a ? 1 : 0;
+        c.sa = u_is_a ? su : sv;
+        c.sb = u_is_a ? sv : su;
+        st_release_cta(done, 1);
     }
 }
 
-// Z1[x] = sum_{d in [lo1,hi1]} P1[d] Z0[x+d] + sum_{d in [lo2,hi2]} P2[d] V0[x+sh+d]
-// for x in [xs, xe): the matrix row applied by one CTA (all threads).
-__device__ void apply_row(uint32_t* out, int64_t xs, int64_t xe, const uint32_t* P1, int lo1,
-                          int hi1, const uint32_t* Z0, int64_t zb, const uint32_t* P2, int lo2,
-                          int hi2, const uint32_t* V0, int64_t vb, int64_t sh, uint32_t* sw,
-                          uint32_t* sv, int ORG, int W, const FieldParams& F) {
+// Warps 1 and 2 of CTA 0: replay the step log into matrix column `col`
+// (both rows), oriented like the chain; then publish it (canonical) to Pg.
+template <int MODE>
+__device__ void run_replay(int col, const StepLog* log, volatile int* logged, volatile int* done,
+                           Fld f, uint32_t* Pg, int* hi_out) {
+    using A = Arith<MODE>;
+    const uint32_t p = f.p;
+    const int lane = threadIdx.x & 31;
+    uint32_t ru[PE], rv[PE];  // rows of the operands held in the chain's u / v
+#pragma unroll
+    for (int e = 0; e < PE; ++e) ru[e] = rv[e] = 0u;
+    // identity: row A col 0 = 1, row B col 1 = 1; start oriented u = A
+    if (lane == 0) {
+        if (col == 0) ru[0] = 1u;
+        else rv[0] = 1u;
+    }
+    bool u_is_a = true;
+    int hu = col == 0 ? 0 : -1, hv = col == 0 ? -1 : 0;
+    const volatile StepLog* vlog = log;
+    int i = 0;
+    for (;;) {
+        int n = __shfl_sync(0xffffffffu, ld_acquire_cta(logged), 0);
+        if (n <= i) {
+            const int d = __shfl_sync(0xffffffffu, ld_acquire_cta(done), 0);
+            n = __shfl_sync(0xffffffffu, ld_acquire_cta(logged), 0);
+            if (n <= i) {
+                if (d) break;
+                __nanosleep(64);  // back off: spinning LDS/SHFL would crowd the chain's
+                continue;         // shuffles out of the SM's MIO pipe
+            }
+        }
+        for (; i < n; ++i) {
+            const uint32_t x = vlog[i].x, y = vlog[i].y;
+            const int z = vlog[i].z;
+            const bool sa = vlog[i].u_is_a != 0;
+            if (sa != u_is_a) {
+#pragma unroll
+                for (int e = 0; e < PE; ++e) {
+                    const uint32_t t = ru[e];
+                    ru[e] = rv[e];
+                    rv[e] = t;
+                }
+                const int t = hu; hu = hv; hv = t;
+                u_is_a = sa;
+            }
+            const uint32_t nx = A::neg(x, p);
+#pragma unroll
+            for (int e = 0; e < PE; ++e) ru[e] = A::comb(y, ru[e], nx, rv[e], f);
+            shift_right(ru, z);
+            hu = max(hu, hv);
+            if (hu >= 0) hu += z;
+        }
+    }
+    uint32_t* Pa = Pg + (0 * 2 + col) * PL;  // row A, column col
+    uint32_t* Pb = Pg + (1 * 2 + col) * PL;  // row B, column col
+#pragma unroll
+    for (int e = 0; e < PE; ++e) {
+        const uint32_t a = A::canon(u_is_a ? ru[e] : rv[e], p);
+        const uint32_t b = A::canon(u_is_a ? rv[e] : ru[e], p);
+        __stcg(Pa + e * 32 + lane, a);
+        __stcg(Pb + e * 32 + lane, b);
+    }
+    if (lane == 0) {
+        hi_out[0 * 2 + col] = min(u_is_a ? hu : hv, PL - 1);
+        hi_out[1 * 2 + col] = min(u_is_a ? hv : hu, PL - 1);
+    }
+}
+
+// out[x] = sum_{e<=h1} P1[e] Z1[x + s1 - e] + sum_{e<=h2} P2[e] Z2[x + s2 - e],
+// x in [xs, xe); Zi[j] = 0 outside [0, bi].  One CTA, all threads.
+__device__ void apply_row(uint32_t* out, long long xs, long long xe, const uint32_t* P1, int h1,
+                          const uint32_t* Z1, long long b1, long long s1, const uint32_t* P2,
+                          int h2, const uint32_t* Z2, long long b2, long long s2, uint32_t* sw,
+                          uint32_t* sv, int ORG, const FieldParams& F) {
     constexpr int R = GCD_R;
-    const int64_t n = xe - xs;
+    const long long n = xe - xs;
     if (n <= 0) return;
-    for (int64_t c0 = 0; c0 < n; c0 += int64_t(GCD_T) * R) {
-        const int64_t cn = i64min(n - c0, int64_t(GCD_T) * R);
+    for (long long c0 = 0; c0 < n; c0 += (long long)GCD_T * R) {
+        const long long cn = min(n - c0, (long long)GCD_T * R);
         uint64_t acc[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) acc[r] = 0;
         uint32_t since = 0;
         for (int term = 0; term < 2; ++term) {
+            const int h = term ? h2 : h1;
+            if (h < 0) continue;
             const uint32_t* Pt = term ? P2 : P1;
-            const int lo = term ? lo2 : lo1, hi = term ? hi2 : hi1;
-            if (lo > hi) continue;
-            const uint32_t* Zt = term ? V0 : Z0;
-            const int64_t zbound = term ? vb : zb;
-            const int64_t off = xs + c0 + (term ? sh : 0) + hi - ORG;  // sv[y] = Zt[y + off]
-            const int width = hi - lo + 1, wpad = (width + R - 1) / R * R;
+            const uint32_t* Zt = term ? Z2 : Z1;
+            const long long zb = term ? b2 : b1;
+            const long long off = xs + c0 + (term ? s2 : s1) - ORG;  // sv[y] = Zt[y + off]
+            const int width = h + 1, wpad = (width + R - 1) / R * R;
             __syncthreads();
-            for (int u = threadIdx.x; u < wpad; u += GCD_T) sw[u] = u < width ? Pt[hi - u + W] : 0u;
-            for (int64_t y = threadIdx.x; y < ORG + cn + R; y += GCD_T) {
-                const int64_t x = y + off;
-                sv[y] = (x >= 0 && x <= zbound) ? __ldcg(Zt + x) : 0u;
+            for (int u = threadIdx.x; u < wpad; u += GCD_T) sw[u] = u < width ? __ldcg(Pt + u) : 0u;
+            for (long long y = threadIdx.x; y < ORG + cn + R; y += GCD_T) {
+                const long long x = y + off;
+                sv[y] = (x >= 0 && x <= zb) ? __ldcg(Zt + x) : 0u;
             }
             __syncthreads();
-            const int64_t y0 = int64_t(threadIdx.x) * R;
+            const long long y0 = (long long)threadIdx.x * R;
             if (y0 < cn) conv_accumulate<R>(acc, sw, wpad / R, sv, int(ORG + y0), since, F);
         }
-        const int64_t y0 = int64_t(threadIdx.x) * R;
+        const long long y0 = (long long)threadIdx.x * R;
 #pragma unroll
         for (int r = 0; r < R; ++r)
             if (y0 + r < cn) __stcg(out + xs + c0 + y0 + r, reduce(acc[r], F));
@@ -247,77 +426,128 @@ __device__ void apply_row(uint32_t* out, int64_t xs, int64_t xe, const uint32_t*
 
 }  // namespace
 
-__global__ void __launch_bounds__(GCD_T) gcd_kernel(GcdArgs g) {
+template <int MODE>
+__global__ void __launch_bounds__(GCD_T, 1) gcd_kernel(GcdArgs g) {
     extern __shared__ __align__(16) uint32_t smem[];
-    __shared__ GcdCtl ctl;
+    __shared__ BatchMeta ctl;
+    __shared__ int hi_s[4];
+    __shared__ volatile int logged, done;
     cg::grid_group grid = cg::this_grid();
-    const int W = g.W, PL = 2 * W + 1;
     const FieldParams F = g.F;
-    const int ORG = ((PL + 3) & ~3) + 3 + 4;
-    const int64_t span = int64_t(GCD_T) * GCD_R;
-    uint32_t* wa = smem;
-    uint32_t* wb = wa + ((W + 3) & ~3);
-    uint32_t* P = wb + ((W + 3) & ~3);
-    uint32_t* sw = P + ((4 * PL + 3) & ~3);
-    uint32_t* sv = sw + ((PL + 3 + 4) & ~3);
+    constexpr int ORG = PL + 8 + 3;
+    StepLog* log = reinterpret_cast<StepLog*>(smem);                 // LOGCAP entries
+    uint32_t* sw = smem + 4 * LOGCAP;                                 // PL + 8 words
+    uint32_t* sv = sw + PL + 8;                                       // ORG + GCD_T*R + R
+    const long long tid = (long long)blockIdx.x * GCD_T + threadIdx.x;
+    const long long nth = (long long)gridDim.x * GCD_T;
+    const int warp = threadIdx.x >> 5;
 
-    const int64_t tid = int64_t(blockIdx.x) * GCD_T + threadIdx.x;
-    const int64_t nthreads = int64_t(gridDim.x) * GCD_T;
-    for (int64_t i = tid; i < g.na; i += nthreads) g.X[0][i] = g.a[i];
-    for (int64_t i = tid; i < g.nb; i += nthreads) g.Y[0][i] = g.b[i];
+    for (long long i = tid; i < g.na; i += nth) g.X[0][i] = g.a[i];
+    for (long long i = tid; i < g.nb; i += nth) g.Y[0][i] = g.b[i];
     if (threadIdx.x == 0) {
         ctl.da1 = g.na - 1;
         ctl.db1 = g.nb - 1;
         ctl.dividend_a = 1;  // oracle_gcd: x = a is the first dividend (oracle.cpp:70)
-        ctl.term = 0;
-        ctl.err = 0;
     }
     grid.sync();
 
     int cur = 0;
     for (;;) {
-        if (threadIdx.x < 32) run_chain(ctl, wa, wb, P, g, g.X[cur], g.Y[cur]);
-        __syncthreads();
-        if (ctl.err || (ctl.steps == 0 && ctl.term == 0)) {
-            // internal invariant broken: report through the length word
-            if (blockIdx.x == 0 && threadIdx.x == 0) *g.ng = ctl.err ? -1 : -2;
-            return;  // grid-uniform decision: every CTA exits here
+        long long t_chain0 = clock64();
+        if (blockIdx.x == 0) {
+            if (threadIdx.x == 0) {
+                logged = 0;
+                done = 0;
+            }
+            __syncthreads();
+            if (warp == 0) {
+                run_chain<MODE>(ctl, log, &logged, &done, g.M, Fld{F.p, F.pinv},
+                                (cur ? g.X[1] : g.X[0]), (cur ? g.Y[1] : g.Y[0]));
+                if (g.stats && threadIdx.x == 0) g.stats[4] += clock64() - t_chain0;
+            }
+            else if (warp <= 2) {
+                run_replay<MODE>(warp - 1, log, &logged, &done, Fld{F.p, F.pinv}, g.Pg, hi_s);
+                if (g.stats && threadIdx.x == 32) g.stats[5] += clock64() - t_chain0;
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                BatchMeta m = ctl;
+                for (int i = 0; i < 4; ++i) m.hi[i] = hi_s[i];
+                m.err = 0;
+                *g.meta = m;
+                __threadfence();
+                if (g.stats) {
+                    g.stats[0] += 1;
+                    g.stats[1] += ctl.steps;
+                    g.stats[2] += clock64() - t_chain0;
+                }
+            }
         }
-        if (ctl.term == 3) break;
-        if (ctl.steps > 0) {
-            // apply the batch matrix: outputs A1[0..da1], B1[0..db1]
-            const int64_t na1 = ctl.da1 + 1 > 0 ? ctl.da1 + 1 : 0;
-            const int64_t nb1 = ctl.db1 + 1 > 0 ? ctl.db1 + 1 : 0;
-            const int64_t per = (na1 + nb1 + gridDim.x - 1) / gridDim.x;
-            const int64_t s0 = int64_t(blockIdx.x) * per, s1 = i64min(s0 + per, na1 + nb1);
-            const int64_t da0 = ctl.da0, db0 = ctl.db0;
-            // A part of this CTA's slice of [A1 | B1]
-            apply_row(g.X[cur ^ 1], i64min(s0, na1), i64min(s1, na1), P + 0 * PL, ctl.lo[0],
-                      ctl.hi[0], g.X[cur], da0, P + 1 * PL, ctl.lo[1], ctl.hi[1], g.Y[cur], db0,
-                      db0 - da0, sw, sv, ORG, W, F);
-            apply_row(g.Y[cur ^ 1], i64max(s0 - na1, 0), i64max(s1 - na1, 0), P + 3 * PL,
-                      ctl.lo[3], ctl.hi[3], g.Y[cur], db0, P + 2 * PL, ctl.lo[2], ctl.hi[2],
-                      g.X[cur], da0, da0 - db0, sw, sv, ORG, W, F);
-            (void)span;
+        grid.sync();
+        // one reader per CTA: every thread polling the same global line would
+        // serialise ~25k requests on one L2 slice per batch
+        __shared__ BatchMeta ms;
+        if (threadIdx.x == 0) {
+            const volatile BatchMeta* vm = g.meta;
+            ms.da0 = vm->da0; ms.db0 = vm->db0; ms.da1 = vm->da1; ms.db1 = vm->db1;
+            ms.steps = vm->steps; ms.term = vm->term; ms.dividend_a = vm->dividend_a;
+            ms.sa = vm->sa; ms.sb = vm->sb;
+            for (int i = 0; i < 4; ++i) ms.hi[i] = vm->hi[i];
+        }
+        __syncthreads();
+        const BatchMeta m = ms;
+        if (m.steps == 0 && m.term == 0) {  // invariant broken: no progress
+            if (tid == 0) *g.ng = -2;
+            return;                         // grid-uniform
+        }
+        if (m.term == 3) break;
+        if (m.steps > 0) {
+            const long long na1 = m.da1 + 1 > 0 ? m.da1 + 1 : 0;
+            const long long nb1 = m.db1 + 1 > 0 ? m.db1 + 1 : 0;
+            const long long per = (na1 + nb1 + gridDim.x - 1) / gridDim.x;
+            const long long s0 = (long long)blockIdx.x * per;
+            const long long s1 = min(s0 + per, na1 + nb1);
+            // A1[x] = Pa1 * A0 (shift sa) + Pa2 * B0 (shift sa + db0 - da0)
+            apply_row((cur ? g.X[0] : g.X[1]), min(s0, na1), min(s1, na1), g.Pg + 0 * PL, m.hi[0],
+                      (cur ? g.X[1] : g.X[0]), m.da0, m.sa, g.Pg + 1 * PL, m.hi[1], (cur ? g.Y[1] : g.Y[0]), m.db0,
+                      m.sa + m.db0 - m.da0, sw, sv, ORG, F);
+            // B1[x] = Pb1 * A0 (shift sb + da0 - db0) + Pb2 * B0 (shift sb)
+            apply_row((cur ? g.Y[0] : g.Y[1]), max(s0 - na1, 0LL), max(s1 - na1, 0LL), g.Pg + 2 * PL,
+                      m.hi[2], (cur ? g.X[1] : g.X[0]), m.da0, m.sb + m.da0 - m.db0, g.Pg + 3 * PL, m.hi[3],
+                      (cur ? g.Y[1] : g.Y[0]), m.db0, m.sb, sw, sv, ORG, F);
             grid.sync();
+            if (g.stats && tid == 0) g.stats[3] += clock64() - t_chain0;
             cur ^= 1;
         }
-        if (ctl.term) break;
+        if (m.term) {
+            ctl.term = m.term;
+            ctl.da1 = m.da1;
+            ctl.db1 = m.db1;
+            break;
+        }
     }
-    // finalize: monic of the surviving operand, or 1
     __syncthreads();
-    if (ctl.term == 3) {
-        if (blockIdx.x == 0 && threadIdx.x == 0) {
+    __shared__ BatchMeta fs;
+    if (threadIdx.x == 0) {
+        const volatile BatchMeta* vm = g.meta;
+        fs.term = vm->term;
+        fs.da1 = vm->da1;
+        fs.db1 = vm->db1;
+    }
+    __syncthreads();
+    const BatchMeta fin = fs;
+    if (fin.term == 3) {
+        if (tid == 0) {
             g.g[0] = 1u;
             *g.ng = 1;
         }
         return;
     }
-    const uint32_t* Z = ctl.term == 1 ? g.Y[cur] : g.X[cur];
-    const int64_t dz = ctl.term == 1 ? ctl.db1 : ctl.da1;
+    const uint32_t* Z = fin.term == 1 ? (cur ? g.Y[1] : g.Y[0]) : (cur ? g.X[1] : g.X[0]);
+    const long long dz = fin.term == 1 ? fin.db1 : fin.da1;
     const uint32_t inv = invmod(__ldcg(Z + dz), F);
-    for (int64_t i = tid; i <= dz; i += nthreads) g.g[i] = mulmod(__ldcg(Z + i), inv, F);
-    if (blockIdx.x == 0 && threadIdx.x == 0) *g.ng = dz + 1;
+    for (long long i = tid; i <= dz; i += nth) g.g[i] = mulmod(__ldcg(Z + i), inv, F);
+    if (tid == 0) *g.ng = dz + 1;
 }
 
 void launch_gcd(const FieldParams& F, const uint32_t* a, int64_t na, const uint32_t* b, int64_t nb,
@@ -331,30 +561,43 @@ void launch_gcd(const FieldParams& F, const uint32_t* a, int64_t na, const uint3
     g.g = gout;
     g.ng = d_ng;
     g.F = F;
-    g.S = int(std::min<int64_t>(s, 1024));
-    g.W = 2 * g.S + 32;
-    g.cap = std::max<int64_t>(std::max(na, nb), 1);
+    g.M = int(std::min<int64_t>(s, LOGCAP));
+    const int64_t cap = std::max<int64_t>(std::max(na, nb), 1);
     Scratch sc(st);
     for (int i = 0; i < 2; ++i) {
-        g.X[i] = sc.get<uint32_t>(size_t(g.cap));
-        g.Y[i] = sc.get<uint32_t>(size_t(g.cap));
+        g.X[i] = sc.get<uint32_t>(size_t(cap));
+        g.Y[i] = sc.get<uint32_t>(size_t(cap));
     }
-    const int W = g.W, PL = 2 * W + 1;
-    const int ORG = ((PL + 3) & ~3) + 3 + 4;
-    const size_t words = size_t(2 * ((W + 3) & ~3) + ((4 * PL + 3) & ~3) + ((PL + 3 + 4) & ~3) +
-                                ORG + int64_t(GCD_T) * GCD_R + GCD_R + 8);
-    const size_t bytes = words * 4;
-    MMM_CUDA(cudaFuncSetAttribute(gcd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  int(bytes)));
+    g.Pg = sc.get<uint32_t>(4 * PL);
+    g.meta = reinterpret_cast<BatchMeta*>(sc.get<uint64_t>((sizeof(BatchMeta) + 7) / 8));
+    constexpr int ORG = PL + 8 + 3;
+    const size_t bytes = size_t(4 * LOGCAP + PL + 8 + ORG + GCD_T * GCD_R + GCD_R + 8) * 4;
+    const int mode = !F.odd ? 2 : (F.p < (1u << 29) ? 0 : 1);
+    const void* fn = mode == 0 ? (const void*)gcd_kernel<0>
+                               : (mode == 1 ? (const void*)gcd_kernel<1> : (const void*)gcd_kernel<2>);
+    MMM_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
     int per_sm = 0;
-    MMM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gcd_kernel, GCD_T, bytes));
-    if (per_sm < 1) throw Error(ST_INVALID, "gcd: s too large for shared memory");
-    const int64_t want = std::max<int64_t>(1, ceil_div(na + nb, 512));
+    MMM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, GCD_T, bytes));
+    if (per_sm < 1) throw Error(ST_INVALID, "gcd: kernel does not fit an SM");
+    const int64_t want = std::max<int64_t>(1, ceil_div(na + nb, 256));
     const int blocks = int(std::min<int64_t>(want, int64_t(sm_count()) * per_sm));
+    const bool want_stats = getenv("MMM_GCD_STATS") != nullptr;
+    if (want_stats) {
+        g.stats = sc.get<long long>(6);
+        MMM_CUDA(cudaMemsetAsync(g.stats, 0, 6 * sizeof(long long), st));
+    }
     void* params[] = {&g};
-    MMM_CUDA(cudaLaunchCooperativeKernel((void*)gcd_kernel, dim3(blocks), dim3(GCD_T), params, bytes,
-                                         st));
+    MMM_CUDA(cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(GCD_T), params, bytes, st));
     check_launch("gcd_kernel");
+    if (want_stats) {
+        long long h[6];
+        MMM_CUDA(cudaMemcpyAsync(h, g.stats, sizeof(h), cudaMemcpyDeviceToHost, st));
+        MMM_CUDA(cudaStreamSynchronize(st));
+        fprintf(stderr,
+                "gcd stats: blocks=%d batches=%lld steps=%lld cta0_cycles=%lld total_cycles=%lld "
+                "chain_warp_cycles=%lld replay_warp_cycles=%lld\n",
+                blocks, h[0], h[1], h[2], h[3], h[4], h[5]);
+    }
 }
 
 }  // namespace mmm_cu
