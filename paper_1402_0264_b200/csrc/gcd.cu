@@ -45,8 +45,8 @@ namespace mmm_cu {
 constexpr int GCD_T = 256;         // threads per CTA
 constexpr int GE = 4;              // window words per lane
 constexpr int W1 = 32 * GE;        // window words per operand (128)
-constexpr int PE = 8;              // matrix words per lane per polynomial
-constexpr int PL = 32 * PE;        // matrix capacity (support < 256)
+constexpr int PE = 4;              // matrix words per lane per polynomial
+constexpr int PL = 32 * PE;        // matrix capacity (support < 128)
 constexpr int LOGCAP = 2048;       // steps per matrix batch, hard cap
 constexpr int BIG = 1 << 30;       // "validity unbounded": window covers the operand
 constexpr int GCD_R = 1;           // outputs per thread in the apply
@@ -79,6 +79,7 @@ struct GcdArgs {
     int M;            // steps per batch (the program parameter s)
     FieldParams F;
     long long* stats; // optional (MMM_GCD_STATS): batches, steps, chain/apply cycles
+    int dbg;          // MMM_GCD_DEBUG bits (timing experiments; 2 = serialise chain and replay)
 };
 
 namespace {
@@ -168,6 +169,32 @@ __device__ __forceinline__ void shift_right(uint32_t (&w)[N], int z) {
     for (int e = N - 1; e >= 0; --e) w[e] = borrow ? (e > 0 ? r[e - 1] : 0u) : r[e];
 }
 
+// Fast one-word shifts (the common renormalisation), touching only the first
+// `na` slots (warp-uniform): words beyond them are dead (past the validity
+// of a window, or past the support of a matrix row).
+template <int N>
+__device__ __forceinline__ void shift_left1(uint32_t (&w)[N], int na) {
+    const int lane = threadIdx.x & 31;
+    uint32_t r[N];
+#pragma unroll
+    for (int e = 0; e < N; ++e)
+        if (e < na) r[e] = __shfl_sync(0xffffffffu, w[e], (lane + 1) & 31);
+#pragma unroll
+    for (int e = 0; e < N; ++e)
+        if (e < na) w[e] = lane == 31 ? (e + 1 < N && e + 1 < na ? r[e + 1] : 0u) : r[e];
+}
+template <int N>
+__device__ __forceinline__ void shift_right1(uint32_t (&w)[N], int na) {
+    const int lane = threadIdx.x & 31;
+    uint32_t r[N];
+#pragma unroll
+    for (int e = 0; e < N; ++e)
+        if (e < na) r[e] = __shfl_sync(0xffffffffu, w[e], (lane - 1) & 31);
+#pragma unroll
+    for (int e = N - 1; e >= 0; --e)
+        if (e < na) w[e] = lane == 0 ? (e > 0 ? r[e - 1] : 0u) : r[e];
+}
+
 // First t >= from with w[t] != 0 (warp-uniform), or -1.
 template <int MODE, int N>
 __device__ __forceinline__ int first_nz(const uint32_t (&w)[N], int from, uint32_t p) {
@@ -198,88 +225,102 @@ __device__ void load_top(uint32_t (&w)[GE], const uint32_t* Z, long long& deg, u
     }
 }
 
+// Log entries: the chain buffers entry s in lane s % 32 and stores 32 at a
+// time, one 16-byte store per lane; `seq` = step index + 1 publishes an entry
+// (the replay warps poll the entry itself, no per-step fence or store).
+__device__ __forceinline__ void log_flush(StepLog* log, int base, int count, uint32_t x,
+                                          uint32_t y, uint32_t zf) {
+    const int lane = threadIdx.x & 31;
+    if (lane < count) {
+        const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(log + base + lane));
+        asm volatile("st.volatile.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(x), "r"(y),
+                     "r"(zf), "r"(unsigned(base + lane + 1))
+                     : "memory");
+    }
+}
+__device__ __forceinline__ uint4 log_get(const StepLog* log, int i) {
+    const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(const_cast<StepLog*>(log + i)));
+    uint4 v;
+    asm volatile("ld.volatile.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(a)
+                 : "memory");
+    return v;
+}
+
 // Warp 0 of CTA 0: the elimination chain of one batch.  Windows are kept
 // oriented: u = current dividend, v = divisor (roles swap with MOVs only, so
 // every shuffle sits in straight-line, warp-uniform code).  Fast path: the
 // new lead is u[1] (z = 1), fetched by one shuffle while the window shifts
-// by one -- no ballot on the critical path.
+// by one; all capacity checks collapse into one budget counter F of steps
+// that provably cannot exhaust the windows or the matrix.
 template <int MODE>
-__device__ void run_chain(BatchMeta& c, StepLog* log, volatile int* logged, volatile int* done,
-                          int M, Fld f, const uint32_t* X, const uint32_t* Y) {
+__device__ void run_chain(BatchMeta& c, StepLog* log, volatile int* done, int M, Fld f,
+                          const uint32_t* X, const uint32_t* Y) {
     using A = Arith<MODE>;
     const uint32_t p = f.p;
-    const int lane = threadIdx.x & 31;
     long long da = c.da1, db = c.db1;
     uint32_t u[GE], v[GE];
     load_top<MODE>(u, X, da, p);
     load_top<MODE>(v, Y, db, p);
     const long long da0 = da, db0 = db;
-    // orient: u holds A, v holds B initially
     bool u_is_a = true;
-    long long du = da, dv = db;
+    int du = int(da), dv = int(db);
     int vu = da < W1 ? BIG : W1, vv = db < W1 ? BIG : W1;
-    int su = 0, sv = 0;      // shifts of the operand held in u / v
-    int hu_sup = 0, hv_sup = 0;  // matrix-row support bounds (max index), as the replay tracks
+    int su = 0, sv = 0, supu = 0, supv = 0;
     uint32_t hu = bcast(u[0]), hv = bcast(v[0]);
-    int dividend_a = c.dividend_a;
-    if (!dividend_a) {  // orient u = dividend
+    auto swap_roles = [&]() {
 #pragma unroll
         for (int e = 0; e < GE; ++e) {
             const uint32_t t = u[e];
             u[e] = v[e];
             v[e] = t;
         }
-        u_is_a = false;
-        long long t1 = du; du = dv; dv = t1;
-        int t2 = vu; vu = vv; vv = t2;
-        uint32_t t3 = hu; hu = hv; hv = t3;
-    }
-    int steps = 0, term = 0;
+        u_is_a = !u_is_a;
+        int t;
+        t = du; du = dv; dv = t;
+        t = vu; vu = vv; vv = t;
+        t = su; su = sv; sv = t;
+        t = supu; supu = supv; supv = t;
+        const uint32_t h = hu; hu = hv; hv = h;
+    };
+    if (!c.dividend_a) swap_roles();
     const int cap = min(M, LOGCAP);
+    const int lane = threadIdx.x & 31;
+    int steps = 0, term = 0, F = 0;
+    uint32_t lx = 0, ly = 0, lz = 0;  // this lane's buffered log entry
     for (;;) {
-        // role rule (oracle.cpp:58-66, 74-75): swap when deg(dividend) < deg(divisor)
-        if (du >= 0 && dv >= 0 && du < dv) {
-#pragma unroll
-            for (int e = 0; e < GE; ++e) {
-                const uint32_t t = u[e];
-                u[e] = v[e];
-                v[e] = t;
-            }
-            u_is_a = !u_is_a;
-            long long t1 = du; du = dv; dv = t1;
-            int t2 = vu; vu = vv; vv = t2;
-            int t4 = su; su = sv; sv = t4;
-            int t5 = hu_sup; hu_sup = hv_sup; hv_sup = t5;
-            uint32_t t3 = hu; hu = hv; hv = t3;
+        if (du >= 0 && dv >= 0 && du < dv) swap_roles();  // oracle.cpp:58-66, 74-75
+        if (F <= 0) {
+            if (du < 0) { term = u_is_a ? 1 : 2; break; }  // dividend vanished: gcd = divisor
+            if (dv < 0) { term = u_is_a ? 2 : 1; break; }  // zero divisor (zero input)
+            F = min(cap - steps, min(min(vu, vv) - 2, PL - 2 - max(supu, supv)));
+            if (F <= 0) break;  // batch length, window or matrix exhausted
         }
-        if (du < 0) { term = u_is_a ? 1 : 2; break; }  // dividend vanished: gcd = divisor
-        if (dv < 0) { term = u_is_a ? 2 : 1; break; }  // zero divisor (zero input)
-        if (dv == 0) { term = 3; break; }                // unit gcd
-        if (steps >= cap || min(vu, vv) < 2) break;      // batch length / window exhausted
-        const int room = PL - 1 - max(hu_sup, hv_sup);   // matrix capacity for this step's shift
-        if (room < 2) break;
+        if (dv == 0) { term = 3; break; }  // constant divisor: unit gcd
         const uint32_t x = hu, y = hv, nx = A::neg(x, p);
+        vu = min(vu, vv);
 #pragma unroll
         for (int e = 0; e < GE; ++e) u[e] = A::comb(y, u[e], nx, v[e], f);
-        vu = min(vu, vv);
-        // speculate z = 1
         const uint32_t h1 = from_lane(u[0], 1);
         int z = 1;
         bool stop = false;
-        if (A::nz(h1, p) && vu > 1) {
-            shift_left(u, 1);
+        if (A::nz(h1, p)) {  // fast path: the next word is the new lead
+            shift_left1(u, GE);
             hu = h1;
+            --F;
         } else {
             z = first_nz<MODE>(u, 1, p);
             if (z < 0 || z >= vu) {
                 if (vu >= BIG) {  // window held the whole operand: it vanished
                     du = -1;
                     z = 0;
-                } else {
-                    z = vu;       // lead not determined inside the valid words
+                } else {          // lead not determined inside the valid words
+                    z = vu;
                     stop = true;
                 }
             }
+            const int room = PL - 1 - max(supu, supv);
             if (z > room) {       // matrix capacity: shift only as far as it holds
                 z = room;
                 stop = true;
@@ -288,21 +329,26 @@ __device__ void run_chain(BatchMeta& c, StepLog* log, volatile int* logged, vola
                 shift_left(u, z);
                 hu = bcast(u[0]);
             }
+            F = 0;                // re-derive the budget
         }
         if (du >= 0) {
             du -= z;
             if (vu < BIG) vu -= z;
         }
         su += z;
-        hu_sup = max(hu_sup, hv_sup) + z;
-        if (lane == 0) {
-            log[steps] = StepLog{x, y, z, u_is_a ? 1 : 0};
-            st_release_cta(logged, steps + 1);
+        supu = max(supu, supv) + z;
+        // buffer the log entry in lane (steps % 32); flush 32 at a time
+        if (lane == (steps & 31)) {
+            lx = x;
+            ly = y;
+            lz = unsigned(z) | (u_is_a ? 0x10000u : 0u);
         }
         ++steps;
+        if ((steps & 31) == 0) log_flush(log, steps - 32, 32, lx, ly, lz);
         if (stop) break;
     }
-    if (lane == 0) {
+    if (steps & 31) log_flush(log, steps & ~31, steps & 31, lx, ly, lz);
+    if ((threadIdx.x & 31) == 0) {
         c.da0 = da0;
         c.db0 = db0;
         c.da1 = u_is_a ? du : dv;
@@ -312,71 +358,63 @@ __device__ void run_chain(BatchMeta& c, StepLog* log, volatile int* logged, vola
         c.dividend_a = u_is_a ? 1 : 0;
         c.sa = u_is_a ? su : sv;
         c.sb = u_is_a ? sv : su;
-        st_release_cta(done, 1);
+        st_release_cta(done, steps + 1);  // done = final count + 1
     }
 }
 
 // Warps 1 and 2 of CTA 0: replay the step log into matrix column `col`
 // (both rows), oriented like the chain; then publish it (canonical) to Pg.
 template <int MODE>
-__device__ void run_replay(int col, const StepLog* log, volatile int* logged, volatile int* done,
-                           Fld f, uint32_t* Pg, int* hi_out) {
+__device__ void run_replay(int col, const StepLog* log, volatile int* done, Fld f, uint32_t* Pg,
+                           int* hi_out) {
     using A = Arith<MODE>;
     const uint32_t p = f.p;
     const int lane = threadIdx.x & 31;
     uint32_t ru[PE], rv[PE];  // rows of the operands held in the chain's u / v
 #pragma unroll
     for (int e = 0; e < PE; ++e) ru[e] = rv[e] = 0u;
-    // identity: row A col 0 = 1, row B col 1 = 1; start oriented u = A
-    if (lane == 0) {
+    if (lane == 0) {  // identity: row A col 0 = 1, row B col 1 = 1; oriented u = A
         if (col == 0) ru[0] = 1u;
         else rv[0] = 1u;
     }
     bool u_is_a = true;
     int hu = col == 0 ? 0 : -1, hv = col == 0 ? -1 : 0;
-    const volatile StepLog* vlog = log;
-    int i = 0;
-    for (;;) {
-        int n = __shfl_sync(0xffffffffu, ld_acquire_cta(logged), 0);
-        if (n <= i) {
-            const int d = __shfl_sync(0xffffffffu, ld_acquire_cta(done), 0);
-            n = __shfl_sync(0xffffffffu, ld_acquire_cta(logged), 0);
-            if (n <= i) {
-                if (d) break;
-                __nanosleep(64);  // back off: spinning LDS/SHFL would crowd the chain's
-                continue;         // shuffles out of the SM's MIO pipe
-            }
+    for (int i = 0;; ++i) {
+        uint4 en = log_get(log, i);
+        while (en.w != unsigned(i + 1)) {
+            const int d = ld_acquire_cta(done);
+            if (d != 0 && d - 1 <= i) break;  // chain finished with i entries
+            __nanosleep(32);
+            en = log_get(log, i);
         }
-        for (; i < n; ++i) {
-            const uint32_t x = vlog[i].x, y = vlog[i].y;
-            const int z = vlog[i].z;
-            const bool sa = vlog[i].u_is_a != 0;
-            if (sa != u_is_a) {
+        if (en.w != unsigned(i + 1)) break;
+        const bool sa = (en.z >> 16) != 0;
+        const int z = int(en.z & 0xFFFFu);
+        if (sa != u_is_a) {
 #pragma unroll
-                for (int e = 0; e < PE; ++e) {
-                    const uint32_t t = ru[e];
-                    ru[e] = rv[e];
-                    rv[e] = t;
-                }
-                const int t = hu; hu = hv; hv = t;
-                u_is_a = sa;
+            for (int e = 0; e < PE; ++e) {
+                const uint32_t t = ru[e];
+                ru[e] = rv[e];
+                rv[e] = t;
             }
-            const uint32_t nx = A::neg(x, p);
-#pragma unroll
-            for (int e = 0; e < PE; ++e) ru[e] = A::comb(y, ru[e], nx, rv[e], f);
-            shift_right(ru, z);
-            hu = max(hu, hv);
-            if (hu >= 0) hu += z;
+            const int t = hu; hu = hv; hv = t;
+            u_is_a = sa;
         }
+        const uint32_t nx = A::neg(en.x, p);
+        const int hmax = max(hu, hv);
+#pragma unroll
+        for (int e = 0; e < PE; ++e) ru[e] = A::comb(en.y, ru[e], nx, rv[e], f);
+        if (z == 1) shift_right1(ru, PE);
+        else shift_right(ru, z);
+        hu = hmax;
+        if (hu >= 0) hu += z;
     }
     uint32_t* Pa = Pg + (0 * 2 + col) * PL;  // row A, column col
     uint32_t* Pb = Pg + (1 * 2 + col) * PL;  // row B, column col
 #pragma unroll
     for (int e = 0; e < PE; ++e) {
-        const uint32_t a = A::canon(u_is_a ? ru[e] : rv[e], p);
-        const uint32_t b = A::canon(u_is_a ? rv[e] : ru[e], p);
-        __stcg(Pa + e * 32 + lane, a);
-        __stcg(Pb + e * 32 + lane, b);
+        __stcg(Pa + e * 32 + lane, A::canon(u_is_a ? ru[e] : rv[e], p));
+        __stcg(Pb + e * 32 + lane, A::canon(u_is_a ? rv[e] : ru[e], p));
     }
     if (lane == 0) {
         hi_out[0 * 2 + col] = min(u_is_a ? hu : hv, PL - 1);
@@ -431,7 +469,7 @@ __global__ void __launch_bounds__(GCD_T, 1) gcd_kernel(GcdArgs g) {
     extern __shared__ __align__(16) uint32_t smem[];
     __shared__ BatchMeta ctl;
     __shared__ int hi_s[4];
-    __shared__ volatile int logged, done;
+    __shared__ volatile int done;
     cg::grid_group grid = cg::this_grid();
     const FieldParams F = g.F;
     constexpr int ORG = PL + 8 + 3;
@@ -455,18 +493,19 @@ __global__ void __launch_bounds__(GCD_T, 1) gcd_kernel(GcdArgs g) {
     for (;;) {
         long long t_chain0 = clock64();
         if (blockIdx.x == 0) {
-            if (threadIdx.x == 0) {
-                logged = 0;
-                done = 0;
-            }
+            for (int i = threadIdx.x; i < LOGCAP; i += GCD_T)
+                reinterpret_cast<uint4*>(log)[i] = make_uint4(0u, 0u, 0u, 0u);
+            if (threadIdx.x == 0) done = 0;
             __syncthreads();
             if (warp == 0) {
-                run_chain<MODE>(ctl, log, &logged, &done, g.M, Fld{F.p, F.pinv},
+                run_chain<MODE>(ctl, log, &done, g.M, Fld{F.p, F.pinv},
                                 (cur ? g.X[1] : g.X[0]), (cur ? g.Y[1] : g.Y[0]));
                 if (g.stats && threadIdx.x == 0) g.stats[4] += clock64() - t_chain0;
             }
             else if (warp <= 2) {
-                run_replay<MODE>(warp - 1, log, &logged, &done, Fld{F.p, F.pinv}, g.Pg, hi_s);
+                if (g.dbg & 2)  // experiment: replay only after the chain finished
+                    while (ld_acquire_cta(&done) == 0) __nanosleep(256);
+                run_replay<MODE>(warp - 1, log, &done, Fld{F.p, F.pinv}, g.Pg, hi_s);
                 if (g.stats && threadIdx.x == 32) g.stats[5] += clock64() - t_chain0;
             }
             __syncthreads();
@@ -582,6 +621,7 @@ void launch_gcd(const FieldParams& F, const uint32_t* a, int64_t na, const uint3
     const int64_t want = std::max<int64_t>(1, ceil_div(na + nb, 256));
     const int blocks = int(std::min<int64_t>(want, int64_t(sm_count()) * per_sm));
     const bool want_stats = getenv("MMM_GCD_STATS") != nullptr;
+    if (const char* d = getenv("MMM_GCD_DEBUG")) g.dbg = atoi(d);
     if (want_stats) {
         g.stats = sc.get<long long>(6);
         MMM_CUDA(cudaMemsetAsync(g.stats, 0, 6 * sizeof(long long), st));
