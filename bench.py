@@ -143,6 +143,24 @@ def digest(x) -> str:
     return hashlib.sha256(a.tobytes()).hexdigest()[:16] if a.size else ""
 
 
+def ncu_traffic(kernel_prefix):
+    """DRAM read+write bytes per launch of `kernel_prefix` from the latest
+    committed `ncu --set full` capture summary (profiles/r*_kernels.csv)."""
+    import csv
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_kernels.csv")))
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    for f in reversed(files):
+        got = {}
+        for row in csv.DictReader(open(f)):
+            if kernel_prefix in row["kernel"].split("(")[0] and \
+                    row["metric"] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                got[row["metric"]] = float(row["value"]) * scale.get(row["unit"], 1)
+        if len(got) == 2:
+            return got["dram__bytes_read.sum"] + got["dram__bytes_write.sum"], os.path.basename(f)
+    return None, None
+
+
 def peaks():
     hbm, src = 6650.0, "fallback (B200_PROFILING.md)"
     if os.path.exists(PEAKS):
@@ -459,7 +477,200 @@ class NttWork(Workload):
                 "restated, C port), 2^32 MACs")
 
 
-WORKLOADS = {"gcd": GcdWork, "mul": MulWork, "div": DivWork, "ntt": NttWork}
+class _Sharded(Workload):
+    """Batched configs: instances split evenly across ranks (no data-path
+    collective), outputs all-gathered to every rank over NCCL inside the timed
+    step ("results gathered over NVLink", BASELINE.json configs[3]/[4])."""
+
+    sharded = True
+
+    def bind(self, dist):
+        from paper_1402_0264_b200.shard import shard_range
+        self.dist, self.world = dist, dist.world
+        self.lo, self.hi = shard_range(self.count, dist.world, dist.rank)
+
+    def _gather(self, t):
+        from paper_1402_0264_b200.shard import gather_rows
+        return gather_rows(t, self.dist.pg, self.world)
+
+
+class NttBatchWork(_Sharded):
+    """configs[3] batch: 256 independent 2^15 x 2^15 products (NTT length 2^16)."""
+
+    name = "ntt_batch"
+
+    def __init__(self, s):
+        import paper_1402_0264_b200 as mmm
+        self.mmm, self.count = mmm, 256
+        rng = ProductRng(42)
+        suites.cfg4_big(rng)  # same stream: the batch follows the big pair
+        c = suites.cfg4_batch(rng)
+        self.A, self.B = c["A"].astype(np.uint32), c["B"].astype(np.uint32)
+        gold = golden()["cfg4_batch"]
+        self.want = gold["f_all"]
+        self.na = self.A.shape[1]
+        self.nf = 2 * self.na - 1
+        self.config = {"workload": "cfg4_batch_256x(2^15x2^15)_ntt_N2^16_p469762049", "p": P,
+                       "seed": 42, "parallelism": "instances sharded across ranks, NCCL "
+                       "all-gather of results", "units": "schoolbook-equivalent MACs",
+                       "l2": "flushed between timed steps"}
+
+    def units(self):
+        return float(self.count) * self.na * self.na
+
+    def device_setup(self):
+        import torch
+        self.dA = _dev(self.A[self.lo:self.hi])
+        self.dB = _dev(self.B[self.lo:self.hi])
+        self.dF = torch.zeros((self.hi - self.lo, self.nf), dtype=torch.int32, device="cuda")
+
+    def device_step(self, stream):
+        self.mmm.ntt_mul_batched_dev(P, self.dA.data_ptr(), self.na, self.na, self.dB.data_ptr(),
+                                     self.na, self.na, self.hi - self.lo, self.dF.data_ptr(),
+                                     self.nf, stream=stream)
+        self.full = self._gather(self.dF)
+
+    def _digest_rows(self, F):
+        import hashlib
+        fs = [digest(np.trim_zeros(F[i].astype(np.int64), "b")) for i in range(F.shape[0])]
+        return hashlib.sha256("".join(fs).encode()).hexdigest()[:16]
+
+    def device_check(self):
+        assert self._digest_rows(self.full.cpu().numpy().view(np.uint32)) == self.want, \
+            "ntt batch result"
+
+    def host_setup(self):
+        (self.hA, self._ta), (self.hB, self._tb) = _pinned(self.A[self.lo:self.hi]), _pinned(
+            self.B[self.lo:self.hi])
+        self.bytes_in = 4 * (self.hA.size + self.hB.size)
+        self.bytes_out = 4 * (self.hi - self.lo) * self.nf
+
+    def host_step(self):
+        return self.mmm.ntt_mul_batched(self.hA, self.hB, P)
+
+    def host_check(self, F):
+        if self.world == 1:
+            assert self._digest_rows(F) == self.want
+
+    def roofline(self, t_step, hbm, imad):
+        n_local = self.hi - self.lo
+        alg = 4.0 * n_local * (2 * self.na + self.nf)
+        achieved = alg / t_step / 1e9
+        return {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm, "traffic": None, "kernel": "ntt_rows",
+                "alg_bytes_per_launch": alg}
+
+    def cpu_ref(self, orc):
+        i = 0
+        a, b = self.A[i].astype(np.int64), self.B[i].astype(np.int64)
+        want = golden()["cfg4_batch"]["f"][i]
+        return (lambda: orc.mul(a, b, P), float(self.na * self.na),
+                lambda out: digest(out) == want, "one 2^15 x 2^15 instance (oracle_mul)")
+
+
+class BatchWork(_Sharded):
+    """configs[4]: 4096 products 4096 x 4096 + 4096 divisions 8192 / 4096 terms."""
+
+    name = "batch"
+
+    def __init__(self, s):
+        import paper_1402_0264_b200 as mmm
+        self.mmm, self.count, self.s = mmm, 4096, s or 0
+        c = suites.cfg5(ProductRng(42))
+        self.A, self.B = c["A"].astype(np.uint32), c["B"].astype(np.uint32)
+        self.C, self.D = c["C"].astype(np.uint32), c["D"].astype(np.uint32)
+        gold = golden()["cfg5"]
+        self.want = (gold["f_all"], gold["qr_all"])
+        self.n = self.A.shape[1]
+        self.config = {"workload": "cfg5_4096x(4096x4096 mul)+4096x(8192/4096 div)_p469762049",
+                       "p": P, "seed": 42, "s_mul": self.s or 8, "s_div": self.s or 64,
+                       "parallelism": "instances sharded across ranks, NCCL all-gather of "
+                       "results", "l2": "inputs 335 MB > L2"}
+
+    def units(self):
+        n = self.n
+        return float(self.count) * (n * n + (n + 1) * n)
+
+    def device_setup(self):
+        import torch
+        sl = slice(self.lo, self.hi)
+        k, n = self.hi - self.lo, self.n
+        self.dA, self.dB, self.dC, self.dD = (_dev(x[sl]) for x in (self.A, self.B, self.C,
+                                                                      self.D))
+        self.dF = torch.zeros((k, 2 * n - 1), dtype=torch.int32, device="cuda")
+        self.dQ = torch.zeros((k, n + 1), dtype=torch.int32, device="cuda")
+        self.dR = torch.zeros((k, n - 1), dtype=torch.int32, device="cuda")
+
+    def device_step(self, stream):
+        k, n = self.hi - self.lo, self.n
+        self.mmm.mul_batched_dev(P, self.dA.data_ptr(), n, n, self.dB.data_ptr(), n, n, k,
+                                 self.dF.data_ptr(), 2 * n - 1, s=self.s or 8, stream=stream)
+        self.mmm.divmod_batched_dev(P, self.dC.data_ptr(), 2 * n, 2 * n, self.dD.data_ptr(), n,
+                                    n, k, self.dQ.data_ptr(), n + 1, self.dR.data_ptr(), n - 1,
+                                    s=self.s or 64, stream=stream)
+        self.fullF = self._gather(self.dF)
+        self.fullQ = self._gather(self.dQ)
+        self.fullR = self._gather(self.dR)
+
+    def _digests(self, F, Q, R):
+        import hashlib
+        def rows(M):
+            return [digest(np.trim_zeros(M[i].astype(np.int64), "b")) for i in range(M.shape[0])]
+        f = hashlib.sha256("".join(rows(F)).encode()).hexdigest()[:16]
+        qr = hashlib.sha256("".join(rows(Q) + rows(R)).encode()).hexdigest()[:16]
+        return f, qr
+
+    def device_check(self):
+        got = self._digests(*(t.cpu().numpy().view(np.uint32) for t in (self.fullF, self.fullQ,
+                                                                          self.fullR)))
+        assert got == self.want, "batch results"
+
+    def host_setup(self):
+        sl = slice(self.lo, self.hi)
+        pins = [_pinned(x[sl]) for x in (self.A, self.B, self.C, self.D)]
+        (self.hA, self.hB, self.hC, self.hD) = (q[0] for q in pins)
+        self._pins = pins
+        k, n = self.hi - self.lo, self.n
+        self.bytes_in = 4 * k * (n + n + 2 * n + n)
+        self.bytes_out = 4 * k * ((2 * n - 1) + (n + 1) + (n - 1))
+
+    def host_step(self):
+        F = self.mmm.mul_batched(self.hA, self.hB, P, s=self.s or 8)
+        Q, R = self.mmm.divmod_batched(self.hC, self.hD, P, s=self.s or 64)
+        return F, Q, R
+
+    def host_check(self, out):
+        if self.world == 1:
+            assert self._digests(*out) == self.want
+
+    def roofline(self, t_step, hbm, imad):
+        k, n = self.hi - self.lo, self.n
+        macs = float(k) * (n * n + (n + 1) * n)
+        achieved = macs / t_step / 1e12
+        peak = (imad or 7.35e12) / 1e12
+        return {"bound": "imad", "achieved": achieved, "peak": peak, "unit": "TMAC/s",
+                "frac": achieved / peak, "traffic": None, "kernel": "mul_kernel+div_cta_kernel",
+                "alg_macs_per_launch": macs,
+                "note": "per-rank MACs over the step time incl. the NCCL gather"}
+
+    def cpu_ref(self, orc):
+        gold = golden()["cfg5"]
+        a, b = self.A[0].astype(np.int64), self.B[0].astype(np.int64)
+        c, d = self.C[0].astype(np.int64), self.D[0].astype(np.int64)
+        n = self.n
+
+        def run():
+            return orc.mul(a, b, P), orc.divmod(c, d, P)
+
+        def ok(out):
+            f, (q, r) = out
+            return (digest(f), digest(q), digest(r)) == (gold["f"][0], gold["q"][0], gold["r"][0])
+        return (run, float(n * n + (n + 1) * n), ok,
+                "instance 0 of each batch (oracle_mul + oracle_divmod)")
+
+
+WORKLOADS = {"gcd": GcdWork, "mul": MulWork, "div": DivWork, "ntt": NttWork,
+             "ntt_batch": NttBatchWork, "batch": BatchWork}
 
 
 # ------------------------------------------------------------------ arms --
@@ -469,6 +680,9 @@ def run_ours(args, dist):
     import paper_1402_0264_b200 as mmm
     mmm.load()
     work = WORKLOADS[args.workload](args.s)
+    sharded = getattr(work, "sharded", False)
+    if sharded:
+        work.bind(dist)
     work.device_setup()
     stream = torch.cuda.current_stream()
     sp = stream.cuda_stream
@@ -497,7 +711,8 @@ def run_ours(args, dist):
     work.device_check()
     t_dev = dist.max(t_dev)
     t_step = t_dev / args.steps
-    value = dist.world * work.units() / t_step
+    # replicas: every rank ran the whole instance; sharded: the ranks split it
+    value = (1 if sharded else dist.world) * work.units() / t_step
 
     # e2e: host-buffer C-ABI call, H2D + kernel + D2H inside the region
     work.host_setup()
@@ -510,16 +725,20 @@ def run_ours(args, dist):
         out = work.host_step()
     t_e2e = dist.max(time.perf_counter() - t0) / args.steps
     work.host_check(out)
-    e2e = {"value": dist.world * work.units() / t_e2e, "unit": UNIT,
+    e2e = {"value": (1 if sharded else dist.world) * work.units() / t_e2e, "unit": UNIT,
            "h2d_bytes_per_step": work.bytes_in, "d2h_bytes_per_step": work.bytes_out,
            "ms_per_step": t_e2e * 1e3}
 
     hbm, src, imad = peaks()
     roof = work.roofline(t_step, hbm, imad)
     roof["peak_source"] = src
+    traffic, tsrc = ncu_traffic(roof["kernel"].split("+")[0])
+    if traffic is not None:
+        roof["traffic"], roof["traffic_source"] = traffic, tsrc
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": dist.world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+            "higher_is_better": True, "scaling": "strong" if sharded else "weak",
+            "vs_baseline": None, "dtype": "u32",
             "data": "synthetic (seeded mt19937_64 inputs, reference random_poly draws)",
             "config": work.config, "impl": "ours", "e2e": e2e, "roofline": roof,
             "gpu_launches": launches, "clocks": clk.summary()}

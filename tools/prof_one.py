@@ -26,6 +26,8 @@ def main():
     import paper_1402_0264_b200 as mmm
     mmm.load()
     w = bench.WORKLOADS[args.workload](args.s)
+    if getattr(w, "sharded", False):
+        w.bind(bench.Dist("ours"))
     w.device_setup()
     sp = torch.cuda.current_stream().cuda_stream
     for _ in range(args.reps):
