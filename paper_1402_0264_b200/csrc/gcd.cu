@@ -43,11 +43,18 @@ namespace cg = cooperative_groups;
 namespace mmm_cu {
 
 constexpr int GCD_T = 256;         // threads per CTA
-constexpr int GE = 4;              // window words per lane
-constexpr int W1 = 32 * GE;        // window words per operand (128)
-constexpr int PE = 4;              // matrix words per lane per polynomial
-constexpr int PL = 32 * PE;        // matrix capacity (support < 128)
+#ifndef GCD_GE
+#define GCD_GE 2
+#endif
+#ifndef GCD_PE
+#define GCD_PE 2
+#endif
+constexpr int GE = GCD_GE;         // window words per lane
+constexpr int W1 = 32 * GE;        // window words per operand
+constexpr int PE = GCD_PE;         // matrix words per lane per polynomial
+constexpr int PL = 32 * PE;        // matrix capacity (support < PL)
 constexpr int LOGCAP = 2048;       // steps per matrix batch, hard cap
+constexpr int LOGCHUNK = 8;        // log entries buffered in registers per flush
 constexpr int BIG = 1 << 30;       // "validity unbounded": window covers the operand
 constexpr int GCD_R = 1;           // outputs per thread in the apply
 
@@ -57,7 +64,7 @@ struct StepLog {
     int u_is_a;  // 1: A was reduced by B, 0: B by A
 };
 
-// Published per batch by CTA 0 (global), read by every CTA after the barrier.
+// Published per batch by CTA 0 into a ring slot, read by the bulk CTAs.
 struct BatchMeta {
     long long da0, db0;  // exact degrees at batch start (-1: zero operand)
     long long da1, db1;  // degree bounds after the batch (-1: vanished)
@@ -66,20 +73,23 @@ struct BatchMeta {
     int hi[4];           // highest nonzero index of Pa1, Pa2, Pb1, Pb2
 };
 
+constexpr int RING = 4;  // published matrices in flight
+
 struct GcdArgs {
     const uint32_t* a;
     const uint32_t* b;
     long long na, nb;
-    uint32_t* X[2];
-    uint32_t* Y[2];
-    uint32_t* Pg;     // 4 * PL words: Pa1, Pa2, Pb1, Pb2 (canonical)
-    BatchMeta* meta;  // global copy
+    uint32_t* XA[3];      // state of A, triple-buffered: batch j reads j%3, writes (j+1)%3
+    uint32_t* XB[3];
+    uint32_t* Pg;         // RING x (Pa1, Pa2, Pb1, Pb2), PL words each, canonical
+    BatchMeta* meta;      // RING slots
+    unsigned* flags;      // [0] batches published by CTA 0, [1] bulk CTA-batches applied
     uint32_t* g;
     int64_t* ng;
-    int M;            // steps per batch (the program parameter s)
+    int M;                // steps per batch (the program parameter s)
     FieldParams F;
-    long long* stats; // optional (MMM_GCD_STATS): batches, steps, chain/apply cycles
-    int dbg;          // MMM_GCD_DEBUG bits (timing experiments; 2 = serialise chain and replay)
+    long long* stats;     // optional (MMM_GCD_STATS)
+    int dbg;              // MMM_GCD_DEBUG bits (timing experiments)
 };
 
 namespace {
@@ -225,7 +235,7 @@ __device__ void load_top(uint32_t (&w)[GE], const uint32_t* Z, long long& deg, u
     }
 }
 
-// Log entries: the chain buffers entry s in lane s % 32 and stores 32 at a
+// Log entries: the chain buffers entry s in lane s % LOGCHUNK and stores them at a
 // time, one 16-byte store per lane; `seq` = step index + 1 publishes an entry
 // (the replay warps poll the entry itself, no per-step fence or store).
 __device__ __forceinline__ void log_flush(StepLog* log, int base, int count, uint32_t x,
@@ -248,116 +258,131 @@ __device__ __forceinline__ uint4 log_get(const StepLog* log, int i) {
     return v;
 }
 
-// Warp 0 of CTA 0: the elimination chain of one batch.  Windows are kept
-// oriented: u = current dividend, v = divisor (roles swap with MOVs only, so
-// every shuffle sits in straight-line, warp-uniform code).  Fast path: the
-// new lead is u[1] (z = 1), fetched by one shuffle while the window shifts
-// by one; all capacity checks collapse into one budget counter F of steps
-// that provably cannot exhaust the windows or the matrix.
+// One elimination: reduce u (the dividend) by v.  Fast path: the new lead is
+// u[1] (z = 1), fetched by one shuffle while the window shifts by one.
+// Returns z (the renormalisation shift); slow path handles z != 1, a vanished
+// operand (du = -1) and an undetermined lead (stop).
+template <int MODE>
+__device__ __forceinline__ int chain_step(uint32_t (&u)[GE], const uint32_t (&v)[GE],
+                                          uint32_t& hu, uint32_t hv, long long& du, int vj,
+                                          int sup, int aged, bool& slow, bool& stop, Fld f) {
+    using A = Arith<MODE>;
+    const uint32_t p = f.p, x = hu, nx = A::neg(x, p);
+#pragma unroll
+    for (int e = 0; e < GE; ++e) u[e] = A::comb(hv, u[e], nx, v[e], f);
+    const uint32_t h1 = from_lane(u[0], 1);
+    if (A::nz(h1, p)) {
+        shift_left1(u, GE);
+        hu = h1;
+        du -= 1;
+        return 1;
+    }
+    slow = true;
+    // bounds aged by the `aged` fast steps taken since they were refreshed
+    const int vmin = vj < BIG ? vj - aged : BIG;
+    const int room = PL - 1 - (sup + aged);
+    int z = first_nz<MODE>(u, 1, p);
+    if (z < 0 || z >= vmin) {
+        if (vmin >= BIG) {  // the window held the whole operand: it vanished
+            du = -1;
+            return 0;
+        }
+        z = vmin;  // lead not determined inside the valid words
+        stop = true;
+    }
+    if (z > room) {  // matrix capacity: shift only as far as it holds
+        z = room;
+        stop = true;
+    }
+    shift_left(u, z);
+    hu = bcast(u[0]);
+    du -= z;
+    return z;
+}
+
+// Warp 0 of CTA 0: the elimination chain of one batch on two fixed windows
+// (wa for A, wb for B; a warp-uniform branch picks the dividend, no swaps).
+// Capacity is checked through a step budget F: each fast step lowers the
+// windows' joint validity and raises the matrix support by at most one, so
+// the bounds are refreshed (pessimistically) only when F runs out or after a
+// slow step.  Role rule, termination: oracle.cpp:58-66, 74-75; gcd.cpp:191-199.
 template <int MODE>
 __device__ void run_chain(BatchMeta& c, StepLog* log, volatile int* done, int M, Fld f,
-                          const uint32_t* X, const uint32_t* Y) {
+                          const uint32_t* winA, const uint32_t* winB) {
     using A = Arith<MODE>;
     const uint32_t p = f.p;
-    long long da = c.da1, db = c.db1;
-    uint32_t u[GE], v[GE];
-    load_top<MODE>(u, X, da, p);
-    load_top<MODE>(v, Y, db, p);
-    const long long da0 = da, db0 = db;
-    bool u_is_a = true;
-    int du = int(da), dv = int(db);
-    int vu = da < W1 ? BIG : W1, vv = db < W1 ? BIG : W1;
-    int su = 0, sv = 0, supu = 0, supv = 0;
-    uint32_t hu = bcast(u[0]), hv = bcast(v[0]);
-    auto swap_roles = [&]() {
-#pragma unroll
-        for (int e = 0; e < GE; ++e) {
-            const uint32_t t = u[e];
-            u[e] = v[e];
-            v[e] = t;
-        }
-        u_is_a = !u_is_a;
-        int t;
-        t = du; du = dv; dv = t;
-        t = vu; vu = vv; vv = t;
-        t = su; su = sv; sv = t;
-        t = supu; supu = supv; supv = t;
-        const uint32_t h = hu; hu = hv; hv = h;
-    };
-    if (!c.dividend_a) swap_roles();
-    const int cap = min(M, LOGCAP);
     const int lane = threadIdx.x & 31;
-    int steps = 0, term = 0, F = 0;
+    long long da = c.da1, db = c.db1;  // exact: the windows start at the leads
+    uint32_t wa[GE], wb[GE];
+#pragma unroll
+    for (int e = 0; e < GE; ++e) {
+        wa[e] = winA[e * 32 + lane];
+        wb[e] = winB[e * 32 + lane];
+    }
+    const long long da0 = da, db0 = db;
+    uint32_t ha = bcast(wa[0]), hb = bcast(wb[0]);
+    // joint validity: valid words of either window from the top (pessimistic);
+    // BIG only while both windows hold their whole operands
+    int vj = (da < W1 && db < W1) ? BIG : W1;
+    int sup = 0;  // max matrix support (pessimistic)
+    int dividend_a = c.dividend_a;
+    const int cap = min(M, LOGCAP);
+    int steps = 0, term = 0, F = 0, F0 = 0;
     uint32_t lx = 0, ly = 0, lz = 0;  // this lane's buffered log entry
     for (;;) {
-        if (du >= 0 && dv >= 0 && du < dv) swap_roles();  // oracle.cpp:58-66, 74-75
-        if (F <= 0) {
-            if (du < 0) { term = u_is_a ? 1 : 2; break; }  // dividend vanished: gcd = divisor
-            if (dv < 0) { term = u_is_a ? 2 : 1; break; }  // zero divisor (zero input)
-            F = min(cap - steps, min(min(vu, vv) - 2, PL - 2 - max(supu, supv)));
-            if (F <= 0) break;  // batch length, window or matrix exhausted
-        }
-        if (dv == 0) { term = 3; break; }  // constant divisor: unit gcd
-        const uint32_t x = hu, y = hv, nx = A::neg(x, p);
-        vu = min(vu, vv);
-#pragma unroll
-        for (int e = 0; e < GE; ++e) u[e] = A::comb(y, u[e], nx, v[e], f);
-        const uint32_t h1 = from_lane(u[0], 1);
-        int z = 1;
-        bool stop = false;
-        if (A::nz(h1, p)) {  // fast path: the next word is the new lead
-            shift_left1(u, GE);
-            hu = h1;
-            --F;
+        // oracle role rule: reduce the dividend while deg(dividend) >= deg(divisor)
+        if (dividend_a) {
+            if (da >= 0 && db >= 0 && da < db) dividend_a = 0;
         } else {
-            z = first_nz<MODE>(u, 1, p);
-            if (z < 0 || z >= vu) {
-                if (vu >= BIG) {  // window held the whole operand: it vanished
-                    du = -1;
-                    z = 0;
-                } else {          // lead not determined inside the valid words
-                    z = vu;
-                    stop = true;
-                }
-            }
-            const int room = PL - 1 - max(supu, supv);
-            if (z > room) {       // matrix capacity: shift only as far as it holds
-                z = room;
-                stop = true;
-            }
-            if (du >= 0) {
-                shift_left(u, z);
-                hu = bcast(u[0]);
-            }
-            F = 0;                // re-derive the budget
+            if (da >= 0 && db >= 0 && db < da) dividend_a = 1;
         }
-        if (du >= 0) {
-            du -= z;
-            if (vu < BIG) vu -= z;
+        if (F <= 0) {
+            // refresh the pessimistic bounds with the F0 fast steps just taken
+            if (vj < BIG) vj -= F0;
+            sup += F0;
+            F0 = 0;
+            if (da < 0) { term = 1; break; }  // A vanished: gcd = B
+            if (db < 0) { term = 2; break; }  // B vanished: gcd = A
+            F = min(cap - steps, min(vj - 2, PL - 2 - sup));
+            if (F <= 0) break;  // batch length, window or matrix exhausted
+            F0 = F;
         }
-        su += z;
-        supu = max(supu, supv) + z;
-        // buffer the log entry in lane (steps % 32); flush 32 at a time
-        if (lane == (steps & 31)) {
+        if ((dividend_a ? db : da) == 0) { term = 3; break; }  // constant divisor: unit gcd
+        const int aged = F0 - F;  // fast steps since the bounds were refreshed
+        bool slow = false, stop = false;
+        int z;
+        const uint32_t x = dividend_a ? ha : hb, y = dividend_a ? hb : ha;
+        if (dividend_a) z = chain_step<MODE>(wa, wb, ha, hb, da, vj, sup, aged, slow, stop, f);
+        else z = chain_step<MODE>(wb, wa, hb, ha, db, vj, sup, aged, slow, stop, f);
+        --F;
+        if (slow) {  // exact bookkeeping for this step, then re-derive the budget
+            const int used = F0 - F - 1;  // fast steps before this one
+            if (vj < BIG) vj -= used + z;
+            sup += used + z;
+            F = 0;
+            F0 = 0;
+        }
+        if (lane == (steps & (LOGCHUNK - 1))) {
             lx = x;
             ly = y;
-            lz = unsigned(z) | (u_is_a ? 0x10000u : 0u);
+            lz = unsigned(z) | (dividend_a ? 0x10000u : 0u);
         }
         ++steps;
-        if ((steps & 31) == 0) log_flush(log, steps - 32, 32, lx, ly, lz);
+        if ((steps & (LOGCHUNK - 1)) == 0) log_flush(log, steps - LOGCHUNK, LOGCHUNK, lx, ly, lz);
         if (stop) break;
     }
-    if (steps & 31) log_flush(log, steps & ~31, steps & 31, lx, ly, lz);
-    if ((threadIdx.x & 31) == 0) {
+    if (steps & (LOGCHUNK - 1))
+        log_flush(log, steps & ~(LOGCHUNK - 1), steps & (LOGCHUNK - 1), lx, ly, lz);
+    if (lane == 0) {
         c.da0 = da0;
         c.db0 = db0;
-        c.da1 = u_is_a ? du : dv;
-        c.db1 = u_is_a ? dv : du;
+        c.da1 = da;
+        c.db1 = db;
         c.steps = steps;
         c.term = term;
-        c.dividend_a = u_is_a ? 1 : 0;
-        c.sa = u_is_a ? su : sv;
-        c.sb = u_is_a ? sv : su;
+        c.dividend_a = dividend_a;
+        c.sa = int(da0 - (da < 0 ? da0 : da));  // top moves (unused for a vanished row)
+        c.sb = int(db0 - (db < 0 ? db0 : db));
         st_release_cta(done, steps + 1);  // done = final count + 1
     }
 }
@@ -366,7 +391,7 @@ __device__ void run_chain(BatchMeta& c, StepLog* log, volatile int* done, int M,
 // (both rows), oriented like the chain; then publish it (canonical) to Pg.
 template <int MODE>
 __device__ void run_replay(int col, const StepLog* log, volatile int* done, Fld f, uint32_t* Pg,
-                           int* hi_out) {
+                           uint32_t* Ps, int* hi_out) {
     using A = Arith<MODE>;
     const uint32_t p = f.p;
     const int lane = threadIdx.x & 31;
@@ -413,8 +438,12 @@ __device__ void run_replay(int col, const StepLog* log, volatile int* done, Fld 
     uint32_t* Pb = Pg + (1 * 2 + col) * PL;  // row B, column col
 #pragma unroll
     for (int e = 0; e < PE; ++e) {
-        __stcg(Pa + e * 32 + lane, A::canon(u_is_a ? ru[e] : rv[e], p));
-        __stcg(Pb + e * 32 + lane, A::canon(u_is_a ? rv[e] : ru[e], p));
+        const uint32_t va = A::canon(u_is_a ? ru[e] : rv[e], p);
+        const uint32_t vb = A::canon(u_is_a ? rv[e] : ru[e], p);
+        __stcg(Pa + e * 32 + lane, va);
+        __stcg(Pb + e * 32 + lane, vb);
+        Ps[(0 * 2 + col) * PL + e * 32 + lane] = va;  // the window builder's copy
+        Ps[(1 * 2 + col) * PL + e * 32 + lane] = vb;
     }
     if (lane == 0) {
         hi_out[0 * 2 + col] = min(u_is_a ? hu : hv, PL - 1);
@@ -464,117 +493,248 @@ __device__ void apply_row(uint32_t* out, long long xs, long long xe, const uint3
 
 }  // namespace
 
+// ------------------------------------------------------- flags (gpu scope) --
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_gpu(unsigned* p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// Thread 0 waits until *p >= target; the CTA then proceeds together.
+__device__ __forceinline__ void cta_wait_ge(const unsigned* p, unsigned target) {
+    if (threadIdx.x == 0)
+        while (ld_acquire_gpu(p) < target) __nanosleep(64);
+    __syncthreads();
+}
+
+// Warp-level: top-aligned W1-word window of Z at degree `deg` into smem; lowers
+// `deg` past zero words until win[0] is the lead (deg = -1: zero operand).
+template <int MODE>
+__device__ void window_from_global(uint32_t* win, const uint32_t* Z, long long& deg, uint32_t p) {
+    uint32_t w[GE];
+    load_top<MODE>(w, Z, deg, p);
+#pragma unroll
+    for (int e = 0; e < GE; ++e) win[e * 32 + (threadIdx.x & 31)] = w[e];
+    __syncwarp();
+}
+
+// top[i] = Z[deg - i] for i < n (0 outside), all threads of the CTA.
+__device__ void load_top_region(uint32_t* top, const uint32_t* Z, long long deg, int n) {
+    for (int i = threadIdx.x; i < n; i += GCD_T) {
+        const long long x = deg - i;
+        top[i] = (x >= 0) ? __ldcg(Z + x) : 0u;
+    }
+}
+
+// win[t] = sum_e P1[e] topA[t+e] + sum_e P2[e] topB[t+e], t < W1: the next
+// batch's top-aligned window computed locally from the previous state.
+__device__ void build_window(uint32_t* win, const uint32_t* P1, int h1, const uint32_t* P2, int h2,
+                             const uint32_t* topA, const uint32_t* topB, int t,
+                             const FieldParams& F) {
+    uint64_t acc = 0;
+    uint32_t since = 0;
+    const uint32_t ft = F.fold_terms;
+#pragma unroll 1
+    for (int half = 0; half < 2; ++half) {
+        const uint32_t* P = half ? P2 : P1;
+        const uint32_t* Z = (half ? topB : topA) + t;
+        const int n = (half ? h2 : h1) + 1;
+        int e = 0;
+        if (ft >= 16) {
+            for (; e + 8 <= n; e += 8) {
+                if (since + 8 > ft) {
+                    acc = fold(acc, F);
+                    since = 0;
+                }
+                since += 8;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) acc = mad_wide(P[e + k], Z[e + k], acc);
+            }
+        }
+        for (; e < n; ++e) {
+            if (++since > ft) {
+                acc = fold(acc, F);
+                since = 1;
+            }
+            acc = mad_wide(P[e], Z[e], acc);
+        }
+    }
+    win[t] = reduce(acc, F);
+}
+
+// CTA 0: the sequential part.  Per batch: chain (warp 0) || replay (warps 1-2)
+// || prefetch of the previous state's top region (warps 3-7); publish the
+// matrix; build the next windows from it.  Never waits for the bulk of the
+// batch it just finished (only for the one before, which had a whole batch).
+template <int MODE>
+__device__ int head_cta(const GcdArgs& g, BatchMeta& ctl, StepLog* log, uint32_t* smem_rest,
+                        volatile int* done, int* hi_s, int nbulk) {
+    const FieldParams F = g.F;
+    const int warp = threadIdx.x >> 5;
+    uint32_t* winA = smem_rest;
+    uint32_t* winB = winA + W1;
+    uint32_t* topA = winB + W1;         // W1 + PL words
+    uint32_t* topB = topA + W1 + PL;
+    uint32_t* Ps = topB + W1 + PL;      // 4 * PL
+    __shared__ int fallback;
+    if (warp == 0) {
+        long long da = g.na - 1, db = g.nb - 1;
+        window_from_global<MODE>(winA, g.XA[0], da, F.p);
+        window_from_global<MODE>(winB, g.XB[0], db, F.p);
+        if ((threadIdx.x & 31) == 0) {
+            ctl.da1 = da;
+            ctl.db1 = db;
+            ctl.dividend_a = 1;  // oracle_gcd: x = a is the first dividend (oracle.cpp:70)
+        }
+    }
+    __syncthreads();
+    for (int j = 0;; ++j) {
+        const long long t0 = clock64();
+        for (int i = threadIdx.x; i < LOGCAP; i += GCD_T)
+            reinterpret_cast<uint4*>(log)[i] = make_uint4(0u, 0u, 0u, 0u);
+        if (threadIdx.x == 0) *done = 0;
+        const long long da0 = ctl.da1, db0 = ctl.db1;
+        __syncthreads();
+        if (warp == 0) {
+            run_chain<MODE>(ctl, log, done, g.M, Fld{F.p, F.pinv}, winA, winB);
+            if (g.stats && threadIdx.x == 0) g.stats[4] += clock64() - t0;
+        } else if (warp <= 2) {
+            run_replay<MODE>(warp - 1, log, done, Fld{F.p, F.pinv}, g.Pg + (j % RING) * 4 * PL,
+                             Ps, hi_s);
+        } else {
+            // prefetch: S_j complete once the bulk applied batch j-1
+            if (threadIdx.x == 96)
+                while (ld_acquire_gpu(g.flags + 1) < unsigned(j) * nbulk) __nanosleep(64);
+            asm volatile("bar.sync 1, 160;" ::: "memory");  // warps 3-7
+            for (int i = threadIdx.x - 96; i < W1 + PL; i += GCD_T - 96) {
+                const long long xa = da0 - i, xb = db0 - i;
+                topA[i] = (xa >= 0) ? __ldcg(g.XA[j % 3] + xa) : 0u;
+                topB[i] = (xb >= 0) ? __ldcg(g.XB[j % 3] + xb) : 0u;
+            }
+        }
+        __syncthreads();
+        BatchMeta m = ctl;
+        m.da0 = da0;
+        m.db0 = db0;
+        for (int i = 0; i < 4; ++i) m.hi[i] = hi_s[i];
+        m.err = (m.steps == 0 && m.term == 0) ? 1 : 0;
+        if (threadIdx.x == 0) {
+            g.meta[j % RING] = m;
+            __threadfence();
+            st_release_gpu(g.flags + 0, unsigned(j + 1));
+            if (g.stats) {
+                g.stats[0] += 1;
+                g.stats[1] += m.steps;
+                g.stats[2] += clock64() - t0;
+            }
+        }
+        if (m.term || m.err) return j;
+        // next windows, top-aligned, from S_j and the batch matrix
+        const int t = threadIdx.x & (W1 - 1);
+        if (threadIdx.x < W1)
+            build_window(winA, Ps + 0 * PL, m.hi[0], Ps + 1 * PL, m.hi[1], topA, topB, t, F);
+        else if (threadIdx.x < 2 * W1)
+            build_window(winB, Ps + 2 * PL, m.hi[2], Ps + 3 * PL, m.hi[3], topA, topB, t, F);
+        if (threadIdx.x == 0) fallback = 0;
+        __syncthreads();
+        // the bound after the batch is not the lead (degree dropped past the
+        // valid words): take the exact state from the bulk instead
+        if (threadIdx.x == 0 &&
+            ((m.da1 >= 0 && winA[0] == 0u) || (m.db1 >= 0 && winB[0] == 0u)))
+            fallback = 1;
+        __syncthreads();
+        if (fallback) {
+            cta_wait_ge(g.flags + 1, unsigned(j + 1) * nbulk);
+            if (warp == 0) {
+                long long da = m.da1, db = m.db1;
+                window_from_global<MODE>(winA, g.XA[(j + 1) % 3], da, F.p);
+                window_from_global<MODE>(winB, g.XB[(j + 1) % 3], db, F.p);
+                if ((threadIdx.x & 31) == 0) {
+                    ctl.da1 = da;
+                    ctl.db1 = db;
+                }
+            }
+            __syncthreads();
+        }
+        if (g.stats && threadIdx.x == 0) g.stats[3] += clock64() - t0;
+    }
+}
+
+// CTAs 1..G-1: apply batch j's matrix to this CTA's slice of both operands,
+// S_{j+1} = P_j(S_j), as soon as it is published and S_j is complete.
+__device__ int bulk_cta(const GcdArgs& g, uint32_t* sw, uint32_t* sv, int nbulk, int me) {
+    const FieldParams F = g.F;
+    constexpr int ORG = PL + 8 + 3;
+    __shared__ BatchMeta ms;
+    for (int j = 0;; ++j) {
+        cta_wait_ge(g.flags + 0, unsigned(j + 1));
+        if (threadIdx.x == 0) {
+            const volatile BatchMeta* vm = g.meta + (j % RING);
+            ms.da0 = vm->da0; ms.db0 = vm->db0; ms.da1 = vm->da1; ms.db1 = vm->db1;
+            ms.steps = vm->steps; ms.term = vm->term; ms.err = vm->err;
+            ms.sa = vm->sa; ms.sb = vm->sb;
+            for (int i = 0; i < 4; ++i) ms.hi[i] = vm->hi[i];
+        }
+        cta_wait_ge(g.flags + 1, unsigned(j) * nbulk);  // S_j complete
+        const BatchMeta m = ms;
+        if (m.steps > 0 && !m.err) {
+            const uint32_t* P = g.Pg + (j % RING) * 4 * PL;
+            const long long na1 = m.da1 + 1 > 0 ? m.da1 + 1 : 0;
+            const long long nb1 = m.db1 + 1 > 0 ? m.db1 + 1 : 0;
+            const long long per = (na1 + nb1 + nbulk - 1) / nbulk;
+            const long long s0 = (long long)me * per;
+            const long long s1 = min(s0 + per, na1 + nb1);
+            const uint32_t *A0 = g.XA[j % 3], *B0 = g.XB[j % 3];
+            apply_row(g.XA[(j + 1) % 3], min(s0, na1), min(s1, na1), P + 0 * PL, m.hi[0], A0,
+                      m.da0, m.sa, P + 1 * PL, m.hi[1], B0, m.db0, m.sa + m.db0 - m.da0, sw, sv,
+                      ORG, F);
+            apply_row(g.XB[(j + 1) % 3], max(s0 - na1, 0LL), max(s1 - na1, 0LL), P + 2 * PL,
+                      m.hi[2], A0, m.da0, m.sb + m.da0 - m.db0, P + 3 * PL, m.hi[3], B0, m.db0,
+                      m.sb, sw, sv, ORG, F);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            atomicAdd(g.flags + 1, 1u);
+        }
+        if (m.term || m.err) return j;
+    }
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(GCD_T, 1) gcd_kernel(GcdArgs g) {
     extern __shared__ __align__(16) uint32_t smem[];
-    __shared__ BatchMeta ctl;
+    __shared__ BatchMeta ctl, fin;
     __shared__ int hi_s[4];
     __shared__ volatile int done;
     cg::grid_group grid = cg::this_grid();
     const FieldParams F = g.F;
-    constexpr int ORG = PL + 8 + 3;
-    StepLog* log = reinterpret_cast<StepLog*>(smem);                 // LOGCAP entries
-    uint32_t* sw = smem + 4 * LOGCAP;                                 // PL + 8 words
-    uint32_t* sv = sw + PL + 8;                                       // ORG + GCD_T*R + R
     const long long tid = (long long)blockIdx.x * GCD_T + threadIdx.x;
     const long long nth = (long long)gridDim.x * GCD_T;
-    const int warp = threadIdx.x >> 5;
+    const int nbulk = gridDim.x - 1;  // >= 1 (launcher)
+    StepLog* log = reinterpret_cast<StepLog*>(smem);
+    uint32_t* rest = smem + 4 * LOGCAP;
 
-    for (long long i = tid; i < g.na; i += nth) g.X[0][i] = g.a[i];
-    for (long long i = tid; i < g.nb; i += nth) g.Y[0][i] = g.b[i];
-    if (threadIdx.x == 0) {
-        ctl.da1 = g.na - 1;
-        ctl.db1 = g.nb - 1;
-        ctl.dividend_a = 1;  // oracle_gcd: x = a is the first dividend (oracle.cpp:70)
-    }
+    for (long long i = tid; i < g.na; i += nth) g.XA[0][i] = g.a[i];
+    for (long long i = tid; i < g.nb; i += nth) g.XB[0][i] = g.b[i];
     grid.sync();
 
-    int cur = 0;
-    for (;;) {
-        long long t_chain0 = clock64();
-        if (blockIdx.x == 0) {
-            for (int i = threadIdx.x; i < LOGCAP; i += GCD_T)
-                reinterpret_cast<uint4*>(log)[i] = make_uint4(0u, 0u, 0u, 0u);
-            if (threadIdx.x == 0) done = 0;
-            __syncthreads();
-            if (warp == 0) {
-                run_chain<MODE>(ctl, log, &done, g.M, Fld{F.p, F.pinv},
-                                (cur ? g.X[1] : g.X[0]), (cur ? g.Y[1] : g.Y[0]));
-                if (g.stats && threadIdx.x == 0) g.stats[4] += clock64() - t_chain0;
-            }
-            else if (warp <= 2) {
-                if (g.dbg & 2)  // experiment: replay only after the chain finished
-                    while (ld_acquire_cta(&done) == 0) __nanosleep(256);
-                run_replay<MODE>(warp - 1, log, &done, Fld{F.p, F.pinv}, g.Pg, hi_s);
-                if (g.stats && threadIdx.x == 32) g.stats[5] += clock64() - t_chain0;
-            }
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                BatchMeta m = ctl;
-                for (int i = 0; i < 4; ++i) m.hi[i] = hi_s[i];
-                m.err = 0;
-                *g.meta = m;
-                __threadfence();
-                if (g.stats) {
-                    g.stats[0] += 1;
-                    g.stats[1] += ctl.steps;
-                    g.stats[2] += clock64() - t_chain0;
-                }
-            }
-        }
-        grid.sync();
-        // one reader per CTA: every thread polling the same global line would
-        // serialise ~25k requests on one L2 slice per batch
-        __shared__ BatchMeta ms;
-        if (threadIdx.x == 0) {
-            const volatile BatchMeta* vm = g.meta;
-            ms.da0 = vm->da0; ms.db0 = vm->db0; ms.da1 = vm->da1; ms.db1 = vm->db1;
-            ms.steps = vm->steps; ms.term = vm->term; ms.dividend_a = vm->dividend_a;
-            ms.sa = vm->sa; ms.sb = vm->sb;
-            for (int i = 0; i < 4; ++i) ms.hi[i] = vm->hi[i];
-        }
-        __syncthreads();
-        const BatchMeta m = ms;
-        if (m.steps == 0 && m.term == 0) {  // invariant broken: no progress
-            if (tid == 0) *g.ng = -2;
-            return;                         // grid-uniform
-        }
-        if (m.term == 3) break;
-        if (m.steps > 0) {
-            const long long na1 = m.da1 + 1 > 0 ? m.da1 + 1 : 0;
-            const long long nb1 = m.db1 + 1 > 0 ? m.db1 + 1 : 0;
-            const long long per = (na1 + nb1 + gridDim.x - 1) / gridDim.x;
-            const long long s0 = (long long)blockIdx.x * per;
-            const long long s1 = min(s0 + per, na1 + nb1);
-            // A1[x] = Pa1 * A0 (shift sa) + Pa2 * B0 (shift sa + db0 - da0)
-            apply_row((cur ? g.X[0] : g.X[1]), min(s0, na1), min(s1, na1), g.Pg + 0 * PL, m.hi[0],
-                      (cur ? g.X[1] : g.X[0]), m.da0, m.sa, g.Pg + 1 * PL, m.hi[1], (cur ? g.Y[1] : g.Y[0]), m.db0,
-                      m.sa + m.db0 - m.da0, sw, sv, ORG, F);
-            // B1[x] = Pb1 * A0 (shift sb + da0 - db0) + Pb2 * B0 (shift sb)
-            apply_row((cur ? g.Y[0] : g.Y[1]), max(s0 - na1, 0LL), max(s1 - na1, 0LL), g.Pg + 2 * PL,
-                      m.hi[2], (cur ? g.X[1] : g.X[0]), m.da0, m.sb + m.da0 - m.db0, g.Pg + 3 * PL, m.hi[3],
-                      (cur ? g.Y[1] : g.Y[0]), m.db0, m.sb, sw, sv, ORG, F);
-            grid.sync();
-            if (g.stats && tid == 0) g.stats[3] += clock64() - t_chain0;
-            cur ^= 1;
-        }
-        if (m.term) {
-            ctl.term = m.term;
-            ctl.da1 = m.da1;
-            ctl.db1 = m.db1;
-            break;
-        }
-    }
-    __syncthreads();
-    __shared__ BatchMeta fs;
+    const int J = blockIdx.x == 0 ? head_cta<MODE>(g, ctl, log, rest, &done, hi_s, nbulk)
+                                  : bulk_cta(g, rest, rest + PL + 8, nbulk, blockIdx.x - 1);
+    // every CTA: wait until the final batch is applied everywhere, then finish
+    cta_wait_ge(g.flags + 1, unsigned(J + 1) * nbulk);
     if (threadIdx.x == 0) {
-        const volatile BatchMeta* vm = g.meta;
-        fs.term = vm->term;
-        fs.da1 = vm->da1;
-        fs.db1 = vm->db1;
+        const volatile BatchMeta* vm = g.meta + (J % RING);
+        fin.da1 = vm->da1; fin.db1 = vm->db1; fin.steps = vm->steps; fin.term = vm->term;
+        fin.err = vm->err;
     }
     __syncthreads();
-    const BatchMeta fin = fs;
+    if (fin.err) {
+        if (tid == 0) *g.ng = -2;  // no progress: internal invariant broken
+        return;
+    }
     if (fin.term == 3) {
         if (tid == 0) {
             g.g[0] = 1u;
@@ -582,7 +742,8 @@ __global__ void __launch_bounds__(GCD_T, 1) gcd_kernel(GcdArgs g) {
         }
         return;
     }
-    const uint32_t* Z = fin.term == 1 ? (cur ? g.Y[1] : g.Y[0]) : (cur ? g.X[1] : g.X[0]);
+    const int buf = fin.steps > 0 ? (J + 1) % 3 : J % 3;
+    const uint32_t* Z = fin.term == 1 ? g.XB[buf] : g.XA[buf];
     const long long dz = fin.term == 1 ? fin.db1 : fin.da1;
     const uint32_t inv = invmod(__ldcg(Z + dz), F);
     for (long long i = tid; i <= dz; i += nth) g.g[i] = mulmod(__ldcg(Z + i), inv, F);
@@ -603,14 +764,19 @@ void launch_gcd(const FieldParams& F, const uint32_t* a, int64_t na, const uint3
     g.M = int(std::min<int64_t>(s, LOGCAP));
     const int64_t cap = std::max<int64_t>(std::max(na, nb), 1);
     Scratch sc(st);
-    for (int i = 0; i < 2; ++i) {
-        g.X[i] = sc.get<uint32_t>(size_t(cap));
-        g.Y[i] = sc.get<uint32_t>(size_t(cap));
+    for (int i = 0; i < 3; ++i) {
+        g.XA[i] = sc.get<uint32_t>(size_t(cap));
+        g.XB[i] = sc.get<uint32_t>(size_t(cap));
     }
-    g.Pg = sc.get<uint32_t>(4 * PL);
-    g.meta = reinterpret_cast<BatchMeta*>(sc.get<uint64_t>((sizeof(BatchMeta) + 7) / 8));
+    g.Pg = sc.get<uint32_t>(size_t(RING) * 4 * PL);
+    g.meta = reinterpret_cast<BatchMeta*>(
+        sc.get<uint64_t>(RING * ((sizeof(BatchMeta) + 7) / 8)));
+    g.flags = sc.get<unsigned>(2);
+    MMM_CUDA(cudaMemsetAsync(g.flags, 0, 2 * sizeof(unsigned), st));
     constexpr int ORG = PL + 8 + 3;
-    const size_t bytes = size_t(4 * LOGCAP + PL + 8 + ORG + GCD_T * GCD_R + GCD_R + 8) * 4;
+    const size_t head_words = 2 * W1 + 2 * (W1 + PL) + 4 * PL;
+    const size_t bulk_words = PL + 8 + ORG + GCD_T * GCD_R + GCD_R + 8;
+    const size_t bytes = (4 * LOGCAP + std::max(head_words, bulk_words)) * 4;
     const int mode = !F.odd ? 2 : (F.p < (1u << 29) ? 0 : 1);
     const void* fn = mode == 0 ? (const void*)gcd_kernel<0>
                                : (mode == 1 ? (const void*)gcd_kernel<1> : (const void*)gcd_kernel<2>);
@@ -618,7 +784,7 @@ void launch_gcd(const FieldParams& F, const uint32_t* a, int64_t na, const uint3
     int per_sm = 0;
     MMM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, GCD_T, bytes));
     if (per_sm < 1) throw Error(ST_INVALID, "gcd: kernel does not fit an SM");
-    const int64_t want = std::max<int64_t>(1, ceil_div(na + nb, 256));
+    const int64_t want = std::max<int64_t>(2, 1 + ceil_div(na + nb, 256));
     const int blocks = int(std::min<int64_t>(want, int64_t(sm_count()) * per_sm));
     const bool want_stats = getenv("MMM_GCD_STATS") != nullptr;
     if (const char* d = getenv("MMM_GCD_DEBUG")) g.dbg = atoi(d);
@@ -634,9 +800,9 @@ void launch_gcd(const FieldParams& F, const uint32_t* a, int64_t na, const uint3
         MMM_CUDA(cudaMemcpyAsync(h, g.stats, sizeof(h), cudaMemcpyDeviceToHost, st));
         MMM_CUDA(cudaStreamSynchronize(st));
         fprintf(stderr,
-                "gcd stats: blocks=%d batches=%lld steps=%lld cta0_cycles=%lld total_cycles=%lld "
-                "chain_warp_cycles=%lld replay_warp_cycles=%lld\n",
-                blocks, h[0], h[1], h[2], h[3], h[4], h[5]);
+                "gcd stats: blocks=%d batches=%lld steps=%lld head_publish_cycles=%lld "
+                "head_total_cycles=%lld chain_warp_cycles=%lld\n",
+                blocks, h[0], h[1], h[2], h[3], h[4]);
     }
 }
 
