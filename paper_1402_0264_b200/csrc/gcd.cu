@@ -264,7 +264,7 @@ __device__ __forceinline__ uint4 log_get(const StepLog* log, int i) {
 // operand (du = -1) and an undetermined lead (stop).
 template <int MODE>
 __device__ __forceinline__ int chain_step(uint32_t (&u)[GE], const uint32_t (&v)[GE],
-                                          uint32_t& hu, uint32_t hv, long long& du, int vj,
+                                          uint32_t& hu, uint32_t hv, int& du, int vj,
                                           int sup, int aged, bool& slow, bool& stop, Fld f) {
     using A = Arith<MODE>;
     const uint32_t p = f.p, x = hu, nx = A::neg(x, p);
@@ -312,14 +312,14 @@ __device__ void run_chain(BatchMeta& c, StepLog* log, volatile int* done, int M,
     using A = Arith<MODE>;
     const uint32_t p = f.p;
     const int lane = threadIdx.x & 31;
-    long long da = c.da1, db = c.db1;  // exact: the windows start at the leads
+    int da = int(c.da1), db = int(c.db1);  // exact: the windows start at the leads
     uint32_t wa[GE], wb[GE];
 #pragma unroll
     for (int e = 0; e < GE; ++e) {
         wa[e] = winA[e * 32 + lane];
         wb[e] = winB[e * 32 + lane];
     }
-    const long long da0 = da, db0 = db;
+    const int da0 = da, db0 = db;
     uint32_t ha = bcast(wa[0]), hb = bcast(wb[0]);
     // joint validity: valid words of either window from the top (pessimistic);
     // BIG only while both windows hold their whole operands
@@ -381,8 +381,8 @@ __device__ void run_chain(BatchMeta& c, StepLog* log, volatile int* done, int M,
         c.steps = steps;
         c.term = term;
         c.dividend_a = dividend_a;
-        c.sa = int(da0 - (da < 0 ? da0 : da));  // top moves (unused for a vanished row)
-        c.sb = int(db0 - (db < 0 ? db0 : db));
+        c.sa = da0 - (da < 0 ? da0 : da);  // top moves (unused for a vanished row)
+        c.sb = db0 - (db < 0 ? db0 : db);
         st_release_cta(done, steps + 1);  // done = final count + 1
     }
 }
