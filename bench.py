@@ -771,16 +771,22 @@ def cpu_baseline(work, seconds):
 
 
 def run_reference(args, dist):
-    """The reference's own CPU path (oracle/_ref, else the C port), all host
-    threads: one independent instance sample per thread per step."""
+    """The reference's own CPU path (oracle/_ref, else the C port) on the
+    workload of our arm.  Single-instance configs: the reference algorithm is
+    serial (oracle_gcd / oracle_divmod / oracle_mul), so one instance per step
+    on one thread -- all the threads it can use.  Batched configs: one
+    instance per host thread per step (a bounded sample of the batch)."""
     if dist.rank != 0:
         return None
     work = WORKLOADS[args.workload](args.s)
     orc, kind = _oracle()
-    cores = os.cpu_count() or 1
+    batched = getattr(work, "sharded", False)
+    cores = (os.cpu_count() or 1) if batched else 1
     fn, units, ok, what = work.cpu_ref(orc)
 
     def step():
+        if cores == 1:
+            return [fn()]
         with ThreadPoolExecutor(cores) as ex:
             return list(ex.map(lambda _: fn(), range(cores)))
 
@@ -798,8 +804,10 @@ def run_reference(args, dist):
             "data": "synthetic (seeded mt19937_64 inputs, reference random_poly draws)",
             "config": work.config, "impl": "reference",
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
-                             "sample": f"{cores} concurrent x {what} per step, one per host "
-                                       f"thread"},
+                             "sample": (f"{cores} concurrent x {what} per step, one per host "
+                                        f"thread") if cores > 1 else
+                                       f"{what} per step, serial (the reference algorithm is "
+                                       f"single-threaded)"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
 

@@ -151,24 +151,29 @@ __global__ void __launch_bounds__(DIV_T) div_cta_kernel(DivArgs g, int borg) {
 }
 
 // ------------------------------------------- cooperative grid, 1 instance ---
-// Shared layout (words): bseg[SEG + S + R + 8] | h[S] | lam[Spad]
-template <int R>
+// Per step of s heads: the heads are staged in shared memory with one
+// coalesced load; the s quotient words are the truncated convolution
+// lambda = h (*) heads computed by all threads with RL-word register tiles;
+// the remainder update gives every thread RU outputs of this CTA's slice.
+// Shared layout (words): bseg | hz (h, zero-padded below) | hd (heads) | lam
+template <int RL, int RU>
 __global__ void __launch_bounds__(DIV_T) div_grid_kernel(DivArgs g, int64_t seg) {
     extern __shared__ __align__(16) uint32_t smem[];
     cg::grid_group grid = cg::this_grid();
     const int64_t na = g.na, nb = g.nb, db = nb - 1;
     const int S = g.S;
-    const int Spad = (S + R - 1) / R * R;
+    const int padL = (S + RL - 1) / RL * RL, padU = (S + RU - 1) / RU * RU;
     const FieldParams F = g.F;
     // this CTA's slice of the active window, relative to its bottom: [y_lo, y_hi)
     const int64_t y_lo = int64_t(blockIdx.x) * seg;
     const int64_t y_hi = y_lo + seg < db ? y_lo + seg : db;
-    // bseg[borg + (y - y_lo)] = b[y], y in [y_lo - Spad, y_hi + R)
-    const int borg = ((Spad + 3) & ~3) + 3;
+    const int borg = ((padU + 3) & ~3) + 3;       // bseg[borg + (y - y_lo)] = b[y]
+    const int horg = ((padL + 3) & ~3) + 3;       // hz[horg + j] = h[j], 0 for j < 0
     uint32_t* bseg = smem;
-    const int64_t blen = borg + seg + R + 1;
-    uint32_t* h = bseg + ((blen + 3) & ~int64_t(3));
-    uint32_t* lam = h + ((S + 3) & ~3);
+    const int64_t blen = borg + seg + RU + 1;
+    uint32_t* hz = bseg + ((blen + 3) & ~int64_t(3));
+    uint32_t* hd = hz + ((horg + padL + 8 + 3) & ~3);
+    uint32_t* lam = hd + ((padL + 3) & ~3);
     uint32_t* A = g.a_work;
 
     for (int64_t j = threadIdx.x; j < blen; j += DIV_T) {
@@ -182,25 +187,44 @@ __global__ void __launch_bounds__(DIV_T) div_grid_kernel(DivArgs g, int64_t seg)
         inverse_series(g.h_glob, S, db,
                        [&](int64_t t) { return t <= db ? __ldcg(g.b + (db - t)) : 0u; }, F);
     grid.sync();
-    for (int k = threadIdx.x; k < S; k += DIV_T) h[k] = __ldcg(g.h_glob + k);
+    for (int k = threadIdx.x; k < horg + padL + 8; k += DIV_T)
+        hz[k] = (k >= horg && k - horg < S) ? __ldcg(g.h_glob + (k - horg)) : 0u;
     __syncthreads();
 
     for (int64_t i = na - 1; i >= db;) {
         const int valid = int(i - db + 1 < S ? i - db + 1 : S);
-        const int padded = (valid + R - 1) / R * R;
-        step_lambdas(lam, valid, padded, h, [&](int t) { return __ldcg(A + (i - t)); },
-                     g.q + (i - db), blockIdx.x == 0, F);
+        const int nl = (valid + RL - 1) / RL * RL, nu = (valid + RU - 1) / RU * RU;
+        for (int t = threadIdx.x; t < nl; t += DIV_T) hd[t] = t < valid ? __ldcg(A + (i - t)) : 0u;
+        for (int t = valid + threadIdx.x; t < nu; t += DIV_T) lam[t] = 0u;
+        __syncthreads();
+        // lambda_k = sum_{t<=k} h[k-t] * A[i-t]   (k < valid)
+        for (int k0 = int(threadIdx.x) * RL; k0 < valid; k0 += DIV_T * RL) {
+            uint64_t acc[RL];
+#pragma unroll
+            for (int r = 0; r < RL; ++r) acc[r] = 0;
+            uint32_t since = 0;
+            conv_accumulate<RL>(acc, hd, nl / RL, hz, horg + k0, since, F);
+#pragma unroll
+            for (int r = 0; r < RL; ++r) {
+                const int k = k0 + r;
+                if (k < valid) {
+                    const uint32_t l = reduce(acc[r], F);
+                    lam[valid - 1 - k] = negmod(l, F);
+                    if (blockIdx.x == 0) g.q[i - db - k] = l;
+                }
+            }
+        }
         __syncthreads();
         const int64_t xlo = i - valid + 1 - db;
-        for (int64_t y0 = y_lo + int64_t(threadIdx.x) * R; y0 < y_hi;
-             y0 += int64_t(DIV_T) * R) {
-            uint64_t acc[R];
+        for (int64_t y0 = y_lo + int64_t(threadIdx.x) * RU; y0 < y_hi;
+             y0 += int64_t(DIV_T) * RU) {
+            uint64_t acc[RU];
 #pragma unroll
-            for (int r = 0; r < R; ++r) acc[r] = (y0 + r < y_hi) ? __ldcg(A + xlo + y0 + r) : 0u;
+            for (int r = 0; r < RU; ++r) acc[r] = (y0 + r < y_hi) ? __ldcg(A + xlo + y0 + r) : 0u;
             uint32_t since = 0;
-            conv_accumulate<R>(acc, lam, padded / R, bseg, int(borg + (y0 - y_lo)), since, F);
+            conv_accumulate<RU>(acc, lam, nu / RU, bseg, int(borg + (y0 - y_lo)), since, F);
 #pragma unroll
-            for (int r = 0; r < R; ++r)
+            for (int r = 0; r < RU; ++r)
                 if (y0 + r < y_hi) __stcg(A + xlo + y0 + r, reduce(acc[r], F));
         }
         grid.sync();
@@ -239,24 +263,25 @@ void run_cta(const DivArgs& g, int64_t count, cudaStream_t st) {
     }
 }
 
-template <int R>
+template <int RL, int RU>
 void run_grid(DivArgs g, cudaStream_t st) {
     const int S = g.S;
-    const int Spad = (S + R - 1) / R * R;
+    const int padL = (S + RL - 1) / RL * RL, padU = (S + RU - 1) / RU * RU;
     const int64_t db = g.nb - 1;
-    int dev = 0, per_sm = 0;
-    MMM_CUDA(cudaGetDevice(&dev));
-    // slice per CTA: >= one full pass of the CTA's threads where possible
+    int per_sm = 0;
+    // slice per CTA: a full pass of the CTA's threads, at most one CTA per SM
     const int ctas_max = sm_count();
-    int64_t seg = std::max<int64_t>(ceil_div(db, ctas_max), 1);
-    seg = ceil_div(seg, R) * R;
-    const int borg = ((Spad + 3) & ~3) + 3;
-    const int64_t blen = borg + seg + R + 1;
-    const size_t bytes = size_t(((blen + 3) & ~int64_t(3)) + ((S + 3) & ~3) + Spad + 4) * 4;
-    MMM_CUDA(cudaFuncSetAttribute(div_grid_kernel<R>,
+    int64_t seg = std::max<int64_t>(ceil_div(db, ctas_max), int64_t(DIV_T) * RU);
+    seg = ceil_div(seg, RU) * RU;
+    const int borg = ((padU + 3) & ~3) + 3, horg = ((padL + 3) & ~3) + 3;
+    const int64_t blen = borg + seg + RU + 1;
+    const size_t words = size_t(((blen + 3) & ~int64_t(3)) + ((horg + padL + 8 + 3) & ~3) +
+                                ((padL + 3) & ~3) + padU + 8);
+    const size_t bytes = words * 4;
+    MMM_CUDA(cudaFuncSetAttribute(div_grid_kernel<RL, RU>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
-    MMM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, div_grid_kernel<R>, DIV_T,
-                                                           bytes));
+    MMM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, div_grid_kernel<RL, RU>,
+                                                           DIV_T, bytes));
     const int64_t blocks = ceil_div(db, seg);
     if (per_sm < 1 || blocks > int64_t(per_sm) * ctas_max)
         throw Error(ST_SIM, "division: grid does not fit co-resident");
@@ -264,7 +289,7 @@ void run_grid(DivArgs g, cudaStream_t st) {
     g.h_glob = sc.get<uint32_t>(size_t(S));
     g.a_work = sc.get<uint32_t>(size_t(g.na));
     void* params[] = {&g, &seg};
-    MMM_CUDA(cudaLaunchCooperativeKernel((void*)div_grid_kernel<R>, dim3(unsigned(blocks)),
+    MMM_CUDA(cudaLaunchCooperativeKernel((void*)div_grid_kernel<RL, RU>, dim3(unsigned(blocks)),
                                          dim3(DIV_T), params, bytes, st));
     check_launch("div_grid_kernel");
 }
@@ -300,9 +325,9 @@ void launch_divmod(const FieldParams& F, const uint32_t* a, int64_t na, const ui
         return;
     }
     switch (R) {
-        case 8: run_grid<8>(g, st); break;
-        case 2: run_grid<2>(g, st); break;
-        default: run_grid<1>(g, st); break;
+        case 8: run_grid<4, 2>(g, st); break;
+        case 2: run_grid<2, 2>(g, st); break;
+        default: run_grid<1, 1>(g, st); break;
     }
 }
 
