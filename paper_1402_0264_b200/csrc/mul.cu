@@ -11,23 +11,28 @@
 // outputs in 64-bit registers (conv.cuh).  The reference's M array of
 // (x-1)*y partial rows and its log2 ADD rounds disappear: when a k-tile's
 // i-range is split over several items, the items' reduced partial sums
-// (< p each) meet in a 64-bit global accumulator through RED.ADD.64 and one
-// finalize pass reduces them -- the segmented add of the paper, done by
-// atomics in L2 instead of log-round launches.  Batched products give each
-// instance whole k-tiles (no split, direct stores).
+// (< p each) meet in a 64-bit global accumulator through RED.ADD.64, and the
+// last item to arrive on a k-tile reduces it (no second launch) -- the ADD
+// rounds of the paper, done in L2 instead of log-round launches.  Batched
+// products give each instance whole k-tiles (no split).  (Double-buffered
+// cp.async staging was measured slower at 4-byte granularity: 72 vs 67 us.)
 #include "common.cuh"
 #include "conv.cuh"
 
 namespace mmm_cu {
 
 constexpr int MUL_T = 128;   // threads per CTA
-constexpr int MUL_TI = 512;  // terms per shared-memory chunk
+#ifndef MUL_TI_WORDS
+#define MUL_TI_WORDS 256
+#endif
+constexpr int MUL_TI = MUL_TI_WORDS;  // terms per shared-memory chunk
 
 struct MulArgs {
     const uint32_t* a;
     const uint32_t* b;
     uint32_t* f;
     unsigned long long* acc;  // split k-tiles accumulate here (single instance)
+    unsigned* arrived;        // per k-tile count of finished items (zeroed with acc)
     int64_t na, nb, lda, ldb, ldf;
     int64_t chunk;  // i-range per item
     FieldParams F;
@@ -84,18 +89,22 @@ __global__ void __launch_bounds__(MUL_T) mul_kernel(MulArgs g) {
                 f[k] = v;
         }
     }
-}
-
-// f[k] = acc[k] mod p for the k-tiles that were split across items.
-__global__ void mul_finalize_kernel(const unsigned long long* __restrict__ acc, uint32_t* f,
-                                    int64_t nf, int64_t nb, int64_t na, int tk, int64_t chunk,
-                                    FieldParams F) {
-    const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (k >= nf) return;
-    const int64_t k0 = (k / tk) * tk;
-    const int64_t ilo = k0 - (nb - 1) > 0 ? k0 - (nb - 1) : 0;
-    const int64_t ihi = k0 + tk < na ? k0 + tk : na;
-    if (ihi - ilo > chunk) f[k] = reduce(acc[k], F);
+    if (!split) return;
+    // the last item to finish this k-tile reduces it (threadfence reduction)
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned items = unsigned((ihi - ilo + g.chunk - 1) / g.chunk);
+        last = atomicAdd(g.arrived + blockIdx.y, 1u) == items - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    for (int t = threadIdx.x; t < TK; t += MUL_T) {
+        const int64_t k = k0 + t;
+        if (k < nf) f[k] = reduce(__ldcg(g.acc + k), g.F);
+    }
 }
 
 namespace {
@@ -141,7 +150,7 @@ void launch_mul(const FieldParams& F, const uint32_t* a, int64_t na, const uint3
         total += hi - lo;
         longest = std::max(longest, hi - lo);
     }
-    const int64_t target = 8LL * sm_count();
+    const int64_t target = 16LL * sm_count();
     int64_t chunk = ceil_div(ceil_div(total, target), MUL_TI) * MUL_TI;
     if (chunk < MUL_TI) chunk = MUL_TI;
     const int64_t items = ceil_div(longest, chunk);
@@ -155,16 +164,13 @@ void launch_mul(const FieldParams& F, const uint32_t* a, int64_t na, const uint3
     g.nb = nb;
     g.chunk = chunk;
     g.F = F;
-    if (items > 1) {
-        g.acc = scratch.get<unsigned long long>(size_t(nf));
-        MMM_CUDA(cudaMemsetAsync(g.acc, 0, size_t(nf) * sizeof(unsigned long long), st));
+    if (items > 1) {  // one zeroing pass for the accumulator and the arrival counters
+        const size_t words = size_t(nf) + size_t(ceil_div(nkt, 2));
+        g.acc = scratch.get<unsigned long long>(words);
+        g.arrived = reinterpret_cast<unsigned*>(g.acc + nf);
+        MMM_CUDA(cudaMemsetAsync(g.acc, 0, words * sizeof(unsigned long long), st));
     }
     dispatch(R, g, dim3(unsigned(items), unsigned(nkt), 1), st);
-    if (items > 1) {
-        mul_finalize_kernel<<<unsigned(ceil_div(nf, 256)), 256, 0, st>>>(g.acc, f, nf, nb, na,
-                                                                         int(TK), chunk, F);
-        check_launch("mul_finalize_kernel");
-    }
 }
 
 void launch_mul_batched(const FieldParams& F, const uint32_t* A, int64_t lda, int64_t na,
