@@ -54,7 +54,6 @@ constexpr int W1 = 32 * GE;        // window words per operand
 constexpr int PE = GCD_PE;         // matrix words per lane per polynomial
 constexpr int PL = 32 * PE;        // matrix capacity (support < PL)
 constexpr int LOGCAP = 2048;       // steps per matrix batch, hard cap
-constexpr int LOGCHUNK = 8;        // log entries buffered in registers per flush
 constexpr int BIG = 1 << 30;       // "validity unbounded": window covers the operand
 constexpr int GCD_R = 1;           // outputs per thread in the apply
 
@@ -235,18 +234,14 @@ __device__ void load_top(uint32_t (&w)[GE], const uint32_t* Z, long long& deg, u
     }
 }
 
-// Log entries: the chain buffers entry s in lane s % LOGCHUNK and stores them at a
-// time, one 16-byte store per lane; `seq` = step index + 1 publishes an entry
-// (the replay warps poll the entry itself, no per-step fence or store).
-__device__ __forceinline__ void log_flush(StepLog* log, int base, int count, uint32_t x,
-                                          uint32_t y, uint32_t zf) {
-    const int lane = threadIdx.x & 31;
-    if (lane < count) {
-        const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(log + base + lane));
-        asm volatile("st.volatile.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(x), "r"(y),
-                     "r"(zf), "r"(unsigned(base + lane + 1))
-                     : "memory");
-    }
+// Log entry, stored by every lane of the chain warp (same address, same
+// value: no divergence, no fence); `seq` = step index + 1 publishes it to the
+// replay warps, which poll the entry itself.
+__device__ __forceinline__ void log_step(StepLog* log, int i, uint32_t x, uint32_t y, int z,
+                                         bool u_is_a) {
+    const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(log + i));
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(x), "r"(y),
+                 "r"(unsigned(z) | (u_is_a ? 0x10000u : 0u)), "r"(unsigned(i + 1)));
 }
 __device__ __forceinline__ uint4 log_get(const StepLog* log, int i) {
     const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(const_cast<StepLog*>(log + i)));
@@ -328,7 +323,6 @@ __device__ void run_chain(BatchMeta& c, StepLog* log, volatile int* done, int M,
     int dividend_a = c.dividend_a;
     const int cap = min(M, LOGCAP);
     int steps = 0, term = 0, F = 0, F0 = 0;
-    uint32_t lx = 0, ly = 0, lz = 0;  // this lane's buffered log entry
     for (;;) {
         // oracle role rule: reduce the dividend while deg(dividend) >= deg(divisor)
         if (dividend_a) {
@@ -362,17 +356,10 @@ __device__ void run_chain(BatchMeta& c, StepLog* log, volatile int* done, int M,
             F = 0;
             F0 = 0;
         }
-        if (lane == (steps & (LOGCHUNK - 1))) {
-            lx = x;
-            ly = y;
-            lz = unsigned(z) | (dividend_a ? 0x10000u : 0u);
-        }
+        log_step(log, steps, x, y, z, dividend_a != 0);
         ++steps;
-        if ((steps & (LOGCHUNK - 1)) == 0) log_flush(log, steps - LOGCHUNK, LOGCHUNK, lx, ly, lz);
         if (stop) break;
     }
-    if (steps & (LOGCHUNK - 1))
-        log_flush(log, steps & ~(LOGCHUNK - 1), steps & (LOGCHUNK - 1), lx, ly, lz);
     if (lane == 0) {
         c.da0 = da0;
         c.db0 = db0;
