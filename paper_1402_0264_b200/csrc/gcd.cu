@@ -55,7 +55,6 @@ constexpr int PE = GCD_PE;         // matrix words per lane per polynomial
 constexpr int PL = 32 * PE;        // matrix capacity (support < PL)
 constexpr int LOGCAP = 2048;       // steps per matrix batch, hard cap
 constexpr int BIG = 1 << 30;       // "validity unbounded": window covers the operand
-constexpr int GCD_R = 1;           // outputs per thread in the apply
 
 struct StepLog {
     uint32_t x, y;
@@ -112,6 +111,21 @@ struct Arith {
         if (MODE == 0) return hi - mp + f.p;  // t < 8p^2 < p*2^32 for p < 2^29: in (0, 2p)
         const uint32_t r = hi - mp;
         return hi < mp ? r + f.p : r;
+    }
+    // (a*x + b*y + c*z) * 2^-32, MODE 0 only: a, b, c canonical, x, y, z lazy
+    // (< 2p), so t < 6p^2 < p*2^32 and the lazy result lies in (0, 2p).
+    static __device__ __forceinline__ uint32_t comb3(uint32_t a, uint32_t x, uint32_t b, uint32_t y,
+                                                      uint32_t c, uint32_t z, Fld f) {
+        const uint64_t t = uint64_t(a) * x + uint64_t(b) * y + uint64_t(c) * z;
+        const uint32_t m = uint32_t(t) * f.pinv;
+        return uint32_t(t >> 32) - __umulhi(m, f.p) + f.p;
+    }
+    // a*b * 2^-32, canonical (MODE 0 operands < 2p)
+    static __device__ __forceinline__ uint32_t mont(uint32_t a, uint32_t b, Fld f) {
+        const uint64_t t = uint64_t(a) * b;
+        const uint32_t m = uint32_t(t) * f.pinv;
+        const uint32_t r = uint32_t(t >> 32) - __umulhi(m, f.p) + f.p;
+        return r >= f.p ? r - f.p : r;
     }
     static __device__ __forceinline__ bool nz(uint32_t v, uint32_t p) {
         return MODE == 0 ? (v != 0u && v != p) : v != 0u;
@@ -204,6 +218,27 @@ __device__ __forceinline__ void shift_right1(uint32_t (&w)[N], int na) {
         if (e < na) w[e] = lane == 0 ? (e > 0 ? r[e - 1] : 0u) : r[e];
 }
 
+// o[t] = w[t + K] (top-aligned copy shifted left by a constant; zeros enter).
+template <int K, int N>
+__device__ __forceinline__ void shl_copy(const uint32_t (&w)[N], uint32_t (&o)[N]) {
+    const int lane = threadIdx.x & 31;
+    uint32_t r[N];
+#pragma unroll
+    for (int e = 0; e < N; ++e) r[e] = __shfl_sync(0xffffffffu, w[e], (lane + K) & 31);
+#pragma unroll
+    for (int e = 0; e < N; ++e) o[e] = lane + K >= 32 ? (e + 1 < N ? r[e + 1] : 0u) : r[e];
+}
+// o[t] = w[t - K] (right-shifted copy; zeros enter at t < K).
+template <int K, int N>
+__device__ __forceinline__ void shr_copy(const uint32_t (&w)[N], uint32_t (&o)[N]) {
+    const int lane = threadIdx.x & 31;
+    uint32_t r[N];
+#pragma unroll
+    for (int e = 0; e < N; ++e) r[e] = __shfl_sync(0xffffffffu, w[e], (lane - K) & 31);
+#pragma unroll
+    for (int e = 0; e < N; ++e) o[e] = lane < K ? (e > 0 ? r[e - 1] : 0u) : r[e];
+}
+
 // First t >= from with w[t] != 0 (warp-uniform), or -1.
 template <int MODE, int N>
 __device__ __forceinline__ int first_nz(const uint32_t (&w)[N], int from, uint32_t p) {
@@ -235,13 +270,17 @@ __device__ void load_top(uint32_t (&w)[GE], const uint32_t* Z, long long& deg, u
 }
 
 // Log entry, stored by every lane of the chain warp (same address, same
-// value: no divergence, no fence); `seq` = step index + 1 publishes it to the
-// replay warps, which poll the entry itself.
-__device__ __forceinline__ void log_step(StepLog* log, int i, uint32_t x, uint32_t y, int z,
-                                         bool u_is_a) {
+// value: no divergence, no fence).  Single step: (x, y, 0, meta), the
+// dividend u <- y*u - x*v shifted by z.  Fused pair (MODE 0): (alpha, beta,
+// gamma, meta), u <- alpha*u[t+2] + beta*v[t+2] + gamma*v[t+1] shifted by a
+// further z - 2.  meta = seq << 20 | fused << 19 | u_is_a << 18 | z, seq =
+// entry index + 1 publishes it to the replay warps, which poll the entry.
+constexpr unsigned LOG_FUSED = 1u << 19, LOG_UA = 1u << 18, LOG_Z = (1u << 18) - 1;
+__device__ __forceinline__ void log_entry(StepLog* log, int i, uint32_t c0, uint32_t c1,
+                                          uint32_t c2, unsigned meta) {
     const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(log + i));
-    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(x), "r"(y),
-                 "r"(unsigned(z) | (u_is_a ? 0x10000u : 0u)), "r"(unsigned(i + 1)));
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(c0), "r"(c1), "r"(c2),
+                 "r"(meta | (unsigned(i + 1) << 20)));
 }
 __device__ __forceinline__ uint4 log_get(const StepLog* log, int i) {
     const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(const_cast<StepLog*>(log + i)));
@@ -253,29 +292,12 @@ __device__ __forceinline__ uint4 log_get(const StepLog* log, int i) {
     return v;
 }
 
-// One elimination: reduce u (the dividend) by v.  Fast path: the new lead is
-// u[1] (z = 1), fetched by one shuffle while the window shifts by one.
-// Returns z (the renormalisation shift); slow path handles z != 1, a vanished
-// operand (du = -1) and an undetermined lead (stop).
+// Renormalisation after a comb whose candidate lead u[0] vanished: the first
+// nonzero t >= 1 within the valid words `vmin` and the matrix room `room`.
+// Returns the shift (du lowered by it; du = -1 if the whole operand vanished).
 template <int MODE>
-__device__ __forceinline__ int chain_step(uint32_t (&u)[GE], const uint32_t (&v)[GE],
-                                          uint32_t& hu, uint32_t hv, int& du, int vj,
-                                          int sup, int aged, bool& slow, bool& stop, Fld f) {
-    using A = Arith<MODE>;
-    const uint32_t p = f.p, x = hu, nx = A::neg(x, p);
-#pragma unroll
-    for (int e = 0; e < GE; ++e) u[e] = A::comb(hv, u[e], nx, v[e], f);
-    const uint32_t h1 = from_lane(u[0], 1);
-    if (A::nz(h1, p)) {
-        shift_left1(u, GE);
-        hu = h1;
-        du -= 1;
-        return 1;
-    }
-    slow = true;
-    // bounds aged by the `aged` fast steps taken since they were refreshed
-    const int vmin = vj < BIG ? vj - aged : BIG;
-    const int room = PL - 1 - (sup + aged);
+__device__ __forceinline__ int renorm(uint32_t (&u)[GE], int& du, int vmin, int room, bool& stop,
+                                      uint32_t p) {
     int z = first_nz<MODE>(u, 1, p);
     if (z < 0 || z >= vmin) {
         if (vmin >= BIG) {  // the window held the whole operand: it vanished
@@ -290,9 +312,114 @@ __device__ __forceinline__ int chain_step(uint32_t (&u)[GE], const uint32_t (&v)
         stop = true;
     }
     shift_left(u, z);
-    hu = bcast(u[0]);
     du -= z;
     return z;
+}
+
+// One elimination: reduce u (the dividend) by v.  Fast path: the new lead is
+// u[1] (z = 1), fetched by one shuffle while the window shifts by one.
+// Returns z (the renormalisation shift); slow path handles z != 1, a vanished
+// operand (du = -1) and an undetermined lead (stop).  hu1 tracks u's second
+// coefficient (MODE 0: the fused pairs need it).
+template <int MODE>
+__device__ __forceinline__ int chain_step(uint32_t (&u)[GE], const uint32_t (&v)[GE],
+                                          uint32_t& hu, uint32_t& hu1, uint32_t hv, int& du,
+                                          int vj, int sup, int aged, bool& slow, bool& stop,
+                                          Fld f) {
+    using A = Arith<MODE>;
+    const uint32_t p = f.p, x = hu, nx = A::neg(x, p);
+#pragma unroll
+    for (int e = 0; e < GE; ++e) u[e] = A::comb(hv, u[e], nx, v[e], f);
+    const uint32_t h1 = from_lane(u[0], 1);
+    const uint32_t h2 = MODE == 0 ? from_lane(u[0], 2) : 0u;
+    if (A::nz(h1, p)) {
+        shift_left1(u, GE);
+        hu = h1;
+        hu1 = h2;
+        du -= 1;
+        return 1;
+    }
+    slow = true;
+    // bounds aged by the `aged` fast steps taken since they were refreshed
+    const int vmin = vj < BIG ? vj - aged : BIG;
+    const int room = PL - 1 - (sup + aged);
+    const int z = renorm<MODE>(u, du, vmin, room, stop, p);
+    hu = bcast(u[0]);
+    if (MODE == 0) hu1 = from_lane(u[0], 1);
+    return z;
+}
+
+// Two eliminations of u by v at once (MODE 0; deg u = deg v + 1 and the
+// first step's new lead cc = (v0*u1 - u0*v1) * 2^-32 nonzero, so the second
+// step reduces u again at equal degree): u1 = (v0*u - u0*X*v)/R, then
+// u2 = (v0*u1 - cc*v)/R = (alpha*u + beta*X*v + gamma*v)/R with alpha = v0^2/R,
+// beta = -u0*v0/R, gamma = -cc; top-aligned u2[t] = alpha*u[t+2] +
+// beta*v[t+2] + gamma*v[t+1].  One 3-term reduction per word and one lead
+// broadcast per two steps.  Returns the total shift z >= 2.
+__device__ __forceinline__ int fused_step(uint32_t (&u)[GE], const uint32_t (&v)[GE], uint32_t& hu,
+                                          uint32_t& hu1, uint32_t hv, uint32_t cc, int& du,
+                                          int vj, int sup, int aged, bool& slow, bool& stop,
+                                          Fld f, uint32_t& al, uint32_t& be, uint32_t& ga) {
+    using A = Arith<0>;
+    const uint32_t p = f.p;
+    uint32_t us2[GE], vs2[GE], vs1[GE];
+    shl_copy<2>(u, us2);
+    shl_copy<2>(v, vs2);
+    shl_copy<1>(v, vs1);
+    al = A::mont(hv, hv, f);
+    be = A::mont(hv, A::neg(hu, p), f);
+    ga = A::canon(A::neg(cc, p), p);
+#pragma unroll
+    for (int e = 0; e < GE; ++e) u[e] = A::comb3(al, us2[e], be, vs2[e], ga, vs1[e], f);
+    const uint32_t n0 = bcast(u[0]), n1 = from_lane(u[0], 1);
+    if (A::nz(n0, p)) {
+        hu = n0;
+        hu1 = n1;
+        du -= 2;
+        return 2;
+    }
+    slow = true;
+    const int vmin = vj < BIG ? vj - aged - 2 : BIG;
+    const int room = PL - 1 - (sup + aged + 2);
+    du -= 2;
+    int z = 0;
+    if (room > 0 && vmin > 0) {
+        z = renorm<0>(u, du, vmin, room, stop, p);
+    } else {
+        stop = true;  // no room left past the pair: end the batch here
+    }
+    hu = bcast(u[0]);
+    hu1 = from_lane(u[0], 1);
+    return 2 + z;
+}
+
+// The fused pair as the steady state's fast path: everything is computed
+// speculatively (the shifted copies before the scalars are known) and kept
+// only if both cc and the new lead are nonzero; otherwise u is untouched and
+// the general path takes over.
+__device__ __forceinline__ bool fused_fast(uint32_t (&u)[GE], const uint32_t (&v)[GE], uint32_t& hu,
+                                           uint32_t& hu1, uint32_t hv, uint32_t hv1, Fld f,
+                                           uint32_t& al, uint32_t& be, uint32_t& ga) {
+    using A = Arith<0>;
+    const uint32_t p = f.p;
+    uint32_t us2[GE], vs2[GE], vs1[GE], nu[GE];
+    shl_copy<2>(u, us2);
+    shl_copy<2>(v, vs2);
+    shl_copy<1>(v, vs1);
+    const uint32_t nx = A::neg(hu, p);
+    const uint32_t cc = A::comb(hv, hu1, nx, hv1, f);
+    al = A::mont(hv, hv, f);
+    be = A::mont(hv, nx, f);
+    ga = A::canon(A::neg(cc, p), p);
+#pragma unroll
+    for (int e = 0; e < GE; ++e) nu[e] = A::comb3(al, us2[e], be, vs2[e], ga, vs1[e], f);
+    const uint32_t n0 = bcast(nu[0]), n1 = from_lane(nu[0], 1);
+    if (!(A::nz(cc, p) && A::nz(n0, p))) return false;
+#pragma unroll
+    for (int e = 0; e < GE; ++e) u[e] = nu[e];
+    hu = n0;
+    hu1 = n1;
+    return true;
 }
 
 // Warp 0 of CTA 0: the elimination chain of one batch on two fixed windows
@@ -316,13 +443,14 @@ __device__ void run_chain(BatchMeta& c, StepLog* log, volatile int* done, int M,
     }
     const int da0 = da, db0 = db;
     uint32_t ha = bcast(wa[0]), hb = bcast(wb[0]);
+    uint32_t ha1 = from_lane(wa[0], 1), hb1 = from_lane(wb[0], 1);
     // joint validity: valid words of either window from the top (pessimistic);
     // BIG only while both windows hold their whole operands
     int vj = (da < W1 && db < W1) ? BIG : W1;
     int sup = 0;  // max matrix support (pessimistic)
     int dividend_a = c.dividend_a;
     const int cap = min(M, LOGCAP);
-    int steps = 0, term = 0, F = 0, F0 = 0;
+    int steps = 0, n = 0, term = 0, F = 0, F0 = 0;
     for (;;) {
         // oracle role rule: reduce the dividend while deg(dividend) >= deg(divisor)
         if (dividend_a) {
@@ -341,13 +469,64 @@ __device__ void run_chain(BatchMeta& c, StepLog* log, volatile int* done, int M,
             if (F <= 0) break;  // batch length, window or matrix exhausted
             F0 = F;
         }
-        if ((dividend_a ? db : da) == 0) { term = 3; break; }  // constant divisor: unit gcd
+        if (MODE == 0) {
+            // steady state: degree-1 quotients, roles alternating every pair
+            while (F >= 2) {
+                const bool a_div = dividend_a != 0;
+                const int du = a_div ? da : db, dv = a_div ? db : da;
+                if (du != dv + 1 || dv < 1) break;
+                uint32_t al, be, ga;
+                const bool ok = a_div ? fused_fast(wa, wb, ha, ha1, hb, hb1, f, al, be, ga)
+                                      : fused_fast(wb, wa, hb, hb1, ha, ha1, f, al, be, ga);
+                if (!ok) break;
+                if (a_div) da -= 2;
+                else db -= 2;
+                F -= 2;
+                steps += 2;
+                log_entry(log, n++, al, be, ga, LOG_FUSED | (a_div ? LOG_UA : 0u) | 2u);
+                dividend_a = !a_div;
+            }
+            if (F <= 0) continue;  // refresh first
+        }
+        const int du = dividend_a ? da : db, dv = dividend_a ? db : da;
+        if (dv == 0) { term = 3; break; }  // constant divisor: unit gcd
         const int aged = F0 - F;  // fast steps since the bounds were refreshed
         bool slow = false, stop = false;
         int z;
+        if (MODE == 0 && F >= 2 && du == dv + 1) {
+            // a degree-1 quotient: fuse its two steps unless the first one
+            // drops the degree by more than one (cc = 0)
+            const uint32_t u0 = dividend_a ? ha : hb, u1 = dividend_a ? ha1 : hb1;
+            const uint32_t v0 = dividend_a ? hb : ha, v1 = dividend_a ? hb1 : ha1;
+            const uint32_t cc = A::comb(v0, u1, A::neg(u0, p), v1, f);
+            if (A::nz(cc, p)) {
+                uint32_t al, be, ga;
+                if (dividend_a)
+                    z = fused_step(wa, wb, ha, ha1, hb, cc, da, vj, sup, aged, slow, stop, f, al,
+                                   be, ga);
+                else
+                    z = fused_step(wb, wa, hb, hb1, ha, cc, db, vj, sup, aged, slow, stop, f, al,
+                                   be, ga);
+                F -= 2;
+                if (slow) {
+                    const int used = F0 - F - 2;
+                    if (vj < BIG) vj -= used + z;
+                    sup += used + z;
+                    F = 0;
+                    F0 = 0;
+                }
+                log_entry(log, n++, al, be, ga,
+                          LOG_FUSED | (dividend_a ? LOG_UA : 0u) | unsigned(z));
+                steps += 2;
+                if (stop) break;
+                continue;
+            }
+        }
         const uint32_t x = dividend_a ? ha : hb, y = dividend_a ? hb : ha;
-        if (dividend_a) z = chain_step<MODE>(wa, wb, ha, hb, da, vj, sup, aged, slow, stop, f);
-        else z = chain_step<MODE>(wb, wa, hb, ha, db, vj, sup, aged, slow, stop, f);
+        if (dividend_a)
+            z = chain_step<MODE>(wa, wb, ha, ha1, hb, da, vj, sup, aged, slow, stop, f);
+        else
+            z = chain_step<MODE>(wb, wa, hb, hb1, ha, db, vj, sup, aged, slow, stop, f);
         --F;
         if (slow) {  // exact bookkeeping for this step, then re-derive the budget
             const int used = F0 - F - 1;  // fast steps before this one
@@ -356,7 +535,7 @@ __device__ void run_chain(BatchMeta& c, StepLog* log, volatile int* done, int M,
             F = 0;
             F0 = 0;
         }
-        log_step(log, steps, x, y, z, dividend_a != 0);
+        log_entry(log, n++, x, y, 0u, (dividend_a ? LOG_UA : 0u) | unsigned(z));
         ++steps;
         if (stop) break;
     }
@@ -370,111 +549,85 @@ __device__ void run_chain(BatchMeta& c, StepLog* log, volatile int* done, int M,
         c.dividend_a = dividend_a;
         c.sa = da0 - (da < 0 ? da0 : da);  // top moves (unused for a vanished row)
         c.sb = db0 - (db < 0 ? db0 : db);
-        st_release_cta(done, steps + 1);  // done = final count + 1
+        st_release_cta(done, n + 1);  // done = final entry count + 1
     }
 }
 
-// Warps 1 and 2 of CTA 0: replay the step log into matrix column `col`
-// (both rows), oriented like the chain; then publish it (canonical) to Pg.
+// One log entry applied to a matrix row: u (the dividend's row) from u, v.
+template <int MODE>
+__device__ __forceinline__ void replay_entry(uint32_t (&u)[PE], const uint32_t (&v)[PE],
+                                             const uint4& en, Fld f) {
+    using A = Arith<MODE>;
+    const int z = int(en.w & LOG_Z);
+    if (MODE == 0 && (en.w & LOG_FUSED)) {
+        // Pu[e] <- alpha*Pu[e-2] + beta*Pv[e-2] + gamma*Pv[e-1], then >> z-2
+        uint32_t us2[PE], vs2[PE], vs1[PE];
+        shr_copy<2>(u, us2);
+        shr_copy<2>(v, vs2);
+        shr_copy<1>(v, vs1);
+#pragma unroll
+        for (int e = 0; e < PE; ++e)
+            u[e] = Arith<0>::comb3(en.x, us2[e], en.y, vs2[e], en.z, vs1[e], f);
+        if (z > 2) shift_right(u, z - 2);
+    } else {
+        const uint32_t nx = A::neg(en.x, f.p);
+#pragma unroll
+        for (int e = 0; e < PE; ++e) u[e] = A::comb(en.y, u[e], nx, v[e], f);
+        if (z == 1) shift_right1(u, PE);
+        else shift_right(u, z);
+    }
+}
+
+// Warps 1 and 2 of CTA 0: replay the step log into matrix column `col` (row
+// A in ra, row B in rb: fixed registers, a uniform branch picks the row the
+// entry reduces); the next entry is fetched while one is applied.  Then
+// publish the column (canonical) to Pg and Ps.
 template <int MODE>
 __device__ void run_replay(int col, const StepLog* log, volatile int* done, Fld f, uint32_t* Pg,
                            uint32_t* Ps, int* hi_out) {
     using A = Arith<MODE>;
     const uint32_t p = f.p;
     const int lane = threadIdx.x & 31;
-    uint32_t ru[PE], rv[PE];  // rows of the operands held in the chain's u / v
+    uint32_t ra[PE], rb[PE];
 #pragma unroll
-    for (int e = 0; e < PE; ++e) ru[e] = rv[e] = 0u;
-    if (lane == 0) {  // identity: row A col 0 = 1, row B col 1 = 1; oriented u = A
-        if (col == 0) ru[0] = 1u;
-        else rv[0] = 1u;
+    for (int e = 0; e < PE; ++e) ra[e] = rb[e] = 0u;
+    if (lane == 0) {  // identity: row A col 0 = 1, row B col 1 = 1
+        if (col == 0) ra[0] = 1u;
+        else rb[0] = 1u;
     }
-    bool u_is_a = true;
-    int hu = col == 0 ? 0 : -1, hv = col == 0 ? -1 : 0;
+    int ha = col == 0 ? 0 : -1, hb = col == 0 ? -1 : 0;  // support bounds
+    uint4 en = log_get(log, 0);
     for (int i = 0;; ++i) {
-        uint4 en = log_get(log, i);
-        while (en.w != unsigned(i + 1)) {
+        while ((en.w >> 20) != unsigned(i + 1)) {
             const int d = ld_acquire_cta(done);
             if (d != 0 && d - 1 <= i) break;  // chain finished with i entries
-            __nanosleep(32);
-            en = log_get(log, i);
+            en = log_get(log, i);  // spin: warps 1-2 do not share the chain's SMSP
         }
-        if (en.w != unsigned(i + 1)) break;
-        const bool sa = (en.z >> 16) != 0;
-        const int z = int(en.z & 0xFFFFu);
-        if (sa != u_is_a) {
-#pragma unroll
-            for (int e = 0; e < PE; ++e) {
-                const uint32_t t = ru[e];
-                ru[e] = rv[e];
-                rv[e] = t;
-            }
-            const int t = hu; hu = hv; hv = t;
-            u_is_a = sa;
+        if ((en.w >> 20) != unsigned(i + 1)) break;
+        const uint4 nx = log_get(log, min(i + 1, LOGCAP - 1));  // prefetch (may be unpublished)
+        const int z = int(en.w & LOG_Z), hmax = max(ha, hb);
+        if (en.w & LOG_UA) {
+            replay_entry<MODE>(ra, rb, en, f);
+            ha = hmax >= 0 ? hmax + z : -1;
+        } else {
+            replay_entry<MODE>(rb, ra, en, f);
+            hb = hmax >= 0 ? hmax + z : -1;
         }
-        const uint32_t nx = A::neg(en.x, p);
-        const int hmax = max(hu, hv);
-#pragma unroll
-        for (int e = 0; e < PE; ++e) ru[e] = A::comb(en.y, ru[e], nx, rv[e], f);
-        if (z == 1) shift_right1(ru, PE);
-        else shift_right(ru, z);
-        hu = hmax;
-        if (hu >= 0) hu += z;
+        en = nx;
     }
     uint32_t* Pa = Pg + (0 * 2 + col) * PL;  // row A, column col
     uint32_t* Pb = Pg + (1 * 2 + col) * PL;  // row B, column col
 #pragma unroll
     for (int e = 0; e < PE; ++e) {
-        const uint32_t va = A::canon(u_is_a ? ru[e] : rv[e], p);
-        const uint32_t vb = A::canon(u_is_a ? rv[e] : ru[e], p);
+        const uint32_t va = A::canon(ra[e], p), vb = A::canon(rb[e], p);
         __stcg(Pa + e * 32 + lane, va);
         __stcg(Pb + e * 32 + lane, vb);
         Ps[(0 * 2 + col) * PL + e * 32 + lane] = va;  // the window builder's copy
         Ps[(1 * 2 + col) * PL + e * 32 + lane] = vb;
     }
     if (lane == 0) {
-        hi_out[0 * 2 + col] = min(u_is_a ? hu : hv, PL - 1);
-        hi_out[1 * 2 + col] = min(u_is_a ? hv : hu, PL - 1);
-    }
-}
-
-// out[x] = sum_{e<=h1} P1[e] Z1[x + s1 - e] + sum_{e<=h2} P2[e] Z2[x + s2 - e],
-// x in [xs, xe); Zi[j] = 0 outside [0, bi].  One CTA, all threads.
-__device__ void apply_row(uint32_t* out, long long xs, long long xe, const uint32_t* P1, int h1,
-                          const uint32_t* Z1, long long b1, long long s1, const uint32_t* P2,
-                          int h2, const uint32_t* Z2, long long b2, long long s2, uint32_t* sw,
-                          uint32_t* sv, int ORG, const FieldParams& F) {
-    constexpr int R = GCD_R;
-    const long long n = xe - xs;
-    if (n <= 0) return;
-    for (long long c0 = 0; c0 < n; c0 += (long long)GCD_T * R) {
-        const long long cn = min(n - c0, (long long)GCD_T * R);
-        uint64_t acc[R];
-#pragma unroll
-        for (int r = 0; r < R; ++r) acc[r] = 0;
-        uint32_t since = 0;
-        for (int term = 0; term < 2; ++term) {
-            const int h = term ? h2 : h1;
-            if (h < 0) continue;
-            const uint32_t* Pt = term ? P2 : P1;
-            const uint32_t* Zt = term ? Z2 : Z1;
-            const long long zb = term ? b2 : b1;
-            const long long off = xs + c0 + (term ? s2 : s1) - ORG;  // sv[y] = Zt[y + off]
-            const int width = h + 1, wpad = (width + R - 1) / R * R;
-            __syncthreads();
-            for (int u = threadIdx.x; u < wpad; u += GCD_T) sw[u] = u < width ? __ldcg(Pt + u) : 0u;
-            for (long long y = threadIdx.x; y < ORG + cn + R; y += GCD_T) {
-                const long long x = y + off;
-                sv[y] = (x >= 0 && x <= zb) ? __ldcg(Zt + x) : 0u;
-            }
-            __syncthreads();
-            const long long y0 = (long long)threadIdx.x * R;
-            if (y0 < cn) conv_accumulate<R>(acc, sw, wpad / R, sv, int(ORG + y0), since, F);
-        }
-        const long long y0 = (long long)threadIdx.x * R;
-#pragma unroll
-        for (int r = 0; r < R; ++r)
-            if (y0 + r < cn) __stcg(out + xs + c0 + y0 + r, reduce(acc[r], F));
+        hi_out[0 * 2 + col] = min(ha, PL - 1);
+        hi_out[1 * 2 + col] = min(hb, PL - 1);
     }
 }
 
@@ -590,6 +743,7 @@ __device__ int head_cta(const GcdArgs& g, BatchMeta& ctl, StepLog* log, uint32_t
         } else if (warp <= 2) {
             run_replay<MODE>(warp - 1, log, done, Fld{F.p, F.pinv}, g.Pg + (j % RING) * 4 * PL,
                              Ps, hi_s);
+            if (g.stats && threadIdx.x == 32) g.stats[5] += clock64() - t0;
         } else {
             // prefetch: S_j complete once the bulk applied batch j-1
             if (threadIdx.x == 96)
@@ -600,6 +754,7 @@ __device__ int head_cta(const GcdArgs& g, BatchMeta& ctl, StepLog* log, uint32_t
                 topA[i] = (xa >= 0) ? __ldcg(g.XA[j % 3] + xa) : 0u;
                 topB[i] = (xb >= 0) ? __ldcg(g.XB[j % 3] + xb) : 0u;
             }
+            if (g.stats && threadIdx.x == 96) g.stats[6] += clock64() - t0;
         }
         __syncthreads();
         BatchMeta m = ctl;
@@ -649,11 +804,81 @@ __device__ int head_cta(const GcdArgs& g, BatchMeta& ctl, StepLog* log, uint32_t
     }
 }
 
+// Bulk apply of one batch matrix to this CTA's outputs [s0, s1) of the new
+// state (row A: indices < na1, then row B):
+//   out[x] = sum_e P1[e] Z1[x + s1 - e] + sum_e P2[e] Z2[x + s2 - e].
+// Per pass of up to APPLY_OUT outputs, P and the four operand windows the
+// pass needs are staged with one L2 round trip; a work item is (4 consecutive
+// outputs, one quarter of the MAC range: term x half of the support), run by
+// the register-tiled conv_accumulate<4>, and the 4 quarters (adjacent lanes)
+// meet in a two-level butterfly.  (gcd.cpp:252-300 UpdateMatrix apply.)
+constexpr int APPLY_OUT = GCD_T;  // outputs per pass: one work item per thread
+constexpr int APPLY_WORDS = 4 * PL + 2 * (APPLY_OUT + 8) + 4 * (PL + 4);
+
+__device__ void apply_batch(const GcdArgs& g, const BatchMeta& m, const uint32_t* Pglob, int j,
+                            long long s0, long long s1, uint32_t* sm) {
+    const FieldParams F = g.F;
+    const int tid = threadIdx.x;
+    uint32_t* P = sm;  // Pa1, Pa2, Pb1, Pb2
+    uint32_t* Wb = sm + 4 * PL;
+    const uint32_t* Z[2] = {g.XA[j % 3], g.XB[j % 3]};
+    const long long deg[2] = {m.da0, m.db0};
+    uint32_t* out[2] = {g.XA[(j + 1) % 3], g.XB[(j + 1) % 3]};
+    const long long na1 = m.da1 + 1 > 0 ? m.da1 + 1 : 0;
+    // shift of term t for row r: Z_t index = x + sh[2r + t] - e
+    const long long sh[4] = {m.sa, m.sa + m.db0 - m.da0, m.sb + m.da0 - m.db0, m.sb};
+    for (int i = tid; i < 4 * PL; i += GCD_T) P[i] = __ldcg(Pglob + i);
+    for (long long c0 = s0; c0 < s1; c0 += APPLY_OUT) {
+        const long long c1 = min(c0 + APPLY_OUT, s1);
+        const long long xs[2] = {min(c0, na1), max(c0 - na1, 0LL)};
+        const int n[2] = {int(min(c1, na1) - xs[0]), int(max(c1 - na1, 0LL) - xs[1])};
+        const int qn[2] = {(n[0] + 3) >> 2, (n[1] + 3) >> 2};
+        const int L[2] = {4 * qn[0] + PL + 4, 4 * qn[1] + PL + 4};
+        uint32_t* W[4] = {Wb, Wb + L[0], Wb + 2 * L[0], Wb + 2 * L[0] + L[1]};
+        __syncthreads();  // previous pass done with the windows
+        // W[2r + t][y] = Z_t[xs_r + sh - (PL - 1) + y], zero outside [0, deg_t]
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+            const int r = w >> 1, t = w & 1;
+            const long long base = xs[r] + sh[w] - (PL - 1);
+            for (int y = tid; y < L[r]; y += GCD_T) {
+                const long long x = base + y;
+                W[w][y] = (n[r] > 0 && x >= 0 && x <= deg[t]) ? __ldcg(Z[t] + x) : 0u;
+            }
+        }
+        __syncthreads();
+        const int items = 4 * (qn[0] + qn[1]);
+        for (int it0 = 0; it0 < items; it0 += GCD_T) {
+            const int item = it0 + tid, q = item >> 2, part = item & 3;
+            const int r = q < qn[0] ? 0 : 1, qi = q - (r ? qn[0] : 0);
+            const int t = part >> 1, e0 = (part & 1) * (PL / 2);
+            uint64_t acc[4] = {0, 0, 0, 0};
+            uint32_t since = 0;
+            const int h = m.hi[2 * r + t];
+            if (item < items && h >= e0) {
+                const int nblk = (min(h + 1, e0 + PL / 2) - e0 + 3) >> 2;
+                conv_accumulate<4>(acc, P + (2 * r + t) * PL + e0, nblk, W[2 * r + t],
+                                   4 * qi + PL - 1 - e0, since, F);
+            }
+            uint32_t v[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) v[k] = reduce(acc[k], F);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) v[k] = addmod(v[k], __shfl_xor_sync(0xffffffffu, v[k], 1), F);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) v[k] = addmod(v[k], __shfl_xor_sync(0xffffffffu, v[k], 2), F);
+            const int i = 4 * qi + part;  // part k stores output k of the quad
+            if (item < items && i < n[r]) {
+                const uint32_t o = part == 0 ? v[0] : part == 1 ? v[1] : part == 2 ? v[2] : v[3];
+                __stcg(out[r] + xs[r] + i, o);
+            }
+        }
+    }
+}
+
 // CTAs 1..G-1: apply batch j's matrix to this CTA's slice of both operands,
 // S_{j+1} = P_j(S_j), as soon as it is published and S_j is complete.
-__device__ int bulk_cta(const GcdArgs& g, uint32_t* sw, uint32_t* sv, int nbulk, int me) {
-    const FieldParams F = g.F;
-    constexpr int ORG = PL + 8 + 3;
+__device__ int bulk_cta(const GcdArgs& g, uint32_t* sm, int nbulk, int me) {
     __shared__ BatchMeta ms;
     for (int j = 0;; ++j) {
         cta_wait_ge(g.flags + 0, unsigned(j + 1));
@@ -665,26 +890,21 @@ __device__ int bulk_cta(const GcdArgs& g, uint32_t* sw, uint32_t* sv, int nbulk,
             for (int i = 0; i < 4; ++i) ms.hi[i] = vm->hi[i];
         }
         cta_wait_ge(g.flags + 1, unsigned(j) * nbulk);  // S_j complete
+        const long long tb = clock64();
         const BatchMeta m = ms;
         if (m.steps > 0 && !m.err) {
-            const uint32_t* P = g.Pg + (j % RING) * 4 * PL;
             const long long na1 = m.da1 + 1 > 0 ? m.da1 + 1 : 0;
             const long long nb1 = m.db1 + 1 > 0 ? m.db1 + 1 : 0;
             const long long per = (na1 + nb1 + nbulk - 1) / nbulk;
-            const long long s0 = (long long)me * per;
+            const long long s0 = min((long long)me * per, na1 + nb1);
             const long long s1 = min(s0 + per, na1 + nb1);
-            const uint32_t *A0 = g.XA[j % 3], *B0 = g.XB[j % 3];
-            apply_row(g.XA[(j + 1) % 3], min(s0, na1), min(s1, na1), P + 0 * PL, m.hi[0], A0,
-                      m.da0, m.sa, P + 1 * PL, m.hi[1], B0, m.db0, m.sa + m.db0 - m.da0, sw, sv,
-                      ORG, F);
-            apply_row(g.XB[(j + 1) % 3], max(s0 - na1, 0LL), max(s1 - na1, 0LL), P + 2 * PL,
-                      m.hi[2], A0, m.da0, m.sb + m.da0 - m.db0, P + 3 * PL, m.hi[3], B0, m.db0,
-                      m.sb, sw, sv, ORG, F);
+            apply_batch(g, m, g.Pg + (j % RING) * 4 * PL, j, s0, s1, sm);
         }
         __syncthreads();
         if (threadIdx.x == 0) {
             __threadfence();
             atomicAdd(g.flags + 1, 1u);
+            if (g.stats && me == 0) g.stats[7] += clock64() - tb;
         }
         if (m.term || m.err) return j;
     }
@@ -709,7 +929,7 @@ __global__ void __launch_bounds__(GCD_T, 1) gcd_kernel(GcdArgs g) {
     grid.sync();
 
     const int J = blockIdx.x == 0 ? head_cta<MODE>(g, ctl, log, rest, &done, hi_s, nbulk)
-                                  : bulk_cta(g, rest, rest + PL + 8, nbulk, blockIdx.x - 1);
+                                  : bulk_cta(g, rest, nbulk, blockIdx.x - 1);
     // every CTA: wait until the final batch is applied everywhere, then finish
     cta_wait_ge(g.flags + 1, unsigned(J + 1) * nbulk);
     if (threadIdx.x == 0) {
@@ -760,9 +980,8 @@ void launch_gcd(const FieldParams& F, const uint32_t* a, int64_t na, const uint3
         sc.get<uint64_t>(RING * ((sizeof(BatchMeta) + 7) / 8)));
     g.flags = sc.get<unsigned>(2);
     MMM_CUDA(cudaMemsetAsync(g.flags, 0, 2 * sizeof(unsigned), st));
-    constexpr int ORG = PL + 8 + 3;
     const size_t head_words = 2 * W1 + 2 * (W1 + PL) + 4 * PL;
-    const size_t bulk_words = PL + 8 + ORG + GCD_T * GCD_R + GCD_R + 8;
+    const size_t bulk_words = APPLY_WORDS;
     const size_t bytes = (4 * LOGCAP + std::max(head_words, bulk_words)) * 4;
     const int mode = !F.odd ? 2 : (F.p < (1u << 29) ? 0 : 1);
     const void* fn = mode == 0 ? (const void*)gcd_kernel<0>
@@ -776,20 +995,21 @@ void launch_gcd(const FieldParams& F, const uint32_t* a, int64_t na, const uint3
     const bool want_stats = getenv("MMM_GCD_STATS") != nullptr;
     if (const char* d = getenv("MMM_GCD_DEBUG")) g.dbg = atoi(d);
     if (want_stats) {
-        g.stats = sc.get<long long>(6);
-        MMM_CUDA(cudaMemsetAsync(g.stats, 0, 6 * sizeof(long long), st));
+        g.stats = sc.get<long long>(8);
+        MMM_CUDA(cudaMemsetAsync(g.stats, 0, 8 * sizeof(long long), st));
     }
     void* params[] = {&g};
     MMM_CUDA(cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(GCD_T), params, bytes, st));
     check_launch("gcd_kernel");
     if (want_stats) {
-        long long h[6];
+        long long h[8];
         MMM_CUDA(cudaMemcpyAsync(h, g.stats, sizeof(h), cudaMemcpyDeviceToHost, st));
         MMM_CUDA(cudaStreamSynchronize(st));
         fprintf(stderr,
                 "gcd stats: blocks=%d batches=%lld steps=%lld head_publish_cycles=%lld "
-                "head_total_cycles=%lld chain_warp_cycles=%lld\n",
-                blocks, h[0], h[1], h[2], h[3], h[4]);
+                "head_total_cycles=%lld chain_warp_cycles=%lld replay_warp_cycles=%lld "
+                "prefetch_cycles=%lld bulk0_apply_cycles=%lld\n",
+                blocks, h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7]);
     }
 }
 
