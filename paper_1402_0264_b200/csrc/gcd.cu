@@ -53,7 +53,7 @@ constexpr int GE = GCD_GE;         // window words per lane
 constexpr int W1 = 32 * GE;        // window words per operand
 constexpr int PE = GCD_PE;         // matrix words per lane per polynomial
 constexpr int PL = 32 * PE;        // matrix capacity (support < PL)
-constexpr int LOGCAP = 2048;       // steps per matrix batch, hard cap
+constexpr int LOGCAP = 512;        // log entries per batch (<= PL + 1 in practice)
 constexpr int BIG = 1 << 30;       // "validity unbounded": window covers the operand
 
 struct StepLog {
@@ -273,17 +273,27 @@ __device__ void load_top(uint32_t (&w)[GE], const uint32_t* Z, long long& deg, u
 // value: no divergence, no fence).  Single step: (x, y, 0, meta), the
 // dividend u <- y*u - x*v shifted by z.  Fused pair (MODE 0): (alpha, beta,
 // gamma, meta), u <- alpha*u[t+2] + beta*v[t+2] + gamma*v[t+1] shifted by a
-// further z - 2.  meta = seq << 20 | fused << 19 | u_is_a << 18 | z, seq =
-// entry index + 1 publishes it to the replay warps, which poll the entry.
-constexpr unsigned LOG_FUSED = 1u << 19, LOG_UA = 1u << 18, LOG_Z = (1u << 18) - 1;
-__device__ __forceinline__ void log_entry(StepLog* log, int i, uint32_t c0, uint32_t c1,
-                                          uint32_t c2, unsigned meta) {
-    const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(log + i));
-    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(c0), "r"(c1), "r"(c2),
-                 "r"(meta | (unsigned(i + 1) << 20)));
+// further z - 2.  meta = tag << 10 | fused << 9 | u_is_a << 8 | z (z < 256):
+// the 22-bit batch tag publishes the entry to the replay warps, which poll it,
+// and retires older batches' entries without clearing the log (cleared only
+// when the tag wraps).
+constexpr unsigned LOG_FUSED = 1u << 9, LOG_UA = 1u << 8, LOG_Z = 0xFFu;
+constexpr unsigned TAG_MASK = (1u << 22) - 1;
+__device__ __forceinline__ unsigned batch_tag(int j) { return unsigned(j) % TAG_MASK + 1u; }
+// The log is addressed through its 32-bit shared-window base (taken once:
+// converting a generic pointer reads SR_CgaCtaId, a slow S2R, every time).
+__device__ __forceinline__ unsigned log_base(const StepLog* log) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(const_cast<StepLog*>(log)));
 }
-__device__ __forceinline__ uint4 log_get(const StepLog* log, int i) {
-    const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(const_cast<StepLog*>(log + i)));
+__device__ __forceinline__ unsigned log_seq(int /*i*/, unsigned tag) { return tag; }
+__device__ __forceinline__ void log_entry(unsigned lb, int i, unsigned par, uint32_t c0, uint32_t c1,
+                                          uint32_t c2, unsigned meta) {
+    const unsigned a = lb + unsigned(i) * 16u;
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(c0), "r"(c1), "r"(c2),
+                 "r"(meta | (log_seq(i, par) << 10)));
+}
+__device__ __forceinline__ uint4 log_get(unsigned lb, int i) {
+    const unsigned a = lb + unsigned(i) * 16u;
     uint4 v;
     asm volatile("ld.volatile.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
                  : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
@@ -429,8 +439,9 @@ __device__ __forceinline__ bool fused_fast(uint32_t (&u)[GE], const uint32_t (&v
 // the bounds are refreshed (pessimistically) only when F runs out or after a
 // slow step.  Role rule, termination: oracle.cpp:58-66, 74-75; gcd.cpp:191-199.
 template <int MODE>
-__device__ void run_chain(BatchMeta& c, StepLog* log, volatile int* done, int M, Fld f,
+__device__ void run_chain(BatchMeta& c, StepLog* log, volatile int* done, int jb, int M, Fld f,
                           const uint32_t* winA, const uint32_t* winB) {
+    const unsigned par = batch_tag(jb);
     using A = Arith<MODE>;
     const uint32_t p = f.p;
     const int lane = threadIdx.x & 31;
@@ -450,6 +461,7 @@ __device__ void run_chain(BatchMeta& c, StepLog* log, volatile int* done, int M,
     int sup = 0;  // max matrix support (pessimistic)
     int dividend_a = c.dividend_a;
     const int cap = min(M, LOGCAP);
+    const unsigned lb = log_base(log);
     int steps = 0, n = 0, term = 0, F = 0, F0 = 0;
     for (;;) {
         // oracle role rule: reduce the dividend while deg(dividend) >= deg(divisor)
@@ -470,21 +482,32 @@ __device__ void run_chain(BatchMeta& c, StepLog* log, volatile int* done, int M,
             F0 = F;
         }
         if (MODE == 0) {
-            // steady state: degree-1 quotients, roles alternating every pair
-            while (F >= 2) {
-                const bool a_div = dividend_a != 0;
-                const int du = a_div ? da : db, dv = a_div ? db : da;
-                if (du != dv + 1 || dv < 1) break;
-                uint32_t al, be, ga;
-                const bool ok = a_div ? fused_fast(wa, wb, ha, ha1, hb, hb1, f, al, be, ga)
-                                      : fused_fast(wb, wa, hb, hb1, ha, ha1, f, al, be, ga);
-                if (!ok) break;
-                if (a_div) da -= 2;
-                else db -= 2;
+            // steady state: degree-1 quotients, roles alternating every pair;
+            // straight-line A-then-B pairs (a taken branch costs ~20 cycles)
+            uint32_t al, be, ga;
+            if (!dividend_a && F >= 2 && db == da + 1 && da >= 1 &&
+                fused_fast(wb, wa, hb, hb1, ha, ha1, f, al, be, ga)) {  // align to A
+                db -= 2;
                 F -= 2;
                 steps += 2;
-                log_entry(log, n++, al, be, ga, LOG_FUSED | (a_div ? LOG_UA : 0u) | 2u);
-                dividend_a = !a_div;
+                log_entry(lb, n++, par, al, be, ga, LOG_FUSED | 2u);
+                dividend_a = 1;
+            }
+            if (dividend_a) {
+                while (F >= 4 && da == db + 1 && db >= 2) {
+                    if (!fused_fast(wa, wb, ha, ha1, hb, hb1, f, al, be, ga)) break;
+                    da -= 2;
+                    F -= 2;
+                    steps += 2;
+                    log_entry(lb, n++, par, al, be, ga, LOG_FUSED | LOG_UA | 2u);
+                    dividend_a = 0;  // now db == da + 1, da >= 1
+                    if (!fused_fast(wb, wa, hb, hb1, ha, ha1, f, al, be, ga)) break;
+                    db -= 2;
+                    F -= 2;
+                    steps += 2;
+                    log_entry(lb, n++, par, al, be, ga, LOG_FUSED | 2u);
+                    dividend_a = 1;
+                }
             }
             if (F <= 0) continue;  // refresh first
         }
@@ -515,7 +538,7 @@ __device__ void run_chain(BatchMeta& c, StepLog* log, volatile int* done, int M,
                     F = 0;
                     F0 = 0;
                 }
-                log_entry(log, n++, al, be, ga,
+                log_entry(lb, n++, par, al, be, ga,
                           LOG_FUSED | (dividend_a ? LOG_UA : 0u) | unsigned(z));
                 steps += 2;
                 if (stop) break;
@@ -535,7 +558,7 @@ __device__ void run_chain(BatchMeta& c, StepLog* log, volatile int* done, int M,
             F = 0;
             F0 = 0;
         }
-        log_entry(log, n++, x, y, 0u, (dividend_a ? LOG_UA : 0u) | unsigned(z));
+        log_entry(lb, n++, par, x, y, 0u, (dividend_a ? LOG_UA : 0u) | unsigned(z));
         ++steps;
         if (stop) break;
     }
@@ -549,11 +572,22 @@ __device__ void run_chain(BatchMeta& c, StepLog* log, volatile int* done, int M,
         c.dividend_a = dividend_a;
         c.sa = da0 - (da < 0 ? da0 : da);  // top moves (unused for a vanished row)
         c.sb = db0 - (db < 0 ? db0 : db);
-        st_release_cta(done, n + 1);  // done = final entry count + 1
+        st_release_cta(done, int((par << 10) | unsigned(n + 1)));  // batch tag | entry count + 1
     }
 }
 
 // One log entry applied to a matrix row: u (the dividend's row) from u, v.
+// Fused pair with no extra shift (the steady state): straight-line.
+__device__ __forceinline__ void replay_fused2(uint32_t (&u)[PE], const uint32_t (&v)[PE],
+                                              const uint4& en, Fld f) {
+    uint32_t us2[PE], vs2[PE], vs1[PE];
+    shr_copy<2>(u, us2);
+    shr_copy<2>(v, vs2);
+    shr_copy<1>(v, vs1);
+#pragma unroll
+    for (int e = 0; e < PE; ++e) u[e] = Arith<0>::comb3(en.x, us2[e], en.y, vs2[e], en.z, vs1[e], f);
+}
+
 template <int MODE>
 __device__ __forceinline__ void replay_entry(uint32_t (&u)[PE], const uint32_t (&v)[PE],
                                              const uint4& en, Fld f) {
@@ -583,8 +617,14 @@ __device__ __forceinline__ void replay_entry(uint32_t (&u)[PE], const uint32_t (
 // entry reduces); the next entry is fetched while one is applied.  Then
 // publish the column (canonical) to Pg and Ps.
 template <int MODE>
-__device__ void run_replay(int col, const StepLog* log, volatile int* done, Fld f, uint32_t* Pg,
-                           uint32_t* Ps, int* hi_out) {
+__device__ void run_replay(int col, const StepLog* log, volatile int* done, int jb, Fld f,
+                           uint32_t* Pg, uint32_t* Ps, int* hi_out) {
+    const unsigned par = batch_tag(jb);
+    // the chain finished this batch with fewer than i + 1 entries
+    auto ended = [&](int i) {
+        const unsigned d = unsigned(ld_acquire_cta(done));
+        return (d >> 10) == par && int(d & 0x3FFu) - 1 <= i;
+    };
     using A = Arith<MODE>;
     const uint32_t p = f.p;
     const int lane = threadIdx.x & 31;
@@ -596,15 +636,43 @@ __device__ void run_replay(int col, const StepLog* log, volatile int* done, Fld 
         else rb[0] = 1u;
     }
     int ha = col == 0 ? 0 : -1, hb = col == 0 ? -1 : 0;  // support bounds
-    uint4 en = log_get(log, 0);
-    for (int i = 0;; ++i) {
-        while ((en.w >> 20) != unsigned(i + 1)) {
-            const int d = ld_acquire_cta(done);
-            if (d != 0 && d - 1 <= i) break;  // chain finished with i entries
-            en = log_get(log, i);  // spin: warps 1-2 do not share the chain's SMSP
+    constexpr unsigned KIND = LOG_FUSED | LOG_UA | LOG_Z;
+    const unsigned lb = log_base(log);
+    const int last = LOGCAP - 1;
+    int i = 0;
+    uint4 en = log_get(lb, 0), nx = log_get(lb, 1);
+    for (;;) {
+        if (MODE == 0) {
+            // steady state: published A pair then B pair, applied straight-line
+            // with the next two entries already in flight (one taken branch)
+            while ((en.w >> 10) == log_seq(i, par) && (nx.w >> 10) == log_seq(i + 1, par) &&
+                   (en.w & KIND) == (LOG_FUSED | LOG_UA | 2u) &&
+                   (nx.w & KIND) == (LOG_FUSED | 2u)) {
+                const uint4 n2 = log_get(lb, min(i + 2, last)), n3 = log_get(lb, min(i + 3, last));
+                replay_fused2(ra, rb, en, f);
+                replay_fused2(rb, ra, nx, f);
+                const int h1 = max(ha, hb) >= 0 ? max(ha, hb) + 2 : -1;
+                ha = h1;
+                hb = h1 >= 0 ? max(h1, hb) + 2 : -1;
+                en = n2;
+                nx = n3;
+                i += 2;
+            }
         }
-        if ((en.w >> 20) != unsigned(i + 1)) break;
-        const uint4 nx = log_get(log, min(i + 1, LOGCAP - 1));  // prefetch (may be unpublished)
+        while ((en.w >> 10) != log_seq(i, par)) {
+            if (ended(i)) break;
+            en = log_get(lb, i);  // spin: warps 1-2 do not share the chain's SMSP
+        }
+        if ((en.w >> 10) != log_seq(i, par)) break;
+        if (MODE == 0 && (en.w & KIND) == (LOG_FUSED | LOG_UA | 2u) &&
+            (nx.w >> 10) != log_seq(i + 1, par)) {
+            // a steady A pair whose partner is not yet published: wait for it
+            while ((nx.w >> 10) != log_seq(i + 1, par)) {
+                if (ended(i + 1)) break;
+                nx = log_get(lb, min(i + 1, last));
+            }
+            if ((nx.w >> 10) == log_seq(i + 1, par) && (nx.w & KIND) == (LOG_FUSED | 2u)) continue;
+        }
         const int z = int(en.w & LOG_Z), hmax = max(ha, hb);
         if (en.w & LOG_UA) {
             replay_entry<MODE>(ra, rb, en, f);
@@ -613,7 +681,9 @@ __device__ void run_replay(int col, const StepLog* log, volatile int* done, Fld 
             replay_entry<MODE>(rb, ra, en, f);
             hb = hmax >= 0 ? hmax + z : -1;
         }
-        en = nx;
+        ++i;
+        en = (nx.w >> 10) == log_seq(i, par) ? nx : log_get(lb, min(i, last));
+        nx = log_get(lb, min(i + 1, last));
     }
     uint32_t* Pa = Pg + (0 * 2 + col) * PL;  // row A, column col
     uint32_t* Pb = Pg + (1 * 2 + col) * PL;  // row B, column col
@@ -622,8 +692,9 @@ __device__ void run_replay(int col, const StepLog* log, volatile int* done, Fld 
         const uint32_t va = A::canon(ra[e], p), vb = A::canon(rb[e], p);
         __stcg(Pa + e * 32 + lane, va);
         __stcg(Pb + e * 32 + lane, vb);
-        Ps[(0 * 2 + col) * PL + e * 32 + lane] = va;  // the window builder's copy
-        Ps[(1 * 2 + col) * PL + e * 32 + lane] = vb;
+        // the window builder's copy, index-reversed (a correlation run as convolution)
+        Ps[(0 * 2 + col) * PL + (PL - 1) - (e * 32 + lane)] = va;
+        Ps[(1 * 2 + col) * PL + (PL - 1) - (e * 32 + lane)] = vb;
     }
     if (lane == 0) {
         hi_out[0 * 2 + col] = min(ha, PL - 1);
@@ -642,10 +713,12 @@ __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
 __device__ __forceinline__ void st_release_gpu(unsigned* p, unsigned v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-// Thread 0 waits until *p >= target; the CTA then proceeds together.
+// Thread 0 waits until *p >= target; the CTA then proceeds together.  A pure
+// spin: one L2 round trip in flight per CTA, and no sleep wake-up delay.
 __device__ __forceinline__ void cta_wait_ge(const unsigned* p, unsigned target) {
     if (threadIdx.x == 0)
-        while (ld_acquire_gpu(p) < target) __nanosleep(64);
+        while (ld_acquire_gpu(p) < target) {
+        }
     __syncthreads();
 }
 
@@ -668,46 +741,53 @@ __device__ void load_top_region(uint32_t* top, const uint32_t* Z, long long deg,
     }
 }
 
-// win[t] = sum_e P1[e] topA[t+e] + sum_e P2[e] topB[t+e], t < W1: the next
-// batch's top-aligned window computed locally from the previous state.
-__device__ void build_window(uint32_t* win, const uint32_t* P1, int h1, const uint32_t* P2, int h2,
-                             const uint32_t* topA, const uint32_t* topB, int t,
-                             const FieldParams& F) {
-    uint64_t acc = 0;
+// Both next windows, top-aligned, from S_j's top region and the batch matrix:
+//   winA[t] = sum_e Pa1[e] topA[t+e] + sum_e Pa2[e] topB[t+e]   (t < W1)
+// and winB likewise with Pb1, Pb2.  Ps holds each polynomial index-reversed
+// (Ps[c][PL-1-e] = P_c[e]), so with u = PL-1-e the sum is the convolution
+// conv_accumulate computes.  Work item = (window, 4 consecutive words, one
+// of BUILD_PARTS parts: term x slice of the support), parts in adjacent
+// lanes meeting in a butterfly.  IMAD.WIDE issues at one warp-instruction per
+// SM-cycle, so the 2*W1*2*PL MACs cost ~W1*PL/8 cycles however they are split;
+// fewer, longer parts spend less on the reduction (ncu: ~9.6 cycles/instr).
+constexpr int BUILD_PARTS = 4;
+constexpr int BUILD_ITEMS = 2 * (W1 / 4) * BUILD_PARTS;  // 128: warps 0-3
+__device__ void build_window_item(int item, uint32_t* winA, uint32_t* winB, const uint32_t* Ps,
+                                  const int* hi, const uint32_t* topA, const uint32_t* topB,
+                                  const FieldParams& F) {
+    constexpr int SPAN = 2 * PL / BUILD_PARTS;  // terms per part
+    const int part = item % BUILD_PARTS, q = (item / BUILD_PARTS) % (W1 / 4);
+    const int w = item / (BUILD_PARTS * (W1 / 4));
+    const int term = part / (BUILD_PARTS / 2), u0 = (part % (BUILD_PARTS / 2)) * SPAN;
+    const int c = 2 * w + term;  // Pa1, Pa2, Pb1, Pb2
+    uint64_t acc[4] = {0, 0, 0, 0};
     uint32_t since = 0;
-    const uint32_t ft = F.fold_terms;
-#pragma unroll 1
-    for (int half = 0; half < 2; ++half) {
-        const uint32_t* P = half ? P2 : P1;
-        const uint32_t* Z = (half ? topB : topA) + t;
-        const int n = (half ? h2 : h1) + 1;
-        int e = 0;
-        if (ft >= 16) {
-            for (; e + 8 <= n; e += 8) {
-                if (since + 8 > ft) {
-                    acc = fold(acc, F);
-                    since = 0;
-                }
-                since += 8;
+    // reversed support: u in [PL-1-hi, PL-1]
+    if (hi[c] >= 0 && u0 + SPAN - 1 >= PL - 1 - hi[c])
+        conv_accumulate<4>(acc, Ps + c * PL + u0, SPAN / 4, term ? topB : topA,
+                           4 * q + PL - 1 - u0, since, F);
+    uint32_t v[4];
 #pragma unroll
-                for (int k = 0; k < 8; ++k) acc = mad_wide(P[e + k], Z[e + k], acc);
-            }
-        }
-        for (; e < n; ++e) {
-            if (++since > ft) {
-                acc = fold(acc, F);
-                since = 1;
-            }
-            acc = mad_wide(P[e], Z[e], acc);
-        }
-    }
-    win[t] = reduce(acc, F);
+    for (int k = 0; k < 4; ++k) v[k] = reduce(acc[k], F);
+#pragma unroll
+    for (int d = 1; d < BUILD_PARTS; d <<= 1)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) v[k] = addmod(v[k], __shfl_xor_sync(0xffffffffu, v[k], d), F);
+    const uint32_t o = part == 0 ? v[0] : part == 1 ? v[1] : part == 2 ? v[2] : v[3];
+    (w ? winB : winA)[4 * q + part] = o;  // part k stores word k of the quad
 }
 
-// CTA 0: the sequential part.  Per batch: chain (warp 0) || replay (warps 1-2)
-// || prefetch of the previous state's top region (warps 3-7); publish the
-// matrix; build the next windows from it.  Never waits for the bulk of the
-// batch it just finished (only for the one before, which had a whole batch).
+// Named barrier over the first n threads' warps (n a multiple of 32).
+__device__ __forceinline__ void bar_sync(int id, int n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+// CTA 0: the sequential part.  Per batch j: chain (warp 0) || replay (warps
+// 1-2) || prefetch of S_j's top region (warps 3-7); then warp 7 publishes
+// the matrix (its fence waits for the stores to reach L2) while warps 0-6
+// build the next windows from it.  Never waits for the bulk of the batch it
+// just finished (only for the one before, which had a whole batch).
+constexpr int BUILDERS = GCD_T - 32;  // warps 0-6
 template <int MODE>
 __device__ int head_cta(const GcdArgs& g, BatchMeta& ctl, StepLog* log, uint32_t* smem_rest,
                         volatile int* done, int* hi_s, int nbulk) {
@@ -719,6 +799,12 @@ __device__ int head_cta(const GcdArgs& g, BatchMeta& ctl, StepLog* log, uint32_t
     uint32_t* topB = topA + W1 + PL;
     uint32_t* Ps = topB + W1 + PL;      // 4 * PL
     __shared__ int fallback;
+    __shared__ long long da0s[2], db0s[2];  // batch start degrees, by batch parity
+    __shared__ long long hst[10];  // MMM_GCD_STATS: accumulated here, flushed at the end
+    if (threadIdx.x < 10) hst[threadIdx.x] = 0;
+    if (threadIdx.x == 0) *done = 0;
+    for (int i = threadIdx.x; i < LOGCAP; i += GCD_T)  // no stale tags from earlier kernels
+        reinterpret_cast<uint4*>(log)[i] = make_uint4(0u, 0u, 0u, 0u);
     if (warp == 0) {
         long long da = g.na - 1, db = g.nb - 1;
         window_from_global<MODE>(winA, g.XA[0], da, F.p);
@@ -727,68 +813,82 @@ __device__ int head_cta(const GcdArgs& g, BatchMeta& ctl, StepLog* log, uint32_t
             ctl.da1 = da;
             ctl.db1 = db;
             ctl.dividend_a = 1;  // oracle_gcd: x = a is the first dividend (oracle.cpp:70)
+            da0s[0] = da;
+            db0s[0] = db;
         }
     }
     __syncthreads();
+    long long t0 = clock64();
     for (int j = 0;; ++j) {
-        const long long t0 = clock64();
-        for (int i = threadIdx.x; i < LOGCAP; i += GCD_T)
-            reinterpret_cast<uint4*>(log)[i] = make_uint4(0u, 0u, 0u, 0u);
-        if (threadIdx.x == 0) *done = 0;
-        const long long da0 = ctl.da1, db0 = ctl.db1;
-        __syncthreads();
         if (warp == 0) {
-            run_chain<MODE>(ctl, log, done, g.M, Fld{F.p, F.pinv}, winA, winB);
-            if (g.stats && threadIdx.x == 0) g.stats[4] += clock64() - t0;
+            run_chain<MODE>(ctl, log, done, j, g.M, Fld{F.p, F.pinv}, winA, winB);
+            if (g.stats && threadIdx.x == 0) hst[4] += clock64() - t0;
         } else if (warp <= 2) {
-            run_replay<MODE>(warp - 1, log, done, Fld{F.p, F.pinv}, g.Pg + (j % RING) * 4 * PL,
-                             Ps, hi_s);
-            if (g.stats && threadIdx.x == 32) g.stats[5] += clock64() - t0;
+            run_replay<MODE>(warp - 1, log, done, j, Fld{F.p, F.pinv},
+                             g.Pg + (j % RING) * 4 * PL, Ps, hi_s);
+            if (g.stats && threadIdx.x == 32) hst[5] += clock64() - t0;
         } else {
             // prefetch: S_j complete once the bulk applied batch j-1
             if (threadIdx.x == 96)
-                while (ld_acquire_gpu(g.flags + 1) < unsigned(j) * nbulk) __nanosleep(64);
-            asm volatile("bar.sync 1, 160;" ::: "memory");  // warps 3-7
+                while (ld_acquire_gpu(g.flags + 1) < unsigned(j) * nbulk) {
+                }
+            bar_sync(1, GCD_T - 96);  // warps 3-7 (warp 7 may come from its publish)
+            const long long da0 = da0s[j & 1], db0 = db0s[j & 1];
             for (int i = threadIdx.x - 96; i < W1 + PL; i += GCD_T - 96) {
                 const long long xa = da0 - i, xb = db0 - i;
                 topA[i] = (xa >= 0) ? __ldcg(g.XA[j % 3] + xa) : 0u;
                 topB[i] = (xb >= 0) ? __ldcg(g.XB[j % 3] + xb) : 0u;
             }
-            if (g.stats && threadIdx.x == 96) g.stats[6] += clock64() - t0;
+            if (g.stats && threadIdx.x == 96) hst[6] += clock64() - t0;
         }
         __syncthreads();
+        if (g.stats && threadIdx.x == 0) hst[2] += clock64() - t0;
         BatchMeta m = ctl;
-        m.da0 = da0;
-        m.db0 = db0;
+        m.da0 = da0s[j & 1];
+        m.db0 = db0s[j & 1];
         for (int i = 0; i < 4; ++i) m.hi[i] = hi_s[i];
         m.err = (m.steps == 0 && m.term == 0) ? 1 : 0;
-        if (threadIdx.x == 0) {
-            g.meta[j % RING] = m;
-            __threadfence();
-            st_release_gpu(g.flags + 0, unsigned(j + 1));
-            if (g.stats) {
-                g.stats[0] += 1;
-                g.stats[1] += m.steps;
-                g.stats[2] += clock64() - t0;
+        const bool last = m.term || m.err;
+        if (warp == 7) {  // publish batch j
+            if (threadIdx.x == 224) {
+                g.meta[j % RING] = m;
+                __threadfence();
+                st_release_gpu(g.flags + 0, unsigned(j + 1));
+                if (g.stats) {
+                    hst[0] += 1;
+                    hst[1] += m.steps;
+                }
             }
+            if (last) {
+                __syncthreads();  // with warps 0-6 (same branch): hst complete
+                if (g.stats && threadIdx.x == 224)
+                    for (int i = 0; i < 10; ++i) g.stats[i == 7 ? 8 : (i == 8 ? 9 : (i == 9 ? 10 : i))] = hst[i];
+                return j;
+            }
+            continue;  // next batch: prefetch group
         }
-        if (m.term || m.err) return j;
-        // next windows, top-aligned, from S_j and the batch matrix
-        const int t = threadIdx.x & (W1 - 1);
-        if (threadIdx.x < W1)
-            build_window(winA, Ps + 0 * PL, m.hi[0], Ps + 1 * PL, m.hi[1], topA, topB, t, F);
-        else if (threadIdx.x < 2 * W1)
-            build_window(winB, Ps + 2 * PL, m.hi[2], Ps + 3 * PL, m.hi[3], topA, topB, t, F);
+        if (last) {
+            __syncthreads();
+            return j;
+        }
+        // warps 0-6: next windows, top-aligned, from S_j and the batch matrix
+        if (threadIdx.x < BUILD_ITEMS)
+            build_window_item(threadIdx.x, winA, winB, Ps, hi_s, topA, topB, F);
         if (threadIdx.x == 0) fallback = 0;
-        __syncthreads();
+        if (g.stats && threadIdx.x == 0) hst[7] += clock64() - t0;
+        bar_sync(2, BUILDERS);
+        if (g.stats && threadIdx.x == 0) hst[8] += clock64() - t0;
         // the bound after the batch is not the lead (degree dropped past the
         // valid words): take the exact state from the bulk instead
         if (threadIdx.x == 0 &&
             ((m.da1 >= 0 && winA[0] == 0u) || (m.db1 >= 0 && winB[0] == 0u)))
             fallback = 1;
-        __syncthreads();
+        bar_sync(2, BUILDERS);
         if (fallback) {
-            cta_wait_ge(g.flags + 1, unsigned(j + 1) * nbulk);
+            if (threadIdx.x == 0)
+                while (ld_acquire_gpu(g.flags + 1) < unsigned(j + 1) * nbulk) {
+                }
+            bar_sync(2, BUILDERS);
             if (warp == 0) {
                 long long da = m.da1, db = m.db1;
                 window_from_global<MODE>(winA, g.XA[(j + 1) % 3], da, F.p);
@@ -798,9 +898,22 @@ __device__ int head_cta(const GcdArgs& g, BatchMeta& ctl, StepLog* log, uint32_t
                     ctl.db1 = db;
                 }
             }
-            __syncthreads();
+            bar_sync(2, BUILDERS);
         }
-        if (g.stats && threadIdx.x == 0) g.stats[3] += clock64() - t0;
+        if (threadIdx.x == 0) {
+            da0s[(j + 1) & 1] = ctl.da1;  // read by the prefetch after its barrier
+            db0s[(j + 1) & 1] = ctl.db1;
+        }
+        if (unsigned(j + 1) % TAG_MASK == 0u)  // tag wraps (2^22 batches): clear the log
+            for (int i = threadIdx.x; i < LOGCAP; i += BUILDERS)
+                reinterpret_cast<uint4*>(log)[i] = make_uint4(0u, 0u, 0u, 0u);
+        if (g.stats && threadIdx.x == 0) {
+            const long long t1 = clock64();
+            hst[3] += t1 - t0;
+            t0 = t1;
+        }
+        bar_sync(2, BUILDERS);  // windows, da0s/db0s ready for the next chain
+        if (g.stats) t0 = clock64();
     }
 }
 
@@ -813,6 +926,9 @@ __device__ int head_cta(const GcdArgs& g, BatchMeta& ctl, StepLog* log, uint32_t
 // the register-tiled conv_accumulate<4>, and the 4 quarters (adjacent lanes)
 // meet in a two-level butterfly.  (gcd.cpp:252-300 UpdateMatrix apply.)
 constexpr int APPLY_OUT = GCD_T;  // outputs per pass: one work item per thread
+#ifndef GCD_OUT_PER_CTA
+#define GCD_OUT_PER_CTA 128  // target outputs per bulk CTA (grid size)
+#endif
 constexpr int APPLY_WORDS = 4 * PL + 2 * (APPLY_OUT + 8) + 4 * (PL + 4);
 
 __device__ void apply_batch(const GcdArgs& g, const BatchMeta& m, const uint32_t* Pglob, int j,
@@ -880,6 +996,7 @@ __device__ void apply_batch(const GcdArgs& g, const BatchMeta& m, const uint32_t
 // S_{j+1} = P_j(S_j), as soon as it is published and S_j is complete.
 __device__ int bulk_cta(const GcdArgs& g, uint32_t* sm, int nbulk, int me) {
     __shared__ BatchMeta ms;
+    long long apply_cycles = 0;  // MMM_GCD_STATS (bulk CTA 0, thread 0)
     for (int j = 0;; ++j) {
         cta_wait_ge(g.flags + 0, unsigned(j + 1));
         if (threadIdx.x == 0) {
@@ -889,7 +1006,10 @@ __device__ int bulk_cta(const GcdArgs& g, uint32_t* sm, int nbulk, int me) {
             ms.sa = vm->sa; ms.sb = vm->sb;
             for (int i = 0; i < 4; ++i) ms.hi[i] = vm->hi[i];
         }
-        cta_wait_ge(g.flags + 1, unsigned(j) * nbulk);  // S_j complete
+        // S_j is complete without a poll: CTA 0 acquired flags[1] >= j * nbulk
+        // (its prefetch) before the bar.sync preceding this batch's release of
+        // flags[0], and no bulk CTA can finish batch j before that release.
+        __syncthreads();  // ms
         const long long tb = clock64();
         const BatchMeta m = ms;
         if (m.steps > 0 && !m.err) {
@@ -904,9 +1024,12 @@ __device__ int bulk_cta(const GcdArgs& g, uint32_t* sm, int nbulk, int me) {
         if (threadIdx.x == 0) {
             __threadfence();
             atomicAdd(g.flags + 1, 1u);
-            if (g.stats && me == 0) g.stats[7] += clock64() - tb;
+            apply_cycles += clock64() - tb;
         }
-        if (m.term || m.err) return j;
+        if (m.term || m.err) {
+            if (g.stats && me == 0 && threadIdx.x == 0) g.stats[7] = apply_cycles;
+            return j;
+        }
     }
 }
 
@@ -990,26 +1113,28 @@ void launch_gcd(const FieldParams& F, const uint32_t* a, int64_t na, const uint3
     int per_sm = 0;
     MMM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, GCD_T, bytes));
     if (per_sm < 1) throw Error(ST_INVALID, "gcd: kernel does not fit an SM");
-    const int64_t want = std::max<int64_t>(2, 1 + ceil_div(na + nb, 256));
-    const int blocks = int(std::min<int64_t>(want, int64_t(sm_count()) * per_sm));
+    const int64_t want = std::max<int64_t>(2, 1 + ceil_div(na + nb, GCD_OUT_PER_CTA));
+    // one CTA per SM: a second CTA on the head's SM would take issue slots from the chain
+    const int blocks = int(std::min<int64_t>(want, int64_t(sm_count())));
     const bool want_stats = getenv("MMM_GCD_STATS") != nullptr;
     if (const char* d = getenv("MMM_GCD_DEBUG")) g.dbg = atoi(d);
     if (want_stats) {
-        g.stats = sc.get<long long>(8);
-        MMM_CUDA(cudaMemsetAsync(g.stats, 0, 8 * sizeof(long long), st));
+        g.stats = sc.get<long long>(12);
+        MMM_CUDA(cudaMemsetAsync(g.stats, 0, 12 * sizeof(long long), st));
     }
     void* params[] = {&g};
     MMM_CUDA(cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(GCD_T), params, bytes, st));
     check_launch("gcd_kernel");
     if (want_stats) {
-        long long h[8];
+        long long h[12];
         MMM_CUDA(cudaMemcpyAsync(h, g.stats, sizeof(h), cudaMemcpyDeviceToHost, st));
         MMM_CUDA(cudaStreamSynchronize(st));
         fprintf(stderr,
-                "gcd stats: blocks=%d batches=%lld steps=%lld head_publish_cycles=%lld "
+                "gcd stats: blocks=%d batches=%lld steps=%lld phase_end_cycles=%lld "
                 "head_total_cycles=%lld chain_warp_cycles=%lld replay_warp_cycles=%lld "
-                "prefetch_cycles=%lld bulk0_apply_cycles=%lld\n",
-                blocks, h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7]);
+                "prefetch_cycles=%lld bulk0_apply_cycles=%lld builder_own_done=%lld "
+                "builders_synced=%lld\n",
+                blocks, h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7], h[8], h[9]);
     }
 }
 

@@ -57,21 +57,21 @@ __global__ void bench(const uint32_t* rnd, long long* out, uint32_t* Pg, int bat
         }
         __syncthreads();
         long long t0 = clock64();
-        if (warp == 0) run_chain<0>(c, log, &done, 1 << 20, Fld{F.p, F.pinv}, winA, winB);
+        if (warp == 0) run_chain<0>(c, log, &done, bt, 1 << 20, Fld{F.p, F.pinv}, winA, winB);
         __syncthreads();
         cycles += clock64() - t0;
         steps += c.steps;
-        entries += done - 1;
+        entries += (done & 0x3FF) - 1;
         if (warp == 1) {
             const long long r0 = clock64();
-            run_replay<0>(0, log, &done, Fld{F.p, F.pinv}, Pg, Ps, hi);
+            run_replay<0>(0, log, &done, bt, Fld{F.p, F.pinv}, Pg, Ps, hi);
             __syncwarp();
             rcycles += clock64() - r0;
         } else if (warp == 2) {
-            run_replay<0>(1, log, &done, Fld{F.p, F.pinv}, Pg, Ps, hi);
+            run_replay<0>(1, log, &done, bt, Fld{F.p, F.pinv}, Pg, Ps, hi);
         }
         __syncthreads();
-        if (warp == 1) pcycles += replay_plain<0>(0, log, done - 1, Fld{F.p, F.pinv}, Pg + 256);
+        if (warp == 1) pcycles += replay_plain<0>(0, log, (done & 0x3FF) - 1, Fld{F.p, F.pinv}, Pg + 256);
         __syncthreads();
         if (threadIdx.x == 0 && bt == batches - 1) {
             out[4] = hi[0]; out[5] = hi[1]; out[6] = hi[2]; out[7] = hi[3];
