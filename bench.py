@@ -258,13 +258,31 @@ class GcdWork(Workload):
                 "frac": achieved / hbm, "traffic": None, "kernel": "gcd_kernel",
                 "alg_bytes_per_launch": alg,
                 "binding": f"dependency chain: {self.steps_} sequential eliminations, "
-                           f"{t_step / self.steps_ * 1e9:.1f} ns per elimination"}
+                           f"{t_step / self.steps_ * 1e9:.1f} ns per elimination",
+                "chain": chain_model(t_step, self.steps_)}
 
     def cpu_ref(self, orc):
         """(callable, coeff-ops per call, checker, sample description)."""
         a, b = self.a.astype(np.int64), self.b.astype(np.int64)
         return (lambda: orc.gcd(a, b, P), self.units(),
                 lambda out: digest(out) == self.want, "full instance (oracle_gcd)")
+
+
+def chain_model(t_step, steps, mhz=1965.0):
+    """The GCD's real bound: its critical path.  A fused pair of eliminations
+    (gcd.cu fused_fast) costs at least comb (lead of the first step) + neg /
+    canonicalise + 3-term comb + lead broadcast and test, in dependent-chain
+    cycles measured by tools/latency.cu (profiles/latency_r1.json)."""
+    try:
+        lat = json.load(open(os.path.join(ROOT, "profiles", "latency_r1.json")))
+    except (OSError, ValueError):
+        return None
+    pair = lat["lazy_redc_comb"] + 8.0 + lat["comb3_chain"] + lat["shfl_bcast_cmp_branch"]
+    floor_ns = pair / 2.0 / mhz * 1e3
+    got_ns = t_step / steps * 1e9
+    return {"ns_per_elimination": got_ns, "floor_ns_per_elimination": floor_ns,
+            "frac": floor_ns / got_ns, "floor_cycles_per_pair": pair, "sm_mhz": mhz,
+            "source": "profiles/latency_r1.json (tools/latency.cu)"}
 
 
 def _dev(x):
@@ -742,6 +760,8 @@ def run_ours(args, dist):
             "data": "synthetic (seeded mt19937_64 inputs, reference random_poly draws)",
             "config": work.config, "impl": "ours", "e2e": e2e, "roofline": roof,
             "gpu_launches": launches, "clocks": clk.summary()}
+    if roof.get("chain") and line["clocks"].get("sm_mhz"):  # at the clock actually run
+        roof["chain"] = chain_model(t_step, work.steps_, float(line["clocks"]["sm_mhz"]))
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(work, args.cpu_seconds)
     return line

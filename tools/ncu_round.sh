@@ -1,10 +1,20 @@
+# tools/ncu_round.sh TAG -- bench lines for every workload, the launch list of
+# the default bench command (after that command exited 0 without ncu), and one
+# `ncu --set full` capture per workload's dominant kernel (after the plain run
+# exited 0).  Outputs under gpurun_out/TAG; summarise with
+#   python tools/ncu_summary.py gpurun_out/TAG profiles/TAG
 set -x
-mkdir -p gpurun_out/r1
-python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/r1/bench_plain.log 2>&1 && \
-ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/r1/launches_gcd.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/r1/ncu_launch.log 2>&1
+T=${1:-r1}
+O=gpurun_out/$T
+mkdir -p $O
+for w in gcd mul div ntt ntt_batch batch; do
+  timeout 300 python bench.py --workload $w --steps 10 --warmup 3 > $O/bench_$w.log 2>&1
+done
+timeout 300 python bench.py --steps 3 --warmup 3 --no-cpu-baseline > $O/bench_plain.log 2>&1 && \
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_gcd.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline > $O/ncu_launch.log 2>&1
 for w in gcd mul div ntt batch; do
   case $w in gcd) k=gcd_kernel;; mul) k=mul_kernel;; div) k=div_grid_kernel;; ntt) k=ntt_rows;; batch) k=div_cta_kernel;; esac
-  python tools/prof_one.py $w --reps 1 > gpurun_out/r1/plain_$w.log 2>&1 && \
-  timeout 600 ncu --set full --import-source on --clock-control none -k regex:$k -c 1 -o gpurun_out/r1/full_$w python tools/prof_one.py $w --reps 1 > gpurun_out/r1/ncu_$w.log 2>&1
-  tail -1 gpurun_out/r1/ncu_$w.log
+  timeout 120 python tools/prof_one.py $w --reps 1 > $O/plain_$w.log 2>&1 && \
+  timeout 600 ncu --set full --import-source on --clock-control none -k regex:$k -c 1 -o $O/full_$w python tools/prof_one.py $w --reps 1 > $O/ncu_$w.log 2>&1
+  tail -1 $O/ncu_$w.log
 done
