@@ -297,9 +297,14 @@ def _pinned(x):
 
 
 class MulWork(Workload):
-    """configs[0]: 2^14 x 2^14 plain multiplication (IMAD-bound)."""
+    """configs[0]: 2^14 x 2^14 plain multiplication (IMAD-bound).  With N > 1
+    ranks the product shards by output range, balanced by work (the triangular
+    profile, shard.balanced_output_ranges): each rank computes its
+    slice with mmm_cu_mul_range_dev, then one NCCL all-gather (padded slices)
+    inside the timed step."""
 
     name = "mul"
+    sharded = True
 
     def __init__(self, s):
         import paper_1402_0264_b200 as mmm
@@ -308,9 +313,23 @@ class MulWork(Workload):
         self.a, self.b = c["a"], c["b"]
         self.want = golden()["cfg1"]["f"]
         self.nf = len(self.a) + len(self.b) - 1
+        self.world, self.dist = 1, None
+        self.ranges = [(0, self.nf)]
+        self.k0, self.k1, self.L = 0, self.nf, self.nf
         self.config = {"workload": "cfg1_mul_2^14x2^14_p469762049", "p": P, "s": self.s,
-                       "seed": 42, "parallelism": "replicas",
+                       "seed": 42, "parallelism": "single GPU",
                        "l2": "flushed between timed steps (inputs < L2)"}
+
+    def bind(self, dist):
+        from paper_1402_0264_b200.shard import balanced_output_ranges
+        self.dist, self.world = dist, dist.world
+        self.ranges = balanced_output_ranges(len(self.a), len(self.b), dist.world, align=32)
+        self.k0, self.k1 = self.ranges[dist.rank]
+        self.L = max(k1 - k0 for k0, k1 in self.ranges)
+        if dist.world > 1:
+            self.config["parallelism"] = (f"output range sharded by work over {dist.world} ranks "
+                                          "(balanced_output_ranges), NCCL all-gather")
+            self.config["ranges"] = self.ranges
 
     def units(self):
         return float(len(self.a) * len(self.b))
@@ -318,28 +337,45 @@ class MulWork(Workload):
     def device_setup(self):
         import torch
         self.da, self.db = _dev(self.a), _dev(self.b)
-        self.df = torch.zeros(self.nf, dtype=torch.int32, device="cuda")
+        self.dloc = torch.zeros(self.L, dtype=torch.int32, device="cuda")
+        self.dall = (torch.zeros(self.world * self.L, dtype=torch.int32, device="cuda")
+                     if self.world > 1 else self.dloc)
 
     def device_step(self, stream):
-        self.mmm.mul_dev(P, self.da.data_ptr(), len(self.a), self.db.data_ptr(), len(self.b),
-                         self.df.data_ptr(), s=self.s, stream=stream)
+        self.mmm.mul_range_dev(P, self.da.data_ptr(), len(self.a), self.db.data_ptr(),
+                               len(self.b), self.k0, self.k1, self.dloc.data_ptr(), s=self.s,
+                               stream=stream)
+        if self.world > 1:
+            self.dist.pg.all_gather_into_tensor(self.dall, self.dloc)
+
+    def _assemble(self, flat):
+        return np.concatenate([flat[r * self.L: r * self.L + (k1 - k0)]
+                               for r, (k0, k1) in enumerate(self.ranges)])
 
     def device_check(self):
-        assert digest(self.df.cpu().numpy().view(np.uint32)) == self.want, "mul result"
+        f = self._assemble(self.dall.cpu().numpy().view(np.uint32))
+        assert digest(f) == self.want, "mul result"
 
     def host_setup(self):
         (self.ha, self._ta), (self.hb, self._tb) = _pinned(self.a), _pinned(self.b)
         self.bytes_in = 4 * (len(self.a) + len(self.b))
-        self.bytes_out = 4 * self.nf
+        self.bytes_out = 4 * (self.nf if self.world == 1 else self.world * self.L)
 
     def host_step(self):
-        return self.mmm.mul(self.ha, self.hb, P, s=self.s)
+        if self.world == 1:  # the host C-ABI call a user makes (mmm_cu_mul)
+            return self.mmm.mul(self.ha, self.hb, P, s=self.s)
+        import torch  # sharded: pinned H2D, the rank's slice, all-gather, D2H
+        self.da.copy_(self._ta, non_blocking=True)
+        self.db.copy_(self._tb, non_blocking=True)
+        self.device_step(torch.cuda.current_stream().cuda_stream)
+        return self._assemble(self.dall.cpu().numpy().view(np.uint32))
 
     def host_check(self, f):
         assert digest(f) == self.want
 
     def roofline(self, t_step, hbm, imad):
-        macs = self.units()
+        from paper_1402_0264_b200.shard import range_work
+        macs = float(range_work(len(self.a), len(self.b), self.k0, self.k1))  # this rank
         achieved = macs / t_step / 1e12
         peak = (imad or 7.35e12) / 1e12
         return {"bound": "imad", "achieved": achieved, "peak": peak, "unit": "TMAC/s",

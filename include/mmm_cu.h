@@ -110,6 +110,11 @@ int mmm_cu_mul_dev(int64_t p, const uint32_t* d_a, int64_t na, const uint32_t* d
                    int64_t s, uint32_t* d_f, void* stream);
 int mmm_cu_divmod_dev(int64_t p, const uint32_t* d_a, int64_t na, const uint32_t* d_b, int64_t nb,
                       int64_t s, uint32_t* d_q, uint32_t* d_r, void* stream);
+/* Coefficients [k0, k1) of the product into d_f[0, k1 - k0): one rank's slice of
+ * an output-range-sharded product (no reference symbol: B200 sharding). */
+int mmm_cu_mul_range_dev(int64_t p, const uint32_t* d_a, int64_t na, const uint32_t* d_b,
+                         int64_t nb, int64_t k0, int64_t k1, int64_t s, uint32_t* d_f,
+                         void* stream);
 /* d_g capacity max(na, nb); *d_ng (device int64) receives the gcd length. */
 int mmm_cu_gcd_dev(int64_t p, const uint32_t* d_a, int64_t na, const uint32_t* d_b, int64_t nb,
                    int64_t s, uint32_t* d_g, int64_t* d_ng, void* stream);

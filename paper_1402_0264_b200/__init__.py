@@ -30,7 +30,8 @@ import numpy as np
 __all__ = [
     "LIB_PATH", "load", "MmmError", "InvalidArgument", "DomainError", "CudaError", "SimError",
     "Field", "Rng", "random_poly", "mul", "divmod", "gcd", "ntt_mul", "mul_batched",
-    "divmod_batched", "ntt_mul_batched", "mul_dev", "divmod_dev", "gcd_dev", "ntt_mul_dev",
+    "divmod_batched", "ntt_mul_batched", "mul_dev", "mul_range_dev", "divmod_dev", "gcd_dev",
+    "ntt_mul_dev",
     "mul_batched_dev", "divmod_batched_dev", "ntt_mul_batched_dev", "launch_count",
 ]
 
@@ -88,6 +89,7 @@ SIGNATURES = {
     "mmm_cu_ntt_mul_batched": (C.c_int, [_I64, _U32P, _I64, _I64, _U32P, _I64, _I64, _I64, _U32P,
                                          _I64]),
     "mmm_cu_mul_dev": (C.c_int, [_I64, _VP, _I64, _VP, _I64, _I64, _VP, _VP]),
+    "mmm_cu_mul_range_dev": (C.c_int, [_I64, _VP, _I64, _VP, _I64, _I64, _I64, _I64, _VP, _VP]),
     "mmm_cu_divmod_dev": (C.c_int, [_I64, _VP, _I64, _VP, _I64, _I64, _VP, _VP, _VP]),
     "mmm_cu_gcd_dev": (C.c_int, [_I64, _VP, _I64, _VP, _I64, _I64, _VP, _VP, _VP]),
     "mmm_cu_ntt_mul_dev": (C.c_int, [_I64, _VP, _I64, _VP, _I64, _VP, _VP]),
@@ -283,6 +285,11 @@ def ntt_mul_batched(A, B, p) -> np.ndarray:
 # cudaStream_t as int (torch.cuda.Stream.cuda_stream) or 0.
 def mul_dev(p, d_a, na, d_b, nb, d_f, s=8, stream=0):
     _check(load().mmm_cu_mul_dev(_pint(p), d_a, na, d_b, nb, s, d_f, stream))
+
+
+def mul_range_dev(p, d_a, na, d_b, nb, k0, k1, d_f, s=8, stream=0):
+    """Product coefficients [k0, k1) into d_f[0, k1 - k0) (a rank's output slice)."""
+    _check(load().mmm_cu_mul_range_dev(_pint(p), d_a, na, d_b, nb, k0, k1, s, d_f, stream))
 
 
 def divmod_dev(p, d_a, na, d_b, nb, d_q, d_r, s=64, stream=0):

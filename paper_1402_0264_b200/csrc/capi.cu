@@ -210,6 +210,18 @@ int mmm_cu_mul_dev(int64_t p, const uint32_t* d_a, int64_t na, const uint32_t* d
     });
 }
 
+int mmm_cu_mul_range_dev(int64_t p, const uint32_t* d_a, int64_t na, const uint32_t* d_b,
+                         int64_t nb, int64_t k0, int64_t k1, int64_t s, uint32_t* d_f,
+                         void* stream) {
+    return guarded([&] {
+        const FieldParams F = field_or_throw(p);
+        if (na < 1 || nb < 1) throw Error(ST_INVALID, "multiplication: operands must be nonzero");
+        if (k0 < 0 || k1 < k0 || k1 > na + nb - 1)
+            throw Error(ST_INVALID, "multiplication: output range outside [0, na + nb - 1)");
+        launch_mul_range(F, d_a, na, d_b, nb, k0, k1, d_f, s, 0, as_stream(stream));
+    });
+}
+
 int mmm_cu_mul_batched(int64_t p, const uint32_t* A, int64_t lda, int64_t na, const uint32_t* B,
                        int64_t ldb, int64_t nb, int64_t count, int64_t s, uint32_t* Fo,
                        int64_t ldf) {

@@ -69,6 +69,9 @@ inline int sm_count() {
 
 // ---- launchers (device pointers, async on `st`; outputs untrimmed) --------
 // multiplication: f[0 .. na+nb-1) = a * b.  s/l are tile hints (mul.cu).
+void launch_mul_range(const FieldParams& F, const uint32_t* a, int64_t na, const uint32_t* b,
+                      int64_t nb, int64_t klo, int64_t khi, uint32_t* f, int64_t s, int64_t l,
+                      cudaStream_t st);
 void launch_mul(const FieldParams& F, const uint32_t* a, int64_t na, const uint32_t* b, int64_t nb,
                 uint32_t* f, int64_t s, int64_t l, cudaStream_t st);
 void launch_mul_batched(const FieldParams& F, const uint32_t* A, int64_t lda, int64_t na,

@@ -35,6 +35,7 @@ struct MulArgs {
     unsigned* arrived;        // per k-tile count of finished items (zeroed with acc)
     int64_t na, nb, lda, ldb, ldf;
     int64_t chunk;  // i-range per item
+    int64_t klo, khi;  // output range [klo, khi): f[k - klo] (whole product: 0, na + nb - 1)
     FieldParams F;
 };
 
@@ -48,8 +49,8 @@ __global__ void __launch_bounds__(MUL_T) mul_kernel(MulArgs g) {
     const int64_t inst = blockIdx.z;
     const uint32_t* __restrict__ a = g.a + inst * g.lda;
     const uint32_t* __restrict__ b = g.b + inst * g.ldb;
-    const int64_t na = g.na, nb = g.nb, nf = na + nb - 1;
-    const int64_t k0 = int64_t(blockIdx.y) * TK;
+    const int64_t na = g.na, nb = g.nb, nf = g.khi;
+    const int64_t k0 = g.klo + int64_t(blockIdx.y) * TK;
     if (k0 >= nf) return;
     const int64_t ilo = k0 - (nb - 1) > 0 ? k0 - (nb - 1) : 0;
     const int64_t ihi = k0 + TK < na ? k0 + TK : na;
@@ -84,9 +85,9 @@ __global__ void __launch_bounds__(MUL_T) mul_kernel(MulArgs g) {
         if (k < nf) {
             const uint32_t v = reduce(acc[r], g.F);
             if (split)
-                atomicAdd(g.acc + k, (unsigned long long)v);
+                atomicAdd(g.acc + (k - g.klo), (unsigned long long)v);
             else
-                f[k] = v;
+                f[k - g.klo] = v;
         }
     }
     if (!split) return;
@@ -103,7 +104,7 @@ __global__ void __launch_bounds__(MUL_T) mul_kernel(MulArgs g) {
     __threadfence();
     for (int t = threadIdx.x; t < TK; t += MUL_T) {
         const int64_t k = k0 + t;
-        if (k < nf) f[k] = reduce(__ldcg(g.acc + k), g.F);
+        if (k < nf) f[k - g.klo] = reduce(__ldcg(g.acc + (k - g.klo)), g.F);
     }
 }
 
@@ -136,16 +137,25 @@ void dispatch(int R, const MulArgs& g, dim3 grid, cudaStream_t st) {
 }  // namespace
 
 void launch_mul(const FieldParams& F, const uint32_t* a, int64_t na, const uint32_t* b, int64_t nb,
-                uint32_t* f, int64_t s, int64_t /*l*/, cudaStream_t st) {
+                uint32_t* f, int64_t s, int64_t l, cudaStream_t st) {
+    launch_mul_range(F, a, na, b, nb, 0, na + nb - 1, f, s, l, st);
+}
+
+// Outputs [klo, khi) of the product into f[0, khi - klo): the per-rank slice of
+// an output-range-sharded product.
+void launch_mul_range(const FieldParams& F, const uint32_t* a, int64_t na, const uint32_t* b,
+                      int64_t nb, int64_t klo, int64_t khi, uint32_t* f, int64_t s, int64_t /*l*/,
+                      cudaStream_t st) {
     const int R = pick_tile(s, F);
     const int64_t TK = int64_t(MUL_T) * R;
-    const int64_t nf = na + nb - 1;
+    const int64_t nf = khi - klo;
+    if (nf <= 0) return;
     const int64_t nkt = ceil_div(nf, TK);
     if (nkt > 65535) throw Error(ST_INVALID, "multiplication: product too long for plain kernel");
     // Total staged terms over all k-tiles; aim for ~8 items per SM.
     int64_t total = 0, longest = 0;
     for (int64_t kt = 0; kt < nkt; ++kt) {
-        const int64_t k0 = kt * TK;
+        const int64_t k0 = klo + kt * TK;
         const int64_t lo = std::max<int64_t>(0, k0 - (nb - 1)), hi = std::min<int64_t>(na, k0 + TK);
         total += hi - lo;
         longest = std::max(longest, hi - lo);
@@ -163,6 +173,8 @@ void launch_mul(const FieldParams& F, const uint32_t* a, int64_t na, const uint3
     g.na = na;
     g.nb = nb;
     g.chunk = chunk;
+    g.klo = klo;
+    g.khi = khi;
     g.F = F;
     if (items > 1) {  // one zeroing pass for the accumulator and the arrival counters
         const size_t words = size_t(nf) + size_t(ceil_div(nkt, 2));
@@ -188,6 +200,8 @@ void launch_mul_batched(const FieldParams& F, const uint32_t* A, int64_t lda, in
     g.ldb = ldb;
     g.ldf = ldf;
     g.chunk = na + nb;  // one item per k-tile: no split, direct stores
+    g.klo = 0;
+    g.khi = nf;
     g.F = F;
     for (int64_t c0 = 0; c0 < count; c0 += 65535) {
         const int64_t c = std::min<int64_t>(65535, count - c0);

@@ -162,6 +162,53 @@ def test_cfg1_plain_mult(cuda_lib, golden_configs):
         assert digest(cuda_lib.mul(c["a"], c["b"], P, s=s)) == golden_configs["cfg1"]["f"], s
 
 
+def _mul_range(mmm, a, b, k0, k1, s):
+    import torch
+    da = torch.from_numpy(np.asarray(a, dtype=np.uint32).view(np.int32)).cuda()
+    db = torch.from_numpy(np.asarray(b, dtype=np.uint32).view(np.int32)).cuda()
+    df = torch.full((max(k1 - k0, 1),), -1, dtype=torch.int32, device="cuda")
+    mmm.mul_range_dev(P, da.data_ptr(), len(a), db.data_ptr(), len(b), k0, k1, df.data_ptr(), s=s,
+                      stream=torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    return df.cpu().numpy().view(np.uint32)[: k1 - k0]
+
+
+def test_mul_range_slices(cuda_lib, port):
+    """Output-range product (the cfg1 shard kernel): every slice, including
+    empty, single-word, tile-straddling and whole ranges, equals the oracle's
+    product coefficients there; the balanced split reassembles the product."""
+    from paper_1402_0264_b200.shard import balanced_output_ranges
+    rng = np.random.default_rng(11)
+    for na, nb in [(300, 200), (1, 50), (50, 1), (2000, 3000)]:
+        a = rng.integers(0, P, na).astype(np.uint32)
+        b = rng.integers(0, P, nb).astype(np.uint32)
+        full = np.zeros(na + nb - 1, np.int64)
+        w = port.mul(a, b, P)
+        full[: len(w)] = w
+        nf = na + nb - 1
+        for k0, k1 in [(0, nf), (0, 1), (nf - 1, nf), (5, 5), (nf // 3, 2 * nf // 3),
+                       (min(1023, nf - 1), min(2049, nf))]:
+            for s in (1, 8):
+                got = _mul_range(cuda_lib, a, b, k0, k1, s)
+                assert np.array_equal(got.astype(np.int64), full[k0:k1]), (na, nb, k0, k1, s)
+        for world in (2, 3, 8):
+            parts = [_mul_range(cuda_lib, a, b, k0, k1, 8)
+                     for k0, k1 in balanced_output_ranges(na, nb, world, align=128)]
+            assert np.array_equal(np.concatenate(parts).astype(np.int64), full)
+    with pytest.raises(cuda_lib.InvalidArgument):
+        _mul_range(cuda_lib, a, b, 0, na + nb, 8)
+
+
+def test_cfg1_sharded_ranges(cuda_lib, golden_configs):
+    from paper_1402_0264_b200.shard import balanced_output_ranges
+    c = suites.cfg1(ProductRng(42))
+    for world in (2, 8):
+        f = np.concatenate([_mul_range(cuda_lib, c["a"], c["b"], k0, k1, 8)
+                            for k0, k1 in balanced_output_ranges(len(c["a"]), len(c["b"]), world,
+                                                                 align=32)])
+        assert digest(f) == golden_configs["cfg1"]["f"], world
+
+
 def test_cfg1_via_ntt(cuda_lib, golden_configs):
     c = suites.cfg1(ProductRng(42))
     assert digest(cuda_lib.ntt_mul(c["a"], c["b"], P)) == golden_configs["cfg1"]["f"]

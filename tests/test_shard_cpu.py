@@ -8,7 +8,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_1402_0264_b200.shard import gather_rows, shard_range
+from paper_1402_0264_b200.shard import (balanced_output_ranges, gather_rows, product_work,
+                                         range_work, shard_range)
 
 
 def test_shard_range_partitions():
@@ -21,6 +22,64 @@ def test_shard_range_partitions():
             assert max(sizes) - min(sizes) <= 1
     with pytest.raises(ValueError):
         shard_range(10, 2, 2)
+
+
+def test_balanced_output_ranges_cover_and_balance():
+    for na, nb in [(1, 1), (1, 9), (9, 1), (5, 5), (100, 7), (7, 100), (1 << 14, 1 << 14)]:
+        nf = na + nb - 1
+        for world in (1, 2, 3, 4, 8):
+            for align in (1, 4, 1024):
+                rs = balanced_output_ranges(na, nb, world, align=align)
+                assert len(rs) == world and rs[0][0] == 0 and rs[-1][1] == nf
+                assert all(a[1] == b[0] and a[0] <= a[1] for a, b in zip(rs, rs[1:]))
+                works = [range_work(na, nb, k0, k1) for k0, k1 in rs]
+                assert sum(works) == na * nb
+                if na * nb <= 10000:
+                    assert works == [sum(product_work(na, nb, k) for k in range(k0, k1))
+                                     for k0, k1 in rs]
+    rs = balanced_output_ranges(1 << 14, 1 << 14, 8, align=32)  # as bench.py shards cfg1
+    works = [range_work(1 << 14, 1 << 14, k0, k1) for k0, k1 in rs]
+    assert max(works) / min(works) < 1.02  # cfg1: equal work (to 32 outputs), not equal counts
+    assert rs[0][1] - rs[0][0] > 2 * (rs[3][1] - rs[3][0])
+
+
+def _range_worker(rank, world, port, q):
+    """Each rank produces its balanced output slice of a product (here the
+    oracle's coefficients stand in for the GPU kernel: host logic only), pads it
+    to the longest slice and all-gathers; every rank reassembles the product."""
+    import numpy as np
+    from oracle import pyoracle
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        p, na, nb = 469762049, 700, 300
+        rng = np.random.default_rng(5)
+        a, b = rng.integers(0, p, na), rng.integers(1, p, nb)
+        full = np.asarray(pyoracle.best().mul(a, b, p), dtype=np.int64)
+        ranges = balanced_output_ranges(na, nb, world, align=64)
+        k0, k1 = ranges[rank]
+        L = max(y - x for x, y in ranges)
+        local = torch.zeros(L, dtype=torch.int64)
+        local[: k1 - k0] = torch.from_numpy(full[k0:k1])
+        parts = [torch.empty(L, dtype=torch.int64) for _ in range(world)]
+        dist.all_gather(parts, local)
+        got = torch.cat([parts[r][: y - x] for r, (x, y) in enumerate(ranges)]).numpy()
+        q.put((rank, bool(np.array_equal(got, full))))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_output_range_gather_two_ranks_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_range_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert res == [(0, True), (1, True)]
 
 
 def _free_port():
