@@ -452,6 +452,35 @@ class DivWork(Workload):
                 "full instance (oracle_divmod)")
 
 
+class FastDivWork(DivWork):
+    """configs[2] by Newton iteration and NTT products: the
+    same (q, r); units stay the schoolbook updates so the rate compares."""
+
+    name = "div_fast"
+
+    def __init__(self, s):
+        super().__init__(s)
+        self.config.update(workload="cfg3_divmod_fast_newton_ntt_deg2^16_by_deg2^15_p469762049",
+                           units="schoolbook-equivalent updates")
+        self.config.pop("s", None)
+
+    def device_step(self, stream):
+        self.mmm.divmod_fast_dev(P, self.da.data_ptr(), len(self.a), self.db.data_ptr(),
+                                 len(self.b), self.dq.data_ptr(), self.dr.data_ptr(),
+                                 stream=stream)
+
+    def host_step(self):
+        return self.mmm.divmod_fast(self.ha, self.hb, P)
+
+    def roofline(self, t_step, hbm, imad):
+        alg = 4.0 * (len(self.a) + len(self.b) + self.nq + self.nr)
+        achieved = alg / t_step / 1e9
+        return {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm, "traffic": None, "kernel": "ntt_rows",
+                "alg_bytes_per_launch": alg,
+                "binding": "~17 Newton doublings + 2 products: launch latency of small NTTs"}
+
+
 class NttWork(Workload):
     """configs[3] (single): 2^20 x 2^20 product through a length-2^21 NTT."""
 
@@ -723,7 +752,8 @@ class BatchWork(_Sharded):
                 "instance 0 of each batch (oracle_mul + oracle_divmod)")
 
 
-WORKLOADS = {"gcd": GcdWork, "mul": MulWork, "div": DivWork, "ntt": NttWork,
+WORKLOADS = {"gcd": GcdWork, "mul": MulWork, "div": DivWork, "div_fast": FastDivWork,
+             "ntt": NttWork,
              "ntt_batch": NttBatchWork, "batch": BatchWork}
 
 

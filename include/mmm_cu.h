@@ -82,6 +82,12 @@ int mmm_cu_mul(int64_t p, const uint32_t* a, int64_t na, const uint32_t* b, int6
 int mmm_cu_divmod(int64_t p, const uint32_t* a, int64_t na, const uint32_t* b, int64_t nb,
                   int64_t s, uint32_t* q, int64_t q_cap, int64_t* nq, uint32_t* r, int64_t r_cap,
                   int64_t* nr);
+/* The same (q, r), contract and errors as mmm_cu_divmod, in O(M(n)): Newton
+ * inverse of rev(b) and NTT products (schoolbook products where the prime
+ * lacks 2-adic roots).  No reference symbol: SURVEY §8f item 4. */
+int mmm_cu_divmod_fast(int64_t p, const uint32_t* a, int64_t na, const uint32_t* b, int64_t nb,
+                       uint32_t* q, int64_t q_cap, int64_t* nq, uint32_t* r, int64_t r_cap,
+                       int64_t* nr);
 /* g = monic gcd(a, b); g_cap >= max(na, nb).  s = steps per matrix batch. */
 int mmm_cu_gcd(int64_t p, const uint32_t* a, int64_t na, const uint32_t* b, int64_t nb, int64_t s,
                uint32_t* g, int64_t g_cap, int64_t* ng);
@@ -110,6 +116,8 @@ int mmm_cu_mul_dev(int64_t p, const uint32_t* d_a, int64_t na, const uint32_t* d
                    int64_t s, uint32_t* d_f, void* stream);
 int mmm_cu_divmod_dev(int64_t p, const uint32_t* d_a, int64_t na, const uint32_t* d_b, int64_t nb,
                       int64_t s, uint32_t* d_q, uint32_t* d_r, void* stream);
+int mmm_cu_divmod_fast_dev(int64_t p, const uint32_t* d_a, int64_t na, const uint32_t* d_b,
+                           int64_t nb, uint32_t* d_q, uint32_t* d_r, void* stream);
 /* Coefficients [k0, k1) of the product into d_f[0, k1 - k0): one rank's slice of
  * an output-range-sharded product (no reference symbol: B200 sharding). */
 int mmm_cu_mul_range_dev(int64_t p, const uint32_t* d_a, int64_t na, const uint32_t* d_b,

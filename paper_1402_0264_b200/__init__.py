@@ -31,6 +31,7 @@ __all__ = [
     "LIB_PATH", "load", "MmmError", "InvalidArgument", "DomainError", "CudaError", "SimError",
     "Field", "Rng", "random_poly", "mul", "divmod", "gcd", "ntt_mul", "mul_batched",
     "divmod_batched", "ntt_mul_batched", "mul_dev", "mul_range_dev", "divmod_dev", "gcd_dev",
+    "divmod_fast", "divmod_fast_dev",
     "ntt_mul_dev",
     "mul_batched_dev", "divmod_batched_dev", "ntt_mul_batched_dev", "launch_count",
 ]
@@ -80,6 +81,9 @@ SIGNATURES = {
     "mmm_cu_mul": (C.c_int, [_I64, _U32P, _I64, _U32P, _I64, _I64, _I64, _U32P, _I64, _I64P]),
     "mmm_cu_divmod": (C.c_int, [_I64, _U32P, _I64, _U32P, _I64, _I64, _U32P, _I64, _I64P, _U32P,
                                 _I64, _I64P]),
+    "mmm_cu_divmod_fast": (C.c_int, [_I64, _U32P, _I64, _U32P, _I64, _U32P, _I64, _I64P, _U32P,
+                                     _I64, _I64P]),
+    "mmm_cu_divmod_fast_dev": (C.c_int, [_I64, _VP, _I64, _VP, _I64, _VP, _VP, _VP]),
     "mmm_cu_gcd": (C.c_int, [_I64, _U32P, _I64, _U32P, _I64, _I64, _U32P, _I64, _I64P]),
     "mmm_cu_ntt_mul": (C.c_int, [_I64, _U32P, _I64, _U32P, _I64, _U32P, _I64, _I64P]),
     "mmm_cu_mul_batched": (C.c_int, [_I64, _U32P, _I64, _I64, _U32P, _I64, _I64, _I64, _I64,
@@ -232,6 +236,21 @@ def divmod(a, b, p, s: int = 64):
     _check(load().mmm_cu_divmod(p, _p(a), a.size, _p(b), b.size, s, _p(q), q.size, C.byref(nq),
                                 _p(r), r.size, C.byref(nr)))
     return q[: nq.value].copy(), r[: nr.value].copy()
+
+
+def divmod_fast(a, b, p):
+    """divmod(a, b) by Newton iteration and NTT products: the same (q, r)."""
+    a, b, p = _u32(a), _u32(b), _pint(p)
+    q = np.zeros(max(a.size, 1), dtype=np.uint32)
+    r = np.zeros(max(a.size, b.size, 1), dtype=np.uint32)
+    nq, nr = C.c_int64(0), C.c_int64(0)
+    _check(load().mmm_cu_divmod_fast(p, _p(a), a.size, _p(b), b.size, _p(q), q.size, C.byref(nq),
+                                     _p(r), r.size, C.byref(nr)))
+    return q[: nq.value].copy(), r[: nr.value].copy()
+
+
+def divmod_fast_dev(p, d_a, na, d_b, nb, d_q, d_r, stream=0):
+    _check(load().mmm_cu_divmod_fast_dev(_pint(p), d_a, na, d_b, nb, d_q, d_r, stream))
 
 
 def gcd(a, b, p, s: int = 64) -> np.ndarray:

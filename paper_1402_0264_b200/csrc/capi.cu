@@ -302,6 +302,51 @@ int mmm_cu_divmod(int64_t p, const uint32_t* a, int64_t na, const uint32_t* b, i
     });
 }
 
+int mmm_cu_divmod_fast(int64_t p, const uint32_t* a, int64_t na, const uint32_t* b, int64_t nb,
+                       uint32_t* q, int64_t q_cap, int64_t* nq, uint32_t* r, int64_t r_cap,
+                       int64_t* nr) {
+    return guarded([&] {  // validation and results exactly as mmm_cu_divmod
+        const FieldParams F = field_or_throw(p);
+        check_canonical(a, na, F.p, "division dividend");
+        check_canonical(b, nb, F.p, "division divisor");
+        *nq = *nr = 0;
+        if (nb == 0) throw Error(ST_DOMAIN, "divmod: division by the zero polynomial");
+        na = trimmed_len(a, na);
+        if (na < nb) {
+            need_cap(r_cap, na, "division remainder");
+            if (na) std::memcpy(r, a, size_t(na) * 4);
+            *nr = na;
+            return;
+        }
+        if (b[nb - 1] == 0) throw Error(ST_DOMAIN, "field: inverse of zero");
+        need_cap(q_cap, na - nb + 1, "division quotient");
+        need_cap(r_cap, nb - 1, "division remainder");
+        cudaStream_t st = thread_stream();
+        {
+            Scratch sc(st);
+            const uint32_t* da = to_device(sc, a, na);
+            const uint32_t* db = to_device(sc, b, nb);
+            uint32_t* dq = sc.get<uint32_t>(size_t(na - nb + 1));
+            uint32_t* dr = sc.get<uint32_t>(size_t(nb));
+            launch_divmod_fast(F, da, na, db, nb, dq, dr, st);
+            to_host(q, dq, na - nb + 1, st);
+            to_host(r, dr, nb - 1, st);
+        }
+        sync(st);
+        *nq = trimmed_len(q, na - nb + 1);
+        *nr = trimmed_len(r, nb - 1);
+    });
+}
+
+int mmm_cu_divmod_fast_dev(int64_t p, const uint32_t* d_a, int64_t na, const uint32_t* d_b,
+                           int64_t nb, uint32_t* d_q, uint32_t* d_r, void* stream) {
+    return guarded([&] {
+        const FieldParams F = field_or_throw(p);
+        if (nb < 1 || na < nb) throw Error(ST_INVALID, "division: requires deg a >= deg b >= 0");
+        launch_divmod_fast(F, d_a, na, d_b, nb, d_q, d_r, as_stream(stream));
+    });
+}
+
 int mmm_cu_divmod_dev(int64_t p, const uint32_t* d_a, int64_t na, const uint32_t* d_b, int64_t nb,
                       int64_t s, uint32_t* d_q, uint32_t* d_r, void* stream) {
     return guarded([&] {

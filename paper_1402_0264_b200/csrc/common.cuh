@@ -83,6 +83,9 @@ void launch_divmod(const FieldParams& F, const uint32_t* a, int64_t na, const ui
 void launch_divmod_batched(const FieldParams& F, const uint32_t* A, int64_t lda, int64_t na,
                            const uint32_t* B, int64_t ldb, int64_t nb, int64_t count, uint32_t* Q,
                            int64_t ldq, uint32_t* R, int64_t ldr, int64_t s, cudaStream_t st);
+// division by Newton iteration over NTT products (fastdiv.cu): same q, r.
+void launch_divmod_fast(const FieldParams& F, const uint32_t* a, int64_t na, const uint32_t* b,
+                        int64_t nb, uint32_t* q, uint32_t* r, cudaStream_t st);
 // gcd: g (capacity max(na,nb)) = monic gcd, *d_ng = its length.
 void launch_gcd(const FieldParams& F, const uint32_t* a, int64_t na, const uint32_t* b, int64_t nb,
                 uint32_t* g, int64_t* d_ng, int64_t s, cudaStream_t st);

@@ -276,3 +276,65 @@ def test_cfg5_batches(cuda_lib, golden_configs):
     qs = [digest(np.trim_zeros(Q[i].astype(np.int64), "b")) for i in range(Q.shape[0])]
     rs = [digest(np.trim_zeros(R[i].astype(np.int64), "b")) for i in range(R.shape[0])]
     assert qs == golden_configs["cfg5"]["q"] and rs == golden_configs["cfg5"]["r"]
+
+
+# ---------------------------------------------- Newton/NTT fast division --
+def test_fast_division_frozen_and_suites(cuda_lib, port, golden_small):
+    """divmod_fast returns exactly oracle_divmod's (q, r): the frozen GF(7)
+    cases and every seeded division suite of the reference's tests."""
+    mmm = cuda_lib
+    for c in golden_small["frozen"]:
+        if c["op"] == "divmod":
+            q, r = mmm.divmod_fast(c["a"], c["b"], c["p"])
+            assert (q.tolist(), r.tolist()) == (c["q"], c["r"]), c
+    for suite in ("mutual_oracle", "divmod_roundtrip", "division_sweep", "acceptance",
+                  "verify_p7", "verify_p101", "verify_p469762049"):
+        cases = golden_small["suites"][suite]["cases"]
+        for c, g in zip(replay(suite, ProductRng, port.mul), cases):
+            if "q" in g:
+                q, r = mmm.divmod_fast(c["a"], c["b"], c["p"])
+                assert (digest(q), digest(r)) == (g["q"], g["r"]), suite
+
+
+def test_fast_division_edges(cuda_lib, port):
+    """Every quotient length around the Newton doubling and the NTT/schoolbook
+    switch, constant and monic divisors, p = 2 and primes without 2-adic roots
+    (schoolbook products), untrimmed inputs, na < nb and the domain errors."""
+    mmm = cuda_lib
+    rng = np.random.default_rng(21)
+    for p in (2, 7, 101, 469762049, 998244353, 2147483647):
+        for na, nb in [(1, 1), (2, 1), (5, 1), (9, 4), (64, 1), (65, 2), (300, 299), (513, 1),
+                       (1024, 511), (1100, 512), (2049, 1025), (3000, 700), (700, 3000)]:
+            a = rng.integers(0, p, na)
+            b = rng.integers(0, p, nb)
+            a[-1] = max(a[-1], 1)
+            b[-1] = max(b[-1], 1)
+            q, r = mmm.divmod_fast(a, b, p)
+            wq, wr = port.divmod(a, b, p)
+            assert np.array_equal(q, wq) and np.array_equal(r, wr), (p, na, nb)
+    q, r = mmm.divmod_fast([1, 2, 0, 1, 0, 0], [1, 1], 7)  # untrimmed dividend
+    assert (q.tolist(), r.tolist()) == ([3, 6, 1], [5])
+    with pytest.raises(mmm.DomainError):
+        mmm.divmod_fast([1, 2, 3], [], 7)
+    with pytest.raises(mmm.DomainError):
+        mmm.divmod_fast([1, 2, 3], [1, 0], 7)  # zero lead of b, na >= nb
+
+
+def test_cfg3_fast_division(cuda_lib, golden_configs):
+    c = suites.cfg3(ProductRng(42))
+    q, r = cuda_lib.divmod_fast(c["a"], c["b"], P)
+    assert (digest(q), digest(r)) == (golden_configs["cfg3"]["q"], golden_configs["cfg3"]["r"])
+
+
+def test_fast_division_roundtrip_at_scale(cuda_lib):
+    """2^20 / 2^19 terms (beyond any oracle run): q*b + r == a, deg r < deg b."""
+    rng = np.random.default_rng(3)
+    a = rng.integers(0, P, (1 << 20) + 3).astype(np.uint32)
+    b = rng.integers(0, P, (1 << 19) + 1).astype(np.uint32)
+    a[-1] |= 1
+    b[-1] |= 1
+    q, r = cuda_lib.divmod_fast(a, b, P)
+    assert len(q) == len(a) - len(b) + 1 and len(r) < len(b)
+    qb = cuda_lib.ntt_mul(q, b, P).astype(np.int64)
+    qb[: len(r)] = (qb[: len(r)] + r) % P
+    assert np.array_equal(qb, a.astype(np.int64))
