@@ -13,8 +13,9 @@
 //                      times w_N^-(n2*k1)     (fused: one read, one write);
 //   K3  column pass  : inverse N1-point transforms, scaled by N^-1,
 //                      written in natural order.
-// Every sub-transform is a radix-2 Stockham autosort network in shared
-// memory (natural order in and out, ping-pong buffers), twiddles staged in
+// Every sub-transform is a Stockham autosort network in shared memory
+// (natural order in and out, ping-pong buffers) taking two radix-2 stages per
+// pass in registers (stockham4: 189 -> 129 us for 2^21), twiddles staged in
 // shared memory with Shoup companions w' = floor(w * 2^32 / p), so each
 // butterfly is add/sub + one Shoup product (IMAD.HI + 2 IMAD + correction).
 // Between passes the data stays in an N-word workspace per operand (L2).
@@ -87,6 +88,59 @@ __device__ uint32_t* stockham(uint32_t* x, uint32_t* y, int logL, int logc, cons
     return x;
 }
 
+// Two Stockham stages at once (radix-4 step): the unit (q, pp), pp < H/2 with
+// H = half/sp, reads the four words x[q + sp*(pp + j*H/2)], j < 4, runs the
+// stage-s butterflies (pp, pp + H/2) and the stage-(s+1) butterflies on their
+// outputs in registers, and writes y[q + sp*(4pp + b0 + 2*b1)]: half the
+// passes, barriers and index arithmetic of two radix-2 stages.
+__device__ uint32_t* stockham4(uint32_t* x, uint32_t* y, int logL, int logc, const uint2* tw,
+                               uint32_t p) {
+    const int L = 1 << logL, half = L >> 1, cols = 1 << logc;
+    int s = 0;
+    for (; s + 1 < logL; s += 2) {
+        const int sp = 1 << s, H = half >> s, H2 = H >> 1;
+        for (int t = threadIdx.x; t < ((L >> 2) << logc); t += blockDim.x) {
+            const int c = t & (cols - 1), u = t >> logc;
+            const int pp = u >> s, q = u & (sp - 1);  // u = q + sp*pp, pp < H/2
+            const int base = c + cols * q, st = cols * sp;
+            const uint32_t a0 = x[base + st * pp];
+            const uint32_t a1 = x[base + st * (pp + H2)];
+            const uint32_t a2 = x[base + st * (pp + H)];
+            const uint32_t a3 = x[base + st * (pp + H2 + H)];
+            const uint2 w0 = tw[pp * sp], w1 = tw[(pp + H2) * sp], w2 = tw[pp * 2 * sp];
+            // stage s: (a0, a2) -> y[2pp], y[2pp+1]; (a1, a3) -> y[2pp+H], y[2pp+H+1]
+            const uint32_t e0 = add_p(a0, a2, p), e1 = shoup(sub_p(a0, a2, p), w0.x, w0.y, p);
+            const uint32_t f0 = add_p(a1, a3, p), f1 = shoup(sub_p(a1, a3, p), w1.x, w1.y, p);
+            // stage s+1, q' = q + sp*b0: (e_b0, f_b0) -> y'[4pp + b0], y'[4pp + b0 + 2]
+            y[base + st * (4 * pp)] = add_p(e0, f0, p);
+            y[base + st * (4 * pp + 2)] = shoup(sub_p(e0, f0, p), w2.x, w2.y, p);
+            y[base + st * (4 * pp + 1)] = add_p(e1, f1, p);
+            y[base + st * (4 * pp + 3)] = shoup(sub_p(e1, f1, p), w2.x, w2.y, p);
+        }
+        __syncthreads();
+        uint32_t* t = x;
+        x = y;
+        y = t;
+    }
+    if (s < logL) {  // odd logL: one radix-2 stage left
+        const int sp = 1 << s;
+        for (int t = threadIdx.x; t < (half << logc); t += blockDim.x) {
+            const int c = t & (cols - 1), i = t >> logc;
+            const int pp = i >> s, q = i & (sp - 1);
+            const uint32_t a = x[c + cols * (q + sp * pp)];
+            const uint32_t b = x[c + cols * (q + sp * (pp + half / sp))];
+            const uint2 w = tw[pp * sp];
+            y[c + cols * (q + sp * (2 * pp))] = add_p(a, b, p);
+            y[c + cols * (q + sp * (2 * pp + 1))] = shoup(sub_p(a, b, p), w.x, w.y, p);
+        }
+        __syncthreads();
+        uint32_t* t = x;
+        x = y;
+        y = t;
+    }
+    return x;
+}
+
 __device__ __forceinline__ uint32_t twiddle(uint32_t v, uint64_t e, const uint2* lo,
                                             const uint2* hi, uint32_t p) {
     const uint2 a = lo[e & ((1u << LO) - 1)];
@@ -126,7 +180,7 @@ __global__ void __launch_bounds__(NTT_T) ntt_cols_fwd(NttArgs g) {
         x[t] = idx < len ? in[idx] : 0u;
     }
     __syncthreads();
-    uint32_t* r = stockham(x, y, P.log1, g.logc, tw, P.p);
+    uint32_t* r = stockham4(x, y, P.log1, g.logc, tw, P.p);
     for (int t = threadIdx.x; t < C * N1; t += NTT_T) {
         const int c = t % C, k1 = t / C;
         const uint64_t e = uint64_t(c0 + c) * uint64_t(k1);
@@ -160,12 +214,12 @@ __global__ void __launch_bounds__(NTT_T) ntt_rows(NttArgs g, FieldParams F) {
     __syncthreads();
     // the two forward transforms as one 2-column network: interleave? keep
     // them separate (same code, half the threads idle per stage otherwise)
-    uint32_t* ra = stockham(xa, ya, P.log2, 0, twf, P.p);
-    uint32_t* rb = stockham(xb, yb, P.log2, 0, twf, P.p);
+    uint32_t* ra = stockham4(xa, ya, P.log2, 0, twf, P.p);
+    uint32_t* rb = stockham4(xb, yb, P.log2, 0, twf, P.p);
     for (int t = threadIdx.x; t < N2; t += NTT_T) ra[t] = mulmod(ra[t], rb[t], F);
     __syncthreads();
     uint32_t* other = ra == xa ? ya : xa;
-    uint32_t* rc = stockham(ra, other, P.log2, 0, twi, P.p);
+    uint32_t* rc = stockham4(ra, other, P.log2, 0, twi, P.p);
     for (int t = threadIdx.x; t < N2; t += NTT_T) {
         const uint64_t e = (uint64_t(1) << P.logN) - (uint64_t(t) * uint64_t(k1));
         wa[t] = twiddle(rc[t], e & ((uint64_t(1) << P.logN) - 1), P.tlo_f, P.thi_f, P.p);
@@ -190,7 +244,7 @@ __global__ void __launch_bounds__(NTT_T) ntt_cols_inv(NttArgs g) {
         x[t] = work[int64_t(N2) * k1 + c0 + c];
     }
     __syncthreads();
-    uint32_t* r = stockham(x, y, P.log1, g.logc, tw, P.p);
+    uint32_t* r = stockham4(x, y, P.log1, g.logc, tw, P.p);
     for (int t = threadIdx.x; t < C * N1; t += NTT_T) {
         const int c = t % C, n1 = t / C;
         const int64_t idx = int64_t(N2) * n1 + c0 + c;
