@@ -173,6 +173,33 @@ def peaks():
     return hbm, src, imad
 
 
+def imad_rate():
+    """Measured plain IMAD rate (profiles/peaks.json, tools/peaks.cu)."""
+    try:
+        with open(IMAD_PEAKS) as fh:
+            return float(json.load(fh)["imad_per_s"])
+    except (OSError, KeyError, ValueError):
+        return 1.82e13
+
+
+def ntt_roofline(logN, count, t_step, kernel):
+    """The NTT's bound is the integer multiply pipe (IMAD-bound
+    when each transform makes <= 1 HBM pass).  IMAD-class ops per step: 3 per
+    butterfly (Shoup product: IMAD.HI + 2 IMAD) over the 3 transforms, 3 per
+    four-step twiddle / scale product (2 per element per operand in the
+    forward columns, 2 in the rows' inverse twiddle, 1 in the scale: 7 per
+    output word), 4 per pointwise Montgomery product."""
+    N = 1 << logN
+    bfly = 3 * (N // 2) * logN * count
+    ops = 3 * bfly + 3 * 7 * N * count + 4 * N * count
+    peak = imad_rate()
+    achieved = ops / t_step
+    return {"bound": "imad", "achieved": achieved / 1e12, "peak": peak / 1e12,
+            "unit": "T IMAD-class/s", "frac": achieved / peak, "traffic": None,
+            "kernel": kernel, "alg_imad_ops_per_step": ops, "butterflies": bfly,
+            "peak_note": "measured IMAD rate (profiles/peaks.json imad_per_s)"}
+
+
 class ProductRng:
     def __init__(self, seed):
         import paper_1402_0264_b200 as mmm
@@ -527,14 +554,11 @@ class NttWork(Workload):
             assert digest(f) == self.want
 
     def roofline(self, t_step, hbm, imad):
+        r = ntt_roofline(21, 1, t_step, "ntt_rows")
         alg = 4.0 * (len(self.a) + len(self.b) + self.nf)
-        achieved = alg / t_step / 1e9
-        N = 1 << 21
-        bfly = 3 * (N // 2) * 21
-        return {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": achieved / hbm, "traffic": None, "kernel": "ntt_rows",
-                "alg_bytes_per_launch": alg, "butterflies": bfly,
-                "butterflies_per_s": bfly / t_step}
+        r["hbm"] = {"achieved_gbs": alg / t_step / 1e9, "peak_gbs": hbm,
+                    "frac": alg / t_step / 1e9 / hbm, "alg_bytes": alg}
+        return r
 
     def cpu_ref(self, orc):
         # bounded sample: 2^12 middle output words of the product, computed
@@ -637,11 +661,11 @@ class NttBatchWork(_Sharded):
 
     def roofline(self, t_step, hbm, imad):
         n_local = self.hi - self.lo
+        r = ntt_roofline(16, n_local, t_step, "ntt_rows")
         alg = 4.0 * n_local * (2 * self.na + self.nf)
-        achieved = alg / t_step / 1e9
-        return {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": achieved / hbm, "traffic": None, "kernel": "ntt_rows",
-                "alg_bytes_per_launch": alg}
+        r["hbm"] = {"achieved_gbs": alg / t_step / 1e9, "peak_gbs": hbm,
+                    "frac": alg / t_step / 1e9 / hbm, "alg_bytes": alg}
+        return r
 
     def cpu_ref(self, orc):
         i = 0
