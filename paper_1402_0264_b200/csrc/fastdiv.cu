@@ -28,10 +28,52 @@ __global__ void rev_prefix(const uint32_t* __restrict__ x, int64_t n, int64_t m,
         y[i] = (n - 1 - i >= 0) ? x[n - 1 - i] : 0u;
 }
 
-// h[0] = b_lead^-1
-__global__ void lead_inverse(const uint32_t* __restrict__ b, int64_t nb, uint32_t* h,
-                             FieldParams F) {
-    if (threadIdx.x == 0 && blockIdx.x == 0) h[0] = invmod(b[nb - 1], F);
+// The first Newton doublings, h = rb^-1 mod X^K for K <= BASE_K, in one CTA
+// with everything in shared memory (k < BASE_K would otherwise cost ~3 small
+// launches per doubling).  Per doubling k -> k2: e[i] = (rb * h)[k + i] =
+// sum_{j} rb[j] h[k + i - j] over h's k known terms, then
+// h[k + i] = -sum_{j <= i} h[j] e[i - j], i < k2 - k.
+constexpr int BASE_K = 512;
+__global__ void __launch_bounds__(FD_T) newton_base(const uint32_t* __restrict__ b, int64_t nb,
+                                                    int K, uint32_t* __restrict__ h_out,
+                                                    FieldParams F) {
+    __shared__ uint32_t rb[BASE_K], h[BASE_K], e[BASE_K];
+    for (int i = threadIdx.x; i < K; i += FD_T) rb[i] = (nb - 1 - i >= 0) ? b[nb - 1 - i] : 0u;
+    __syncthreads();
+    if (threadIdx.x == 0) h[0] = invmod(rb[0], F);
+    __syncthreads();
+    const uint32_t ft = F.fold_terms;
+    for (int k = 1; k < K;) {
+        const int k2 = min(2 * k, K), n = k2 - k;
+        for (int i = threadIdx.x; i < n; i += FD_T) {  // e[i], terms j in [i+1, k+i]
+            uint64_t acc = 0;
+            uint32_t since = 0;
+            for (int j = i + 1; j <= k + i; ++j) {
+                if (++since > ft) {
+                    acc = fold(acc, F);
+                    since = 1;
+                }
+                acc = mad_wide(rb[j], h[k + i - j], acc);
+            }
+            e[i] = reduce(acc, F);
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < n; i += FD_T) {
+            uint64_t acc = 0;
+            uint32_t since = 0;
+            for (int j = 0; j <= i; ++j) {
+                if (++since > ft) {
+                    acc = fold(acc, F);
+                    since = 1;
+                }
+                acc = mad_wide(h[j], e[i - j], acc);
+            }
+            h[k + i] = negmod(reduce(acc, F), F);
+        }
+        __syncthreads();
+        k = k2;
+    }
+    for (int i = threadIdx.x; i < K; i += FD_T) h_out[i] = h[i];
 }
 
 // h[k + i] = -t[i], i < n
@@ -77,9 +119,10 @@ void launch_divmod_fast(const FieldParams& F, const uint32_t* a, int64_t na, con
     uint32_t* t2 = sc.get<uint32_t>(size_t(2 * mu));
     rev_prefix<<<blocks_for(nrb), FD_T, 0, st>>>(b, nb, nrb, rb);
     check_launch("rev_prefix");
-    lead_inverse<<<1, 32, 0, st>>>(b, nb, h, F);
-    check_launch("lead_inverse");
-    for (int64_t k = 1; k < mu;) {
+    const int K0 = int(std::min<int64_t>(mu, BASE_K));
+    newton_base<<<1, FD_T, 0, st>>>(b, nb, K0, h, F);
+    check_launch("newton_base");
+    for (int64_t k = K0; k < mu;) {
         const int64_t k2 = std::min(2 * k, mu), nr = std::min(k2, nrb);
         // e = coefficients [k, k2) of rb[0:k2] * h[0:k]
         product(F, rb, nr, h, k, t1, st);
