@@ -25,6 +25,9 @@
 //     memory; one grid barrier per step of s heads (the paper's "launch").
 #include <cooperative_groups.h>
 
+#include <cstdio>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "conv.cuh"
 
@@ -235,6 +238,388 @@ __global__ void __launch_bounds__(DIV_T) div_grid_kernel(DivArgs g, int64_t seg)
         g.r[x] = __ldcg(A + x);
 }
 
+// ------------------------------------------- pipelined single instance --
+// div_pipe_kernel: the large single division without a grid barrier per step.
+// Steps j = 0..J-1 retire the heads [i_j - v_j + 1, i_j] (v_j = S but the
+// last), i_j = max(na - 1 - j*S, db - 1).  The step's update
+//   A[x] += sum_{k<v} nl_k * b[x - i_j + db + k],   nl_k = -lambda_k,
+// depends only on the step's lambdas, so updates commute and may be applied
+// to different positions at different times.  CTA 0 (head) keeps the top
+// WH = 2S positions of A in shared memory, computes each step's lambdas from
+// its window (split-K tiled convolution with h = rev(b)^-1), publishes them
+// as the quotient words (q) with a release flag, updates its window and the
+// S positions entering it, then slides.  Entering positions come from global
+// A, where the bulk CTAs have applied every step up to j - L; the head adds
+// the last L steps from its lambda history.  Bulk CTAs own fixed blocks of
+// PIPE_B positions (round robin) and apply published steps k to positions
+// x <= i_{k+L} - WH, several steps per pass; each publishes its progress.
+// The head waits only for the owners of its entering positions, L steps
+// behind.  Result: identical to the grid kernel (and the oracle).
+constexpr int PIPE_L = 2;      // bulk lag (steps) the head absorbs
+constexpr int PIPE_CT = 256;    // compute threads of the head (8 warps)
+constexpr int PIPE_T = PIPE_CT + 32;  // + the head's control warp
+constexpr int PIPE_B = 256;     // positions per bulk block
+constexpr int PIPE_MAXB = 4;    // steps per bulk pass
+
+struct PipeArgs {
+    const uint32_t* a;
+    const uint32_t* b;
+    uint32_t* q;
+    uint32_t* r;
+    int64_t na, nb;
+    int S;
+    FieldParams F;
+    uint32_t* A;            // working copy of the dividend (L2 resident)
+    uint32_t* h_glob;       // inverse series (S words)
+    unsigned* published;    // steps whose lambdas are in q
+    unsigned* progress;     // per bulk CTA: steps applied to all of its blocks
+    long long* stats;       // optional (MMM_DIV_STATS): cycle counters
+};
+
+namespace {
+
+__device__ __forceinline__ void bar_sync_n(int id, int n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ unsigned pipe_ld_acquire(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void pipe_st_release(unsigned* p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// i(k): the top of step k's heads (db - 1 once all steps are done)
+__device__ __forceinline__ int64_t pipe_i(int64_t na, int64_t db, int S, int64_t k) {
+    const int64_t v = na - 1 - k * S;
+    return v > db - 1 ? v : db - 1;
+}
+
+// v[k] = the reduced sum over the quad's P parts (adjacent lanes, P a power
+// of two <= 32) of accumulator k, on every part's lane.  Lane `part` then
+// stores the words r = part, part + P, ... < 4 of the quad.
+__device__ __forceinline__ void quad_reduce(uint64_t (&acc)[4], int P, uint32_t (&v)[4],
+                                            const FieldParams& F) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = reduce(acc[k], F);
+    for (int d = 1; d < P; d <<= 1)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) v[k] = addmod(v[k], __shfl_xor_sync(0xffffffffu, v[k], d), F);
+}
+
+}  // namespace
+
+__device__ void pipe_head(const PipeArgs& g, uint32_t* sm, int nbulk) {
+    constexpr int L = PIPE_L, CT = PIPE_CT;
+    const FieldParams F = g.F;
+    const int S = g.S, tid = threadIdx.x, WH = 2 * S, WR = 4 * S;  // ring size (pow2 >= 3S)
+    const int logS = 31 - __clz(S);
+    const int64_t na = g.na, db = g.nb - 1;
+    const int64_t J = (na - db + S - 1) / S;
+    const bool control = tid >= CT;  // warp 8: publish, poll owners, stage entering words
+    // shared layout (16-byte aligned pieces)
+    const int horg = ((S / 4 + 3) & ~3) + 3 > 67 ? ((S / 4 + 3) & ~3) + 3 : 67;
+    uint32_t* hz = sm;                                   // h at hz[horg + m]
+    uint32_t* hd = hz + ((horg + S + 8 + 3) & ~3);      // heads, S words
+    uint32_t* lamh = hd + S;                             // L x S negated lambdas
+    uint32_t* win = lamh + L * S;                        // ring by absolute position
+    uint32_t* stage = win + WR;                          // 2 x S entering words
+    uint32_t* bt3 = stage + 2 * S;                       // bt3[3 + m] = b[db - m]
+    const int MB = (L + 2) * S + 16;
+    for (int m = tid; m < horg + S + 8; m += PIPE_T) {
+        const int j = m - horg;
+        hz[m] = (j >= 0 && j < S) ? __ldcg(g.h_glob + j) : 0u;
+    }
+    for (int m = tid; m < MB; m += PIPE_T) {
+        const int64_t x = db - (m - 3);
+        bt3[m] = (m >= 3 && x >= 0) ? g.b[x] : 0u;
+    }
+    for (int m = tid; m < L * S; m += PIPE_T) lamh[m] = 0u;
+    const int64_t i0 = na - 1;
+    for (int t = tid; t < WH; t += PIPE_T) {  // initial window: positions i0 - t
+        const int64_t x = i0 - t;
+        win[x & (WR - 1)] = x >= 0 ? __ldcg(g.A + x) : 0u;
+    }
+    // entering words of slide j: [i(j+1) - WH + 1, i(j) - WH], loaded by the
+    // control warp one step ahead once their bulk owners applied steps <= j-L
+    auto stage_entering = [&](int64_t jj) {
+        const int64_t hi = pipe_i(na, db, S, jj) - WH, lo = pipe_i(na, db, S, jj + 1) - WH + 1;
+        if (hi < 0 || hi < lo) return;
+        const int lane = tid & 31;
+        const int64_t need = jj - L + 1;
+        if (lane < 2 && need > 0) {
+            const int64_t x = lane == 0 ? (lo > 0 ? lo : 0) : hi;
+            const int owner = int((x / PIPE_B) % nbulk);
+            while (int64_t(pipe_ld_acquire(g.progress + owner)) < need) {
+            }
+        }
+        __syncwarp();
+        uint32_t* st = stage + (jj & 1) * S;
+        for (int64_t x = lo + lane; x <= hi; x += 32) st[x - lo] = x >= 0 ? __ldcg(g.A + x) : 0u;
+    };
+    if (control) stage_entering(0);
+    __syncthreads();
+    // lambda tiling: S/4 quads x PL parts over the S head terms
+    const int PL = (S / 4) < (1024 / S) ? (S / 4) : (1024 / S);
+    const int logPL = 31 - __clz(PL), SPANL = S / PL;
+    long long c_loop = clock64(), c_pub = 0, c_stage = 0, c_lam = 0, c_win = 0, c_ent = 0;
+    for (int64_t j = 0; j < J; ++j) {
+        const int64_t i = pipe_i(na, db, S, j), inext = pipe_i(na, db, S, j + 1);
+        const int v = int(i - inext);
+        if (control) {
+            bar_sync_n(2, PIPE_T);  // lambdas of step j written
+            const long long c0 = clock64();
+            if ((tid & 31) == 0) {
+                __threadfence();
+                pipe_st_release(g.published, unsigned(j + 1));
+            }
+            const long long c1 = clock64();
+            stage_entering(j + 1);
+            c_pub += c1 - c0;
+            c_stage += clock64() - c1;
+            continue;
+        }
+        const long long p0 = clock64();
+        for (int t = tid; t < S; t += CT) hd[t] = t < v ? win[(i - t) & (WR - 1)] : 0u;
+        bar_sync_n(1, CT);
+        // lambda_k = sum_{t<=k} h[k-t] * hd[t], k < v
+        if (tid < ((S / 4) << logPL)) {
+            const int part = tid & (PL - 1), q4 = tid >> logPL, k0 = 4 * q4, t0 = part * SPANL;
+            uint64_t acc[4] = {0, 0, 0, 0};
+            uint32_t since = 0;
+            if (t0 <= k0 + 3)
+                conv_accumulate<4>(acc, hd + t0, SPANL / 4, hz, horg + k0 - t0, since, F);
+            uint32_t lv[4];
+            quad_reduce(acc, PL, lv, F);
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const int k = k0 + r;
+                if ((r & (PL - 1)) == part && part < 4) {
+                    if (k < v) {
+                        g.q[i - db - k] = lv[r];
+                        lamh[(j % L) * S + k] = negmod(lv[r], F);
+                    } else {
+                        lamh[(j % L) * S + k] = 0u;
+                    }
+                }
+            }
+        }
+        bar_sync_n(2, PIPE_T);  // with the control warp: publish step j
+        const long long p1 = clock64();
+        c_lam += p1 - p0;
+        // window (t in [v, WH)): step j; entering words copied in from the stage
+        {
+            const int tq = v & ~3, NQ = (WH - tq) >> 2;
+            int logP = 0;
+            while (logP < 5 && (NQ << (logP + 1)) <= CT && (S >> (logP + 1)) >= 4 &&
+                   ((S >> (logP + 1)) & 3) == 0)
+                ++logP;
+            const int P = 1 << logP, SPAN = S >> logP, vp = (v + 3) & ~3;
+            for (int it0 = 0; it0 < (NQ << logP); it0 += CT) {
+                const int it = it0 + tid;
+                const bool live = it < (NQ << logP);
+                const int part = it & (P - 1), t0 = tq + 4 * (it >> logP), k0 = part * SPAN;
+                uint64_t acc[4] = {0, 0, 0, 0};
+                uint32_t since = 0;
+                if (live && k0 < vp)
+                    conv_accumulate<4>(acc, lamh + (j % L) * S + k0, min(SPAN, vp - k0) / 4, bt3,
+                                       t0 - k0 + 3, since, F);
+                uint32_t add[4];
+                quad_reduce(acc, P, add, F);
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const int t = t0 + r;
+                    const int64_t x = i - t;
+                    if (live && (r & (P - 1)) == part && part < 4 && t >= v && t < WH && x >= 0) {
+                        uint32_t* w = win + (x & (WR - 1));
+                        *w = addmod(*w, add[r], F);
+                    }
+                }
+            }
+            const uint32_t* st = stage + (j & 1) * S;
+            for (int u = tid; u < v; u += CT) {  // t = WH + u, x = i - WH - u
+                const int64_t x = i - WH - u;
+                if (x >= 0) win[x & (WR - 1)] = st[(i - WH - (inext - WH + 1)) - u];
+            }
+        }
+        bar_sync_n(1, CT);
+        const long long p2 = clock64();
+        c_win += p2 - p1;
+        // entering (t in [WH, WH + v)): steps j - L + 1 .. j
+        {
+            const int NQ = (v + 3) >> 2, TT = L * S;
+            int logP = 0;
+            while (logP < 5 && (NQ << (logP + 1)) <= CT && (TT >> (logP + 1)) >= 4 &&
+                   ((TT >> (logP + 1)) & 3) == 0)  // whole conv blocks per part
+                ++logP;
+            const int P = 1 << logP, SPAN = TT >> logP;
+            for (int it0 = 0; it0 < (NQ << logP); it0 += CT) {
+                const int it = it0 + tid;
+                const bool live = it < (NQ << logP);
+                const int part = it & (P - 1), t0 = WH + 4 * (it >> logP);
+                uint64_t acc[4] = {0, 0, 0, 0};
+                uint32_t since = 0;
+                for (int c0 = part * SPAN; live && c0 < (part + 1) * SPAN;) {
+                    const int d = c0 >> logS, k0 = c0 & (S - 1);
+                    const int n = min(S - k0, (part + 1) * SPAN - c0);
+                    const int lim = d == 0 ? ((v + 3) & ~3) : S;
+                    if (j - d >= 0 && k0 < lim)
+                        conv_accumulate<4>(acc, lamh + ((j - d) % L) * S + k0, min(n, lim - k0) / 4,
+                                           bt3, t0 + d * S - k0 + 3, since, F);
+                    c0 += n;
+                }
+                uint32_t add[4];
+                quad_reduce(acc, P, add, F);
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const int t = t0 + r;
+                    const int64_t x = i - t;
+                    if (live && (r & (P - 1)) == part && part < 4 && t < WH + v && x >= 0) {
+                        uint32_t* w = win + (x & (WR - 1));
+                        *w = addmod(*w, add[r], F);
+                    }
+                }
+            }
+        }
+        bar_sync_n(1, CT);
+        c_ent += clock64() - p2;
+    }
+    if (g.stats && tid == 0) {
+        g.stats[0] = J;
+        g.stats[1] = clock64() - c_loop;
+        g.stats[8] = c_lam;
+        g.stats[9] = c_win;
+        g.stats[10] = c_ent;
+    }
+    if (g.stats && tid == CT) {
+        g.stats[2] = c_pub;
+        g.stats[3] = c_stage;
+    }
+    // the final window holds the top of the remainder
+    __syncthreads();
+    for (int t = tid; t < WH; t += PIPE_T) {
+        const int64_t x = (db - 1) - t;
+        if (x >= 0) __stcg(g.A + x, win[x & (WR - 1)]);
+    }
+}
+
+__device__ void pipe_bulk(const PipeArgs& g, uint32_t* sm, int nbulk, int me) {
+    constexpr int L = PIPE_L;
+    const FieldParams F = g.F;
+    const int S = g.S, tid = threadIdx.x, WH = 2 * S;
+    const int64_t na = g.na, db = g.nb - 1;
+    const int64_t J = (na - db + S - 1) / S;
+    const int64_t nblocks = (na + PIPE_B - 1) / PIPE_B;  // every position below the heads
+    uint32_t* lam = sm;               // reversed negated lambdas of one step, S words
+    uint32_t* bw = lam + S + 4;       // b window: PIPE_B + S + 8 words
+    __shared__ unsigned pub_s;
+    // 4 positions per thread, 4 parts over the step's terms: PIPE_B/4 x 4 = the
+    // first PIPE_B threads (whole warps; the ninth warp only stages and syncs)
+    static_assert(PIPE_B == PIPE_CT, "pipe_bulk: one quad x part per compute thread");
+    const bool worker = tid < PIPE_B;
+    const int part = tid & 3, qd = tid >> 2;
+    long long c_wait = 0, c_work = 0, passes = 0;
+    int64_t k = 0;
+    while (k < J) {
+        const long long tw = clock64();
+        if (tid == 0) {
+            unsigned p;
+            while ((p = pipe_ld_acquire(g.published)) <= unsigned(k)) {
+            }
+            pub_s = p;
+        }
+        __syncthreads();
+        const long long tb = clock64();
+        c_wait += tb - tw;
+        ++passes;
+        const int64_t kend = min(int64_t(pub_s), k + int64_t(PIPE_MAXB));
+        for (int64_t beta = me; beta < nblocks; beta += nbulk) {
+            const int64_t blo = beta * PIPE_B, bhi = min(blo + int64_t(PIPE_B), na);
+            const int64_t x0 = blo + 4 * qd;
+            uint64_t acc[4] = {0, 0, 0, 0};  // sum of per-step canonical partials
+            bool touched = false, mine = false;  // mine: x0 + part got a step (store it)
+            for (int64_t kk = k; kk < kend; ++kk) {
+                const int64_t ik = pipe_i(na, db, S, kk);
+                const int64_t v = ik - pipe_i(na, db, S, kk + 1);
+                const int64_t xlo = ik - v + 1 - db;
+                const int64_t top = min(pipe_i(na, db, S, kk + L) - int64_t(WH), ik - v);
+                if (bhi - 1 < xlo || blo > top) continue;  // uniform over the CTA
+                touched = true;
+                if (x0 + part >= xlo && x0 + part <= top) mine = true;
+                const int vp = int((v + 3) & ~3);
+                __syncthreads();  // previous step's staging consumed
+                for (int u = tid; u < vp; u += PIPE_T) {  // lam[u] = nl_{v-1-u}
+                    const int64_t kp = v - 1 - u;
+                    lam[u] = kp >= 0 ? negmod(__ldcg(g.q + (ik - db - kp)), F) : 0u;
+                }
+                const int64_t bwlo = blo - ik + db + v - vp;  // bw[y] = b[bwlo + y]
+                for (int y = tid; y < PIPE_B + vp + 8; y += PIPE_T) {
+                    const int64_t bx = bwlo + y;
+                    bw[y] = (bx >= 0 && bx <= db) ? __ldcg(g.b + bx) : 0u;
+                }
+                __syncthreads();
+                // part's terms: [u0, u0 + n), multiples of 4
+                const int span = ((vp / 4 + 3) & ~3) > 4 ? ((vp / 4 + 3) & ~3) : 4;
+                const int u0 = part * span;
+                if (worker && u0 < vp) {
+                    uint64_t pa[4] = {0, 0, 0, 0};
+                    uint32_t since = 0;
+                    conv_accumulate<4>(pa, lam + u0, min(span, vp - u0) / 4, bw,
+                                       4 * qd + vp - 1 - u0, since, F);
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        const int64_t x = x0 + r;
+                        if (x >= xlo && x <= top && x < bhi) acc[r] += reduce(pa[r], F);
+                    }
+                }
+            }
+            if (!touched || !worker) continue;
+            uint32_t add[4];
+            quad_reduce(acc, 4, add, F);
+            const uint32_t ad = part == 0 ? add[0] : part == 1 ? add[1] : part == 2 ? add[2] : add[3];
+            // store only positions a step updated: the rest may belong to the
+            // head, whose final window must not be overwritten by a late pass
+            const int64_t x = x0 + part;
+            if (mine && x < bhi) __stcg(g.A + x, addmod(__ldcg(g.A + x), ad, F));
+        }
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence();
+            pipe_st_release(g.progress + me, unsigned(kend));
+        }
+        c_work += clock64() - tb;
+        k = kend;
+    }
+    if (g.stats && me == 0 && tid == 0) {
+        g.stats[5] = c_wait;
+        g.stats[6] = c_work;
+        g.stats[7] = passes;
+    }
+}
+
+__global__ void __launch_bounds__(PIPE_T) div_pipe_kernel(PipeArgs g) {
+    extern __shared__ __align__(16) uint32_t smem[];
+    cg::grid_group grid = cg::this_grid();
+    const int64_t na = g.na, db = g.nb - 1;
+    for (int64_t i = int64_t(blockIdx.x) * PIPE_T + threadIdx.x; i < na;
+         i += int64_t(gridDim.x) * PIPE_T)
+        g.A[i] = g.a[i];
+    if (blockIdx.x == 0 && threadIdx.x < 32)
+        inverse_series(g.h_glob, g.S, db,
+                       [&](int64_t t) { return t <= db ? __ldcg(g.b + (db - t)) : 0u; }, g.F);
+    grid.sync();
+    const int nbulk = gridDim.x - 1;
+    if (blockIdx.x == 0)
+        pipe_head(g, smem, nbulk);
+    else
+        pipe_bulk(g, smem, nbulk, blockIdx.x - 1);
+    grid.sync();
+    for (int64_t x = int64_t(blockIdx.x) * PIPE_T + threadIdx.x; x < db;
+         x += int64_t(gridDim.x) * PIPE_T)
+        g.r[x] = __ldcg(g.A + x);
+}
+
 namespace {
 
 int pick_R(const FieldParams& F) { return F.fold_terms >= 8 ? 8 : (F.fold_terms >= 2 ? 2 : 1); }
@@ -294,6 +679,62 @@ void run_grid(DivArgs g, cudaStream_t st) {
     check_launch("div_grid_kernel");
 }
 
+// Pipelined schedule (div_pipe_kernel): S = s rounded down to a power of two
+// in [32, 256] (the result does not depend on S); needs 4 products per fold.
+bool pipe_eligible(const FieldParams& F, int64_t s) { return s >= 32 && F.fold_terms >= 8; }
+
+void run_pipe(const DivArgs& d, int64_t s, cudaStream_t st) {
+    int S = 32;
+    while (S * 2 <= s && S < 256) S *= 2;
+    PipeArgs g{};
+    g.a = d.a;
+    g.b = d.b;
+    g.q = d.q;
+    g.r = d.r;
+    g.na = d.na;
+    g.nb = d.nb;
+    g.S = S;
+    g.F = d.F;
+    const int L = PIPE_L;
+    const int horg = std::max(((S / 4 + 3) & ~3) + 3, 67);
+    const size_t head =
+        size_t(((horg + S + 8 + 3) & ~3) + S + L * S + 4 * S + 2 * S + (L + 2) * S + 16);
+    const size_t bulk = size_t(S + 4 + PIPE_B + S + 8 + 8);
+    const size_t bytes = std::max(head, bulk) * 4;
+    MMM_CUDA(cudaFuncSetAttribute(div_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(bytes)));
+    int per_sm = 0;
+    MMM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, div_pipe_kernel, PIPE_T, bytes));
+    if (per_sm < 1) throw Error(ST_SIM, "division: pipelined grid does not fit");
+    // one CTA per SM (the head's SM to itself), no more bulk CTAs than blocks
+    const int blocks = int(std::min<int64_t>(sm_count(), 1 + ceil_div(d.na, PIPE_B)));
+    Scratch sc(st);
+    g.A = sc.get<uint32_t>(size_t(d.na));
+    g.h_glob = sc.get<uint32_t>(size_t(S));
+    g.published = sc.get<unsigned>(size_t(blocks) + 1);
+    g.progress = g.published + 1;
+    MMM_CUDA(cudaMemsetAsync(g.published, 0, (size_t(blocks) + 1) * sizeof(unsigned), st));
+    const bool want_stats = getenv("MMM_DIV_STATS") != nullptr;
+    if (want_stats) {
+        g.stats = sc.get<long long>(12);
+        MMM_CUDA(cudaMemsetAsync(g.stats, 0, 12 * sizeof(long long), st));
+    }
+    void* params[] = {&g};
+    MMM_CUDA(cudaLaunchCooperativeKernel((void*)div_pipe_kernel, dim3(unsigned(blocks)),
+                                         dim3(PIPE_T), params, bytes, st));
+    check_launch("div_pipe_kernel");
+    if (want_stats) {
+        long long h[12];
+        MMM_CUDA(cudaMemcpyAsync(h, g.stats, sizeof(h), cudaMemcpyDeviceToHost, st));
+        MMM_CUDA(cudaStreamSynchronize(st));
+        fprintf(stderr,
+                "div pipe stats: S=%d blocks=%d steps=%lld head_loop=%lld ctl_publish=%lld "
+                "ctl_stage=%lld | hd+lambda=%lld window=%lld entering=%lld | bulk0 wait=%lld "
+                "work=%lld passes=%lld\n",
+                S, blocks, h[0], h[1], h[2], h[3], h[8], h[9], h[10], h[5], h[6], h[7]);
+    }
+}
+
 }  // namespace
 
 void launch_divmod(const FieldParams& F, const uint32_t* a, int64_t na, const uint32_t* b,
@@ -322,6 +763,10 @@ void launch_divmod(const FieldParams& F, const uint32_t* a, int64_t na, const ui
             case 2: run_cta<2>(g, 1, st); break;
             default: run_cta<1>(g, 1, st); break;
         }
+        return;
+    }
+    if (pipe_eligible(F, s) && !getenv("MMM_DIV_GRID")) {
+        run_pipe(g, s, st);
         return;
     }
     switch (R) {

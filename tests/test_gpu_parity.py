@@ -338,3 +338,25 @@ def test_fast_division_roundtrip_at_scale(cuda_lib):
     qb = cuda_lib.ntt_mul(q, b, P).astype(np.int64)
     qb[: len(r)] = (qb[: len(r)] + r) % P
     assert np.array_equal(qb, a.astype(np.int64))
+
+
+# ------------------------------------------ pipelined single-instance division --
+@pytest.mark.parametrize("p", [469762049, 101, 7, 2, 2147483647])
+def test_division_pipelined_shapes(cuda_lib, port, p):
+    """Large single divisions take the pipelined head/bulk schedule (s >= 32,
+    S = s rounded to a power of two in [32, 256]); p = 2^31 - 1 falls back to
+    the grid schedule.  Quotient lengths that are not multiples of S (short
+    last step), remainders shorter than the head window, remainder lengths
+    that are not multiples of the bulk block, every S: exactly the oracle."""
+    mmm = cuda_lib
+    rng = np.random.default_rng(p % 1000)
+    for na, nb in [(12000, 6000), (9001, 700), (5000, 4097), (7000, 300), (20000, 19000),
+                   (4500, 30)]:
+        a = rng.integers(0, p, na)
+        b = rng.integers(0, p, nb)
+        a[-1] = max(a[-1], 1)
+        b[-1] = max(b[-1], 1)
+        wq, wr = port.divmod(a, b, p)
+        for s in (32, 100, 128, 256, 1000):
+            q, r = mmm.divmod(a, b, p, s=s)
+            assert np.array_equal(q, wq) and np.array_equal(r, wr), (p, na, nb, s)
