@@ -281,11 +281,6 @@ namespace {
 __device__ __forceinline__ void bar_sync_n(int id, int n) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
-__device__ __forceinline__ unsigned pipe_ld_acquire(const unsigned* p) {
-    unsigned v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
 __device__ __forceinline__ void pipe_st_release(unsigned* p, unsigned v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -351,8 +346,7 @@ __device__ void pipe_head(const PipeArgs& g, uint32_t* sm, int nbulk) {
         if (lane < 2 && need > 0) {
             const int64_t x = lane == 0 ? (lo > 0 ? lo : 0) : hi;
             const int owner = int((x / PIPE_B) % nbulk);
-            while (int64_t(pipe_ld_acquire(g.progress + owner)) < need) {
-            }
+            spin_until_geq_fence(g.progress + owner, unsigned(need));
         }
         __syncwarp();
         uint32_t* st = stage + (jj & 1) * S;
@@ -523,12 +517,7 @@ __device__ void pipe_bulk(const PipeArgs& g, uint32_t* sm, int nbulk, int me) {
     int64_t k = 0;
     while (k < J) {
         const long long tw = clock64();
-        if (tid == 0) {
-            unsigned p;
-            while ((p = pipe_ld_acquire(g.published)) <= unsigned(k)) {
-            }
-            pub_s = p;
-        }
+        if (tid == 0) pub_s = spin_until_geq_fence(g.published, unsigned(k) + 1u);
         __syncthreads();
         const long long tb = clock64();
         c_wait += tb - tw;
@@ -598,7 +587,7 @@ __device__ void pipe_bulk(const PipeArgs& g, uint32_t* sm, int nbulk, int me) {
     }
 }
 
-__global__ void __launch_bounds__(PIPE_T) div_pipe_kernel(PipeArgs g) {
+__global__ void __launch_bounds__(PIPE_T, 1) div_pipe_kernel(PipeArgs g) {
     extern __shared__ __align__(16) uint32_t smem[];
     cg::grid_group grid = cg::this_grid();
     const int64_t na = g.na, db = g.nb - 1;

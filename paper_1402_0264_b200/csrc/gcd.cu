@@ -716,9 +716,7 @@ __device__ __forceinline__ void st_release_gpu(unsigned* p, unsigned v) {
 // Thread 0 waits until *p >= target; the CTA then proceeds together.  A pure
 // spin: one L2 round trip in flight per CTA, and no sleep wake-up delay.
 __device__ __forceinline__ void cta_wait_ge(const unsigned* p, unsigned target) {
-    if (threadIdx.x == 0)
-        while (ld_acquire_gpu(p) < target) {
-        }
+    if (threadIdx.x == 0) spin_until_geq(p, target);
     __syncthreads();
 }
 
@@ -830,8 +828,7 @@ __device__ int head_cta(const GcdArgs& g, BatchMeta& ctl, StepLog* log, uint32_t
         } else {
             // prefetch: S_j complete once the bulk applied batch j-1
             if (threadIdx.x == 96)
-                while (ld_acquire_gpu(g.flags + 1) < unsigned(j) * nbulk) {
-                }
+                spin_until_geq(g.flags + 1, unsigned(j) * nbulk);
             bar_sync(1, GCD_T - 96);  // warps 3-7 (warp 7 may come from its publish)
             const long long da0 = da0s[j & 1], db0 = db0s[j & 1];
             for (int i = threadIdx.x - 96; i < W1 + PL; i += GCD_T - 96) {
@@ -886,8 +883,7 @@ __device__ int head_cta(const GcdArgs& g, BatchMeta& ctl, StepLog* log, uint32_t
         bar_sync(2, BUILDERS);
         if (fallback) {
             if (threadIdx.x == 0)
-                while (ld_acquire_gpu(g.flags + 1) < unsigned(j + 1) * nbulk) {
-                }
+                spin_until_geq(g.flags + 1, unsigned(j + 1) * nbulk);
             bar_sync(2, BUILDERS);
             if (warp == 0) {
                 long long da = m.da1, db = m.db1;
