@@ -960,16 +960,27 @@ __device__ void apply_batch(const GcdArgs& g, const BatchMeta& m, const uint32_t
         }
         __syncthreads();
         const int items = 4 * (qn[0] + qn[1]);
+        // selects instead of runtime-indexed arrays (those live in local memory)
+        const int h00 = m.hi[0], h01 = m.hi[1], h10 = m.hi[2], h11 = m.hi[3];
+        uint32_t* const W0 = W[0];
+        uint32_t* const W1 = W[1];
+        uint32_t* const W2 = W[2];
+        uint32_t* const W3 = W[3];
+        const int n0 = n[0], n1 = n[1], qn0 = qn[0];
+        const long long xs0 = xs[0], xs1 = xs[1];
+        uint32_t* const out0 = out[0];
+        uint32_t* const out1 = out[1];
         for (int it0 = 0; it0 < items; it0 += GCD_T) {
             const int item = it0 + tid, q = item >> 2, part = item & 3;
-            const int r = q < qn[0] ? 0 : 1, qi = q - (r ? qn[0] : 0);
+            const int r = q < qn0 ? 0 : 1, qi = q - (r ? qn0 : 0);
             const int t = part >> 1, e0 = (part & 1) * (PL / 2);
             uint64_t acc[4] = {0, 0, 0, 0};
             uint32_t since = 0;
-            const int h = m.hi[2 * r + t];
+            const int h = r ? (t ? h11 : h10) : (t ? h01 : h00);
             if (item < items && h >= e0) {
                 const int nblk = (min(h + 1, e0 + PL / 2) - e0 + 3) >> 2;
-                conv_accumulate<4>(acc, P + (2 * r + t) * PL + e0, nblk, W[2 * r + t],
+                uint32_t* const Wrt = r ? (t ? W3 : W2) : (t ? W1 : W0);
+                conv_accumulate<4>(acc, P + (2 * r + t) * PL + e0, nblk, Wrt,
                                    4 * qi + PL - 1 - e0, since, F);
             }
             uint32_t v[4];
@@ -980,9 +991,9 @@ __device__ void apply_batch(const GcdArgs& g, const BatchMeta& m, const uint32_t
 #pragma unroll
             for (int k = 0; k < 4; ++k) v[k] = addmod(v[k], __shfl_xor_sync(0xffffffffu, v[k], 2), F);
             const int i = 4 * qi + part;  // part k stores output k of the quad
-            if (item < items && i < n[r]) {
+            if (item < items && i < (r ? n1 : n0)) {
                 const uint32_t o = part == 0 ? v[0] : part == 1 ? v[1] : part == 2 ? v[2] : v[3];
-                __stcg(out[r] + xs[r] + i, o);
+                __stcg((r ? out1 + xs1 : out0 + xs0) + i, o);
             }
         }
     }
@@ -1007,7 +1018,7 @@ __device__ int bulk_cta(const GcdArgs& g, uint32_t* sm, int nbulk, int me) {
         // flags[0], and no bulk CTA can finish batch j before that release.
         __syncthreads();  // ms
         const long long tb = clock64();
-        const BatchMeta m = ms;
+        const BatchMeta& m = ms;  // shared: runtime-indexed fields stay out of local memory
         if (m.steps > 0 && !m.err) {
             const long long na1 = m.da1 + 1 > 0 ? m.da1 + 1 : 0;
             const long long nb1 = m.db1 + 1 > 0 ? m.db1 + 1 : 0;
