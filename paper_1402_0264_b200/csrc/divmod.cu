@@ -338,6 +338,7 @@ __device__ void pipe_head(const PipeArgs& g, uint32_t* sm, int nbulk) {
     }
     // entering words of slide j: [i(j+1) - WH + 1, i(j) - WH], loaded by the
     // control warp one step ahead once their bulk owners applied steps <= j-L
+    long long c_poll = 0, c_waitA = 0;
     auto stage_entering = [&](int64_t jj) {
         const int64_t hi = pipe_i(na, db, S, jj) - WH, lo = pipe_i(na, db, S, jj + 1) - WH + 1;
         if (hi < 0 || hi < lo) return;
@@ -346,7 +347,9 @@ __device__ void pipe_head(const PipeArgs& g, uint32_t* sm, int nbulk) {
         if (lane < 2 && need > 0) {
             const int64_t x = lane == 0 ? (lo > 0 ? lo : 0) : hi;
             const int owner = int((x / PIPE_B) % nbulk);
+            const long long cp = clock64();
             spin_until_geq_fence(g.progress + owner, unsigned(need));
+            c_poll += clock64() - cp;
         }
         __syncwarp();
         uint32_t* st = stage + (jj & 1) * S;
@@ -399,8 +402,10 @@ __device__ void pipe_head(const PipeArgs& g, uint32_t* sm, int nbulk) {
                 }
             }
         }
+        const long long pa = clock64();
         bar_sync_n(2, PIPE_T);  // with the control warp: publish step j
         const long long p1 = clock64();
+        c_waitA += p1 - pa;
         c_lam += p1 - p0;
         // window (t in [v, WH)): step j; entering words copied in from the stage
         {
@@ -485,10 +490,12 @@ __device__ void pipe_head(const PipeArgs& g, uint32_t* sm, int nbulk) {
         g.stats[8] = c_lam;
         g.stats[9] = c_win;
         g.stats[10] = c_ent;
+        g.stats[11] = c_waitA;
     }
     if (g.stats && tid == CT) {
         g.stats[2] = c_pub;
         g.stats[3] = c_stage;
+        g.stats[4] = c_poll;
     }
     // the final window holds the top of the remainder
     __syncthreads();
@@ -689,7 +696,9 @@ void run_pipe(const DivArgs& d, int64_t s, cudaStream_t st) {
     const size_t head =
         size_t(((horg + S + 8 + 3) & ~3) + S + L * S + 4 * S + 2 * S + (L + 2) * S + 16);
     const size_t bulk = size_t(S + 4 + PIPE_B + S + 8 + 8);
-    const size_t bytes = std::max(head, bulk) * 4;
+    // more than half an SM's shared memory: one CTA per SM, so no bulk CTA
+    // shares (and takes issue slots from) the head's SM
+    const size_t bytes = std::max<size_t>(std::max(head, bulk) * 4, 120 * 1024);
     MMM_CUDA(cudaFuncSetAttribute(div_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(bytes)));
     int per_sm = 0;
@@ -718,9 +727,10 @@ void run_pipe(const DivArgs& d, int64_t s, cudaStream_t st) {
         MMM_CUDA(cudaStreamSynchronize(st));
         fprintf(stderr,
                 "div pipe stats: S=%d blocks=%d steps=%lld head_loop=%lld ctl_publish=%lld "
-                "ctl_stage=%lld | hd+lambda=%lld window=%lld entering=%lld | bulk0 wait=%lld "
-                "work=%lld passes=%lld\n",
-                S, blocks, h[0], h[1], h[2], h[3], h[8], h[9], h[10], h[5], h[6], h[7]);
+                "ctl_stage=%lld (poll=%lld) | hd+lambda=%lld (waitA=%lld) window=%lld "
+                "entering=%lld | bulk0 wait=%lld work=%lld passes=%lld\n",
+                S, blocks, h[0], h[1], h[2], h[3], h[4], h[8], h[11], h[9], h[10], h[5], h[6],
+                h[7]);
     }
 }
 
