@@ -14,8 +14,8 @@
 // (< p each) meet in a 64-bit global accumulator through RED.ADD.64, and the
 // last item to arrive on a k-tile reduces it (no second launch) -- the ADD
 // rounds of the paper, done in L2 instead of log-round launches.  Batched
-// products give each instance whole k-tiles (no split).  (Double-buffered
-// cp.async staging was measured slower at 4-byte granularity: 72 vs 67 us.)
+// products give each instance whole k-tiles (no split).  Chunks are double
+// buffered through registers (cp.async at 4-byte granularity measured slower).
 #include "common.cuh"
 #include "conv.cuh"
 
@@ -43,8 +43,12 @@ template <int R>
 __global__ void __launch_bounds__(MUL_T) mul_kernel(MulArgs g) {
     constexpr int TK = MUL_T * R;
     constexpr int ORIGIN = MUL_TI + 3;  // == 3 (mod 4): aligned window reloads
-    __shared__ __align__(16) uint32_t sw[MUL_TI];
-    __shared__ __align__(16) uint32_t sv[MUL_TI + TK + 4];
+    constexpr int SV = MUL_TI + TK + 4;
+    constexpr int NW = (MUL_TI + MUL_T - 1) / MUL_T, NV = (SV + MUL_T - 1) / MUL_T;
+    // two buffers: the next chunk is loaded into registers while this one is
+    // multiplied, then written to the other buffer (one barrier per chunk)
+    __shared__ __align__(16) uint32_t sw[2][MUL_TI];
+    __shared__ __align__(16) uint32_t sv[2][SV];
 
     const int64_t inst = blockIdx.z;
     const uint32_t* __restrict__ a = g.a + inst * g.lda;
@@ -64,18 +68,43 @@ __global__ void __launch_bounds__(MUL_T) mul_kernel(MulArgs g) {
     for (int r = 0; r < R; ++r) acc[r] = 0;
     uint32_t since = 0;
     const int base = ORIGIN + int(threadIdx.x) * R;
-
+    const int tid = threadIdx.x;
+    uint32_t wr[NW], vr[NV];
+    auto fetch = [&](int64_t ic) {  // chunk [ic, ic + MUL_TI) into registers
+        const int cnt = int(i_end - ic < MUL_TI ? i_end - ic : MUL_TI);
+        const int64_t off = k0 - ic - ORIGIN;  // sv[x] = b[x + off]
+#pragma unroll
+        for (int k = 0; k < NW; ++k) {
+            const int u = tid + k * MUL_T;
+            wr[k] = (u < MUL_TI && u < cnt) ? a[ic + u] : 0u;
+        }
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            const int x = tid + k * MUL_T;
+            const int64_t j = x + off;
+            vr[k] = (x < SV && j >= 0 && j < nb) ? b[j] : 0u;
+        }
+    };
+    auto store = [&](int buf) {
+#pragma unroll
+        for (int k = 0; k < NW; ++k)
+            if (tid + k * MUL_T < MUL_TI) sw[buf][tid + k * MUL_T] = wr[k];
+#pragma unroll
+        for (int k = 0; k < NV; ++k)
+            if (tid + k * MUL_T < SV) sv[buf][tid + k * MUL_T] = vr[k];
+    };
+    fetch(i_begin);
+    store(0);
+    __syncthreads();
+    int buf = 0;
     for (int64_t ic = i_begin; ic < i_end; ic += MUL_TI) {
         const int cnt = int(i_end - ic < MUL_TI ? i_end - ic : MUL_TI);
+        const bool more = ic + MUL_TI < i_end;
+        if (more) fetch(ic + MUL_TI);  // in flight during the multiply
+        conv_accumulate<R>(acc, sw[buf], (cnt + R - 1) / R, sv[buf], base, since, g.F);
+        if (more) store(buf ^ 1);
         __syncthreads();
-        for (int u = threadIdx.x; u < MUL_TI; u += MUL_T) sw[u] = u < cnt ? a[ic + u] : 0u;
-        const int64_t off = k0 - ic - ORIGIN;  // sv[x] = b[x + off]
-        for (int x = threadIdx.x; x < MUL_TI + TK + 4; x += MUL_T) {
-            const int64_t j = x + off;
-            sv[x] = (j >= 0 && j < nb) ? b[j] : 0u;
-        }
-        __syncthreads();
-        conv_accumulate<R>(acc, sw, (cnt + R - 1) / R, sv, base, since, g.F);
+        buf ^= 1;
     }
 
     uint32_t* __restrict__ f = g.f + inst * g.ldf;
