@@ -509,9 +509,13 @@ class FastDivWork(DivWork):
 
 
 class NttWork(Workload):
-    """configs[3] (single): 2^20 x 2^20 product through a length-2^21 NTT."""
+    """configs[3] (single): 2^20 x 2^20 product through a length-2^21 NTT.
+    With N > 1 ranks the transform is sharded (four-step: column slices,
+    all-to-all, row slices, all-to-all, column slices, all-reduce of the
+    disjoint outputs; shard.ntt_mul_sharded) -- strong scaling."""
 
     name = "ntt"
+    sharded = True
 
     def __init__(self, s):
         import paper_1402_0264_b200 as mmm
@@ -521,9 +525,16 @@ class NttWork(Workload):
         self.want = golden()["cfg4_big"].get("f")
         self.nf = len(self.a) + len(self.b) - 1
         self.config = {"workload": "cfg4_ntt_2^20x2^20_N2^21_p469762049", "p": P, "seed": 42,
-                       "transform": "four-step 2^10 x 2^11, radix-2 Stockham in smem",
-                       "parallelism": "replicas", "units": "schoolbook-equivalent MACs",
+                       "transform": "four-step 2^10 x 2^11, radix-4/8 Stockham in smem",
+                       "parallelism": "single GPU", "units": "schoolbook-equivalent MACs",
                        "l2": "flushed between timed steps"}
+        self.world, self.dist = 1, None
+
+    def bind(self, dist):
+        self.dist, self.world = dist, dist.world
+        if dist.world > 1:
+            self.config["parallelism"] = (f"four-step NTT sharded over {dist.world} ranks: "
+                                          "2 NCCL all-to-alls + 1 all-reduce")
 
     def units(self):
         return float(len(self.a) * len(self.b))
@@ -534,8 +545,13 @@ class NttWork(Workload):
         self.df = torch.zeros(self.nf, dtype=torch.int32, device="cuda")
 
     def device_step(self, stream):
-        self.mmm.ntt_mul_dev(P, self.da.data_ptr(), len(self.a), self.db.data_ptr(), len(self.b),
-                             self.df.data_ptr(), stream=stream)
+        if self.world == 1:
+            self.mmm.ntt_mul_dev(P, self.da.data_ptr(), len(self.a), self.db.data_ptr(),
+                                 len(self.b), self.df.data_ptr(), stream=stream)
+        else:
+            from paper_1402_0264_b200.shard import ntt_mul_sharded
+            ntt_mul_sharded(self.mmm, P, self.da, len(self.a), self.db, len(self.b), self.df,
+                            self.dist.pg, self.world, self.dist.rank, stream)
 
     def device_check(self):
         if self.want:
@@ -547,7 +563,13 @@ class NttWork(Workload):
         self.bytes_out = 4 * self.nf
 
     def host_step(self):
-        return self.mmm.ntt_mul(self.ha, self.hb, P)
+        if self.world == 1:  # the host C-ABI call a user makes (mmm_cu_ntt_mul)
+            return self.mmm.ntt_mul(self.ha, self.hb, P)
+        import torch  # sharded: pinned H2D, the sharded product, D2H
+        self.da.copy_(self._ta, non_blocking=True)
+        self.db.copy_(self._tb, non_blocking=True)
+        self.device_step(torch.cuda.current_stream().cuda_stream)
+        return np.trim_zeros(self.df.cpu().numpy().view(np.uint32), "b")
 
     def host_check(self, f):
         if self.want:
@@ -555,6 +577,9 @@ class NttWork(Workload):
 
     def roofline(self, t_step, hbm, imad):
         r = ntt_roofline(21, 1, t_step, "ntt_rows")
+        if self.world > 1:  # this rank's share of the transform work
+            r["achieved"] /= self.world
+            r["frac"] /= self.world
         alg = 4.0 * (len(self.a) + len(self.b) + self.nf)
         r["hbm"] = {"achieved_gbs": alg / t_step / 1e9, "peak_gbs": hbm,
                     "frac": alg / t_step / 1e9 / hbm, "alg_bytes": alg}

@@ -116,6 +116,18 @@ int mmm_cu_mul_dev(int64_t p, const uint32_t* d_a, int64_t na, const uint32_t* d
                    int64_t s, uint32_t* d_f, void* stream);
 int mmm_cu_divmod_dev(int64_t p, const uint32_t* d_a, int64_t na, const uint32_t* d_b, int64_t nb,
                       int64_t s, uint32_t* d_q, uint32_t* d_r, void* stream);
+/* Sharded four-step NTT product (no reference symbol: SURVEY §8f item 4).
+ * mmm_cu_ntt_shape: the transform for nf = na+nb-1 outputs is N = n1 x n2.
+ * mmm_cu_ntt_phase_dev: phase 0 = forward column transforms [start, start+n)
+ * of both operands into the N-word workspaces (layout w[n2*k1 + col]);
+ * 1 = rows [start, start+n): forward, pointwise product, inverse (result in
+ * d_work_a); 2 = inverse columns [start, start+n) into d_f (nf words, only
+ * the positions of those columns).  Column slices are multiples of 4.  Ranks
+ * exchange workspace blocks between phases (paper_1402_0264_b200/shard.py). */
+int mmm_cu_ntt_shape(int64_t p, int64_t nf, int64_t* n1, int64_t* n2);
+int mmm_cu_ntt_phase_dev(int64_t p, int phase, const uint32_t* d_a, int64_t na,
+                         const uint32_t* d_b, int64_t nb, int64_t start, int64_t n,
+                         uint32_t* d_work_a, uint32_t* d_work_b, uint32_t* d_f, void* stream);
 int mmm_cu_divmod_fast_dev(int64_t p, const uint32_t* d_a, int64_t na, const uint32_t* d_b,
                            int64_t nb, uint32_t* d_q, uint32_t* d_r, void* stream);
 /* Coefficients [k0, k1) of the product into d_f[0, k1 - k0): one rank's slice of

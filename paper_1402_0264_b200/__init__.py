@@ -31,7 +31,7 @@ __all__ = [
     "LIB_PATH", "load", "MmmError", "InvalidArgument", "DomainError", "CudaError", "SimError",
     "Field", "Rng", "random_poly", "mul", "divmod", "gcd", "ntt_mul", "mul_batched",
     "divmod_batched", "ntt_mul_batched", "mul_dev", "mul_range_dev", "divmod_dev", "gcd_dev",
-    "divmod_fast", "divmod_fast_dev",
+    "divmod_fast", "divmod_fast_dev", "ntt_shape", "ntt_phase_dev",
     "ntt_mul_dev",
     "mul_batched_dev", "divmod_batched_dev", "ntt_mul_batched_dev", "launch_count",
 ]
@@ -84,6 +84,9 @@ SIGNATURES = {
     "mmm_cu_divmod_fast": (C.c_int, [_I64, _U32P, _I64, _U32P, _I64, _U32P, _I64, _I64P, _U32P,
                                      _I64, _I64P]),
     "mmm_cu_divmod_fast_dev": (C.c_int, [_I64, _VP, _I64, _VP, _I64, _VP, _VP, _VP]),
+    "mmm_cu_ntt_shape": (C.c_int, [_I64, _I64, _I64P, _I64P]),
+    "mmm_cu_ntt_phase_dev": (C.c_int, [_I64, C.c_int, _VP, _I64, _VP, _I64, _I64, _I64, _VP, _VP,
+                                       _VP, _VP]),
     "mmm_cu_gcd": (C.c_int, [_I64, _U32P, _I64, _U32P, _I64, _I64, _U32P, _I64, _I64P]),
     "mmm_cu_ntt_mul": (C.c_int, [_I64, _U32P, _I64, _U32P, _I64, _U32P, _I64, _I64P]),
     "mmm_cu_mul_batched": (C.c_int, [_I64, _U32P, _I64, _I64, _U32P, _I64, _I64, _I64, _I64,
@@ -251,6 +254,19 @@ def divmod_fast(a, b, p):
 
 def divmod_fast_dev(p, d_a, na, d_b, nb, d_q, d_r, stream=0):
     _check(load().mmm_cu_divmod_fast_dev(_pint(p), d_a, na, d_b, nb, d_q, d_r, stream))
+
+
+def ntt_shape(p, nf):
+    """(n1, n2): the four-step split of the NTT for an nf-word product."""
+    n1, n2 = C.c_int64(0), C.c_int64(0)
+    _check(load().mmm_cu_ntt_shape(_pint(p), nf, C.byref(n1), C.byref(n2)))
+    return n1.value, n2.value
+
+
+def ntt_phase_dev(p, phase, d_a, na, d_b, nb, start, n, d_work_a, d_work_b, d_f, stream=0):
+    """One phase of the sharded four-step NTT product (see include/mmm_cu.h)."""
+    _check(load().mmm_cu_ntt_phase_dev(_pint(p), phase, d_a, na, d_b, nb, start, n, d_work_a,
+                                       d_work_b, d_f, stream))
 
 
 def gcd(a, b, p, s: int = 64) -> np.ndarray:

@@ -302,6 +302,29 @@ int mmm_cu_divmod(int64_t p, const uint32_t* a, int64_t na, const uint32_t* b, i
     });
 }
 
+int mmm_cu_ntt_shape(int64_t p, int64_t nf, int64_t* n1, int64_t* n2) {
+    return guarded([&] {
+        const FieldParams F = field_or_throw(p);
+        if (nf < 1 || !ntt_supported(F.p, nf))
+            throw Error(ST_INVALID, "ntt: the prime has no 2-adic root for this length");
+        ntt_shape(F.p, nf, n1, n2);
+    });
+}
+
+int mmm_cu_ntt_phase_dev(int64_t p, int phase, const uint32_t* d_a, int64_t na,
+                         const uint32_t* d_b, int64_t nb, int64_t start, int64_t n,
+                         uint32_t* d_work_a, uint32_t* d_work_b, uint32_t* d_f, void* stream) {
+    return guarded([&] {
+        const FieldParams F = field_or_throw(p);
+        if (na < 1 || nb < 1 || phase < 0 || phase > 2)
+            throw Error(ST_INVALID, "ntt phase: bad operands or phase");
+        if (!ntt_supported(F.p, na + nb - 1))
+            throw Error(ST_INVALID, "ntt: the prime has no 2-adic root for this length");
+        launch_ntt_phase(F, phase, d_a, na, d_b, nb, start, n, d_work_a, d_work_b, d_f,
+                         as_stream(stream));
+    });
+}
+
 int mmm_cu_divmod_fast(int64_t p, const uint32_t* a, int64_t na, const uint32_t* b, int64_t nb,
                        uint32_t* q, int64_t q_cap, int64_t* nq, uint32_t* r, int64_t r_cap,
                        int64_t* nr) {

@@ -123,6 +123,11 @@ void launch_gcd(const FieldParams& F, const uint32_t* a, int64_t na, const uint3
 bool ntt_supported(uint32_t p, int64_t out_len);
 void launch_ntt_mul(const FieldParams& F, const uint32_t* a, int64_t na, const uint32_t* b,
                     int64_t nb, uint32_t* f, cudaStream_t st);
+// sharded four-step NTT product phases (ntt.cu); N = n1 * n2 for nf outputs
+void ntt_shape(uint32_t p, int64_t nf, int64_t* n1, int64_t* n2);
+void launch_ntt_phase(const FieldParams& F, int phase, const uint32_t* a, int64_t na,
+                      const uint32_t* b, int64_t nb, int64_t start, int64_t n, uint32_t* work_a,
+                      uint32_t* work_b, uint32_t* f, cudaStream_t st);
 void launch_ntt_mul_batched(const FieldParams& F, const uint32_t* A, int64_t lda, int64_t na,
                             const uint32_t* B, int64_t ldb, int64_t nb, int64_t count,
                             uint32_t* Fo, int64_t ldf, cudaStream_t st);

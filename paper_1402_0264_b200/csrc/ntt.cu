@@ -31,6 +31,7 @@ namespace mmm_cu {
 namespace {
 
 constexpr int NTT_T = 256;
+constexpr int NTT_PHASE_COLS = 4;  // column granularity of the sharded phases
 
 __device__ __forceinline__ uint32_t shoup(uint32_t x, uint32_t w, uint32_t wp, uint32_t p) {
     const uint32_t q = __umulhi(x, wp);
@@ -204,6 +205,7 @@ struct NttArgs {
     int64_t nf, ldf;
     int cols;           // columns per CTA in the column passes
     int logc;           // log2(cols)
+    int col0, row0;     // first column / row of this launch (sharded phases)
 };
 
 // K1: forward column transforms of both operands (grid.y = operand).
@@ -219,7 +221,7 @@ __global__ void __launch_bounds__(NTT_T) ntt_cols_fwd(NttArgs g) {
     uint2* tw = reinterpret_cast<uint2*>(sm);
     uint32_t* x = sm + N1;  // N1/2 uint2 = N1 words
     uint32_t* y = x + C * N1;
-    const int c0 = blockIdx.x * C;
+    const int c0 = g.col0 + blockIdx.x * C;
     for (int j = threadIdx.x; j < N1 / 2; j += NTT_T) tw[j] = P.r1f[j];
     for (int t = threadIdx.x; t < C * N1; t += NTT_T) {
         const int c = t & (C - 1), n1 = t >> g.logc;
@@ -240,7 +242,7 @@ __global__ void __launch_bounds__(NTT_T) ntt_rows(NttArgs g, FieldParams F) {
     extern __shared__ __align__(16) uint32_t sm[];
     const NttPlan& P = g.P;
     const int N2 = 1 << P.log2;
-    const int k1 = blockIdx.x;
+    const int k1 = g.row0 + blockIdx.x;
     const int64_t inst = blockIdx.z;
     uint32_t* wa = g.work[0] + (inst << P.logN) + int64_t(k1) * N2;
     const uint32_t* wb = g.work[1] + (inst << P.logN) + int64_t(k1) * N2;
@@ -284,7 +286,7 @@ __global__ void __launch_bounds__(NTT_T) ntt_cols_inv(NttArgs g) {
     uint2* tw = reinterpret_cast<uint2*>(sm);
     uint32_t* x = sm + N1;
     uint32_t* y = x + C * N1;
-    const int c0 = blockIdx.x * C;
+    const int c0 = g.col0 + blockIdx.x * C;
     for (int j = threadIdx.x; j < N1 / 2; j += NTT_T) tw[j] = P.r1i[j];
     for (int t = threadIdx.x; t < C * N1; t += NTT_T) {
         const int c = t & (C - 1), k1 = t >> g.logc;
@@ -449,6 +451,63 @@ void run_ntt(const FieldParams& F, const uint32_t* A, int64_t lda, int64_t na, c
 }
 
 }  // namespace
+
+// One phase of the four-step product over a slice (the sharded NTT, SURVEY
+// §8f): 0 = forward columns [start, start + n) of both operands into the
+// N-word workspaces, 1 = rows [start, start + n) (forward, pointwise,
+// inverse), 2 = inverse columns [start, start + n) into f (natural order,
+// only the positions of those columns).  Column slices are multiples of
+// NTT_PHASE_COLS.
+void launch_ntt_phase(const FieldParams& F, int phase, const uint32_t* a, int64_t na,
+                      const uint32_t* b, int64_t nb, int64_t start, int64_t n, uint32_t* work_a,
+                      uint32_t* work_b, uint32_t* f, cudaStream_t st) {
+    const int64_t nf = na + nb - 1;
+    const int logN = log2_len(nf);
+    if (logN > 30) throw Error(ST_INVALID, "ntt: product too long");
+    const NttPlan& P = get_plan(F.p, logN);
+    const int N1 = 1 << P.log1, N2 = 1 << P.log2;
+    NttArgs g{};
+    g.P = P;
+    g.in[0] = a;
+    g.in[1] = b;
+    g.len[0] = na;
+    g.len[1] = nb;
+    g.ld[0] = na;
+    g.ld[1] = nb;
+    g.nf = nf;
+    g.work[0] = work_a;
+    g.work[1] = work_b;
+    g.out = f;
+    g.ldf = nf;
+    g.cols = std::min(NTT_PHASE_COLS, N2);
+    g.logc = 0;
+    while ((1 << g.logc) < g.cols) ++g.logc;
+    const int64_t lim = phase == 1 ? N1 : N2;
+    if (n < 0 || start < 0 || start + n > lim || (phase != 1 && (start % g.cols || n % g.cols)))
+        throw Error(ST_INVALID, "ntt phase: slice outside the transform or not column-aligned");
+    if (n == 0) return;
+    const size_t sm1 = size_t(N1 + 2 * g.cols * N1) * 4;
+    const size_t sm2 = size_t(2 * N2 + 4 * N2) * 4;
+    if (phase == 1) {
+        MMM_CUDA(cudaFuncSetAttribute(ntt_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(sm2)));
+        g.row0 = int(start);
+        ntt_rows<<<dim3(unsigned(n), 1, 1), NTT_T, sm2, st>>>(g, F);
+        check_launch("ntt_rows");
+    } else {
+        auto fn = phase == 0 ? ntt_cols_fwd : ntt_cols_inv;
+        MMM_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm1)));
+        g.col0 = int(start);
+        fn<<<dim3(unsigned(n / g.cols), phase == 0 ? 2 : 1, 1), NTT_T, sm1, st>>>(g);
+        check_launch(phase == 0 ? "ntt_cols_fwd" : "ntt_cols_inv");
+    }
+}
+
+void ntt_shape(uint32_t p, int64_t nf, int64_t* n1, int64_t* n2) {
+    const int logN = log2_len(nf);
+    *n1 = int64_t(1) << (logN / 2);
+    *n2 = int64_t(1) << (logN - logN / 2);
+}
 
 bool ntt_supported(uint32_t p, int64_t out_len) {
     if (p < 3 || (p & 1) == 0) return false;

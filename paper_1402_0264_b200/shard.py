@@ -91,3 +91,119 @@ def gather_rows(local, dist, world: int):
                       device=local.device)
     dist.all_gather_into_tensor(out, local.contiguous())
     return out
+
+
+# --------------------------------------------------- sharded four-step NTT --
+class NttShards:
+    """Layout of the four-step NTT product over `world` ranks.
+
+    The N = n1 x n2 workspace w[n2*k1 + col] is a n1 x n2 matrix.  Rank r
+    owns the columns [r*n2/W, (r+1)*n2/W) in the column phases (0: forward
+    columns of both operands, 2: inverse columns into the output) and the rows
+    [r*n1/W, (r+1)*n1/W) in the row phase (1: forward rows, pointwise product,
+    inverse rows).  Between them the workspace blocks move with one
+    all-to-all each way: block (rows of q) x (cols of r) goes from r to q."""
+
+    def __init__(self, n1: int, n2: int, world: int):
+        if world < 1 or n1 % world or n2 % (4 * world):
+            raise ValueError(f"sharded NTT: {n1} x {n2} does not split over {world} ranks")
+        self.n1, self.n2, self.W = n1, n2, world
+        self.R, self.Cw = n1 // world, n2 // world
+
+    def cols(self, r: int):
+        return r * self.Cw, self.Cw
+
+    def rows(self, r: int):
+        return r * self.R, self.R
+
+    def _blocks(self, work):  # [W (row group), R, W (col group), Cw] view
+        return work.view(self.W, self.R, self.W, self.Cw)
+
+    def pack_to_rows(self, work, r: int):
+        """After phase 0 on rank r: chunk q = (rows of q) x (cols of r)."""
+        return self._blocks(work)[:, :, r, :].contiguous()
+
+    def unpack_rows(self, recv, work, r: int):
+        """recv[q] = (rows of r) x (cols of q), from rank q."""
+        self._blocks(work)[r] = recv.permute(1, 0, 2)
+
+    def pack_to_cols(self, work, r: int):
+        """After phase 1 on rank r: chunk q = (rows of r) x (cols of q)."""
+        return self._blocks(work)[r].permute(1, 0, 2).contiguous()
+
+    def unpack_cols(self, recv, work, r: int):
+        """recv[q] = (rows of q) x (cols of r), from rank q."""
+        self._blocks(work)[:, :, r, :] = recv
+
+
+def ntt_mul_sharded(mmm, p, d_a, na, d_b, nb, d_f, dist, world: int, rank: int, stream: int):
+    """f = a * b (nf = na+nb-1 words in d_f, int32 tensor on this rank's GPU)
+    with the NTT split over the ranks: three phase kernels, two all-to-alls of
+    workspace blocks and one all-reduce of the disjoint column outputs, all on
+    NCCL over NVLink.  d_a, d_b: replicated int32 device tensors."""
+    import torch
+
+    nf = na + nb - 1
+    n1, n2 = mmm.ntt_shape(p, nf)
+    sh = NttShards(n1, n2, world)
+    wa = torch.empty(n1 * n2, dtype=torch.int32, device=d_a.device)
+    wb = torch.empty_like(wa)
+    c0, cn = sh.cols(rank)
+    mmm.ntt_phase_dev(p, 0, d_a.data_ptr(), na, d_b.data_ptr(), nb, c0, cn, wa.data_ptr(),
+                      wb.data_ptr(), 0, stream)
+    if world > 1:
+        for w in (wa, wb):
+            send = sh.pack_to_rows(w, rank)
+            recv = torch.empty_like(send)
+            dist.all_to_all_single(recv, send)
+            sh.unpack_rows(recv, w, rank)
+    r0, rn = sh.rows(rank)
+    mmm.ntt_phase_dev(p, 1, d_a.data_ptr(), na, d_b.data_ptr(), nb, r0, rn, wa.data_ptr(),
+                      wb.data_ptr(), 0, stream)
+    if world > 1:
+        send = sh.pack_to_cols(wa, rank)
+        recv = torch.empty_like(send)
+        dist.all_to_all_single(recv, send)
+        sh.unpack_cols(recv, wa, rank)
+    d_f.zero_()
+    mmm.ntt_phase_dev(p, 2, d_a.data_ptr(), na, d_b.data_ptr(), nb, c0, cn, wa.data_ptr(),
+                      wb.data_ptr(), d_f.data_ptr(), stream)
+    if world > 1:
+        dist.all_reduce(d_f)  # every word was written by exactly one rank (< p < 2^31)
+    return d_f
+
+
+def ntt_mul_virtual(mmm, p, d_a, na, d_b, nb, world: int, stream: int):
+    """The sharded product with `world` virtual ranks on one GPU (the
+    all-to-alls become local block copies): exercises the phase kernels'
+    slices and the block layout exactly as ntt_mul_sharded runs them."""
+    import torch
+
+    nf = na + nb - 1
+    n1, n2 = mmm.ntt_shape(p, nf)
+    sh = NttShards(n1, n2, world)
+    wa = [torch.empty(n1 * n2, dtype=torch.int32, device=d_a.device) for _ in range(world)]
+    wb = [torch.empty_like(wa[0]) for _ in range(world)]
+    for r in range(world):
+        c0, cn = sh.cols(r)
+        mmm.ntt_phase_dev(p, 0, d_a.data_ptr(), na, d_b.data_ptr(), nb, c0, cn, wa[r].data_ptr(),
+                          wb[r].data_ptr(), 0, stream)
+    for ws in (wa, wb):
+        sends = [sh.pack_to_rows(ws[r], r) for r in range(world)]
+        for r in range(world):
+            sh.unpack_rows(torch.stack([sends[q][r] for q in range(world)]), ws[r], r)
+    for r in range(world):
+        r0, rn = sh.rows(r)
+        mmm.ntt_phase_dev(p, 1, d_a.data_ptr(), na, d_b.data_ptr(), nb, r0, rn, wa[r].data_ptr(),
+                          wb[r].data_ptr(), 0, stream)
+    sends = [sh.pack_to_cols(wa[r], r) for r in range(world)]
+    for r in range(world):
+        sh.unpack_cols(torch.stack([sends[q][r] for q in range(world)]), wa[r], r)
+    f = torch.zeros(nf, dtype=torch.int64, device=d_a.device)
+    for r in range(world):
+        fr = torch.zeros(nf, dtype=torch.int32, device=d_a.device)
+        c0, cn = sh.cols(r)
+        mmm.ntt_phase_dev(p, 2, d_a.data_ptr(), na, d_b.data_ptr(), nb, c0, cn, wa[r].data_ptr(),
+                          wb[r].data_ptr(), fr.data_ptr(), stream)
+        f += fr.to(torch.int64)
+    return f

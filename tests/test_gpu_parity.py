@@ -360,3 +360,46 @@ def test_division_pipelined_shapes(cuda_lib, port, p):
         for s in (32, 100, 128, 256, 1000):
             q, r = mmm.divmod(a, b, p, s=s)
             assert np.array_equal(q, wq) and np.array_equal(r, wr), (p, na, nb, s)
+
+
+# ------------------------------------------------------ sharded four-step NTT --
+def test_ntt_sharded_virtual_ranks(cuda_lib, port):
+    """The sharded NTT product (phase kernels over column/row slices, block
+    exchanges) with W = 1, 2, 4, 8 virtual ranks on one GPU equals the product,
+    for several primes and sizes; bad slices are rejected."""
+    import torch
+    from paper_1402_0264_b200.shard import ntt_mul_virtual
+    mmm = cuda_lib
+    rng = np.random.default_rng(13)
+    st = torch.cuda.current_stream().cuda_stream
+    for p, na, nb in [(469762049, 3000, 2000), (998244353, 700, 1300), (7340033, 5000, 5000),
+                      (12289, 100, 200), (469762049, 40000, 30000)]:
+        a = rng.integers(0, p, na).astype(np.uint32)
+        b = rng.integers(0, p, nb).astype(np.uint32)
+        want = np.zeros(na + nb - 1, np.int64)
+        w = port.mul(a, b, p) if na * nb <= 4e7 else mmm.mul(a, b, p).astype(np.int64)
+        want[: len(w)] = w
+        da = torch.from_numpy(a.view(np.int32)).cuda()
+        db = torch.from_numpy(b.view(np.int32)).cuda()
+        for world in (1, 2, 4, 8):
+            n1, n2 = mmm.ntt_shape(p, na + nb - 1)
+            if n1 % world or n2 % (4 * world):
+                continue
+            f = ntt_mul_virtual(mmm, p, da, na, db, nb, world, st).cpu().numpy()
+            assert np.array_equal(f, want), (p, na, nb, world)
+    with pytest.raises(mmm.InvalidArgument):  # column slice not a multiple of 4
+        mmm.ntt_phase_dev(469762049, 0, da.data_ptr(), na, db.data_ptr(), nb, 2, 4, 0, 0, 0, st)
+
+
+def test_cfg4_big_sharded_virtual(cuda_lib, golden_configs):
+    import torch
+    from paper_1402_0264_b200.shard import ntt_mul_virtual
+    c = suites.cfg4_big(ProductRng(42))
+    if "f" not in golden_configs["cfg4_big"]:
+        pytest.skip("no golden product digest")
+    da = torch.from_numpy(np.asarray(c["a"], np.uint32).view(np.int32)).cuda()
+    db = torch.from_numpy(np.asarray(c["b"], np.uint32).view(np.int32)).cuda()
+    st = torch.cuda.current_stream().cuda_stream
+    for world in (2, 8):
+        f = ntt_mul_virtual(cuda_lib, P, da, len(c["a"]), db, len(c["b"]), world, st)
+        assert digest(f.cpu().numpy()) == golden_configs["cfg4_big"]["f"], world

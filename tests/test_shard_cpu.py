@@ -82,6 +82,61 @@ def test_output_range_gather_two_ranks_gloo():
     assert res == [(0, True), (1, True)]
 
 
+def _ntt_exchange_worker(rank, world, port, q):
+    """The sharded NTT's two block exchanges and final reduction over gloo:
+    column slices -> row slices -> column slices, against the whole matrix."""
+    from paper_1402_0264_b200.shard import NttShards
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n1, n2 = 16, 32
+        sh = NttShards(n1, n2, world)
+        full = torch.arange(n1 * n2, dtype=torch.int64).view(n1, n2)
+        w = torch.full((n1 * n2,), -1, dtype=torch.int64)
+        c0, cn = sh.cols(rank)
+        w.view(n1, n2)[:, c0:c0 + cn] = full[:, c0:c0 + cn]  # "phase 0": my columns
+        send = sh.pack_to_rows(w, rank)
+        recv = torch.empty_like(send)
+        dist.all_to_all_single(recv, send)
+        sh.unpack_rows(recv, w, rank)
+        r0, rn = sh.rows(rank)
+        ok1 = torch.equal(w.view(n1, n2)[r0:r0 + rn], full[r0:r0 + rn])
+        w.view(n1, n2)[r0:r0 + rn] *= -3  # "phase 1": my rows
+        send = sh.pack_to_cols(w, rank)
+        recv = torch.empty_like(send)
+        dist.all_to_all_single(recv, send)
+        sh.unpack_cols(recv, w, rank)
+        ok2 = torch.equal(w.view(n1, n2)[:, c0:c0 + cn], -3 * full[:, c0:c0 + cn])
+        out = torch.zeros(n1, n2, dtype=torch.int64)  # "phase 2": disjoint columns
+        out[:, c0:c0 + cn] = w.view(n1, n2)[:, c0:c0 + cn]
+        dist.all_reduce(out)
+        ok3 = torch.equal(out, -3 * full)
+        q.put((rank, bool(ok1), bool(ok2), bool(ok3)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_ntt_block_exchange_two_ranks_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ntt_exchange_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert res == [(0, True, True, True), (1, True, True, True)]
+
+
+def test_ntt_shards_validation():
+    from paper_1402_0264_b200.shard import NttShards
+    with pytest.raises(ValueError):
+        NttShards(16, 32, 3)
+    sh = NttShards(1024, 2048, 8)
+    assert sh.cols(7) == (7 * 256, 256) and sh.rows(7) == (7 * 128, 128)
+
+
 def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
