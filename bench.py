@@ -467,10 +467,12 @@ class DivWork(Workload):
         alg = 4.0 * (len(self.a) + len(self.b) + self.nq + self.nr)
         achieved = alg / t_step / 1e9
         return {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": achieved / hbm, "traffic": None, "kernel": "div_grid_kernel",
+                "frac": achieved / hbm, "traffic": None,
+                "kernel": "div_pipe_kernel" if self.s >= 32 else "div_grid_kernel",
                 "alg_bytes_per_launch": alg,
                 "imad_frac": self.units() / t_step / (imad or 7.35e12),
-                "binding": f"{-(-self.nq // self.s)} grid-wide steps of s={self.s} heads"}
+                "binding": f"{-(-self.nq // self.s)} dependent steps of s={self.s} heads "
+                           "(pipelined head CTA for s >= 32)"}
 
     def cpu_ref(self, orc):
         a, b = self.a.astype(np.int64), self.b.astype(np.int64)

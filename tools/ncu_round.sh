@@ -7,13 +7,13 @@ set -x
 T=${1:-r1}
 O=gpurun_out/$T
 mkdir -p $O
-for w in gcd mul div ntt ntt_batch batch; do
+for w in gcd mul div div_fast ntt ntt_batch batch; do
   timeout 300 python bench.py --workload $w --steps 10 --warmup 3 > $O/bench_$w.log 2>&1
 done
 timeout 300 python bench.py --steps 3 --warmup 3 --no-cpu-baseline > $O/bench_plain.log 2>&1 && \
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_gcd.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline > $O/ncu_launch.log 2>&1
 for w in gcd mul div ntt batch; do
-  case $w in gcd) k=gcd_kernel;; mul) k=mul_kernel;; div) k=div_grid_kernel;; ntt) k=ntt_rows;; batch) k=div_cta_kernel;; esac
+  case $w in gcd) k=gcd_kernel;; mul) k=mul_kernel;; div) k=div_pipe_kernel;; ntt) k=ntt_rows;; batch) k=div_cta_kernel;; esac
   timeout 120 python tools/prof_one.py $w --reps 1 > $O/plain_$w.log 2>&1 && \
   timeout 600 ncu --set full --import-source on --clock-control none -k regex:$k -c 1 -o $O/full_$w python tools/prof_one.py $w --reps 1 > $O/ncu_$w.log 2>&1
   tail -1 $O/ncu_$w.log
