@@ -255,6 +255,11 @@ __global__ void __launch_bounds__(DIV_T) div_grid_kernel(DivArgs g, int64_t seg)
 // x <= i_{k+L} - WH, several steps per pass; each publishes its progress.
 // The head waits only for the owners of its entering positions, L steps
 // behind.  Result: identical to the grid kernel (and the oracle).
+#ifdef PIPE_DBG_NOCONV  // timing experiments only (tools/head_bench.cu)
+#define PIPE_CONV(x) (void)0
+#else
+#define PIPE_CONV(x) x
+#endif
 constexpr int PIPE_L = 2;      // bulk lag (steps) the head absorbs
 constexpr int PIPE_CT = 256;    // compute threads of the head (8 warps)
 constexpr int PIPE_T = PIPE_CT + 32;  // + the head's control warp
@@ -296,11 +301,41 @@ __device__ __forceinline__ int64_t pipe_i(int64_t na, int64_t db, int S, int64_t
 // stores the words r = part, part + P, ... < 4 of the quad.
 __device__ __forceinline__ void quad_reduce(uint64_t (&acc)[4], int P, uint32_t (&v)[4],
                                             const FieldParams& F) {
+#ifdef PIPE_DBG_NOREDUCE  // timing experiments only (tools/head_bench.cu)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = uint32_t(acc[k]);
+    return;
+#endif
 #pragma unroll
     for (int k = 0; k < 4; ++k) v[k] = reduce(acc[k], F);
     for (int d = 1; d < P; d <<= 1)
 #pragma unroll
         for (int k = 0; k < 4; ++k) v[k] = addmod(v[k], __shfl_xor_sync(0xffffffffu, v[k], d), F);
+}
+
+// Split-K tiled sum with the parts across warps and the quads across lanes:
+// item it -> (quad it % NQ, part it / NQ), so a warp's lanes hold consecutive
+// quads of one part (shared-memory reads broadcast or consecutive: no bank
+// conflicts) and the parts meet in a shared-memory reduction (red: P x 4*NQ
+// words) instead of a lane butterfly.  item(qd, part, acc) adds the part's
+// terms for the quad's 4 outputs; store(t, v) receives output t < 4*NQ.
+template <class Item, class Store>
+__device__ __forceinline__ void tiled_sum(int NQ, int P, uint32_t* red, Item item, Store store,
+                                          const FieldParams& F, int nthreads, int barid) {
+    const int tid = threadIdx.x, NO = 4 * NQ;
+    for (int it = tid; it < NQ * P; it += nthreads) {
+        const int part = it / NQ, qd = it - part * NQ;
+        uint64_t acc[4] = {0, 0, 0, 0};
+        item(qd, part, acc);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) red[part * NO + 4 * qd + r] = reduce(acc[r], F);
+    }
+    bar_sync_n(barid, nthreads);
+    for (int t = tid; t < NO; t += nthreads) {
+        uint64_t sum = 0;
+        for (int p = 0; p < P; ++p) sum += red[p * NO + t];
+        store(t, reduce(sum, F));
+    }
 }
 
 }  // namespace
@@ -322,6 +357,7 @@ __device__ void pipe_head(const PipeArgs& g, uint32_t* sm, int nbulk) {
     uint32_t* stage = win + WR;                          // 2 x S entering words
     uint32_t* bt3 = stage + 2 * S;                       // bt3[3 + m] = b[db - m]
     const int MB = (L + 2) * S + 16;
+    uint32_t* red = bt3 + ((MB + 3) & ~3);               // tiled_sum partials, 4 * CT words
     for (int m = tid; m < horg + S + 8; m += PIPE_T) {
         const int j = m - horg;
         hz[m] = (j >= 0 && j < S) ? __ldcg(g.h_glob + j) : 0u;
@@ -381,27 +417,20 @@ __device__ void pipe_head(const PipeArgs& g, uint32_t* sm, int nbulk) {
         for (int t = tid; t < S; t += CT) hd[t] = t < v ? win[(i - t) & (WR - 1)] : 0u;
         bar_sync_n(1, CT);
         // lambda_k = sum_{t<=k} h[k-t] * hd[t], k < v
-        if (tid < ((S / 4) << logPL)) {
-            const int part = tid & (PL - 1), q4 = tid >> logPL, k0 = 4 * q4, t0 = part * SPANL;
-            uint64_t acc[4] = {0, 0, 0, 0};
-            uint32_t since = 0;
-            if (t0 <= k0 + 3)
-                conv_accumulate<4>(acc, hd + t0, SPANL / 4, hz, horg + k0 - t0, since, F);
-            uint32_t lv[4];
-            quad_reduce(acc, PL, lv, F);
-#pragma unroll
-            for (int r = 0; r < 4; ++r) {
-                const int k = k0 + r;
-                if ((r & (PL - 1)) == part && part < 4) {
-                    if (k < v) {
-                        g.q[i - db - k] = lv[r];
-                        lamh[(j % L) * S + k] = negmod(lv[r], F);
-                    } else {
-                        lamh[(j % L) * S + k] = 0u;
-                    }
-                }
-            }
-        }
+        tiled_sum(
+            S / 4, PL, red,
+            [&](int qd, int part, uint64_t (&acc)[4]) {
+                const int k0 = 4 * qd, t0 = part * SPANL;
+                uint32_t since = 0;
+                if (t0 <= k0 + 3)
+                    PIPE_CONV(conv_accumulate<4>(acc, hd + t0, SPANL / 4, hz, horg + k0 - t0, since,
+                                                 F));
+            },
+            [&](int k, uint32_t lam) {
+                if (k < v) g.q[i - db - k] = lam;
+                lamh[(j % L) * S + k] = k < v ? negmod(lam, F) : 0u;
+            },
+            F, CT, 1);
         const long long pa = clock64();
         bar_sync_n(2, PIPE_T);  // with the control warp: publish step j
         const long long p1 = clock64();
@@ -409,33 +438,29 @@ __device__ void pipe_head(const PipeArgs& g, uint32_t* sm, int nbulk) {
         c_lam += p1 - p0;
         // window (t in [v, WH)): step j; entering words copied in from the stage
         {
-            const int tq = v & ~3, NQ = (WH - tq) >> 2;
-            int logP = 0;
-            while (logP < 5 && (NQ << (logP + 1)) <= CT && (S >> (logP + 1)) >= 4 &&
-                   ((S >> (logP + 1)) & 3) == 0)
-                ++logP;
-            const int P = 1 << logP, SPAN = S >> logP, vp = (v + 3) & ~3;
-            for (int it0 = 0; it0 < (NQ << logP); it0 += CT) {
-                const int it = it0 + tid;
-                const bool live = it < (NQ << logP);
-                const int part = it & (P - 1), t0 = tq + 4 * (it >> logP), k0 = part * SPAN;
-                uint64_t acc[4] = {0, 0, 0, 0};
-                uint32_t since = 0;
-                if (live && k0 < vp)
-                    conv_accumulate<4>(acc, lamh + (j % L) * S + k0, min(SPAN, vp - k0) / 4, bt3,
-                                       t0 - k0 + 3, since, F);
-                uint32_t add[4];
-                quad_reduce(acc, P, add, F);
-#pragma unroll
-                for (int r = 0; r < 4; ++r) {
-                    const int t = t0 + r;
+            const int tq = v & ~3, NQ = (WH - tq) >> 2, vp = (v + 3) & ~3;
+            int P = 1;
+            while (NQ * P * 2 <= CT && (S / (P * 2)) >= 4 && ((S / (P * 2)) & 3) == 0) P *= 2;
+            const int SPAN = S / P;
+            tiled_sum(
+                NQ, P, red,
+                [&](int qd, int part, uint64_t (&acc)[4]) {
+                    const int t0 = tq + 4 * qd, k0 = part * SPAN;
+                    uint32_t since = 0;
+                    if (k0 < vp)
+                        PIPE_CONV(conv_accumulate<4>(acc, lamh + (j % L) * S + k0,
+                                                     min(SPAN, vp - k0) / 4, bt3, t0 - k0 + 3,
+                                                     since, F));
+                },
+                [&](int tt, uint32_t add) {
+                    const int t = tq + tt;
                     const int64_t x = i - t;
-                    if (live && (r & (P - 1)) == part && part < 4 && t >= v && t < WH && x >= 0) {
+                    if (t >= v && t < WH && x >= 0) {
                         uint32_t* w = win + (x & (WR - 1));
-                        *w = addmod(*w, add[r], F);
+                        *w = addmod(*w, add, F);
                     }
-                }
-            }
+                },
+                F, CT, 1);
             const uint32_t* st = stage + (j & 1) * S;
             for (int u = tid; u < v; u += CT) {  // t = WH + u, x = i - WH - u
                 const int64_t x = i - WH - u;
@@ -448,38 +473,34 @@ __device__ void pipe_head(const PipeArgs& g, uint32_t* sm, int nbulk) {
         // entering (t in [WH, WH + v)): steps j - L + 1 .. j
         {
             const int NQ = (v + 3) >> 2, TT = L * S;
-            int logP = 0;
-            while (logP < 5 && (NQ << (logP + 1)) <= CT && (TT >> (logP + 1)) >= 4 &&
-                   ((TT >> (logP + 1)) & 3) == 0)  // whole conv blocks per part
-                ++logP;
-            const int P = 1 << logP, SPAN = TT >> logP;
-            for (int it0 = 0; it0 < (NQ << logP); it0 += CT) {
-                const int it = it0 + tid;
-                const bool live = it < (NQ << logP);
-                const int part = it & (P - 1), t0 = WH + 4 * (it >> logP);
-                uint64_t acc[4] = {0, 0, 0, 0};
-                uint32_t since = 0;
-                for (int c0 = part * SPAN; live && c0 < (part + 1) * SPAN;) {
-                    const int d = c0 >> logS, k0 = c0 & (S - 1);
-                    const int n = min(S - k0, (part + 1) * SPAN - c0);
-                    const int lim = d == 0 ? ((v + 3) & ~3) : S;
-                    if (j - d >= 0 && k0 < lim)
-                        conv_accumulate<4>(acc, lamh + ((j - d) % L) * S + k0, min(n, lim - k0) / 4,
-                                           bt3, t0 + d * S - k0 + 3, since, F);
-                    c0 += n;
-                }
-                uint32_t add[4];
-                quad_reduce(acc, P, add, F);
-#pragma unroll
-                for (int r = 0; r < 4; ++r) {
-                    const int t = t0 + r;
-                    const int64_t x = i - t;
-                    if (live && (r & (P - 1)) == part && part < 4 && t < WH + v && x >= 0) {
-                        uint32_t* w = win + (x & (WR - 1));
-                        *w = addmod(*w, add[r], F);
+            int P = 1;
+            while (NQ * P * 2 <= CT && (TT / (P * 2)) >= 4 && ((TT / (P * 2)) & 3) == 0) P *= 2;
+            const int SPAN = TT / P;
+            tiled_sum(
+                NQ, P, red,
+                [&](int qd, int part, uint64_t (&acc)[4]) {
+                    const int t0 = WH + 4 * qd;
+                    uint32_t since = 0;
+                    for (int c0 = part * SPAN; c0 < (part + 1) * SPAN;) {
+                        const int d = c0 >> logS, k0 = c0 & (S - 1);
+                        const int n = min(S - k0, (part + 1) * SPAN - c0);
+                        const int lim = d == 0 ? ((v + 3) & ~3) : S;
+                        if (j - d >= 0 && k0 < lim)
+                            PIPE_CONV(conv_accumulate<4>(acc, lamh + ((j - d) % L) * S + k0,
+                                                         min(n, lim - k0) / 4, bt3,
+                                                         t0 + d * S - k0 + 3, since, F));
+                        c0 += n;
                     }
-                }
-            }
+                },
+                [&](int tt, uint32_t add) {
+                    const int t = WH + tt;
+                    const int64_t x = i - t;
+                    if (t < WH + v && x >= 0) {
+                        uint32_t* w = win + (x & (WR - 1));
+                        *w = addmod(*w, add, F);
+                    }
+                },
+                F, CT, 1);
         }
         bar_sync_n(1, CT);
         c_ent += clock64() - p2;
@@ -694,7 +715,7 @@ void run_pipe(const DivArgs& d, int64_t s, cudaStream_t st) {
     const int L = PIPE_L;
     const int horg = std::max(((S / 4 + 3) & ~3) + 3, 67);
     const size_t head =
-        size_t(((horg + S + 8 + 3) & ~3) + S + L * S + 4 * S + 2 * S + (L + 2) * S + 16);
+        size_t(((horg + S + 8 + 3) & ~3) + S + L * S + 4 * S + 2 * S + (L + 2) * S + 16 + 4 * PIPE_CT);
     const size_t bulk = size_t(S + 4 + PIPE_B + S + 8 + 8);
     // more than half an SM's shared memory: one CTA per SM, so no bulk CTA
     // shares (and takes issue slots from) the head's SM
