@@ -743,19 +743,17 @@ __device__ void load_top_region(uint32_t* top, const uint32_t* Z, long long deg,
 //   winA[t] = sum_e Pa1[e] topA[t+e] + sum_e Pa2[e] topB[t+e]   (t < W1)
 // and winB likewise with Pb1, Pb2.  Ps holds each polynomial index-reversed
 // (Ps[c][PL-1-e] = P_c[e]), so with u = PL-1-e the sum is the convolution
-// conv_accumulate computes.  Work item = (window, 4 consecutive words, one
-// of BUILD_PARTS parts: term x slice of the support), parts in adjacent
-// lanes meeting in a butterfly.  IMAD.WIDE issues at one warp-instruction per
-// SM-cycle, so the 2*W1*2*PL MACs cost ~W1*PL/8 cycles however they are split;
-// fewer, longer parts spend less on the reduction (ncu: ~9.6 cycles/instr).
+// conv_accumulate computes.  Split-K over BUILD_PARTS parts (term x half of
+// the support), one part per warp; the 32 lanes hold the 2 x W1/4 quads of
+// 4 consecutive words (shared-memory reads: broadcast or consecutive, no
+// bank conflicts), and the parts meet in a shared-memory reduction.
 constexpr int BUILD_PARTS = 4;
-constexpr int BUILD_ITEMS = 2 * (W1 / 4) * BUILD_PARTS;  // 128: warps 0-3
-__device__ void build_window_item(int item, uint32_t* winA, uint32_t* winB, const uint32_t* Ps,
-                                  const int* hi, const uint32_t* topA, const uint32_t* topB,
+static_assert(2 * (W1 / 4) == 32, "window builder: one (window, quad) per lane");
+__device__ void build_window_part(int part, uint32_t* red, const uint32_t* Ps, const int* hi,
+                                  const uint32_t* topA, const uint32_t* topB,
                                   const FieldParams& F) {
     constexpr int SPAN = 2 * PL / BUILD_PARTS;  // terms per part
-    const int part = item % BUILD_PARTS, q = (item / BUILD_PARTS) % (W1 / 4);
-    const int w = item / (BUILD_PARTS * (W1 / 4));
+    const int lane = threadIdx.x & 31, w = lane >> 4, q = lane & 15;
     const int term = part / (BUILD_PARTS / 2), u0 = (part % (BUILD_PARTS / 2)) * SPAN;
     const int c = 2 * w + term;  // Pa1, Pa2, Pb1, Pb2
     uint64_t acc[4] = {0, 0, 0, 0};
@@ -764,15 +762,8 @@ __device__ void build_window_item(int item, uint32_t* winA, uint32_t* winB, cons
     if (hi[c] >= 0 && u0 + SPAN - 1 >= PL - 1 - hi[c])
         conv_accumulate<4>(acc, Ps + c * PL + u0, SPAN / 4, term ? topB : topA,
                            4 * q + PL - 1 - u0, since, F);
-    uint32_t v[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) v[k] = reduce(acc[k], F);
-#pragma unroll
-    for (int d = 1; d < BUILD_PARTS; d <<= 1)
-#pragma unroll
-        for (int k = 0; k < 4; ++k) v[k] = addmod(v[k], __shfl_xor_sync(0xffffffffu, v[k], d), F);
-    const uint32_t o = part == 0 ? v[0] : part == 1 ? v[1] : part == 2 ? v[2] : v[3];
-    (w ? winB : winA)[4 * q + part] = o;  // part k stores word k of the quad
+    for (int r = 0; r < 4; ++r) red[part * (2 * W1) + w * W1 + 4 * q + r] = reduce(acc[r], F);
 }
 
 // Named barrier over the first n threads' warps (n a multiple of 32).
@@ -796,6 +787,7 @@ __device__ int head_cta(const GcdArgs& g, BatchMeta& ctl, StepLog* log, uint32_t
     uint32_t* topA = winB + W1;         // W1 + PL words
     uint32_t* topB = topA + W1 + PL;
     uint32_t* Ps = topB + W1 + PL;      // 4 * PL
+    uint32_t* red = Ps + 4 * PL;        // BUILD_PARTS x 2 * W1 builder partials
     __shared__ int fallback;
     __shared__ long long da0s[2], db0s[2];  // batch start degrees, by batch parity
     __shared__ long long hst[10];  // MMM_GCD_STATS: accumulated here, flushed at the end
@@ -869,8 +861,14 @@ __device__ int head_cta(const GcdArgs& g, BatchMeta& ctl, StepLog* log, uint32_t
             return j;
         }
         // warps 0-6: next windows, top-aligned, from S_j and the batch matrix
-        if (threadIdx.x < BUILD_ITEMS)
-            build_window_item(threadIdx.x, winA, winB, Ps, hi_s, topA, topB, F);
+        if (warp < BUILD_PARTS) build_window_part(warp, red, Ps, hi_s, topA, topB, F);
+        bar_sync(2, BUILDERS);
+        if (threadIdx.x < 2 * W1) {  // sum the parts: winA then winB
+            uint64_t sum = 0;
+#pragma unroll
+            for (int pt = 0; pt < BUILD_PARTS; ++pt) sum += red[pt * (2 * W1) + threadIdx.x];
+            (threadIdx.x < W1 ? winA : winB)[threadIdx.x & (W1 - 1)] = reduce(sum, F);
+        }
         if (threadIdx.x == 0) fallback = 0;
         if (g.stats && threadIdx.x == 0) hst[7] += clock64() - t0;
         bar_sync(2, BUILDERS);
@@ -1110,7 +1108,7 @@ void launch_gcd(const FieldParams& F, const uint32_t* a, int64_t na, const uint3
         sc.get<uint64_t>(RING * ((sizeof(BatchMeta) + 7) / 8)));
     g.flags = sc.get<unsigned>(2);
     MMM_CUDA(cudaMemsetAsync(g.flags, 0, 2 * sizeof(unsigned), st));
-    const size_t head_words = 2 * W1 + 2 * (W1 + PL) + 4 * PL;
+    const size_t head_words = 2 * W1 + 2 * (W1 + PL) + 4 * PL + BUILD_PARTS * 2 * W1;
     const size_t bulk_words = APPLY_WORDS;
     const size_t bytes = (4 * LOGCAP + std::max(head_words, bulk_words)) * 4;
     const int mode = !F.odd ? 2 : (F.p < (1u << 29) ? 0 : 1);

@@ -1,4 +1,4 @@
-// build_bench.cu -- cycles of the GCD window builder (build_window_item in
+// build_bench.cu -- cycles of the GCD window builder (build_window_part in
 // paper_1402_0264_b200/csrc/gcd.cu) on synthetic P and top regions, run as in
 // the head CTA (warps 0-6, warp 0 taking the last 32 items), and all 8 warps.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o tools/build_bench tools/build_bench.cu
@@ -13,7 +13,8 @@ Scratch::~Scratch() {}
 using namespace mmm_cu;
 
 __global__ void bench(const uint32_t* rnd, long long* out, uint32_t* sink, int reps, FieldParams F) {
-    __shared__ __align__(16) uint32_t win[2 * W1], top[2 * (W1 + PL)], Ps[4 * PL];
+    __shared__ __align__(16) uint32_t win[2 * W1], top[2 * (W1 + PL)], Ps[4 * PL],
+        red[BUILD_PARTS * 2 * W1];
     __shared__ int hi[4];
     for (int i = threadIdx.x; i < 2 * (W1 + PL); i += blockDim.x) top[i] = rnd[i] % F.p;
     for (int i = threadIdx.x; i < 4 * PL; i += blockDim.x) Ps[i] = rnd[1024 + i] % F.p;
@@ -24,15 +25,21 @@ __global__ void bench(const uint32_t* rnd, long long* out, uint32_t* sink, int r
         __syncthreads();
         long long t0 = clock64();
         if (threadIdx.x < BUILDERS) {
-            if (threadIdx.x < BUILD_ITEMS)
-                build_window_item(threadIdx.x, win, win + W1, Ps, hi, top, top + W1 + PL, F);
+            if ((threadIdx.x >> 5) < BUILD_PARTS)
+                build_window_part(threadIdx.x >> 5, red, Ps, hi, top, top + W1 + PL, F);
+            bar_sync(2, BUILDERS);
+            if (threadIdx.x < 2 * W1) {
+                uint64_t sum = 0;
+                for (int pt = 0; pt < BUILD_PARTS; ++pt) sum += red[pt * 2 * W1 + threadIdx.x];
+                win[threadIdx.x] = reduce(sum, F);
+            }
             bar_sync(2, BUILDERS);
         }
         if (threadIdx.x == 0) c7 += clock64() - t0;
         __syncthreads();
         t0 = clock64();
-        if (threadIdx.x < BUILD_ITEMS)
-            build_window_item(threadIdx.x, win, win + W1, Ps, hi, top, top + W1 + PL, F);
+        if ((threadIdx.x >> 5) < BUILD_PARTS)
+            build_window_part(threadIdx.x >> 5, red, Ps, hi, top, top + W1 + PL, F);
         __syncthreads();
         if (threadIdx.x == 0) c8 += clock64() - t0;
     }
