@@ -46,6 +46,28 @@ __device__ __forceinline__ uint32_t sub_p(uint32_t a, uint32_t b, uint32_t p) {
     return a >= b ? a - b : a + p - b;
 }
 
+// Butterfly halves, exact (LZ = false: canonical in and out) or lazy (LZ =
+// true, p < 2^30: values in [0, 2p) in and out; Harvey's trick -- the sum
+// needs one conditional subtraction of 2p, the difference none: a - b + 2p
+// < 4p < 2^32 goes straight into a Shoup product, whose unreduced result
+// x*w - q*p lies in [0, 2p) for any x < 2^32).  Half the ALU work per
+// butterfly of the exact form, which the ALU-bound transform feels directly.
+template <bool LZ>
+__device__ __forceinline__ uint32_t bf_add(uint32_t a, uint32_t b, uint32_t p) {
+    if (!LZ) return add_p(a, b, p);
+    const uint32_t s = a + b, p2 = 2 * p;
+    return s >= p2 ? s - p2 : s;
+}
+template <bool LZ>
+__device__ __forceinline__ uint32_t shoup_l(uint32_t x, uint32_t w, uint32_t wp, uint32_t p) {
+    if (!LZ) return shoup(x, w, wp, p);
+    return x * w - __umulhi(x, wp) * p;
+}
+template <bool LZ>
+__device__ __forceinline__ uint32_t bf_subw(uint32_t a, uint32_t b, uint2 w, uint32_t p) {
+    return LZ ? shoup_l<true>(a - b + 2 * p, w.x, w.y, p) : shoup(sub_p(a, b, p), w.x, w.y, p);
+}
+
 // Device tables for one (p, N): roots of the two sub-transform lengths and
 // the two-level four-step twiddles, each value followed by its Shoup
 // companion (interleaved pairs).
@@ -64,36 +86,12 @@ struct NttPlan {
 };
 constexpr int LO = 10;
 
-// Radix-2 Stockham DIF network over L = 2^logL words, `cols` independent
-// columns laid out as x[c + cols*i]; tw = w_L^j pairs (j < L/2) in smem.
-// Result ends in `x` if logL is even, else in `y`; returns the final buffer.
-__device__ uint32_t* stockham(uint32_t* x, uint32_t* y, int logL, int logc, const uint2* tw,
-                              uint32_t p) {
-    const int L = 1 << logL, half = L >> 1, cols = 1 << logc;
-    for (int s = 0; s < logL; ++s) {
-        const int sp = 1 << s;  // stride of this stage
-        for (int t = threadIdx.x; t < (half << logc); t += blockDim.x) {
-            const int c = t & (cols - 1), i = t >> logc;
-            const int pp = i >> s, q = i & (sp - 1);
-            const uint32_t a = x[c + cols * (q + sp * pp)];
-            const uint32_t b = x[c + cols * (q + sp * (pp + half / sp))];
-            const uint2 w = tw[pp * sp];
-            y[c + cols * (q + sp * (2 * pp))] = add_p(a, b, p);
-            y[c + cols * (q + sp * (2 * pp + 1))] = shoup(sub_p(a, b, p), w.x, w.y, p);
-        }
-        __syncthreads();
-        uint32_t* t = x;
-        x = y;
-        y = t;
-    }
-    return x;
-}
-
 // Two Stockham stages at once (radix-4 step): the unit (q, pp), pp < H/2 with
 // H = half/sp, reads the four words x[q + sp*(pp + j*H/2)], j < 4, runs the
 // stage-s butterflies (pp, pp + H/2) and the stage-(s+1) butterflies on their
 // outputs in registers, and writes y[q + sp*(4pp + b0 + 2*b1)]: half the
 // passes, barriers and index arithmetic of two radix-2 stages.
+template <bool LZ>
 __device__ uint32_t* stockham4(uint32_t* x, uint32_t* y, int logL, int logc, const uint2* tw,
                                uint32_t p) {
     const int L = 1 << logL, half = L >> 1, cols = 1 << logc;
@@ -115,8 +113,8 @@ __device__ uint32_t* stockham4(uint32_t* x, uint32_t* y, int logL, int logc, con
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 const uint2 w = tw[(pp + j * Q) * sp];
-                e[2 * j] = add_p(v[j], v[j + 4], p);
-                e[2 * j + 1] = shoup(sub_p(v[j], v[j + 4], p), w.x, w.y, p);
+                e[2 * j] = bf_add<LZ>(v[j], v[j + 4], p);
+                e[2 * j + 1] = bf_subw<LZ>(v[j], v[j + 4], w, p);
             }
             uint32_t f[8];  // f[4j + 2b1 + b0]... indexed f[j][b0][b1] = f[4j + 2 b0 + b1]
 #pragma unroll
@@ -125,8 +123,8 @@ __device__ uint32_t* stockham4(uint32_t* x, uint32_t* y, int logL, int logc, con
 #pragma unroll
                 for (int b0 = 0; b0 < 2; ++b0) {
                     const uint32_t a0 = e[2 * j + b0], a1 = e[2 * (j + 2) + b0];
-                    f[4 * j + 2 * b0] = add_p(a0, a1, p);
-                    f[4 * j + 2 * b0 + 1] = shoup(sub_p(a0, a1, p), w.x, w.y, p);
+                    f[4 * j + 2 * b0] = bf_add<LZ>(a0, a1, p);
+                    f[4 * j + 2 * b0 + 1] = bf_subw<LZ>(a0, a1, w, p);
                 }
             }
             const uint2 w = tw[pp * 4 * sp];
@@ -136,8 +134,8 @@ __device__ uint32_t* stockham4(uint32_t* x, uint32_t* y, int logL, int logc, con
                 for (int b1 = 0; b1 < 2; ++b1) {
                     const uint32_t a0 = f[2 * b0 + b1], a1 = f[4 + 2 * b0 + b1];
                     const int o = 8 * pp + b0 + 2 * b1;
-                    y[base + st * o] = add_p(a0, a1, p);
-                    y[base + st * (o + 4)] = shoup(sub_p(a0, a1, p), w.x, w.y, p);
+                    y[base + st * o] = bf_add<LZ>(a0, a1, p);
+                    y[base + st * (o + 4)] = bf_subw<LZ>(a0, a1, w, p);
                 }
         }
         __syncthreads();
@@ -157,13 +155,13 @@ __device__ uint32_t* stockham4(uint32_t* x, uint32_t* y, int logL, int logc, con
             const uint32_t a3 = x[base + st * (pp + H2 + H)];
             const uint2 w0 = tw[pp * sp], w1 = tw[(pp + H2) * sp], w2 = tw[pp * 2 * sp];
             // stage s: (a0, a2) -> y[2pp], y[2pp+1]; (a1, a3) -> y[2pp+H], y[2pp+H+1]
-            const uint32_t e0 = add_p(a0, a2, p), e1 = shoup(sub_p(a0, a2, p), w0.x, w0.y, p);
-            const uint32_t f0 = add_p(a1, a3, p), f1 = shoup(sub_p(a1, a3, p), w1.x, w1.y, p);
+            const uint32_t e0 = bf_add<LZ>(a0, a2, p), e1 = bf_subw<LZ>(a0, a2, w0, p);
+            const uint32_t f0 = bf_add<LZ>(a1, a3, p), f1 = bf_subw<LZ>(a1, a3, w1, p);
             // stage s+1, q' = q + sp*b0: (e_b0, f_b0) -> y'[4pp + b0], y'[4pp + b0 + 2]
-            y[base + st * (4 * pp)] = add_p(e0, f0, p);
-            y[base + st * (4 * pp + 2)] = shoup(sub_p(e0, f0, p), w2.x, w2.y, p);
-            y[base + st * (4 * pp + 1)] = add_p(e1, f1, p);
-            y[base + st * (4 * pp + 3)] = shoup(sub_p(e1, f1, p), w2.x, w2.y, p);
+            y[base + st * (4 * pp)] = bf_add<LZ>(e0, f0, p);
+            y[base + st * (4 * pp + 2)] = bf_subw<LZ>(e0, f0, w2, p);
+            y[base + st * (4 * pp + 1)] = bf_add<LZ>(e1, f1, p);
+            y[base + st * (4 * pp + 3)] = bf_subw<LZ>(e1, f1, w2, p);
         }
         __syncthreads();
         uint32_t* t = x;
@@ -178,8 +176,8 @@ __device__ uint32_t* stockham4(uint32_t* x, uint32_t* y, int logL, int logc, con
             const uint32_t a = x[c + cols * (q + sp * pp)];
             const uint32_t b = x[c + cols * (q + sp * (pp + half / sp))];
             const uint2 w = tw[pp * sp];
-            y[c + cols * (q + sp * (2 * pp))] = add_p(a, b, p);
-            y[c + cols * (q + sp * (2 * pp + 1))] = shoup(sub_p(a, b, p), w.x, w.y, p);
+            y[c + cols * (q + sp * (2 * pp))] = bf_add<LZ>(a, b, p);
+            y[c + cols * (q + sp * (2 * pp + 1))] = bf_subw<LZ>(a, b, w, p);
         }
         __syncthreads();
         uint32_t* t = x;
@@ -189,11 +187,12 @@ __device__ uint32_t* stockham4(uint32_t* x, uint32_t* y, int logL, int logc, con
     return x;
 }
 
+template <bool LZ>
 __device__ __forceinline__ uint32_t twiddle(uint32_t v, uint64_t e, const uint2* lo,
                                             const uint2* hi, uint32_t p) {
     const uint2 a = lo[e & ((1u << LO) - 1)];
     const uint2 b = hi[e >> LO];
-    return shoup(shoup(v, a.x, a.y, p), b.x, b.y, p);
+    return shoup_l<LZ>(shoup_l<LZ>(v, a.x, a.y, p), b.x, b.y, p);
 }
 
 struct NttArgs {
@@ -209,6 +208,7 @@ struct NttArgs {
 };
 
 // K1: forward column transforms of both operands (grid.y = operand).
+template <bool LZ>
 __global__ void __launch_bounds__(NTT_T) ntt_cols_fwd(NttArgs g) {
     extern __shared__ __align__(16) uint32_t sm[];
     const NttPlan& P = g.P;
@@ -229,15 +229,16 @@ __global__ void __launch_bounds__(NTT_T) ntt_cols_fwd(NttArgs g) {
         x[t] = idx < len ? in[idx] : 0u;
     }
     __syncthreads();
-    uint32_t* r = stockham4(x, y, P.log1, g.logc, tw, P.p);
+    uint32_t* r = stockham4<LZ>(x, y, P.log1, g.logc, tw, P.p);
     for (int t = threadIdx.x; t < C * N1; t += NTT_T) {
         const int c = t & (C - 1), k1 = t >> g.logc;
         const uint64_t e = uint64_t(c0 + c) * uint64_t(k1);
-        work[int64_t(N2) * k1 + c0 + c] = twiddle(r[t], e, P.tlo_f, P.thi_f, P.p);
+        work[int64_t(N2) * k1 + c0 + c] = twiddle<LZ>(r[t], e, P.tlo_f, P.thi_f, P.p);
     }
 }
 
 // K2: per row: forward both, pointwise product, inverse, inverse twiddle.
+template <bool LZ>
 __global__ void __launch_bounds__(NTT_T) ntt_rows(NttArgs g, FieldParams F) {
     extern __shared__ __align__(16) uint32_t sm[];
     const NttPlan& P = g.P;
@@ -263,19 +264,20 @@ __global__ void __launch_bounds__(NTT_T) ntt_rows(NttArgs g, FieldParams F) {
     __syncthreads();
     // the two forward transforms as one 2-column network: interleave? keep
     // them separate (same code, half the threads idle per stage otherwise)
-    uint32_t* ra = stockham4(xa, ya, P.log2, 0, twf, P.p);
-    uint32_t* rb = stockham4(xb, yb, P.log2, 0, twf, P.p);
+    uint32_t* ra = stockham4<LZ>(xa, ya, P.log2, 0, twf, P.p);
+    uint32_t* rb = stockham4<LZ>(xb, yb, P.log2, 0, twf, P.p);
     for (int t = threadIdx.x; t < N2; t += NTT_T) ra[t] = mulmod(ra[t], rb[t], F);
     __syncthreads();
     uint32_t* other = ra == xa ? ya : xa;
-    uint32_t* rc = stockham4(ra, other, P.log2, 0, twi, P.p);
+    uint32_t* rc = stockham4<LZ>(ra, other, P.log2, 0, twi, P.p);
     for (int t = threadIdx.x; t < N2; t += NTT_T) {
         const uint64_t e = (uint64_t(1) << P.logN) - (uint64_t(t) * uint64_t(k1));
-        wa[t] = twiddle(rc[t], e & ((uint64_t(1) << P.logN) - 1), P.tlo_f, P.thi_f, P.p);
+        wa[t] = twiddle<LZ>(rc[t], e & ((uint64_t(1) << P.logN) - 1), P.tlo_f, P.thi_f, P.p);
     }
 }
 
 // K3: inverse column transforms, N^-1 scale, natural-order output.
+template <bool LZ>
 __global__ void __launch_bounds__(NTT_T) ntt_cols_inv(NttArgs g) {
     extern __shared__ __align__(16) uint32_t sm[];
     const NttPlan& P = g.P;
@@ -293,7 +295,7 @@ __global__ void __launch_bounds__(NTT_T) ntt_cols_inv(NttArgs g) {
         x[t] = work[int64_t(N2) * k1 + c0 + c];
     }
     __syncthreads();
-    uint32_t* r = stockham4(x, y, P.log1, g.logc, tw, P.p);
+    uint32_t* r = stockham4<LZ>(x, y, P.log1, g.logc, tw, P.p);
     for (int t = threadIdx.x; t < C * N1; t += NTT_T) {
         const int c = t & (C - 1), n1 = t >> g.logc;
         const int64_t idx = int64_t(N2) * n1 + c0 + c;
@@ -404,6 +406,12 @@ int log2_len(int64_t nf) {
     return k;
 }
 
+template <bool LZ>
+void run_ntt_launches(NttArgs g, const FieldParams& F, int N1, int N2, int64_t count,
+                      int64_t chunk, const uint32_t* A, int64_t lda, const uint32_t* B,
+                      int64_t ldb, uint32_t* Fo, int64_t ldf, size_t sm1, size_t sm2,
+                      cudaStream_t st);
+
 void run_ntt(const FieldParams& F, const uint32_t* A, int64_t lda, int64_t na, const uint32_t* B,
              int64_t ldb, int64_t nb, int64_t count, uint32_t* Fo, int64_t ldf, cudaStream_t st) {
     const int64_t nf = na + nb - 1;
@@ -427,11 +435,22 @@ void run_ntt(const FieldParams& F, const uint32_t* A, int64_t lda, int64_t na, c
     g.work[1] = sc.get<uint32_t>(size_t(chunk) << logN);
     const size_t sm1 = size_t(N1 + 2 * g.cols * N1) * 4;
     const size_t sm2 = size_t(2 * N2 + 4 * N2) * 4;
-    MMM_CUDA(cudaFuncSetAttribute(ntt_cols_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (F.p < (1u << 30))
+        run_ntt_launches<true>(g, F, N1, N2, count, chunk, A, lda, B, ldb, Fo, ldf, sm1, sm2, st);
+    else
+        run_ntt_launches<false>(g, F, N1, N2, count, chunk, A, lda, B, ldb, Fo, ldf, sm1, sm2, st);
+}
+
+template <bool LZ>
+void run_ntt_launches(NttArgs g, const FieldParams& F, int N1, int N2, int64_t count,
+                      int64_t chunk, const uint32_t* A, int64_t lda, const uint32_t* B,
+                      int64_t ldb, uint32_t* Fo, int64_t ldf, size_t sm1, size_t sm2,
+                      cudaStream_t st) {
+    MMM_CUDA(cudaFuncSetAttribute(ntt_cols_fwd<LZ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(sm1)));
-    MMM_CUDA(cudaFuncSetAttribute(ntt_cols_inv, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    MMM_CUDA(cudaFuncSetAttribute(ntt_cols_inv<LZ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(sm1)));
-    MMM_CUDA(cudaFuncSetAttribute(ntt_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    MMM_CUDA(cudaFuncSetAttribute(ntt_rows<LZ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(sm2)));
     for (int64_t c0 = 0; c0 < count; c0 += chunk) {
         const unsigned c = unsigned(std::min<int64_t>(chunk, count - c0));
@@ -441,16 +460,34 @@ void run_ntt(const FieldParams& F, const uint32_t* A, int64_t lda, int64_t na, c
         g.ld[1] = ldb;
         g.out = Fo + c0 * ldf;
         g.ldf = ldf;
-        ntt_cols_fwd<<<dim3(N2 / g.cols, 2, c), NTT_T, sm1, st>>>(g);
+        ntt_cols_fwd<LZ><<<dim3(N2 / g.cols, 2, c), NTT_T, sm1, st>>>(g);
         check_launch("ntt_cols_fwd");
-        ntt_rows<<<dim3(N1, 1, c), NTT_T, sm2, st>>>(g, F);
+        ntt_rows<LZ><<<dim3(N1, 1, c), NTT_T, sm2, st>>>(g, F);
         check_launch("ntt_rows");
-        ntt_cols_inv<<<dim3(N2 / g.cols, 1, c), NTT_T, sm1, st>>>(g);
+        ntt_cols_inv<LZ><<<dim3(N2 / g.cols, 1, c), NTT_T, sm1, st>>>(g);
         check_launch("ntt_cols_inv");
     }
 }
 
 }  // namespace
+
+template <bool LZ>
+void phase_launch(NttArgs g, const FieldParams& F, int phase, int64_t start, int64_t n, size_t sm1,
+                  size_t sm2, cudaStream_t st) {
+    if (phase == 1) {
+        MMM_CUDA(cudaFuncSetAttribute(ntt_rows<LZ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(sm2)));
+        g.row0 = int(start);
+        ntt_rows<LZ><<<dim3(unsigned(n), 1, 1), NTT_T, sm2, st>>>(g, F);
+        check_launch("ntt_rows");
+    } else {
+        auto fn = phase == 0 ? ntt_cols_fwd<LZ> : ntt_cols_inv<LZ>;
+        MMM_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm1)));
+        g.col0 = int(start);
+        fn<<<dim3(unsigned(n / g.cols), phase == 0 ? 2 : 1, 1), NTT_T, sm1, st>>>(g);
+        check_launch(phase == 0 ? "ntt_cols_fwd" : "ntt_cols_inv");
+    }
+}
 
 // One phase of the four-step product over a slice (the sharded NTT, SURVEY
 // §8f): 0 = forward columns [start, start + n) of both operands into the
@@ -488,19 +525,10 @@ void launch_ntt_phase(const FieldParams& F, int phase, const uint32_t* a, int64_
     if (n == 0) return;
     const size_t sm1 = size_t(N1 + 2 * g.cols * N1) * 4;
     const size_t sm2 = size_t(2 * N2 + 4 * N2) * 4;
-    if (phase == 1) {
-        MMM_CUDA(cudaFuncSetAttribute(ntt_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      int(sm2)));
-        g.row0 = int(start);
-        ntt_rows<<<dim3(unsigned(n), 1, 1), NTT_T, sm2, st>>>(g, F);
-        check_launch("ntt_rows");
-    } else {
-        auto fn = phase == 0 ? ntt_cols_fwd : ntt_cols_inv;
-        MMM_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm1)));
-        g.col0 = int(start);
-        fn<<<dim3(unsigned(n / g.cols), phase == 0 ? 2 : 1, 1), NTT_T, sm1, st>>>(g);
-        check_launch(phase == 0 ? "ntt_cols_fwd" : "ntt_cols_inv");
-    }
+    if (F.p < (1u << 30))
+        phase_launch<true>(g, F, phase, start, n, sm1, sm2, st);
+    else
+        phase_launch<false>(g, F, phase, start, n, sm1, sm2, st);
 }
 
 void ntt_shape(uint32_t p, int64_t nf, int64_t* n1, int64_t* n2) {

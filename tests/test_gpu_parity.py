@@ -14,7 +14,7 @@ import suites
 pytestmark = pytest.mark.gpu
 
 P = suites.P_BENCH
-NTT_PRIMES = [469762049, 998244353, 7340033, 12289, 257, 17]
+NTT_PRIMES = [469762049, 998244353, 7340033, 12289, 257, 17, 2013265921]  # the last: > 2^30 (exact butterflies)
 
 
 def _mul_cpu(port):
