@@ -86,6 +86,12 @@ struct NttPlan {
 };
 constexpr int LO = 10;
 
+// Shared-memory data words are stored padded, one word per 32: the Stockham
+// passes write at strides 8 and 64 (radix-8), which without padding hit 4-8
+// words per bank (ncu: ~47 % of ntt_rows' shared wavefronts were replays).
+__device__ __forceinline__ int PD(int i) { return i + (i >> 5); }
+constexpr int padded_words(int n) { return n + (n >> 5) + 1; }
+
 // Two Stockham stages at once (radix-4 step): the unit (q, pp), pp < H/2 with
 // H = half/sp, reads the four words x[q + sp*(pp + j*H/2)], j < 4, runs the
 // stage-s butterflies (pp, pp + H/2) and the stage-(s+1) butterflies on their
@@ -99,7 +105,7 @@ __device__ uint32_t* stockham4(uint32_t* x, uint32_t* y, int logL, int logc, con
     // three stages per pass while at least three remain (radix-8 step): the
     // unit (q, pp), pp < H/4, owns x[q + sp*(pp + j*H/4)], j < 8; stage s
     // pairs (j, j+4), stage s+1 pairs (j, j+2) of the results, stage s+2 pairs
-    // (0, 1); outputs land at y[q + sp*(8pp + b0 + 2 b1 + 4 b2)].
+    // (0, 1); outputs land at y[q + sp*(8pp + b0 + 2 b1 + 4 b2)] (padded: PD).
     for (; s + 2 < logL && (logL - s) != 4; s += 3) {
         const int sp = 1 << s, Q = (half >> s) >> 2;
         for (int t = threadIdx.x; t < ((L >> 3) << logc); t += blockDim.x) {
@@ -108,7 +114,7 @@ __device__ uint32_t* stockham4(uint32_t* x, uint32_t* y, int logL, int logc, con
             const int base = c + cols * q, st = cols * sp;
             uint32_t v[8];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) v[j] = x[base + st * (pp + j * Q)];
+            for (int j = 0; j < 8; ++j) v[j] = x[PD(base + st * (pp + j * Q))];
             uint32_t e[8];  // e[2j + b0]: stage-s outputs of pair (j, j+4)
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
@@ -134,8 +140,8 @@ __device__ uint32_t* stockham4(uint32_t* x, uint32_t* y, int logL, int logc, con
                 for (int b1 = 0; b1 < 2; ++b1) {
                     const uint32_t a0 = f[2 * b0 + b1], a1 = f[4 + 2 * b0 + b1];
                     const int o = 8 * pp + b0 + 2 * b1;
-                    y[base + st * o] = bf_add<LZ>(a0, a1, p);
-                    y[base + st * (o + 4)] = bf_subw<LZ>(a0, a1, w, p);
+                    y[PD(base + st * o)] = bf_add<LZ>(a0, a1, p);
+                    y[PD(base + st * (o + 4))] = bf_subw<LZ>(a0, a1, w, p);
                 }
         }
         __syncthreads();
@@ -149,19 +155,19 @@ __device__ uint32_t* stockham4(uint32_t* x, uint32_t* y, int logL, int logc, con
             const int c = t & (cols - 1), u = t >> logc;
             const int pp = u >> s, q = u & (sp - 1);  // u = q + sp*pp, pp < H/2
             const int base = c + cols * q, st = cols * sp;
-            const uint32_t a0 = x[base + st * pp];
-            const uint32_t a1 = x[base + st * (pp + H2)];
-            const uint32_t a2 = x[base + st * (pp + H)];
-            const uint32_t a3 = x[base + st * (pp + H2 + H)];
+            const uint32_t a0 = x[PD(base + st * pp)];
+            const uint32_t a1 = x[PD(base + st * (pp + H2))];
+            const uint32_t a2 = x[PD(base + st * (pp + H))];
+            const uint32_t a3 = x[PD(base + st * (pp + H2 + H))];
             const uint2 w0 = tw[pp * sp], w1 = tw[(pp + H2) * sp], w2 = tw[pp * 2 * sp];
             // stage s: (a0, a2) -> y[2pp], y[2pp+1]; (a1, a3) -> y[2pp+H], y[2pp+H+1]
             const uint32_t e0 = bf_add<LZ>(a0, a2, p), e1 = bf_subw<LZ>(a0, a2, w0, p);
             const uint32_t f0 = bf_add<LZ>(a1, a3, p), f1 = bf_subw<LZ>(a1, a3, w1, p);
             // stage s+1, q' = q + sp*b0: (e_b0, f_b0) -> y'[4pp + b0], y'[4pp + b0 + 2]
-            y[base + st * (4 * pp)] = bf_add<LZ>(e0, f0, p);
-            y[base + st * (4 * pp + 2)] = bf_subw<LZ>(e0, f0, w2, p);
-            y[base + st * (4 * pp + 1)] = bf_add<LZ>(e1, f1, p);
-            y[base + st * (4 * pp + 3)] = bf_subw<LZ>(e1, f1, w2, p);
+            y[PD(base + st * (4 * pp))] = bf_add<LZ>(e0, f0, p);
+            y[PD(base + st * (4 * pp + 2))] = bf_subw<LZ>(e0, f0, w2, p);
+            y[PD(base + st * (4 * pp + 1))] = bf_add<LZ>(e1, f1, p);
+            y[PD(base + st * (4 * pp + 3))] = bf_subw<LZ>(e1, f1, w2, p);
         }
         __syncthreads();
         uint32_t* t = x;
@@ -173,11 +179,11 @@ __device__ uint32_t* stockham4(uint32_t* x, uint32_t* y, int logL, int logc, con
         for (int t = threadIdx.x; t < (half << logc); t += blockDim.x) {
             const int c = t & (cols - 1), i = t >> logc;
             const int pp = i >> s, q = i & (sp - 1);
-            const uint32_t a = x[c + cols * (q + sp * pp)];
-            const uint32_t b = x[c + cols * (q + sp * (pp + half / sp))];
+            const uint32_t a = x[PD(c + cols * (q + sp * pp))];
+            const uint32_t b = x[PD(c + cols * (q + sp * (pp + half / sp)))];
             const uint2 w = tw[pp * sp];
-            y[c + cols * (q + sp * (2 * pp))] = bf_add<LZ>(a, b, p);
-            y[c + cols * (q + sp * (2 * pp + 1))] = bf_subw<LZ>(a, b, w, p);
+            y[PD(c + cols * (q + sp * (2 * pp)))] = bf_add<LZ>(a, b, p);
+            y[PD(c + cols * (q + sp * (2 * pp + 1)))] = bf_subw<LZ>(a, b, w, p);
         }
         __syncthreads();
         uint32_t* t = x;
@@ -220,20 +226,20 @@ __global__ void __launch_bounds__(NTT_T) ntt_cols_fwd(NttArgs g) {
     uint32_t* work = g.work[op] + (inst << P.logN);
     uint2* tw = reinterpret_cast<uint2*>(sm);
     uint32_t* x = sm + N1;  // N1/2 uint2 = N1 words
-    uint32_t* y = x + C * N1;
+    uint32_t* y = x + padded_words(C * N1);
     const int c0 = g.col0 + blockIdx.x * C;
     for (int j = threadIdx.x; j < N1 / 2; j += NTT_T) tw[j] = P.r1f[j];
     for (int t = threadIdx.x; t < C * N1; t += NTT_T) {
         const int c = t & (C - 1), n1 = t >> g.logc;
         const int64_t idx = int64_t(N2) * n1 + c0 + c;
-        x[t] = idx < len ? in[idx] : 0u;
+        x[PD(t)] = idx < len ? in[idx] : 0u;
     }
     __syncthreads();
     uint32_t* r = stockham4<LZ>(x, y, P.log1, g.logc, tw, P.p);
     for (int t = threadIdx.x; t < C * N1; t += NTT_T) {
         const int c = t & (C - 1), k1 = t >> g.logc;
         const uint64_t e = uint64_t(c0 + c) * uint64_t(k1);
-        work[int64_t(N2) * k1 + c0 + c] = twiddle<LZ>(r[t], e, P.tlo_f, P.thi_f, P.p);
+        work[int64_t(N2) * k1 + c0 + c] = twiddle<LZ>(r[PD(t)], e, P.tlo_f, P.thi_f, P.p);
     }
 }
 
@@ -250,29 +256,29 @@ __global__ void __launch_bounds__(NTT_T) ntt_rows(NttArgs g, FieldParams F) {
     uint2* twf = reinterpret_cast<uint2*>(sm);
     uint2* twi = twf + N2 / 2;
     uint32_t* xa = sm + 2 * N2;
-    uint32_t* ya = xa + N2;
-    uint32_t* xb = ya + N2;
-    uint32_t* yb = xb + N2;
+    uint32_t* ya = xa + padded_words(N2);
+    uint32_t* xb = ya + padded_words(N2);
+    uint32_t* yb = xb + padded_words(N2);
     for (int j = threadIdx.x; j < N2 / 2; j += NTT_T) {
         twf[j] = P.r2f[j];
         twi[j] = P.r2i[j];
     }
     for (int t = threadIdx.x; t < N2; t += NTT_T) {
-        xa[t] = wa[t];
-        xb[t] = wb[t];
+        xa[PD(t)] = wa[t];
+        xb[PD(t)] = wb[t];
     }
     __syncthreads();
     // the two forward transforms as one 2-column network: interleave? keep
     // them separate (same code, half the threads idle per stage otherwise)
     uint32_t* ra = stockham4<LZ>(xa, ya, P.log2, 0, twf, P.p);
     uint32_t* rb = stockham4<LZ>(xb, yb, P.log2, 0, twf, P.p);
-    for (int t = threadIdx.x; t < N2; t += NTT_T) ra[t] = mulmod(ra[t], rb[t], F);
+    for (int t = threadIdx.x; t < N2; t += NTT_T) ra[PD(t)] = mulmod(ra[PD(t)], rb[PD(t)], F);
     __syncthreads();
     uint32_t* other = ra == xa ? ya : xa;
     uint32_t* rc = stockham4<LZ>(ra, other, P.log2, 0, twi, P.p);
     for (int t = threadIdx.x; t < N2; t += NTT_T) {
         const uint64_t e = (uint64_t(1) << P.logN) - (uint64_t(t) * uint64_t(k1));
-        wa[t] = twiddle<LZ>(rc[t], e & ((uint64_t(1) << P.logN) - 1), P.tlo_f, P.thi_f, P.p);
+        wa[t] = twiddle<LZ>(rc[PD(t)], e & ((uint64_t(1) << P.logN) - 1), P.tlo_f, P.thi_f, P.p);
     }
 }
 
@@ -287,19 +293,19 @@ __global__ void __launch_bounds__(NTT_T) ntt_cols_inv(NttArgs g) {
     uint32_t* out = g.out + inst * g.ldf;
     uint2* tw = reinterpret_cast<uint2*>(sm);
     uint32_t* x = sm + N1;
-    uint32_t* y = x + C * N1;
+    uint32_t* y = x + padded_words(C * N1);
     const int c0 = g.col0 + blockIdx.x * C;
     for (int j = threadIdx.x; j < N1 / 2; j += NTT_T) tw[j] = P.r1i[j];
     for (int t = threadIdx.x; t < C * N1; t += NTT_T) {
         const int c = t & (C - 1), k1 = t >> g.logc;
-        x[t] = work[int64_t(N2) * k1 + c0 + c];
+        x[PD(t)] = work[int64_t(N2) * k1 + c0 + c];
     }
     __syncthreads();
     uint32_t* r = stockham4<LZ>(x, y, P.log1, g.logc, tw, P.p);
     for (int t = threadIdx.x; t < C * N1; t += NTT_T) {
         const int c = t & (C - 1), n1 = t >> g.logc;
         const int64_t idx = int64_t(N2) * n1 + c0 + c;
-        if (idx < g.nf) out[idx] = shoup(r[t], P.scale, P.scale_p, P.p);
+        if (idx < g.nf) out[idx] = shoup(r[PD(t)], P.scale, P.scale_p, P.p);
     }
 }
 
@@ -433,8 +439,8 @@ void run_ntt(const FieldParams& F, const uint32_t* A, int64_t lda, int64_t na, c
     const int64_t chunk = std::min<int64_t>(count, 65535);
     g.work[0] = sc.get<uint32_t>(size_t(chunk) << logN);
     g.work[1] = sc.get<uint32_t>(size_t(chunk) << logN);
-    const size_t sm1 = size_t(N1 + 2 * g.cols * N1) * 4;
-    const size_t sm2 = size_t(2 * N2 + 4 * N2) * 4;
+    const size_t sm1 = size_t(N1 + 2 * padded_words(g.cols * N1)) * 4;
+    const size_t sm2 = size_t(2 * N2 + 4 * padded_words(N2)) * 4;
     if (F.p < (1u << 30))
         run_ntt_launches<true>(g, F, N1, N2, count, chunk, A, lda, B, ldb, Fo, ldf, sm1, sm2, st);
     else
@@ -523,8 +529,8 @@ void launch_ntt_phase(const FieldParams& F, int phase, const uint32_t* a, int64_
     if (n < 0 || start < 0 || start + n > lim || (phase != 1 && (start % g.cols || n % g.cols)))
         throw Error(ST_INVALID, "ntt phase: slice outside the transform or not column-aligned");
     if (n == 0) return;
-    const size_t sm1 = size_t(N1 + 2 * g.cols * N1) * 4;
-    const size_t sm2 = size_t(2 * N2 + 4 * N2) * 4;
+    const size_t sm1 = size_t(N1 + 2 * padded_words(g.cols * N1)) * 4;
+    const size_t sm2 = size_t(2 * N2 + 4 * padded_words(N2)) * 4;
     if (F.p < (1u << 30))
         phase_launch<true>(g, F, phase, start, n, sm1, sm2, st);
     else
