@@ -705,11 +705,6 @@ __device__ void run_replay(int col, const StepLog* log, volatile int* done, int 
 }  // namespace
 
 // ------------------------------------------------------- flags (gpu scope) --
-__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
-    unsigned v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
 __device__ __forceinline__ void st_release_gpu(unsigned* p, unsigned v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -731,13 +726,6 @@ __device__ void window_from_global(uint32_t* win, const uint32_t* Z, long long& 
     __syncwarp();
 }
 
-// top[i] = Z[deg - i] for i < n (0 outside), all threads of the CTA.
-__device__ void load_top_region(uint32_t* top, const uint32_t* Z, long long deg, int n) {
-    for (int i = threadIdx.x; i < n; i += GCD_T) {
-        const long long x = deg - i;
-        top[i] = (x >= 0) ? __ldcg(Z + x) : 0u;
-    }
-}
 
 // Both next windows, top-aligned, from S_j's top region and the batch matrix:
 //   winA[t] = sum_e Pa1[e] topA[t+e] + sum_e Pa2[e] topB[t+e]   (t < W1)
