@@ -69,6 +69,7 @@ struct BatchMeta {
     int steps, term, dividend_a, err;
     int sa, sb;          // total shifts of A and B (top moves)
     int hi[4];           // highest nonzero index of Pa1, Pa2, Pb1, Pb2
+    long long tpub;      // MMM_GCD_STATS: %globaltimer at publication
 };
 
 constexpr int RING = 4;  // published matrices in flight
@@ -403,32 +404,92 @@ __device__ __forceinline__ int fused_step(uint32_t (&u)[GE], const uint32_t (&v)
     return 2 + z;
 }
 
-// The fused pair as the steady state's fast path: everything is computed
-// speculatively (the shifted copies before the scalars are known) and kept
-// only if both cc and the new lead are nonzero; otherwise u is untouched and
-// the general path takes over.
-__device__ __forceinline__ bool fused_fast(uint32_t (&u)[GE], const uint32_t (&v)[GE], uint32_t& hu,
-                                           uint32_t& hu1, uint32_t hv, uint32_t hv1, Fld f,
-                                           uint32_t& al, uint32_t& be, uint32_t& ga) {
+// The fused pair as the steady state's fast path, with scalar lookahead: the
+// new leads u'0 = (alpha*u2 + beta*v2 + gamma*v1)/R and u'1 (the same one
+// word down) are computed as scalars from the operands' broadcast words 0..3,
+// so the critical path is cc -> gamma -> one 3-term reduction; the vector
+// update and the broadcast of u'2, u'3 (needed two pairs later as the
+// dividend's, one pair later as the divisor's) run off it.  Everything is
+// speculative and kept only if cc and u'0 are nonzero; otherwise u and its
+// words are untouched and the general path takes over.
+__device__ __forceinline__ bool fused_la(uint32_t (&u)[GE], const uint32_t (&v)[GE], uint32_t& u0,
+                                         uint32_t& u1, uint32_t& u2, uint32_t& u3, uint32_t v0,
+                                         uint32_t v1, uint32_t v2, uint32_t v3, Fld f,
+                                         uint32_t& al, uint32_t& be, uint32_t& ga) {
     using A = Arith<0>;
     const uint32_t p = f.p;
     uint32_t us2[GE], vs2[GE], vs1[GE], nu[GE];
     shl_copy<2>(u, us2);
     shl_copy<2>(v, vs2);
     shl_copy<1>(v, vs1);
-    const uint32_t nx = A::neg(hu, p);
-    const uint32_t cc = A::comb(hv, hu1, nx, hv1, f);
-    al = A::mont(hv, hv, f);
-    be = A::mont(hv, nx, f);
+    const uint32_t nx = A::neg(u0, p);
+    const uint32_t cc = A::comb(v0, u1, nx, v1, f);
+    al = A::mont(v0, v0, f);
+    be = A::mont(v0, nx, f);
     ga = A::canon(A::neg(cc, p), p);
+    const uint32_t n0 = A::comb3(al, u2, be, v2, ga, v1, f);
+    const uint32_t n1 = A::comb3(al, u3, be, v3, ga, v2, f);
 #pragma unroll
     for (int e = 0; e < GE; ++e) nu[e] = A::comb3(al, us2[e], be, vs2[e], ga, vs1[e], f);
-    const uint32_t n0 = bcast(nu[0]), n1 = from_lane(nu[0], 1);
     if (!(A::nz(cc, p) && A::nz(n0, p))) return false;
 #pragma unroll
     for (int e = 0; e < GE; ++e) u[e] = nu[e];
-    hu = n0;
-    hu1 = n1;
+    u0 = n0;
+    u1 = n1;
+    u2 = from_lane(nu[0], 2);
+    u3 = from_lane(nu[0], 3);
+    return true;
+}
+
+// Two fused pairs back to back (u by v, then v by the new u) as one
+// branch-free block: the four nonzero conditions are checked once at the end
+// and nothing is committed unless all hold, so the scheduler can interleave
+// the second pair's scalar chain with the first pair's vector update (in-order
+// issue would otherwise stall the second chain behind the first's shuffles).
+struct PairOut {
+    uint32_t al1, be1, ga1, al2, be2, ga2;
+};
+__device__ __forceinline__ bool fused_pair_la(uint32_t (&u)[GE], uint32_t (&v)[GE], uint32_t& u0,
+                                              uint32_t& u1, uint32_t& u2, uint32_t& u3,
+                                              uint32_t& v0, uint32_t& v1, uint32_t& v2,
+                                              uint32_t& v3, Fld f, PairOut& o) {
+    using A = Arith<0>;
+    const uint32_t p = f.p;
+    uint32_t us2[GE], vs2[GE], vs1[GE], nu[GE], nus2[GE], nus1[GE], nv[GE];
+    shl_copy<2>(u, us2);
+    shl_copy<2>(v, vs2);
+    shl_copy<1>(v, vs1);
+    // pair 1: u <- u - (q1 X + q0) v
+    const uint32_t nx = A::neg(u0, p);
+    const uint32_t cc1 = A::comb(v0, u1, nx, v1, f);
+    const uint32_t al1 = A::mont(v0, v0, f), be1 = A::mont(v0, nx, f);
+    const uint32_t ga1 = A::canon(A::neg(cc1, p), p);
+    const uint32_t n0 = A::comb3(al1, u2, be1, v2, ga1, v1, f);
+    const uint32_t n1 = A::comb3(al1, u3, be1, v3, ga1, v2, f);
+#pragma unroll
+    for (int e = 0; e < GE; ++e) nu[e] = A::comb3(al1, us2[e], be1, vs2[e], ga1, vs1[e], f);
+    const uint32_t n2 = from_lane(nu[0], 2), n3 = from_lane(nu[0], 3);
+    shl_copy<2>(nu, nus2);
+    shl_copy<1>(nu, nus1);
+    // pair 2: v <- v - (r1 X + r0) u'
+    const uint32_t ny = A::neg(v0, p);
+    const uint32_t cc2 = A::comb(n0, v1, ny, n1, f);
+    const uint32_t al2 = A::mont(n0, n0, f), be2 = A::mont(n0, ny, f);
+    const uint32_t ga2 = A::canon(A::neg(cc2, p), p);
+    const uint32_t m0 = A::comb3(al2, v2, be2, n2, ga2, n1, f);
+    const uint32_t m1 = A::comb3(al2, v3, be2, n3, ga2, n2, f);
+#pragma unroll
+    for (int e = 0; e < GE; ++e) nv[e] = A::comb3(al2, vs2[e], be2, nus2[e], ga2, nus1[e], f);
+    const uint32_t m2 = from_lane(nv[0], 2), m3 = from_lane(nv[0], 3);
+    if (!(A::nz(cc1, p) & A::nz(n0, p) & A::nz(cc2, p) & A::nz(m0, p))) return false;
+#pragma unroll
+    for (int e = 0; e < GE; ++e) {
+        u[e] = nu[e];
+        v[e] = nv[e];
+    }
+    u0 = n0, u1 = n1, u2 = n2, u3 = n3;
+    v0 = m0, v1 = m1, v2 = m2, v3 = m3;
+    o = PairOut{al1, be1, ga1, al2, be2, ga2};
     return true;
 }
 
@@ -483,30 +544,36 @@ __device__ void run_chain(BatchMeta& c, StepLog* log, volatile int* done, int jb
         }
         if (MODE == 0) {
             // steady state: degree-1 quotients, roles alternating every pair;
-            // straight-line A-then-B pairs (a taken branch costs ~20 cycles)
+            // straight-line A-then-B pairs (a taken branch costs ~20 cycles).
+            // Words 2, 3 of both windows as scalars for the lookahead (F >= 4
+            // keeps at least 6 valid words).
             uint32_t al, be, ga;
-            if (!dividend_a && F >= 2 && db == da + 1 && da >= 1 &&
-                fused_fast(wb, wa, hb, hb1, ha, ha1, f, al, be, ga)) {  // align to A
-                db -= 2;
-                F -= 2;
-                steps += 2;
-                log_entry(lb, n++, par, al, be, ga, LOG_FUSED | 2u);
-                dividend_a = 1;
-            }
-            if (dividend_a) {
-                while (F >= 4 && da == db + 1 && db >= 2) {
-                    if (!fused_fast(wa, wb, ha, ha1, hb, hb1, f, al, be, ga)) break;
-                    da -= 2;
-                    F -= 2;
-                    steps += 2;
-                    log_entry(lb, n++, par, al, be, ga, LOG_FUSED | LOG_UA | 2u);
-                    dividend_a = 0;  // now db == da + 1, da >= 1
-                    if (!fused_fast(wb, wa, hb, hb1, ha, ha1, f, al, be, ga)) break;
-                    db -= 2;
+            if (F >= 4 && (dividend_a ? da == db + 1 && db >= 2 : db == da + 1 && da >= 2)) {
+                uint32_t ha2 = from_lane(wa[0], 2), ha3 = from_lane(wa[0], 3);
+                uint32_t hb2 = from_lane(wb[0], 2), hb3 = from_lane(wb[0], 3);
+                if (!dividend_a &&
+                    fused_la(wb, wa, hb, hb1, hb2, hb3, ha, ha1, ha2, ha3, f, al, be, ga)) {
+                    db -= 2;  // align to A
                     F -= 2;
                     steps += 2;
                     log_entry(lb, n++, par, al, be, ga, LOG_FUSED | 2u);
                     dividend_a = 1;
+                }
+                if (dividend_a) {
+                    // whole A-then-B rounds (F >= 4 also covers the second pair's
+                    // lookahead words).  A failed round commits nothing:
+                    // the general path below retakes its first pair.
+                    PairOut o;
+                    while (F >= 4 && da == db + 1 && db >= 2 &&
+                           fused_pair_la(wa, wb, ha, ha1, ha2, ha3, hb, hb1, hb2, hb3, f, o)) {
+                        log_entry(lb, n, par, o.al1, o.be1, o.ga1, LOG_FUSED | LOG_UA | 2u);
+                        log_entry(lb, n + 1, par, o.al2, o.be2, o.ga2, LOG_FUSED | 2u);
+                        n += 2;
+                        da -= 2;
+                        db -= 2;
+                        F -= 4;
+                        steps += 4;
+                    }
                 }
             }
             if (F <= 0) continue;  // refresh first
@@ -705,6 +772,11 @@ __device__ void run_replay(int col, const StepLog* log, volatile int* done, int 
 }  // namespace
 
 // ------------------------------------------------------- flags (gpu scope) --
+__device__ __forceinline__ long long gtimer() {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 __device__ __forceinline__ void st_release_gpu(unsigned* p, unsigned v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -778,8 +850,10 @@ __device__ int head_cta(const GcdArgs& g, BatchMeta& ctl, StepLog* log, uint32_t
     uint32_t* red = Ps + 4 * PL;        // BUILD_PARTS x 2 * W1 builder partials
     __shared__ int fallback;
     __shared__ long long da0s[2], db0s[2];  // batch start degrees, by batch parity
-    __shared__ long long hst[10];  // MMM_GCD_STATS: accumulated here, flushed at the end
-    if (threadIdx.x < 10) hst[threadIdx.x] = 0;
+    __shared__ long long hst[12];  // MMM_GCD_STATS: accumulated here, flushed at the end
+    __shared__ long long tpub_s;
+    if (threadIdx.x < 12) hst[threadIdx.x] = 0;
+    if (threadIdx.x == 0) tpub_s = 0;
     if (threadIdx.x == 0) *done = 0;
     for (int i = threadIdx.x; i < LOGCAP; i += GCD_T)  // no stale tags from earlier kernels
         reinterpret_cast<uint4*>(log)[i] = make_uint4(0u, 0u, 0u, 0u);
@@ -807,8 +881,13 @@ __device__ int head_cta(const GcdArgs& g, BatchMeta& ctl, StepLog* log, uint32_t
             if (g.stats && threadIdx.x == 32) hst[5] += clock64() - t0;
         } else {
             // prefetch: S_j complete once the bulk applied batch j-1
-            if (threadIdx.x == 96)
+            if (threadIdx.x == 96) {
                 spin_until_geq(g.flags + 1, unsigned(j) * nbulk);
+                if (g.stats && j > 0) {
+                    hst[10] += gtimer() - tpub_s;
+                    hst[11] += 1;
+                }
+            }
             bar_sync(1, GCD_T - 96);  // warps 3-7 (warp 7 may come from its publish)
             const long long da0 = da0s[j & 1], db0 = db0s[j & 1];
             for (int i = threadIdx.x - 96; i < W1 + PL; i += GCD_T - 96) {
@@ -828,6 +907,10 @@ __device__ int head_cta(const GcdArgs& g, BatchMeta& ctl, StepLog* log, uint32_t
         const bool last = m.term || m.err;
         if (warp == 7) {  // publish batch j
             if (threadIdx.x == 224) {
+                if (g.stats) {
+                    m.tpub = gtimer();
+                    tpub_s = m.tpub;
+                }
                 g.meta[j % RING] = m;
                 __threadfence();
                 st_release_gpu(g.flags + 0, unsigned(j + 1));
@@ -838,8 +921,11 @@ __device__ int head_cta(const GcdArgs& g, BatchMeta& ctl, StepLog* log, uint32_t
             }
             if (last) {
                 __syncthreads();  // with warps 0-6 (same branch): hst complete
-                if (g.stats && threadIdx.x == 224)
+                if (g.stats && threadIdx.x == 224) {
                     for (int i = 0; i < 10; ++i) g.stats[i == 7 ? 8 : (i == 8 ? 9 : (i == 9 ? 10 : i))] = hst[i];
+                    g.stats[17] = hst[10];
+                    g.stats[19] = hst[11];
+                }
                 return j;
             }
             continue;  // next batch: prefetch group
@@ -914,7 +1000,8 @@ constexpr int APPLY_OUT = GCD_T;  // outputs per pass: one work item per thread
 constexpr int APPLY_WORDS = 4 * PL + 2 * (APPLY_OUT + 8) + 4 * (PL + 4);
 
 __device__ void apply_batch(const GcdArgs& g, const BatchMeta& m, const uint32_t* Pglob, int j,
-                            long long s0, long long s1, uint32_t* sm) {
+                            long long s0, long long s1, uint32_t* sm, long long* ph) {
+    const long long tb = ph ? clock64() : 0;
     const FieldParams F = g.F;
     const int tid = threadIdx.x;
     uint32_t* P = sm;  // Pa1, Pa2, Pb1, Pb2
@@ -934,6 +1021,7 @@ __device__ void apply_batch(const GcdArgs& g, const BatchMeta& m, const uint32_t
         const int L[2] = {4 * qn[0] + PL + 4, 4 * qn[1] + PL + 4};
         uint32_t* W[4] = {Wb, Wb + L[0], Wb + 2 * L[0], Wb + 2 * L[0] + L[1]};
         __syncthreads();  // previous pass done with the windows
+        if (ph && c0 == s0) ph[0] += clock64() - tb;
         // W[2r + t][y] = Z_t[xs_r + sh - (PL - 1) + y], zero outside [0, deg_t]
 #pragma unroll
         for (int w = 0; w < 4; ++w) {
@@ -945,6 +1033,7 @@ __device__ void apply_batch(const GcdArgs& g, const BatchMeta& m, const uint32_t
             }
         }
         __syncthreads();
+        if (ph && c0 == s0) ph[1] += clock64() - tb;
         const int items = 4 * (qn[0] + qn[1]);
         // selects instead of runtime-indexed arrays (those live in local memory)
         const int h00 = m.hi[0], h01 = m.hi[1], h10 = m.hi[2], h11 = m.hi[3];
@@ -983,6 +1072,7 @@ __device__ void apply_batch(const GcdArgs& g, const BatchMeta& m, const uint32_t
             }
         }
     }
+    if (ph) ph[2] += clock64() - tb;
 }
 
 // CTAs 1..G-1: apply batch j's matrix to this CTA's slice of both operands,
@@ -990,6 +1080,7 @@ __device__ void apply_batch(const GcdArgs& g, const BatchMeta& m, const uint32_t
 __device__ int bulk_cta(const GcdArgs& g, uint32_t* sm, int nbulk, int me) {
     __shared__ BatchMeta ms;
     long long apply_cycles = 0;  // MMM_GCD_STATS (bulk CTA 0, thread 0)
+    long long ph[3] = {0, 0, 0}, seen_ns = 0;
     for (int j = 0;; ++j) {
         cta_wait_ge(g.flags + 0, unsigned(j + 1));
         if (threadIdx.x == 0) {
@@ -998,6 +1089,7 @@ __device__ int bulk_cta(const GcdArgs& g, uint32_t* sm, int nbulk, int me) {
             ms.steps = vm->steps; ms.term = vm->term; ms.err = vm->err;
             ms.sa = vm->sa; ms.sb = vm->sb;
             for (int i = 0; i < 4; ++i) ms.hi[i] = vm->hi[i];
+            if (g.stats) seen_ns += gtimer() - vm->tpub;
         }
         // S_j is complete without a poll: CTA 0 acquired flags[1] >= j * nbulk
         // (its prefetch) before the bar.sync preceding this batch's release of
@@ -1011,7 +1103,8 @@ __device__ int bulk_cta(const GcdArgs& g, uint32_t* sm, int nbulk, int me) {
             const long long per = (na1 + nb1 + nbulk - 1) / nbulk;
             const long long s0 = min((long long)me * per, na1 + nb1);
             const long long s1 = min(s0 + per, na1 + nb1);
-            apply_batch(g, m, g.Pg + (j % RING) * 4 * PL, j, s0, s1, sm);
+            apply_batch(g, m, g.Pg + (j % RING) * 4 * PL, j, s0, s1, sm,
+                        (g.stats && me == 0 && threadIdx.x == 0) ? ph : nullptr);
         }
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -1020,7 +1113,14 @@ __device__ int bulk_cta(const GcdArgs& g, uint32_t* sm, int nbulk, int me) {
             apply_cycles += clock64() - tb;
         }
         if (m.term || m.err) {
-            if (g.stats && me == 0 && threadIdx.x == 0) g.stats[7] = apply_cycles;
+            if (g.stats && me == 0 && threadIdx.x == 0) {
+                g.stats[7] = apply_cycles;
+                g.stats[12] = seen_ns;
+                g.stats[13] = ph[0];
+                g.stats[14] = ph[1];
+                g.stats[15] = ph[2];
+            }
+            if (g.stats && me == nbulk - 1 && threadIdx.x == 0) g.stats[18] = seen_ns;
             return j;
         }
     }
@@ -1112,14 +1212,14 @@ void launch_gcd(const FieldParams& F, const uint32_t* a, int64_t na, const uint3
     const bool want_stats = getenv("MMM_GCD_STATS") != nullptr;
     if (const char* d = getenv("MMM_GCD_DEBUG")) g.dbg = atoi(d);
     if (want_stats) {
-        g.stats = sc.get<long long>(12);
-        MMM_CUDA(cudaMemsetAsync(g.stats, 0, 12 * sizeof(long long), st));
+        g.stats = sc.get<long long>(24);
+        MMM_CUDA(cudaMemsetAsync(g.stats, 0, 24 * sizeof(long long), st));
     }
     void* params[] = {&g};
     MMM_CUDA(cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(GCD_T), params, bytes, st));
     check_launch("gcd_kernel");
     if (want_stats) {
-        long long h[12];
+        long long h[24];
         MMM_CUDA(cudaMemcpyAsync(h, g.stats, sizeof(h), cudaMemcpyDeviceToHost, st));
         MMM_CUDA(cudaStreamSynchronize(st));
         fprintf(stderr,
@@ -1128,6 +1228,10 @@ void launch_gcd(const FieldParams& F, const uint32_t* a, int64_t na, const uint3
                 "prefetch_cycles=%lld bulk0_apply_cycles=%lld builder_own_done=%lld "
                 "builders_synced=%lld\n",
                 blocks, h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7], h[8], h[9]);
+        fprintf(stderr,
+                "gcd latency: bulk0_seen_ns=%lld bulk0_P_cyc=%lld bulk0_win_cyc=%lld "
+                "bulk0_comp_cyc=%lld head_prefetch_seen_ns=%lld (%lld) bulkLast_seen_ns=%lld\n",
+                h[12], h[13], h[14], h[15], h[17], h[19], h[18]);
     }
 }
 
