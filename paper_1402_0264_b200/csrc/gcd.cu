@@ -54,7 +54,10 @@ constexpr int W1 = 32 * GE;        // window words per operand
 constexpr int PE = GCD_PE;         // matrix words per lane per polynomial
 constexpr int PL = 32 * PE;        // matrix capacity (support < PL)
 constexpr int LOGCAP = 512;        // log entries per batch (<= PL + 1 in practice)
-constexpr int BIG = 1 << 30;       // "validity unbounded": window covers the operand
+constexpr int BIG = 1 << 30;
+#ifndef GCD_CHAIN_LA
+#define GCD_CHAIN_LA 0  // steady state: 1 = scalar-lookahead rounds (faster alone, slower in the kernel)
+#endif       // "validity unbounded": window covers the operand
 
 struct StepLog {
     uint32_t x, y;
@@ -63,26 +66,40 @@ struct StepLog {
 };
 
 // Published per batch by CTA 0 into a ring slot, read by the bulk CTAs.
+// All 32-bit fields, in the order of the record's meta words, so that lane l
+// of the bulk's polling warp stores word l with one shared store (a switch
+// over the fields diverges and costs ~1 us of serial address conversions).
 struct BatchMeta {
-    long long da0, db0;  // exact degrees at batch start (-1: zero operand)
-    long long da1, db1;  // degree bounds after the batch (-1: vanished)
+    int da0, db0;        // exact degrees at batch start (-1: zero operand)
+    int da1, db1;        // degree bounds after the batch (-1: vanished)
     int steps, term, dividend_a, err;
     int sa, sb;          // total shifts of A and B (top moves)
     int hi[4];           // highest nonzero index of Pa1, Pa2, Pb1, Pb2
-    long long tpub;      // MMM_GCD_STATS: %globaltimer at publication
+    int tpub_lo, tpub_hi;  // MMM_GCD_STATS: %globaltimer at publication
+    int minprog;         // min bulk progress the head saw (bulk ring guard)
 };
 
-constexpr int RING = 4;  // published matrices in flight
+constexpr int RING = 4;  // published batch records in flight
+constexpr int NBUF = 4;  // state buffers: batch j reads j % NBUF, writes (j+1) % NBUF
+constexpr int META_W = 17;             // meta words of a batch record
+constexpr int REC_W = 4 * PL + META_W;  // record: Pa1, Pa2, Pb1, Pb2 (canonical), meta
 
+// Cross-CTA data are tagged words, (tag << 32) | value, written and read with
+// single-copy-atomic 64-bit relaxed accesses: a reader polls the very words it
+// needs until their tag is the one it expects, so no flag, fence or counter
+// sits between a producer's store and a consumer's use (one L2 round trip).
+// State S_j (the operands after j batches) carries tag j + 1; batch j's record
+// tag j + 1.
 struct GcdArgs {
     const uint32_t* a;
     const uint32_t* b;
     long long na, nb;
-    uint32_t* XA[3];      // state of A, triple-buffered: batch j reads j%3, writes (j+1)%3
-    uint32_t* XB[3];
-    uint32_t* Pg;         // RING x (Pa1, Pa2, Pb1, Pb2), PL words each, canonical
-    BatchMeta* meta;      // RING slots
-    unsigned* flags;      // [0] batches published by CTA 0, [1] bulk CTA-batches applied
+    uint64_t* XA[NBUF];   // tagged state of A
+    uint64_t* XB[NBUF];
+    uint64_t* rec;        // RING tagged batch records (REC_W words each)
+    long long cap;        // words per state buffer
+    unsigned* prog;       // per bulk CTA: batches finished (ring-reuse guards only; a
+                          // shared counter would serialise 147 atomics per batch)
     uint32_t* g;
     int64_t* ng;
     int M;                // steps per batch (the program parameter s)
@@ -152,6 +169,48 @@ __device__ __forceinline__ int ld_acquire_cta(volatile int* p) {
     return v;
 }
 
+__device__ __forceinline__ long long gtimer() {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ uint64_t ld_rlx64(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ void st_tag(uint64_t* p, uint32_t v, unsigned tag) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"((uint64_t(tag) << 32) | v)
+                 : "memory");
+}
+// The value of a tagged word already loaded as w, re-polled until it carries `tag`.
+__device__ __forceinline__ uint32_t tag_resolve(const uint64_t* p, uint64_t w, unsigned tag) {
+    while (unsigned(w >> 32) != tag) {
+#ifdef GCD_POLL_SLEEP
+        __nanosleep(GCD_POLL_SLEEP);
+#endif
+        w = ld_rlx64(p);
+    }
+    return uint32_t(w);
+}
+// K tagged words already loaded into w[]: re-poll every stale one together
+// (one round trip per round, not one per word) until all carry `tag`.
+template <int K>
+__device__ __forceinline__ void tag_resolve_all(const uint64_t* const (&p)[K], uint64_t (&w)[K],
+                                                unsigned tag) {
+    for (;;) {
+        bool ok = true;
+#pragma unroll
+        for (int k = 0; k < K; ++k) ok &= unsigned(w[k] >> 32) == tag;
+        if (ok) return;
+#pragma unroll
+        for (int k = 0; k < K; ++k)
+            if (unsigned(w[k] >> 32) != tag) w[k] = ld_rlx64(p[k]);
+    }
+}
+__device__ __forceinline__ uint32_t ld_tag(const uint64_t* p, unsigned tag) {
+    return tag_resolve(p, ld_rlx64(p), tag);
+}
 __device__ __forceinline__ uint32_t bcast(uint32_t v) { return __shfl_sync(0xffffffffu, v, 0); }
 __device__ __forceinline__ uint32_t from_lane(uint32_t v, int l) {
     return __shfl_sync(0xffffffffu, v, l);
@@ -253,23 +312,6 @@ __device__ __forceinline__ int first_nz(const uint32_t (&w)[N], int from, uint32
     return z;
 }
 
-// Load the top W1 words of Z below `deg` into w; lower `deg` past zero words
-// until w[0] is the nonzero lead (or deg = -1: zero operand).  Warp-uniform.
-template <int MODE>
-__device__ void load_top(uint32_t (&w)[GE], const uint32_t* Z, long long& deg, uint32_t p) {
-    const int lane = threadIdx.x & 31;
-    while (deg >= 0) {
-#pragma unroll
-        for (int e = 0; e < GE; ++e) {
-            const long long x = deg - (e * 32 + lane);
-            w[e] = x >= 0 ? __ldcg(Z + x) : 0u;
-        }
-        const int z = first_nz<MODE>(w, 0, p);
-        if (z == 0) return;
-        deg -= z < 0 ? W1 : z;
-    }
-}
-
 // Log entry, stored by every lane of the chain warp (same address, same
 // value: no divergence, no fence).  Single step: (x, y, 0, meta), the
 // dividend u <- y*u - x*v shifted by z.  Fused pair (MODE 0): (alpha, beta,
@@ -287,8 +329,14 @@ __device__ __forceinline__ unsigned log_base(const StepLog* log) {
     return static_cast<unsigned>(__cvta_generic_to_shared(const_cast<StepLog*>(log)));
 }
 __device__ __forceinline__ unsigned log_seq(int /*i*/, unsigned tag) { return tag; }
+#ifdef GCD_TRACE  // tools/chain_bench2: per-entry write / replay clocks
+__device__ long long g_tw[LOGCAP], g_tr[LOGCAP], g_tp[LOGCAP], g_ta[LOGCAP], g_tb[LOGCAP];
+#endif
 __device__ __forceinline__ void log_entry(unsigned lb, int i, unsigned par, uint32_t c0, uint32_t c1,
                                           uint32_t c2, unsigned meta) {
+#ifdef GCD_TRACE
+    if ((threadIdx.x & 31) == 0) g_tw[i] = clock64();
+#endif
     const unsigned a = lb + unsigned(i) * 16u;
     asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(c0), "r"(c1), "r"(c2),
                  "r"(meta | (log_seq(i, par) << 10)));
@@ -402,6 +450,35 @@ __device__ __forceinline__ int fused_step(uint32_t (&u)[GE], const uint32_t (&v)
     hu = bcast(u[0]);
     hu1 = from_lane(u[0], 1);
     return 2 + z;
+}
+
+// The fused pair as the steady state's fast path: everything is computed
+// speculatively (the shifted copies before the scalars are known) and kept
+// only if both cc and the new lead are nonzero; otherwise u is untouched and
+// the general path takes over.
+__device__ __forceinline__ bool fused_fast(uint32_t (&u)[GE], const uint32_t (&v)[GE], uint32_t& hu,
+                                           uint32_t& hu1, uint32_t hv, uint32_t hv1, Fld f,
+                                           uint32_t& al, uint32_t& be, uint32_t& ga) {
+    using A = Arith<0>;
+    const uint32_t p = f.p;
+    uint32_t us2[GE], vs2[GE], vs1[GE], nu[GE];
+    shl_copy<2>(u, us2);
+    shl_copy<2>(v, vs2);
+    shl_copy<1>(v, vs1);
+    const uint32_t nx = A::neg(hu, p);
+    const uint32_t cc = A::comb(hv, hu1, nx, hv1, f);
+    al = A::mont(hv, hv, f);
+    be = A::mont(hv, nx, f);
+    ga = A::canon(A::neg(cc, p), p);
+#pragma unroll
+    for (int e = 0; e < GE; ++e) nu[e] = A::comb3(al, us2[e], be, vs2[e], ga, vs1[e], f);
+    const uint32_t n0 = bcast(nu[0]), n1 = from_lane(nu[0], 1);
+    if (!(A::nz(cc, p) && A::nz(n0, p))) return false;
+#pragma unroll
+    for (int e = 0; e < GE; ++e) u[e] = nu[e];
+    hu = n0;
+    hu1 = n1;
+    return true;
 }
 
 // The fused pair as the steady state's fast path, with scalar lookahead: the
@@ -548,6 +625,32 @@ __device__ void run_chain(BatchMeta& c, StepLog* log, volatile int* done, int jb
             // Words 2, 3 of both windows as scalars for the lookahead (F >= 4
             // keeps at least 6 valid words).
             uint32_t al, be, ga;
+#if GCD_CHAIN_LA == 0
+            if (!dividend_a && F >= 2 && db == da + 1 && da >= 1 &&
+                fused_fast(wb, wa, hb, hb1, ha, ha1, f, al, be, ga)) {  // align to A
+                db -= 2;
+                F -= 2;
+                steps += 2;
+                log_entry(lb, n++, par, al, be, ga, LOG_FUSED | 2u);
+                dividend_a = 1;
+            }
+            if (dividend_a) {
+                while (F >= 4 && da == db + 1 && db >= 2) {
+                    if (!fused_fast(wa, wb, ha, ha1, hb, hb1, f, al, be, ga)) break;
+                    da -= 2;
+                    F -= 2;
+                    steps += 2;
+                    log_entry(lb, n++, par, al, be, ga, LOG_FUSED | LOG_UA | 2u);
+                    dividend_a = 0;  // now db == da + 1, da >= 1
+                    if (!fused_fast(wb, wa, hb, hb1, ha, ha1, f, al, be, ga)) break;
+                    db -= 2;
+                    F -= 2;
+                    steps += 2;
+                    log_entry(lb, n++, par, al, be, ga, LOG_FUSED | 2u);
+                    dividend_a = 1;
+                }
+            }
+#else
             if (F >= 4 && (dividend_a ? da == db + 1 && db >= 2 : db == da + 1 && da >= 2)) {
                 uint32_t ha2 = from_lane(wa[0], 2), ha3 = from_lane(wa[0], 3);
                 uint32_t hb2 = from_lane(wb[0], 2), hb3 = from_lane(wb[0], 3);
@@ -576,6 +679,7 @@ __device__ void run_chain(BatchMeta& c, StepLog* log, volatile int* done, int jb
                     }
                 }
             }
+#endif
             if (F <= 0) continue;  // refresh first
         }
         const int du = dividend_a ? da : db, dv = dividend_a ? db : da;
@@ -685,11 +789,17 @@ __device__ __forceinline__ void replay_entry(uint32_t (&u)[PE], const uint32_t (
 // publish the column (canonical) to Pg and Ps.
 template <int MODE>
 __device__ void run_replay(int col, const StepLog* log, volatile int* done, int jb, Fld f,
-                           uint32_t* Pg, uint32_t* Ps, int* hi_out) {
+                           uint64_t* rec, unsigned rtag, uint32_t* Ps, int* hi_out,
+                           volatile int* ring_ok, long long* tex = nullptr) {
     const unsigned par = batch_tag(jb);
     // the chain finished this batch with fewer than i + 1 entries
+    // A plain (volatile) read: `done` only bounds the entry count, and every
+    // entry carries its own tag.  The shared address is converted once (the
+    // conversion reads SR_CgaCtaId, slow, and this runs in the polling loop).
+    const unsigned done_sa = static_cast<unsigned>(__cvta_generic_to_shared(const_cast<int*>(done)));
     auto ended = [&](int i) {
-        const unsigned d = unsigned(ld_acquire_cta(done));
+        unsigned d;
+        asm volatile("ld.volatile.shared::cta.u32 %0, [%1];" : "=r"(d) : "r"(done_sa));
         return (d >> 10) == par && int(d & 0x3FFu) - 1 <= i;
     };
     using A = Arith<MODE>;
@@ -715,7 +825,13 @@ __device__ void run_replay(int col, const StepLog* log, volatile int* done, int 
             while ((en.w >> 10) == log_seq(i, par) && (nx.w >> 10) == log_seq(i + 1, par) &&
                    (en.w & KIND) == (LOG_FUSED | LOG_UA | 2u) &&
                    (nx.w & KIND) == (LOG_FUSED | 2u)) {
+#ifdef GCD_TRACE
+                if (col == 0 && lane == 0) g_tb[i] = clock64();
+#endif
                 const uint4 n2 = log_get(lb, min(i + 2, last)), n3 = log_get(lb, min(i + 3, last));
+#ifdef GCD_TRACE
+                if (col == 0 && lane == 0) g_tr[i] = clock64();
+#endif
                 replay_fused2(ra, rb, en, f);
                 replay_fused2(rb, ra, nx, f);
                 const int h1 = max(ha, hb) >= 0 ? max(ha, hb) + 2 : -1;
@@ -731,6 +847,9 @@ __device__ void run_replay(int col, const StepLog* log, volatile int* done, int 
             en = log_get(lb, i);  // spin: warps 1-2 do not share the chain's SMSP
         }
         if ((en.w >> 10) != log_seq(i, par)) break;
+#ifdef GCD_TRACE
+        if (col == 0 && lane == 0) g_tp[i] = clock64();
+#endif
         if (MODE == 0 && (en.w & KIND) == (LOG_FUSED | LOG_UA | 2u) &&
             (nx.w >> 10) != log_seq(i + 1, par)) {
             // a steady A pair whose partner is not yet published: wait for it
@@ -738,9 +857,15 @@ __device__ void run_replay(int col, const StepLog* log, volatile int* done, int 
                 if (ended(i + 1)) break;
                 nx = log_get(lb, min(i + 1, last));
             }
+#ifdef GCD_TRACE
+            if (col == 0 && lane == 0) g_ta[i] = clock64();
+#endif
             if ((nx.w >> 10) == log_seq(i + 1, par) && (nx.w & KIND) == (LOG_FUSED | 2u)) continue;
         }
         const int z = int(en.w & LOG_Z), hmax = max(ha, hb);
+#ifdef GCD_TRACE
+        if (col == 0 && lane == 0) g_tr[i] = clock64();
+#endif
         if (en.w & LOG_UA) {
             replay_entry<MODE>(ra, rb, en, f);
             ha = hmax >= 0 ? hmax + z : -1;
@@ -752,13 +877,16 @@ __device__ void run_replay(int col, const StepLog* log, volatile int* done, int 
         en = (nx.w >> 10) == log_seq(i, par) ? nx : log_get(lb, min(i, last));
         nx = log_get(lb, min(i + 1, last));
     }
-    uint32_t* Pa = Pg + (0 * 2 + col) * PL;  // row A, column col
-    uint32_t* Pb = Pg + (1 * 2 + col) * PL;  // row B, column col
+    if (tex && lane == 0) *tex = clock64();
+    while (ld_acquire_cta(ring_ok) < jb) {
+    }
+    uint64_t* Pa = rec + (0 * 2 + col) * PL;  // row A, column col
+    uint64_t* Pb = rec + (1 * 2 + col) * PL;  // row B, column col
 #pragma unroll
     for (int e = 0; e < PE; ++e) {
         const uint32_t va = A::canon(ra[e], p), vb = A::canon(rb[e], p);
-        __stcg(Pa + e * 32 + lane, va);
-        __stcg(Pb + e * 32 + lane, vb);
+        st_tag(Pa + e * 32 + lane, va, rtag);
+        st_tag(Pb + e * 32 + lane, vb, rtag);
         // the window builder's copy, index-reversed (a correlation run as convolution)
         Ps[(0 * 2 + col) * PL + (PL - 1) - (e * 32 + lane)] = va;
         Ps[(1 * 2 + col) * PL + (PL - 1) - (e * 32 + lane)] = vb;
@@ -772,10 +900,20 @@ __device__ void run_replay(int col, const StepLog* log, volatile int* done, int 
 }  // namespace
 
 // ------------------------------------------------------- flags (gpu scope) --
-__device__ __forceinline__ long long gtimer() {
-    long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
+// Warp-level: min over the bulk CTAs' progress words (all loads in flight).
+constexpr int MAXBULK = 160;
+__device__ __forceinline__ unsigned min_progress(const unsigned* prog, int nbulk) {
+    const int lane = threadIdx.x & 31;
+    unsigned v[MAXBULK / 32];
+#pragma unroll
+    for (int k = 0; k < MAXBULK / 32; ++k)
+        v[k] = lane + 32 * k < nbulk ? ld_relaxed_gpu(prog + lane + 32 * k) : ~0u;
+    unsigned mn = ~0u;
+#pragma unroll
+    for (int k = 0; k < MAXBULK / 32; ++k) mn = min(mn, v[k]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    return mn;
 }
 __device__ __forceinline__ void st_release_gpu(unsigned* p, unsigned v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
@@ -787,12 +925,38 @@ __device__ __forceinline__ void cta_wait_ge(const unsigned* p, unsigned target) 
     __syncthreads();
 }
 
+// Load the top W1 words of tagged state Z below `deg` into w; lower `deg` past
+// zero words until w[0] is the nonzero lead (or deg = -1: zero operand).
+// Warp-uniform.
+template <int MODE>
+__device__ void load_top(uint32_t (&w)[GE], const uint64_t* Z, unsigned tag, long long& deg,
+                         uint32_t p) {
+    const int lane = threadIdx.x & 31;
+    while (deg >= 0) {
+        uint64_t r[GE];
+#pragma unroll
+        for (int e = 0; e < GE; ++e) {
+            const long long x = deg - (e * 32 + lane);
+            r[e] = x >= 0 ? ld_rlx64(Z + x) : (uint64_t(tag) << 32);
+        }
+#pragma unroll
+        for (int e = 0; e < GE; ++e) {
+            const long long x = deg - (e * 32 + lane);
+            w[e] = tag_resolve(Z + (x >= 0 ? x : 0), r[e], tag);
+        }
+        const int z = first_nz<MODE>(w, 0, p);
+        if (z == 0) return;
+        deg -= z < 0 ? W1 : z;
+    }
+}
+
 // Warp-level: top-aligned W1-word window of Z at degree `deg` into smem; lowers
 // `deg` past zero words until win[0] is the lead (deg = -1: zero operand).
 template <int MODE>
-__device__ void window_from_global(uint32_t* win, const uint32_t* Z, long long& deg, uint32_t p) {
+__device__ void window_from_global(uint32_t* win, const uint64_t* Z, unsigned tag, long long& deg,
+                                   uint32_t p) {
     uint32_t w[GE];
-    load_top<MODE>(w, Z, deg, p);
+    load_top<MODE>(w, Z, tag, deg, p);
 #pragma unroll
     for (int e = 0; e < GE; ++e) win[e * 32 + (threadIdx.x & 31)] = w[e];
     __syncwarp();
@@ -809,6 +973,7 @@ __device__ void window_from_global(uint32_t* win, const uint32_t* Z, long long& 
 // bank conflicts), and the parts meet in a shared-memory reduction.
 constexpr int BUILD_PARTS = 4;
 static_assert(2 * (W1 / 4) == 32, "window builder: one (window, quad) per lane");
+static_assert(BUILD_PARTS <= GCD_T / 32 - 1, "window builder: one part per warp (0-6)");
 __device__ void build_window_part(int part, uint32_t* red, const uint32_t* Ps, const int* hi,
                                   const uint32_t* topA, const uint32_t* topB,
                                   const FieldParams& F) {
@@ -851,16 +1016,21 @@ __device__ int head_cta(const GcdArgs& g, BatchMeta& ctl, StepLog* log, uint32_t
     __shared__ int fallback;
     __shared__ long long da0s[2], db0s[2];  // batch start degrees, by batch parity
     __shared__ long long hst[12];  // MMM_GCD_STATS: accumulated here, flushed at the end
-    __shared__ long long tpub_s;
+    __shared__ long long tpub_s, tex_s;
+    __shared__ volatile int ring_ok;  // record slot of batch <= ring_ok is free
+    __shared__ unsigned minprog_s;    // min bulk progress seen this batch
     if (threadIdx.x < 12) hst[threadIdx.x] = 0;
-    if (threadIdx.x == 0) tpub_s = 0;
+    if (threadIdx.x == 0) {
+        tpub_s = 0;
+        ring_ok = -1;
+    }
     if (threadIdx.x == 0) *done = 0;
     for (int i = threadIdx.x; i < LOGCAP; i += GCD_T)  // no stale tags from earlier kernels
         reinterpret_cast<uint4*>(log)[i] = make_uint4(0u, 0u, 0u, 0u);
     if (warp == 0) {
         long long da = g.na - 1, db = g.nb - 1;
-        window_from_global<MODE>(winA, g.XA[0], da, F.p);
-        window_from_global<MODE>(winB, g.XB[0], db, F.p);
+        window_from_global<MODE>(winA, g.XA[0], 1u, da, F.p);
+        window_from_global<MODE>(winB, g.XB[0], 1u, db, F.p);
         if ((threadIdx.x & 31) == 0) {
             ctl.da1 = da;
             ctl.db1 = db;
@@ -876,24 +1046,56 @@ __device__ int head_cta(const GcdArgs& g, BatchMeta& ctl, StepLog* log, uint32_t
             run_chain<MODE>(ctl, log, done, j, g.M, Fld{F.p, F.pinv}, winA, winB);
             if (g.stats && threadIdx.x == 0) hst[4] += clock64() - t0;
         } else if (warp <= 2) {
-            run_replay<MODE>(warp - 1, log, done, j, Fld{F.p, F.pinv},
-                             g.Pg + (j % RING) * 4 * PL, Ps, hi_s);
-            if (g.stats && threadIdx.x == 32) hst[5] += clock64() - t0;
+            // (record slot j % RING is written at the end, once ring_ok says it is free)
+            run_replay<MODE>(warp - 1, log, done, j, Fld{F.p, F.pinv}, g.rec + (j % RING) * REC_W,
+                             unsigned(j + 1), Ps, hi_s, &ring_ok,
+                             (g.stats && warp == 1) ? &tex_s : nullptr);
+            if (g.stats && threadIdx.x == 32) {
+                hst[5] += clock64() - t0;
+                hst[9] += tex_s - t0;
+            }
         } else {
-            // prefetch: S_j complete once the bulk applied batch j-1
-            if (threadIdx.x == 96) {
-                spin_until_geq(g.flags + 1, unsigned(j) * nbulk);
-                if (g.stats && j > 0) {
+            // Warp 3 prefetches S_j's top region: tagged words, each polled until
+            // the bulk CTA that owns it wrote it for batch j - 1.  Only warps 3
+            // and 7 (SMSP 3) work here: a polling warp on SMSPs 0-2 would take
+            // issue slots from the chain (warp 0) or a replay warp (1, 2).
+            if (warp == 3) {
+                const long long da0 = da0s[j & 1], db0 = db0s[j & 1];  // ordered by bar 2
+                const uint64_t* ZA = g.XA[j % NBUF];
+                const uint64_t* ZB = g.XB[j % NBUF];
+                const unsigned tg = unsigned(j + 1);
+                constexpr int K = (W1 + PL) / 32;
+                const int lane = threadIdx.x & 31;
+                const uint64_t* ad[2 * K];
+                uint64_t r[2 * K];
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    const long long xa = da0 - (lane + 32 * k), xb = db0 - (lane + 32 * k);
+                    ad[k] = ZA + (xa >= 0 ? xa : 0);
+                    ad[K + k] = ZB + (xb >= 0 ? xb : 0);
+                    r[k] = xa >= 0 ? ld_rlx64(ad[k]) : uint64_t(tg) << 32;
+                    r[K + k] = xb >= 0 ? ld_rlx64(ad[K + k]) : uint64_t(tg) << 32;
+                }
+                tag_resolve_all<2 * K>(ad, r, tg);
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    topA[lane + 32 * k] = uint32_t(r[k]);
+                    topB[lane + 32 * k] = uint32_t(r[K + k]);
+                }
+                if (g.stats && j > 0 && lane == 0) {
                     hst[10] += gtimer() - tpub_s;
                     hst[11] += 1;
                 }
-            }
-            bar_sync(1, GCD_T - 96);  // warps 3-7 (warp 7 may come from its publish)
-            const long long da0 = da0s[j & 1], db0 = db0s[j & 1];
-            for (int i = threadIdx.x - 96; i < W1 + PL; i += GCD_T - 96) {
-                const long long xa = da0 - i, xb = db0 - i;
-                topA[i] = (xa >= 0) ? __ldcg(g.XA[j % 3] + xa) : 0u;
-                topB[i] = (xb >= 0) ? __ldcg(g.XB[j % 3] + xb) : 0u;
+            } else if (warp == 7) {
+                // record slot j % RING is free once every bulk CTA finished batch
+                // j - RING (the replay's matrix and warp 7's meta wait for this);
+                // the minimum also travels in the record for the bulk's guard
+                unsigned mn = min_progress(g.prog, nbulk);
+                while (j >= RING && mn < unsigned(j - RING + 1)) mn = min_progress(g.prog, nbulk);
+                if ((threadIdx.x & 31) == 0) {
+                    minprog_s = mn;
+                    st_release_cta(&ring_ok, j);
+                }
             }
             if (g.stats && threadIdx.x == 96) hst[6] += clock64() - t0;
         }
@@ -905,19 +1107,26 @@ __device__ int head_cta(const GcdArgs& g, BatchMeta& ctl, StepLog* log, uint32_t
         for (int i = 0; i < 4; ++i) m.hi[i] = hi_s[i];
         m.err = (m.steps == 0 && m.term == 0) ? 1 : 0;
         const bool last = m.term || m.err;
-        if (warp == 7) {  // publish batch j
-            if (threadIdx.x == 224) {
-                if (g.stats) {
-                    m.tpub = gtimer();
-                    tpub_s = m.tpub;
-                }
-                g.meta[j % RING] = m;
-                __threadfence();
-                st_release_gpu(g.flags + 0, unsigned(j + 1));
-                if (g.stats) {
-                    hst[0] += 1;
-                    hst[1] += m.steps;
-                }
+        if (warp == 7) {  // publish batch j: the record's meta words (the replay wrote P)
+            const int l = threadIdx.x - 224;
+            // selects on registers (a runtime index into m would put it in local memory)
+            const int h0 = m.hi[0], h1 = m.hi[1], h2 = m.hi[2], h3 = m.hi[3];
+            int v = l == 0 ? int(m.da0) : l == 1 ? int(m.db0) : l == 2 ? int(m.da1)
+                  : l == 3 ? int(m.db1) : l == 4 ? m.steps : l == 5 ? m.term
+                  : l == 6 ? m.dividend_a : l == 7 ? m.err : l == 8 ? m.sa
+                  : l == 9 ? m.sb : l == 10 ? h0 : l == 11 ? h1 : l == 12 ? h2 : h3;
+            long long tp = g.stats ? gtimer() : 0;
+            tp = __shfl_sync(0xffffffffu, tp, 0);
+            if (l == 14) v = int(uint32_t(tp));
+            if (l == 15) v = int(uint32_t(uint64_t(tp) >> 32));
+            if (l == 16) v = int(minprog_s);
+            if (l < META_W)
+                st_tag(g.rec + (j % RING) * REC_W + 4 * PL + l, uint32_t(v), unsigned(j + 1));
+
+            if (threadIdx.x == 224 && g.stats) {
+                tpub_s = tp;
+                hst[0] += 1;
+                hst[1] += m.steps;
             }
             if (last) {
                 __syncthreads();  // with warps 0-6 (same branch): hst complete
@@ -928,7 +1137,7 @@ __device__ int head_cta(const GcdArgs& g, BatchMeta& ctl, StepLog* log, uint32_t
                 }
                 return j;
             }
-            continue;  // next batch: prefetch group
+            continue;  // next batch
         }
         if (last) {
             __syncthreads();
@@ -954,13 +1163,10 @@ __device__ int head_cta(const GcdArgs& g, BatchMeta& ctl, StepLog* log, uint32_t
             fallback = 1;
         bar_sync(2, BUILDERS);
         if (fallback) {
-            if (threadIdx.x == 0)
-                spin_until_geq(g.flags + 1, unsigned(j + 1) * nbulk);
-            bar_sync(2, BUILDERS);
-            if (warp == 0) {
+            if (warp == 0) {  // tagged reads wait for the bulk's batch j
                 long long da = m.da1, db = m.db1;
-                window_from_global<MODE>(winA, g.XA[(j + 1) % 3], da, F.p);
-                window_from_global<MODE>(winB, g.XB[(j + 1) % 3], db, F.p);
+                window_from_global<MODE>(winA, g.XA[(j + 1) % NBUF], unsigned(j + 2), da, F.p);
+                window_from_global<MODE>(winB, g.XB[(j + 1) % NBUF], unsigned(j + 2), db, F.p);
                 if ((threadIdx.x & 31) == 0) {
                     ctl.da1 = da;
                     ctl.db1 = db;
@@ -969,7 +1175,7 @@ __device__ int head_cta(const GcdArgs& g, BatchMeta& ctl, StepLog* log, uint32_t
             bar_sync(2, BUILDERS);
         }
         if (threadIdx.x == 0) {
-            da0s[(j + 1) & 1] = ctl.da1;  // read by the prefetch after its barrier
+            da0s[(j + 1) & 1] = ctl.da1;  // read by the prefetch after the barrier below
             db0s[(j + 1) & 1] = ctl.db1;
         }
         if (unsigned(j + 1) % TAG_MASK == 0u)  // tag wraps (2^22 batches): clear the log
@@ -999,20 +1205,22 @@ constexpr int APPLY_OUT = GCD_T;  // outputs per pass: one work item per thread
 #endif
 constexpr int APPLY_WORDS = 4 * PL + 2 * (APPLY_OUT + 8) + 4 * (PL + 4);
 
-__device__ void apply_batch(const GcdArgs& g, const BatchMeta& m, const uint32_t* Pglob, int j,
-                            long long s0, long long s1, uint32_t* sm, long long* ph) {
+static_assert(APPLY_OUT + PL + 4 <= 2 * GCD_T, "apply: two staged words per thread and window");
+static_assert(4 * PL == GCD_T, "apply: one matrix word per thread");
+__device__ void apply_batch(const GcdArgs& g, const BatchMeta& m, int j, long long s0, long long s1,
+                            uint32_t* sm, const uint64_t* rec, long long* ph) {
     const long long tb = ph ? clock64() : 0;
     const FieldParams F = g.F;
     const int tid = threadIdx.x;
-    uint32_t* P = sm;  // Pa1, Pa2, Pb1, Pb2
+    uint32_t* P = sm;  // Pa1, Pa2, Pb1, Pb2: the record's matrix, staged with the first pass
     uint32_t* Wb = sm + 4 * PL;
-    const uint32_t* Z[2] = {g.XA[j % 3], g.XB[j % 3]};
+    const uint64_t* Z[2] = {g.XA[j % NBUF], g.XB[j % NBUF]};
+    const unsigned tg = unsigned(j + 1);  // S_j in, S_{j+1} out
     const long long deg[2] = {m.da0, m.db0};
-    uint32_t* out[2] = {g.XA[(j + 1) % 3], g.XB[(j + 1) % 3]};
+    uint64_t* out[2] = {g.XA[(j + 1) % NBUF], g.XB[(j + 1) % NBUF]};
     const long long na1 = m.da1 + 1 > 0 ? m.da1 + 1 : 0;
     // shift of term t for row r: Z_t index = x + sh[2r + t] - e
     const long long sh[4] = {m.sa, m.sa + m.db0 - m.da0, m.sb + m.da0 - m.db0, m.sb};
-    for (int i = tid; i < 4 * PL; i += GCD_T) P[i] = __ldcg(Pglob + i);
     for (long long c0 = s0; c0 < s1; c0 += APPLY_OUT) {
         const long long c1 = min(c0 + APPLY_OUT, s1);
         const long long xs[2] = {min(c0, na1), max(c0 - na1, 0LL)};
@@ -1022,18 +1230,41 @@ __device__ void apply_batch(const GcdArgs& g, const BatchMeta& m, const uint32_t
         uint32_t* W[4] = {Wb, Wb + L[0], Wb + 2 * L[0], Wb + 2 * L[0] + L[1]};
         __syncthreads();  // previous pass done with the windows
         if (ph && c0 == s0) ph[0] += clock64() - tb;
-        // W[2r + t][y] = Z_t[xs_r + sh - (PL - 1) + y], zero outside [0, deg_t]
+        // W[2r + t][y] = Z_t[xs_r + sh - (PL - 1) + y], zero outside [0, deg_t]:
+        // all loads in flight first, then each polled until tagged S_j
+        // (slot 8: this thread's matrix word, first pass only)
+        const uint64_t* ad[9];
+        uint64_t rw[9];
+        unsigned live = 0;
 #pragma unroll
         for (int w = 0; w < 4; ++w) {
             const int r = w >> 1, t = w & 1;
             const long long base = xs[r] + sh[w] - (PL - 1);
-            for (int y = tid; y < L[r]; y += GCD_T) {
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                const int y = tid + k * GCD_T;
                 const long long x = base + y;
-                W[w][y] = (n[r] > 0 && x >= 0 && x <= deg[t]) ? __ldcg(Z[t] + x) : 0u;
+                const bool lv = y < L[r] && n[r] > 0 && x >= 0 && x <= deg[t];
+                ad[2 * w + k] = Z[t] + (lv ? x : 0);
+                rw[2 * w + k] = lv ? ld_rlx64(ad[2 * w + k]) : uint64_t(tg) << 32;
+                live |= lv ? 1u << (2 * w + k) : 0u;
             }
         }
+        ad[8] = rec + tid;
+        rw[8] = c0 == s0 ? ld_rlx64(ad[8]) : uint64_t(tg) << 32;
+        tag_resolve_all<9>(ad, rw, tg);
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+            const int r = w >> 1;
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                const int y = tid + k * GCD_T;
+                if (y < L[r]) W[w][y] = (live >> (2 * w + k)) & 1u ? uint32_t(rw[2 * w + k]) : 0u;
+            }
+        }
+        if (c0 == s0) P[tid] = uint32_t(rw[8]);
         __syncthreads();
-        if (ph && c0 == s0) ph[1] += clock64() - tb;
+
         const int items = 4 * (qn[0] + qn[1]);
         // selects instead of runtime-indexed arrays (those live in local memory)
         const int h00 = m.hi[0], h01 = m.hi[1], h10 = m.hi[2], h11 = m.hi[3];
@@ -1043,8 +1274,8 @@ __device__ void apply_batch(const GcdArgs& g, const BatchMeta& m, const uint32_t
         uint32_t* const W3 = W[3];
         const int n0 = n[0], n1 = n[1], qn0 = qn[0];
         const long long xs0 = xs[0], xs1 = xs[1];
-        uint32_t* const out0 = out[0];
-        uint32_t* const out1 = out[1];
+        uint64_t* const out0 = out[0];
+        uint64_t* const out1 = out[1];
         for (int it0 = 0; it0 < items; it0 += GCD_T) {
             const int item = it0 + tid, q = item >> 2, part = item & 3;
             const int r = q < qn0 ? 0 : 1, qi = q - (r ? qn0 : 0);
@@ -1068,33 +1299,66 @@ __device__ void apply_batch(const GcdArgs& g, const BatchMeta& m, const uint32_t
             const int i = 4 * qi + part;  // part k stores output k of the quad
             if (item < items && i < (r ? n1 : n0)) {
                 const uint32_t o = part == 0 ? v[0] : part == 1 ? v[1] : part == 2 ? v[2] : v[3];
-                __stcg((r ? out1 + xs1 : out0 + xs0) + i, o);
+                st_tag((r ? out1 + xs1 : out0 + xs0) + i, o, tg + 1u);
             }
         }
     }
-    if (ph) ph[2] += clock64() - tb;
 }
 
 // CTAs 1..G-1: apply batch j's matrix to this CTA's slice of both operands,
-// S_{j+1} = P_j(S_j), as soon as it is published and S_j is complete.
+// S_{j+1} = P_j(S_j), as soon as its record is published (every record word
+// polled until tagged j + 1: the matrix lands in shared memory, the meta in
+// ms).  S_j's words are polled the same way inside apply_batch.
 __device__ int bulk_cta(const GcdArgs& g, uint32_t* sm, int nbulk, int me) {
     __shared__ BatchMeta ms;
     long long apply_cycles = 0;  // MMM_GCD_STATS (bulk CTA 0, thread 0)
-    long long ph[3] = {0, 0, 0}, seen_ns = 0;
+    long long ph[3] = {0, 0, 0}, seen_ns = 0, tseen0 = 0, warp_seen_ns = 0, nspin = 0, spin_ns = 0,
+              tsw = 0, done_ns = 0;
+    static_assert(REC_W <= 2 * GCD_T, "record: at most two words per thread");
     for (int j = 0;; ++j) {
-        cta_wait_ge(g.flags + 0, unsigned(j + 1));
-        if (threadIdx.x == 0) {
-            const volatile BatchMeta* vm = g.meta + (j % RING);
-            ms.da0 = vm->da0; ms.db0 = vm->db0; ms.da1 = vm->da1; ms.db1 = vm->db1;
-            ms.steps = vm->steps; ms.term = vm->term; ms.err = vm->err;
-            ms.sa = vm->sa; ms.sb = vm->sb;
-            for (int i = 0; i < 4; ++i) ms.hi[i] = vm->hi[i];
-            if (g.stats) seen_ns += gtimer() - vm->tpub;
+        const uint64_t* rec = g.rec + (j % RING) * REC_W;
+        const unsigned tg = unsigned(j + 1);
+        // state buffer (j+1) % NBUF is free once every bulk CTA finished batch
+        // j + 1 - NBUF (the head read S_{j+1-NBUF} before publishing that batch)
+        // (normally the head's minimum in the record says so already)
+        const unsigned need = j + 2 - NBUF > 0 ? unsigned(j + 2 - NBUF) : 0u;
+        // the meta words (one cache line), polled by warp 0 alone: 147 CTAs
+        // polling the whole record would queue the head's stores behind them
+        const long long tpoll = (g.stats && me == 0) ? gtimer() : 0;
+        if (threadIdx.x < 32) {
+            const int l = threadIdx.x;
+            const uint64_t* mp = rec + 4 * PL + (l < META_W ? l : 0);
+            uint64_t w = ld_rlx64(mp);
+            while (!__all_sync(0xffffffffu, unsigned(w >> 32) == tg)) {
+                if (g.dbg & 2) __nanosleep(256);
+                w = ld_rlx64(mp);
+            }
+            if (g.stats && me == 0 && l == 0) tseen0 = gtimer();
+            static_assert(sizeof(BatchMeta) == META_W * sizeof(int), "meta words = BatchMeta");
+            if (l < META_W) reinterpret_cast<int*>(&ms)[l] = int(uint32_t(w));
+            __syncwarp();
+            if (g.stats && me == 0 && l == 0) tsw = gtimer();
         }
-        // S_j is complete without a poll: CTA 0 acquired flags[1] >= j * nbulk
-        // (its prefetch) before the bar.sync preceding this batch's release of
-        // flags[0], and no bulk CTA can finish batch j before that release.
-        __syncthreads();  // ms
+        __syncthreads();  // the meta (the matrix words are read with S_j in apply_batch)
+        long long tg0 = (g.stats && me == 0 && threadIdx.x == 0) ? gtimer() : 0;
+        if (ms.minprog < need) {  // uniform; rare
+            if (threadIdx.x < 32)
+                while (min_progress(g.prog, nbulk) < need) {
+                }
+            __syncthreads();
+            if (g.stats && me == 0) nspin += 1;
+        }
+        if (g.stats && me == 0 && threadIdx.x == 0) ph[2] += gtimer() - tg0;
+        const long long mtp = (long long)(((unsigned long long)(unsigned)ms.tpub_hi << 32) |
+                                          (unsigned)ms.tpub_lo);
+        if (g.stats && me == 0 && threadIdx.x == 0) {
+            const long long now = gtimer();
+            seen_ns += now - mtp;
+            warp_seen_ns += tseen0 - mtp;
+            spin_ns += tsw - tseen0;
+            ph[1] += now - (tpoll > mtp ? tpoll : mtp);  // poll latency once published
+        }
+        if (g.stats && me == nbulk - 1 && threadIdx.x == 0) seen_ns += gtimer() - mtp;
         const long long tb = clock64();
         const BatchMeta& m = ms;  // shared: runtime-indexed fields stay out of local memory
         if (m.steps > 0 && !m.err) {
@@ -1103,24 +1367,33 @@ __device__ int bulk_cta(const GcdArgs& g, uint32_t* sm, int nbulk, int me) {
             const long long per = (na1 + nb1 + nbulk - 1) / nbulk;
             const long long s0 = min((long long)me * per, na1 + nb1);
             const long long s1 = min(s0 + per, na1 + nb1);
-            apply_batch(g, m, g.Pg + (j % RING) * 4 * PL, j, s0, s1, sm,
-                        (g.stats && me == 0 && threadIdx.x == 0) ? ph : nullptr);
+            apply_batch(g, m, j, s0, s1, sm, rec, (g.stats && me == 0 && threadIdx.x == 0) ? ph : nullptr);
         }
-        __syncthreads();
+        const bool last = m.term || m.err;
+        __syncthreads();  // sm and ms reused by the next batch
         if (threadIdx.x == 0) {
-            __threadfence();
-            atomicAdd(g.flags + 1, 1u);
+            // finished reading S_j and record j (the ring guards).  No release:
+            // those reads are complete (their values were consumed before the
+            // barrier above), and a fence costs ~1 us on this part.
+            asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(g.prog + me), "r"(unsigned(j + 1))
+                         : "memory");
             apply_cycles += clock64() - tb;
+            if (g.stats && me == nbulk - 1) done_ns += gtimer() - mtp;
         }
-        if (m.term || m.err) {
+        if (last) {
             if (g.stats && me == 0 && threadIdx.x == 0) {
                 g.stats[7] = apply_cycles;
                 g.stats[12] = seen_ns;
-                g.stats[13] = ph[0];
-                g.stats[14] = ph[1];
+                g.stats[16] = nspin;
+                g.stats[14] = spin_ns;
+                g.stats[13] = warp_seen_ns;
+                g.stats[14] = spin_ns;
                 g.stats[15] = ph[2];
             }
-            if (g.stats && me == nbulk - 1 && threadIdx.x == 0) g.stats[18] = seen_ns;
+            if (g.stats && me == nbulk - 1 && threadIdx.x == 0) {
+                g.stats[18] = seen_ns;
+                g.stats[20] = done_ns;
+            }
             return j;
         }
     }
@@ -1140,18 +1413,27 @@ __global__ void __launch_bounds__(GCD_T, 1) gcd_kernel(GcdArgs g) {
     StepLog* log = reinterpret_cast<StepLog*>(smem);
     uint32_t* rest = smem + 4 * LOGCAP;
 
-    for (long long i = tid; i < g.na; i += nth) g.XA[0][i] = g.a[i];
-    for (long long i = tid; i < g.nb; i += nth) g.XB[0][i] = g.b[i];
+    // S_0 tagged 1; every other state word and record word untagged (0), so
+    // no tag left by an earlier call can be mistaken for this one's
+    for (long long i = tid; i < g.cap; i += nth) {
+        g.XA[0][i] = i < g.na ? (uint64_t(1) << 32) | g.a[i] : 0ull;
+        g.XB[0][i] = i < g.nb ? (uint64_t(1) << 32) | g.b[i] : 0ull;
+#pragma unroll
+        for (int r = 1; r < NBUF; ++r) g.XA[r][i] = g.XB[r][i] = 0ull;
+    }
+    for (long long i = tid; i < RING * REC_W; i += nth) g.rec[i] = 0ull;
     grid.sync();
 
     const int J = blockIdx.x == 0 ? head_cta<MODE>(g, ctl, log, rest, &done, hi_s, nbulk)
                                   : bulk_cta(g, rest, nbulk, blockIdx.x - 1);
-    // every CTA: wait until the final batch is applied everywhere, then finish
-    cta_wait_ge(g.flags + 1, unsigned(J + 1) * nbulk);
-    if (threadIdx.x == 0) {
-        const volatile BatchMeta* vm = g.meta + (J % RING);
-        fin.da1 = vm->da1; fin.db1 = vm->db1; fin.steps = vm->steps; fin.term = vm->term;
-        fin.err = vm->err;
+    // every CTA: the final record, then the final state (tagged reads wait for it)
+    if (threadIdx.x < 8) {
+        const int v = int(ld_tag(g.rec + (J % RING) * REC_W + 4 * PL + threadIdx.x, unsigned(J + 1)));
+        if (threadIdx.x == 2) fin.da1 = v;
+        if (threadIdx.x == 3) fin.db1 = v;
+        if (threadIdx.x == 4) fin.steps = v;
+        if (threadIdx.x == 5) fin.term = v;
+        if (threadIdx.x == 7) fin.err = v;
     }
     __syncthreads();
     if (fin.err) {
@@ -1165,11 +1447,12 @@ __global__ void __launch_bounds__(GCD_T, 1) gcd_kernel(GcdArgs g) {
         }
         return;
     }
-    const int buf = fin.steps > 0 ? (J + 1) % 3 : J % 3;
-    const uint32_t* Z = fin.term == 1 ? g.XB[buf] : g.XA[buf];
+    const int buf = fin.steps > 0 ? (J + 1) % NBUF : J % NBUF;
+    const unsigned tg = fin.steps > 0 ? unsigned(J + 2) : unsigned(J + 1);
+    const uint64_t* Z = fin.term == 1 ? g.XB[buf] : g.XA[buf];
     const long long dz = fin.term == 1 ? fin.db1 : fin.da1;
-    const uint32_t inv = invmod(__ldcg(Z + dz), F);
-    for (long long i = tid; i <= dz; i += nth) g.g[i] = mulmod(__ldcg(Z + i), inv, F);
+    const uint32_t inv = invmod(ld_tag(Z + dz, tg), F);
+    for (long long i = tid; i <= dz; i += nth) g.g[i] = mulmod(ld_tag(Z + i, tg), inv, F);
     if (tid == 0) *g.ng = dz + 1;
 }
 
@@ -1187,15 +1470,14 @@ void launch_gcd(const FieldParams& F, const uint32_t* a, int64_t na, const uint3
     g.M = int(std::min<int64_t>(s, LOGCAP));
     const int64_t cap = std::max<int64_t>(std::max(na, nb), 1);
     Scratch sc(st);
-    for (int i = 0; i < 3; ++i) {
-        g.XA[i] = sc.get<uint32_t>(size_t(cap));
-        g.XB[i] = sc.get<uint32_t>(size_t(cap));
+    for (int i = 0; i < NBUF; ++i) {
+        g.XA[i] = sc.get<uint64_t>(size_t(cap));
+        g.XB[i] = sc.get<uint64_t>(size_t(cap));
     }
-    g.Pg = sc.get<uint32_t>(size_t(RING) * 4 * PL);
-    g.meta = reinterpret_cast<BatchMeta*>(
-        sc.get<uint64_t>(RING * ((sizeof(BatchMeta) + 7) / 8)));
-    g.flags = sc.get<unsigned>(2);
-    MMM_CUDA(cudaMemsetAsync(g.flags, 0, 2 * sizeof(unsigned), st));
+    g.cap = cap;
+    g.rec = sc.get<uint64_t>(size_t(RING) * REC_W);
+    g.prog = sc.get<unsigned>(MAXBULK);
+    MMM_CUDA(cudaMemsetAsync(g.prog, 0, MAXBULK * sizeof(unsigned), st));
     const size_t head_words = 2 * W1 + 2 * (W1 + PL) + 4 * PL + BUILD_PARTS * 2 * W1;
     const size_t bulk_words = APPLY_WORDS;
     const size_t bytes = (4 * LOGCAP + std::max(head_words, bulk_words)) * 4;
@@ -1208,7 +1490,7 @@ void launch_gcd(const FieldParams& F, const uint32_t* a, int64_t na, const uint3
     if (per_sm < 1) throw Error(ST_INVALID, "gcd: kernel does not fit an SM");
     const int64_t want = std::max<int64_t>(2, 1 + ceil_div(na + nb, GCD_OUT_PER_CTA));
     // one CTA per SM: a second CTA on the head's SM would take issue slots from the chain
-    const int blocks = int(std::min<int64_t>(want, int64_t(sm_count())));
+    const int blocks = int(std::min<int64_t>(std::min<int64_t>(want, int64_t(sm_count())), MAXBULK + 1));
     const bool want_stats = getenv("MMM_GCD_STATS") != nullptr;
     if (const char* d = getenv("MMM_GCD_DEBUG")) g.dbg = atoi(d);
     if (want_stats) {
@@ -1229,9 +1511,9 @@ void launch_gcd(const FieldParams& F, const uint32_t* a, int64_t na, const uint3
                 "builders_synced=%lld\n",
                 blocks, h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7], h[8], h[9]);
         fprintf(stderr,
-                "gcd latency: bulk0_seen_ns=%lld bulk0_P_cyc=%lld bulk0_win_cyc=%lld "
-                "bulk0_comp_cyc=%lld head_prefetch_seen_ns=%lld (%lld) bulkLast_seen_ns=%lld\n",
-                h[12], h[13], h[14], h[15], h[17], h[19], h[18]);
+                "gcd latency: bulk0_seen_ns=%lld bulk0_warp_seen_ns=%lld bulk0_switch_ns=%lld "
+                "bulk0_barrier_ns=%lld spins=%lld head_prefetch_seen_ns=%lld (%lld) bulkLast_seen_ns=%lld replay_loop_exit_cyc=%lld bulkLast_done_ns=%lld\n",
+                h[12], h[13], h[14], h[15], h[16], h[17], h[19], h[18], h[10], h[20]);
     }
 }
 
