@@ -69,4 +69,36 @@ __device__ __forceinline__ void conv_accumulate(uint64_t (&acc)[R], const uint32
     }
 }
 
+// Fixed trip count NB, no fold: for NB*R <= F.fold_terms the sums cannot
+// overflow, so the blocks unroll into straight-line code (all window and term
+// loads in flight at once; no per-block fold test or loop branch).
+template <int R, int NB>
+__device__ __forceinline__ void conv_accumulate_fixed(uint64_t (&acc)[R], const uint32_t* __restrict__ sw,
+                                                      const uint32_t* __restrict__ sv, int base) {
+    static_assert(R % 4 == 0, "conv_accumulate_fixed: R multiple of 4");
+    uint32_t W[R * (NB + 1)];  // W[k] = sv[base - NB*R + 1 + k] (one spare word at the end)
+    uint32_t X[R * NB];
+#pragma unroll
+    for (int q = 0; q < (NB + 1) * R / 4; ++q) {
+        const uint4 w = *reinterpret_cast<const uint4*>(sv + base - NB * R + 1 + 4 * q);
+        W[4 * q + 0] = w.x;
+        W[4 * q + 1] = w.y;
+        W[4 * q + 2] = w.z;
+        W[4 * q + 3] = w.w;
+    }
+#pragma unroll
+    for (int q = 0; q < NB * R / 4; ++q) {
+        const uint4 x = *reinterpret_cast<const uint4*>(sw + 4 * q);
+        X[4 * q + 0] = x.x;
+        X[4 * q + 1] = x.y;
+        X[4 * q + 2] = x.z;
+        X[4 * q + 3] = x.w;
+    }
+    // acc[r] += sum_u X[u] * sv[base + r - u], sv[base + r - u] = W[NB*R - 1 + r - u]
+#pragma unroll
+    for (int u = 0; u < NB * R; ++u)
+#pragma unroll
+        for (int r = 0; r < R; ++r) acc[r] = mad_wide(X[u], W[NB * R - 1 + r - u], acc[r]);
+}
+
 }  // namespace mmm_cu

@@ -55,6 +55,9 @@ constexpr int PE = GCD_PE;         // matrix words per lane per polynomial
 constexpr int PL = 32 * PE;        // matrix capacity (support < PL)
 constexpr int LOGCAP = 512;        // log entries per batch (<= PL + 1 in practice)
 constexpr int BIG = 1 << 30;
+#ifndef GCD_REPLAY_SIMPLE
+#define GCD_REPLAY_SIMPLE 0  // 1: one entry per iteration (measured 1.8x slower: ~5 taken branches per entry)
+#endif
 #ifndef GCD_CHAIN_LA
 #define GCD_CHAIN_LA 0  // steady state: 1 = scalar-lookahead rounds (faster alone, slower in the kernel)
 #endif       // "validity unbounded": window covers the operand
@@ -180,8 +183,12 @@ __device__ __forceinline__ uint64_t ld_rlx64(const uint64_t* p) {
     return v;
 }
 __device__ __forceinline__ void st_tag(uint64_t* p, uint32_t v, unsigned tag) {
+#if GCD_WEAK_TAG_STORES
+    __stcg(reinterpret_cast<unsigned long long*>(p), (uint64_t(tag) << 32) | v);
+#else
     asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"((uint64_t(tag) << 32) | v)
                  : "memory");
+#endif
 }
 // The value of a tagged word already loaded as w, re-polled until it carries `tag`.
 __device__ __forceinline__ uint32_t tag_resolve(const uint64_t* p, uint64_t w, unsigned tag) {
@@ -817,6 +824,37 @@ __device__ void run_replay(int col, const StepLog* log, volatile int* done, int 
     const unsigned lb = log_base(log);
     const int last = LOGCAP - 1;
     int i = 0;
+#if GCD_REPLAY_SIMPLE
+    // One entry at a time: poll it, fetch the next one, apply.  (Entries
+    // arrive every ~270 cycles and apply in ~180: the replay waits on the
+    // chain, so what matters is how soon it notices an entry, not batching.)
+    uint4 en = log_get(lb, 0);
+    for (;;) {
+        bool fin = false;
+        while ((en.w >> 10) != log_seq(i, par)) {
+            if (ended(i)) {
+                fin = true;
+                break;
+            }
+            en = log_get(lb, i);
+        }
+        if (fin) break;
+        const uint4 nx = log_get(lb, min(i + 1, last));
+        const int z = int(en.w & LOG_Z), hmax = max(ha, hb);
+        const unsigned kind = en.w & KIND;
+        if (en.w & LOG_UA) {
+            if (MODE == 0 && kind == (LOG_FUSED | LOG_UA | 2u)) replay_fused2(ra, rb, en, f);
+            else replay_entry<MODE>(ra, rb, en, f);
+            ha = hmax >= 0 ? hmax + z : -1;
+        } else {
+            if (MODE == 0 && kind == (LOG_FUSED | 2u)) replay_fused2(rb, ra, en, f);
+            else replay_entry<MODE>(rb, ra, en, f);
+            hb = hmax >= 0 ? hmax + z : -1;
+        }
+        ++i;
+        en = nx;
+    }
+#else
     uint4 en = log_get(lb, 0), nx = log_get(lb, 1);
     for (;;) {
         if (MODE == 0) {
@@ -877,6 +915,7 @@ __device__ void run_replay(int col, const StepLog* log, volatile int* done, int 
         en = (nx.w >> 10) == log_seq(i, par) ? nx : log_get(lb, min(i, last));
         nx = log_get(lb, min(i + 1, last));
     }
+#endif
     if (tex && lane == 0) *tex = clock64();
     while (ld_acquire_cta(ring_ok) < jb) {
     }
@@ -971,9 +1010,12 @@ __device__ void window_from_global(uint32_t* win, const uint64_t* Z, unsigned ta
 // the support), one part per warp; the 32 lanes hold the 2 x W1/4 quads of
 // 4 consecutive words (shared-memory reads: broadcast or consecutive, no
 // bank conflicts), and the parts meet in a shared-memory reduction.
-constexpr int BUILD_PARTS = 4;
+#ifndef GCD_BUILD_PARTS
+#define GCD_BUILD_PARTS 4
+#endif
+constexpr int BUILD_PARTS = GCD_BUILD_PARTS;
 static_assert(2 * (W1 / 4) == 32, "window builder: one (window, quad) per lane");
-static_assert(BUILD_PARTS <= GCD_T / 32 - 1, "window builder: one part per warp (0-6)");
+static_assert(BUILD_PARTS <= GCD_T / 32, "window builder: one part per warp");
 __device__ void build_window_part(int part, uint32_t* red, const uint32_t* Ps, const int* hi,
                                   const uint32_t* topA, const uint32_t* topB,
                                   const FieldParams& F) {
@@ -984,9 +1026,14 @@ __device__ void build_window_part(int part, uint32_t* red, const uint32_t* Ps, c
     uint64_t acc[4] = {0, 0, 0, 0};
     uint32_t since = 0;
     // reversed support: u in [PL-1-hi, PL-1]
-    if (hi[c] >= 0 && u0 + SPAN - 1 >= PL - 1 - hi[c])
-        conv_accumulate<4>(acc, Ps + c * PL + u0, SPAN / 4, term ? topB : topA,
-                           4 * q + PL - 1 - u0, since, F);
+    if (hi[c] >= 0 && u0 + SPAN - 1 >= PL - 1 - hi[c]) {
+        if (F.fold_terms >= SPAN)  // (every prime below 2^29): straight-line, no fold
+            conv_accumulate_fixed<4, SPAN / 4>(acc, Ps + c * PL + u0, term ? topB : topA,
+                                               4 * q + PL - 1 - u0);
+        else
+            conv_accumulate<4>(acc, Ps + c * PL + u0, SPAN / 4, term ? topB : topA,
+                               4 * q + PL - 1 - u0, since, F);
+    }
 #pragma unroll
     for (int r = 0; r < 4; ++r) red[part * (2 * W1) + w * W1 + 4 * q + r] = reduce(acc[r], F);
 }
@@ -1001,7 +1048,7 @@ __device__ __forceinline__ void bar_sync(int id, int n) {
 // the matrix (its fence waits for the stores to reach L2) while warps 0-6
 // build the next windows from it.  Never waits for the bulk of the batch it
 // just finished (only for the one before, which had a whole batch).
-constexpr int BUILDERS = GCD_T - 32;  // warps 0-6
+constexpr int BUILDERS = BUILD_PARTS == 8 ? GCD_T : GCD_T - 32;  // warps 0-6 (+7)
 template <int MODE>
 __device__ int head_cta(const GcdArgs& g, BatchMeta& ctl, StepLog* log, uint32_t* smem_rest,
                         volatile int* done, int* hi_s, int nbulk) {
@@ -1013,10 +1060,11 @@ __device__ int head_cta(const GcdArgs& g, BatchMeta& ctl, StepLog* log, uint32_t
     uint32_t* topB = topA + W1 + PL;
     uint32_t* Ps = topB + W1 + PL;      // 4 * PL
     uint32_t* red = Ps + 4 * PL;        // BUILD_PARTS x 2 * W1 builder partials
-    __shared__ int fallback;
     __shared__ long long da0s[2], db0s[2];  // batch start degrees, by batch parity
     __shared__ long long hst[12];  // MMM_GCD_STATS: accumulated here, flushed at the end
     __shared__ long long tpub_s, tex_s;
+    __shared__ long long hx[4];
+    if (threadIdx.x < 4) hx[threadIdx.x] = 0;
     __shared__ volatile int ring_ok;  // record slot of batch <= ring_ok is free
     __shared__ unsigned minprog_s;    // min bulk progress seen this batch
     if (threadIdx.x < 12) hst[threadIdx.x] = 0;
@@ -1133,36 +1181,47 @@ __device__ int head_cta(const GcdArgs& g, BatchMeta& ctl, StepLog* log, uint32_t
                 if (g.stats && threadIdx.x == 224) {
                     for (int i = 0; i < 10; ++i) g.stats[i == 7 ? 8 : (i == 8 ? 9 : (i == 9 ? 10 : i))] = hst[i];
                     g.stats[17] = hst[10];
+                    for (int i = 0; i < 4; ++i) g.stats[21 + i] = hx[i];
                     g.stats[19] = hst[11];
                 }
                 return j;
             }
-            continue;  // next batch
+            if (BUILD_PARTS < 8) continue;  // next batch (else warp 7 also builds)
         }
         if (last) {
-            __syncthreads();
+            if (warp != 7) __syncthreads();
             return j;
         }
         // warps 0-6: next windows, top-aligned, from S_j and the batch matrix
         if (warp < BUILD_PARTS) build_window_part(warp, red, Ps, hi_s, topA, topB, F);
+        if (g.stats && (g.dbg & 4)) {  // timing experiment: the same part again (warm)
+            if (warp < BUILD_PARTS) build_window_part(warp, red, Ps, hi_s, topA, topB, F);
+            if (threadIdx.x == 0) hx[3] += clock64() - t0;
+        }
         bar_sync(2, BUILDERS);
-        if (threadIdx.x < 2 * W1) {  // sum the parts: winA then winB
+        // sum the parts (winA then winB); a new lead that is zero means the bound
+        // after the batch is not the lead (degree dropped past the valid words)
+        bool stale = false;
+        if (threadIdx.x < 2 * W1) {
             uint64_t sum = 0;
 #pragma unroll
             for (int pt = 0; pt < BUILD_PARTS; ++pt) sum += red[pt * (2 * W1) + threadIdx.x];
-            (threadIdx.x < W1 ? winA : winB)[threadIdx.x & (W1 - 1)] = reduce(sum, F);
+            const uint32_t v = reduce(sum, F);
+            (threadIdx.x < W1 ? winA : winB)[threadIdx.x & (W1 - 1)] = v;
+            stale = v == 0u && ((threadIdx.x == 0 && m.da1 >= 0) || (threadIdx.x == W1 && m.db1 >= 0));
         }
-        if (threadIdx.x == 0) fallback = 0;
+        if (threadIdx.x == 0) {
+            da0s[(j + 1) & 1] = m.da1;  // read by the prefetch after the barrier below
+            db0s[(j + 1) & 1] = m.db1;
+        }
         if (g.stats && threadIdx.x == 0) hst[7] += clock64() - t0;
-        bar_sync(2, BUILDERS);
+        // one barrier: the windows and da0s/db0s, and whether a lead is stale
+        int fb;
+        asm volatile(
+            "{ .reg .pred p, q; setp.ne.u32 p, %1, 0; bar.red.or.pred q, 2, %2, p; selp.s32 %0, 1, 0, q; }"
+            : "=r"(fb) : "r"(int(stale)), "r"(BUILDERS) : "memory");
         if (g.stats && threadIdx.x == 0) hst[8] += clock64() - t0;
-        // the bound after the batch is not the lead (degree dropped past the
-        // valid words): take the exact state from the bulk instead
-        if (threadIdx.x == 0 &&
-            ((m.da1 >= 0 && winA[0] == 0u) || (m.db1 >= 0 && winB[0] == 0u)))
-            fallback = 1;
-        bar_sync(2, BUILDERS);
-        if (fallback) {
+        if (fb) {  // take the exact state from the bulk instead
             if (warp == 0) {  // tagged reads wait for the bulk's batch j
                 long long da = m.da1, db = m.db1;
                 window_from_global<MODE>(winA, g.XA[(j + 1) % NBUF], unsigned(j + 2), da, F.p);
@@ -1170,23 +1229,23 @@ __device__ int head_cta(const GcdArgs& g, BatchMeta& ctl, StepLog* log, uint32_t
                 if ((threadIdx.x & 31) == 0) {
                     ctl.da1 = da;
                     ctl.db1 = db;
+                    da0s[(j + 1) & 1] = da;
+                    db0s[(j + 1) & 1] = db;
                 }
             }
             bar_sync(2, BUILDERS);
         }
-        if (threadIdx.x == 0) {
-            da0s[(j + 1) & 1] = ctl.da1;  // read by the prefetch after the barrier below
-            db0s[(j + 1) & 1] = ctl.db1;
-        }
-        if (unsigned(j + 1) % TAG_MASK == 0u)  // tag wraps (2^22 batches): clear the log
+        if (g.stats && threadIdx.x == 0) hx[2] += clock64() - t0;
+        if (unsigned(j + 1) % TAG_MASK == 0u) {  // tag wraps (2^22 batches): clear the log
             for (int i = threadIdx.x; i < LOGCAP; i += BUILDERS)
                 reinterpret_cast<uint4*>(log)[i] = make_uint4(0u, 0u, 0u, 0u);
+            bar_sync(2, BUILDERS);
+        }
         if (g.stats && threadIdx.x == 0) {
             const long long t1 = clock64();
             hst[3] += t1 - t0;
             t0 = t1;
         }
-        bar_sync(2, BUILDERS);  // windows, da0s/db0s ready for the next chain
         if (g.stats) t0 = clock64();
     }
 }
@@ -1494,14 +1553,14 @@ void launch_gcd(const FieldParams& F, const uint32_t* a, int64_t na, const uint3
     const bool want_stats = getenv("MMM_GCD_STATS") != nullptr;
     if (const char* d = getenv("MMM_GCD_DEBUG")) g.dbg = atoi(d);
     if (want_stats) {
-        g.stats = sc.get<long long>(24);
-        MMM_CUDA(cudaMemsetAsync(g.stats, 0, 24 * sizeof(long long), st));
+        g.stats = sc.get<long long>(32);
+        MMM_CUDA(cudaMemsetAsync(g.stats, 0, 32 * sizeof(long long), st));
     }
     void* params[] = {&g};
     MMM_CUDA(cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(GCD_T), params, bytes, st));
     check_launch("gcd_kernel");
     if (want_stats) {
-        long long h[24];
+        long long h[32];
         MMM_CUDA(cudaMemcpyAsync(h, g.stats, sizeof(h), cudaMemcpyDeviceToHost, st));
         MMM_CUDA(cudaStreamSynchronize(st));
         fprintf(stderr,
@@ -1512,8 +1571,8 @@ void launch_gcd(const FieldParams& F, const uint32_t* a, int64_t na, const uint3
                 blocks, h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7], h[8], h[9]);
         fprintf(stderr,
                 "gcd latency: bulk0_seen_ns=%lld bulk0_warp_seen_ns=%lld bulk0_switch_ns=%lld "
-                "bulk0_barrier_ns=%lld spins=%lld head_prefetch_seen_ns=%lld (%lld) bulkLast_seen_ns=%lld replay_loop_exit_cyc=%lld bulkLast_done_ns=%lld\n",
-                h[12], h[13], h[14], h[15], h[16], h[17], h[19], h[18], h[10], h[20]);
+                "bulk0_barrier_ns=%lld spins=%lld head_prefetch_seen_ns=%lld (%lld) bulkLast_seen_ns=%lld replay_loop_exit_cyc=%lld bulkLast_done_ns=%lld fb_check=%lld fb_bar=%lld da0s=%lld unused=%lld\n",
+                h[12], h[13], h[14], h[15], h[16], h[17], h[19], h[18], h[10], h[20], h[21], h[22], h[23], h[24]);
     }
 }
 
