@@ -56,7 +56,7 @@ constexpr int PL = 32 * PE;        // matrix capacity (support < PL)
 constexpr int LOGCAP = 512;        // log entries per batch (<= PL + 1 in practice)
 constexpr int BIG = 1 << 30;
 #ifndef GCD_REPLAY_SIMPLE
-#define GCD_REPLAY_SIMPLE 0  // 1: one entry per iteration (measured 1.8x slower: ~5 taken branches per entry)
+#define GCD_REPLAY_SIMPLE 0  // 0: pair loop + prefetch; 2: one poll loop per pair (5 % slower in the kernel); 1: one entry per iteration (1.8x slower replay)
 #endif
 #ifndef GCD_CHAIN_LA
 #define GCD_CHAIN_LA 0  // steady state: 1 = scalar-lookahead rounds (faster alone, slower in the kernel)
@@ -824,7 +824,44 @@ __device__ void run_replay(int col, const StepLog* log, volatile int* done, int 
     const unsigned lb = log_base(log);
     const int last = LOGCAP - 1;
     int i = 0;
-#if GCD_REPLAY_SIMPLE
+#if GCD_REPLAY_SIMPLE == 2
+    // One poll loop for the next pair (A then B entry, the steady state) with
+    // the chain's end: the common path falls through (taken branches cost
+    // tens of cycles here), and an ended chain leaves a single entry or none.
+    for (;;) {
+        uint4 en = log_get(lb, i), nx = log_get(lb, min(i + 1, last));
+        unsigned d;
+        for (;;) {
+            asm volatile("ld.volatile.shared::cta.u32 %0, [%1];" : "=r"(d) : "r"(done_sa));
+            const bool h0 = (en.w >> 10) == par, h1 = (nx.w >> 10) == par;
+            const int cnt = (d >> 10) == par ? int(d & 0x3FFu) - 1 : 1 << 20;  // entries, once ended
+            if ((h0 && h1) || (h0 && cnt <= i + 1) || cnt <= i) break;
+            en = log_get(lb, i);
+            nx = log_get(lb, min(i + 1, last));
+        }
+        const bool h0 = (en.w >> 10) == par, h1 = (nx.w >> 10) == par;
+        if (!h0) break;  // the chain ended before entry i
+        if (MODE == 0 && h1 && (en.w & KIND) == (LOG_FUSED | LOG_UA | 2u) &&
+            (nx.w & KIND) == (LOG_FUSED | 2u)) {
+            replay_fused2(ra, rb, en, f);
+            replay_fused2(rb, ra, nx, f);
+            const int h1s = max(ha, hb) >= 0 ? max(ha, hb) + 2 : -1;
+            ha = h1s;
+            hb = h1s >= 0 ? max(h1s, hb) + 2 : -1;
+            i += 2;
+            continue;
+        }
+        const int z = int(en.w & LOG_Z), hmax = max(ha, hb);
+        if (en.w & LOG_UA) {
+            replay_entry<MODE>(ra, rb, en, f);
+            ha = hmax >= 0 ? hmax + z : -1;
+        } else {
+            replay_entry<MODE>(rb, ra, en, f);
+            hb = hmax >= 0 ? hmax + z : -1;
+        }
+        ++i;
+    }
+#elif GCD_REPLAY_SIMPLE
     // One entry at a time: poll it, fetch the next one, apply.  (Entries
     // arrive every ~270 cycles and apply in ~180: the replay waits on the
     // chain, so what matters is how soon it notices an entry, not batching.)
