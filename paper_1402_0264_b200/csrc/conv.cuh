@@ -71,21 +71,24 @@ __device__ __forceinline__ void conv_accumulate(uint64_t (&acc)[R], const uint32
 
 // Fixed trip count NB, no fold: for NB*R <= F.fold_terms the sums cannot
 // overflow, so the blocks unroll into straight-line code (all window and term
-// loads in flight at once; no per-block fold test or loop branch).
+// loads in flight at once; no per-block fold test or loop branch).  Reads the
+// same words as conv_accumulate (sv[base - NB*R + 1 .. base + R - 1]).
 template <int R, int NB>
 __device__ __forceinline__ void conv_accumulate_fixed(uint64_t (&acc)[R], const uint32_t* __restrict__ sw,
                                                       const uint32_t* __restrict__ sv, int base) {
     static_assert(R % 4 == 0, "conv_accumulate_fixed: R multiple of 4");
-    uint32_t W[R * (NB + 1)];  // W[k] = sv[base - NB*R + 1 + k] (one spare word at the end)
+    uint32_t W[R * NB + R - 1];  // W[k] = sv[base - NB*R + 1 + k]
     uint32_t X[R * NB];
 #pragma unroll
-    for (int q = 0; q < (NB + 1) * R / 4; ++q) {
+    for (int q = 0; q < NB * R / 4; ++q) {
         const uint4 w = *reinterpret_cast<const uint4*>(sv + base - NB * R + 1 + 4 * q);
         W[4 * q + 0] = w.x;
         W[4 * q + 1] = w.y;
         W[4 * q + 2] = w.z;
         W[4 * q + 3] = w.w;
     }
+#pragma unroll
+    for (int j = 0; j < R - 1; ++j) W[NB * R + j] = sv[base + 1 + j];
 #pragma unroll
     for (int q = 0; q < NB * R / 4; ++q) {
         const uint4 x = *reinterpret_cast<const uint4*>(sw + 4 * q);
@@ -99,6 +102,25 @@ __device__ __forceinline__ void conv_accumulate_fixed(uint64_t (&acc)[R], const 
     for (int u = 0; u < NB * R; ++u)
 #pragma unroll
         for (int r = 0; r < R; ++r) acc[r] = mad_wide(X[u], W[NB * R - 1 + r - u], acc[r]);
+}
+
+// conv_accumulate<4> with straight-line code for the common block counts
+// (1, 2, 4, 8) when the terms fit before the next fold.
+__device__ __forceinline__ void conv_accumulate4_fast(uint64_t (&acc)[4], const uint32_t* __restrict__ sw,
+                                                      int nblk, const uint32_t* __restrict__ sv,
+                                                      int base, uint32_t& since,
+                                                      const FieldParams& F) {
+    if (since + 4u * unsigned(nblk) <= F.fold_terms) {
+        since += 4u * unsigned(nblk);
+        switch (nblk) {
+            case 1: conv_accumulate_fixed<4, 1>(acc, sw, sv, base); return;
+            case 2: conv_accumulate_fixed<4, 2>(acc, sw, sv, base); return;
+            case 4: conv_accumulate_fixed<4, 4>(acc, sw, sv, base); return;
+            case 8: conv_accumulate_fixed<4, 8>(acc, sw, sv, base); return;
+            default: since -= 4u * unsigned(nblk); break;
+        }
+    }
+    conv_accumulate<4>(acc, sw, nblk, sv, base, since, F);
 }
 
 }  // namespace mmm_cu

@@ -423,7 +423,7 @@ __device__ void pipe_head(const PipeArgs& g, uint32_t* sm, int nbulk) {
                 const int k0 = 4 * qd, t0 = part * SPANL;
                 uint32_t since = 0;
                 if (t0 <= k0 + 3)
-                    PIPE_CONV(conv_accumulate<4>(acc, hd + t0, SPANL / 4, hz, horg + k0 - t0, since,
+                    PIPE_CONV(conv_accumulate4_fast(acc, hd + t0, SPANL / 4, hz, horg + k0 - t0, since,
                                                  F));
             },
             [&](int k, uint32_t lam) {
@@ -448,7 +448,7 @@ __device__ void pipe_head(const PipeArgs& g, uint32_t* sm, int nbulk) {
                     const int t0 = tq + 4 * qd, k0 = part * SPAN;
                     uint32_t since = 0;
                     if (k0 < vp)
-                        PIPE_CONV(conv_accumulate<4>(acc, lamh + (j % L) * S + k0,
+                        PIPE_CONV(conv_accumulate4_fast(acc, lamh + (j % L) * S + k0,
                                                      min(SPAN, vp - k0) / 4, bt3, t0 - k0 + 3,
                                                      since, F));
                 },
@@ -486,7 +486,7 @@ __device__ void pipe_head(const PipeArgs& g, uint32_t* sm, int nbulk) {
                         const int n = min(S - k0, (part + 1) * SPAN - c0);
                         const int lim = d == 0 ? ((v + 3) & ~3) : S;
                         if (j - d >= 0 && k0 < lim)
-                            PIPE_CONV(conv_accumulate<4>(acc, lamh + ((j - d) % L) * S + k0,
+                            PIPE_CONV(conv_accumulate4_fast(acc, lamh + ((j - d) % L) * S + k0,
                                                          min(n, lim - k0) / 4, bt3,
                                                          t0 + d * S - k0 + 3, since, F));
                         c0 += n;
