@@ -16,12 +16,19 @@
 // rounds of the paper, done in L2 instead of log-round launches.  Batched
 // products give each instance whole k-tiles (no split).  Chunks are double
 // buffered through registers (cp.async at 4-byte granularity measured slower).
+#include <map>
+#include <mutex>
+#include <utility>
+
 #include "common.cuh"
 #include "conv.cuh"
 
 namespace mmm_cu {
 
 constexpr int MUL_T = 128;   // threads per CTA
+#ifndef MUL_ARRIVE
+#define MUL_ARRIVE 2  // split k-tile arrival: 1 = __threadfence + atomicAdd, 2 = one acq_rel atomic
+#endif
 #ifndef MUL_TI_WORDS
 #define MUL_TI_WORDS 256
 #endif
@@ -32,7 +39,10 @@ struct MulArgs {
     const uint32_t* b;
     uint32_t* f;
     unsigned long long* acc;  // split k-tiles accumulate here (single instance)
-    unsigned* arrived;        // per k-tile count of finished items (zeroed with acc)
+    unsigned* arrived;        // per k-tile count of finished items
+    // acc and arrived are persistent per stream and all-zero between calls:
+    // the last item of a k-tile reads its words and zeroes them (and resets
+    // its counter), so no zeroing pass runs before the kernel
     int64_t na, nb, lda, ldb, ldf;
     int64_t chunk;  // i-range per item
     int64_t klo, khi;  // output range [klo, khi): f[k - klo] (whole product: 0, na + nb - 1)
@@ -122,22 +132,64 @@ __global__ void __launch_bounds__(MUL_T) mul_kernel(MulArgs g) {
     if (!split) return;
     // the last item to finish this k-tile reduces it (threadfence reduction)
     __shared__ bool last;
+#if MUL_ARRIVE == 1
     __threadfence();
+#endif
     __syncthreads();
     if (threadIdx.x == 0) {
         const unsigned items = unsigned((ihi - ilo + g.chunk - 1) / g.chunk);
+#if MUL_ARRIVE == 1
         last = atomicAdd(g.arrived + blockIdx.y, 1u) == items - 1;
+#else
+        // release: this CTA's accumulator REDs (ordered before the barrier
+        // above by every thread's cumulativity through bar.sync) happen
+        // before the arrival; acquire: the last arriver sees every item's
+        unsigned old;
+        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old)
+                     : "l"(g.arrived + blockIdx.y) : "memory");
+        last = old == items - 1;
+#endif
     }
     __syncthreads();
     if (!last) return;
+#if MUL_ARRIVE == 1
     __threadfence();
+#endif
     for (int t = threadIdx.x; t < TK; t += MUL_T) {
         const int64_t k = k0 + t;
-        if (k < nf) f[k - g.klo] = reduce(__ldcg(g.acc + (k - g.klo)), g.F);
+        if (k < nf) {
+            f[k - g.klo] = reduce(__ldcg(g.acc + (k - g.klo)), g.F);
+            __stcg(g.acc + (k - g.klo), 0ull);  // zero for the next call on this stream
+        }
     }
+    if (threadIdx.x == 0) g.arrived[blockIdx.y] = 0u;
 }
 
 namespace {
+
+// The split-k accumulator and arrival counters of each (device, stream):
+// zeroed once when allocated, left zeroed by every kernel (see mul_kernel), so
+// calls on one stream (which are ordered) share it; another stream gets its own.
+struct AccBuf {
+    unsigned long long* p = nullptr;
+    size_t words = 0;
+};
+unsigned long long* persistent_acc(size_t words, cudaStream_t st) {
+    static std::mutex mu;
+    static std::map<std::pair<int, cudaStream_t>, AccBuf> bufs;
+    int dev = 0;
+    MMM_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(mu);
+    AccBuf& b = bufs[{dev, st}];
+    if (b.words < words) {
+        if (b.p) MMM_CUDA(cudaFreeAsync(b.p, st));
+        const size_t n = std::max(words, size_t(1) << 16);
+        MMM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&b.p), n * sizeof(unsigned long long), st));
+        MMM_CUDA(cudaMemsetAsync(b.p, 0, n * sizeof(unsigned long long), st));
+        b.words = n;
+    }
+    return b.p;
+}
 
 int pick_tile(int64_t s, const FieldParams& F) {
     int R = 1;
@@ -194,7 +246,6 @@ void launch_mul_range(const FieldParams& F, const uint32_t* a, int64_t na, const
     if (chunk < MUL_TI) chunk = MUL_TI;
     const int64_t items = ceil_div(longest, chunk);
 
-    Scratch scratch(st);
     MulArgs g{};
     g.a = a;
     g.b = b;
@@ -205,11 +256,10 @@ void launch_mul_range(const FieldParams& F, const uint32_t* a, int64_t na, const
     g.klo = klo;
     g.khi = khi;
     g.F = F;
-    if (items > 1) {  // one zeroing pass for the accumulator and the arrival counters
+    if (items > 1) {  // the stream's persistent all-zero accumulator and counters
         const size_t words = size_t(nf) + size_t(ceil_div(nkt, 2));
-        g.acc = scratch.get<unsigned long long>(words);
+        g.acc = persistent_acc(words, st);
         g.arrived = reinterpret_cast<unsigned*>(g.acc + nf);
-        MMM_CUDA(cudaMemsetAsync(g.acc, 0, words * sizeof(unsigned long long), st));
     }
     dispatch(R, g, dim3(unsigned(items), unsigned(nkt), 1), st);
 }
