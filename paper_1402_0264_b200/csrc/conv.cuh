@@ -123,4 +123,29 @@ __device__ __forceinline__ void conv_accumulate4_fast(uint64_t (&acc)[4], const 
     conv_accumulate<4>(acc, sw, nblk, sv, base, since, F);
 }
 
+// conv_accumulate<R> in straight-line groups of 32 terms (R % 4 == 0): one
+// fold test per group instead of per block, no loop branch inside a group.
+template <int R>
+__device__ __forceinline__ void conv_accumulate_grouped(uint64_t (&acc)[R], const uint32_t* __restrict__ sw,
+                                                        int nblk, const uint32_t* __restrict__ sv,
+                                                        int base, uint32_t& since,
+                                                        const FieldParams& F) {
+    constexpr int G = 32 / R;  // blocks per group
+    if (R % 4 != 0 || G < 1 || F.fold_terms < unsigned(G * R)) {
+        conv_accumulate<R>(acc, sw, nblk, sv, base, since, F);
+        return;
+    }
+    int blk = 0;
+    for (; blk + G <= nblk; blk += G) {
+        if (since + G * R > F.fold_terms) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) acc[r] = fold(acc[r], F);
+            since = 0;
+        }
+        conv_accumulate_fixed<R, (G > 0 ? G : 1)>(acc, sw + blk * R, sv, base - blk * R);
+        since += G * R;
+    }
+    if (blk < nblk) conv_accumulate<R>(acc, sw + blk * R, nblk - blk, sv, base - blk * R, since, F);
+}
+
 }  // namespace mmm_cu

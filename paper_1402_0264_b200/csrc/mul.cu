@@ -26,6 +26,9 @@
 namespace mmm_cu {
 
 constexpr int MUL_T = 128;   // threads per CTA
+#ifndef MUL_GROUPED
+#define MUL_GROUPED 1  // straight-line 32-term groups in the inner loop
+#endif
 #ifndef MUL_ARRIVE
 #define MUL_ARRIVE 2  // split k-tile arrival: 1 = __threadfence + atomicAdd, 2 = one acq_rel atomic
 #endif
@@ -111,7 +114,12 @@ __global__ void __launch_bounds__(MUL_T) mul_kernel(MulArgs g) {
         const int cnt = int(i_end - ic < MUL_TI ? i_end - ic : MUL_TI);
         const bool more = ic + MUL_TI < i_end;
         if (more) fetch(ic + MUL_TI);  // in flight during the multiply
-        conv_accumulate<R>(acc, sw[buf], (cnt + R - 1) / R, sv[buf], base, since, g.F);
+#if MUL_GROUPED
+        if constexpr (R % 4 == 0)
+            conv_accumulate_grouped<R>(acc, sw[buf], (cnt + R - 1) / R, sv[buf], base, since, g.F);
+        else
+#endif
+            conv_accumulate<R>(acc, sw[buf], (cnt + R - 1) / R, sv[buf], base, since, g.F);
         if (more) store(buf ^ 1);
         __syncthreads();
         buf ^= 1;
