@@ -148,4 +148,15 @@ __device__ __forceinline__ void conv_accumulate_grouped(uint64_t (&acc)[R], cons
     if (blk < nblk) conv_accumulate<R>(acc, sw + blk * R, nblk - blk, sv, base - blk * R, since, F);
 }
 
+// The fastest variant for the tile: straight-line groups when R % 4 == 0.
+template <int R>
+__device__ __forceinline__ void conv_accumulate_auto(uint64_t (&acc)[R], const uint32_t* __restrict__ sw,
+                                                     int nblk, const uint32_t* __restrict__ sv,
+                                                     int base, uint32_t& since, const FieldParams& F) {
+    if constexpr (R % 4 == 0)
+        conv_accumulate_grouped<R>(acc, sw, nblk, sv, base, since, F);
+    else
+        conv_accumulate<R>(acc, sw, nblk, sv, base, since, F);
+}
+
 }  // namespace mmm_cu

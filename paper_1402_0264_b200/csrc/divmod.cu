@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(DIV_T) div_cta_kernel(DivArgs g, int borg) {
 #pragma unroll
             for (int r = 0; r < R; ++r) acc[r] = (y0 + r < db) ? A[xlo + y0 + r] : 0u;
             uint32_t since = 0;
-            conv_accumulate<R>(acc, lam, padded / R, bs, int(borg + y0), since, F);
+            conv_accumulate_auto<R>(acc, lam, padded / R, bs, int(borg + y0), since, F);
 #pragma unroll
             for (int r = 0; r < R; ++r)
                 if (y0 + r < db) A[xlo + y0 + r] = reduce(acc[r], F);
@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(DIV_T) div_grid_kernel(DivArgs g, int64_t seg)
 #pragma unroll
             for (int r = 0; r < RL; ++r) acc[r] = 0;
             uint32_t since = 0;
-            conv_accumulate<RL>(acc, hd, nl / RL, hz, horg + k0, since, F);
+            conv_accumulate_auto<RL>(acc, hd, nl / RL, hz, horg + k0, since, F);
 #pragma unroll
             for (int r = 0; r < RL; ++r) {
                 const int k = k0 + r;
@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(DIV_T) div_grid_kernel(DivArgs g, int64_t seg)
 #pragma unroll
             for (int r = 0; r < RU; ++r) acc[r] = (y0 + r < y_hi) ? __ldcg(A + xlo + y0 + r) : 0u;
             uint32_t since = 0;
-            conv_accumulate<RU>(acc, lam, nu / RU, bseg, int(borg + (y0 - y_lo)), since, F);
+            conv_accumulate_auto<RU>(acc, lam, nu / RU, bseg, int(borg + (y0 - y_lo)), since, F);
 #pragma unroll
             for (int r = 0; r < RU; ++r)
                 if (y0 + r < y_hi) __stcg(A + xlo + y0 + r, reduce(acc[r], F));
@@ -582,7 +582,7 @@ __device__ void pipe_bulk(const PipeArgs& g, uint32_t* sm, int nbulk, int me) {
                 if (worker && u0 < vp) {
                     uint64_t pa[4] = {0, 0, 0, 0};
                     uint32_t since = 0;
-                    conv_accumulate<4>(pa, lam + u0, min(span, vp - u0) / 4, bw,
+                    conv_accumulate4_fast(pa, lam + u0, min(span, vp - u0) / 4, bw,
                                        4 * qd + vp - 1 - u0, since, F);
 #pragma unroll
                     for (int r = 0; r < 4; ++r) {

@@ -1382,7 +1382,7 @@ __device__ void apply_batch(const GcdArgs& g, const BatchMeta& m, int j, long lo
             if (item < items && h >= e0) {
                 const int nblk = (min(h + 1, e0 + PL / 2) - e0 + 3) >> 2;
                 uint32_t* const Wrt = r ? (t ? W3 : W2) : (t ? W1 : W0);
-                conv_accumulate<4>(acc, P + (2 * r + t) * PL + e0, nblk, Wrt,
+                conv_accumulate4_fast(acc, P + (2 * r + t) * PL + e0, nblk, Wrt,
                                    4 * qi + PL - 1 - e0, since, F);
             }
             uint32_t v[4];
