@@ -1048,7 +1048,7 @@ __device__ void window_from_global(uint32_t* win, const uint64_t* Z, unsigned ta
 // 4 consecutive words (shared-memory reads: broadcast or consecutive, no
 // bank conflicts), and the parts meet in a shared-memory reduction.
 #ifndef GCD_BUILD_PARTS
-#define GCD_BUILD_PARTS 4
+#define GCD_BUILD_PARTS 4  // 8 (warp 7 builds, publishes after) measured 15 % slower
 #endif
 constexpr int BUILD_PARTS = GCD_BUILD_PARTS;
 static_assert(2 * (W1 / 4) == 32, "window builder: one (window, quad) per lane");
@@ -1192,7 +1192,8 @@ __device__ int head_cta(const GcdArgs& g, BatchMeta& ctl, StepLog* log, uint32_t
         for (int i = 0; i < 4; ++i) m.hi[i] = hi_s[i];
         m.err = (m.steps == 0 && m.term == 0) ? 1 : 0;
         const bool last = m.term || m.err;
-        if (warp == 7) {  // publish batch j: the record's meta words (the replay wrote P)
+        // warp 7 publishes batch j: the record's meta words (the replay wrote P)
+        auto publish = [&]() {
             const int l = threadIdx.x - 224;
             // selects on registers (a runtime index into m would put it in local memory)
             const int h0 = m.hi[0], h1 = m.hi[1], h2 = m.hi[2], h3 = m.hi[3];
@@ -1207,30 +1208,31 @@ __device__ int head_cta(const GcdArgs& g, BatchMeta& ctl, StepLog* log, uint32_t
             if (l == 16) v = int(minprog_s);
             if (l < META_W)
                 st_tag(g.rec + (j % RING) * REC_W + 4 * PL + l, uint32_t(v), unsigned(j + 1));
-
             if (threadIdx.x == 224 && g.stats) {
                 tpub_s = tp;
                 hst[0] += 1;
                 hst[1] += m.steps;
             }
-            if (last) {
-                __syncthreads();  // with warps 0-6 (same branch): hst complete
-                if (g.stats && threadIdx.x == 224) {
-                    for (int i = 0; i < 10; ++i) g.stats[i == 7 ? 8 : (i == 8 ? 9 : (i == 9 ? 10 : i))] = hst[i];
-                    g.stats[17] = hst[10];
-                    for (int i = 0; i < 4; ++i) g.stats[21 + i] = hx[i];
-                    g.stats[19] = hst[11];
-                }
-                return j;
-            }
-            if (BUILD_PARTS < 8) continue;  // next batch (else warp 7 also builds)
-        }
+        };
         if (last) {
-            if (warp != 7) __syncthreads();
+            if (warp == 7) publish();
+            __syncthreads();  // hst complete
+            if (g.stats && threadIdx.x == 224) {
+                for (int i = 0; i < 10; ++i) g.stats[i == 7 ? 8 : (i == 8 ? 9 : (i == 9 ? 10 : i))] = hst[i];
+                g.stats[17] = hst[10];
+                for (int i = 0; i < 4; ++i) g.stats[21 + i] = hx[i];
+                g.stats[19] = hst[11];
+            }
             return j;
         }
-        // warps 0-6: next windows, top-aligned, from S_j and the batch matrix
+        if (warp == 7 && BUILD_PARTS < 8) {  // publish now; the next batch's prefetch group
+            publish();
+            continue;
+        }
+        // next windows, top-aligned, from S_j and the batch matrix (with 8
+        // parts warp 7 builds first and publishes after: the bulk has slack)
         if (warp < BUILD_PARTS) build_window_part(warp, red, Ps, hi_s, topA, topB, F);
+        if (BUILD_PARTS == 8 && warp == 7) publish();
         if (g.stats && (g.dbg & 4)) {  // timing experiment: the same part again (warm)
             if (warp < BUILD_PARTS) build_window_part(warp, red, Ps, hi_s, topA, topB, F);
             if (threadIdx.x == 0) hx[3] += clock64() - t0;
