@@ -37,7 +37,7 @@ __all__ = [
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libmmm_cu.so")
+LIB_PATH = os.environ.get("MMM_CU_LIB") or os.path.join(HERE, "lib", "libmmm_cu.so")
 
 
 class MmmError(RuntimeError):
