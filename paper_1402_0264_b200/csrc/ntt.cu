@@ -75,13 +75,14 @@ __device__ __forceinline__ uint32_t shoup(uint32_t x, uint32_t w, uint32_t wp, u
     const uint32_t r = x * w - q * p;
     return umin(r, r - p);
 }
+// Sums and differences as min(a +- b, a +- b -+ m): IADD3 + VIADDMNMX, both on
+// the ALU pipe (a plain a + b tends to become IMAD.IADD on the multiply pipe,
+// the one the Shoup products saturate).
 __device__ __forceinline__ uint32_t add_p(uint32_t a, uint32_t b, uint32_t p) {
-    const uint32_t s = a + b;
-    return umin(s, s - p);
+    return __viaddmin_u32(a, b, a + b - p);
 }
 __device__ __forceinline__ uint32_t sub_p(uint32_t a, uint32_t b, uint32_t p) {
-    const uint32_t d = a - b;
-    return umin(d, d + p);
+    return __viaddmin_u32(a, 0u - b, a - b + p);
 }
 
 // Butterfly halves, exact (LZ = false: canonical in and out) or lazy (LZ =
@@ -92,8 +93,7 @@ __device__ __forceinline__ uint32_t sub_p(uint32_t a, uint32_t b, uint32_t p) {
 template <bool LZ>
 __device__ __forceinline__ uint32_t bf_add(uint32_t a, uint32_t b, uint32_t p) {
     if (!LZ) return add_p(a, b, p);
-    const uint32_t s = a + b;
-    return umin(s, s - 2 * p);
+    return __viaddmin_u32(a, b, a + b - 2 * p);
 }
 template <bool LZ>
 __device__ __forceinline__ uint32_t shoup_l(uint32_t x, uint32_t w, uint32_t wp, uint32_t p) {
@@ -107,8 +107,7 @@ __device__ __forceinline__ uint32_t bf_subw(uint32_t a, uint32_t b, uint2 w, uin
 template <bool LZ>
 __device__ __forceinline__ uint32_t bf_sub1(uint32_t a, uint32_t b, uint32_t p) {  // twiddle 1
     if (!LZ) return sub_p(a, b, p);
-    const uint32_t d = a - b + 2 * p;
-    return umin(d, d - 2 * p);
+    return __viaddmin_u32(a, 0u - b, a - b + 2 * p);
 }
 __device__ __forceinline__ uint32_t canon(uint32_t v, uint32_t p) { return umin(v, v - p); }
 
@@ -224,22 +223,23 @@ template <int LOGL, int S, int K, bool LZ>
 __device__ __forceinline__ void radix(uint32_t (&v)[1 << K], int pp, const uint2* __restrict__ tw,
                                       uint32_t p) {
     constexpr int R = 1 << K, L = 1 << LOGL;
+    constexpr bool LASTP = S + K == LOGL;  // last pass: pp == 0, so j == 0 has twiddle 1
 #pragma unroll
     for (int i = 0; i < K; ++i) {
         uint32_t w[R];
-        const uint2* tb = tw + (pp << (S + i));
+        const uint2* tb = tw + (LASTP ? 0 : (pp << (S + i)));
 #pragma unroll
         for (int j = 0; j < (R >> (i + 1)); ++j) {
+            const bool one = (S + i == LOGL - 1) || (LASTP && j == 0);
             uint2 t = make_uint2(1, 0);
-            if (S + i != LOGL - 1) t = ldg2(tb + j * (L >> (K - i)));
+            if (!one) t = ldg2(tb + j * (L >> (K - i)));
 #pragma unroll
             for (int bb = 0; bb < (1 << i); ++bb) {
                 const int r = (j << i) | bb;
                 const uint32_t a0 = v[r], a1 = v[r + R / 2];
                 const int o = (j << (i + 1)) | bb;
                 w[o] = bf_add<LZ>(a0, a1, p);
-                w[o | (1 << i)] =
-                    (S + i == LOGL - 1) ? bf_sub1<LZ>(a0, a1, p) : bf_subw<LZ>(a0, a1, t, p);
+                w[o | (1 << i)] = one ? bf_sub1<LZ>(a0, a1, p) : bf_subw<LZ>(a0, a1, t, p);
             }
         }
 #pragma unroll
@@ -301,11 +301,25 @@ __device__ __forceinline__ void mid_passes(uint32_t* const (&buf)[NOPS], const u
     }
 }
 
+// Programmatic dependent launch: K2 and K3 are launched with the
+// programmatic-serialization attribute, so their CTAs are scheduled while the
+// previous kernel's last CTAs run and wait here for its completion (and its
+// memory) before touching the workspace.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// Table entry by 32-bit byte offset (LOP3/SHF + a 64-bit add on the ALU pipe,
+// not an IMAD.WIDE on the multiply pipe).
+__device__ __forceinline__ uint2 ldg_at(const uint2* t, uint32_t byte_off) {
+    return __ldg(reinterpret_cast<const uint2*>(reinterpret_cast<uintptr_t>(t) + byte_off));
+}
 template <bool LZ>
 __device__ __forceinline__ uint32_t twiddle(uint32_t v, uint32_t e, const uint2* lo,
                                             const uint2* hi, uint32_t p) {
-    const uint2 a = ldg2(lo + (e & ((1u << LO) - 1)));
-    const uint2 b = ldg2(hi + (e >> LO));
+    const uint2 a = ldg_at(lo, (e << 3) & (((1u << LO) - 1) << 3));
+    const uint2 b = ldg_at(hi, (e >> LO) << 3);
     return shoup_l<LZ>(shoup_l<LZ>(v, a.x, a.y, p), b.x, b.y, p);
 }
 
@@ -324,17 +338,19 @@ struct NttArgs {
 // K1 (OUT = false) and K3 (OUT = true): the column transforms of a tile of C
 // consecutive columns.  K1: grid.y = operand; reads the zero-padded input,
 // writes the twiddled workspace.  K3: reads the workspace, writes f.
-template <int LOGL, int LOGC, bool OUT, bool LZ>
+template <int LOGL, int LOGC, int D, bool OUT, bool LZ>
 __global__ void __launch_bounds__(Geo<LOGL, LOGC, 0>::T, NTT_MINB) ntt_cols(NttArgs g) {
     using GE = Geo<LOGL, LOGC, 0>;
     constexpr int T = GE::T;
     using P0 = PassT<GE, 0>;
     using PL = PassT<GE, GE::P - 1>;
     constexpr int NU = GE::U0 / T;
+    constexpr int N2 = GE::L << D;  // row length: log2 = log1 + D
     extern __shared__ __align__(16) uint32_t sm[];
+    pdl_wait();     // K3: K2's workspace (no-op when launched without PDL)
+    pdl_trigger();  // let the next kernel's CTAs take the SMs this grid's tail frees
     const NttPlan& P = g.P;
     const uint32_t p = P.p;
-    const int N2 = 1 << P.log2;
     const int op = OUT ? 0 : blockIdx.y;
     const int64_t inst = blockIdx.z;
     const int c0 = g.col0 + blockIdx.x * GE::C;
@@ -342,27 +358,27 @@ __global__ void __launch_bounds__(Geo<LOGL, LOGC, 0>::T, NTT_MINB) ntt_cols(NttA
     uint32_t v[NU][P0::R];
     // first pass: global -> registers
     if constexpr (!OUT) {
-        const uint32_t* in = g.in[op] + inst * g.ld[op];
         const int64_t len = g.len[op];
 #pragma unroll
         for (int n = 0; n < NU; ++n) {
             const int x = threadIdx.x + n * T;
             const int c = P0::c_of(x), u = P0::u_of(x);
+            const uint32_t* in = g.in[op] + inst * g.ld[op] + (c0 + c + u * N2);
+            // element j at in[j*UR*N2] (immediate offsets); zero past len
+            const int64_t lim64 = len - (c0 + c + int64_t(u) * N2);
+            const int lim = lim64 < 0 ? 0 : (lim64 > (1 << 30) ? (1 << 30) : int(lim64));
 #pragma unroll
-            for (int j = 0; j < P0::R; ++j) {
-                const int64_t idx = int64_t(N2) * (u + j * P0::UR) + c0 + c;
-                v[n][j] = idx < len ? __ldg(in + idx) : 0u;
-            }
+            for (int j = 0; j < P0::R; ++j)
+                v[n][j] = j * P0::UR * N2 < lim ? __ldg(in + j * P0::UR * N2) : 0u;
         }
     } else {
         const uint32_t* work = g.work[0] + (inst << P.logN);
 #pragma unroll
         for (int n = 0; n < NU; ++n) {
             const int x = threadIdx.x + n * T;
-            const int c = P0::c_of(x), u = P0::u_of(x);
+            const uint32_t* w = work + (c0 + P0::c_of(x) + P0::u_of(x) * N2);
 #pragma unroll
-            for (int j = 0; j < P0::R; ++j)
-                v[n][j] = __ldg(work + int64_t(N2) * (u + j * P0::UR) + c0 + c);
+            for (int j = 0; j < P0::R; ++j) v[n][j] = __ldg(w + j * P0::UR * N2);
         }
     }
 #pragma unroll
@@ -388,21 +404,24 @@ __global__ void __launch_bounds__(Geo<LOGL, LOGC, 0>::T, NTT_MINB) ntt_cols(NttA
         const int x = threadIdx.x + n * T;
         const int c = PL::c_of(x), u = PL::u_of(x);
         if constexpr (!OUT) {
-            uint32_t* work = g.work[op] + (inst << P.logN);
+            uint32_t* work = g.work[op] + (inst << P.logN) + (c0 + c + u * N2);
             const uint2* hi = op == 0 ? P.thi : P.thi_s;
+            const uint32_t e0 = uint32_t(c0 + c) * uint32_t(u), de = uint32_t(c0 + c) * PL::UR;
 #pragma unroll
-            for (int b = 0; b < PL::R; ++b) {
-                const int k1 = u + b * PL::UR;
-                work[int64_t(N2) * k1 + c0 + c] =
-                    twiddle<LZ>(v[n][b], uint32_t(c0 + c) * uint32_t(k1), P.tlo, hi, p);
-            }
+            for (int b = 0; b < PL::R; ++b)  // k1 = u + b*UR, twiddle w_N^(n2*k1)
+                work[b * PL::UR * N2] = twiddle<LZ>(v[n][b], e0 + b * de, P.tlo, hi, p);
         } else {
-            uint32_t* out = g.out + inst * g.ldf;
+            // m = N2*(u + b*UR) + c0 + c  ->  f[(N - m) mod N]; only m == 0 wraps
+            const int m0 = N2 * u + c0 + c;
+            const int64_t nf = g.nf;
+            uint32_t* out = g.out + inst * g.ldf + (N - m0);
 #pragma unroll
             for (int b = 0; b < PL::R; ++b) {
-                const int m = N2 * (u + b * PL::UR) + c0 + c;
-                const int nidx = (N - m) & (N - 1);
-                if (nidx < g.nf) out[nidx] = canon(v[n][b], p);
+                const int nidx = N - m0 - b * PL::UR * N2;
+                if (m0 == 0 && b == 0)
+                    g.out[inst * g.ldf] = canon(v[n][b], p);
+                else if (nidx < nf)
+                    out[-b * PL::UR * N2] = canon(v[n][b], p);
             }
         }
     }
@@ -419,22 +438,24 @@ __global__ void __launch_bounds__(Geo<LOGL, 0, LOGG>::U0, NTT_MINB_ROWS) ntt_row
     using PL = PassT<GE, GE::P - 1>;
     static_assert(P0::K == PL::K, "symmetric schedule");
     extern __shared__ __align__(16) uint32_t sm[];
+    pdl_wait();  // K1's workspace
+    pdl_trigger();
     const NttPlan& P = g.P;
     const uint32_t p = P.p;
-    const int N2 = 1 << P.log2;
+    constexpr int N2 = GE::L;
     const int64_t inst = blockIdx.z;
     const int x = threadIdx.x;
     const int u = P0::u_of(x);
     const int k1 = g.row0 + blockIdx.x * GE::G + P0::g_of(x);
     const bool valid = k1 < g.row_end;
-    uint32_t* wa = g.work[0] + (inst << P.logN) + int64_t(k1) * N2;
-    const uint32_t* wb = g.work[1] + (inst << P.logN) + int64_t(k1) * N2;
+    uint32_t* wa = g.work[0] + (inst << P.logN) + (k1 * N2 + u);
+    const uint32_t* wb = g.work[1] + (inst << P.logN) + (k1 * N2 + u);
     const uint2* tw = P.r2;
     uint32_t va[P0::R], vb[P0::R];
 #pragma unroll
     for (int j = 0; j < P0::R; ++j) {
-        va[j] = valid ? wa[u + j * P0::UR] : 0u;
-        vb[j] = valid ? __ldg(wb + u + j * P0::UR) : 0u;
+        va[j] = valid ? wa[j * P0::UR] : 0u;
+        vb[j] = valid ? __ldg(wb + j * P0::UR) : 0u;
     }
     radix<LOGL, 0, P0::K, LZ>(va, u, tw, p);
     radix<LOGL, 0, P0::K, LZ>(vb, u, tw, p);
@@ -469,11 +490,10 @@ __global__ void __launch_bounds__(Geo<LOGL, 0, LOGG>::U0, NTT_MINB_ROWS) ntt_row
         radix<LOGL, PL::S, PL::K, LZ>(va, 0, tw, p);
     }
     if (valid) {
+        const uint32_t e0 = uint32_t(k1) * uint32_t(u), de = uint32_t(k1) * PL::UR;
 #pragma unroll
-        for (int b = 0; b < PL::R; ++b) {
-            const int m2 = u + b * PL::UR;
-            wa[m2] = twiddle<LZ>(va[b], uint32_t(k1) * uint32_t(m2), P.tlo, P.thi, p);
-        }
+        for (int b = 0; b < PL::R; ++b)  // m2 = u + b*UR, twiddle w_N^(k1*m2)
+            wa[b * PL::UR] = twiddle<LZ>(va[b], e0 + b * de, P.tlo, P.thi, p);
     }
 }
 
@@ -498,22 +518,22 @@ struct ColsKernel {
     size_t smem;
 };
 
-template <int LOGL, int LOGC, bool OUT, bool LZ>
+template <int LOGL, int LOGC, int D, bool OUT, bool LZ>
 ColsKernel cols_kernel() {
     using GE = Geo<LOGL, LOGC, 0>;
     const size_t smem = GE::P > 1 ? size_t(GE::WORDS) * 4 : 0;
-    ColsKernel k{ntt_cols<LOGL, LOGC, OUT, LZ>, GE::T, GE::C, smem};
+    ColsKernel k{ntt_cols<LOGL, LOGC, D, OUT, LZ>, GE::T, GE::C, smem};
     if (smem > 48 * 1024)
         MMM_CUDA(cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     return k;
 }
 
 template <int LOGL, bool OUT, bool LZ>
-ColsKernel cols_for(bool phase) {
+ColsKernel cols_for(bool phase, int d) {
     constexpr int LM = main_logc(LOGL);
     constexpr int LP = LOGL < 2 ? LOGL : 2;  // phases: NTT_PHASE_COLS columns (N2 >= L)
-    if (phase) return cols_kernel<LOGL, LP, OUT, LZ>();
-    return cols_kernel<LOGL, LM, OUT, LZ>();
+    if (phase) return d ? cols_kernel<LOGL, LP, 1, OUT, LZ>() : cols_kernel<LOGL, LP, 0, OUT, LZ>();
+    return d ? cols_kernel<LOGL, LM, 1, OUT, LZ>() : cols_kernel<LOGL, LM, 0, OUT, LZ>();
 }
 
 struct RowsKernel {
@@ -532,11 +552,11 @@ RowsKernel rows_for() {
 }
 
 template <bool OUT, bool LZ>
-ColsKernel pick_cols(int logl, bool phase) {
+ColsKernel pick_cols(int logl, int log2, bool phase) {
     switch (logl) {
 #define MMM_NTT_CASE(n) \
     case n:             \
-        return cols_for<n, OUT, LZ>(phase);
+        return cols_for<n, OUT, LZ>(phase, log2 - logl);
         MMM_NTT_CASE(1) MMM_NTT_CASE(2) MMM_NTT_CASE(3) MMM_NTT_CASE(4) MMM_NTT_CASE(5)
         MMM_NTT_CASE(6) MMM_NTT_CASE(7) MMM_NTT_CASE(8) MMM_NTT_CASE(9) MMM_NTT_CASE(10)
         MMM_NTT_CASE(11) MMM_NTT_CASE(12) MMM_NTT_CASE(13)
@@ -662,12 +682,26 @@ uint32_t p_inverse(uint32_t p) {  // p^-1 mod 2^32, odd p
     return inv;
 }
 
+void launch_pdl(ColsFn fn, dim3 grid, int threads, size_t smem, cudaStream_t st, NttArgs g) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(unsigned(threads));
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    MMM_CUDA(cudaLaunchKernelEx(&cfg, fn, g));
+}
+
 template <bool LZ>
 void run_ntt_launches(NttArgs g, int64_t count, int64_t chunk, const uint32_t* A, int64_t lda,
                       const uint32_t* B, int64_t ldb, uint32_t* Fo, int64_t ldf, cudaStream_t st) {
     const int N1 = 1 << g.P.log1, N2 = 1 << g.P.log2;
-    const ColsKernel kf = pick_cols<false, LZ>(g.P.log1, false);
-    const ColsKernel ko = pick_cols<true, LZ>(g.P.log1, false);
+    const ColsKernel kf = pick_cols<false, LZ>(g.P.log1, g.P.log2, false);
+    const ColsKernel ko = pick_cols<true, LZ>(g.P.log1, g.P.log2, false);
     const RowsKernel kr = pick_rows<LZ>(g.P.log2);
     g.col0 = 0;
     g.row0 = 0;
@@ -682,9 +716,9 @@ void run_ntt_launches(NttArgs g, int64_t count, int64_t chunk, const uint32_t* A
         g.ldf = ldf;
         kf.fn<<<dim3(N2 / kf.cols, 2, c), kf.threads, kf.smem, st>>>(g);
         check_launch("ntt_cols_fwd");
-        kr.fn<<<dim3((N1 + kr.rows - 1) / kr.rows, 1, c), kr.threads, kr.smem, st>>>(g);
+        launch_pdl(kr.fn, dim3((N1 + kr.rows - 1) / kr.rows, 1, c), kr.threads, kr.smem, st, g);
         check_launch("ntt_rows");
-        ko.fn<<<dim3(N2 / ko.cols, 1, c), ko.threads, ko.smem, st>>>(g);
+        launch_pdl(ko.fn, dim3(N2 / ko.cols, 1, c), ko.threads, ko.smem, st, g);
         check_launch("ntt_cols_out");
     }
 }
@@ -729,8 +763,8 @@ void phase_launch(NttArgs g, int phase, int64_t start, int64_t n, cudaStream_t s
         kr.fn<<<dim3(unsigned((n + kr.rows - 1) / kr.rows), 1, 1), kr.threads, kr.smem, st>>>(g);
         check_launch("ntt_rows");
     } else {
-        const ColsKernel k = phase == 0 ? pick_cols<false, LZ>(g.P.log1, true)
-                                        : pick_cols<true, LZ>(g.P.log1, true);
+        const ColsKernel k = phase == 0 ? pick_cols<false, LZ>(g.P.log1, g.P.log2, true)
+                                        : pick_cols<true, LZ>(g.P.log1, g.P.log2, true);
         g.col0 = int(start);
         k.fn<<<dim3(unsigned(n / k.cols), phase == 0 ? 2 : 1, 1), k.threads, k.smem, st>>>(g);
         check_launch(phase == 0 ? "ntt_cols_fwd" : "ntt_cols_out");
