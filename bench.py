@@ -184,20 +184,25 @@ def imad_rate():
 
 def ntt_roofline(logN, count, t_step, kernel):
     """The NTT's bound is the integer multiply pipe (IMAD-bound
-    when each transform makes <= 1 HBM pass).  IMAD-class ops per step: 3 per
-    butterfly (Shoup product: IMAD.HI + 2 IMAD) over the 3 transforms, 3 per
-    four-step twiddle / scale product (2 per element per operand in the
-    forward columns, 2 in the rows' inverse twiddle, 1 in the scale: 7 per
-    output word), 4 per pointwise Montgomery product."""
+    when each transform makes <= 1 HBM pass).  Every modular product is a
+    Shoup product (IMAD.HI + 2 IMAD) or, for the pointwise product, a
+    Montgomery REDC (IMAD.WIDE + IMAD + IMAD.HI).  IMAD.HI and IMAD.WIDE issue
+    at half the IMAD rate on this part (profiles/peaks.json: 8.76e12 vs
+    1.82e13 /s), so in IMAD issue slots a Shoup product costs 4 and a REDC 5.
+    Products per step: one per butterfly over the 3 transforms (3 (N/2) logN),
+    6 N four-step twiddle products (2 per word per operand after the forward
+    columns, 2 per word after the rows; the N^-1 scale rides in operand b's
+    table) and N pointwise REDCs.  Peak: the measured IMAD rate."""
     N = 1 << logN
     bfly = 3 * (N // 2) * logN * count
-    ops = 3 * bfly + 3 * 7 * N * count + 4 * N * count
+    slots = 4 * (bfly + 6 * N * count) + 5 * N * count
     peak = imad_rate()
-    achieved = ops / t_step
+    achieved = slots / t_step
     return {"bound": "imad", "achieved": achieved / 1e12, "peak": peak / 1e12,
-            "unit": "T IMAD-class/s", "frac": achieved / peak, "traffic": None,
-            "kernel": kernel, "alg_imad_ops_per_step": ops, "butterflies": bfly,
-            "peak_note": "measured IMAD rate (profiles/peaks.json imad_per_s)"}
+            "unit": "T IMAD-slots/s", "frac": achieved / peak, "traffic": None,
+            "kernel": kernel, "alg_imad_slots_per_step": slots, "butterflies": bfly,
+            "peak_note": "measured IMAD rate (profiles/peaks.json imad_per_s); "
+                         "IMAD.HI/IMAD.WIDE count as 2 slots"}
 
 
 class ProductRng:
