@@ -12,9 +12,10 @@ for w in gcd mul div div_fast ntt ntt_batch batch; do
 done
 timeout 300 python bench.py --steps 3 --warmup 3 --no-cpu-baseline > $O/bench_plain.log 2>&1 && \
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_gcd.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline > $O/ncu_launch.log 2>&1
-for w in gcd mul div ntt batch; do
-  case $w in gcd) k=gcd_kernel;; mul) k=mul_kernel;; div) k=div_pipe_kernel;; ntt) k=ntt_rows;; batch) k=div_cta_kernel;; esac
+for w in gcd mul div ntt ntt_batch batch; do
+  c=1
+  case $w in gcd) k=gcd_kernel;; mul) k=mul_kernel;; div) k=div_pipe_kernel;; ntt|ntt_batch) k=ntt_; c=3;; batch) k=div_cta_kernel;; esac
   timeout 120 python tools/prof_one.py $w --reps 1 > $O/plain_$w.log 2>&1 && \
-  timeout 600 ncu --set full --import-source on --clock-control none -k regex:$k -c 1 -o $O/full_$w python tools/prof_one.py $w --reps 1 > $O/ncu_$w.log 2>&1
+  timeout 600 ncu --set full --import-source on --clock-control none -k regex:$k -c $c -o $O/full_$w python tools/prof_one.py $w --reps 1 > $O/ncu_$w.log 2>&1
   tail -1 $O/ncu_$w.log
 done

@@ -21,6 +21,9 @@ KEYS = [
     "smsp__inst_executed.avg.per_cycle_active", "sm__warps_active.avg.pct_of_peak_sustained_active",
     "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
     "smsp__average_warp_latency_issue_stalled_wait", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
+    "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed",
+    "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__issue_active.avg.pct_of_peak_sustained_elapsed",
 ]
 
 
@@ -56,12 +59,13 @@ def kernels(reps, out):
             r = list(csv.reader(raw.splitlines()))
             if len(r) < 3:
                 continue
-            h, units, vals = r[0], r[1], r[2]
-            kname = vals[h.index("Kernel Name")] if "Kernel Name" in h else "?"
-            for key in KEYS:
-                if key in h:
-                    i = h.index(key)
-                    w.writerow([os.path.basename(rep), kname, key, units[i], vals[i]])
+            h, units = r[0], r[1]
+            for vals in r[2:]:  # every captured launch
+                kname = vals[h.index("Kernel Name")] if "Kernel Name" in h else "?"
+                for key in KEYS:
+                    if key in h:
+                        i = h.index(key)
+                        w.writerow([os.path.basename(rep), kname, key, units[i], vals[i]])
 
 
 def main():
