@@ -31,6 +31,7 @@
 #include <map>
 #include <memory>
 #include <mutex>
+#include <type_traits>
 #include <vector>
 
 #include "common.cuh"
@@ -57,6 +58,9 @@ constexpr int NTT_PHASE_COLS = 4;  // column granularity of the sharded phases
 #endif
 #ifndef NTT_CHUNK_WORDS
 #define NTT_CHUNK_WORDS (1 << 30)
+#endif
+#ifndef NTT_PREFER_END
+#define NTT_PREFER_END 1  // 1: largest end radix (e.g. 2^10 = 4+2+4 instead of 3+4+3)
 #endif
 #ifndef NTT_CL_LOG
 #define NTT_CL_LOG 13
@@ -148,7 +152,7 @@ constexpr Sched make_sched(int logl) {
             const int rem = logl - 2 * ke, mid = P - 2;
             const bool ok = mid == 0 ? rem == 0 : (rem >= mid && rem <= mid * KMAX);
             if (!ok) continue;
-            const int mn = mid == 0 ? ke : (rem / mid < ke ? rem / mid : ke);
+            const int mn = NTT_PREFER_END ? ke : (mid == 0 ? ke : (rem / mid < ke ? rem / mid : ke));
             if (mn > best_min) {
                 best_min = mn;
                 best_ke = ke;
@@ -333,6 +337,7 @@ struct NttArgs {
     int col0;           // first column of this launch (sharded phases)
     int row0, row_end;  // rows [row0, row_end) of this launch
     uint32_t pinv;      // p^-1 mod 2^32 (Montgomery REDC of the pointwise product)
+    bool vec_in[2];     // operand rows 16-byte aligned (vector loads in K1)
 };
 
 // K1 (OUT = false) and K3 (OUT = true): the column transforms of a tile of C
@@ -355,73 +360,101 @@ __global__ void __launch_bounds__(Geo<LOGL, LOGC, 0>::T, NTT_MINB) ntt_cols(NttA
     const int64_t inst = blockIdx.z;
     const int c0 = g.col0 + blockIdx.x * GE::C;
     const uint2* tw = P.r1;
+    // End passes: each thread owns V units of consecutive columns (same u),
+    // so a row segment of V words moves as one vector access.
+    constexpr int V = (NU % 4 == 0 && GE::C >= 4) ? 4 : ((NU % 2 == 0 && GE::C >= 2) ? 2 : 1);
+    constexpr int NG = NU / V;
+    using VecT = typename std::conditional<V == 4, uint4, typename std::conditional<V == 2, uint2, uint32_t>::type>::type;
     uint32_t v[NU][P0::R];
     // first pass: global -> registers
     if constexpr (!OUT) {
         const int64_t len = g.len[op];
+        const bool vec_ok = g.vec_in[op];
 #pragma unroll
-        for (int n = 0; n < NU; ++n) {
-            const int x = threadIdx.x + n * T;
-            const int c = P0::c_of(x), u = P0::u_of(x);
+        for (int gi = 0; gi < NG; ++gi) {
+            const int xb = V * (threadIdx.x + gi * T);
+            const int c = P0::c_of(xb), u = P0::u_of(xb);
             const uint32_t* in = g.in[op] + inst * g.ld[op] + (c0 + c + u * N2);
-            // element j at in[j*UR*N2] (immediate offsets); zero past len
+            // element j of the group at in[j*UR*N2 + i] (immediate offsets); zero past len
             const int64_t lim64 = len - (c0 + c + int64_t(u) * N2);
             const int lim = lim64 < 0 ? 0 : (lim64 > (1 << 30) ? (1 << 30) : int(lim64));
 #pragma unroll
-            for (int j = 0; j < P0::R; ++j)
-                v[n][j] = j * P0::UR * N2 < lim ? __ldg(in + j * P0::UR * N2) : 0u;
+            for (int j = 0; j < P0::R; ++j) {
+                const int o = j * P0::UR * N2;
+                if (V > 1 && vec_ok && o + V <= lim) {
+                    const VecT t = __ldg(reinterpret_cast<const VecT*>(in + o));
+#pragma unroll
+                    for (int i = 0; i < V; ++i) v[gi * V + i][j] = reinterpret_cast<const uint32_t*>(&t)[i];
+                } else {
+#pragma unroll
+                    for (int i = 0; i < V; ++i) v[gi * V + i][j] = o + i < lim ? __ldg(in + o + i) : 0u;
+                }
+            }
         }
     } else {
         const uint32_t* work = g.work[0] + (inst << P.logN);
 #pragma unroll
-        for (int n = 0; n < NU; ++n) {
-            const int x = threadIdx.x + n * T;
-            const uint32_t* w = work + (c0 + P0::c_of(x) + P0::u_of(x) * N2);
+        for (int gi = 0; gi < NG; ++gi) {
+            const int xb = V * (threadIdx.x + gi * T);
+            const uint32_t* w = work + (c0 + P0::c_of(xb) + P0::u_of(xb) * N2);
 #pragma unroll
-            for (int j = 0; j < P0::R; ++j) v[n][j] = __ldg(w + j * P0::UR * N2);
+            for (int j = 0; j < P0::R; ++j) {
+                const VecT t = __ldg(reinterpret_cast<const VecT*>(w + j * P0::UR * N2));
+#pragma unroll
+                for (int i = 0; i < V; ++i) v[gi * V + i][j] = reinterpret_cast<const uint32_t*>(&t)[i];
+            }
         }
     }
 #pragma unroll
     for (int n = 0; n < NU; ++n)
-        radix<LOGL, 0, P0::K, LZ>(v[n], P0::u_of(threadIdx.x + n * T), tw, p);
+        radix<LOGL, 0, P0::K, LZ>(v[n], P0::u_of(V * (threadIdx.x + (n / V) * T)), tw, p);
     if constexpr (GE::P > 1) {
 #pragma unroll
-        for (int n = 0; n < NU; ++n) sts_unit<P0>(sm, threadIdx.x + n * T, v[n]);
+        for (int n = 0; n < NU; ++n) sts_unit<P0>(sm, V * (threadIdx.x + (n / V) * T) + n % V, v[n]);
         __syncthreads();
         uint32_t* const bufs[1] = {sm};
         mid_passes<GE, T, 1, 1, LZ>(bufs, tw, p);
 #pragma unroll
         for (int n = 0; n < NU; ++n) {
-            const int x = threadIdx.x + n * T;
-            lds_unit<PL>(sm, x, v[n]);
+            lds_unit<PL>(sm, V * (threadIdx.x + (n / V) * T) + n % V, v[n]);
             radix<LOGL, PL::S, PL::K, LZ>(v[n], 0, tw, p);
         }
     }
     // last pass: registers -> global; output b of unit (c, u) is point u + b*L/R
     const int N = 1 << P.logN;
 #pragma unroll
-    for (int n = 0; n < NU; ++n) {
-        const int x = threadIdx.x + n * T;
-        const int c = PL::c_of(x), u = PL::u_of(x);
+    for (int gi = 0; gi < NG; ++gi) {
+        const int xb = V * (threadIdx.x + gi * T);
+        const int cb = PL::c_of(xb), u = PL::u_of(xb);
         if constexpr (!OUT) {
-            uint32_t* work = g.work[op] + (inst << P.logN) + (c0 + c + u * N2);
+            uint32_t* work = g.work[op] + (inst << P.logN) + (c0 + cb + u * N2);
             const uint2* hi = op == 0 ? P.thi : P.thi_s;
-            const uint32_t e0 = uint32_t(c0 + c) * uint32_t(u), de = uint32_t(c0 + c) * PL::UR;
 #pragma unroll
-            for (int b = 0; b < PL::R; ++b)  // k1 = u + b*UR, twiddle w_N^(n2*k1)
-                work[b * PL::UR * N2] = twiddle<LZ>(v[n][b], e0 + b * de, P.tlo, hi, p);
+            for (int b = 0; b < PL::R; ++b) {  // k1 = u + b*UR, twiddle w_N^(n2*k1)
+                VecT t;
+#pragma unroll
+                for (int i = 0; i < V; ++i) {
+                    const uint32_t n2 = uint32_t(c0 + cb + i);
+                    reinterpret_cast<uint32_t*>(&t)[i] =
+                        twiddle<LZ>(v[gi * V + i][b], n2 * uint32_t(u + b * PL::UR), P.tlo, hi, p);
+                }
+                *reinterpret_cast<VecT*>(work + b * PL::UR * N2) = t;
+            }
         } else {
-            // m = N2*(u + b*UR) + c0 + c  ->  f[(N - m) mod N]; only m == 0 wraps
-            const int m0 = N2 * u + c0 + c;
             const int64_t nf = g.nf;
-            uint32_t* out = g.out + inst * g.ldf + (N - m0);
 #pragma unroll
-            for (int b = 0; b < PL::R; ++b) {
-                const int nidx = N - m0 - b * PL::UR * N2;
-                if (m0 == 0 && b == 0)
-                    g.out[inst * g.ldf] = canon(v[n][b], p);
-                else if (nidx < nf)
-                    out[-b * PL::UR * N2] = canon(v[n][b], p);
+            for (int i = 0; i < V; ++i) {
+                // m = N2*(u + b*UR) + c0 + c  ->  f[(N - m) mod N]; only m == 0 wraps
+                const int m0 = N2 * u + c0 + cb + i;
+                uint32_t* out = g.out + inst * g.ldf + (N - m0);
+#pragma unroll
+                for (int b = 0; b < PL::R; ++b) {
+                    const int nidx = N - m0 - b * PL::UR * N2;
+                    if (m0 == 0 && b == 0)
+                        g.out[inst * g.ldf] = canon(v[gi * V + i][b], p);
+                    else if (nidx < nf)
+                        out[-b * PL::UR * N2] = canon(v[gi * V + i][b], p);
+                }
             }
         }
     }
@@ -710,6 +743,8 @@ void run_ntt_launches(NttArgs g, int64_t count, int64_t chunk, const uint32_t* A
         const unsigned c = unsigned(std::min<int64_t>(chunk, count - c0));
         g.in[0] = A + c0 * lda;
         g.in[1] = B + c0 * ldb;
+        g.vec_in[0] = (reinterpret_cast<uintptr_t>(g.in[0]) % 16 == 0) && (lda % 4 == 0 || c == 1);
+        g.vec_in[1] = (reinterpret_cast<uintptr_t>(g.in[1]) % 16 == 0) && (ldb % 4 == 0 || c == 1);
         g.ld[0] = lda;
         g.ld[1] = ldb;
         g.out = Fo + c0 * ldf;
@@ -791,6 +826,8 @@ void launch_ntt_phase(const FieldParams& F, int phase, const uint32_t* a, int64_
     NttArgs g = base_args(P, nf);
     g.in[0] = a;
     g.in[1] = b;
+    g.vec_in[0] = reinterpret_cast<uintptr_t>(a) % 16 == 0;
+    g.vec_in[1] = reinterpret_cast<uintptr_t>(b) % 16 == 0;
     g.len[0] = na;
     g.len[1] = nb;
     g.ld[0] = na;
