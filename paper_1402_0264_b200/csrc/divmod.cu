@@ -261,9 +261,12 @@ __global__ void __launch_bounds__(DIV_T) div_grid_kernel(DivArgs g, int64_t seg)
 #define PIPE_CONV(x) x
 #endif
 constexpr int PIPE_L = 2;      // bulk lag (steps) the head absorbs
-constexpr int PIPE_CT = 256;    // compute threads of the head (8 warps)
+#ifndef DIV_PIPE_CT
+#define DIV_PIPE_CT 256
+#endif
+constexpr int PIPE_CT = DIV_PIPE_CT;  // compute threads of the head (8 warps)
 constexpr int PIPE_T = PIPE_CT + 32;  // + the head's control warp
-constexpr int PIPE_B = 256;     // positions per bulk block
+constexpr int PIPE_B = PIPE_CT;       // positions per bulk block
 constexpr int PIPE_MAXB = 4;    // steps per bulk pass
 
 struct PipeArgs {

@@ -132,6 +132,68 @@ def test_ntt_matches_plain(cuda_lib, port):
             assert np.array_equal(mmm.ntt_mul(a, b, p), port.mul(a, b, p)), (p, na, nb)
 
 
+def _eval_mod(poly, x, p, chunk=1 << 12):
+    """poly(x) mod p, vectorised: chunk dot products against x^j, Horner over chunks."""
+    poly = np.asarray(poly, dtype=np.int64)
+    pw = np.empty(chunk, dtype=np.int64)
+    v = 1
+    for j in range(chunk):
+        pw[j] = v
+        v = v * x % p
+    X = v  # x^chunk
+    n = -(-len(poly) // chunk) * chunk
+    padded = np.zeros(n, dtype=np.int64)
+    padded[: len(poly)] = poly
+    rows = padded.reshape(-1, chunk)
+    acc = 0
+    for lo in range(rows.shape[0] - 1, -1, -256):  # top chunks first
+        blk = rows[max(0, lo - 255): lo + 1]
+        inner = ((blk * pw) % p).sum(axis=1) % p
+        for val in inner[::-1]:
+            acc = (acc * X + int(val)) % p
+    return acc
+
+
+def test_ntt_every_length(cuda_lib):
+    """Every transform length the NTT supports (N = 2^2 .. 2^26: every column /
+    row template instantiation, both row-length parities) for a lazy prime
+    (< 2^30) and an exact one (> 2^30): bit-exact against the GPU schoolbook
+    product (itself pinned to the reference) up to N = 2^14, Schwartz-Zippel
+    evaluation at two points beyond."""
+    mmm = cuda_lib
+    rng = np.random.default_rng(26)
+    for p in (469762049, 2013265921):
+        for logn in range(2, 27):
+            n = 1 << logn
+            na = n // 2 if logn % 2 else n // 2 - 3
+            nb = n - na  # na + nb - 1 = n - 1 -> transform length n
+            a = rng.integers(0, p, max(na, 1)).astype(np.uint32)
+            b = rng.integers(0, p, max(nb, 1)).astype(np.uint32)
+            a[-1] = b[-1] = 1
+            f = mmm.ntt_mul(a, b, p)
+            if logn <= 14:
+                assert np.array_equal(f, mmm.mul(a, b, p)), (p, logn)
+            else:
+                assert len(f) == len(a) + len(b) - 1, (p, logn)
+                for x in (rng.integers(2, p), rng.integers(2, p)):
+                    x = int(x)
+                    assert _eval_mod(f, x, p) == _eval_mod(a, x, p) * _eval_mod(b, x, p) % p, (p, logn)
+
+
+def test_ntt_batched_unaligned_rows(cuda_lib):
+    """Batched NTT products whose rows are not 16-byte aligned (odd leading
+    dimension: the column kernel's scalar-load path) equal the single products."""
+    mmm = cuda_lib
+    rng = np.random.default_rng(27)
+    for na, nb in ((1001, 999), (4097, 31), (3, 2)):
+        A = rng.integers(0, P, (5, na)).astype(np.uint32)
+        B = rng.integers(0, P, (5, nb)).astype(np.uint32)
+        F = mmm.ntt_mul_batched(A, B, P)
+        for i in range(5):
+            want = mmm.mul(A[i], B[i], P)
+            assert np.array_equal(np.trim_zeros(F[i].astype(np.int64), "b"), want), (na, nb, i)
+
+
 def test_ntt_rejects_unsupported_prime(cuda_lib):
     with pytest.raises(cuda_lib.InvalidArgument):
         cuda_lib.ntt_mul([1, 2, 3], [4, 5], 7)
