@@ -19,3 +19,16 @@ for w in gcd mul div ntt ntt_batch batch; do
   timeout 600 ncu --set full --import-source on --clock-control none -k regex:$k -c $c -o $O/full_$w python tools/prof_one.py $w --reps 1 > $O/ncu_$w.log 2>&1
   tail -1 $O/ncu_$w.log
 done
+# Summarise on the box (gpurun copies back at most 64 MiB): per-kernel metric
+# CSVs, a brief with stall samples and the source page of each capture; then
+# drop the largest reports until the directory fits.
+python tools/ncu_summary.py $O $O/sum > /dev/null 2>&1
+for r in $O/full_*.ncu-rep; do
+  python tools/ncu_brief.py $r > ${r%.ncu-rep}_brief.txt 2>&1
+  ncu -i $r --page source --csv --print-source cuda > ${r%.ncu-rep}_src.csv 2>/dev/null
+done
+gzip -f $O/*_src.csv
+for r in $(ls -S $O/full_*.ncu-rep); do
+  [ $(du -sm gpurun_out | cut -f1) -lt 56 ] && break
+  rm -f $r
+done
