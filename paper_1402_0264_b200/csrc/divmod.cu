@@ -261,6 +261,9 @@ __global__ void __launch_bounds__(DIV_T) div_grid_kernel(DivArgs g, int64_t seg)
 #define PIPE_CONV(x) x
 #endif
 constexpr int PIPE_L = 2;      // bulk lag (steps) the head absorbs
+#ifndef DIV_PIPE_SPLIT
+#define DIV_PIPE_SPLIT 1       // 1: pipe_head_split (entering off the critical path)
+#endif
 #ifndef DIV_PIPE_CT
 #define DIV_PIPE_CT 256
 #endif
@@ -282,6 +285,7 @@ struct PipeArgs {
     unsigned* published;    // steps whose lambdas are in q
     unsigned* progress;     // per bulk CTA: steps applied to all of its blocks
     long long* stats;       // optional (MMM_DIV_STATS): cycle counters
+    bool b_smem;            // bulk CTAs hold all of b in shared memory
 };
 
 namespace {
@@ -289,8 +293,29 @@ namespace {
 __device__ __forceinline__ void bar_sync_n(int id, int n) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
+__device__ __forceinline__ void bar_arrive_n(int id, int n) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+// Publishing after a CTA barrier: the barrier orders the CTA's writes before
+// the publishing thread's release store, which is cumulative at gpu scope
+// (the pattern of CUTLASS's semaphore release).  A __threadfence() before it
+// compiles to MEMBAR.SC.GPU (~1 us measured); DIV_PIPE_SCFENCE=1 restores it.
+#ifndef DIV_PIPE_SCFENCE
+#define DIV_PIPE_SCFENCE 0
+#endif
+__device__ __forceinline__ void pipe_sc_fence() {
+#if DIV_PIPE_SCFENCE
+    __threadfence();
+#endif
+}
 __device__ __forceinline__ void pipe_st_release(unsigned* p, unsigned v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Origin of h in the head's zero-padded copy: a lambda part reads up to
+// SPANL - 1 + 3 words below it (SPANL <= max(64, S / 2)).
+__host__ __device__ constexpr int pipe_horg(int S) {
+    return ((S / 2 + 3) & ~3) + 3 > 67 ? ((S / 2 + 3) & ~3) + 3 : 67;
 }
 
 // i(k): the top of step k's heads (db - 1 once all steps are done)
@@ -324,8 +349,9 @@ __device__ __forceinline__ void quad_reduce(uint64_t (&acc)[4], int P, uint32_t 
 // terms for the quad's 4 outputs; store(t, v) receives output t < 4*NQ.
 template <class Item, class Store>
 __device__ __forceinline__ void tiled_sum(int NQ, int P, uint32_t* red, Item item, Store store,
-                                          const FieldParams& F, int nthreads, int barid) {
-    const int tid = threadIdx.x, NO = 4 * NQ;
+                                          const FieldParams& F, int nthreads, int barid,
+                                          int tid) {
+    const int NO = 4 * NQ;
     for (int it = tid; it < NQ * P; it += nthreads) {
         const int part = it / NQ, qd = it - part * NQ;
         uint64_t acc[4] = {0, 0, 0, 0};
@@ -352,7 +378,7 @@ __device__ void pipe_head(const PipeArgs& g, uint32_t* sm, int nbulk) {
     const int64_t J = (na - db + S - 1) / S;
     const bool control = tid >= CT;  // warp 8: publish, poll owners, stage entering words
     // shared layout (16-byte aligned pieces)
-    const int horg = ((S / 4 + 3) & ~3) + 3 > 67 ? ((S / 4 + 3) & ~3) + 3 : 67;
+    const int horg = pipe_horg(S);
     uint32_t* hz = sm;                                   // h at hz[horg + m]
     uint32_t* hd = hz + ((horg + S + 8 + 3) & ~3);      // heads, S words
     uint32_t* lamh = hd + S;                             // L x S negated lambdas
@@ -407,7 +433,7 @@ __device__ void pipe_head(const PipeArgs& g, uint32_t* sm, int nbulk) {
             bar_sync_n(2, PIPE_T);  // lambdas of step j written
             const long long c0 = clock64();
             if ((tid & 31) == 0) {
-                __threadfence();
+                pipe_sc_fence();
                 pipe_st_release(g.published, unsigned(j + 1));
             }
             const long long c1 = clock64();
@@ -433,7 +459,7 @@ __device__ void pipe_head(const PipeArgs& g, uint32_t* sm, int nbulk) {
                 if (k < v) g.q[i - db - k] = lam;
                 lamh[(j % L) * S + k] = k < v ? negmod(lam, F) : 0u;
             },
-            F, CT, 1);
+            F, CT, 1, tid);
         const long long pa = clock64();
         bar_sync_n(2, PIPE_T);  // with the control warp: publish step j
         const long long p1 = clock64();
@@ -463,7 +489,7 @@ __device__ void pipe_head(const PipeArgs& g, uint32_t* sm, int nbulk) {
                         *w = addmod(*w, add, F);
                     }
                 },
-                F, CT, 1);
+                F, CT, 1, tid);
             const uint32_t* st = stage + (j & 1) * S;
             for (int u = tid; u < v; u += CT) {  // t = WH + u, x = i - WH - u
                 const int64_t x = i - WH - u;
@@ -503,7 +529,7 @@ __device__ void pipe_head(const PipeArgs& g, uint32_t* sm, int nbulk) {
                         *w = addmod(*w, add, F);
                     }
                 },
-                F, CT, 1);
+                F, CT, 1, tid);
         }
         bar_sync_n(1, CT);
         c_ent += clock64() - p2;
@@ -529,6 +555,232 @@ __device__ void pipe_head(const PipeArgs& g, uint32_t* sm, int nbulk) {
     }
 }
 
+// pipe_head_split: the same head with its compute warps in two groups, so the
+// entering update leaves the per-step critical path.  Step j's lambdas need
+// the heads (window [0, S) after step j-1); the window update of step j
+// (positions [v, 2S)) feeds step j+1's heads; the entering words of step j
+// (positions [2S, 2S + v), steps j-1 and j on top of the bulk's) are needed
+// only by step j+1's window update.  Group A (DIV_PIPE_AW warps) runs
+// lambda -> window; group B (the other compute warps) runs entering_j
+// concurrently with A's window_j and lambda_{j+1}.  Hand-offs are named
+// barriers with arrive (producer) / sync (consumer), by step parity:
+//   LAM(j): A's lambda_j written        -> B and the control warp
+//   ENT(j): B's entering_j in the window -> A, before window_{j+1}
+//   STG(j): control staged E_j          -> B
+// The lambda history is a ring of L + 1 steps (B reads j-1 and j while A
+// writes j+1).  Same arithmetic, same result as pipe_head.
+#ifndef DIV_PIPE_AW
+#define DIV_PIPE_AW 4
+#endif
+__device__ void pipe_head_split(const PipeArgs& g, uint32_t* sm, int nbulk) {
+    constexpr int L = PIPE_L, LR = PIPE_L + 1, CT = PIPE_CT;
+    constexpr int AT = 32 * DIV_PIPE_AW, BT = CT - AT;
+    static_assert(L == 2 && AT > 0 && BT > 0, "pipe_head_split: L = 2, both groups non-empty");
+    constexpr int BAR_A = 1, BAR_B = 2, BAR_LAM = 3, BAR_ENT = 5, BAR_STG = 7;
+    const FieldParams F = g.F;
+    const int S = g.S, tid = threadIdx.x, WH = 2 * S, WR = 4 * S;
+    const int logS = 31 - __clz(S);
+    const int64_t na = g.na, db = g.nb - 1;
+    const int64_t J = (na - db + S - 1) / S;
+    const bool control = tid >= CT, groupA = tid < AT;
+    const int horg = pipe_horg(S);
+    uint32_t* hz = sm;                                   // h at hz[horg + m]
+    uint32_t* hd = hz + ((horg + S + 8 + 3) & ~3);      // heads, S words
+    uint32_t* lamh = hd + S;                             // LR x S negated lambdas
+    uint32_t* win = lamh + LR * S;                       // ring by absolute position
+    uint32_t* stage = win + WR;                          // 2 x S entering words
+    uint32_t* bt3 = stage + 2 * S;                       // bt3[3 + m] = b[db - m]
+    const int MB = (L + 2) * S + 16;
+    uint32_t* redA = bt3 + ((MB + 3) & ~3);              // tiled_sum partials, 4 * AT words
+    uint32_t* redB = redA + 4 * AT;                      // 4 * BT words
+    for (int m = tid; m < horg + S + 8; m += PIPE_T) {
+        const int j = m - horg;
+        hz[m] = (j >= 0 && j < S) ? __ldcg(g.h_glob + j) : 0u;
+    }
+    for (int m = tid; m < MB; m += PIPE_T) {
+        const int64_t x = db - (m - 3);
+        bt3[m] = (m >= 3 && x >= 0) ? g.b[x] : 0u;
+    }
+    for (int m = tid; m < LR * S; m += PIPE_T) lamh[m] = 0u;
+    const int64_t i0 = na - 1;
+    for (int t = tid; t < WH; t += PIPE_T) {
+        const int64_t x = i0 - t;
+        win[x & (WR - 1)] = x >= 0 ? __ldcg(g.A + x) : 0u;
+    }
+    long long c_poll = 0;
+    auto stage_entering = [&](int64_t jj) {
+        const int64_t hi = pipe_i(na, db, S, jj) - WH, lo = pipe_i(na, db, S, jj + 1) - WH + 1;
+        if (hi < 0 || hi < lo) return;
+        const int lane = tid & 31;
+        const int64_t need = jj - L + 1;
+        if (lane < 2 && need > 0) {
+            const int64_t x = lane == 0 ? (lo > 0 ? lo : 0) : hi;
+            const int owner = int((x / PIPE_B) % nbulk);
+            const long long cp = clock64();
+            spin_until_geq_fence(g.progress + owner, unsigned(need));
+#ifdef PIPE_DBG_FAKE_POLL  // timing experiments only (tools/head_bench.cu): a bulk round trip
+            while (clock64() - cp < PIPE_DBG_FAKE_POLL) {
+            }
+#endif
+            c_poll += clock64() - cp;
+        }
+        __syncwarp();
+        uint32_t* st = stage + (jj & 1) * S;
+        for (int64_t x = lo + lane; x <= hi; x += 32) st[x - lo] = x >= 0 ? __ldcg(g.A + x) : 0u;
+    };
+    if (control) stage_entering(0);
+    __syncthreads();
+    long long c_loop = clock64(), c_pub = 0, c_stage = 0, c_lam = 0, c_win = 0, c_ent = 0,
+              c_wait = 0;
+    if (control) {
+        for (int64_t j = 0; j < J; ++j) {
+            bar_sync_n(BAR_LAM + int(j & 1), PIPE_T);  // lambdas of step j written
+            const long long c0 = clock64();
+            if ((tid & 31) == 0) {
+                pipe_sc_fence();
+                pipe_st_release(g.published, unsigned(j + 1));
+            }
+            const long long c1 = clock64();
+            if (j + 1 < J) {
+                stage_entering(j + 1);
+                bar_arrive_n(BAR_STG + int((j + 1) & 1), BT + 32);
+            }
+            c_pub += c1 - c0;
+            c_stage += clock64() - c1;
+        }
+    } else if (groupA) {
+        int PL = 1;  // lambda tiling: S/4 quads x PL parts over the S head terms
+        while ((S / 4) * PL * 2 <= AT && PL * 2 <= S / 4) PL *= 2;
+        const int SPANL = S / PL;
+        for (int64_t j = 0; j < J; ++j) {
+            const int64_t i = pipe_i(na, db, S, j), inext = pipe_i(na, db, S, j + 1);
+            const int v = int(i - inext);
+            const long long p0 = clock64();
+            for (int t = tid; t < S; t += AT) hd[t] = t < v ? win[(i - t) & (WR - 1)] : 0u;
+            bar_sync_n(BAR_A, AT);
+            uint32_t* lj = lamh + int(j % LR) * S;
+            tiled_sum(
+                S / 4, PL, redA,
+                [&](int qd, int part, uint64_t (&acc)[4]) {
+                    const int k0 = 4 * qd, t0 = part * SPANL;
+                    uint32_t since = 0;
+                    if (t0 <= k0 + 3)
+                        PIPE_CONV(conv_accumulate4_fast(acc, hd + t0, SPANL / 4, hz, horg + k0 - t0,
+                                                        since, F));
+                },
+                [&](int k, uint32_t lam) {
+                    if (k < v) g.q[i - db - k] = lam;
+                    lj[k] = k < v ? negmod(lam, F) : 0u;
+                },
+                F, AT, BAR_A, tid);
+            bar_arrive_n(BAR_LAM + int(j & 1), PIPE_T);
+            const long long p1 = clock64();
+            c_lam += p1 - p0;
+            if (j >= 1) bar_sync_n(BAR_ENT + int((j - 1) & 1), CT);  // E_{j-1} complete
+            const long long p2 = clock64();
+            c_wait += p2 - p1;
+            // window (t in [v, WH)): step j
+            const int tq = v & ~3, NQ = (WH - tq) >> 2, vp = (v + 3) & ~3;
+            int P = 1;
+            while (NQ * P * 2 <= AT && (S / (P * 2)) >= 4 && ((S / (P * 2)) & 3) == 0) P *= 2;
+            const int SPAN = S / P;
+            tiled_sum(
+                NQ, P, redA,
+                [&](int qd, int part, uint64_t (&acc)[4]) {
+                    const int t0 = tq + 4 * qd, k0 = part * SPAN;
+                    uint32_t since = 0;
+                    if (k0 < vp)
+                        PIPE_CONV(conv_accumulate4_fast(acc, lj + k0, min(SPAN, vp - k0) / 4, bt3,
+                                                        t0 - k0 + 3, since, F));
+                },
+                [&](int tt, uint32_t add) {
+                    const int t = tq + tt;
+                    const int64_t x = i - t;
+                    if (t >= v && t < WH && x >= 0) {
+                        uint32_t* w = win + (x & (WR - 1));
+                        *w = addmod(*w, add, F);
+                    }
+                },
+                F, AT, BAR_A, tid);
+            bar_sync_n(BAR_A, AT);
+            c_win += clock64() - p2;
+        }
+        if (J >= 1) bar_sync_n(BAR_ENT + int((J - 1) & 1), CT);  // the last entering words
+    } else {
+        const int tb = tid - AT;
+        for (int64_t j = 0; j < J; ++j) {
+            const int64_t i = pipe_i(na, db, S, j), inext = pipe_i(na, db, S, j + 1);
+            const int v = int(i - inext);
+            const long long p0 = clock64();
+            bar_sync_n(BAR_LAM + int(j & 1), PIPE_T);                // lambda_j
+            if (j >= 1) bar_sync_n(BAR_STG + int(j & 1), BT + 32);  // E_j staged
+            const long long p1 = clock64();
+            c_wait += p1 - p0;
+            // entering (t in [WH, WH + v)): stage + steps j - 1 .. j
+            const uint32_t* st = stage + (j & 1) * S;
+            const int NQ = (v + 3) >> 2, TT = L * S;
+            int P = 1;
+            while (NQ * P * 2 <= BT && (TT / (P * 2)) >= 4 && ((TT / (P * 2)) & 3) == 0) P *= 2;
+            const int SPAN = TT / P;
+            tiled_sum(
+                NQ, P, redB,
+                [&](int qd, int part, uint64_t (&acc)[4]) {
+                    const int t0 = WH + 4 * qd;
+                    uint32_t since = 0;
+                    for (int c0 = part * SPAN; c0 < (part + 1) * SPAN;) {
+                        const int d = c0 >> logS, k0 = c0 & (S - 1);
+                        const int n = min(S - k0, (part + 1) * SPAN - c0);
+                        const int lim = d == 0 ? ((v + 3) & ~3) : S;
+                        if (j - d >= 0 && k0 < lim)
+                            PIPE_CONV(conv_accumulate4_fast(acc, lamh + int((j - d) % LR) * S + k0,
+                                                            min(n, lim - k0) / 4, bt3,
+                                                            t0 + d * S - k0 + 3, since, F));
+                        c0 += n;
+                    }
+                },
+                [&](int tt, uint32_t add) {
+                    const int t = WH + tt;
+                    const int64_t x = i - t;
+                    if (tt < v && x >= 0) win[x & (WR - 1)] = addmod(st[v - 1 - tt], add, F);
+                },
+                F, BT, BAR_B, tb);
+            bar_arrive_n(BAR_ENT + int(j & 1), CT);
+            c_ent += clock64() - p1;
+        }
+    }
+    if (g.stats && tid == 0) {
+        g.stats[0] = J;
+        g.stats[1] = clock64() - c_loop;
+        g.stats[8] = c_lam;
+        g.stats[9] = c_win;
+        g.stats[11] = c_wait;
+    }
+    if (g.stats && tid == AT) {
+        g.stats[10] = c_ent;
+        g.stats[3] = c_wait;
+    }
+    if (g.stats && tid == CT) {
+        g.stats[2] = c_pub;
+        g.stats[4] = c_poll;
+    }
+    (void)c_stage;
+    __syncthreads();
+    for (int t = tid; t < WH; t += PIPE_T) {
+        const int64_t x = (db - 1) - t;
+        if (x >= 0) __stcg(g.A + x, win[x & (WR - 1)]);
+    }
+}
+
+// Bulk shared layout (words): lam [PIPE_MAXB * S + 4] | bw [PIPE_B + S + 8,
+// padded] | bz [nb + 2 * PIPE_PADB] when the whole divisor fits (g.b_smem):
+// bz[PIPE_PADB + x] = b[x], zero outside [0, db], loaded once per launch, so
+// a step's b window is a shared-memory copy instead of an L2 round trip.
+constexpr int PIPE_PADB = PIPE_B + 264;
+__host__ __device__ constexpr int64_t pipe_bulk_words(int S, int64_t nb, bool b_smem) {
+    return int64_t(PIPE_MAXB) * S + 4 + ((PIPE_B + S + 8 + 3) & ~3) +
+           (b_smem ? nb + 2 * PIPE_PADB : 0);
+}
+
 __device__ void pipe_bulk(const PipeArgs& g, uint32_t* sm, int nbulk, int me) {
     constexpr int L = PIPE_L;
     const FieldParams F = g.F;
@@ -536,8 +788,15 @@ __device__ void pipe_bulk(const PipeArgs& g, uint32_t* sm, int nbulk, int me) {
     const int64_t na = g.na, db = g.nb - 1;
     const int64_t J = (na - db + S - 1) / S;
     const int64_t nblocks = (na + PIPE_B - 1) / PIPE_B;  // every position below the heads
-    uint32_t* lam = sm;               // reversed negated lambdas of one step, S words
-    uint32_t* bw = lam + S + 4;       // b window: PIPE_B + S + 8 words
+    uint32_t* lam = sm;                          // per step of the pass: S reversed negated lambdas
+    uint32_t* bw = lam + PIPE_MAXB * S + 4;      // b window: PIPE_B + S + 8 words
+    uint32_t* bz = bw + ((PIPE_B + S + 8 + 3) & ~3);
+    const bool b_smem = g.b_smem;
+    if (b_smem)
+        for (int64_t y = tid; y < g.nb + 2 * PIPE_PADB; y += PIPE_T) {
+            const int64_t x = y - PIPE_PADB;
+            bz[y] = (x >= 0 && x <= db) ? __ldcg(g.b + x) : 0u;
+        }
     __shared__ unsigned pub_s;
     // 4 positions per thread, 4 parts over the step's terms: PIPE_B/4 x 4 = the
     // first PIPE_B threads (whole warps; the ninth warp only stages and syncs)
@@ -554,9 +813,22 @@ __device__ void pipe_bulk(const PipeArgs& g, uint32_t* sm, int nbulk, int me) {
         c_wait += tb - tw;
         ++passes;
         const int64_t kend = min(int64_t(pub_s), k + int64_t(PIPE_MAXB));
+        // the pass's lambdas, once for all blocks: lam[(kk - k) * S + u] = nl_{v-1-u}
+        for (int64_t kk = k; kk < kend; ++kk) {
+            const int64_t ik = pipe_i(na, db, S, kk);
+            const int v = int(ik - pipe_i(na, db, S, kk + 1)), vp = (v + 3) & ~3;
+            uint32_t* lk = lam + (kk - k) * S;
+            for (int u = tid; u < vp; u += PIPE_T) {
+                const int kp = v - 1 - u;
+                lk[u] = kp >= 0 ? negmod(__ldcg(g.q + (ik - db - kp)), F) : 0u;
+            }
+        }
         for (int64_t beta = me; beta < nblocks; beta += nbulk) {
             const int64_t blo = beta * PIPE_B, bhi = min(blo + int64_t(PIPE_B), na);
             const int64_t x0 = blo + 4 * qd;
+            const int64_t x = x0 + part;
+            // this thread's stored position, loaded ahead: only this CTA writes it
+            const uint32_t a_old = (worker && x < bhi) ? __ldcg(g.A + x) : 0u;
             uint64_t acc[4] = {0, 0, 0, 0};  // sum of per-step canonical partials
             bool touched = false, mine = false;  // mine: x0 + part got a step (store it)
             for (int64_t kk = k; kk < kend; ++kk) {
@@ -566,17 +838,17 @@ __device__ void pipe_bulk(const PipeArgs& g, uint32_t* sm, int nbulk, int me) {
                 const int64_t top = min(pipe_i(na, db, S, kk + L) - int64_t(WH), ik - v);
                 if (bhi - 1 < xlo || blo > top) continue;  // uniform over the CTA
                 touched = true;
-                if (x0 + part >= xlo && x0 + part <= top) mine = true;
+                if (x >= xlo && x <= top) mine = true;
                 const int vp = int((v + 3) & ~3);
-                __syncthreads();  // previous step's staging consumed
-                for (int u = tid; u < vp; u += PIPE_T) {  // lam[u] = nl_{v-1-u}
-                    const int64_t kp = v - 1 - u;
-                    lam[u] = kp >= 0 ? negmod(__ldcg(g.q + (ik - db - kp)), F) : 0u;
-                }
+                __syncthreads();  // previous step's window consumed (and the pass's lambdas in)
                 const int64_t bwlo = blo - ik + db + v - vp;  // bw[y] = b[bwlo + y]
-                for (int y = tid; y < PIPE_B + vp + 8; y += PIPE_T) {
-                    const int64_t bx = bwlo + y;
-                    bw[y] = (bx >= 0 && bx <= db) ? __ldcg(g.b + bx) : 0u;
+                if (b_smem) {
+                    for (int y = tid; y < PIPE_B + vp + 8; y += PIPE_T) bw[y] = bz[PIPE_PADB + bwlo + y];
+                } else {
+                    for (int y = tid; y < PIPE_B + vp + 8; y += PIPE_T) {
+                        const int64_t bx = bwlo + y;
+                        bw[y] = (bx >= 0 && bx <= db) ? __ldcg(g.b + bx) : 0u;
+                    }
                 }
                 __syncthreads();
                 // part's terms: [u0, u0 + n), multiples of 4
@@ -585,12 +857,12 @@ __device__ void pipe_bulk(const PipeArgs& g, uint32_t* sm, int nbulk, int me) {
                 if (worker && u0 < vp) {
                     uint64_t pa[4] = {0, 0, 0, 0};
                     uint32_t since = 0;
-                    conv_accumulate4_fast(pa, lam + u0, min(span, vp - u0) / 4, bw,
-                                       4 * qd + vp - 1 - u0, since, F);
+                    conv_accumulate4_fast(pa, lam + (kk - k) * S + u0, min(span, vp - u0) / 4, bw,
+                                          4 * qd + vp - 1 - u0, since, F);
 #pragma unroll
                     for (int r = 0; r < 4; ++r) {
-                        const int64_t x = x0 + r;
-                        if (x >= xlo && x <= top && x < bhi) acc[r] += reduce(pa[r], F);
+                        const int64_t xr = x0 + r;
+                        if (xr >= xlo && xr <= top && xr < bhi) acc[r] += reduce(pa[r], F);
                     }
                 }
             }
@@ -600,12 +872,11 @@ __device__ void pipe_bulk(const PipeArgs& g, uint32_t* sm, int nbulk, int me) {
             const uint32_t ad = part == 0 ? add[0] : part == 1 ? add[1] : part == 2 ? add[2] : add[3];
             // store only positions a step updated: the rest may belong to the
             // head, whose final window must not be overwritten by a late pass
-            const int64_t x = x0 + part;
-            if (mine && x < bhi) __stcg(g.A + x, addmod(__ldcg(g.A + x), ad, F));
+            if (mine && x < bhi) __stcg(g.A + x, addmod(a_old, ad, F));
         }
         __syncthreads();
         if (tid == 0) {
-            __threadfence();
+            pipe_sc_fence();
             pipe_st_release(g.progress + me, unsigned(kend));
         }
         c_work += clock64() - tb;
@@ -631,7 +902,11 @@ __global__ void __launch_bounds__(PIPE_T, 1) div_pipe_kernel(PipeArgs g) {
     grid.sync();
     const int nbulk = gridDim.x - 1;
     if (blockIdx.x == 0)
+#if DIV_PIPE_SPLIT
+        pipe_head_split(g, smem, nbulk);
+#else
         pipe_head(g, smem, nbulk);
+#endif
     else
         pipe_bulk(g, smem, nbulk, blockIdx.x - 1);
     grid.sync();
@@ -716,10 +991,11 @@ void run_pipe(const DivArgs& d, int64_t s, cudaStream_t st) {
     g.S = S;
     g.F = d.F;
     const int L = PIPE_L;
-    const int horg = std::max(((S / 4 + 3) & ~3) + 3, 67);
+    const int horg = pipe_horg(S);
     const size_t head =
-        size_t(((horg + S + 8 + 3) & ~3) + S + L * S + 4 * S + 2 * S + (L + 2) * S + 16 + 4 * PIPE_CT);
-    const size_t bulk = size_t(S + 4 + PIPE_B + S + 8 + 8);
+        size_t(((horg + S + 8 + 3) & ~3) + S + (L + 1) * S + 4 * S + 2 * S + (L + 2) * S + 16 + 4 * PIPE_CT);
+    g.b_smem = pipe_bulk_words(S, d.nb, true) * 4 <= 220 * 1024 && !getenv("MMM_DIV_BULK_GLOBAL_B");
+    const size_t bulk = size_t(pipe_bulk_words(S, d.nb, g.b_smem));
     // more than half an SM's shared memory: one CTA per SM, so no bulk CTA
     // shares (and takes issue slots from) the head's SM
     const size_t bytes = std::max<size_t>(std::max(head, bulk) * 4, 120 * 1024);
@@ -751,7 +1027,7 @@ void run_pipe(const DivArgs& d, int64_t s, cudaStream_t st) {
         MMM_CUDA(cudaStreamSynchronize(st));
         fprintf(stderr,
                 "div pipe stats: S=%d blocks=%d steps=%lld head_loop=%lld ctl_publish=%lld "
-                "ctl_stage=%lld (poll=%lld) | hd+lambda=%lld (waitA=%lld) window=%lld "
+                "ctl_stage|B_wait=%lld (poll=%lld) | hd+lambda=%lld (waitA=%lld) window=%lld "
                 "entering=%lld | bulk0 wait=%lld work=%lld passes=%lld\n",
                 S, blocks, h[0], h[1], h[2], h[3], h[4], h[8], h[11], h[9], h[10], h[5], h[6],
                 h[7]);

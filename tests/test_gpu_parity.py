@@ -424,6 +424,24 @@ def test_division_pipelined_shapes(cuda_lib, port, p):
             assert np.array_equal(q, wq) and np.array_equal(r, wr), (p, na, nb, s)
 
 
+@pytest.mark.parametrize("env", ["MMM_DIV_BULK_GLOBAL_B", "MMM_DIV_GRID"])
+def test_division_schedule_fallbacks(cuda_lib, port, env, monkeypatch):
+    """The pipelined division with the divisor read from L2 per step (the path
+    of divisors too large for the bulk CTAs' shared memory) and the grid
+    schedule: the same (q, r) as the oracle."""
+    monkeypatch.setenv(env, "1")
+    rng = np.random.default_rng(77)
+    for na, nb in [(12000, 6000), (9001, 700)]:
+        a = rng.integers(0, P, na)
+        b = rng.integers(0, P, nb)
+        a[-1] = max(a[-1], 1)
+        b[-1] = max(b[-1], 1)
+        wq, wr = port.divmod(a, b, P)
+        for s in (32, 128, 256):
+            q, r = cuda_lib.divmod(a, b, P, s=s)
+            assert np.array_equal(q, wq) and np.array_equal(r, wr), (env, na, nb, s)
+
+
 # ------------------------------------------------------ sharded four-step NTT --
 def test_ntt_sharded_virtual_ranks(cuda_lib, port):
     """The sharded NTT product (phase kernels over column/row slices, block

@@ -11,9 +11,11 @@ for v in 0 1; do
   done
 done
 cat $O/head_bench.jsonl
-timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "division or cfg3 or frozen or suite" > $O/pytest_div.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "division or cfg3 or frozen or suite or fallback" > $O/pytest_div.log 2>&1
 tail -2 $O/pytest_div.log
 MMM_DIV_STATS=1 timeout 120 python tools/prof_one.py div --reps 1 > $O/stats_div.log 2>&1
 tail -3 $O/stats_div.log
 timeout 300 python bench.py --workload div --steps 10 --warmup 3 > $O/bench_div.log 2>&1
 tail -1 $O/bench_div.log | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print("div ms", d["ms_per_step"], "e2e ms", d["e2e"]["ms_per_step"], d["clocks"])'
+MMM_DIV_STATS=1 MMM_DIV_BULK_GLOBAL_B=1 timeout 120 python tools/prof_one.py div --reps 1 > $O/stats_div_globalb.log 2>&1
+tail -2 $O/stats_div_globalb.log

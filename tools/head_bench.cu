@@ -18,7 +18,11 @@ __global__ void __launch_bounds__(PIPE_T, 1) head_only(PipeArgs g) {
         inverse_series(g.h_glob, g.S, g.nb - 1,
                        [&](int64_t t) { return t <= g.nb - 1 ? g.b[g.nb - 1 - t] : 0u; }, g.F);
     __syncthreads();
+#if DIV_PIPE_SPLIT
+    pipe_head_split(g, smem, 1);
+#else
     pipe_head(g, smem, 1);
+#endif
 }
 
 int main(int argc, char** argv) {
@@ -57,9 +61,11 @@ int main(int argc, char** argv) {
         cudaError_t e = cudaDeviceSynchronize();
         if (rep == 1)
             printf("{\"S\": %d, \"steps\": %lld, \"loop\": %lld, \"per_step\": %.0f, \"lambda\": %.0f, "
-                   "\"window\": %.0f, \"entering\": %.0f, \"err\": \"%s\"}\n", S, st[0], st[1],
+                   "\"window\": %.0f, \"entering\": %.0f, \"waitA\": %.0f, \"waitB\": %.0f, "
+                   "\"split\": %d, \"err\": \"%s\"}\n", S, st[0], st[1],
                    double(st[1]) / st[0], double(st[8]) / st[0], double(st[9]) / st[0],
-                   double(st[10]) / st[0], cudaGetErrorString(e));
+                   double(st[10]) / st[0], double(st[11]) / st[0], double(st[3]) / st[0],
+                   DIV_PIPE_SPLIT, cudaGetErrorString(e));
     }
     return 0;
 }
