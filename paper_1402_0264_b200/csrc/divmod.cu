@@ -260,14 +260,17 @@ __global__ void __launch_bounds__(DIV_T) div_grid_kernel(DivArgs g, int64_t seg)
 #else
 #define PIPE_CONV(x) x
 #endif
-constexpr int PIPE_L = 2;      // bulk lag (steps) the head absorbs
+#ifndef DIV_PIPE_L
+#define DIV_PIPE_L 4
+#endif
+constexpr int PIPE_L = DIV_PIPE_L;  // bulk lag (steps) the head absorbs
 #ifndef DIV_PIPE_SPLIT
 #define DIV_PIPE_SPLIT 1       // 1: pipe_head_split (entering off the critical path)
 #endif
 #ifndef DIV_PIPE_CT
-#define DIV_PIPE_CT 256
+#define DIV_PIPE_CT 384
 #endif
-constexpr int PIPE_CT = DIV_PIPE_CT;  // compute threads of the head (8 warps)
+constexpr int PIPE_CT = DIV_PIPE_CT;  // compute threads of the head (12 warps: A 4, B 8)
 constexpr int PIPE_T = PIPE_CT + 32;  // + the head's control warp
 constexpr int PIPE_B = PIPE_CT;       // positions per bulk block
 constexpr int PIPE_MAXB = 4;    // steps per bulk pass
@@ -575,7 +578,7 @@ __device__ void pipe_head(const PipeArgs& g, uint32_t* sm, int nbulk) {
 __device__ void pipe_head_split(const PipeArgs& g, uint32_t* sm, int nbulk) {
     constexpr int L = PIPE_L, LR = PIPE_L + 1, CT = PIPE_CT;
     constexpr int AT = 32 * DIV_PIPE_AW, BT = CT - AT;
-    static_assert(L == 2 && AT > 0 && BT > 0, "pipe_head_split: L = 2, both groups non-empty");
+    static_assert(L >= 1 && AT > 0 && BT > 0, "pipe_head_split: both groups non-empty");
     constexpr int BAR_A = 1, BAR_B = 2, BAR_LAM = 3, BAR_ENT = 5, BAR_STG = 7;
     const FieldParams F = g.F;
     const int S = g.S, tid = threadIdx.x, WH = 2 * S, WR = 4 * S;
@@ -781,6 +784,19 @@ __host__ __device__ constexpr int64_t pipe_bulk_words(int S, int64_t nb, bool b_
            (b_smem ? nb + 2 * PIPE_PADB : 0);
 }
 
+constexpr int PIPE_HS_OFF = 16384;  // head: h computed here (words; the head layout ends below)
+
+__device__ void pipe_bulk_load_b(const PipeArgs& g, uint32_t* sm) {
+    if (!g.b_smem) return;
+    uint32_t* bz = sm + PIPE_MAXB * g.S + 4 + ((PIPE_B + g.S + 8 + 3) & ~3);
+    const int64_t n = g.nb + 2 * PIPE_PADB, db = g.nb - 1;
+#pragma unroll 8
+    for (int64_t y = threadIdx.x; y < n; y += PIPE_T) {
+        const int64_t x = y - PIPE_PADB;
+        bz[y] = (x >= 0 && x <= db) ? __ldcg(g.b + x) : 0u;
+    }
+}
+
 __device__ void pipe_bulk(const PipeArgs& g, uint32_t* sm, int nbulk, int me) {
     constexpr int L = PIPE_L;
     const FieldParams F = g.F;
@@ -791,12 +807,7 @@ __device__ void pipe_bulk(const PipeArgs& g, uint32_t* sm, int nbulk, int me) {
     uint32_t* lam = sm;                          // per step of the pass: S reversed negated lambdas
     uint32_t* bw = lam + PIPE_MAXB * S + 4;      // b window: PIPE_B + S + 8 words
     uint32_t* bz = bw + ((PIPE_B + S + 8 + 3) & ~3);
-    const bool b_smem = g.b_smem;
-    if (b_smem)
-        for (int64_t y = tid; y < g.nb + 2 * PIPE_PADB; y += PIPE_T) {
-            const int64_t x = y - PIPE_PADB;
-            bz[y] = (x >= 0 && x <= db) ? __ldcg(g.b + x) : 0u;
-        }
+    const bool b_smem = g.b_smem;  // bz loaded by pipe_bulk_load_b before the grid barrier
     __shared__ unsigned pub_s;
     // 4 positions per thread, 4 parts over the step's terms: PIPE_B/4 x 4 = the
     // first PIPE_B threads (whole warps; the ninth warp only stages and syncs)
@@ -896,9 +907,17 @@ __global__ void __launch_bounds__(PIPE_T, 1) div_pipe_kernel(PipeArgs g) {
     for (int64_t i = int64_t(blockIdx.x) * PIPE_T + threadIdx.x; i < na;
          i += int64_t(gridDim.x) * PIPE_T)
         g.A[i] = g.a[i];
-    if (blockIdx.x == 0 && threadIdx.x < 32)
-        inverse_series(g.h_glob, g.S, db,
+    // Before the grid barrier: the head's warp 0 computes h in shared memory
+    // (each coefficient reads the earlier ones: an L2 round trip apiece if h
+    // lived in global memory) and publishes it; the bulk CTAs load b.
+    if (blockIdx.x == 0 && threadIdx.x < 32) {
+        uint32_t* hs = smem + PIPE_HS_OFF;
+        inverse_series(hs, g.S, db,
                        [&](int64_t t) { return t <= db ? __ldcg(g.b + (db - t)) : 0u; }, g.F);
+        for (int t = threadIdx.x; t < g.S; t += 32) g.h_glob[t] = hs[t];
+    } else if (blockIdx.x > 0) {
+        pipe_bulk_load_b(g, smem);
+    }
     grid.sync();
     const int nbulk = gridDim.x - 1;
     if (blockIdx.x == 0)
@@ -998,7 +1017,8 @@ void run_pipe(const DivArgs& d, int64_t s, cudaStream_t st) {
     const size_t bulk = size_t(pipe_bulk_words(S, d.nb, g.b_smem));
     // more than half an SM's shared memory: one CTA per SM, so no bulk CTA
     // shares (and takes issue slots from) the head's SM
-    const size_t bytes = std::max<size_t>(std::max(head, bulk) * 4, 120 * 1024);
+    const size_t bytes = std::max<size_t>(std::max(std::max(head, bulk), size_t(PIPE_HS_OFF + S)) * 4,
+                                          120 * 1024);
     MMM_CUDA(cudaFuncSetAttribute(div_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(bytes)));
     int per_sm = 0;
