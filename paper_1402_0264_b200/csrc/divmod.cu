@@ -247,7 +247,7 @@ __global__ void __launch_bounds__(DIV_T) div_grid_kernel(DivArgs g, int64_t seg)
 // to different positions at different times.  CTA 0 (head) keeps the top
 // WH = 2S positions of A in shared memory, computes each step's lambdas from
 // its window (split-K tiled convolution with h = rev(b)^-1), publishes them
-// as the quotient words (q) with a release flag, updates its window and the
+// as tagged words (lam_t: no flag, no fence), updates its window and the
 // S positions entering it, then slides.  Entering positions come from global
 // A, where the bulk CTAs have applied every step up to j - L; the head adds
 // the last L steps from its lambda history.  Bulk CTAs own fixed blocks of
@@ -264,9 +264,6 @@ __global__ void __launch_bounds__(DIV_T) div_grid_kernel(DivArgs g, int64_t seg)
 #define DIV_PIPE_L 4
 #endif
 constexpr int PIPE_L = DIV_PIPE_L;  // bulk lag (steps) the head absorbs
-#ifndef DIV_PIPE_SPLIT
-#define DIV_PIPE_SPLIT 1       // 1: pipe_head_split (entering off the critical path)
-#endif
 #ifndef DIV_PIPE_CT
 #define DIV_PIPE_CT 384
 #endif
@@ -285,7 +282,7 @@ struct PipeArgs {
     FieldParams F;
     uint32_t* A;            // working copy of the dividend (L2 resident)
     uint32_t* h_glob;       // inverse series (S words)
-    unsigned* published;    // steps whose lambdas are in q
+    uint64_t* lam_t;        // step k's negated lambdas, tagged (k + 1) << 32 | value: J * S words
     unsigned* progress;     // per bulk CTA: steps applied to all of its blocks
     long long* stats;       // optional (MMM_DIV_STATS): cycle counters
     bool b_smem;            // bulk CTAs hold all of b in shared memory
@@ -298,6 +295,25 @@ __device__ __forceinline__ void bar_sync_n(int id, int n) {
 }
 __device__ __forceinline__ void bar_arrive_n(int id, int n) {
     asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+// Tagged words (tag << 32 | value), single-copy-atomic 64-bit relaxed accesses:
+// a reader polls the word it needs until it carries the expected tag, so the
+// lambdas reach the bulk CTAs with no flag and no fence (a release store on the
+// head's SM measured ~8k cycles).
+__device__ __forceinline__ void pipe_st_tag(uint64_t* p, uint32_t v, unsigned tag) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"((uint64_t(tag) << 32) | v)
+                 : "memory");
+}
+__device__ __forceinline__ uint64_t pipe_ld_rlx64(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint32_t pipe_ld_tag(const uint64_t* p, unsigned tag) {
+    uint64_t w;
+    while (unsigned((w = pipe_ld_rlx64(p)) >> 32) != tag) {
+    }
+    return uint32_t(w);
 }
 // Publishing after a CTA barrier: the barrier orders the CTA's writes before
 // the publishing thread's release store, which is cumulative at gpu scope
@@ -372,192 +388,6 @@ __device__ __forceinline__ void tiled_sum(int NQ, int P, uint32_t* red, Item ite
 
 }  // namespace
 
-__device__ void pipe_head(const PipeArgs& g, uint32_t* sm, int nbulk) {
-    constexpr int L = PIPE_L, CT = PIPE_CT;
-    const FieldParams F = g.F;
-    const int S = g.S, tid = threadIdx.x, WH = 2 * S, WR = 4 * S;  // ring size (pow2 >= 3S)
-    const int logS = 31 - __clz(S);
-    const int64_t na = g.na, db = g.nb - 1;
-    const int64_t J = (na - db + S - 1) / S;
-    const bool control = tid >= CT;  // warp 8: publish, poll owners, stage entering words
-    // shared layout (16-byte aligned pieces)
-    const int horg = pipe_horg(S);
-    uint32_t* hz = sm;                                   // h at hz[horg + m]
-    uint32_t* hd = hz + ((horg + S + 8 + 3) & ~3);      // heads, S words
-    uint32_t* lamh = hd + S;                             // L x S negated lambdas
-    uint32_t* win = lamh + L * S;                        // ring by absolute position
-    uint32_t* stage = win + WR;                          // 2 x S entering words
-    uint32_t* bt3 = stage + 2 * S;                       // bt3[3 + m] = b[db - m]
-    const int MB = (L + 2) * S + 16;
-    uint32_t* red = bt3 + ((MB + 3) & ~3);               // tiled_sum partials, 4 * CT words
-    for (int m = tid; m < horg + S + 8; m += PIPE_T) {
-        const int j = m - horg;
-        hz[m] = (j >= 0 && j < S) ? __ldcg(g.h_glob + j) : 0u;
-    }
-    for (int m = tid; m < MB; m += PIPE_T) {
-        const int64_t x = db - (m - 3);
-        bt3[m] = (m >= 3 && x >= 0) ? g.b[x] : 0u;
-    }
-    for (int m = tid; m < L * S; m += PIPE_T) lamh[m] = 0u;
-    const int64_t i0 = na - 1;
-    for (int t = tid; t < WH; t += PIPE_T) {  // initial window: positions i0 - t
-        const int64_t x = i0 - t;
-        win[x & (WR - 1)] = x >= 0 ? __ldcg(g.A + x) : 0u;
-    }
-    // entering words of slide j: [i(j+1) - WH + 1, i(j) - WH], loaded by the
-    // control warp one step ahead once their bulk owners applied steps <= j-L
-    long long c_poll = 0, c_waitA = 0;
-    auto stage_entering = [&](int64_t jj) {
-        const int64_t hi = pipe_i(na, db, S, jj) - WH, lo = pipe_i(na, db, S, jj + 1) - WH + 1;
-        if (hi < 0 || hi < lo) return;
-        const int lane = tid & 31;
-        const int64_t need = jj - L + 1;
-        if (lane < 2 && need > 0) {
-            const int64_t x = lane == 0 ? (lo > 0 ? lo : 0) : hi;
-            const int owner = int((x / PIPE_B) % nbulk);
-            const long long cp = clock64();
-            spin_until_geq_fence(g.progress + owner, unsigned(need));
-            c_poll += clock64() - cp;
-        }
-        __syncwarp();
-        uint32_t* st = stage + (jj & 1) * S;
-        for (int64_t x = lo + lane; x <= hi; x += 32) st[x - lo] = x >= 0 ? __ldcg(g.A + x) : 0u;
-    };
-    if (control) stage_entering(0);
-    __syncthreads();
-    // lambda tiling: S/4 quads x PL parts over the S head terms
-    const int PL = (S / 4) < (1024 / S) ? (S / 4) : (1024 / S);
-    const int logPL = 31 - __clz(PL), SPANL = S / PL;
-    long long c_loop = clock64(), c_pub = 0, c_stage = 0, c_lam = 0, c_win = 0, c_ent = 0;
-    for (int64_t j = 0; j < J; ++j) {
-        const int64_t i = pipe_i(na, db, S, j), inext = pipe_i(na, db, S, j + 1);
-        const int v = int(i - inext);
-        if (control) {
-            bar_sync_n(2, PIPE_T);  // lambdas of step j written
-            const long long c0 = clock64();
-            if ((tid & 31) == 0) {
-                pipe_sc_fence();
-                pipe_st_release(g.published, unsigned(j + 1));
-            }
-            const long long c1 = clock64();
-            stage_entering(j + 1);
-            c_pub += c1 - c0;
-            c_stage += clock64() - c1;
-            continue;
-        }
-        const long long p0 = clock64();
-        for (int t = tid; t < S; t += CT) hd[t] = t < v ? win[(i - t) & (WR - 1)] : 0u;
-        bar_sync_n(1, CT);
-        // lambda_k = sum_{t<=k} h[k-t] * hd[t], k < v
-        tiled_sum(
-            S / 4, PL, red,
-            [&](int qd, int part, uint64_t (&acc)[4]) {
-                const int k0 = 4 * qd, t0 = part * SPANL;
-                uint32_t since = 0;
-                if (t0 <= k0 + 3)
-                    PIPE_CONV(conv_accumulate4_fast(acc, hd + t0, SPANL / 4, hz, horg + k0 - t0, since,
-                                                 F));
-            },
-            [&](int k, uint32_t lam) {
-                if (k < v) g.q[i - db - k] = lam;
-                lamh[(j % L) * S + k] = k < v ? negmod(lam, F) : 0u;
-            },
-            F, CT, 1, tid);
-        const long long pa = clock64();
-        bar_sync_n(2, PIPE_T);  // with the control warp: publish step j
-        const long long p1 = clock64();
-        c_waitA += p1 - pa;
-        c_lam += p1 - p0;
-        // window (t in [v, WH)): step j; entering words copied in from the stage
-        {
-            const int tq = v & ~3, NQ = (WH - tq) >> 2, vp = (v + 3) & ~3;
-            int P = 1;
-            while (NQ * P * 2 <= CT && (S / (P * 2)) >= 4 && ((S / (P * 2)) & 3) == 0) P *= 2;
-            const int SPAN = S / P;
-            tiled_sum(
-                NQ, P, red,
-                [&](int qd, int part, uint64_t (&acc)[4]) {
-                    const int t0 = tq + 4 * qd, k0 = part * SPAN;
-                    uint32_t since = 0;
-                    if (k0 < vp)
-                        PIPE_CONV(conv_accumulate4_fast(acc, lamh + (j % L) * S + k0,
-                                                     min(SPAN, vp - k0) / 4, bt3, t0 - k0 + 3,
-                                                     since, F));
-                },
-                [&](int tt, uint32_t add) {
-                    const int t = tq + tt;
-                    const int64_t x = i - t;
-                    if (t >= v && t < WH && x >= 0) {
-                        uint32_t* w = win + (x & (WR - 1));
-                        *w = addmod(*w, add, F);
-                    }
-                },
-                F, CT, 1, tid);
-            const uint32_t* st = stage + (j & 1) * S;
-            for (int u = tid; u < v; u += CT) {  // t = WH + u, x = i - WH - u
-                const int64_t x = i - WH - u;
-                if (x >= 0) win[x & (WR - 1)] = st[(i - WH - (inext - WH + 1)) - u];
-            }
-        }
-        bar_sync_n(1, CT);
-        const long long p2 = clock64();
-        c_win += p2 - p1;
-        // entering (t in [WH, WH + v)): steps j - L + 1 .. j
-        {
-            const int NQ = (v + 3) >> 2, TT = L * S;
-            int P = 1;
-            while (NQ * P * 2 <= CT && (TT / (P * 2)) >= 4 && ((TT / (P * 2)) & 3) == 0) P *= 2;
-            const int SPAN = TT / P;
-            tiled_sum(
-                NQ, P, red,
-                [&](int qd, int part, uint64_t (&acc)[4]) {
-                    const int t0 = WH + 4 * qd;
-                    uint32_t since = 0;
-                    for (int c0 = part * SPAN; c0 < (part + 1) * SPAN;) {
-                        const int d = c0 >> logS, k0 = c0 & (S - 1);
-                        const int n = min(S - k0, (part + 1) * SPAN - c0);
-                        const int lim = d == 0 ? ((v + 3) & ~3) : S;
-                        if (j - d >= 0 && k0 < lim)
-                            PIPE_CONV(conv_accumulate4_fast(acc, lamh + ((j - d) % L) * S + k0,
-                                                         min(n, lim - k0) / 4, bt3,
-                                                         t0 + d * S - k0 + 3, since, F));
-                        c0 += n;
-                    }
-                },
-                [&](int tt, uint32_t add) {
-                    const int t = WH + tt;
-                    const int64_t x = i - t;
-                    if (t < WH + v && x >= 0) {
-                        uint32_t* w = win + (x & (WR - 1));
-                        *w = addmod(*w, add, F);
-                    }
-                },
-                F, CT, 1, tid);
-        }
-        bar_sync_n(1, CT);
-        c_ent += clock64() - p2;
-    }
-    if (g.stats && tid == 0) {
-        g.stats[0] = J;
-        g.stats[1] = clock64() - c_loop;
-        g.stats[8] = c_lam;
-        g.stats[9] = c_win;
-        g.stats[10] = c_ent;
-        g.stats[11] = c_waitA;
-    }
-    if (g.stats && tid == CT) {
-        g.stats[2] = c_pub;
-        g.stats[3] = c_stage;
-        g.stats[4] = c_poll;
-    }
-    // the final window holds the top of the remainder
-    __syncthreads();
-    for (int t = tid; t < WH; t += PIPE_T) {
-        const int64_t x = (db - 1) - t;
-        if (x >= 0) __stcg(g.A + x, win[x & (WR - 1)]);
-    }
-}
-
 // pipe_head_split: the same head with its compute warps in two groups, so the
 // entering update leaves the per-step critical path.  Step j's lambdas need
 // the heads (window [0, S) after step j-1); the window update of step j
@@ -620,7 +450,7 @@ __device__ void pipe_head_split(const PipeArgs& g, uint32_t* sm, int nbulk) {
             const int64_t x = lane == 0 ? (lo > 0 ? lo : 0) : hi;
             const int owner = int((x / PIPE_B) % nbulk);
             const long long cp = clock64();
-            spin_until_geq_fence(g.progress + owner, unsigned(need));
+            spin_until_geq(g.progress + owner, unsigned(need));  // acquire load, no MEMBAR
 #ifdef PIPE_DBG_FAKE_POLL  // timing experiments only (tools/head_bench.cu): a bulk round trip
             while (clock64() - cp < PIPE_DBG_FAKE_POLL) {
             }
@@ -637,18 +467,12 @@ __device__ void pipe_head_split(const PipeArgs& g, uint32_t* sm, int nbulk) {
               c_wait = 0;
     if (control) {
         for (int64_t j = 0; j < J; ++j) {
-            bar_sync_n(BAR_LAM + int(j & 1), PIPE_T);  // lambdas of step j written
-            const long long c0 = clock64();
-            if ((tid & 31) == 0) {
-                pipe_sc_fence();
-                pipe_st_release(g.published, unsigned(j + 1));
-            }
+            bar_sync_n(BAR_LAM + int(j & 1), PIPE_T);
             const long long c1 = clock64();
             if (j + 1 < J) {
                 stage_entering(j + 1);
                 bar_arrive_n(BAR_STG + int((j + 1) & 1), BT + 32);
             }
-            c_pub += c1 - c0;
             c_stage += clock64() - c1;
         }
     } else if (groupA) {
@@ -672,8 +496,12 @@ __device__ void pipe_head_split(const PipeArgs& g, uint32_t* sm, int nbulk) {
                                                         since, F));
                 },
                 [&](int k, uint32_t lam) {
-                    if (k < v) g.q[i - db - k] = lam;
-                    lj[k] = k < v ? negmod(lam, F) : 0u;
+                    const uint32_t nl = k < v ? negmod(lam, F) : 0u;
+                    if (k < v) {
+                        g.q[i - db - k] = lam;
+                        pipe_st_tag(g.lam_t + j * S + k, nl, unsigned(j + 1));
+                    }
+                    lj[k] = nl;
                 },
                 F, AT, BAR_A, tid);
             bar_arrive_n(BAR_LAM + int(j & 1), PIPE_T);
@@ -763,10 +591,10 @@ __device__ void pipe_head_split(const PipeArgs& g, uint32_t* sm, int nbulk) {
         g.stats[3] = c_wait;
     }
     if (g.stats && tid == CT) {
-        g.stats[2] = c_pub;
+        g.stats[2] = c_stage;
         g.stats[4] = c_poll;
     }
-    (void)c_stage;
+    (void)c_pub;
     __syncthreads();
     for (int t = tid; t < WH; t += PIPE_T) {
         const int64_t x = (db - 1) - t;
@@ -818,7 +646,14 @@ __device__ void pipe_bulk(const PipeArgs& g, uint32_t* sm, int nbulk, int me) {
     int64_t k = 0;
     while (k < J) {
         const long long tw = clock64();
-        if (tid == 0) pub_s = spin_until_geq_fence(g.published, unsigned(k) + 1u);
+        if (tid == 0) {  // step k's first lambda carries its tag; later steps: no wait
+            pipe_ld_tag(g.lam_t + k * S, unsigned(k + 1));
+            int64_t e = k + 1;
+            while (e < J && e < k + PIPE_MAXB &&
+                   unsigned(pipe_ld_rlx64(g.lam_t + e * S) >> 32) == unsigned(e + 1))
+                ++e;
+            pub_s = unsigned(e);
+        }
         __syncthreads();
         const long long tb = clock64();
         c_wait += tb - tw;
@@ -831,7 +666,7 @@ __device__ void pipe_bulk(const PipeArgs& g, uint32_t* sm, int nbulk, int me) {
             uint32_t* lk = lam + (kk - k) * S;
             for (int u = tid; u < vp; u += PIPE_T) {
                 const int kp = v - 1 - u;
-                lk[u] = kp >= 0 ? negmod(__ldcg(g.q + (ik - db - kp)), F) : 0u;
+                lk[u] = kp >= 0 ? pipe_ld_tag(g.lam_t + kk * S + kp, unsigned(kk + 1)) : 0u;
             }
         }
         for (int64_t beta = me; beta < nblocks; beta += nbulk) {
@@ -921,11 +756,7 @@ __global__ void __launch_bounds__(PIPE_T, 1) div_pipe_kernel(PipeArgs g) {
     grid.sync();
     const int nbulk = gridDim.x - 1;
     if (blockIdx.x == 0)
-#if DIV_PIPE_SPLIT
         pipe_head_split(g, smem, nbulk);
-#else
-        pipe_head(g, smem, nbulk);
-#endif
     else
         pipe_bulk(g, smem, nbulk, blockIdx.x - 1);
     grid.sync();
@@ -1029,9 +860,11 @@ void run_pipe(const DivArgs& d, int64_t s, cudaStream_t st) {
     Scratch sc(st);
     g.A = sc.get<uint32_t>(size_t(d.na));
     g.h_glob = sc.get<uint32_t>(size_t(S));
-    g.published = sc.get<unsigned>(size_t(blocks) + 1);
-    g.progress = g.published + 1;
-    MMM_CUDA(cudaMemsetAsync(g.published, 0, (size_t(blocks) + 1) * sizeof(unsigned), st));
+    g.progress = sc.get<unsigned>(size_t(blocks));
+    MMM_CUDA(cudaMemsetAsync(g.progress, 0, size_t(blocks) * sizeof(unsigned), st));
+    const int64_t J = (d.na - (d.nb - 1) + S - 1) / S;
+    g.lam_t = sc.get<uint64_t>(size_t(J) * S);  // tags start at 1: zeroed words never match
+    MMM_CUDA(cudaMemsetAsync(g.lam_t, 0, size_t(J) * S * sizeof(uint64_t), st));
     const bool want_stats = getenv("MMM_DIV_STATS") != nullptr;
     if (want_stats) {
         g.stats = sc.get<long long>(12);
@@ -1046,8 +879,8 @@ void run_pipe(const DivArgs& d, int64_t s, cudaStream_t st) {
         MMM_CUDA(cudaMemcpyAsync(h, g.stats, sizeof(h), cudaMemcpyDeviceToHost, st));
         MMM_CUDA(cudaStreamSynchronize(st));
         fprintf(stderr,
-                "div pipe stats: S=%d blocks=%d steps=%lld head_loop=%lld ctl_publish=%lld "
-                "ctl_stage|B_wait=%lld (poll=%lld) | hd+lambda=%lld (waitA=%lld) window=%lld "
+                "div pipe stats: S=%d blocks=%d steps=%lld head_loop=%lld ctl_stage=%lld "
+                "B_wait=%lld (ctl poll=%lld) | hd+lambda=%lld (waitA=%lld) window=%lld "
                 "entering=%lld | bulk0 wait=%lld work=%lld passes=%lld\n",
                 S, blocks, h[0], h[1], h[2], h[3], h[4], h[8], h[11], h[9], h[10], h[5], h[6],
                 h[7]);

@@ -18,11 +18,7 @@ __global__ void __launch_bounds__(PIPE_T, 1) head_only(PipeArgs g) {
         inverse_series(g.h_glob, g.S, g.nb - 1,
                        [&](int64_t t) { return t <= g.nb - 1 ? g.b[g.nb - 1 - t] : 0u; }, g.F);
     __syncthreads();
-#if DIV_PIPE_SPLIT
     pipe_head_split(g, smem, 1);
-#else
-    pipe_head(g, smem, 1);
-#endif
 }
 
 int main(int argc, char** argv) {
@@ -52,7 +48,9 @@ int main(int argc, char** argv) {
     flags[1] = 1u << 30;  // progress of the single fake bulk owner: always ahead
     PipeArgs g{};
     g.a = a; g.b = b; g.q = q; g.r = nullptr; g.na = na; g.nb = nb; g.S = S; g.F = F;
-    g.A = A; g.h_glob = h; g.published = flags; g.progress = flags + 1; g.stats = st;
+    uint64_t* lam_t;
+    cudaMalloc(&lam_t, size_t(na) * 8);
+    g.A = A; g.h_glob = h; g.lam_t = lam_t; g.progress = flags + 1; g.stats = st;
     const size_t bytes = 64 * 1024;
     cudaFuncSetAttribute(head_only, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
     for (int rep = 0; rep < 2; ++rep) {
@@ -62,10 +60,10 @@ int main(int argc, char** argv) {
         if (rep == 1)
             printf("{\"S\": %d, \"steps\": %lld, \"loop\": %lld, \"per_step\": %.0f, \"lambda\": %.0f, "
                    "\"window\": %.0f, \"entering\": %.0f, \"waitA\": %.0f, \"waitB\": %.0f, "
-                   "\"split\": %d, \"err\": \"%s\"}\n", S, st[0], st[1],
+                   "\"err\": \"%s\"}\n", S, st[0], st[1],
                    double(st[1]) / st[0], double(st[8]) / st[0], double(st[9]) / st[0],
                    double(st[10]) / st[0], double(st[11]) / st[0], double(st[3]) / st[0],
-                   DIV_PIPE_SPLIT, cudaGetErrorString(e));
+                   cudaGetErrorString(e));
     }
     return 0;
 }
