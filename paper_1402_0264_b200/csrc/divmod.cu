@@ -261,13 +261,13 @@ __global__ void __launch_bounds__(DIV_T) div_grid_kernel(DivArgs g, int64_t seg)
 #define PIPE_CONV(x) x
 #endif
 #ifndef DIV_PIPE_L
-#define DIV_PIPE_L 4
+#define DIV_PIPE_L 2
 #endif
 constexpr int PIPE_L = DIV_PIPE_L;  // bulk lag (steps) the head absorbs
 #ifndef DIV_PIPE_CT
-#define DIV_PIPE_CT 384
+#define DIV_PIPE_CT 256
 #endif
-constexpr int PIPE_CT = DIV_PIPE_CT;  // compute threads of the head (12 warps: A 4, B 8)
+constexpr int PIPE_CT = DIV_PIPE_CT;  // compute threads of the head (8 warps: A 4, B 4)
 constexpr int PIPE_T = PIPE_CT + 32;  // + the head's control warp
 constexpr int PIPE_B = PIPE_CT;       // positions per bulk block
 constexpr int PIPE_MAXB = 4;    // steps per bulk pass
