@@ -59,9 +59,15 @@ class Dist:
         self.rank = int(os.environ.get("RANK", "0"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
         self.pg = None
-        if self.world > 1 and impl == "ours":
+        # MMM_BENCH_PEER=1: a process group even at N = 1, so the symmetric-memory
+        # fan-out path (PeerOutputs) can be exercised on one GPU
+        if impl == "ours" and (self.world > 1 or os.environ.get("MMM_BENCH_PEER")):
             import torch.distributed as dist
-            dist.init_process_group("nccl", device_id=None)
+            if self.world == 1:
+                os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+                os.environ.setdefault("MASTER_PORT", "29533")
+            dist.init_process_group("nccl", device_id=None, rank=self.rank,
+                                    world_size=self.world)
             self.pg = dist
 
     def max(self, x: float) -> float:
@@ -226,6 +232,44 @@ class Workload:
         raise NotImplementedError
 
 
+def try_peer_outputs(work, sizes):
+    """Sharded workloads at N > 1: every rank's full outputs in symmetric memory
+    (shard.PeerOutputs), written by the fan-out kernels (the all-gather fused
+    into their epilogues).  All ranks fall back to the NCCL gather together if
+    any rank cannot map the buffers; the caller validates one step too."""
+    from paper_1402_0264_b200.shard import PeerOutputs
+    work.peer, work.peer_note = None, ""
+    if work.world == 1 and not (os.environ.get("MMM_BENCH_PEER") and work.dist.pg is not None):
+        return
+    bad = 0.0
+    try:
+        work.peer = PeerOutputs(sizes, work.dist.pg)
+    except Exception as e:  # no symmetric memory on this box: NCCL gather
+        bad, work.peer_note = 1.0, f"symmetric memory unavailable ({type(e).__name__})"
+    if work.dist.max(bad) > 0:
+        work.peer = None
+        work.peer_note = work.peer_note or "a peer could not map symmetric memory"
+
+
+def validate_peer_outputs(work):
+    """One fan-out step, checked on every rank; any mismatch sends all ranks back
+    to the NCCL gather (recorded in config)."""
+    import torch
+    if work.peer is None:
+        return
+    bad = 0.0
+    try:
+        work.device_step(torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        work.dist.barrier()
+        work.device_check()
+    except Exception as e:
+        bad, work.peer_note = 1.0, f"fan-out validation failed ({type(e).__name__})"
+    if work.dist.max(bad) > 0:
+        work.peer = None
+        work.peer_note = work.peer_note or "fan-out validation failed on a peer"
+
+
 class GcdWork(Workload):
     """configs[1]: single-instance Euclidean GCD (replicas only across GPUs)."""
 
@@ -370,7 +414,7 @@ class MulWork(Workload):
         self.L = max(k1 - k0 for k0, k1 in self.ranges)
         if dist.world > 1:
             self.config["parallelism"] = (f"output range sharded by work over {dist.world} ranks "
-                                          "(balanced_output_ranges), NCCL all-gather")
+                                          "(balanced_output_ranges); gather: see config.gather")
             self.config["ranges"] = self.ranges
 
     def units(self):
@@ -382,8 +426,21 @@ class MulWork(Workload):
         self.dloc = torch.zeros(self.L, dtype=torch.int32, device="cuda")
         self.dall = (torch.zeros(self.world * self.L, dtype=torch.int32, device="cuda")
                      if self.world > 1 else self.dloc)
+        try_peer_outputs(self, [self.nf])
+        validate_peer_outputs(self)
+        if self.world > 1 or self.peer is not None:
+            self.config["gather"] = ("fan-out: each rank's range stored into every rank's "
+                                     "symmetric-memory product (NVLink), device barrier"
+                                     if self.peer is not None else
+                                     f"NCCL all-gather of padded slices ({self.peer_note})")
 
     def device_step(self, stream):
+        if getattr(self, "peer", None) is not None:
+            self.mmm.mul_range_fanout_dev(P, self.da.data_ptr(), len(self.a), self.db.data_ptr(),
+                                          len(self.b), self.k0, self.k1,
+                                          self.peer.ptrs(0, self.k0), s=self.s, stream=stream)
+            self.peer.barrier()
+            return
         self.mmm.mul_range_dev(P, self.da.data_ptr(), len(self.a), self.db.data_ptr(),
                                len(self.b), self.k0, self.k1, self.dloc.data_ptr(), s=self.s,
                                stream=stream)
@@ -394,14 +451,19 @@ class MulWork(Workload):
         return np.concatenate([flat[r * self.L: r * self.L + (k1 - k0)]
                                for r, (k0, k1) in enumerate(self.ranges)])
 
+    def _result(self):
+        if getattr(self, "peer", None) is not None:
+            return self.peer.view(0, (self.nf,)).cpu().numpy().view(np.uint32)
+        return self._assemble(self.dall.cpu().numpy().view(np.uint32))
+
     def device_check(self):
-        f = self._assemble(self.dall.cpu().numpy().view(np.uint32))
-        assert digest(f) == self.want, "mul result"
+        assert digest(self._result()) == self.want, "mul result"
 
     def host_setup(self):
         (self.ha, self._ta), (self.hb, self._tb) = _pinned(self.a), _pinned(self.b)
         self.bytes_in = 4 * (len(self.a) + len(self.b))
-        self.bytes_out = 4 * (self.nf if self.world == 1 else self.world * self.L)
+        self.bytes_out = 4 * (self.nf if self.world == 1 or getattr(self, "peer", None) is not None
+                              else self.world * self.L)
 
     def host_step(self):
         if self.world == 1:  # the host C-ABI call a user makes (mmm_cu_mul)
@@ -410,7 +472,7 @@ class MulWork(Workload):
         self.da.copy_(self._ta, non_blocking=True)
         self.db.copy_(self._tb, non_blocking=True)
         self.device_step(torch.cuda.current_stream().cuda_stream)
-        return self._assemble(self.dall.cpu().numpy().view(np.uint32))
+        return self._result()
 
     def host_check(self, f):
         assert digest(f) == self.want
@@ -733,8 +795,8 @@ class BatchWork(_Sharded):
         self.n = self.A.shape[1]
         self.config = {"workload": "cfg5_4096x(4096x4096 mul)+4096x(8192/4096 div)_p469762049",
                        "p": P, "seed": 42, "s_mul": self.s or 8, "s_div": self.s or 64,
-                       "parallelism": "instances sharded across ranks, NCCL all-gather of "
-                       "results", "l2": "inputs 335 MB > L2"}
+                       "parallelism": "instances sharded across ranks; results gathered to "
+                       "every rank (config.gather)", "l2": "inputs 335 MB > L2"}
 
     def units(self):
         n = self.n
@@ -749,9 +811,34 @@ class BatchWork(_Sharded):
         self.dF = torch.zeros((k, 2 * n - 1), dtype=torch.int32, device="cuda")
         self.dQ = torch.zeros((k, n + 1), dtype=torch.int32, device="cuda")
         self.dR = torch.zeros((k, n - 1), dtype=torch.int32, device="cuda")
+        c = self.count
+        try_peer_outputs(self, [c * (2 * n - 1), c * (n + 1), c * (n - 1)])
+        validate_peer_outputs(self)
+        if self.world > 1 or self.peer is not None:
+            self.config["gather"] = ("fan-out: each rank's rows stored into every rank's "
+                                     "symmetric-memory results (NVLink), device barrier"
+                                     if self.peer is not None else
+                                     f"NCCL all-gather ({self.peer_note})")
 
     def device_step(self, stream):
         k, n = self.hi - self.lo, self.n
+        pe = getattr(self, "peer", None)
+        if pe is not None:
+            lo = self.lo
+            self.mmm.mul_batched_fanout_dev(P, self.dA.data_ptr(), n, n, self.dB.data_ptr(), n,
+                                            n, k, pe.ptrs(0, lo * (2 * n - 1)), 2 * n - 1,
+                                            s=self.s or 8, stream=stream)
+            self.mmm.divmod_batched_fanout_dev(P, self.dC.data_ptr(), 2 * n, 2 * n,
+                                               self.dD.data_ptr(), n, n, k,
+                                               pe.ptrs(1, lo * (n + 1)), n + 1,
+                                               pe.ptrs(2, lo * (n - 1)), n - 1,
+                                               s=self.s or 64, stream=stream)
+            pe.barrier()
+            c = self.count
+            self.fullF = pe.view(0, (c, 2 * n - 1))
+            self.fullQ = pe.view(1, (c, n + 1))
+            self.fullR = pe.view(2, (c, n - 1))
+            return
         self.mmm.mul_batched_dev(P, self.dA.data_ptr(), n, n, self.dB.data_ptr(), n, n, k,
                                  self.dF.data_ptr(), 2 * n - 1, s=self.s or 8, stream=stream)
         self.mmm.divmod_batched_dev(P, self.dC.data_ptr(), 2 * n, 2 * n, self.dD.data_ptr(), n,

@@ -151,6 +151,29 @@ int mmm_cu_ntt_mul_batched_dev(int64_t p, const uint32_t* d_A, int64_t lda, int6
                                const uint32_t* d_B, int64_t ldb, int64_t nb, int64_t count,
                                uint32_t* d_F, int64_t ldf, void* stream);
 
+/* Fan-out variants of the sharded entry points.  `d_f` / `d_F` /
+ * `d_Q` / `d_R` are HOST arrays of n_out (1..8) device pointers with the same
+ * layout as the single-output call; every output word is stored into each of
+ * them.  Passing the buffers of every rank (symmetric / IPC-mapped memory, peer
+ * access over NVLink) fuses the all-gather of a sharded product or batch into
+ * the producing kernel's epilogue: rank r's slice or rows land in every rank's
+ * full result with no gather collective.  The caller orders the ranks after the
+ * kernels (a barrier) before reading.  Reference interface replaced: the gather
+ * of results the reference's callers do after run_multiplication / run_division
+ * (bench.cpp:43-64, mmm_cli.cpp:207-221), which have no multi-GPU counterpart. */
+int mmm_cu_mul_range_fanout_dev(int64_t p, const uint32_t* d_a, int64_t na, const uint32_t* d_b,
+                                int64_t nb, int64_t k0, int64_t k1, int64_t s,
+                                uint32_t* const* d_f, int32_t n_out, void* stream);
+int mmm_cu_mul_batched_fanout_dev(int64_t p, const uint32_t* d_A, int64_t lda, int64_t na,
+                                  const uint32_t* d_B, int64_t ldb, int64_t nb, int64_t count,
+                                  int64_t s, uint32_t* const* d_F, int32_t n_out, int64_t ldf,
+                                  void* stream);
+int mmm_cu_divmod_batched_fanout_dev(int64_t p, const uint32_t* d_A, int64_t lda, int64_t na,
+                                     const uint32_t* d_B, int64_t ldb, int64_t nb, int64_t count,
+                                     int64_t s, uint32_t* const* d_Q, int64_t ldq,
+                                     uint32_t* const* d_R, int64_t ldr, int32_t n_out,
+                                     void* stream);
+
 #ifdef __cplusplus
 }
 #endif

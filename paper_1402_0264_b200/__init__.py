@@ -106,6 +106,14 @@ SIGNATURES = {
                                             _VP, _I64, _VP, _I64, _VP]),
     "mmm_cu_ntt_mul_batched_dev": (C.c_int, [_I64, _VP, _I64, _I64, _VP, _I64, _I64, _I64, _VP,
                                              _I64, _VP]),
+    "mmm_cu_mul_range_fanout_dev": (C.c_int, [_I64, _VP, _I64, _VP, _I64, _I64, _I64, _I64,
+                                              C.POINTER(C.c_void_p), C.c_int32, _VP]),
+    "mmm_cu_mul_batched_fanout_dev": (C.c_int, [_I64, _VP, _I64, _I64, _VP, _I64, _I64, _I64,
+                                                _I64, C.POINTER(C.c_void_p), C.c_int32, _I64,
+                                                _VP]),
+    "mmm_cu_divmod_batched_fanout_dev": (C.c_int, [_I64, _VP, _I64, _I64, _VP, _I64, _I64, _I64,
+                                                   _I64, C.POINTER(C.c_void_p), _I64,
+                                                   C.POINTER(C.c_void_p), _I64, C.c_int32, _VP]),
 }
 
 _lib: Optional[C.CDLL] = None
@@ -353,3 +361,34 @@ def divmod_batched_dev(p, d_A, lda, na, d_B, ldb, nb, count, d_Q, ldq, d_R, ldr,
 def ntt_mul_batched_dev(p, d_A, lda, na, d_B, ldb, nb, count, d_F, ldf, stream=0):
     _check(load().mmm_cu_ntt_mul_batched_dev(_pint(p), d_A, lda, na, d_B, ldb, nb, count, d_F,
                                              ldf, stream))
+
+
+# ------------------------------------------------- fan-out (fused gather) --
+# `outs` lists device pointers (ints) with one layout; each output word is
+# stored into every one of them -- with every rank's buffer (symmetric memory
+# over NVLink) the gather of a sharded batch happens in the kernel's epilogue.
+def _ptrs(outs):
+    outs = [int(x) for x in outs]
+    return (C.c_void_p * len(outs))(*outs), len(outs)
+
+
+def mul_range_fanout_dev(p, d_a, na, d_b, nb, k0, k1, outs, s=8, stream=0):
+    arr, n = _ptrs(outs)
+    _check(load().mmm_cu_mul_range_fanout_dev(_pint(p), d_a, na, d_b, nb, k0, k1, s, arr, n,
+                                              stream))
+
+
+def mul_batched_fanout_dev(p, d_A, lda, na, d_B, ldb, nb, count, outs, ldf, s=8, stream=0):
+    arr, n = _ptrs(outs)
+    _check(load().mmm_cu_mul_batched_fanout_dev(_pint(p), d_A, lda, na, d_B, ldb, nb, count, s,
+                                                arr, n, ldf, stream))
+
+
+def divmod_batched_fanout_dev(p, d_A, lda, na, d_B, ldb, nb, count, q_outs, ldq, r_outs, ldr,
+                              s=64, stream=0):
+    if len(q_outs) != len(r_outs):
+        raise InvalidArgument("division batch: q and r fan-outs differ in length")
+    qa, n = _ptrs(q_outs)
+    ra, _ = _ptrs(r_outs)
+    _check(load().mmm_cu_divmod_batched_fanout_dev(_pint(p), d_A, lda, na, d_B, ldb, nb, count, s,
+                                                   qa, ldq, ra, ldr, n, stream))

@@ -264,6 +264,71 @@ int mmm_cu_mul_batched_dev(int64_t p, const uint32_t* d_A, int64_t lda, int64_t 
     });
 }
 
+// ------------------------------------------------------------ fan-out -----
+// Outputs stored into every buffer of a set (1..MMM_MAX_FAN device pointers,
+// same layout): with the buffers of every rank (symmetric / IPC-mapped memory
+// over NVLink) the all-gather of a sharded batch is fused into the kernel.
+namespace {
+Fan fan_or_throw(uint32_t* const* ptrs, int32_t n, const char* what) {
+    if (n < 1 || n > MMM_MAX_FAN || ptrs == nullptr)
+        throw Error(ST_INVALID, std::string(what) + ": fan-out count must be in [1, " +
+                                    std::to_string(MMM_MAX_FAN) + "]");
+    Fan f{};
+    for (int q = 0; q < n; ++q) {
+        if (ptrs[q] == nullptr) throw Error(ST_INVALID, std::string(what) + ": null output");
+        f.p[q] = ptrs[q];
+    }
+    f.n = n;
+    return f;
+}
+}  // namespace
+
+int mmm_cu_mul_range_fanout_dev(int64_t p, const uint32_t* d_a, int64_t na, const uint32_t* d_b,
+                                int64_t nb, int64_t k0, int64_t k1, int64_t s,
+                                uint32_t* const* d_f, int32_t n_out, void* stream) {
+    return guarded([&] {
+        const FieldParams F = field_or_throw(p);
+        const Fan f = fan_or_throw(d_f, n_out, "multiplication");
+        if (na < 1 || nb < 1) throw Error(ST_INVALID, "multiplication: operands must be nonzero");
+        if (k0 < 0 || k1 < k0 || k1 > na + nb - 1)
+            throw Error(ST_INVALID, "multiplication: output range outside [0, na + nb - 1)");
+        launch_mul_range_fan(F, d_a, na, d_b, nb, k0, k1, f, s, 0, as_stream(stream));
+    });
+}
+
+int mmm_cu_mul_batched_fanout_dev(int64_t p, const uint32_t* d_A, int64_t lda, int64_t na,
+                                  const uint32_t* d_B, int64_t ldb, int64_t nb, int64_t count,
+                                  int64_t s, uint32_t* const* d_F, int32_t n_out, int64_t ldf,
+                                  void* stream) {
+    return guarded([&] {
+        const FieldParams F = field_or_throw(p);
+        const Fan f = fan_or_throw(d_F, n_out, "multiplication batch");
+        if (na < 1 || nb < 1 || count < 0 || lda < na || ldb < nb || ldf < na + nb - 1)
+            throw Error(ST_INVALID, "multiplication batch: bad shape");
+        if (count)
+            launch_mul_batched_fan(F, d_A, lda, na, d_B, ldb, nb, count, f, ldf, s,
+                                   as_stream(stream));
+    });
+}
+
+int mmm_cu_divmod_batched_fanout_dev(int64_t p, const uint32_t* d_A, int64_t lda, int64_t na,
+                                     const uint32_t* d_B, int64_t ldb, int64_t nb, int64_t count,
+                                     int64_t s, uint32_t* const* d_Q, int64_t ldq,
+                                     uint32_t* const* d_R, int64_t ldr, int32_t n_out,
+                                     void* stream) {
+    return guarded([&] {
+        const FieldParams F = field_or_throw(p);
+        const Fan q = fan_or_throw(d_Q, n_out, "division batch");
+        const Fan r = fan_or_throw(d_R, n_out, "division batch");
+        if (nb < 1 || na < nb || count < 0 || lda < na || ldb < nb || ldq < na - nb + 1 ||
+            ldr < nb - 1)
+            throw Error(ST_INVALID, "division batch: bad shape");
+        if (count)
+            launch_divmod_batched_fan(F, d_A, lda, na, d_B, ldb, nb, count, q, ldq, r, ldr, s,
+                                      as_stream(stream));
+    });
+}
+
 // ------------------------------------------------------------- divmod -----
 int mmm_cu_divmod(int64_t p, const uint32_t* a, int64_t na, const uint32_t* b, int64_t nb,
                   int64_t s, uint32_t* q, int64_t q_cap, int64_t* nq, uint32_t* r, int64_t r_cap,

@@ -58,6 +58,40 @@ struct Scratch {
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// Fan-out outputs: a kernel stores each output word into every pointer of the
+// set (same layout behind each).  With the pointers of other GPUs' buffers
+// (symmetric / IPC-mapped memory over NVLink) this is an all-gather fused into
+// the producing kernel's epilogue: no gather collective after it.
+constexpr int MMM_MAX_FAN = 8;
+struct Fan {
+    uint32_t* p[MMM_MAX_FAN];
+    int n;
+};
+inline Fan fan_of(uint32_t* f) {
+    Fan o{};
+    o.p[0] = f;
+    o.n = 1;
+    return o;
+}
+inline Fan fan_offset(Fan o, int64_t words) {
+    for (int q = 0; q < o.n; ++q) o.p[q] += words;
+    return o;
+}
+#ifdef __CUDACC__
+// FAN = false: the single-output instantiation (no extra registers on the hot path)
+template <bool FAN>
+__device__ __forceinline__ void fan_store(const Fan& o, int64_t i, uint32_t v) {
+    if constexpr (!FAN) {
+        o.p[0][i] = v;
+        return;
+    }
+    o.p[0][i] = v;
+#pragma unroll
+    for (int q = 1; q < MMM_MAX_FAN; ++q)  // static indices: the pointers stay kernel parameters
+        if (q < o.n) o.p[q][i] = v;
+}
+#endif
+
 #ifdef __CUDACC__
 // Spin until *p >= target, then acquire.  The polling loads are relaxed: an
 // ld.acquire.gpu compiles to LDG.STRONG.GPU + CCTL.IVALL, i.e. it invalidates
@@ -113,6 +147,16 @@ void launch_divmod(const FieldParams& F, const uint32_t* a, int64_t na, const ui
 void launch_divmod_batched(const FieldParams& F, const uint32_t* A, int64_t lda, int64_t na,
                            const uint32_t* B, int64_t ldb, int64_t nb, int64_t count, uint32_t* Q,
                            int64_t ldq, uint32_t* R, int64_t ldr, int64_t s, cudaStream_t st);
+// Fan-out variants (outputs stored into every pointer of the set; see Fan).
+void launch_mul_range_fan(const FieldParams& F, const uint32_t* a, int64_t na, const uint32_t* b,
+                          int64_t nb, int64_t klo, int64_t khi, Fan f, int64_t s, int64_t l,
+                          cudaStream_t st);
+void launch_mul_batched_fan(const FieldParams& F, const uint32_t* A, int64_t lda, int64_t na,
+                            const uint32_t* B, int64_t ldb, int64_t nb, int64_t count, Fan Fo,
+                            int64_t ldf, int64_t s, cudaStream_t st);
+void launch_divmod_batched_fan(const FieldParams& F, const uint32_t* A, int64_t lda, int64_t na,
+                               const uint32_t* B, int64_t ldb, int64_t nb, int64_t count, Fan Q,
+                               int64_t ldq, Fan Rr, int64_t ldr, int64_t s, cudaStream_t st);
 // division by Newton iteration over NTT products (fastdiv.cu): same q, r.
 void launch_divmod_fast(const FieldParams& F, const uint32_t* a, int64_t na, const uint32_t* b,
                         int64_t nb, uint32_t* q, uint32_t* r, cudaStream_t st);

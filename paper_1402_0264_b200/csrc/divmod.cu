@@ -64,10 +64,10 @@ __device__ void inverse_series(uint32_t* h, int S, int64_t db, BT bt, const Fiel
 }
 
 // lambda for one step: lam_rev[valid-1-k] = p - lambda_k  (negated, reversed,
-// zero-padded to a multiple of R), q[i-db-k] = lambda_k.  heads(t) = A[i-t].
-template <class HD>
+// zero-padded to a multiple of R), write_q(k, lambda_k).  heads(t) = A[i-t].
+template <class HD, class QW>
 __device__ void step_lambdas(uint32_t* lam_rev, int valid, int padded, const uint32_t* h, HD heads,
-                             uint32_t* q_top, bool write_q, const FieldParams& F) {
+                             QW write_q, const FieldParams& F) {
     for (int k = threadIdx.x; k < padded; k += blockDim.x) {
         uint32_t lam = 0;
         if (k < valid) {
@@ -81,7 +81,7 @@ __device__ void step_lambdas(uint32_t* lam_rev, int valid, int padded, const uin
                 acc = mad_wide(h[k - t], heads(t), acc);
             }
             lam = reduce(acc, F);
-            if (write_q) q_top[-k] = lam;
+            write_q(k, lam);
             lam_rev[valid - 1 - k] = negmod(lam, F);
         } else {
             lam_rev[k] = 0;
@@ -99,13 +99,14 @@ struct DivArgs {
     int64_t na, nb, lda, ldb, ldq, ldr;
     int S;
     FieldParams F;
+    Fan qf, rf;        // CTA kernel: q and r outputs (fan-out: every pointer gets the words)
     uint32_t* h_glob;  // grid kernel: inverse series
     uint32_t* a_work;  // grid kernel: working copy of A (L2 resident)
 };
 
 // ------------------------------------------------ one CTA per instance -----
 // Shared layout (words): A[na] | bpad[BORG + nb + R] | h[S] | lam[Spad]
-template <int R>
+template <int R, bool FAN>
 __global__ void __launch_bounds__(DIV_T) div_cta_kernel(DivArgs g, int borg) {
     extern __shared__ __align__(16) uint32_t smem[];
     const int64_t inst = blockIdx.x;
@@ -119,8 +120,7 @@ __global__ void __launch_bounds__(DIV_T) div_cta_kernel(DivArgs g, int borg) {
     uint32_t* lam = h + ((S + 3) & ~3);
     const uint32_t* a_g = g.a + inst * g.lda;
     const uint32_t* b_g = g.b + inst * g.ldb;
-    uint32_t* q_g = g.q + inst * g.ldq;
-    uint32_t* r_g = g.r + inst * g.ldr;
+    const int64_t qbase = inst * g.ldq, rbase = inst * g.ldr;
 
     for (int64_t i = threadIdx.x; i < na; i += DIV_T) A[i] = a_g[i];
     for (int64_t j = threadIdx.x; j < borg + nb + R; j += DIV_T)
@@ -133,8 +133,8 @@ __global__ void __launch_bounds__(DIV_T) div_cta_kernel(DivArgs g, int borg) {
     for (int64_t i = na - 1; i >= db;) {
         const int valid = int(i - db + 1 < S ? i - db + 1 : S);
         const int padded = (valid + R - 1) / R * R;
-        step_lambdas(lam, valid, padded, h, [&](int t) { return A[i - t]; }, q_g + (i - db), true,
-                     F);
+        step_lambdas(lam, valid, padded, h, [&](int t) { return A[i - t]; },
+                     [&](int k, uint32_t l) { fan_store<FAN>(g.qf, qbase + (i - db) - k, l); }, F);
         __syncthreads();
         const int64_t xlo = i - valid + 1 - db;  // update window [xlo, xlo + db)
         for (int64_t y0 = int64_t(threadIdx.x) * R; y0 < db; y0 += int64_t(DIV_T) * R) {
@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(DIV_T) div_cta_kernel(DivArgs g, int borg) {
         __syncthreads();
         i -= valid;
     }
-    for (int64_t x = threadIdx.x; x < db; x += DIV_T) r_g[x] = A[x];
+    for (int64_t x = threadIdx.x; x < db; x += DIV_T) fan_store<FAN>(g.rf, rbase + x, A[x]);
 }
 
 // ------------------------------------------- cooperative grid, 1 instance ---
@@ -779,16 +779,18 @@ void run_cta(const DivArgs& g, int64_t count, cudaStream_t st) {
     const int Spad = (g.S + R - 1) / R * R;
     const int borg = ((Spad + 3) & ~3) + 3;
     const size_t bytes = cta_smem_words(g.na, g.nb, g.S, R, borg) * 4;
-    MMM_CUDA(cudaFuncSetAttribute(div_cta_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    const bool fan = g.qf.n > 1 || g.rf.n > 1;
+    auto kern = fan ? div_cta_kernel<R, true> : div_cta_kernel<R, false>;
+    MMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(bytes)));
     for (int64_t c0 = 0; c0 < count; c0 += 65535) {
         DivArgs gg = g;
         gg.a += c0 * g.lda;
         gg.b += c0 * g.ldb;
-        gg.q += c0 * g.ldq;
-        gg.r += c0 * g.ldr;
+        gg.qf = fan_offset(g.qf, c0 * g.ldq);
+        gg.rf = fan_offset(g.rf, c0 * g.ldr);
         const unsigned n = unsigned(std::min<int64_t>(65535, count - c0));
-        div_cta_kernel<R><<<n, DIV_T, bytes, st>>>(gg, borg);
+        kern<<<n, DIV_T, bytes, st>>>(gg, borg);
         check_launch("div_cta_kernel");
     }
 }
@@ -899,6 +901,8 @@ void launch_divmod(const FieldParams& F, const uint32_t* a, int64_t na, const ui
     g.b = b;
     g.q = q;
     g.r = r;
+    g.qf = fan_of(q);
+    g.rf = fan_of(r);
     g.na = na;
     g.nb = nb;
     g.S = S;
@@ -931,13 +935,20 @@ void launch_divmod(const FieldParams& F, const uint32_t* a, int64_t na, const ui
 void launch_divmod_batched(const FieldParams& F, const uint32_t* A, int64_t lda, int64_t na,
                            const uint32_t* B, int64_t ldb, int64_t nb, int64_t count, uint32_t* Q,
                            int64_t ldq, uint32_t* Rr, int64_t ldr, int64_t s, cudaStream_t st) {
+    launch_divmod_batched_fan(F, A, lda, na, B, ldb, nb, count, fan_of(Q), ldq, fan_of(Rr), ldr, s,
+                              st);
+}
+
+void launch_divmod_batched_fan(const FieldParams& F, const uint32_t* A, int64_t lda, int64_t na,
+                               const uint32_t* B, int64_t ldb, int64_t nb, int64_t count, Fan Q,
+                               int64_t ldq, Fan Rr, int64_t ldr, int64_t s, cudaStream_t st) {
     if (s < 1) throw Error(ST_INVALID, "division: block parameter must be >= 1");
     const int64_t mu = na - nb + 1;
     DivArgs g{};
     g.a = A;
     g.b = B;
-    g.q = Q;
-    g.r = Rr;
+    g.qf = Q;
+    g.rf = Rr;
     g.na = na;
     g.nb = nb;
     g.lda = lda;

@@ -40,7 +40,7 @@ constexpr int MUL_TI = MUL_TI_WORDS;  // terms per shared-memory chunk
 struct MulArgs {
     const uint32_t* a;
     const uint32_t* b;
-    uint32_t* f;
+    uint32_t* f;              // output word k - klo of instance inst at f[inst * ldf + k - klo]
     unsigned long long* acc;  // split k-tiles accumulate here (single instance)
     unsigned* arrived;        // per k-tile count of finished items
     // acc and arrived are persistent per stream and all-zero between calls:
@@ -50,9 +50,10 @@ struct MulArgs {
     int64_t chunk;  // i-range per item
     int64_t klo, khi;  // output range [klo, khi): f[k - klo] (whole product: 0, na + nb - 1)
     FieldParams F;
+    Fan fan;  // fan-out instantiation: the same words into every fan.p[q] (fan.p[0] == f)
 };
 
-template <int R>
+template <int R, bool FAN>
 __global__ void __launch_bounds__(MUL_T) mul_kernel(MulArgs g) {
     constexpr int TK = MUL_T * R;
     constexpr int ORIGIN = MUL_TI + 3;  // == 3 (mod 4): aligned window reloads
@@ -126,6 +127,7 @@ __global__ void __launch_bounds__(MUL_T) mul_kernel(MulArgs g) {
     }
 
     uint32_t* __restrict__ f = g.f + inst * g.ldf;
+    const int64_t fbase = inst * g.ldf - g.klo;  // FAN: word k at every g.fan.p[q][fbase + k]
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         const int64_t k = k0 + int64_t(threadIdx.x) * R + r;
@@ -134,7 +136,10 @@ __global__ void __launch_bounds__(MUL_T) mul_kernel(MulArgs g) {
             if (split)
                 atomicAdd(g.acc + (k - g.klo), (unsigned long long)v);
             else
-                f[k - g.klo] = v;
+                if constexpr (FAN)
+                    fan_store<true>(g.fan, fbase + k, v);
+                else
+                    f[k - g.klo] = v;
         }
     }
     if (!split) return;
@@ -166,7 +171,11 @@ __global__ void __launch_bounds__(MUL_T) mul_kernel(MulArgs g) {
     for (int t = threadIdx.x; t < TK; t += MUL_T) {
         const int64_t k = k0 + t;
         if (k < nf) {
-            f[k - g.klo] = reduce(__ldcg(g.acc + (k - g.klo)), g.F);
+            const uint32_t v = reduce(__ldcg(g.acc + (k - g.klo)), g.F);
+            if constexpr (FAN)
+                fan_store<true>(g.fan, fbase + k, v);
+            else
+                f[k - g.klo] = v;
             __stcg(g.acc + (k - g.klo), 0ull);  // zero for the next call on this stream
         }
     }
@@ -209,7 +218,10 @@ int pick_tile(int64_t s, const FieldParams& F) {
 
 template <int R>
 void launch_tile(const MulArgs& g, dim3 grid, cudaStream_t st) {
-    mul_kernel<R><<<grid, MUL_T, 0, st>>>(g);
+    if (g.fan.n > 1)
+        mul_kernel<R, true><<<grid, MUL_T, 0, st>>>(g);
+    else
+        mul_kernel<R, false><<<grid, MUL_T, 0, st>>>(g);
     check_launch("mul_kernel");
 }
 
@@ -233,8 +245,14 @@ void launch_mul(const FieldParams& F, const uint32_t* a, int64_t na, const uint3
 // Outputs [klo, khi) of the product into f[0, khi - klo): the per-rank slice of
 // an output-range-sharded product.
 void launch_mul_range(const FieldParams& F, const uint32_t* a, int64_t na, const uint32_t* b,
-                      int64_t nb, int64_t klo, int64_t khi, uint32_t* f, int64_t s, int64_t /*l*/,
+                      int64_t nb, int64_t klo, int64_t khi, uint32_t* f, int64_t s, int64_t l,
                       cudaStream_t st) {
+    launch_mul_range_fan(F, a, na, b, nb, klo, khi, fan_of(f), s, l, st);
+}
+
+void launch_mul_range_fan(const FieldParams& F, const uint32_t* a, int64_t na, const uint32_t* b,
+                          int64_t nb, int64_t klo, int64_t khi, Fan f, int64_t s, int64_t /*l*/,
+                          cudaStream_t st) {
     const int R = pick_tile(s, F);
     const int64_t TK = int64_t(MUL_T) * R;
     const int64_t nf = khi - klo;
@@ -257,7 +275,8 @@ void launch_mul_range(const FieldParams& F, const uint32_t* a, int64_t na, const
     MulArgs g{};
     g.a = a;
     g.b = b;
-    g.f = f;
+    g.f = f.p[0];
+    g.fan = f;
     g.na = na;
     g.nb = nb;
     g.chunk = chunk;
@@ -275,6 +294,12 @@ void launch_mul_range(const FieldParams& F, const uint32_t* a, int64_t na, const
 void launch_mul_batched(const FieldParams& F, const uint32_t* A, int64_t lda, int64_t na,
                         const uint32_t* B, int64_t ldb, int64_t nb, int64_t count, uint32_t* Fo,
                         int64_t ldf, int64_t s, cudaStream_t st) {
+    launch_mul_batched_fan(F, A, lda, na, B, ldb, nb, count, fan_of(Fo), ldf, s, st);
+}
+
+void launch_mul_batched_fan(const FieldParams& F, const uint32_t* A, int64_t lda, int64_t na,
+                            const uint32_t* B, int64_t ldb, int64_t nb, int64_t count, Fan Fo,
+                            int64_t ldf, int64_t s, cudaStream_t st) {
     const int R = pick_tile(s, F);
     const int64_t TK = int64_t(MUL_T) * R;
     const int64_t nf = na + nb - 1;
@@ -294,7 +319,8 @@ void launch_mul_batched(const FieldParams& F, const uint32_t* A, int64_t lda, in
         const int64_t c = std::min<int64_t>(65535, count - c0);
         g.a = A + c0 * lda;
         g.b = B + c0 * ldb;
-        g.f = Fo + c0 * ldf;
+        g.fan = fan_offset(Fo, c0 * ldf);
+        g.f = g.fan.p[0];
         dispatch(R, g, dim3(1, unsigned(nkt), unsigned(c)), st);
     }
 }

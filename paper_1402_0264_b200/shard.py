@@ -93,6 +93,41 @@ def gather_rows(local, dist, world: int):
     return out
 
 
+class PeerOutputs:
+    """Full-size output regions on every rank in one symmetric-memory
+    allocation (torch symmetric memory: each rank's buffer is mapped into every
+    peer's address space; stores travel over NVLink/NVSwitch).  A fan-out kernel
+    (mmm_cu_*_fanout_dev) given `ptrs(i, off)` stores its rows or range into
+    region i of *every* rank's buffer, so the all-gather of a sharded batch
+    happens in the producing kernel's epilogue; `barrier()` (device-side, on the
+    current stream) orders the ranks before anyone reads.  Raises if symmetric
+    memory is unavailable: callers fall back to gather_rows (NCCL)."""
+
+    def __init__(self, sizes, dist):
+        import itertools
+
+        import torch
+        import torch.distributed._symmetric_memory as symm_mem
+
+        self.sizes = [int(n) for n in sizes]
+        self.offs = list(itertools.accumulate([0] + self.sizes[:-1]))
+        self.t = symm_mem.empty(sum(self.sizes), dtype=torch.int32, device="cuda")
+        self.h = symm_mem.rendezvous(self.t, dist.group.WORLD)
+        off = int(getattr(self.h, "offset", 0) or 0)
+        self.bases = [int(p) + off for p in self.h.buffer_ptrs]
+        if self.bases[dist.get_rank()] != self.t.data_ptr():
+            raise RuntimeError("symmetric buffer pointers do not match the local tensor")
+
+    def view(self, i, shape):
+        return self.t[self.offs[i]: self.offs[i] + self.sizes[i]].view(shape)
+
+    def ptrs(self, i, off_words=0):
+        return [b + 4 * (self.offs[i] + off_words) for b in self.bases]
+
+    def barrier(self):
+        self.h.barrier()
+
+
 # --------------------------------------------------- sharded four-step NTT --
 class NttShards:
     """Layout of the four-step NTT product over `world` ranks.

@@ -94,6 +94,20 @@ def test_validation_errors_before_any_device_work():
     assert q.size == 0 and r.tolist() == [1, 2]
 
 
+def test_fanout_validation_before_any_device_work():
+    """Fan-out entry points reject an empty or oversized output set, null
+    outputs and mismatched q/r sets before touching the device."""
+    for outs in ([], [1] * 9, [0]):
+        with pytest.raises(mmm.InvalidArgument):
+            mmm.mul_range_fanout_dev(7, 1, 2, 1, 2, 0, 3, outs)
+        with pytest.raises(mmm.InvalidArgument):
+            mmm.mul_batched_fanout_dev(7, 1, 2, 2, 1, 2, 2, 1, outs, 3)
+    with pytest.raises(mmm.InvalidArgument):
+        mmm.divmod_batched_fanout_dev(7, 1, 3, 3, 1, 2, 2, 1, [1], 2, [1, 2], 1)
+    with pytest.raises(mmm.InvalidArgument):  # shape checked too
+        mmm.mul_batched_fanout_dev(7, 1, 1, 2, 1, 2, 2, 1, [1], 3)
+
+
 def test_no_cpu_fallback_without_gpu():
     import torch
     if torch.cuda.is_available():

@@ -483,3 +483,78 @@ def test_cfg4_big_sharded_virtual(cuda_lib, golden_configs):
     for world in (2, 8):
         f = ntt_mul_virtual(cuda_lib, P, da, len(c["a"]), db, len(c["b"]), world, st)
         assert digest(f.cpu().numpy()) == golden_configs["cfg4_big"]["f"], world
+
+
+# ------------------------------------- fan-out outputs (fused all-gather) --
+def _dev_u32(x):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.uint32).view(np.int32)).cuda()
+
+
+def test_fanout_mul_range_virtual_ranks(cuda_lib, port):
+    """W virtual ranks on one GPU: rank r computes its balanced output range and
+    stores it into all W full-product buffers (the symmetric-memory all-gather
+    fused into the epilogue); every buffer ends up the whole product, for the
+    direct-store and the split-k (finalize) paths."""
+    import torch
+    from paper_1402_0264_b200.shard import balanced_output_ranges
+    rng = np.random.default_rng(21)
+    for na, nb in [(3000, 2000), (16384, 16384), (70, 1)]:
+        a = rng.integers(0, P, na).astype(np.uint32)
+        b = rng.integers(0, P, nb).astype(np.uint32)
+        want = np.zeros(na + nb - 1, np.int64)
+        w = port.mul(a, b, P)
+        want[: len(w)] = w
+        da, db = _dev_u32(a), _dev_u32(b)
+        for world in (1, 3, 8):
+            bufs = [torch.full((na + nb - 1,), -1, dtype=torch.int32, device="cuda")
+                    for _ in range(world)]
+            for k0, k1 in balanced_output_ranges(na, nb, world, align=32):
+                cuda_lib.mul_range_fanout_dev(P, da.data_ptr(), na, db.data_ptr(), nb, k0, k1,
+                                              [t.data_ptr() + 4 * k0 for t in bufs], s=4)
+            torch.cuda.synchronize()
+            for t in bufs:
+                assert np.array_equal(t.cpu().numpy().view(np.uint32).astype(np.int64), want), \
+                    (na, nb, world)
+
+
+def test_fanout_batches_virtual_ranks(cuda_lib, port):
+    """cfg5-shaped batches split over W virtual ranks: each rank's rows of the
+    product and quotient/remainder batches land in every rank's full buffers."""
+    import torch
+    from paper_1402_0264_b200.shard import shard_range
+    rng = np.random.default_rng(22)
+    count, na, nb, nd = 10, 300, 200, 150
+    A = rng.integers(0, P, (count, na)).astype(np.uint32)
+    B = rng.integers(0, P, (count, nb)).astype(np.uint32)
+    A[:, -1] |= 1
+    B[:, -1] |= 1
+    D = rng.integers(0, P, (count, nd)).astype(np.uint32)
+    D[:, -1] |= 1
+    dA, dB, dD = _dev_u32(A), _dev_u32(B), _dev_u32(D)
+    nf, nq, nr = na + nb - 1, na - nd + 1, nd - 1
+    for world in (1, 2, 3):
+        F = [torch.full((count, nf), -1, dtype=torch.int32, device="cuda") for _ in range(world)]
+        Q = [torch.full((count, nq), -1, dtype=torch.int32, device="cuda") for _ in range(world)]
+        R = [torch.full((count, nr), -1, dtype=torch.int32, device="cuda") for _ in range(world)]
+        for r in range(world):
+            i0, i1 = shard_range(count, world, r)
+            if i1 <= i0:
+                continue
+            cuda_lib.mul_batched_fanout_dev(P, dA.data_ptr() + 4 * i0 * na, na, na,
+                                            dB.data_ptr() + 4 * i0 * nb, nb, nb, i1 - i0,
+                                            [t.data_ptr() + 4 * i0 * nf for t in F], nf, s=8)
+            cuda_lib.divmod_batched_fanout_dev(P, dA.data_ptr() + 4 * i0 * na, na, na,
+                                               dD.data_ptr() + 4 * i0 * nd, nd, nd, i1 - i0,
+                                               [t.data_ptr() + 4 * i0 * nq for t in Q], nq,
+                                               [t.data_ptr() + 4 * i0 * nr for t in R], nr, s=64)
+        torch.cuda.synchronize()
+        for i in range(count):
+            wf = port.mul(A[i], B[i], P)
+            wq, wr = port.divmod(A[i], D[i], P)
+            for q in range(world):
+                f = F[q][i].cpu().numpy().view(np.uint32).astype(np.int64)
+                assert np.array_equal(np.trim_zeros(f, "b"), wf), (world, q, i)
+                assert np.array_equal(Q[q][i].cpu().numpy().view(np.uint32).astype(np.int64), wq)
+                rr = R[q][i].cpu().numpy().view(np.uint32).astype(np.int64)
+                assert np.array_equal(np.trim_zeros(rr, "b"), wr), (world, q, i)
