@@ -722,8 +722,8 @@ class NttBatchWork(_Sharded):
         self.na = self.A.shape[1]
         self.nf = 2 * self.na - 1
         self.config = {"workload": "cfg4_batch_256x(2^15x2^15)_ntt_N2^16_p469762049", "p": P,
-                       "seed": 42, "parallelism": "instances sharded across ranks, NCCL "
-                       "all-gather of results", "units": "schoolbook-equivalent MACs",
+                       "seed": 42, "parallelism": "instances sharded across ranks; results "
+                       "gathered to every rank (config.gather)", "units": "schoolbook-equivalent MACs",
                        "l2": "flushed between timed steps (256 MB written then read: clean lines)"}
 
     def units(self):
@@ -734,11 +734,26 @@ class NttBatchWork(_Sharded):
         self.dA = _dev(self.A[self.lo:self.hi])
         self.dB = _dev(self.B[self.lo:self.hi])
         self.dF = torch.zeros((self.hi - self.lo, self.nf), dtype=torch.int32, device="cuda")
+        try_peer_outputs(self, [self.count * self.nf])
+        validate_peer_outputs(self)
+        if self.world > 1 or self.peer is not None:
+            self.config["gather"] = ("peer push: one kernel stores the rank's rows into every "
+                                     "rank's symmetric-memory results (NVLink), device barrier"
+                                     if self.peer is not None else
+                                     f"NCCL all-gather ({self.peer_note})")
 
     def device_step(self, stream):
+        k = self.hi - self.lo
         self.mmm.ntt_mul_batched_dev(P, self.dA.data_ptr(), self.na, self.na, self.dB.data_ptr(),
-                                     self.na, self.na, self.hi - self.lo, self.dF.data_ptr(),
+                                     self.na, self.na, k, self.dF.data_ptr(),
                                      self.nf, stream=stream)
+        pe = getattr(self, "peer", None)
+        if pe is not None:
+            self.mmm.fanout_copy_dev(self.dF.data_ptr(), k * self.nf,
+                                     pe.ptrs(0, self.lo * self.nf), stream=stream)
+            pe.barrier()
+            self.full = pe.view(0, (self.count, self.nf))
+            return
         self.full = self._gather(self.dF)
 
     def _digest_rows(self, F):

@@ -168,6 +168,11 @@ int mmm_cu_mul_batched_fanout_dev(int64_t p, const uint32_t* d_A, int64_t lda, i
                                   const uint32_t* d_B, int64_t ldb, int64_t nb, int64_t count,
                                   int64_t s, uint32_t* const* d_F, int32_t n_out, int64_t ldf,
                                   void* stream);
+/* Push n words of d_src into every one of the n_out (1..8) buffers d_dst[q]:
+ * the gather for results whose kernels have no fan-out epilogue (the NTT
+ * batch), as one peer-store kernel over NVLink instead of a collective. */
+int mmm_cu_fanout_copy_dev(const uint32_t* d_src, int64_t n, uint32_t* const* d_dst,
+                           int32_t n_out, void* stream);
 int mmm_cu_divmod_batched_fanout_dev(int64_t p, const uint32_t* d_A, int64_t lda, int64_t na,
                                      const uint32_t* d_B, int64_t ldb, int64_t nb, int64_t count,
                                      int64_t s, uint32_t* const* d_Q, int64_t ldq,

@@ -106,6 +106,7 @@ SIGNATURES = {
                                             _VP, _I64, _VP, _I64, _VP]),
     "mmm_cu_ntt_mul_batched_dev": (C.c_int, [_I64, _VP, _I64, _I64, _VP, _I64, _I64, _I64, _VP,
                                              _I64, _VP]),
+    "mmm_cu_fanout_copy_dev": (C.c_int, [_VP, _I64, C.POINTER(C.c_void_p), C.c_int32, _VP]),
     "mmm_cu_mul_range_fanout_dev": (C.c_int, [_I64, _VP, _I64, _VP, _I64, _I64, _I64, _I64,
                                               C.POINTER(C.c_void_p), C.c_int32, _VP]),
     "mmm_cu_mul_batched_fanout_dev": (C.c_int, [_I64, _VP, _I64, _I64, _VP, _I64, _I64, _I64,
@@ -392,3 +393,9 @@ def divmod_batched_fanout_dev(p, d_A, lda, na, d_B, ldb, nb, count, q_outs, ldq,
     ra, _ = _ptrs(r_outs)
     _check(load().mmm_cu_divmod_batched_fanout_dev(_pint(p), d_A, lda, na, d_B, ldb, nb, count, s,
                                                    qa, ldq, ra, ldr, n, stream))
+
+
+def fanout_copy_dev(d_src, n, outs, stream=0):
+    """n words of d_src into every device buffer of `outs` (one peer-store kernel)."""
+    arr, k = _ptrs(outs)
+    _check(load().mmm_cu_fanout_copy_dev(d_src, n, arr, k, stream))

@@ -283,6 +283,46 @@ Fan fan_or_throw(uint32_t* const* ptrs, int32_t n, const char* what) {
 }
 }  // namespace
 
+// Push one buffer into every buffer of a fan (the gather for kernels without a
+// fan-out epilogue, e.g. the NTT batch): 16-byte loads and stores when every
+// pointer is aligned, one pass over the source.
+__global__ void fanout_copy_kernel(const uint32_t* __restrict__ src, int64_t n, Fan dst,
+                                   bool vec) {
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (vec) {
+        const int64_t n4 = n / 4;
+        for (; i < n4; i += stride) {
+            const uint4 v = __ldcs(reinterpret_cast<const uint4*>(src) + i);
+#pragma unroll
+            for (int q = 0; q < MMM_MAX_FAN; ++q)
+                if (q < dst.n) reinterpret_cast<uint4*>(dst.p[q])[i] = v;
+        }
+        i = 4 * n4 + int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    }
+    for (; i < n; i += stride) {
+        const uint32_t v = src[i];
+#pragma unroll
+        for (int q = 0; q < MMM_MAX_FAN; ++q)
+            if (q < dst.n) dst.p[q][i] = v;
+    }
+}
+
+int mmm_cu_fanout_copy_dev(const uint32_t* d_src, int64_t n, uint32_t* const* d_dst,
+                           int32_t n_out, void* stream) {
+    return guarded([&] {
+        const Fan f = fan_or_throw(d_dst, n_out, "fan-out copy");
+        if (n < 0) throw Error(ST_INVALID, "fan-out copy: negative length");
+        if (n == 0) return;
+        bool vec = reinterpret_cast<uintptr_t>(d_src) % 16 == 0;
+        for (int q = 0; q < f.n; ++q) vec = vec && reinterpret_cast<uintptr_t>(f.p[q]) % 16 == 0;
+        const int64_t work = vec ? (n + 3) / 4 : n;
+        const unsigned blocks = unsigned(std::min<int64_t>((work + 255) / 256, 8LL * sm_count()));
+        fanout_copy_kernel<<<blocks, 256, 0, as_stream(stream)>>>(d_src, n, f, vec);
+        check_launch("fanout_copy_kernel");
+    });
+}
+
 int mmm_cu_mul_range_fanout_dev(int64_t p, const uint32_t* d_a, int64_t na, const uint32_t* d_b,
                                 int64_t nb, int64_t k0, int64_t k1, int64_t s,
                                 uint32_t* const* d_f, int32_t n_out, void* stream) {

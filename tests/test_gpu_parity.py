@@ -558,3 +558,19 @@ def test_fanout_batches_virtual_ranks(cuda_lib, port):
                 assert np.array_equal(Q[q][i].cpu().numpy().view(np.uint32).astype(np.int64), wq)
                 rr = R[q][i].cpu().numpy().view(np.uint32).astype(np.int64)
                 assert np.array_equal(np.trim_zeros(rr, "b"), wr), (world, q, i)
+
+
+def test_fanout_copy(cuda_lib):
+    """The peer push kernel: every destination equals the source, for aligned
+    (vector) and unaligned (scalar) pointers and ragged lengths."""
+    import torch
+    rng = np.random.default_rng(23)
+    for n in (0, 1, 5, 4096, 100003):
+        src = _dev_u32(rng.integers(0, P, n + 3).astype(np.uint32))
+        for off in (0, 1):
+            dst = [torch.full((n + 8,), -1, dtype=torch.int32, device="cuda") for _ in range(3)]
+            cuda_lib.fanout_copy_dev(src.data_ptr() + 4 * off, n, [t.data_ptr() + 4 * off for t in dst])
+            torch.cuda.synchronize()
+            for t in dst:
+                assert torch.equal(t[off: off + n], src[off: off + n]), (n, off)
+                assert int((t[off + n:] == -1).sum()) == n + 8 - off - n
