@@ -461,13 +461,14 @@ class MulWork(Workload):
 
     def host_setup(self):
         (self.ha, self._ta), (self.hb, self._tb) = _pinned(self.a), _pinned(self.b)
+        self.hout, self._to = _pinned(np.zeros(self.nf, np.uint32))  # result lands in pinned memory
         self.bytes_in = 4 * (len(self.a) + len(self.b))
         self.bytes_out = 4 * (self.nf if self.world == 1 or getattr(self, "peer", None) is not None
                               else self.world * self.L)
 
     def host_step(self):
         if self.world == 1:  # the host C-ABI call a user makes (mmm_cu_mul)
-            return self.mmm.mul(self.ha, self.hb, P, s=self.s)
+            return self.mmm.mul(self.ha, self.hb, P, s=self.s, out=self.hout)
         import torch  # sharded: pinned H2D, the rank's slice, all-gather, D2H
         self.da.copy_(self._ta, non_blocking=True)
         self.db.copy_(self._tb, non_blocking=True)
@@ -638,12 +639,13 @@ class NttWork(Workload):
 
     def host_setup(self):
         (self.ha, self._ta), (self.hb, self._tb) = _pinned(self.a), _pinned(self.b)
+        self.hout, self._to = _pinned(np.zeros(self.nf, np.uint32))
         self.bytes_in = 4 * (len(self.a) + len(self.b))
         self.bytes_out = 4 * self.nf
 
     def host_step(self):
         if self.world == 1:  # the host C-ABI call a user makes (mmm_cu_ntt_mul)
-            return self.mmm.ntt_mul(self.ha, self.hb, P)
+            return self.mmm.ntt_mul(self.ha, self.hb, P, out=self.hout)
         import torch  # sharded: pinned H2D, the sharded product, D2H
         self.da.copy_(self._ta, non_blocking=True)
         self.db.copy_(self._tb, non_blocking=True)
@@ -768,11 +770,12 @@ class NttBatchWork(_Sharded):
     def host_setup(self):
         (self.hA, self._ta), (self.hB, self._tb) = _pinned(self.A[self.lo:self.hi]), _pinned(
             self.B[self.lo:self.hi])
+        self.hout, self._to = _pinned(np.zeros((self.hi - self.lo, self.nf), np.uint32))
         self.bytes_in = 4 * (self.hA.size + self.hB.size)
         self.bytes_out = 4 * (self.hi - self.lo) * self.nf
 
     def host_step(self):
-        return self.mmm.ntt_mul_batched(self.hA, self.hB, P)
+        return self.mmm.ntt_mul_batched(self.hA, self.hB, P, out=self.hout)
 
     def host_check(self, F):
         if self.world == 1:
@@ -882,12 +885,16 @@ class BatchWork(_Sharded):
         (self.hA, self.hB, self.hC, self.hD) = (q[0] for q in pins)
         self._pins = pins
         k, n = self.hi - self.lo, self.n
+        outs = [_pinned(np.zeros(shape, np.uint32))
+                for shape in ((k, 2 * n - 1), (k, n + 1), (k, max(n - 1, 1)))]
+        (self.hF, self.hQ, self.hR), self._pouts = (o[0] for o in outs), outs
         self.bytes_in = 4 * k * (n + n + 2 * n + n)
         self.bytes_out = 4 * k * ((2 * n - 1) + (n + 1) + (n - 1))
 
     def host_step(self):
-        F = self.mmm.mul_batched(self.hA, self.hB, P, s=self.s or 8)
-        Q, R = self.mmm.divmod_batched(self.hC, self.hD, P, s=self.s or 64)
+        F = self.mmm.mul_batched(self.hA, self.hB, P, s=self.s or 8, out=self.hF)
+        Q, R = self.mmm.divmod_batched(self.hC, self.hD, P, s=self.s or 64, q_out=self.hQ,
+                                       r_out=self.hR)
         return F, Q, R
 
     def host_check(self, out):

@@ -227,17 +227,27 @@ def random_poly(rng: Rng, terms: int, F) -> np.ndarray:
     return rng.random_poly(terms, F.p() if isinstance(F, Field) else int(F))
 
 
+def _out(out, shape):
+    """A caller-supplied result array (e.g. pinned host memory, so the
+    device-to-host copy runs at full link speed) or a new one."""
+    if out is None:
+        return np.zeros(shape, dtype=np.uint32)
+    if out.dtype != np.uint32 or not out.flags.c_contiguous or tuple(out.shape) != tuple(shape):
+        raise InvalidArgument(f"out: need a C-contiguous uint32 array of shape {tuple(shape)}")
+    return out
+
+
 def _pint(p) -> int:
     return p.p() if isinstance(p, Field) else int(p)
 
 
 # ------------------------------------------------------------- host API ---
-def mul(a, b, p, s: int = 8, l: int = 128) -> np.ndarray:
+def mul(a, b, p, s: int = 8, l: int = 128, out=None) -> np.ndarray:
     a, b, p = _u32(a), _u32(b), _pint(p)
-    f = np.zeros(max(a.size + b.size - 1, 1), dtype=np.uint32)
+    f = _out(out, (max(a.size + b.size - 1, 1),))
     n = C.c_int64(0)
     _check(load().mmm_cu_mul(p, _p(a), a.size, _p(b), b.size, s, l, _p(f), f.size, C.byref(n)))
-    return f[: n.value].copy()
+    return f[: n.value] if out is not None else f[: n.value].copy()
 
 
 def divmod(a, b, p, s: int = 64):
@@ -286,39 +296,39 @@ def gcd(a, b, p, s: int = 64) -> np.ndarray:
     return g[: n.value].copy()
 
 
-def ntt_mul(a, b, p) -> np.ndarray:
+def ntt_mul(a, b, p, out=None) -> np.ndarray:
     a, b, p = _u32(a), _u32(b), _pint(p)
-    f = np.zeros(max(a.size + b.size - 1, 1), dtype=np.uint32)
+    f = _out(out, (max(a.size + b.size - 1, 1),))
     n = C.c_int64(0)
     _check(load().mmm_cu_ntt_mul(p, _p(a), a.size, _p(b), b.size, _p(f), f.size, C.byref(n)))
-    return f[: n.value].copy()
+    return f[: n.value] if out is not None else f[: n.value].copy()
 
 
-def mul_batched(A, B, p, s: int = 8) -> np.ndarray:
+def mul_batched(A, B, p, s: int = 8, out=None) -> np.ndarray:
     A, B, p = _u32(A), _u32(B), _pint(p)
     cnt, na = A.shape
     nb = B.shape[1]
-    F = np.zeros((cnt, na + nb - 1), dtype=np.uint32)
+    F = _out(out, (cnt, na + nb - 1))
     _check(load().mmm_cu_mul_batched(p, _p(A), na, na, _p(B), nb, nb, cnt, s, _p(F), F.shape[1]))
     return F
 
 
-def divmod_batched(A, B, p, s: int = 64):
+def divmod_batched(A, B, p, s: int = 64, q_out=None, r_out=None):
     A, B, p = _u32(A), _u32(B), _pint(p)
     cnt, na = A.shape
     nb = B.shape[1]
-    Q = np.zeros((cnt, na - nb + 1), dtype=np.uint32)
-    R = np.zeros((cnt, max(nb - 1, 1)), dtype=np.uint32)
+    Q = _out(q_out, (cnt, na - nb + 1))
+    R = _out(r_out, (cnt, max(nb - 1, 1)))
     _check(load().mmm_cu_divmod_batched(p, _p(A), na, na, _p(B), nb, nb, cnt, s, _p(Q),
                                         Q.shape[1], _p(R), R.shape[1]))
     return Q, R[:, : nb - 1]
 
 
-def ntt_mul_batched(A, B, p) -> np.ndarray:
+def ntt_mul_batched(A, B, p, out=None) -> np.ndarray:
     A, B, p = _u32(A), _u32(B), _pint(p)
     cnt, na = A.shape
     nb = B.shape[1]
-    F = np.zeros((cnt, na + nb - 1), dtype=np.uint32)
+    F = _out(out, (cnt, na + nb - 1))
     _check(load().mmm_cu_ntt_mul_batched(p, _p(A), na, na, _p(B), nb, nb, cnt, _p(F),
                                          F.shape[1]))
     return F

@@ -10,6 +10,9 @@
 #include <algorithm>
 #include <cstring>
 #include <mutex>
+#include <thread>
+#include <tuple>
+#include <map>
 #include <new>
 #include <random>
 #include <string>
@@ -21,21 +24,46 @@ namespace mmm_cu {
 
 std::atomic<uint64_t> g_launches{0};
 
-Scratch::Scratch(cudaStream_t s) : stream(s) {
-    static std::once_flag once[64];
+Arena& arena_for(cudaStream_t s) {
+    static std::mutex mu;
+    static std::map<std::tuple<int, cudaStream_t, std::thread::id>, Arena> arenas;
     int dev = 0;
     cudaGetDevice(&dev);
-    std::call_once(once[dev & 63], [dev] {
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-            uint64_t thr = UINT64_MAX;
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    std::lock_guard<std::mutex> lock(mu);
+    return arenas[{dev, s, std::this_thread::get_id()}];  // node-based: references stay valid
+}
+
+Scratch::Scratch(cudaStream_t s) : stream(s), arena(&arena_for(s)) {
+    ci0 = arena->ci;
+    off0 = arena->off;
+}
+
+void* Scratch::get_bytes(size_t bytes) {
+    bytes = (bytes + 255) & ~size_t(255);
+    Arena& a = *arena;
+    for (;;) {
+        if (a.ci < a.chunks.size()) {
+            auto& c = a.chunks[a.ci];
+            if (a.off + bytes <= c.second) {
+                void* p = c.first + a.off;
+                a.off += bytes;
+                return p;
+            }
+            ++a.ci;  // the rest of this chunk stays unused until the position unwinds
+            a.off = 0;
+            continue;
         }
-    });
+        size_t size = std::max<size_t>(bytes, size_t(4) << 20);
+        if (!a.chunks.empty()) size = std::max(size, 2 * a.chunks.back().second);
+        void* p = nullptr;
+        MMM_CUDA(cudaMallocAsync(&p, size, stream));
+        a.chunks.push_back({static_cast<char*>(p), size});
+    }
 }
 
 Scratch::~Scratch() {
-    for (void* p : blocks) cudaFreeAsync(p, stream);
+    arena->ci = ci0;
+    arena->off = off0;
 }
 
 }  // namespace mmm_cu
@@ -78,10 +106,16 @@ FieldParams field_or_throw(int64_t p) {
 void check_canonical(const uint32_t* c, int64_t n, uint32_t p, const char* who) {
     if (n < 0) throw Error(ST_INVALID, std::string(who) + ": negative length");
     if (n > 0 && c == nullptr) throw Error(ST_INVALID, std::string(who) + ": null pointer");
-    for (int64_t i = 0; i < n; ++i)
-        if (c[i] >= p)
+    // blockwise maximum without an early exit, so the scan vectorises (the
+    // branchy per-word test was most of the host time of a large e2e call)
+    for (int64_t i0 = 0; i0 < n; i0 += 8192) {
+        const int64_t e = std::min<int64_t>(n, i0 + 8192);
+        uint32_t m = 0;
+        for (int64_t i = i0; i < e; ++i) m = c[i] > m ? c[i] : m;
+        if (m >= p)
             throw Error(ST_INVALID,
                         std::string(who) + ": coefficients must be canonical field elements");
+    }
 }
 
 int64_t trimmed_len(const uint32_t* c, int64_t n) {
@@ -115,6 +149,21 @@ void to_host(uint32_t* h, const uint32_t* d, int64_t n, cudaStream_t st) {
 }
 
 void sync(cudaStream_t st) { MMM_CUDA(cudaStreamSynchronize(st)); }
+
+// Per-thread pinned host staging (grown on demand, kept): device-to-host reads
+// that must complete before the call returns go here, so one synchronisation
+// covers them all.
+uint32_t* pinned_stage(size_t bytes) {
+    thread_local std::pair<void*, size_t> buf{nullptr, 0};
+    if (buf.second < bytes) {
+        if (buf.first) cudaFreeHost(buf.first);
+        const size_t n = std::max(bytes, size_t(1) << 20);
+        void* p = nullptr;
+        MMM_CUDA(cudaMallocHost(&p, n));
+        buf = {p, n};
+    }
+    return static_cast<uint32_t*>(buf.first);
+}
 
 cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 
@@ -557,13 +606,18 @@ int mmm_cu_gcd(int64_t p, const uint32_t* a, int64_t na, const uint32_t* b, int6
             uint32_t* dg = sc.get<uint32_t>(size_t(std::max(na, nb)));
             int64_t* dng = sc.get<int64_t>(1);
             launch_gcd(F, da, na, db, nb, dg, dng, s, st);
-            MMM_CUDA(cudaMemcpyAsync(&len, dng, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+            // one synchronisation: the length and the whole result buffer come back
+            // together into pinned staging, then len words go to the caller
+            const int64_t n = std::max(na, nb);
+            uint32_t* stage = pinned_stage(size_t(n) * 4 + 8);
+            MMM_CUDA(cudaMemcpyAsync(stage, dng, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+            MMM_CUDA(cudaMemcpyAsync(stage + 2, dg, size_t(n) * 4, cudaMemcpyDeviceToHost, st));
             sync(st);
+            std::memcpy(&len, stage, sizeof(int64_t));
             if (len == -1) throw Error(ST_SIM, "gcd: offset matrix left its window");
-            if (len < 0 || len > std::max(na, nb)) throw Error(ST_SIM, "gcd: batch made no progress");
-            to_host(g, dg, len, st);
+            if (len < 0 || len > n) throw Error(ST_SIM, "gcd: batch made no progress");
+            std::memcpy(g, stage + 2, size_t(len) * 4);
         }
-        sync(st);
         *ng = len;
     });
 }

@@ -37,20 +37,28 @@ inline void check_launch(const char* what) {
     cuda_check(cudaGetLastError(), what);
 }
 
-// Stream-ordered scratch: cudaMallocAsync from the device's default pool
-// (its release threshold is raised once so blocks stay cached across calls).
+// Stream-ordered scratch from a per-(device, stream, host thread) arena: a list
+// of device chunks (cudaMallocAsync, kept for the process), handed out by a
+// bump pointer that each Scratch restores on destruction (LIFO, nested Scratch
+// objects included).  Reuse is safe because every use of a Scratch's memory is
+// ordered on its stream.  In steady state a call makes no allocation API call
+// (a dozen cudaMallocAsync/cudaFreeAsync pairs per GCD call showed up in e2e).
+struct Arena {
+    std::vector<std::pair<char*, size_t>> chunks;
+    size_t ci = 0, off = 0;  // current chunk, offset in it
+};
+Arena& arena_for(cudaStream_t s);
 struct Scratch {
     cudaStream_t stream;
-    std::vector<void*> blocks;
+    Arena* arena;
+    size_t ci0, off0;
     explicit Scratch(cudaStream_t s);
     ~Scratch();
+    void* get_bytes(size_t bytes);
     template <class T>
     T* get(size_t count) {
-        void* p = nullptr;
         if (count == 0) count = 1;
-        MMM_CUDA(cudaMallocAsync(&p, count * sizeof(T), stream));
-        blocks.push_back(p);
-        return static_cast<T*>(p);
+        return static_cast<T*>(get_bytes(count * sizeof(T)));
     }
     Scratch(const Scratch&) = delete;
     Scratch& operator=(const Scratch&) = delete;

@@ -36,6 +36,8 @@
 #include "conv.cuh"
 
 #include <cstdio>
+#include <map>
+#include <mutex>
 #include <cstdlib>
 
 namespace cg = cooperative_groups;
@@ -1582,9 +1584,23 @@ void launch_gcd(const FieldParams& F, const uint32_t* a, int64_t na, const uint3
     const int mode = !F.odd ? 2 : (F.p < (1u << 29) ? 0 : 1);
     const void* fn = mode == 0 ? (const void*)gcd_kernel<0>
                                : (mode == 1 ? (const void*)gcd_kernel<1> : (const void*)gcd_kernel<2>);
-    MMM_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
+    // attribute and occupancy once per (device, flavour): host time in every e2e call otherwise
+    static std::mutex fit_mu;
+    static std::map<std::pair<int, int>, int> fit;
+    int dev = 0;
+    MMM_CUDA(cudaGetDevice(&dev));
     int per_sm = 0;
-    MMM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, GCD_T, bytes));
+    {
+        std::lock_guard<std::mutex> lock(fit_mu);
+        auto it = fit.find({dev, mode});
+        if (it == fit.end()) {
+            MMM_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
+            MMM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, GCD_T, bytes));
+            fit[{dev, mode}] = per_sm;
+        } else {
+            per_sm = it->second;
+        }
+    }
     if (per_sm < 1) throw Error(ST_INVALID, "gcd: kernel does not fit an SM");
     const int64_t want = std::max<int64_t>(2, 1 + ceil_div(na + nb, GCD_OUT_PER_CTA));
     // one CTA per SM: a second CTA on the head's SM would take issue slots from the chain

@@ -5,7 +5,16 @@
 #include "../paper_1402_0264_b200/csrc/gcd.cu"
 namespace mmm_cu {
 std::atomic<uint64_t> g_launches{0};
-Scratch::Scratch(cudaStream_t s) : stream(s) {}
+Arena& arena_for(cudaStream_t) {
+    static Arena a;
+    return a;
+}
+Scratch::Scratch(cudaStream_t s) : stream(s), arena(&arena_for(s)), ci0(0), off0(0) {}
+void* Scratch::get_bytes(size_t b) {
+    void* p = nullptr;
+    cudaMalloc(&p, b);
+    return p;
+}
 Scratch::~Scratch() {}
 }  // namespace mmm_cu
 using namespace mmm_cu;
