@@ -5,20 +5,29 @@ mod-p coefficient operations per second).
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                     [--workload gcd|mul|div|ntt|ntt_batch|batch] [--s S]
 
-Default workload: BASELINE.json configs[1] -- the Euclidean GCD of
-a = g*u, b = g*v over p = 469762049 (deg a = 12288, deg b = 12287, seed 42),
-one instance per GPU.  The unit of work ("coefficient update") is the
-oracle's: for every head elimination of the Euclidean run, deg(divisor)+1
-coefficient updates (oracle.cpp:63-64); 134,225,920 for this input.
+Default workload: BASELINE.json configs[4] (cfg5) -- 4096 products of
+4096 x 4096 terms plus 4096 divisions of 8192 by 4096 terms over
+p = 469762049, seed 42: the largest single-GPU config and the one the
+north star shards across 1/2/4/8 GPUs.  Instances split evenly over the
+ranks; each rank's kernels store their rows into every rank's results
+(symmetric memory over NVLink, fan-out epilogues), NCCL all-gather as the
+validated fallback.  The unit of work is the modular coefficient MAC:
+n^2 per product, (n+1) n per division.  `--workload gcd`
+(configs[1]), `mul`, `div`, `div_fast`, `ntt`, `ntt_batch` time the others.
+
+    python bench.py --gpus N ...   # N > 1 re-launches itself under torchrun
+                                   # (one process per GPU); under torchrun,
+                                   # WORLD_SIZE must equal --gpus
 
 One JSON line on rank 0.  `value` = device time of the CUDA path with inputs
 resident in HBM (CUDA events on the launch stream, L2 flushed between timed
 steps, max over ranks); `e2e` = the same metric through the host-buffer C-ABI
-call (mmm_cu_gcd: H2D of the inputs, kernel, D2H of the result inside the
-timed region); `roofline` = the dominant kernel vs the measured peak;
-`cpu_baseline` = the reference oracle (oracle/_ref, else the C port) on the
-host cores.  `--impl reference` times the reference's CPU implementation of
-the same workload on all host threads (rank 0 only).
+calls (H2D of the inputs, kernels, D2H of the results inside the timed
+region); `roofline` = the dominant kernel (per-kernel CUDA events) vs its
+peak; `cpu_baseline` = the reference oracle (oracle/_ref, else the C port) on
+one host core.  `--impl reference` times the reference's CPU implementation
+of the same workload on all host threads (rank 0 only), with inputs drawn
+through the reference itself.
 """
 from __future__ import annotations
 
@@ -54,11 +63,15 @@ def log(*a):
 
 # --------------------------------------------------------------- plumbing --
 class Dist:
-    def __init__(self, impl: str):
+    """One process per GPU (torchrun env).  Our arm at N > 1: NCCL process
+    group (max-over-ranks timing, barriers, the gather fallback); `backend`
+    "gloo" runs the same plumbing on CPU (--launcher-check)."""
+
+    def __init__(self, impl: str, backend: str = "nccl"):
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.rank = int(os.environ.get("RANK", "0"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
-        self.pg = None
+        self.pg, self.backend = None, backend
         # MMM_BENCH_PEER=1: a process group even at N = 1, so the symmetric-memory
         # fan-out path (PeerOutputs) can be exercised on one GPU
         if impl == "ours" and (self.world > 1 or os.environ.get("MMM_BENCH_PEER")):
@@ -66,22 +79,35 @@ class Dist:
             if self.world == 1:
                 os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
                 os.environ.setdefault("MASTER_PORT", "29533")
-            dist.init_process_group("nccl", device_id=None, rank=self.rank,
-                                    world_size=self.world)
+            dist.init_process_group(backend, rank=self.rank, world_size=self.world)
             self.pg = dist
+
+    def _dev(self):
+        return "cuda" if self.backend == "nccl" else "cpu"
 
     def max(self, x: float) -> float:
         if self.pg is None:
             return x
         import torch
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device=self._dev())
         self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum(self, x: float) -> float:
+        if self.pg is None:
+            return x
+        import torch
+        t = torch.tensor([x], dtype=torch.float64, device=self._dev())
+        self.pg.all_reduce(t)
         return float(t.item())
 
     def barrier(self):
         if self.pg is not None:
-            import torch
-            self.pg.barrier(device_ids=[torch.cuda.current_device()])
+            if self.backend == "nccl":
+                import torch
+                self.pg.barrier(device_ids=[torch.cuda.current_device()])
+            else:
+                self.pg.barrier()
 
     def close(self):
         if self.pg is not None:
@@ -149,22 +175,20 @@ def digest(x) -> str:
     return hashlib.sha256(a.tobytes()).hexdigest()[:16] if a.size else ""
 
 
-def ncu_traffic(kernel_prefix):
-    """DRAM read+write bytes per launch of `kernel_prefix` from the latest
-    committed `ncu --set full` capture summary (profiles/r*_kernels.csv)."""
-    import csv
-    import glob
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_kernels.csv")))
-    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-    for f in reversed(files):
-        got = {}
-        for row in csv.DictReader(open(f)):
-            if kernel_prefix in row["kernel"].split("(")[0] and \
-                    row["metric"] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
-                got[row["metric"]] = float(row["value"]) * scale.get(row["unit"], 1)
-        if len(got) == 2:
-            return got["dram__bytes_read.sum"] + got["dram__bytes_write.sum"], os.path.basename(f)
-    return None, None
+TRAFFIC = os.path.join(ROOT, "profiles", "traffic.json")
+
+
+def ncu_traffic(workload, kernel):
+    """DRAM read+write bytes per launch of `kernel` in the ncu --set full
+    capture of THIS workload's bench command (profiles/traffic.json, written by
+    tools/ncu_traffic.py from the committed capture summaries): keyed by
+    workload and kernel, never matched across captures."""
+    try:
+        with open(TRAFFIC) as fh:
+            t = json.load(fh)[workload][kernel]
+        return float(t["dram_bytes_per_launch"]), t["capture"]
+    except (OSError, KeyError, ValueError, TypeError):
+        return None, None
 
 
 def peaks():
@@ -177,6 +201,28 @@ def peaks():
         with open(IMAD_PEAKS) as fh:
             imad = float(json.load(fh)["imad_wide_per_s"])
     return hbm, src, imad
+
+
+IMAD_PEAK_SOURCE = ("builder-measured IMAD.WIDE.U32 rate (tools/peaks.cu -> profiles/peaks.json; "
+                    "MEASURED_PEAKS.json has no integer peak)")
+
+
+def imad_nominal(mhz=1965.0, sms=148):
+    """Nominal IMAD.WIDE.U32 issue rate: 32 lanes/clk/SM (half the 64-lane
+    IMAD rate) x 148 SMs x the max SM clock."""
+    return 32.0 * sms * mhz * 1e6
+
+
+def imad_line(macs, t, imad):
+    """Roofline entry for an IMAD.WIDE-bound kernel: `macs` modular MACs in t s."""
+    peak = imad or 8.0647e12
+    ach = macs / t
+    nom = imad_nominal()
+    return {"bound": "imad", "achieved": ach / 1e12, "peak": peak / 1e12, "unit": "TMAC/s",
+            "frac": ach / peak, "peak_source": IMAD_PEAK_SOURCE,
+            "peak_nominal": nom / 1e12, "frac_nominal": ach / nom,
+            "peak_nominal_source": "32 IMAD.WIDE lanes/clk/SM x 148 SMs x 1965 MHz",
+            "traffic": None}
 
 
 def imad_rate():
@@ -211,10 +257,13 @@ def ntt_roofline(logN, count, t_step, kernel):
                          "IMAD.HI/IMAD.WIDE count as 2 slots"}
 
 
-class ProductRng:
+class OursGen:
+    """Inputs through the product's own host generator (libmmm_cu: mmm_rng_*,
+    std::mt19937_64 + the reference's random_poly draws) and its GPU product."""
+
     def __init__(self, seed):
         import paper_1402_0264_b200 as mmm
-        self.g = mmm.Rng(seed)
+        self.mmm, self.g = mmm, mmm.Rng(seed)
 
     def next(self):
         return self.g()
@@ -222,14 +271,87 @@ class ProductRng:
     def random_poly(self, terms, p):
         return self.g.random_poly(terms, p)
 
+    def mul(self, a, b, p):
+        return self.mmm.mul(a, b, p)
+
+    def monic(self, a, p):
+        return self.mmm.mul(a, [self.mmm.Field(p).inv(int(a[-1]))], p)
+
+
+class RefGen:
+    """Inputs through the reference oracle only (oracle/_ref: ref_rng_*,
+    ref_random_poly, ref_mul, ref_inv -- the reference's own random_poly and
+    oracle_mul), else its C restatement: the reference arm never loads the
+    product library."""
+
+    def __init__(self, seed):
+        from oracle import pyoracle
+        self.orc, self.kind = _oracle()
+        if self.kind == "reference":
+            self.h = self.orc.rng_new(seed)
+        else:
+            import ctypes as C
+            lib = self.orc.lib
+            lib.orc_mt_seed.argtypes = [C.c_void_p, C.c_uint64]
+            lib.orc_mt_next.argtypes = [C.c_void_p]
+            lib.orc_mt_next.restype = C.c_uint64
+            lib.orc_random_poly.argtypes = [C.c_void_p, C.c_int64, C.c_int64,
+                                            C.POINTER(C.c_int64)]
+            self.h = C.create_string_buffer(312 * 8 + 64)
+            lib.orc_mt_seed(self.h, seed)
+        self.pyoracle = pyoracle
+
+    def next(self):
+        if self.kind == "reference":
+            return self.orc.rng_next(self.h)
+        return self.orc.lib.orc_mt_next(self.h)
+
+    def random_poly(self, terms, p):
+        import ctypes as C
+        out = np.zeros(terms, dtype=np.int64)
+        ptr = out.ctypes.data_as(C.POINTER(C.c_int64))
+        st = (self.orc._random_poly(self.h, terms, p, ptr) if self.kind == "reference"
+              else self.orc.lib.orc_random_poly(self.h, terms, p, ptr))
+        assert st == 0, "random_poly"
+        return out
+
+    def mul(self, a, b, p):
+        return self.orc.mul(a, b, p)
+
+    def monic(self, a, p):
+        return self.orc.mul(a, [self.orc.inv_raw(int(a[-1]), p)], p)
+
 
 # -------------------------------------------------------------- workloads --
 class Workload:
+    """One BASELINE config.  __init__(s, gen) draws the seeded inputs through
+    `gen` (OursGen for our arm, RefGen for the reference arm) and checks them
+    against the reference's input digests; attach(mmm) binds the product
+    library for our arm only."""
+
     name = ""
     config = {}
 
+    mark_events = None  # list while the timed region records per-kernel events
+    last_part = None    # label of the segment after the last mark
+
+    def attach(self, mmm):
+        self.mmm = mmm
+
+    def _mark(self, label):
+        """End of a kernel's segment of the step (CUDA event on the launch stream)."""
+        if self.mark_events is not None:
+            import torch
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record(self.tstream)
+            self.mark_events.append((label, ev))
+
     def units(self) -> float:  # coeff-ops per instance-step
         raise NotImplementedError
+
+    def cpu_ref_kind(self, kind):
+        """kind of the CPU sample cpu_ref() runs ("reference" or "port")."""
+        return kind
 
 
 def try_peer_outputs(work, sizes):
@@ -275,17 +397,11 @@ class GcdWork(Workload):
 
     name = "gcd"
 
-    def __init__(self, s):
-        import paper_1402_0264_b200 as mmm
-        self.mmm, self.s = mmm, s or 128
+    def __init__(self, s, gen):
+        self.s = s or 128
         gold = golden()["cfg2"]
-        rng = ProductRng(42)
-        g = mmm.Field(P)
-        gp = rng.random_poly((1 << 12) + 1, P)
-        gp = mmm.mul(gp, [g.inv(int(gp[-1]))], P)  # monic(g)
-        u = rng.random_poly((1 << 13) + 1, P)
-        v = rng.random_poly(1 << 13, P)
-        self.a, self.b = mmm.mul(gp, u, P), mmm.mul(gp, v, P)
+        c = suites.cfg2(gen, gen.mul, gen.monic)
+        self.a, self.b = c["a"].astype(np.uint32), c["b"].astype(np.uint32)
         assert (digest(self.a), digest(self.b)) == (gold["a"], gold["b"]), "cfg2 inputs"
         self.want = gold["g"]
         self.steps_, self.updates, self.ng = gold["steps"], gold["updates"], gold["deg_g"] + 1
@@ -327,7 +443,7 @@ class GcdWork(Workload):
     def host_check(self, g):
         assert digest(g) == self.want
 
-    def roofline(self, t_step, hbm, imad):
+    def roofline(self, t_step, hbm, imad, parts=None):
         alg = 4.0 * (len(self.a) + len(self.b) + self.ng)  # inputs read once, gcd written once
         achieved = alg / t_step / 1e9
         return {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
@@ -392,10 +508,9 @@ class MulWork(Workload):
     name = "mul"
     sharded = True
 
-    def __init__(self, s):
-        import paper_1402_0264_b200 as mmm
-        self.mmm, self.s = mmm, s or 4  # s = 4: fastest in the sweep (PAPER.md:1781 too)
-        c = suites.cfg1(ProductRng(42))
+    def __init__(self, s, gen):
+        self.s = s or 4  # s = 4: fastest in the sweep (PAPER.md:1781 too)
+        c = suites.cfg1(gen)
         self.a, self.b = c["a"], c["b"]
         self.want = golden()["cfg1"]["f"]
         self.nf = len(self.a) + len(self.b) - 1
@@ -478,16 +593,13 @@ class MulWork(Workload):
     def host_check(self, f):
         assert digest(f) == self.want
 
-    def roofline(self, t_step, hbm, imad):
+    def roofline(self, t_step, hbm, imad, parts=None):
         from paper_1402_0264_b200.shard import range_work
         macs = float(range_work(len(self.a), len(self.b), self.k0, self.k1))  # this rank
-        achieved = macs / t_step / 1e12
-        peak = (imad or 7.35e12) / 1e12
-        return {"bound": "imad", "achieved": achieved, "peak": peak, "unit": "TMAC/s",
-                "frac": achieved / peak, "traffic": None, "kernel": "mul_kernel",
-                "alg_macs_per_launch": macs,
-                "note": "integer pipe: one IMAD.WIDE.U32 per modular MAD; peak = measured "
-                        "IMAD.WIDE.U32 rate (profiles/peaks.json); no tensor cores"}
+        r = imad_line(macs, t_step, imad)
+        r.update(kernel="mul_kernel", alg_macs_per_launch=macs,
+                 note="integer pipe: one IMAD.WIDE.U32 per modular MAD; no tensor cores")
+        return r
 
     def cpu_ref(self, orc):
         a, b = self.a.astype(np.int64), self.b.astype(np.int64)
@@ -500,10 +612,9 @@ class DivWork(Workload):
 
     name = "div"
 
-    def __init__(self, s):
-        import paper_1402_0264_b200 as mmm
-        self.mmm, self.s = mmm, s or 128
-        c = suites.cfg3(ProductRng(42))
+    def __init__(self, s, gen):
+        self.s = s or 128
+        c = suites.cfg3(gen)
         self.a, self.b = c["a"], c["b"]
         g = golden()["cfg3"]
         self.want = (g["q"], g["r"])
@@ -541,14 +652,14 @@ class DivWork(Workload):
     def host_check(self, qr):
         assert (digest(qr[0]), digest(qr[1])) == self.want
 
-    def roofline(self, t_step, hbm, imad):
+    def roofline(self, t_step, hbm, imad, parts=None):
         alg = 4.0 * (len(self.a) + len(self.b) + self.nq + self.nr)
         achieved = alg / t_step / 1e9
         return {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                 "frac": achieved / hbm, "traffic": None,
                 "kernel": "div_pipe_kernel" if self.s >= 32 else "div_grid_kernel",
                 "alg_bytes_per_launch": alg,
-                "imad_frac": self.units() / t_step / (imad or 7.35e12),
+                "imad_frac": self.units() / t_step / (imad or 8.0647e12),
                 "binding": f"{-(-self.nq // self.s)} dependent steps of s={self.s} heads "
                            "(pipelined head CTA for s >= 32)"}
 
@@ -565,8 +676,8 @@ class FastDivWork(DivWork):
 
     name = "div_fast"
 
-    def __init__(self, s):
-        super().__init__(s)
+    def __init__(self, s, gen):
+        super().__init__(s, gen)
         self.config.update(workload="cfg3_divmod_fast_newton_ntt_deg2^16_by_deg2^15_p469762049",
                            units="schoolbook-equivalent updates")
         self.config.pop("s", None)
@@ -579,7 +690,7 @@ class FastDivWork(DivWork):
     def host_step(self):
         return self.mmm.divmod_fast(self.ha, self.hb, P)
 
-    def roofline(self, t_step, hbm, imad):
+    def roofline(self, t_step, hbm, imad, parts=None):
         alg = 4.0 * (len(self.a) + len(self.b) + self.nq + self.nr)
         achieved = alg / t_step / 1e9
         return {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
@@ -597,10 +708,8 @@ class NttWork(Workload):
     name = "ntt"
     sharded = True
 
-    def __init__(self, s):
-        import paper_1402_0264_b200 as mmm
-        self.mmm = mmm
-        c = suites.cfg4_big(ProductRng(42))
+    def __init__(self, s, gen):
+        c = suites.cfg4_big(gen)
         self.a, self.b = c["a"], c["b"]
         self.want = golden()["cfg4_big"].get("f")
         self.nf = len(self.a) + len(self.b) - 1
@@ -656,7 +765,7 @@ class NttWork(Workload):
         if self.want:
             assert digest(f) == self.want
 
-    def roofline(self, t_step, hbm, imad):
+    def roofline(self, t_step, hbm, imad, parts=None):
         r = ntt_roofline(21, 1, t_step, "ntt_rows")
         if self.world > 1:  # this rank's share of the transform work
             r["achieved"] /= self.world
@@ -665,6 +774,9 @@ class NttWork(Workload):
         r["hbm"] = {"achieved_gbs": alg / t_step / 1e9, "peak_gbs": hbm,
                     "frac": alg / t_step / 1e9 / hbm, "alg_bytes": alg}
         return r
+
+    def cpu_ref_kind(self, kind):
+        return "port"  # the reference has no output-range routine: the C restatement runs
 
     def cpu_ref(self, orc):
         # bounded sample: 2^12 middle output words of the product, computed
@@ -712,12 +824,10 @@ class NttBatchWork(_Sharded):
 
     name = "ntt_batch"
 
-    def __init__(self, s):
-        import paper_1402_0264_b200 as mmm
-        self.mmm, self.count = mmm, 256
-        rng = ProductRng(42)
-        suites.cfg4_big(rng)  # same stream: the batch follows the big pair
-        c = suites.cfg4_batch(rng)
+    def __init__(self, s, gen):
+        self.count = 256
+        suites.cfg4_big(gen)  # same stream: the batch follows the big pair
+        c = suites.cfg4_batch(gen)
         self.A, self.B = c["A"].astype(np.uint32), c["B"].astype(np.uint32)
         gold = golden()["cfg4_batch"]
         self.want = gold["f_all"]
@@ -781,7 +891,7 @@ class NttBatchWork(_Sharded):
         if self.world == 1:
             assert self._digest_rows(F) == self.want
 
-    def roofline(self, t_step, hbm, imad):
+    def roofline(self, t_step, hbm, imad, parts=None):
         n_local = self.hi - self.lo
         r = ntt_roofline(16, n_local, t_step, "ntt_rows")
         alg = 4.0 * n_local * (2 * self.na + self.nf)
@@ -802,10 +912,9 @@ class BatchWork(_Sharded):
 
     name = "batch"
 
-    def __init__(self, s):
-        import paper_1402_0264_b200 as mmm
-        self.mmm, self.count, self.s = mmm, 4096, s or 0
-        c = suites.cfg5(ProductRng(42))
+    def __init__(self, s, gen):
+        self.count, self.s = 4096, s or 0
+        c = suites.cfg5(gen)
         self.A, self.B = c["A"].astype(np.uint32), c["B"].astype(np.uint32)
         self.C, self.D = c["C"].astype(np.uint32), c["D"].astype(np.uint32)
         gold = golden()["cfg5"]
@@ -846,6 +955,7 @@ class BatchWork(_Sharded):
             self.mmm.mul_batched_fanout_dev(P, self.dA.data_ptr(), n, n, self.dB.data_ptr(), n,
                                             n, k, pe.ptrs(0, lo * (2 * n - 1)), 2 * n - 1,
                                             s=self.s or 8, stream=stream)
+            self._mark("mul_kernel")
             self.mmm.divmod_batched_fanout_dev(P, self.dC.data_ptr(), 2 * n, 2 * n,
                                                self.dD.data_ptr(), n, n, k,
                                                pe.ptrs(1, lo * (n + 1)), n + 1,
@@ -859,6 +969,7 @@ class BatchWork(_Sharded):
             return
         self.mmm.mul_batched_dev(P, self.dA.data_ptr(), n, n, self.dB.data_ptr(), n, n, k,
                                  self.dF.data_ptr(), 2 * n - 1, s=self.s or 8, stream=stream)
+        self._mark("mul_kernel")
         self.mmm.divmod_batched_dev(P, self.dC.data_ptr(), 2 * n, 2 * n, self.dD.data_ptr(), n,
                                     n, k, self.dQ.data_ptr(), n + 1, self.dR.data_ptr(), n - 1,
                                     s=self.s or 64, stream=stream)
@@ -897,19 +1008,37 @@ class BatchWork(_Sharded):
                                        r_out=self.hR)
         return F, Q, R
 
+    def host_step_default(self):
+        F = self.mmm.mul_batched(self.hA, self.hB, P, s=self.s or 8)
+        Q, R = self.mmm.divmod_batched(self.hC, self.hD, P, s=self.s or 64)
+        return F, Q, R
+
     def host_check(self, out):
         if self.world == 1:
             assert self._digests(*out) == self.want
 
-    def roofline(self, t_step, hbm, imad):
+    last_part = "div_cta_kernel"
+
+    def roofline(self, t_step, hbm, imad, parts=None):
+        """Per kernel (CUDA events between the two launches of each step):
+        algorithmic modular MACs of this rank's share (mul: n^2 per product;
+        div: (n+1) n per division, SURVEY §8d) over the kernel's mean time;
+        the dominant kernel is the headline.  With a gather, it rides in the
+        division's segment (the barrier after it)."""
         k, n = self.hi - self.lo, self.n
-        macs = float(k) * (n * n + (n + 1) * n)
-        achieved = macs / t_step / 1e12
-        peak = (imad or 7.35e12) / 1e12
-        return {"bound": "imad", "achieved": achieved, "peak": peak, "unit": "TMAC/s",
-                "frac": achieved / peak, "traffic": None, "kernel": "mul_kernel+div_cta_kernel",
-                "alg_macs_per_launch": macs,
-                "note": "per-rank MACs over the step time incl. the NCCL gather"}
+        work = {"mul_kernel": float(k) * n * n, "div_cta_kernel": float(k) * (n + 1) * n}
+        parts = parts or {"mul_kernel+div_cta_kernel": t_step}
+        if "mul_kernel+div_cta_kernel" in parts:
+            work = {"mul_kernel+div_cta_kernel": sum(work.values())}
+        out = {}
+        for name, t in parts.items():
+            out[name] = imad_line(work[name], t, imad)
+            out[name]["ms"] = t * 1e3
+        dom = max(parts, key=lambda x: parts[x])
+        r = dict(out[dom])
+        r.update(kernel=dom, parts=out, alg_macs_per_launch=work[dom],
+                 alg_unit="modular MACs (one IMAD.WIDE.U32 each)")
+        return r
 
     def cpu_ref(self, orc):
         gold = golden()["cfg5"]
@@ -938,13 +1067,15 @@ def run_ours(args, dist):
     torch.cuda.set_device(dist.local)
     import paper_1402_0264_b200 as mmm
     mmm.load()
-    work = WORKLOADS[args.workload](args.s)
+    work = WORKLOADS[args.workload](args.s, OursGen(42))
+    work.attach(mmm)
     sharded = getattr(work, "sharded", False)
     if sharded:
         work.bind(dist)
     work.device_setup()
     stream = torch.cuda.current_stream()
     sp = stream.cuda_stream
+    work.tstream = stream
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     for _ in range(args.warmup):
         work.device_step(sp)
@@ -952,28 +1083,39 @@ def run_ours(args, dist):
     work.device_check()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
+    marks = [[] for _ in range(args.steps)]
     dist.barrier()
     torch.cuda.synchronize()
     n0 = mmm.launch_count()
     with Clocks(torch.cuda.current_device()) as clk:
-        for e0, e1 in ev:
+        for (e0, e1), mk in zip(ev, marks):
             # flush L2: write a 256 MB buffer (> L2), then read it back so the
             # L2 is left holding clean lines -- otherwise the timed kernels pay
             # for writing back up to 126 MB of the flush's dirty lines
             flush.zero_()
-            flush_sum = flush.view(torch.int32).sum()
+            flush_sum = flush.view(torch.int32).sum()  # noqa: F841
             e0.record(stream)
+            work.mark_events = mk
             work.device_step(sp)
+            work.mark_events = None
             e1.record(stream)
         torch.cuda.synchronize()
         launches = mmm.launch_count() - n0
-        # keep the sampler alive over a comparable busy window for short runs
         t_dev = sum(e0.elapsed_time(e1) for e0, e1 in ev) / 1e3
     dist.barrier()
     torch.cuda.synchronize()
     work.device_check()
     t_dev = dist.max(t_dev)
     t_step = t_dev / args.steps
+    # per-kernel segments of the step (this rank), for the roofline's dominant kernel
+    parts = None
+    if marks[0]:
+        parts = {}
+        for (e0, e1), mk in zip(ev, marks):
+            prev = e0
+            for label, e in mk + [(work.last_part, e1)]:
+                parts[label] = parts.get(label, 0.0) + prev.elapsed_time(e) / 1e3 / args.steps
+                prev = e
     # replicas: every rank ran the whole instance; sharded: the ranks split it
     value = (1 if sharded else dist.world) * work.units() / t_step
 
@@ -990,12 +1132,22 @@ def run_ours(args, dist):
     work.host_check(out)
     e2e = {"value": (1 if sharded else dist.world) * work.units() / t_e2e, "unit": UNIT,
            "h2d_bytes_per_step": work.bytes_in, "d2h_bytes_per_step": work.bytes_out,
-           "ms_per_step": t_e2e * 1e3}
+           "ms_per_step": t_e2e * 1e3,
+           "how": "the host C-ABI call a user makes (host buffers; H2D, kernels, D2H and "
+                  "input validation inside the timed region), pinned result arrays"}
+    if hasattr(work, "host_step_default") and dist.world == 1:
+        work.host_step_default()
+        t0 = time.perf_counter()
+        n_def = 3
+        for _ in range(n_def):
+            work.host_step_default()
+        e2e["default_out_ms_per_step"] = (time.perf_counter() - t0) / n_def * 1e3
+        e2e["default_out_note"] = "same call with out=None (library-allocated pageable results)"
 
     hbm, src, imad = peaks()
-    roof = work.roofline(t_step, hbm, imad)
-    roof["peak_source"] = src
-    traffic, tsrc = ncu_traffic(roof["kernel"].split("+")[0])
+    roof = work.roofline(t_step, hbm, imad, parts=parts)
+    roof.setdefault("peak_source", src)
+    traffic, tsrc = ncu_traffic(work.name, roof["kernel"])
     if traffic is not None:
         roof["traffic"], roof["traffic_source"] = traffic, tsrc
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": dist.world,
@@ -1013,6 +1165,9 @@ def run_ours(args, dist):
 
 
 def _oracle():
+    """The reference oracle compiled unmodified (oracle/_ref), else its C
+    restatement; (backend, kind).  Test infrastructure: only the cpu_baseline
+    leg and the reference arm call it."""
     from oracle import pyoracle
     if pyoracle.reference_available():
         return pyoracle.Reference(), "reference"
@@ -1023,7 +1178,8 @@ def _oracle():
 def cpu_baseline(work, seconds):
     """The CPU oracle on this host, rank 0, one core, a bounded sample."""
     orc, kind = _oracle()
-    fn, units, ok, what = work.cpu_ref(orc)
+    fn, units, ok, what = work.cpu_ref(orc)[:4]
+    kind = work.cpu_ref_kind(kind)
     fn()  # warm
     n, t0 = 0, time.perf_counter()
     while time.perf_counter() - t0 < seconds or n == 0:
@@ -1036,18 +1192,23 @@ def cpu_baseline(work, seconds):
 
 
 def run_reference(args, dist):
-    """The reference's own CPU path (oracle/_ref, else the C port) on the
-    workload of our arm.  Single-instance configs: the reference algorithm is
-    serial (oracle_gcd / oracle_divmod / oracle_mul), so one instance per step
-    on one thread -- all the threads it can use.  Batched configs: one
-    instance per host thread per step (a bounded sample of the batch)."""
+    """The reference's own CPU path on the workload of our arm: the reference
+    oracle compiled unmodified (oracle/_ref; its C restatement only if that is
+    missing, and for the NTT sample, which has no reference routine -> kind
+    "port").  Inputs are drawn through the reference's own random_poly and
+    oracle_mul (RefGen); this arm never loads the product library.
+    Single-instance configs: the reference algorithm is serial, so one
+    instance per step on one thread.  Batched configs: one instance per host
+    thread per step (a bounded sample of the batch).  Rank 0 only."""
     if dist.rank != 0:
         return None
-    work = WORKLOADS[args.workload](args.s)
-    orc, kind = _oracle()
+    gen = RefGen(42)
+    work = WORKLOADS[args.workload](args.s, gen)
+    orc, kind = gen.orc, gen.kind
+    kind = work.cpu_ref_kind(kind)
     batched = getattr(work, "sharded", False)
     cores = (os.cpu_count() or 1) if batched else 1
-    fn, units, ok, what = work.cpu_ref(orc)
+    fn, units, ok, what = work.cpu_ref(orc)[:4]
 
     def step():
         if cores == 1:
@@ -1077,18 +1238,59 @@ def run_reference(args, dist):
                     "d2h_bytes_per_step": 0}}
 
 
+def launcher_check(args, dist):
+    """CPU check of the N-rank launch (gloo): every rank joins, max/sum over
+    ranks work; rank 0 reports what a bench line would carry."""
+    ranks = dist.sum(1.0)
+    slowest = dist.max(float(dist.rank))
+    dist.barrier()
+    return {"launcher_check": True, "n_gpus": dist.world, "ranks_joined": int(ranks),
+            "max_rank": int(slowest), "backend": dist.backend, "impl": args.impl}
+
+
+def _free_port():
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="gcd")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="batch")
     ap.add_argument("--s", type=int, default=0)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--launcher-check", action="store_true",
+                    help="CPU: launch the ranks over gloo and report them (no GPU work)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch this command under torchrun
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+               f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        log(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}; refusing to time a "
+            "different number of ranks than asked for")
+        sys.exit(2)
+    if args.launcher_check:
+        dist = Dist("ours" if world > 1 else "none", backend="gloo")
+        try:
+            line = launcher_check(args, dist)
+            if dist.rank == 0:
+                print(json.dumps(line), flush=True)
+        finally:
+            dist.close()
+        return
     dist = Dist(args.impl)
     try:
         line = run_ours(args, dist) if args.impl == "ours" else run_reference(args, dist)

@@ -30,9 +30,9 @@
  * zero polynomial, gcd of two zeros, inverse of zero), as the oracle throws
  * them (oracle.cpp:52,71; field.cpp:28).
  *
- * Threading: pure functions without global state; host entry points run on a
- * per-thread CUDA stream of the current device and are safe to call
- * concurrently.  Device entry points are asynchronous on the
+ * Threading: pure functions without global state; host entry points run on the
+ * calling thread's CUDA stream of the current device (one per thread and
+ * device) and are safe to call concurrently.  Device entry points are asynchronous on the
  * caller's stream (a cudaStream_t passed as void*; NULL = legacy default).
  */
 #ifndef MMM_CU_H
@@ -58,6 +58,13 @@ const char* mmm_last_error(void);
 int mmm_version(void);
 /* Number of CUDA kernels this library has launched in this process. */
 uint64_t mmm_cu_launch_count(void);
+/* Frees the calling thread's per-device streams, scratch arenas, zero buffers
+ * and pinned staging (waiting for their queued work first).  They are also
+ * freed when the thread exits; the next call recreates them. */
+int mmm_cu_release_scratch(void);
+/* mmm_cu_release_scratch() plus the process-wide NTT plans, after
+ * synchronising every device.  No other thread may have calls in flight. */
+int mmm_cu_release_all(void);
 
 /* ---- field and inputs (host) ------------------------------------------- */
 int mmm_field_check(int64_t p);
@@ -178,6 +185,47 @@ int mmm_cu_divmod_batched_fanout_dev(int64_t p, const uint32_t* d_A, int64_t lda
                                      int64_t s, uint32_t* const* d_Q, int64_t ldq,
                                      uint32_t* const* d_R, int64_t ldr, int32_t n_out,
                                      void* stream);
+
+/* ---- one process, several GPUs (no PyTorch, no NCCL) ---------
+ * `devices` lists n_dev device ordinals; the `count` independent instances are
+ * split into contiguous near-equal shares, share r on devices[r] (a device may
+ * repeat: its shares then run on separate streams).
+ *
+ * Host-buffer versions: one worker thread per share runs the single-device
+ * host entry point on its rows (H2D of its share, kernels, D2H of its rows),
+ * all devices concurrently; synchronous, same validation and errors as the
+ * single-device calls (a failing share's status and message are returned). */
+int mmm_cu_mul_batched_multi(int64_t p, const uint32_t* A, int64_t lda, int64_t na,
+                             const uint32_t* B, int64_t ldb, int64_t nb, int64_t count, int64_t s,
+                             uint32_t* F, int64_t ldf, const int32_t* devices, int32_t n_dev);
+int mmm_cu_divmod_batched_multi(int64_t p, const uint32_t* A, int64_t lda, int64_t na,
+                                const uint32_t* B, int64_t ldb, int64_t nb, int64_t count,
+                                int64_t s, uint32_t* Q, int64_t ldq, uint32_t* R, int64_t ldr,
+                                const int32_t* devices, int32_t n_dev);
+int mmm_cu_ntt_mul_batched_multi(int64_t p, const uint32_t* A, int64_t lda, int64_t na,
+                                 const uint32_t* B, int64_t ldb, int64_t nb, int64_t count,
+                                 uint32_t* F, int64_t ldf, const int32_t* devices, int32_t n_dev);
+/* Device-buffer versions: inputs and outputs live on the root devices[0] and
+ * `stream` is a stream of the root.  Each share's inputs are copied from the
+ * root over NVLink (peer copies), its kernel stores its rows straight into the
+ * root's outputs through peer access (fan-out epilogue: the gather is fused
+ * into the producing kernel; the NTT batch pushes its rows with one copy), and
+ * `stream` waits on every device (events).  Asynchronous on `stream`.  Peer
+ * access is enabled on first use; MMM_CUDA_ERROR if a device cannot reach the
+ * root. */
+int mmm_cu_mul_batched_multi_dev(int64_t p, const uint32_t* d_A, int64_t lda, int64_t na,
+                                 const uint32_t* d_B, int64_t ldb, int64_t nb, int64_t count,
+                                 int64_t s, uint32_t* d_F, int64_t ldf, const int32_t* devices,
+                                 int32_t n_dev, void* stream);
+int mmm_cu_divmod_batched_multi_dev(int64_t p, const uint32_t* d_A, int64_t lda, int64_t na,
+                                    const uint32_t* d_B, int64_t ldb, int64_t nb, int64_t count,
+                                    int64_t s, uint32_t* d_Q, int64_t ldq, uint32_t* d_R,
+                                    int64_t ldr, const int32_t* devices, int32_t n_dev,
+                                    void* stream);
+int mmm_cu_ntt_mul_batched_multi_dev(int64_t p, const uint32_t* d_A, int64_t lda, int64_t na,
+                                     const uint32_t* d_B, int64_t ldb, int64_t nb, int64_t count,
+                                     uint32_t* d_F, int64_t ldf, const int32_t* devices,
+                                     int32_t n_dev, void* stream);
 
 #ifdef __cplusplus
 }

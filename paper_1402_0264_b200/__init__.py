@@ -34,6 +34,9 @@ __all__ = [
     "divmod_fast", "divmod_fast_dev", "ntt_shape", "ntt_phase_dev",
     "ntt_mul_dev",
     "mul_batched_dev", "divmod_batched_dev", "ntt_mul_batched_dev", "launch_count",
+    "mul_batched_multi", "divmod_batched_multi", "ntt_mul_batched_multi",
+    "mul_batched_multi_dev", "divmod_batched_multi_dev", "ntt_mul_batched_multi_dev",
+    "release_scratch",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -64,6 +67,7 @@ _ERR = {1: InvalidArgument, 2: DomainError, 3: CudaError, 4: MmmError, 5: SimErr
 
 _U32P = C.POINTER(C.c_uint32)
 _I64P = C.POINTER(C.c_int64)
+_I32P = C.POINTER(C.c_int32)
 _I64 = C.c_int64
 _VP = C.c_void_p
 
@@ -72,6 +76,8 @@ SIGNATURES = {
     "mmm_last_error": (C.c_char_p, []),
     "mmm_version": (C.c_int, []),
     "mmm_cu_launch_count": (C.c_uint64, []),
+    "mmm_cu_release_scratch": (C.c_int, []),
+    "mmm_cu_release_all": (C.c_int, []),
     "mmm_field_check": (C.c_int, [_I64]),
     "mmm_field_inv": (C.c_int, [_I64, _I64, _I64P]),
     "mmm_rng_create": (_VP, [C.c_uint64]),
@@ -115,6 +121,19 @@ SIGNATURES = {
     "mmm_cu_divmod_batched_fanout_dev": (C.c_int, [_I64, _VP, _I64, _I64, _VP, _I64, _I64, _I64,
                                                    _I64, C.POINTER(C.c_void_p), _I64,
                                                    C.POINTER(C.c_void_p), _I64, C.c_int32, _VP]),
+    "mmm_cu_mul_batched_multi": (C.c_int, [_I64, _U32P, _I64, _I64, _U32P, _I64, _I64, _I64, _I64,
+                                           _U32P, _I64, _I32P, C.c_int32]),
+    "mmm_cu_divmod_batched_multi": (C.c_int, [_I64, _U32P, _I64, _I64, _U32P, _I64, _I64, _I64,
+                                              _I64, _U32P, _I64, _U32P, _I64, _I32P, C.c_int32]),
+    "mmm_cu_ntt_mul_batched_multi": (C.c_int, [_I64, _U32P, _I64, _I64, _U32P, _I64, _I64, _I64,
+                                               _U32P, _I64, _I32P, C.c_int32]),
+    "mmm_cu_mul_batched_multi_dev": (C.c_int, [_I64, _VP, _I64, _I64, _VP, _I64, _I64, _I64, _I64,
+                                               _VP, _I64, _I32P, C.c_int32, _VP]),
+    "mmm_cu_divmod_batched_multi_dev": (C.c_int, [_I64, _VP, _I64, _I64, _VP, _I64, _I64, _I64,
+                                                  _I64, _VP, _I64, _VP, _I64, _I32P, C.c_int32,
+                                                  _VP]),
+    "mmm_cu_ntt_mul_batched_multi_dev": (C.c_int, [_I64, _VP, _I64, _I64, _VP, _I64, _I64, _I64,
+                                                   _VP, _I64, _I32P, C.c_int32, _VP]),
 }
 
 _lib: Optional[C.CDLL] = None
@@ -409,3 +428,70 @@ def fanout_copy_dev(d_src, n, outs, stream=0):
     """n words of d_src into every device buffer of `outs` (one peer-store kernel)."""
     arr, k = _ptrs(outs)
     _check(load().mmm_cu_fanout_copy_dev(d_src, n, arr, k, stream))
+
+
+# ------------------------------------------ several GPUs from one process --
+# `devices`: device ordinals (repeats allowed); the batch splits into
+# contiguous shares, one per entry (include/mmm_cu.h, "several GPUs").
+def _devs(devices):
+    d = np.ascontiguousarray(np.asarray(list(devices), dtype=np.int32))
+    return d.ctypes.data_as(_I32P), d.size, d
+
+
+def mul_batched_multi(A, B, p, devices, s: int = 8, out=None) -> np.ndarray:
+    A, B, p = _u32(A), _u32(B), _pint(p)
+    cnt, na = A.shape
+    nb = B.shape[1]
+    F = _out(out, (cnt, na + nb - 1))
+    dp, nd, _keep = _devs(devices)
+    _check(load().mmm_cu_mul_batched_multi(p, _p(A), na, na, _p(B), nb, nb, cnt, s, _p(F),
+                                           F.shape[1], dp, nd))
+    return F
+
+
+def divmod_batched_multi(A, B, p, devices, s: int = 64):
+    A, B, p = _u32(A), _u32(B), _pint(p)
+    cnt, na = A.shape
+    nb = B.shape[1]
+    Q = np.zeros((cnt, na - nb + 1), dtype=np.uint32)
+    R = np.zeros((cnt, max(nb - 1, 1)), dtype=np.uint32)
+    dp, nd, _keep = _devs(devices)
+    _check(load().mmm_cu_divmod_batched_multi(p, _p(A), na, na, _p(B), nb, nb, cnt, s, _p(Q),
+                                              Q.shape[1], _p(R), R.shape[1], dp, nd))
+    return Q, R[:, : nb - 1]
+
+
+def ntt_mul_batched_multi(A, B, p, devices, out=None) -> np.ndarray:
+    A, B, p = _u32(A), _u32(B), _pint(p)
+    cnt, na = A.shape
+    nb = B.shape[1]
+    F = _out(out, (cnt, na + nb - 1))
+    dp, nd, _keep = _devs(devices)
+    _check(load().mmm_cu_ntt_mul_batched_multi(p, _p(A), na, na, _p(B), nb, nb, cnt, _p(F),
+                                               F.shape[1], dp, nd))
+    return F
+
+
+def mul_batched_multi_dev(p, d_A, lda, na, d_B, ldb, nb, count, d_F, ldf, devices, s=8,
+                          stream=0):
+    dp, nd, _keep = _devs(devices)
+    _check(load().mmm_cu_mul_batched_multi_dev(_pint(p), d_A, lda, na, d_B, ldb, nb, count, s,
+                                               d_F, ldf, dp, nd, stream))
+
+
+def divmod_batched_multi_dev(p, d_A, lda, na, d_B, ldb, nb, count, d_Q, ldq, d_R, ldr, devices,
+                             s=64, stream=0):
+    dp, nd, _keep = _devs(devices)
+    _check(load().mmm_cu_divmod_batched_multi_dev(_pint(p), d_A, lda, na, d_B, ldb, nb, count, s,
+                                                  d_Q, ldq, d_R, ldr, dp, nd, stream))
+
+
+def ntt_mul_batched_multi_dev(p, d_A, lda, na, d_B, ldb, nb, count, d_F, ldf, devices, stream=0):
+    dp, nd, _keep = _devs(devices)
+    _check(load().mmm_cu_ntt_mul_batched_multi_dev(_pint(p), d_A, lda, na, d_B, ldb, nb, count,
+                                                   d_F, ldf, dp, nd, stream))
+
+
+def release_scratch() -> None:
+    """Free this thread's streams, arenas and staging (mmm_cu_release_scratch)."""
+    _check(load().mmm_cu_release_scratch())

@@ -24,16 +24,70 @@ namespace mmm_cu {
 
 std::atomic<uint64_t> g_launches{0};
 
-Arena& arena_for(cudaStream_t s) {
-    static std::mutex mu;
-    static std::map<std::tuple<int, cudaStream_t, std::thread::id>, Arena> arenas;
+namespace {
+
+// Everything the library keeps per host thread: per device, the thread's
+// stream for the host entry points, its scratch arena and its zero buffer; and
+// the pinned staging buffer.  Freed when the thread exits (errors ignored: at
+// process exit the CUDA runtime may already be gone) or by
+// mmm_cu_release_scratch().
+constexpr int MAX_DEV = 64;
+struct DevState {
+    cudaStream_t stream = nullptr;
+    Arena arena;
+    ZeroBuf zero;
+    bool used = false;
+};
+struct ThreadState {
+    DevState dev[MAX_DEV];
+    std::pair<void*, size_t> pinned{nullptr, 0};
+    void release() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        for (int d = 0; d < MAX_DEV; ++d) {
+            DevState& s = dev[d];
+            if (!s.used) continue;
+            cudaSetDevice(d);
+            if (s.arena.last) cudaEventSynchronize(s.arena.last);
+            if (s.zero.last) cudaEventSynchronize(s.zero.last);
+            if (s.stream) cudaStreamSynchronize(s.stream);
+            for (auto& c : s.arena.chunks) cudaFree(c.first);
+            if (s.zero.p) cudaFree(s.zero.p);
+            if (s.arena.last) cudaEventDestroy(s.arena.last);
+            if (s.zero.last) cudaEventDestroy(s.zero.last);
+            if (s.stream) cudaStreamDestroy(s.stream);
+            s = DevState{};
+        }
+        if (pinned.first) cudaFreeHost(pinned.first);
+        pinned = {nullptr, 0};
+        if (cur >= 0) cudaSetDevice(cur);
+    }
+    ~ThreadState() { release(); }
+};
+thread_local ThreadState t_state;
+
+DevState& dev_state() {
     int dev = 0;
-    cudaGetDevice(&dev);
-    std::lock_guard<std::mutex> lock(mu);
-    return arenas[{dev, s, std::this_thread::get_id()}];  // node-based: references stay valid
+    MMM_CUDA(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= MAX_DEV) throw Error(ST_CUDA, "device ordinal out of range");
+    DevState& s = t_state.dev[dev];
+    s.used = true;
+    return s;
 }
 
-Scratch::Scratch(cudaStream_t s) : stream(s), arena(&arena_for(s)) {
+}  // namespace
+
+Arena& arena_for() { return dev_state().arena; }
+
+Scratch::Scratch(cudaStream_t s) : stream(s), arena(&arena_for()) {
+    if (arena->depth++ == 0 && arena->last) {
+        // order this call after the arena's previous user (maybe another stream)
+        cudaError_t e = cudaStreamWaitEvent(stream, arena->last, 0);
+        if (e != cudaSuccess) {
+            --arena->depth;
+            cuda_check(e, "cudaStreamWaitEvent(scratch)");
+        }
+    }
     ci0 = arena->ci;
     off0 = arena->off;
 }
@@ -64,32 +118,46 @@ void* Scratch::get_bytes(size_t bytes) {
 Scratch::~Scratch() {
     arena->ci = ci0;
     arena->off = off0;
+    if (--arena->depth == 0) {
+        if (!arena->last) cudaEventCreateWithFlags(&arena->last, cudaEventDisableTiming);
+        if (arena->last) cudaEventRecord(arena->last, stream);
+    }
 }
 
+unsigned long long* zero_buf_acquire(size_t words, cudaStream_t st) {
+    ZeroBuf& b = dev_state().zero;
+    if (!b.last) MMM_CUDA(cudaEventCreateWithFlags(&b.last, cudaEventDisableTiming));
+    MMM_CUDA(cudaStreamWaitEvent(st, b.last, 0));  // after the buffer's previous user
+    if (b.words < words) {
+        if (b.p) MMM_CUDA(cudaFreeAsync(b.p, st));  // ordered after that user too
+        b.p = nullptr;
+        b.words = 0;
+        const size_t n = std::max(words, size_t(1) << 16);
+        MMM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&b.p), n * sizeof(unsigned long long), st));
+        MMM_CUDA(cudaMemsetAsync(b.p, 0, n * sizeof(unsigned long long), st));
+        b.words = n;
+    }
+    return b.p;
+}
+
+void zero_buf_release(cudaStream_t st) {
+    ZeroBuf& b = dev_state().zero;
+    MMM_CUDA(cudaEventRecord(b.last, st));
+}
+
+}  // namespace mmm_cu
+
+namespace {
+thread_local std::string t_err;
+}
+
+namespace mmm_cu {
+void set_last_error(const std::string& m) { t_err = m; }
 }  // namespace mmm_cu
 
 using namespace mmm_cu;
 
 namespace {
-
-thread_local std::string t_err;
-
-template <class Fn>
-int guarded(Fn&& fn) {
-    try {
-        fn();
-        return MMM_OK;
-    } catch (const Error& e) {
-        t_err = e.what();
-        return e.status;
-    } catch (const std::bad_alloc&) {
-        t_err = "host allocation failed";
-        return MMM_INVALID_ARGUMENT;
-    } catch (const std::exception& e) {
-        t_err = e.what();
-        return MMM_SIM_ERROR;
-    }
-}
 
 // Field::Field (field.cpp:10-25).
 FieldParams field_or_throw(int64_t p) {
@@ -123,13 +191,11 @@ int64_t trimmed_len(const uint32_t* c, int64_t n) {
     return n;
 }
 
+// The calling thread's stream on the current device (created on first use).
 cudaStream_t thread_stream() {
-    thread_local cudaStream_t s = [] {
-        cudaStream_t st = nullptr;
-        MMM_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-        return st;
-    }();
-    return s;
+    DevState& s = dev_state();
+    if (!s.stream) MMM_CUDA(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
+    return s.stream;
 }
 
 void need_cap(int64_t cap, int64_t need, const char* what) {
@@ -154,7 +220,7 @@ void sync(cudaStream_t st) { MMM_CUDA(cudaStreamSynchronize(st)); }
 // that must complete before the call returns go here, so one synchronisation
 // covers them all.
 uint32_t* pinned_stage(size_t bytes) {
-    thread_local std::pair<void*, size_t> buf{nullptr, 0};
+    auto& buf = t_state.pinned;
     if (buf.second < bytes) {
         if (buf.first) cudaFreeHost(buf.first);
         const size_t n = std::max(bytes, size_t(1) << 20);
@@ -176,6 +242,25 @@ struct mmm_rng {
 extern "C" {
 
 const char* mmm_last_error(void) { return t_err.c_str(); }
+
+int mmm_cu_release_scratch(void) {
+    return guarded([&] { t_state.release(); });
+}
+
+int mmm_cu_release_all(void) {
+    return guarded([&] {
+        int n = 0, cur = 0;
+        MMM_CUDA(cudaGetDevice(&cur));
+        MMM_CUDA(cudaGetDeviceCount(&n));
+        for (int d = 0; d < n; ++d) {
+            MMM_CUDA(cudaSetDevice(d));
+            MMM_CUDA(cudaDeviceSynchronize());
+        }
+        MMM_CUDA(cudaSetDevice(cur));
+        release_plans();
+        t_state.release();
+    });
+}
 int mmm_version(void) { return 1; }
 uint64_t mmm_cu_launch_count(void) { return g_launches.load(); }
 
@@ -357,18 +442,28 @@ __global__ void fanout_copy_kernel(const uint32_t* __restrict__ src, int64_t n, 
     }
 }
 
+}  // extern "C"
+
+namespace mmm_cu {
+void launch_fanout_copy(const uint32_t* src, int64_t n, Fan f, cudaStream_t st) {
+    if (n <= 0) return;
+    bool vec = reinterpret_cast<uintptr_t>(src) % 16 == 0;
+    for (int q = 0; q < f.n; ++q) vec = vec && reinterpret_cast<uintptr_t>(f.p[q]) % 16 == 0;
+    const int64_t work = vec ? (n + 3) / 4 : n;
+    const unsigned blocks = unsigned(std::min<int64_t>((work + 255) / 256, 8LL * sm_count()));
+    fanout_copy_kernel<<<blocks, 256, 0, st>>>(src, n, f, vec);
+    check_launch("fanout_copy_kernel");
+}
+}  // namespace mmm_cu
+
+extern "C" {
+
 int mmm_cu_fanout_copy_dev(const uint32_t* d_src, int64_t n, uint32_t* const* d_dst,
                            int32_t n_out, void* stream) {
     return guarded([&] {
         const Fan f = fan_or_throw(d_dst, n_out, "fan-out copy");
         if (n < 0) throw Error(ST_INVALID, "fan-out copy: negative length");
-        if (n == 0) return;
-        bool vec = reinterpret_cast<uintptr_t>(d_src) % 16 == 0;
-        for (int q = 0; q < f.n; ++q) vec = vec && reinterpret_cast<uintptr_t>(f.p[q]) % 16 == 0;
-        const int64_t work = vec ? (n + 3) / 4 : n;
-        const unsigned blocks = unsigned(std::min<int64_t>((work + 255) / 256, 8LL * sm_count()));
-        fanout_copy_kernel<<<blocks, 256, 0, as_stream(stream)>>>(d_src, n, f, vec);
-        check_launch("fanout_copy_kernel");
+        launch_fanout_copy(d_src, n, f, as_stream(stream));
     });
 }
 
@@ -614,7 +709,6 @@ int mmm_cu_gcd(int64_t p, const uint32_t* a, int64_t na, const uint32_t* b, int6
             MMM_CUDA(cudaMemcpyAsync(stage + 2, dg, size_t(n) * 4, cudaMemcpyDeviceToHost, st));
             sync(st);
             std::memcpy(&len, stage, sizeof(int64_t));
-            if (len == -1) throw Error(ST_SIM, "gcd: offset matrix left its window");
             if (len < 0 || len > n) throw Error(ST_SIM, "gcd: batch made no progress");
             std::memcpy(g, stage + 2, size_t(len) * 4);
         }

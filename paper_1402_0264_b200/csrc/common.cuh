@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <new>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -20,6 +21,28 @@ struct Error : std::runtime_error {
     Error(int st, const std::string& m) : std::runtime_error(m), status(st) {}
 };
 constexpr int ST_INVALID = 1, ST_DOMAIN = 2, ST_CUDA = 3, ST_NCCL = 4, ST_SIM = 5;
+
+// The message behind mmm_last_error() (thread-local, capi.cu).
+void set_last_error(const std::string& m);
+
+// Runs one C-ABI entry point: exceptions become an mmm_status plus the
+// thread's last-error message.
+template <class Fn>
+int guarded(Fn&& fn) {
+    try {
+        fn();
+        return 0;
+    } catch (const Error& e) {
+        set_last_error(e.what());
+        return e.status;
+    } catch (const std::bad_alloc&) {
+        set_last_error("host allocation failed");
+        return ST_INVALID;
+    } catch (const std::exception& e) {
+        set_last_error(e.what());
+        return ST_SIM;
+    }
+}
 
 inline void cuda_check(cudaError_t e, const char* what) {
     if (e != cudaSuccess)
@@ -37,17 +60,23 @@ inline void check_launch(const char* what) {
     cuda_check(cudaGetLastError(), what);
 }
 
-// Stream-ordered scratch from a per-(device, stream, host thread) arena: a list
-// of device chunks (cudaMallocAsync, kept for the process), handed out by a
-// bump pointer that each Scratch restores on destruction (LIFO, nested Scratch
-// objects included).  Reuse is safe because every use of a Scratch's memory is
-// ordered on its stream.  In steady state a call makes no allocation API call
-// (a dozen cudaMallocAsync/cudaFreeAsync pairs per GCD call showed up in e2e).
+// Stream-ordered scratch from a per-(host thread, device) arena: a list of
+// device chunks (cudaMallocAsync), handed out by a bump pointer that each
+// Scratch restores on destruction (LIFO, nested Scratch objects included).  In
+// steady state a call makes no allocation API call (a dozen
+// cudaMallocAsync/cudaFreeAsync pairs per GCD call showed up in e2e).
+// Reuse across streams is ordered by an event: the outermost Scratch waits on
+// the event its predecessor recorded when it was released, so a call on
+// another stream (or on a recycled stream handle) never overwrites memory that
+// queued work still uses.  The arena belongs to its thread and is freed when
+// the thread exits (or by mmm_cu_release_scratch()).
 struct Arena {
     std::vector<std::pair<char*, size_t>> chunks;
     size_t ci = 0, off = 0;  // current chunk, offset in it
+    int depth = 0;           // live Scratch objects
+    cudaEvent_t last = nullptr;  // recorded when the outermost Scratch is released
 };
-Arena& arena_for(cudaStream_t s);
+Arena& arena_for();  // the calling thread's arena on the current device
 struct Scratch {
     cudaStream_t stream;
     Arena* arena;
@@ -63,6 +92,20 @@ struct Scratch {
     Scratch(const Scratch&) = delete;
     Scratch& operator=(const Scratch&) = delete;
 };
+
+// A zero-filled device buffer that kernels leave zeroed (the product's split-k
+// accumulator and arrival counters), one per (host thread, device).  acquire()
+// orders the stream after the buffer's previous user (event); release() marks
+// the stream's use.  Growing frees the old buffer in stream order.
+struct ZeroBuf {
+    unsigned long long* p = nullptr;
+    size_t words = 0;
+    cudaEvent_t last = nullptr;
+};
+unsigned long long* zero_buf_acquire(size_t words, cudaStream_t st);
+void zero_buf_release(cudaStream_t st);
+// Frees every NTT plan (ntt.cu); the caller guarantees no queued work uses one.
+void release_plans();
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
@@ -165,6 +208,8 @@ void launch_mul_batched_fan(const FieldParams& F, const uint32_t* A, int64_t lda
 void launch_divmod_batched_fan(const FieldParams& F, const uint32_t* A, int64_t lda, int64_t na,
                                const uint32_t* B, int64_t ldb, int64_t nb, int64_t count, Fan Q,
                                int64_t ldq, Fan Rr, int64_t ldr, int64_t s, cudaStream_t st);
+// n words of src into every pointer of the fan (capi.cu: fanout_copy_kernel).
+void launch_fanout_copy(const uint32_t* src, int64_t n, Fan dst, cudaStream_t st);
 // division by Newton iteration over NTT products (fastdiv.cu): same q, r.
 void launch_divmod_fast(const FieldParams& F, const uint32_t* a, int64_t na, const uint32_t* b,
                         int64_t nb, uint32_t* q, uint32_t* r, cudaStream_t st);

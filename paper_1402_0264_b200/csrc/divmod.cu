@@ -27,6 +27,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 
 #include "common.cuh"
 #include "conv.cuh"
@@ -765,7 +766,47 @@ __global__ void __launch_bounds__(PIPE_T, 1) div_pipe_kernel(PipeArgs g) {
         g.r[x] = __ldcg(g.A + x);
 }
 
+// ------------------------------------------ division by a constant (nb = 1) --
+// oracle_divmod with deg b = 0 (oracle.cpp:51-67): every head i yields
+// lambda = r[i] * lc(b)^-1, q[i] = lambda, and r[i] -= lambda * b[0] leaves 0,
+// so q = a * b[0]^-1 and r = 0 (the zero-head skip gives the same q[i] = 0).
+// Grid (chunks, instances); one inverse per CTA.
+template <bool FAN>
+__global__ void __launch_bounds__(256) div_const_kernel(const uint32_t* __restrict__ A, int64_t lda,
+                                                        int64_t na, const uint32_t* __restrict__ B,
+                                                        int64_t ldb, Fan Q, int64_t ldq,
+                                                        FieldParams F) {
+    __shared__ uint32_t cinv;
+    const int64_t inst = blockIdx.y;
+    if (threadIdx.x == 0) cinv = invmod(B[inst * ldb], F);
+    __syncthreads();
+    const uint32_t c = cinv;
+    const uint32_t* a = A + inst * lda;
+    const int64_t qb = inst * ldq;
+    for (int64_t j = int64_t(blockIdx.x) * 256 + threadIdx.x; j < na; j += int64_t(gridDim.x) * 256)
+        fan_store<FAN>(Q, qb + j, mulmod(__ldg(a + j), c, F));
+}
+
 namespace {
+
+void run_const(const FieldParams& F, const uint32_t* A, int64_t lda, int64_t na,
+               const uint32_t* B, int64_t ldb, int64_t count, Fan Q, int64_t ldq,
+               cudaStream_t st) {
+    const int64_t per = std::max<int64_t>(1, std::min<int64_t>(ceil_div(na, 256),
+                                                               ceil_div(8LL * sm_count(), count)));
+    for (int64_t c0 = 0; c0 < count; c0 += 65535) {
+        const unsigned n = unsigned(std::min<int64_t>(65535, count - c0));
+        const dim3 grid(unsigned(std::min<int64_t>(per, 65535)), n);
+        const Fan q = fan_offset(Q, c0 * ldq);
+        if (Q.n > 1)
+            div_const_kernel<true><<<grid, 256, 0, st>>>(A + c0 * lda, lda, na, B + c0 * ldb, ldb,
+                                                         q, ldq, F);
+        else
+            div_const_kernel<false><<<grid, 256, 0, st>>>(A + c0 * lda, lda, na, B + c0 * ldb, ldb,
+                                                          q, ldq, F);
+        check_launch("div_const_kernel");
+    }
+}
 
 int pick_R(const FieldParams& F) { return F.fold_terms >= 8 ? 8 : (F.fold_terms >= 2 ? 2 : 1); }
 
@@ -911,9 +952,12 @@ void launch_divmod(const FieldParams& F, const uint32_t* a, int64_t na, const ui
     const int Spad = (S + R - 1) / R * R;
     const int borg = ((Spad + 3) & ~3) + 3;
     const size_t cta_bytes = cta_smem_words(na, nb, S, R, borg) * 4;
+    if (nb == 1) {  // division by a constant: q = a * b[0]^-1, no remainder words
+        run_const(F, a, na, na, b, 1, 1, g.qf, 0, st);
+        return;
+    }
     const bool small = double(mu) * double(nb) < 4.0e6 && cta_bytes <= 200 * 1024;
-    if (small || nb == 1) {
-        if (cta_bytes > 200 * 1024) throw Error(ST_INVALID, "division: instance too large");
+    if (small) {
         switch (R) {
             case 8: run_cta<8>(g, 1, st); break;
             case 2: run_cta<2>(g, 1, st); break;
@@ -921,7 +965,12 @@ void launch_divmod(const FieldParams& F, const uint32_t* a, int64_t na, const ui
         }
         return;
     }
-    if (pipe_eligible(F, s) && !getenv("MMM_DIV_GRID")) {
+    // the pipeline keeps 2S remainder words and S entering words per step in
+    // its head: divisors shorter than that take the grid schedule
+    const char* force = getenv("MMM_DIV_SCHED");  // tests/tools: "grid" or "pipe"
+    const bool want_pipe = force ? std::string(force) == "pipe"
+                                 : (nb > 4 * 256 && !getenv("MMM_DIV_GRID"));
+    if (pipe_eligible(F, s) && want_pipe) {
         run_pipe(g, s, st);
         return;
     }
@@ -960,8 +1009,24 @@ void launch_divmod_batched_fan(const FieldParams& F, const uint32_t* A, int64_t 
     const int R = pick_R(F);
     const int Spad = (g.S + R - 1) / R * R;
     const int borg = ((Spad + 3) & ~3) + 3;
-    if (cta_smem_words(na, nb, g.S, R, borg) * 4 > 200 * 1024)
-        throw Error(ST_INVALID, "division batch: instance too large for one CTA");
+    if (nb == 1) {
+        run_const(F, A, lda, na, B, ldb, count, Q, ldq, st);
+        return;
+    }
+    if (cta_smem_words(na, nb, g.S, R, borg) * 4 > 200 * 1024) {
+        // instances too large for one CTA: one single-instance division each
+        // (grid or pipelined schedule), results fanned out by a copy kernel
+        const int64_t lq = na - nb + 1, lr = nb - 1;
+        for (int64_t i = 0; i < count; ++i) {
+            Scratch sc(st);
+            uint32_t* q = sc.get<uint32_t>(size_t(lq));
+            uint32_t* r = sc.get<uint32_t>(size_t(lr));
+            launch_divmod(F, A + i * lda, na, B + i * ldb, nb, q, r, s, st);
+            launch_fanout_copy(q, lq, fan_offset(Q, i * ldq), st);
+            launch_fanout_copy(r, lr, fan_offset(Rr, i * ldr), st);
+        }
+        return;
+    }
     switch (R) {
         case 8: run_cta<8>(g, count, st); break;
         case 2: run_cta<2>(g, count, st); break;

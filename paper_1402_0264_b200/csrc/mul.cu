@@ -43,7 +43,7 @@ struct MulArgs {
     uint32_t* f;              // output word k - klo of instance inst at f[inst * ldf + k - klo]
     unsigned long long* acc;  // split k-tiles accumulate here (single instance)
     unsigned* arrived;        // per k-tile count of finished items
-    // acc and arrived are persistent per stream and all-zero between calls:
+    // acc and arrived are the thread's ZeroBuf, all-zero between calls:
     // the last item of a k-tile reads its words and zeroes them (and resets
     // its counter), so no zeroing pass runs before the kernel
     int64_t na, nb, lda, ldb, ldf;
@@ -184,30 +184,6 @@ __global__ void __launch_bounds__(MUL_T) mul_kernel(MulArgs g) {
 
 namespace {
 
-// The split-k accumulator and arrival counters of each (device, stream):
-// zeroed once when allocated, left zeroed by every kernel (see mul_kernel), so
-// calls on one stream (which are ordered) share it; another stream gets its own.
-struct AccBuf {
-    unsigned long long* p = nullptr;
-    size_t words = 0;
-};
-unsigned long long* persistent_acc(size_t words, cudaStream_t st) {
-    static std::mutex mu;
-    static std::map<std::pair<int, cudaStream_t>, AccBuf> bufs;
-    int dev = 0;
-    MMM_CUDA(cudaGetDevice(&dev));
-    std::lock_guard<std::mutex> lock(mu);
-    AccBuf& b = bufs[{dev, st}];
-    if (b.words < words) {
-        if (b.p) MMM_CUDA(cudaFreeAsync(b.p, st));
-        const size_t n = std::max(words, size_t(1) << 16);
-        MMM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&b.p), n * sizeof(unsigned long long), st));
-        MMM_CUDA(cudaMemsetAsync(b.p, 0, n * sizeof(unsigned long long), st));
-        b.words = n;
-    }
-    return b.p;
-}
-
 int pick_tile(int64_t s, const FieldParams& F) {
     int R = 1;
     for (int c : {2, 4, 8, 16})
@@ -283,10 +259,13 @@ void launch_mul_range_fan(const FieldParams& F, const uint32_t* a, int64_t na, c
     g.klo = klo;
     g.khi = khi;
     g.F = F;
-    if (items > 1) {  // the stream's persistent all-zero accumulator and counters
+    if (items > 1) {  // the thread's all-zero accumulator and counters (ZeroBuf)
         const size_t words = size_t(nf) + size_t(ceil_div(nkt, 2));
-        g.acc = persistent_acc(words, st);
+        g.acc = zero_buf_acquire(words, st);
         g.arrived = reinterpret_cast<unsigned*>(g.acc + nf);
+        dispatch(R, g, dim3(unsigned(items), unsigned(nkt), 1), st);
+        zero_buf_release(st);
+        return;
     }
     dispatch(R, g, dim3(unsigned(items), unsigned(nkt), 1), st);
 }

@@ -703,6 +703,24 @@ const NttPlan& get_plan(uint32_t p, int logN) {
     return ref;
 }
 
+}  // namespace
+
+void release_plans() {
+    std::lock_guard<std::mutex> lk(g_plans.mu);
+    int cur = 0;
+    cudaGetDevice(&cur);
+    for (auto& kv : g_plans.plans) {
+        cudaSetDevice(std::get<0>(kv.first));
+        for (uint2* t : {kv.second->r1, kv.second->r2, kv.second->tlo, kv.second->thi,
+                         kv.second->thi_s})
+            cudaFree(t);
+    }
+    g_plans.plans.clear();
+    cudaSetDevice(cur);
+}
+
+namespace {
+
 int log2_len(int64_t nf) {
     int k = 2;
     while ((int64_t(1) << k) < nf) ++k;

@@ -3,7 +3,7 @@
 // Every arithmetic entry point converts Poly <-> uint32 residues, calls the
 // sm_100a library (mmm_cu_*), and rethrows its status as the exception the
 // reference throws.  Input checks of the kernel programs follow
-// proj/src/multiplication.cpp:25-34, division.cpp:182-196, gcd.cpp:508-522.
+// proj/src/multiplication.cpp:25-34, division.cpp:182-196, gcd.cpp:340-357.
 #include "../../include/mmm_b200.hpp"
 
 #include <algorithm>
