@@ -11,6 +11,7 @@
 #include <cstring>
 #include <mutex>
 #include <thread>
+#include <vector>
 #include <tuple>
 #include <map>
 #include <new>
@@ -34,6 +35,8 @@ namespace {
 constexpr int MAX_DEV = 64;
 struct DevState {
     cudaStream_t stream = nullptr;
+    cudaStream_t aux[2] = {nullptr, nullptr};  // the batch pipeline's copy/compute lanes
+    cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
     Arena arena;
     ZeroBuf zero;
     bool used = false;
@@ -56,6 +59,10 @@ struct ThreadState {
             if (s.arena.last) cudaEventDestroy(s.arena.last);
             if (s.zero.last) cudaEventDestroy(s.zero.last);
             if (s.stream) cudaStreamDestroy(s.stream);
+            for (auto& a : s.aux)
+                if (a) cudaStreamDestroy(a);
+            for (auto& e : s.ev)
+                if (e) cudaEventDestroy(e);
             s = DevState{};
         }
         if (pinned.first) cudaFreeHost(pinned.first);
@@ -153,6 +160,17 @@ thread_local std::string t_err;
 
 namespace mmm_cu {
 void set_last_error(const std::string& m) { t_err = m; }
+
+__global__ void check_rows_kernel(const uint32_t* __restrict__ d, int64_t rows, int64_t n,
+                                  uint32_t p, unsigned* flag) {
+    unsigned bad = 0;
+    for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+        const uint32_t* row = d + r * n;
+        for (int64_t c = threadIdx.x; c < n; c += blockDim.x) bad |= __ldg(row + c) >= p;
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1u);
+}
+
 }  // namespace mmm_cu
 
 using namespace mmm_cu;
@@ -232,6 +250,96 @@ uint32_t* pinned_stage(size_t bytes) {
 }
 
 cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+// ---- pipelined batches (host buffers) --------------------------------------
+// A batched host call streams its instances through the GPU in chunks on two
+// lanes: chunk k's H2D, coefficient check, kernels and D2H are ordered on lane
+// k % 2, so chunk k+1's copies overlap chunk k's kernels (and the copy engines
+// run both directions at once).  The canonical-coefficient check
+// (run_util.hpp:24-29) runs on the device as each chunk lands -- the host scan
+// of a cfg5 batch (335 MB) cost more than its transfer -- and is reported after
+// the join (outputs are then unspecified, as for any failed call).  D2H of
+// chunk k is issued after chunk k+1's H2D and kernels, so pageable (blocking)
+// copies still overlap.
+struct HostIn {
+    const uint32_t* p;
+    int64_t ld, n;
+    const char* what;  // error message subject
+};
+struct HostOut {
+    uint32_t* p;
+    int64_t ld, n;
+};
+
+template <class Launch>
+void pipelined_batch(const FieldParams& F, int64_t count, std::vector<HostIn> ins,
+                     std::vector<HostOut> outs, Launch launch) {
+    DevState& ds = dev_state();
+    const cudaStream_t st0 = thread_stream();
+    for (auto& a : ds.aux)
+        if (!a) MMM_CUDA(cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking));
+    for (auto& e : ds.ev)
+        if (!e) MMM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    int64_t row_words = 0;
+    for (auto& i : ins) row_words += i.n;
+    for (auto& o : outs) row_words += o.n;
+    // chunks of >= 2 waves of one CTA per SM and >= 4 MB, about 8 per call
+    int64_t chunk = std::max<int64_t>(ceil_div(count, 8), 2LL * sm_count());
+    chunk = std::max<int64_t>(chunk, ceil_div(int64_t(4) << 20, 4 * std::max<int64_t>(row_words, 1)));
+    chunk = std::min<int64_t>(chunk, count);
+    const int64_t nchunks = ceil_div(count, chunk);
+    const int lanes = nchunks > 1 ? 2 : 1;
+    uint32_t* stage = pinned_stage(ins.size() * 4 + 16);
+    {
+        Scratch sc(st0);
+        std::vector<uint32_t*> din[2], dout[2];
+        for (int l = 0; l < lanes; ++l) {
+            for (auto& i : ins) din[l].push_back(sc.get<uint32_t>(size_t(chunk * i.n)));
+            for (auto& o : outs) dout[l].push_back(sc.get<uint32_t>(size_t(chunk * std::max<int64_t>(o.n, 1))));
+        }
+        unsigned* flags = sc.get<unsigned>(ins.size());
+        MMM_CUDA(cudaMemsetAsync(flags, 0, ins.size() * sizeof(unsigned), st0));
+        MMM_CUDA(cudaEventRecord(ds.ev[0], st0));  // fork: scratch and flags ready
+        for (int l = 0; l < lanes; ++l) MMM_CUDA(cudaStreamWaitEvent(ds.aux[l], ds.ev[0], 0));
+        auto d2h = [&](int64_t k) {
+            const int l = int(k % lanes);
+            const int64_t c0 = k * chunk, c = std::min(chunk, count - c0);
+            for (size_t j = 0; j < outs.size(); ++j)
+                if (outs[j].n)
+                    MMM_CUDA(cudaMemcpy2DAsync(outs[j].p + c0 * outs[j].ld, size_t(outs[j].ld) * 4,
+                                               dout[l][j], size_t(outs[j].n) * 4,
+                                               size_t(outs[j].n) * 4, size_t(c),
+                                               cudaMemcpyDeviceToHost, ds.aux[l]));
+        };
+        for (int64_t k = 0; k < nchunks; ++k) {
+            const int l = int(k % lanes);
+            const cudaStream_t st = ds.aux[l];
+            const int64_t c0 = k * chunk, c = std::min(chunk, count - c0);
+            for (size_t j = 0; j < ins.size(); ++j) {
+                MMM_CUDA(cudaMemcpy2DAsync(din[l][j], size_t(ins[j].n) * 4, ins[j].p + c0 * ins[j].ld,
+                                           size_t(ins[j].ld) * 4, size_t(ins[j].n) * 4, size_t(c),
+                                           cudaMemcpyHostToDevice, st));
+                const unsigned blocks = unsigned(std::min<int64_t>(c, 4LL * sm_count()));
+                check_rows_kernel<<<blocks, 256, 0, st>>>(din[l][j], c, ins[j].n, F.p, flags + j);
+                check_launch("check_rows_kernel");
+            }
+            launch(din[l], dout[l], c, st);
+            if (k > 0) d2h(k - 1);
+        }
+        d2h(nchunks - 1);
+        for (int l = 0; l < lanes; ++l) {  // join before the scratch is released
+            MMM_CUDA(cudaEventRecord(ds.ev[1 + l], ds.aux[l]));
+            MMM_CUDA(cudaStreamWaitEvent(st0, ds.ev[1 + l], 0));
+        }
+        MMM_CUDA(cudaMemcpyAsync(stage, flags, ins.size() * sizeof(unsigned),
+                                 cudaMemcpyDeviceToHost, st0));
+    }
+    sync(st0);
+    for (size_t j = 0; j < ins.size(); ++j)
+        if (stage[j])
+            throw Error(ST_INVALID, std::string(ins[j].what) +
+                                        ": coefficients must be canonical field elements");
+}
 
 }  // namespace
 
@@ -363,26 +471,16 @@ int mmm_cu_mul_batched(int64_t p, const uint32_t* A, int64_t lda, int64_t na, co
         const FieldParams F = field_or_throw(p);
         if (na < 1 || nb < 1 || count < 0 || lda < na || ldb < nb || ldf < na + nb - 1)
             throw Error(ST_INVALID, "multiplication batch: bad shape");
-        for (int64_t i = 0; i < count; ++i) {
-            check_canonical(A + i * lda, na, F.p, "multiplication batch first operand");
-            check_canonical(B + i * ldb, nb, F.p, "multiplication batch second operand");
-        }
         if (count == 0) return;
-        cudaStream_t st = thread_stream();
-        {
-            Scratch sc(st);
-            uint32_t* dA = sc.get<uint32_t>(size_t(count * na));
-            uint32_t* dB = sc.get<uint32_t>(size_t(count * nb));
-            uint32_t* dF = sc.get<uint32_t>(size_t(count * (na + nb - 1)));
-            MMM_CUDA(cudaMemcpy2DAsync(dA, na * 4, A, lda * 4, na * 4, count,
-                                       cudaMemcpyHostToDevice, st));
-            MMM_CUDA(cudaMemcpy2DAsync(dB, nb * 4, B, ldb * 4, nb * 4, count,
-                                       cudaMemcpyHostToDevice, st));
-            launch_mul_batched(F, dA, na, na, dB, nb, nb, count, dF, na + nb - 1, s, st);
-            MMM_CUDA(cudaMemcpy2DAsync(Fo, ldf * 4, dF, (na + nb - 1) * 4, (na + nb - 1) * 4,
-                                       count, cudaMemcpyDeviceToHost, st));
-        }
-        sync(st);
+        const int64_t nf = na + nb - 1;
+        pipelined_batch(F, count,
+                        {{A, lda, na, "multiplication batch first operand"},
+                         {B, ldb, nb, "multiplication batch second operand"}},
+                        {{Fo, ldf, nf}},
+                        [&](const std::vector<uint32_t*>& in, const std::vector<uint32_t*>& out,
+                            int64_t c, cudaStream_t st) {
+                            launch_mul_batched(F, in[0], na, na, in[1], nb, nb, c, out[0], nf, s, st);
+                        });
     });
 }
 
@@ -636,32 +734,19 @@ int mmm_cu_divmod_batched(int64_t p, const uint32_t* A, int64_t lda, int64_t na,
         if (nb < 1 || na < nb || count < 0 || lda < na || ldb < nb || ldq < na - nb + 1 ||
             ldr < nb - 1)
             throw Error(ST_INVALID, "division batch: bad shape");
-        for (int64_t i = 0; i < count; ++i) {
-            check_canonical(A + i * lda, na, F.p, "division batch dividend");
-            check_canonical(B + i * ldb, nb, F.p, "division batch divisor");
+        for (int64_t i = 0; i < count; ++i)  // the divisors' leads: one word per row, on the host
             if (B[i * ldb + nb - 1] == 0) throw Error(ST_DOMAIN, "field: inverse of zero");
-        }
         if (count == 0) return;
         const int64_t lq = na - nb + 1, lr = nb - 1;
-        cudaStream_t st = thread_stream();
-        {
-            Scratch sc(st);
-            uint32_t* dA = sc.get<uint32_t>(size_t(count * na));
-            uint32_t* dB = sc.get<uint32_t>(size_t(count * nb));
-            uint32_t* dQ = sc.get<uint32_t>(size_t(count * lq));
-            uint32_t* dR = sc.get<uint32_t>(size_t(count * std::max<int64_t>(lr, 1)));
-            MMM_CUDA(cudaMemcpy2DAsync(dA, na * 4, A, lda * 4, na * 4, count,
-                                       cudaMemcpyHostToDevice, st));
-            MMM_CUDA(cudaMemcpy2DAsync(dB, nb * 4, B, ldb * 4, nb * 4, count,
-                                       cudaMemcpyHostToDevice, st));
-            launch_divmod_batched(F, dA, na, na, dB, nb, nb, count, dQ, lq, dR, lr, s, st);
-            MMM_CUDA(cudaMemcpy2DAsync(Q, ldq * 4, dQ, lq * 4, lq * 4, count,
-                                       cudaMemcpyDeviceToHost, st));
-            if (lr)
-                MMM_CUDA(cudaMemcpy2DAsync(R, ldr * 4, dR, lr * 4, lr * 4, count,
-                                           cudaMemcpyDeviceToHost, st));
-        }
-        sync(st);
+        pipelined_batch(F, count,
+                        {{A, lda, na, "division batch dividend"},
+                         {B, ldb, nb, "division batch divisor"}},
+                        {{Q, ldq, lq}, {R, ldr, lr}},
+                        [&](const std::vector<uint32_t*>& in, const std::vector<uint32_t*>& out,
+                            int64_t c, cudaStream_t st) {
+                            launch_divmod_batched(F, in[0], na, na, in[1], nb, nb, c, out[0], lq,
+                                                  out[1], std::max<int64_t>(lr, 1), s, st);
+                        });
     });
 }
 
@@ -774,27 +859,16 @@ int mmm_cu_ntt_mul_batched(int64_t p, const uint32_t* A, int64_t lda, int64_t na
             throw Error(ST_INVALID, "ntt batch: bad shape");
         if (!ntt_supported(F.p, na + nb - 1))
             throw Error(ST_INVALID, "ntt: p has no 2-adic root of unity of the needed order");
-        for (int64_t i = 0; i < count; ++i) {
-            check_canonical(A + i * lda, na, F.p, "ntt batch first operand");
-            check_canonical(B + i * ldb, nb, F.p, "ntt batch second operand");
-        }
         if (count == 0) return;
         const int64_t nf = na + nb - 1;
-        cudaStream_t st = thread_stream();
-        {
-            Scratch sc(st);
-            uint32_t* dA = sc.get<uint32_t>(size_t(count * na));
-            uint32_t* dB = sc.get<uint32_t>(size_t(count * nb));
-            uint32_t* dF = sc.get<uint32_t>(size_t(count * nf));
-            MMM_CUDA(cudaMemcpy2DAsync(dA, na * 4, A, lda * 4, na * 4, count,
-                                       cudaMemcpyHostToDevice, st));
-            MMM_CUDA(cudaMemcpy2DAsync(dB, nb * 4, B, ldb * 4, nb * 4, count,
-                                       cudaMemcpyHostToDevice, st));
-            launch_ntt_mul_batched(F, dA, na, na, dB, nb, nb, count, dF, nf, st);
-            MMM_CUDA(cudaMemcpy2DAsync(Fo, ldf * 4, dF, nf * 4, nf * 4, count,
-                                       cudaMemcpyDeviceToHost, st));
-        }
-        sync(st);
+        pipelined_batch(F, count,
+                        {{A, lda, na, "ntt batch first operand"},
+                         {B, ldb, nb, "ntt batch second operand"}},
+                        {{Fo, ldf, nf}},
+                        [&](const std::vector<uint32_t*>& in, const std::vector<uint32_t*>& out,
+                            int64_t c, cudaStream_t st) {
+                            launch_ntt_mul_batched(F, in[0], na, na, in[1], nb, nb, c, out[0], nf, st);
+                        });
     });
 }
 
