@@ -8,8 +8,8 @@
 // semantics, exception types (std::invalid_argument, std::domain_error,
 // SimError) and the capacity rules of the kernel programs (2l <= Z, 7s <= Z,
 // 6s <= Z, 2sl+2s-1 <= Z, s >= 2 for the blocked GCD).
-// Changed: SimReport carries the real launch schedule of the B200 run
-// (kernels launched, device time) instead of simulator counters; Rat is a
+// Changed: SimReport keeps the reference's shape but is filled from the real
+// launch schedule of the B200 run (simulator-only counters are zero); Rat is a
 // Boost-free 64-bit rational with the subset of the API the callers use.
 #pragma once
 
@@ -105,9 +105,48 @@ struct MachineParams {  // machine.hpp:24-28
     bool parallel = true;
 };
 
-// What the B200 actually ran (replaces the simulator's counters).
-struct SimReport {
-    std::int64_t kernels = 0;      // CUDA kernel launches of this call
+// ---- metrics (metrics.hpp:12-72, simtypes.hpp:16-20), same shape ---------
+// Filled from the launch schedule the B200 actually ran (mmm_cu_last_schedule):
+// one KernelMetrics per CUDA launch (name, blocks, threads per block), and the
+// structural metrics of that launch DAG -- a chain on one stream, so
+// N = sum of blocks, L = pi = launches, K = max blocks (graph.cpp:56-110).
+// The per-thread work/span/overhead counters (W, S, O, C, alpha, beta,
+// max_accesses, per_block) exist only in the reference's simulator; here they
+// are 0 / empty.  device_ms and block_param are B200 additions.
+struct BlockMetrics {  // metrics.hpp:22-31
+    std::int64_t W = 0, S = 0, alpha = 0, beta = 0, max_accesses = 0;
+    Rat O;
+    Rat C() const { return Rat(S) + O; }
+};
+struct KernelMetrics {  // metrics.hpp:36-48
+    std::string name;
+    std::int64_t blocks = 0;
+    std::int64_t threads = 0;  // threads per block
+    std::vector<BlockMetrics> per_block;
+    std::int64_t W() const { return 0; }
+    std::int64_t S() const { return 0; }
+    Rat O() const { return Rat(0); }
+    Rat max_block_C() const { return Rat(0); }
+    std::int64_t max_accesses() const { return 0; }
+};
+struct StructuralMetrics {  // metrics.hpp:51-56
+    std::int64_t N = 0;   // total blocks over all kernels
+    std::int64_t L = 0;   // vertices on a longest path
+    std::int64_t K = 0;   // maximum antichain weight (blocks)
+    std::int64_t pi = 0;  // minimum number of parallel rounds (= L)
+};
+struct ProgramMetrics {  // metrics.hpp:59-65
+    std::int64_t W = 0;
+    std::int64_t S = 0;
+    Rat O;
+    Rat C;
+    StructuralMetrics structure;
+};
+struct SimReport {  // simtypes.hpp:16-20
+    ProgramMetrics metrics;
+    std::vector<KernelMetrics> kernels;
+    std::int64_t max_thread_accesses = 0;
+    // B200 additions
     std::int64_t block_param = 0;  // s (or l) the kernels used
     double device_ms = 0;          // wall time of the synchronous call
 };

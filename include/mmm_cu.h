@@ -58,6 +58,18 @@ const char* mmm_last_error(void);
 int mmm_version(void);
 /* Number of CUDA kernels this library has launched in this process. */
 uint64_t mmm_cu_launch_count(void);
+/* The kernels the calling thread's last host-buffer compute call launched, in
+ * launch order (all on one stream, so the launch DAG is a chain): name, grid
+ * blocks and threads per block.  At most `cap` records are copied; *n gets
+ * the total.  The drop-in's SimReport (include/mmm_b200.hpp) is built from
+ * this: N = sum of blocks, L = pi = launches, K = max blocks
+ * (graph.cpp:56-110 on a chain). */
+typedef struct mmm_kernel_rec {
+    char name[40];
+    int64_t blocks;
+    int32_t threads;
+} mmm_kernel_rec;
+int mmm_cu_last_schedule(mmm_kernel_rec* out, int32_t cap, int32_t* n);
 /* Frees the calling thread's per-device streams, scratch arenas, zero buffers
  * and pinned staging (waiting for their queued work first).  They are also
  * freed when the thread exits; the next call recreates them. */

@@ -36,7 +36,7 @@ __all__ = [
     "mul_batched_dev", "divmod_batched_dev", "ntt_mul_batched_dev", "launch_count",
     "mul_batched_multi", "divmod_batched_multi", "ntt_mul_batched_multi",
     "mul_batched_multi_dev", "divmod_batched_multi_dev", "ntt_mul_batched_multi_dev",
-    "release_scratch",
+    "release_scratch", "last_schedule",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -68,6 +68,11 @@ _ERR = {1: InvalidArgument, 2: DomainError, 3: CudaError, 4: MmmError, 5: SimErr
 _U32P = C.POINTER(C.c_uint32)
 _I64P = C.POINTER(C.c_int64)
 _I32P = C.POINTER(C.c_int32)
+
+
+class KernelRec(C.Structure):
+    """mmm_kernel_rec (include/mmm_cu.h)."""
+    _fields_ = [("name", C.c_char * 40), ("blocks", C.c_int64), ("threads", C.c_int32)]
 _I64 = C.c_int64
 _VP = C.c_void_p
 
@@ -77,6 +82,7 @@ SIGNATURES = {
     "mmm_version": (C.c_int, []),
     "mmm_cu_launch_count": (C.c_uint64, []),
     "mmm_cu_release_scratch": (C.c_int, []),
+    "mmm_cu_last_schedule": (C.c_int, [C.POINTER(KernelRec), C.c_int32, _I32P]),
     "mmm_cu_release_all": (C.c_int, []),
     "mmm_field_check": (C.c_int, [_I64]),
     "mmm_field_inv": (C.c_int, [_I64, _I64, _I64P]),
@@ -495,3 +501,12 @@ def ntt_mul_batched_multi_dev(p, d_A, lda, na, d_B, ldb, nb, count, d_F, ldf, de
 def release_scratch() -> None:
     """Free this thread's streams, arenas and staging (mmm_cu_release_scratch)."""
     _check(load().mmm_cu_release_scratch())
+
+
+def last_schedule():
+    """[(name, blocks, threads)] of the kernels this thread's last host call launched."""
+    n = C.c_int32(0)
+    _check(load().mmm_cu_last_schedule(None, 0, C.byref(n)))
+    recs = (KernelRec * max(n.value, 1))()
+    _check(load().mmm_cu_last_schedule(recs, n.value, C.byref(n)))
+    return [(r.name.decode(), r.blocks, r.threads) for r in recs[: n.value]]

@@ -161,6 +161,29 @@ thread_local std::string t_err;
 namespace mmm_cu {
 void set_last_error(const std::string& m) { t_err = m; }
 
+namespace {
+struct Schedule {
+    std::vector<mmm_kernel_rec> recs;
+    int64_t total = 0;
+};
+thread_local Schedule t_sched;
+}  // namespace
+
+void schedule_reset() {
+    t_sched.recs.clear();
+    t_sched.total = 0;
+}
+
+void schedule_record(const char* what, dim3 grid, dim3 block) {
+    ++t_sched.total;
+    if (t_sched.recs.size() >= 65536) return;  // counted, not kept
+    mmm_kernel_rec r{};
+    std::strncpy(r.name, what, sizeof(r.name) - 1);
+    r.blocks = int64_t(grid.x) * grid.y * grid.z;
+    r.threads = int32_t(block.x * block.y * block.z);
+    t_sched.recs.push_back(r);
+}
+
 __global__ void check_rows_kernel(const uint32_t* __restrict__ d, int64_t rows, int64_t n,
                                   uint32_t p, unsigned* flag) {
     unsigned bad = 0;
@@ -321,7 +344,7 @@ void pipelined_batch(const FieldParams& F, int64_t count, std::vector<HostIn> in
                                            cudaMemcpyHostToDevice, st));
                 const unsigned blocks = unsigned(std::min<int64_t>(c, 4LL * sm_count()));
                 check_rows_kernel<<<blocks, 256, 0, st>>>(din[l][j], c, ins[j].n, F.p, flags + j);
-                check_launch("check_rows_kernel");
+                check_launch("check_rows_kernel", dim3(blocks), dim3(256));
             }
             launch(din[l], dout[l], c, st);
             if (k > 0) d2h(k - 1);
@@ -350,6 +373,14 @@ struct mmm_rng {
 extern "C" {
 
 const char* mmm_last_error(void) { return t_err.c_str(); }
+
+int mmm_cu_last_schedule(mmm_kernel_rec* out, int32_t cap, int32_t* n) {
+    const auto& r = t_sched.recs;
+    const int32_t k = int32_t(std::min<size_t>(r.size(), size_t(std::max(cap, 0))));
+    if (k && out) std::memcpy(out, r.data(), size_t(k) * sizeof(mmm_kernel_rec));
+    if (n) *n = int32_t(std::min<int64_t>(t_sched.total, INT32_MAX));
+    return MMM_OK;
+}
 
 int mmm_cu_release_scratch(void) {
     return guarded([&] { t_state.release(); });
@@ -421,6 +452,7 @@ int mmm_random_poly(mmm_rng* g, int64_t terms, int64_t p, uint32_t* out) {
 int mmm_cu_mul(int64_t p, const uint32_t* a, int64_t na, const uint32_t* b, int64_t nb, int64_t s,
                int64_t l, uint32_t* f, int64_t f_cap, int64_t* nf) {
     return guarded([&] {
+        schedule_reset();
         const FieldParams F = field_or_throw(p);
         check_canonical(a, na, F.p, "multiplication first operand");
         check_canonical(b, nb, F.p, "multiplication second operand");
@@ -468,6 +500,7 @@ int mmm_cu_mul_batched(int64_t p, const uint32_t* A, int64_t lda, int64_t na, co
                        int64_t ldb, int64_t nb, int64_t count, int64_t s, uint32_t* Fo,
                        int64_t ldf) {
     return guarded([&] {
+        schedule_reset();
         const FieldParams F = field_or_throw(p);
         if (na < 1 || nb < 1 || count < 0 || lda < na || ldb < nb || ldf < na + nb - 1)
             throw Error(ST_INVALID, "multiplication batch: bad shape");
@@ -550,7 +583,7 @@ void launch_fanout_copy(const uint32_t* src, int64_t n, Fan f, cudaStream_t st) 
     const int64_t work = vec ? (n + 3) / 4 : n;
     const unsigned blocks = unsigned(std::min<int64_t>((work + 255) / 256, 8LL * sm_count()));
     fanout_copy_kernel<<<blocks, 256, 0, st>>>(src, n, f, vec);
-    check_launch("fanout_copy_kernel");
+    check_launch("fanout_copy_kernel", dim3(blocks), dim3(256));
 }
 }  // namespace mmm_cu
 
@@ -616,6 +649,7 @@ int mmm_cu_divmod(int64_t p, const uint32_t* a, int64_t na, const uint32_t* b, i
                   int64_t s, uint32_t* q, int64_t q_cap, int64_t* nq, uint32_t* r, int64_t r_cap,
                   int64_t* nr) {
     return guarded([&] {
+        schedule_reset();
         const FieldParams F = field_or_throw(p);
         check_canonical(a, na, F.p, "division dividend");
         check_canonical(b, nb, F.p, "division divisor");
@@ -676,6 +710,7 @@ int mmm_cu_divmod_fast(int64_t p, const uint32_t* a, int64_t na, const uint32_t*
                        uint32_t* q, int64_t q_cap, int64_t* nq, uint32_t* r, int64_t r_cap,
                        int64_t* nr) {
     return guarded([&] {  // validation and results exactly as mmm_cu_divmod
+        schedule_reset();
         const FieldParams F = field_or_throw(p);
         check_canonical(a, na, F.p, "division dividend");
         check_canonical(b, nb, F.p, "division divisor");
@@ -730,6 +765,7 @@ int mmm_cu_divmod_batched(int64_t p, const uint32_t* A, int64_t lda, int64_t na,
                           const uint32_t* B, int64_t ldb, int64_t nb, int64_t count, int64_t s,
                           uint32_t* Q, int64_t ldq, uint32_t* R, int64_t ldr) {
     return guarded([&] {
+        schedule_reset();
         const FieldParams F = field_or_throw(p);
         if (nb < 1 || na < nb || count < 0 || lda < na || ldb < nb || ldq < na - nb + 1 ||
             ldr < nb - 1)
@@ -769,6 +805,7 @@ int mmm_cu_divmod_batched_dev(int64_t p, const uint32_t* d_A, int64_t lda, int64
 int mmm_cu_gcd(int64_t p, const uint32_t* a, int64_t na, const uint32_t* b, int64_t nb, int64_t s,
                uint32_t* g, int64_t g_cap, int64_t* ng) {
     return guarded([&] {
+        schedule_reset();
         const FieldParams F = field_or_throw(p);
         check_canonical(a, na, F.p, "gcd first operand");
         check_canonical(b, nb, F.p, "gcd second operand");
@@ -815,6 +852,7 @@ int mmm_cu_gcd_dev(int64_t p, const uint32_t* d_a, int64_t na, const uint32_t* d
 int mmm_cu_ntt_mul(int64_t p, const uint32_t* a, int64_t na, const uint32_t* b, int64_t nb,
                    uint32_t* f, int64_t f_cap, int64_t* nf) {
     return guarded([&] {
+        schedule_reset();
         const FieldParams F = field_or_throw(p);
         check_canonical(a, na, F.p, "ntt first operand");
         check_canonical(b, nb, F.p, "ntt second operand");
@@ -854,6 +892,7 @@ int mmm_cu_ntt_mul_batched(int64_t p, const uint32_t* A, int64_t lda, int64_t na
                            const uint32_t* B, int64_t ldb, int64_t nb, int64_t count, uint32_t* Fo,
                            int64_t ldf) {
     return guarded([&] {
+        schedule_reset();
         const FieldParams F = field_or_throw(p);
         if (na < 1 || nb < 1 || count < 0 || lda < na || ldb < nb || ldf < na + nb - 1)
             throw Error(ST_INVALID, "ntt batch: bad shape");

@@ -55,9 +55,14 @@ inline void cuda_check(cudaError_t e, const char* what) {
 // the number inside its timed region as gpu_launches).
 extern std::atomic<uint64_t> g_launches;
 inline void note_launch(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
-inline void check_launch(const char* what) {
+// The calling thread's launch log since the last schedule_reset(): what the
+// drop-in reports as SimReport.kernels (name, blocks, threads per block).
+void schedule_record(const char* what, dim3 grid, dim3 block);
+void schedule_reset();
+inline void check_launch(const char* what, dim3 grid = dim3(0, 0, 0), dim3 block = dim3(0, 0, 0)) {
     note_launch();
     cuda_check(cudaGetLastError(), what);
+    schedule_record(what, grid, block);
 }
 
 // Stream-ordered scratch from a per-(host thread, device) arena: a list of

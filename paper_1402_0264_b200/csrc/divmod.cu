@@ -804,7 +804,7 @@ void run_const(const FieldParams& F, const uint32_t* A, int64_t lda, int64_t na,
         else
             div_const_kernel<false><<<grid, 256, 0, st>>>(A + c0 * lda, lda, na, B + c0 * ldb, ldb,
                                                           q, ldq, F);
-        check_launch("div_const_kernel");
+        check_launch("div_const_kernel", grid, dim3(256));
     }
 }
 
@@ -832,7 +832,7 @@ void run_cta(const DivArgs& g, int64_t count, cudaStream_t st) {
         gg.rf = fan_offset(g.rf, c0 * g.ldr);
         const unsigned n = unsigned(std::min<int64_t>(65535, count - c0));
         kern<<<n, DIV_T, bytes, st>>>(gg, borg);
-        check_launch("div_cta_kernel");
+        check_launch("div_cta_kernel", dim3(n), dim3(DIV_T));
     }
 }
 
@@ -864,7 +864,7 @@ void run_grid(DivArgs g, cudaStream_t st) {
     void* params[] = {&g, &seg};
     MMM_CUDA(cudaLaunchCooperativeKernel((void*)div_grid_kernel<RL, RU>, dim3(unsigned(blocks)),
                                          dim3(DIV_T), params, bytes, st));
-    check_launch("div_grid_kernel");
+    check_launch("div_grid_kernel", dim3(unsigned(blocks)), dim3(DIV_T));
 }
 
 // Pipelined schedule (div_pipe_kernel): S = s rounded down to a power of two
@@ -916,7 +916,7 @@ void run_pipe(const DivArgs& d, int64_t s, cudaStream_t st) {
     void* params[] = {&g};
     MMM_CUDA(cudaLaunchCooperativeKernel((void*)div_pipe_kernel, dim3(unsigned(blocks)),
                                          dim3(PIPE_T), params, bytes, st));
-    check_launch("div_pipe_kernel");
+    check_launch("div_pipe_kernel", dim3(unsigned(blocks)), dim3(PIPE_T));
     if (want_stats) {
         long long h[12];
         MMM_CUDA(cudaMemcpyAsync(h, g.stats, sizeof(h), cudaMemcpyDeviceToHost, st));

@@ -118,10 +118,10 @@ void launch_divmod_fast(const FieldParams& F, const uint32_t* a, int64_t na, con
     uint32_t* t1 = sc.get<uint32_t>(size_t(2 * std::max(mu, nb)));
     uint32_t* t2 = sc.get<uint32_t>(size_t(2 * mu));
     rev_prefix<<<blocks_for(nrb), FD_T, 0, st>>>(b, nb, nrb, rb);
-    check_launch("rev_prefix");
+    check_launch("rev_prefix", dim3(blocks_for(nrb)), dim3(FD_T));
     const int K0 = int(std::min<int64_t>(mu, BASE_K));
     newton_base<<<1, FD_T, 0, st>>>(b, nb, K0, h, F);
-    check_launch("newton_base");
+    check_launch("newton_base", dim3(1), dim3(FD_T));
     for (int64_t k = K0; k < mu;) {
         const int64_t k2 = std::min(2 * k, mu), nr = std::min(k2, nrb);
         // e = coefficients [k, k2) of rb[0:k2] * h[0:k]
@@ -132,7 +132,7 @@ void launch_divmod_fast(const FieldParams& F, const uint32_t* a, int64_t na, con
             const int64_t ne = std::min(k2, nr + k - 1) - k;  // nonzero part of e
             product(F, h, k, t1 + k, ne, t2, st);
             neg_into<<<blocks_for(k2 - k), FD_T, 0, st>>>(t2, k2 - k, h + k, F);
-            check_launch("neg_into");
+            check_launch("neg_into", dim3(blocks_for(k2 - k)), dim3(FD_T));
             // t2 holds k + ne - 1 >= k2 - k terms when ne == k2 - k; pad otherwise
             if (k + ne - 1 < k2 - k)
                 MMM_CUDA(cudaMemsetAsync(h + k + (k + ne - 1), 0,
@@ -142,10 +142,10 @@ void launch_divmod_fast(const FieldParams& F, const uint32_t* a, int64_t na, con
     }
     // rev(q) = rev(a)[0:mu] * h mod X^mu, q = rev(rev(q))
     rev_prefix<<<blocks_for(mu), FD_T, 0, st>>>(a, na, mu, ra);
-    check_launch("rev_prefix");
+    check_launch("rev_prefix", dim3(blocks_for(mu)), dim3(FD_T));
     product(F, ra, mu, h, mu, t2, st);
     rev_prefix<<<blocks_for(mu), FD_T, 0, st>>>(t2, mu, mu, q);
-    check_launch("rev_prefix");
+    check_launch("rev_prefix", dim3(blocks_for(mu)), dim3(FD_T));
     // r = (a - q * b) mod X^(nb-1)
     if (nb > 1) {
         if (std::min(mu, nb) >= NTT_MIN && ntt_supported(F.p, mu + nb - 1))
@@ -153,7 +153,7 @@ void launch_divmod_fast(const FieldParams& F, const uint32_t* a, int64_t na, con
         else
             launch_mul_range(F, q, mu, b, nb, 0, nb - 1, t1, 8, 0, st);  // low nb-1 only
         sub_into<<<blocks_for(nb - 1), FD_T, 0, st>>>(a, t1, nb - 1, r, F);
-        check_launch("sub_into");
+        check_launch("sub_into", dim3(blocks_for(nb - 1)), dim3(FD_T));
     }
 }
 

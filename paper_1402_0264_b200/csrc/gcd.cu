@@ -1613,7 +1613,7 @@ void launch_gcd(const FieldParams& F, const uint32_t* a, int64_t na, const uint3
     }
     void* params[] = {&g};
     MMM_CUDA(cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(GCD_T), params, bytes, st));
-    check_launch("gcd_kernel");
+    check_launch("gcd_kernel", dim3(blocks), dim3(GCD_T));
     if (want_stats) {
         long long h[32];
         MMM_CUDA(cudaMemcpyAsync(h, g.stats, sizeof(h), cudaMemcpyDeviceToHost, st));

@@ -198,7 +198,7 @@ void launch_tile(const MulArgs& g, dim3 grid, cudaStream_t st) {
         mul_kernel<R, true><<<grid, MUL_T, 0, st>>>(g);
     else
         mul_kernel<R, false><<<grid, MUL_T, 0, st>>>(g);
-    check_launch("mul_kernel");
+    check_launch("mul_kernel", grid, dim3(MUL_T));
 }
 
 void dispatch(int R, const MulArgs& g, dim3 grid, cudaStream_t st) {

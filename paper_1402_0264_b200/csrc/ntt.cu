@@ -768,11 +768,11 @@ void run_ntt_launches(NttArgs g, int64_t count, int64_t chunk, const uint32_t* A
         g.out = Fo + c0 * ldf;
         g.ldf = ldf;
         kf.fn<<<dim3(N2 / kf.cols, 2, c), kf.threads, kf.smem, st>>>(g);
-        check_launch("ntt_cols_fwd");
+        check_launch("ntt_cols_fwd", dim3(N2 / kf.cols, 2, c), dim3(kf.threads));
         launch_pdl(kr.fn, dim3((N1 + kr.rows - 1) / kr.rows, 1, c), kr.threads, kr.smem, st, g);
-        check_launch("ntt_rows");
+        check_launch("ntt_rows", dim3((N1 + kr.rows - 1) / kr.rows, 1, c), dim3(kr.threads));
         launch_pdl(ko.fn, dim3(N2 / ko.cols, 1, c), ko.threads, ko.smem, st, g);
-        check_launch("ntt_cols_out");
+        check_launch("ntt_cols_out", dim3(N2 / ko.cols, 1, c), dim3(ko.threads));
     }
 }
 
@@ -814,13 +814,14 @@ void phase_launch(NttArgs g, int phase, int64_t start, int64_t n, cudaStream_t s
         g.row0 = int(start);
         g.row_end = int(start + n);
         kr.fn<<<dim3(unsigned((n + kr.rows - 1) / kr.rows), 1, 1), kr.threads, kr.smem, st>>>(g);
-        check_launch("ntt_rows");
+        check_launch("ntt_rows", dim3(unsigned((n + kr.rows - 1) / kr.rows)), dim3(kr.threads));
     } else {
         const ColsKernel k = phase == 0 ? pick_cols<false, LZ>(g.P.log1, g.P.log2, true)
                                         : pick_cols<true, LZ>(g.P.log1, g.P.log2, true);
         g.col0 = int(start);
         k.fn<<<dim3(unsigned(n / k.cols), phase == 0 ? 2 : 1, 1), k.threads, k.smem, st>>>(g);
-        check_launch(phase == 0 ? "ntt_cols_fwd" : "ntt_cols_out");
+        check_launch(phase == 0 ? "ntt_cols_fwd" : "ntt_cols_out",
+                     dim3(unsigned(n / k.cols), phase == 0 ? 2 : 1, 1), dim3(k.threads));
     }
 }
 

@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <chrono>
 #include <numeric>
+#include <vector>
 
 #include "../../include/mmm_cu.h"
 
@@ -47,15 +48,28 @@ Poly from_u32(const uint32_t* w, int64_t n) {
 }
 
 struct Clock {
-    uint64_t k0 = mmm_cu_launch_count();
     std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
     SimReport report(std::int64_t s) const {
         SimReport r;
-        r.kernels = std::int64_t(mmm_cu_launch_count() - k0);
         r.block_param = s;
         r.device_ms = std::chrono::duration<double, std::milli>(
                           std::chrono::steady_clock::now() - t0)
                           .count();
+        int32_t n = 0;
+        ok(mmm_cu_last_schedule(nullptr, 0, &n));
+        std::vector<mmm_kernel_rec> recs(size_t(std::max(n, 0)));
+        ok(mmm_cu_last_schedule(recs.data(), int32_t(recs.size()), &n));
+        StructuralMetrics& st = r.metrics.structure;
+        for (const auto& k : recs) {
+            KernelMetrics km;
+            km.name = k.name;
+            km.blocks = k.blocks;
+            km.threads = k.threads;
+            st.N += k.blocks;
+            st.K = std::max(st.K, k.blocks);
+            r.kernels.push_back(std::move(km));
+        }
+        st.L = st.pi = std::int64_t(recs.size());
         return r;
     }
 };

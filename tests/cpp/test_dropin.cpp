@@ -173,7 +173,11 @@ static void multiplication_cases() {  // test_multiplication.cpp
                 for (std::int64_t l : {1, 4, 16}) {
                     auto res = mmm::run_multiplication(params(), G, A, B, s, l);
                     CHECK(res.f == want);
-                    CHECK(res.sim.kernels >= 1);
+                    CHECK(!res.sim.kernels.empty());
+                    CHECK(res.sim.metrics.structure.L == int64_t(res.sim.kernels.size()));
+                    CHECK(res.sim.metrics.structure.N >= res.sim.metrics.structure.K);
+                    CHECK(res.sim.metrics.structure.K >= 1);
+                    CHECK(res.sim.kernels[0].name.rfind("mul_kernel", 0) == 0);
                 }
         }
     }

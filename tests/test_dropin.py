@@ -43,3 +43,25 @@ def test_verify_detects_injected_fault(binaries):
     r = subprocess.run([os.path.join(binaries, "mmm_verify"), "--inject-fault", "--trials", "5",
                         "--app", "division"], capture_output=True, text=True, timeout=300)
     assert r.returncode == 2, r.stdout + r.stderr
+
+
+REF_BENCH_SRC = "/root/reference/proj/tools/bench.cpp"
+REF_BENCH_BIN = os.path.join(ROOT, "oracle", "_ref", "ref_tools_bench")
+
+
+@pytest.mark.skipif(not os.path.exists(REF_BENCH_SRC), reason="reference sources absent")
+def test_reference_bench_tool_builds_against_dropin(binaries):
+    """/root/reference/proj/tools/bench.cpp:43-64 reads run_*(...).sim.metrics.W:
+    compiled unmodified against include/ it must build and link."""
+    subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "tests", "cpp"), "refbench"],
+                   check=True)
+    assert os.path.exists(REF_BENCH_BIN)
+
+
+@pytest.mark.gpu
+def test_reference_bench_tool_runs(binaries):
+    if not os.path.exists(REF_BENCH_BIN):
+        pytest.skip("oracle/_ref/ref_tools_bench not built (needs /root/reference at build time)")
+    r = subprocess.run([REF_BENCH_BIN], capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "MISMATCH" not in r.stdout and r.stdout.count("\n") >= 6, r.stdout

@@ -272,3 +272,22 @@ def test_out_arrays_dirty_and_rejected(cuda_lib, port):
             mmm.mul_batched(A, B, P, out=bad)
     with pytest.raises(mmm.InvalidArgument):
         mmm.mul(A[0], B[0], P, out=np.zeros(10, np.uint32))
+
+
+def test_last_schedule_reports_the_launches(cuda_lib, port):
+    """mmm_cu_last_schedule: the kernels of the thread's last host call (what
+    the drop-in's SimReport.kernels and N/L/K are built from)."""
+    mmm = cuda_lib
+    rng = np.random.default_rng(51)
+    a, b = _rand(rng, P, 3000), _rand(rng, P, 1200)
+    mmm.gcd(port.mul(a[:500], b[:300], P), b, P)
+    sched = mmm.last_schedule()
+    assert [k[0] for k in sched] == ["gcd_kernel"] and sched[0][1] >= 2 and sched[0][2] > 0
+    mmm.mul(a, b, P)
+    sched = mmm.last_schedule()
+    assert sched and all(k[0] == "mul_kernel" for k in sched)
+    big_a, big_b = _rand(rng, P, 70_000), _rand(rng, P, 33_000)
+    mmm.divmod(big_a, big_b, P, s=128)
+    assert [k[0] for k in mmm.last_schedule()] == ["div_pipe_kernel"]
+    mmm.divmod(big_a, big_b[:1], P)
+    assert [k[0] for k in mmm.last_schedule()] == ["div_const_kernel"]
