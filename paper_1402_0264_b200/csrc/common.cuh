@@ -197,6 +197,11 @@ void launch_mul(const FieldParams& F, const uint32_t* a, int64_t na, const uint3
 void launch_mul_batched(const FieldParams& F, const uint32_t* A, int64_t lda, int64_t na,
                         const uint32_t* B, int64_t ldb, int64_t nb, int64_t count, uint32_t* Fo,
                         int64_t ldf, int64_t s, cudaStream_t st);
+// tensor-core batched product (tcmul.cu): na, nb <= 4096, exact like launch_mul_batched.
+bool tcmul_supported(int64_t na, int64_t nb, int64_t count);
+void launch_tcmul_batched(const FieldParams& F, const uint32_t* A, int64_t lda, int64_t na,
+                          const uint32_t* B, int64_t ldb, int64_t nb, int64_t count, Fan Fo,
+                          int64_t ldf, cudaStream_t st);
 // division: q[0 .. na-nb+1), r[0 .. nb-1).  b[nb-1] != 0, na >= nb >= 1.
 void launch_divmod(const FieldParams& F, const uint32_t* a, int64_t na, const uint32_t* b,
                    int64_t nb, uint32_t* q, uint32_t* r, int64_t s, cudaStream_t st);

@@ -279,6 +279,10 @@ void launch_mul_batched(const FieldParams& F, const uint32_t* A, int64_t lda, in
 void launch_mul_batched_fan(const FieldParams& F, const uint32_t* A, int64_t lda, int64_t na,
                             const uint32_t* B, int64_t ldb, int64_t nb, int64_t count, Fan Fo,
                             int64_t ldf, int64_t s, cudaStream_t st) {
+    if (tcmul_supported(na, nb, count)) {  // integer tensor core (tcmul.cu)
+        launch_tcmul_batched(F, A, lda, na, B, ldb, nb, count, Fo, ldf, st);
+        return;
+    }
     const int R = pick_tile(s, F);
     const int64_t TK = int64_t(MUL_T) * R;
     const int64_t nf = na + nb - 1;

@@ -1,0 +1,325 @@
+// tcmul.cu -- batched exact polynomial products over Z/pZ on the sm_100a
+// integer tensor core (tcgen05.mma kind::i8, u8 x u8 -> s32 in TMEM).
+//
+// Computes exactly what oracle_mul computes (proj/src/oracle.cpp:8-15),
+// f[k] = sum_i a[i] b[k-i] mod p, for every instance of a batch with
+// na, nb <= 4096 terms (cfg5's 4096 x 4096 products).
+//
+// Block Toeplitz form (block size 128).  With
+//   H_d[r][t] = a[128 d + r - t]   (0 outside [0, na)),  B_j[t] = b[128 j + t],
+// output block c of the product is f[128 c + r] = sum_{d + j = c} (H_d B_j)[r]:
+// for each d, one 128 x 128 Toeplitz tile times all of b's blocks -- a GEMM
+// with M = 128 (rows r), K = 128 (t), N = b's blocks.  Exactness: residues
+// (< 2^31) split into four u8 limbs, a = sum_u 2^(8u) a_u, b = sum_v 2^(8v) b_v;
+// the u8 x u8 products accumulate exactly in s32.
+//
+// Everything accumulates in TMEM.  Plane s = u + v (0..6) holds, for every
+// output block c (0..63), column 64 s + c of the 128-lane accumulator:
+//   P_s[r][c] = sum_{u+v=s} sum_{d+j=c} (H^u_d B^v_j)[r]   (< 33*4*128*255^2 < 2^31).
+// The B operand of d's MMAs lists rows n = 64 v + j (v = 0..3, j < 32: the
+// limb blocks of b, zero rows between), so the MMA for limb u of H_d written
+// at TMEM column 64 u + d lands (u, v, j) on column 64 (u + v) + (d + j):
+// limb-plane and output-block bookkeeping are both done by the tensor core's
+// column offset.  MMA D columns must be even: odd d uses a copy of the B
+// operand shifted by one row and the column offset d - 1.  At the end,
+//   f[128 c + r] = sum_s P_s[r][c] 2^(8 s)  mod p        (one reduction).
+//
+// Per instance: stage a (smem), build both B copies (limb transpose), zero
+// TMEM; then for each d the 4 limb tiles of H_d are built into one of two
+// buffers while the tensor core runs the previous d's 16 MMAs (128 x N x 32,
+// N = 224 / 240); one thread issues, tcgen05.commit -> mbarrier frees the
+// buffer.  Persistent: one CTA per SM walks the batch.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdlib>
+
+#include "common.cuh"
+#include "tc.cuh"
+
+namespace mmm_cu {
+
+namespace {
+
+constexpr int TCM_T = 256;                 // 8 warps: all build, warp 0 lane 0 issues
+constexpr int TCM_MAXN = 4096;             // terms per operand
+constexpr int TCM_APAD = 128;              // zero words before a (and after, to 4096 + 256)
+constexpr int TCM_AWORDS = TCM_APAD + TCM_MAXN + 256;
+constexpr uint32_t TILE = 128 * 128;       // one limb tile of H_d (bytes)
+constexpr uint32_t HBUF = 4 * TILE;        // four limb tiles
+constexpr uint32_t BROWS_E = 224, BROWS_O = 240;
+// shared layout (bytes, from a 1024-aligned base)
+constexpr uint32_t OFF_H = 0;                            // 2 x HBUF
+constexpr uint32_t OFF_BE = OFF_H + 2 * HBUF;            // 224 rows
+constexpr uint32_t OFF_BO = OFF_BE + BROWS_E * 128;      // 240 rows
+constexpr uint32_t OFF_A = OFF_BO + BROWS_O * 128;       // u32 a, padded
+constexpr uint32_t SMEM_BYTES = OFF_A + TCM_AWORDS * 4 + 1024;
+
+struct TcArgs {
+    const uint32_t* A;
+    const uint32_t* B;
+    int64_t lda, ldb, ldf;
+    int na, nb;
+    int64_t count;
+    Fan F;
+    FieldParams Fp;
+    uint32_t c_hi[3];  // 2^32, 2^40, 2^48 mod p
+};
+
+// 4 x 4 byte transpose: out[u] = byte u of w0, w1, w2, w3 (little-endian order)
+__device__ __forceinline__ void limb_transpose(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3,
+                                               uint32_t& l0, uint32_t& l1, uint32_t& l2,
+                                               uint32_t& l3) {
+    const uint32_t x0 = __byte_perm(w0, w1, 0x5140), x1 = __byte_perm(w0, w1, 0x7362);
+    const uint32_t x2 = __byte_perm(w2, w3, 0x5140), x3 = __byte_perm(w2, w3, 0x7362);
+    l0 = __byte_perm(x0, x2, 0x5410);
+    l1 = __byte_perm(x0, x2, 0x7632);
+    l2 = __byte_perm(x1, x3, 0x5410);
+    l3 = __byte_perm(x1, x3, 0x7632);
+}
+
+__device__ __forceinline__ void sts128(uint8_t* base, uint32_t off, uint32_t a, uint32_t b,
+                                       uint32_t c, uint32_t d) {
+    *reinterpret_cast<uint4*>(base + off) = make_uint4(a, b, c, d);
+}
+
+// 16 words w[0..15] (element t = 16c + t') of row `row`, chunk c, into the four
+// limb tiles at `h` (tile u at h + u * TILE).
+__device__ __forceinline__ void put_row_chunk(uint8_t* h, uint32_t tile_stride, uint32_t row,
+                                              uint32_t c, const uint32_t (&w)[16]) {
+    uint32_t L[4][4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+        limb_transpose(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3], L[0][q], L[1][q],
+                       L[2][q], L[3][q]);
+    const uint32_t off = tc::sw128(row, 16 * c);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) sts128(h + u * tile_stride, off, L[u][0], L[u][1], L[u][2], L[u][3]);
+}
+
+// H_d limb tiles: thread (warp w, lane L) builds rows 4 rg .. 4 rg + 3 of chunk c,
+// rg = 4 w + L / 8, c = L % 8 (conflict-free loads and swizzled stores).
+__device__ __forceinline__ void build_h(uint8_t* hbuf, const uint32_t* a_pad, int d) {
+    const int w = threadIdx.x >> 5, L = threadIdx.x & 31;
+    const int rg = 4 * w + (L >> 3), c = L & 7;
+    // rows r = 4 rg + k need a[i0 + k - t'], t' = 0..15, i0 = 128 d + 4 rg - 16 c:
+    // words a[i0 - 16 .. i0 + 3] (20, 16-byte aligned with the pad of 128)
+    const int i0 = 128 * d + 4 * rg - 16 * c;
+    const uint4* src = reinterpret_cast<const uint4*>(a_pad + TCM_APAD + i0 - 16);
+    uint32_t x[20];
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+        const uint4 v = src[q];
+        x[4 * q] = v.x;
+        x[4 * q + 1] = v.y;
+        x[4 * q + 2] = v.z;
+        x[4 * q + 3] = v.w;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        uint32_t wv[16];
+#pragma unroll
+        for (int t = 0; t < 16; ++t) wv[t] = x[16 + k - t];  // a[i0 + k - t]
+        put_row_chunk(hbuf, TILE, uint32_t(4 * rg + k), uint32_t(c), wv);
+    }
+}
+
+__device__ __forceinline__ void tmem_st32_zero(uint32_t taddr) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+        "{%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,"
+        "%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr),
+        "r"(0u)
+        : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+                   "=r"(v[6]), "=r"(v[7])
+                 : "r"(taddr));
+}
+
+template <bool FAN>
+__global__ void __launch_bounds__(TCM_T, 1) tcmul_kernel(TcArgs g) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+    uint8_t* sH = sm + OFF_H;
+    uint8_t* sBE = sm + OFF_BE;
+    uint8_t* sBO = sm + OFF_BO;
+    uint32_t* a_pad = reinterpret_cast<uint32_t*>(sm + OFF_A);
+    __shared__ uint64_t mbar[2];  // H buffer b's MMAs done
+    __shared__ uint32_t tslot;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int na = g.na, nb = g.nb;
+    const int mB = (nb + 127) >> 7;
+    const int D = (na + 126) / 128 + 1;           // d = 0 .. D-1 (H_d nonzero)
+    const int nf = na + nb - 1;
+    const int nc = (nf + 127) >> 7;               // output blocks
+
+    // zero the B copies and the a pad once (data rows are rewritten per instance)
+    for (uint32_t i = tid; i < (BROWS_E + BROWS_O) * 128 / 16; i += TCM_T)
+        reinterpret_cast<uint4*>(sBE)[i] = make_uint4(0, 0, 0, 0);
+    for (int i = tid; i < TCM_AWORDS; i += TCM_T) a_pad[i] = 0;
+    if (warp == 0) tc::tmem_alloc<512>(&tslot);
+    if (tid == 0) {
+        tc::mbar_init(&mbar[0], 1);
+        tc::mbar_init(&mbar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    const uint32_t tbase = tslot;
+    uint32_t ph[2] = {0, 0};
+    constexpr uint32_t ID_E = tc::idesc_u8(128, BROWS_E), ID_O = tc::idesc_u8(128, BROWS_O);
+
+    for (int64_t inst = blockIdx.x; inst < g.count; inst += gridDim.x) {
+        const uint32_t* a = g.A + inst * g.lda;
+        const uint32_t* b = g.B + inst * g.ldb;
+        // ---- stage a, build the B operand copies, zero the accumulator ----
+        for (int i = tid; i < na; i += TCM_T) a_pad[TCM_APAD + i] = __ldg(a + i);
+        // B rows: (v, j) -> E row 64 v + j, O row 64 v + j + 1; unit = (j, chunk c)
+        for (int u = tid; u < mB * 8; u += TCM_T) {
+            const int j = u >> 3, c = u & 7;
+            uint32_t wv[16];
+#pragma unroll
+            for (int t = 0; t < 16; ++t) {
+                const int k = 128 * j + 16 * c + t;
+                wv[t] = k < nb ? __ldg(b + k) : 0u;
+            }
+            uint32_t L[4][4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                limb_transpose(wv[4 * q], wv[4 * q + 1], wv[4 * q + 2], wv[4 * q + 3], L[0][q],
+                               L[1][q], L[2][q], L[3][q]);
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                sts128(sBE, tc::sw128(64 * v + j, 16 * c), L[v][0], L[v][1], L[v][2], L[v][3]);
+                sts128(sBO, tc::sw128(64 * v + j + 1, 16 * c), L[v][0], L[v][1], L[v][2], L[v][3]);
+            }
+        }
+        if (warp < 4) {
+#pragma unroll
+            for (int c0 = 0; c0 < 512; c0 += 32) tmem_st32_zero(tbase + (uint32_t(warp * 32) << 16) + c0);
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        }
+        __syncthreads();  // a staged
+        build_h(sH, a_pad, 0);
+        tc::fence_async_smem();
+        tc::fence_before_sync();
+        __syncthreads();
+        tc::fence_after_sync();
+
+        for (int d = 0; d < D; ++d) {
+            const int buf = d & 1;
+            if (tid == 0) {
+                const uint32_t hb = tc::smem_u32(sH + buf * HBUF);
+                const bool odd = d & 1;
+                const uint32_t bb = tc::smem_u32(odd ? sBO : sBE);
+                const uint32_t idesc = odd ? ID_O : ID_E;
+                const uint32_t col = uint32_t(d & ~1);
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        tc::mma_u8(tbase + 64 * u + col, tc::desc_sw128(hb + u * TILE + 32 * k),
+                                   tc::desc_sw128(bb + 32 * k), idesc, 1u);
+                tc::commit(&mbar[buf]);
+            }
+            if (d + 1 < D) {
+                if (d >= 1) {  // buffer (d+1)&1 was read by d-1's MMAs
+                    tc::mbar_wait(&mbar[buf ^ 1], ph[buf ^ 1]);
+                    ph[buf ^ 1] ^= 1;
+                }
+                build_h(sH + (buf ^ 1) * HBUF, a_pad, d + 1);
+                tc::fence_async_smem();
+            }
+            tc::fence_before_sync();
+            __syncthreads();
+            tc::fence_after_sync();
+        }
+        // drain: D-1's commit covers every MMA issued so far; D-2's commit (the
+        // other buffer, not waited in the loop) has completed too -- consume it
+        {
+            const int lb = (D - 1) & 1;
+            tc::mbar_wait(&mbar[lb], ph[lb]);
+            ph[lb] ^= 1;
+            if (D >= 2) {
+                tc::mbar_wait(&mbar[lb ^ 1], ph[lb ^ 1]);
+                ph[lb ^ 1] ^= 1;
+            }
+        }
+        tc::fence_after_sync();
+        // ---- epilogue: warps w and w+4 share lanes 32 (w % 4) .. +31 ----
+        {
+            const int r = 32 * (warp & 3) + lane;
+            const int cbeg = (warp >> 2) * 32;
+            const uint32_t lane_addr = tbase + (uint32_t(32 * (warp & 3)) << 16);
+            const FieldParams& Fp = g.Fp;
+            const int64_t fb = inst * g.ldf;
+            for (int c0 = cbeg; c0 < cbeg + 32 && c0 < nc; c0 += 8) {
+                uint32_t x[7][8];
+#pragma unroll
+                for (int s = 0; s < 7; ++s) tmem_ld8(lane_addr + 64 * s + c0, x[s]);
+                tc::tmem_ld_wait();
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    const int k = 128 * (c0 + e) + r;
+                    uint64_t v = uint64_t(x[0][e]) + (uint64_t(x[1][e]) << 8) +
+                                 (uint64_t(x[2][e]) << 16) + (uint64_t(x[3][e]) << 24);
+                    v += uint64_t(x[4][e]) * g.c_hi[0];
+                    v += uint64_t(x[5][e]) * g.c_hi[1];
+                    v += uint64_t(x[6][e]) * g.c_hi[2];
+                    if (k < nf) fan_store<FAN>(g.F, fb + k, reduce(v, Fp));
+                }
+            }
+        }
+        tc::fence_before_sync();
+        __syncthreads();  // TMEM read before the next instance zeroes it
+        tc::fence_after_sync();
+    }
+    __syncthreads();
+    if (warp == 0) tc::tmem_free<512>(tbase);
+}
+
+}  // namespace
+
+bool tcmul_supported(int64_t na, int64_t nb, int64_t count) {
+    if (const char* e = getenv("MMM_MUL_TC")) return atoi(e) != 0 && na <= TCM_MAXN && nb <= TCM_MAXN && na >= 1 && nb >= 1;
+    // worth a persistent tensor-core pass: enough products of enough terms
+    return na <= TCM_MAXN && nb <= TCM_MAXN && na >= 512 && nb >= 512 &&
+           double(na) * double(nb) * double(count) >= 1.0e9;
+}
+
+void launch_tcmul_batched(const FieldParams& F, const uint32_t* A, int64_t lda, int64_t na,
+                          const uint32_t* B, int64_t ldb, int64_t nb, int64_t count, Fan Fo,
+                          int64_t ldf, cudaStream_t st) {
+    if (count <= 0) return;
+    if (na < 1 || nb < 1 || na > TCM_MAXN || nb > TCM_MAXN)
+        throw Error(ST_INVALID, "tensor-core product: operands of 1..4096 terms");
+    TcArgs g{};
+    g.A = A;
+    g.B = B;
+    g.lda = lda;
+    g.ldb = ldb;
+    g.ldf = ldf;
+    g.na = int(na);
+    g.nb = int(nb);
+    g.count = count;
+    g.F = Fo;
+    g.Fp = F;
+    for (int s = 0; s < 3; ++s) {
+        uint64_t x = 1;
+        for (int e = 0; e < 32 + 8 * s; ++e) x = (x * 2) % F.p;
+        g.c_hi[s] = uint32_t(x);
+    }
+    auto kern = Fo.n > 1 ? tcmul_kernel<true> : tcmul_kernel<false>;
+    MMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES)));
+    const int blocks = int(std::min<int64_t>(count, sm_count()));
+    kern<<<blocks, TCM_T, SMEM_BYTES, st>>>(g);
+    check_launch("tcmul_kernel", dim3(blocks), dim3(TCM_T));
+}
+
+}  // namespace mmm_cu

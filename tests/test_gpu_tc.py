@@ -1,0 +1,93 @@
+"""GPU parity of the tensor-core batched product (csrc/tcmul.cu: tcgen05
+kind::i8 limb-split Toeplitz GEMM) against the CPU oracle and the IMAD.WIDE
+product kernel: bit-exact for every shape class it accepts (1..4096 terms per
+operand, ragged block edges, odd/even Toeplitz offsets, primes from 2 to
+2^31 - 1, limb values up to 255 in every position)."""
+import numpy as np
+import pytest
+
+import suites
+
+pytestmark = pytest.mark.gpu
+
+P = suites.P_BENCH
+
+
+def _batch(rng, p, cnt, na, nb, extreme=False):
+    if extreme:  # every limb 255 where p allows: the s32 accumulation bound
+        A = np.full((cnt, na), p - 1, dtype=np.int64)
+        B = np.full((cnt, nb), p - 1, dtype=np.int64)
+    else:
+        A = rng.integers(0, p, (cnt, na))
+        B = rng.integers(0, p, (cnt, nb))
+    return A, B
+
+
+@pytest.mark.parametrize("p", [P, 2147483647, 2013265921, 101, 7, 2])
+def test_tc_product_vs_oracle(cuda_lib, port, monkeypatch, p):
+    mmm = cuda_lib
+    rng = np.random.default_rng(p % 10007)
+    monkeypatch.setenv("MMM_MUL_TC", "1")
+    shapes = [(1, 1), (1, 4096), (4096, 1), (128, 128), (129, 127), (1000, 3000), (4096, 4096),
+              (4095, 4093), (257, 4096), (4096, 300)]
+    for na, nb in shapes:
+        A, B = _batch(rng, p, 3, na, nb)
+        F = mmm.mul_batched(A, B, p)
+        for i in range(3):
+            want = port.mul(A[i], B[i], p)
+            got = np.trim_zeros(F[i].astype(np.int64), "b")
+            assert np.array_equal(got, want), (p, na, nb, i)
+
+
+def test_tc_product_accumulation_bound(cuda_lib, port, monkeypatch):
+    """All coefficients p - 1 (limbs 0xFF where possible): the largest plane sums."""
+    mmm = cuda_lib
+    monkeypatch.setenv("MMM_MUL_TC", "1")
+    for p in (2147483647, P):
+        A, B = _batch(None, p, 2, 4096, 4096, extreme=True)
+        F = mmm.mul_batched(A, B, p)
+        want = port.mul(A[0], B[0], p)
+        assert np.array_equal(F[0].astype(np.int64), want)
+        assert np.array_equal(F[1], F[0])
+
+
+def test_tc_product_equals_imad_kernel_large_batch(cuda_lib, monkeypatch):
+    """A batch larger than the grid (instances walk the persistent CTAs) with
+    strided rows: tensor-core and IMAD.WIDE kernels agree word for word."""
+    import torch
+    mmm = cuda_lib
+    rng = np.random.default_rng(3)
+    cnt, na, nb = 400, 2048, 1500
+    A = rng.integers(0, P, (cnt, na + 5)).astype(np.uint32)
+    B = rng.integers(0, P, (cnt, nb + 3)).astype(np.uint32)
+    dA = torch.from_numpy(A.view(np.int32)).cuda()
+    dB = torch.from_numpy(B.view(np.int32)).cuda()
+    nf = na + nb - 1
+    outs = []
+    for tc in ("1", "0"):
+        monkeypatch.setenv("MMM_MUL_TC", tc)
+        dF = torch.full((cnt, nf + 7), -1, dtype=torch.int32, device="cuda")
+        mmm.mul_batched_dev(P, dA.data_ptr(), na + 5, na, dB.data_ptr(), nb + 3, nb, cnt,
+                            dF.data_ptr(), nf + 7, stream=torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        outs.append(dF.cpu().numpy())
+    assert np.array_equal(outs[0], outs[1])
+    assert (outs[0][:, nf:] == -1).all()  # nothing written past each row
+
+
+def test_tc_product_fanout(cuda_lib, monkeypatch):
+    import torch
+    mmm = cuda_lib
+    monkeypatch.setenv("MMM_MUL_TC", "1")
+    rng = np.random.default_rng(4)
+    cnt, n = 5, 700
+    A = rng.integers(0, P, (cnt, n)).astype(np.uint32)
+    dA = torch.from_numpy(A.view(np.int32)).cuda()
+    outs = [torch.zeros((cnt, 2 * n - 1), dtype=torch.int32, device="cuda") for _ in range(3)]
+    mmm.mul_batched_fanout_dev(P, dA.data_ptr(), n, n, dA.data_ptr(), n, n, cnt,
+                               [o.data_ptr() for o in outs], 2 * n - 1,
+                               stream=torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    want = mmm.mul_batched(A, A, P)
+    for o in outs:
+        assert np.array_equal(o.cpu().numpy().view(np.uint32), want)
