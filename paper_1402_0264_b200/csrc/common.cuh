@@ -202,6 +202,11 @@ bool tcmul_supported(int64_t na, int64_t nb, int64_t count);
 void launch_tcmul_batched(const FieldParams& F, const uint32_t* A, int64_t lda, int64_t na,
                           const uint32_t* B, int64_t ldb, int64_t nb, int64_t count, Fan Fo,
                           int64_t ldf, cudaStream_t st);
+// tensor-core batched division (tcdiv.cu): 2 <= nb <= 4096, nb <= na <= 8192.
+bool tcdiv_supported(int64_t na, int64_t nb, int64_t count);
+void launch_tcdiv_batched(const FieldParams& F, const uint32_t* A, int64_t lda, int64_t na,
+                          const uint32_t* B, int64_t ldb, int64_t nb, int64_t count, Fan Q,
+                          int64_t ldq, Fan R, int64_t ldr, cudaStream_t st);
 // division: q[0 .. na-nb+1), r[0 .. nb-1).  b[nb-1] != 0, na >= nb >= 1.
 void launch_divmod(const FieldParams& F, const uint32_t* a, int64_t na, const uint32_t* b,
                    int64_t nb, uint32_t* q, uint32_t* r, int64_t s, cudaStream_t st);

@@ -1013,6 +1013,10 @@ void launch_divmod_batched_fan(const FieldParams& F, const uint32_t* A, int64_t 
         run_const(F, A, lda, na, B, ldb, count, Q, ldq, st);
         return;
     }
+    if (tcdiv_supported(na, nb, count)) {  // 128 heads per step on the tensor core (tcdiv.cu)
+        launch_tcdiv_batched(F, A, lda, na, B, ldb, nb, count, Q, ldq, Rr, ldr, st);
+        return;
+    }
     if (cta_smem_words(na, nb, g.S, R, borg) * 4 > 200 * 1024) {
         // instances too large for one CTA: one single-instance division each
         // (grid or pipelined schedule), results fanned out by a copy kernel

@@ -32,28 +32,18 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "common.cuh"
 #include "tc.cuh"
+#include "tctile.cuh"
 
 namespace mmm_cu {
 
 namespace {
 
-constexpr int TCM_T = 256;                 // 8 warps: all build, warp 0 lane 0 issues
-constexpr int TCM_MAXN = 4096;             // terms per operand
-constexpr int TCM_APAD = 128;              // zero words before a (and after, to 4096 + 256)
-constexpr int TCM_AWORDS = TCM_APAD + TCM_MAXN + 256;
-constexpr uint32_t TILE = 128 * 128;       // one limb tile of H_d (bytes)
-constexpr uint32_t HBUF = 4 * TILE;        // four limb tiles
-constexpr uint32_t BROWS_E = 224, BROWS_O = 240;
-// shared layout (bytes, from a 1024-aligned base)
-constexpr uint32_t OFF_H = 0;                            // 2 x HBUF
-constexpr uint32_t OFF_BE = OFF_H + 2 * HBUF;            // 224 rows
-constexpr uint32_t OFF_BO = OFF_BE + BROWS_E * 128;      // 240 rows
-constexpr uint32_t OFF_A = OFF_BO + BROWS_O * 128;       // u32 a, padded
-constexpr uint32_t SMEM_BYTES = OFF_A + TCM_AWORDS * 4 + 1024;
+using namespace tct;
 
 struct TcArgs {
     const uint32_t* A;
@@ -66,79 +56,8 @@ struct TcArgs {
     uint32_t c_hi[3];  // 2^32, 2^40, 2^48 mod p
 };
 
-// 4 x 4 byte transpose: out[u] = byte u of w0, w1, w2, w3 (little-endian order)
-__device__ __forceinline__ void limb_transpose(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3,
-                                               uint32_t& l0, uint32_t& l1, uint32_t& l2,
-                                               uint32_t& l3) {
-    const uint32_t x0 = __byte_perm(w0, w1, 0x5140), x1 = __byte_perm(w0, w1, 0x7362);
-    const uint32_t x2 = __byte_perm(w2, w3, 0x5140), x3 = __byte_perm(w2, w3, 0x7362);
-    l0 = __byte_perm(x0, x2, 0x5410);
-    l1 = __byte_perm(x0, x2, 0x7632);
-    l2 = __byte_perm(x1, x3, 0x5410);
-    l3 = __byte_perm(x1, x3, 0x7632);
-}
-
-__device__ __forceinline__ void sts128(uint8_t* base, uint32_t off, uint32_t a, uint32_t b,
-                                       uint32_t c, uint32_t d) {
-    *reinterpret_cast<uint4*>(base + off) = make_uint4(a, b, c, d);
-}
-
-// 16 words w[0..15] (element t = 16c + t') of row `row`, chunk c, into the four
-// limb tiles at `h` (tile u at h + u * TILE).
-__device__ __forceinline__ void put_row_chunk(uint8_t* h, uint32_t tile_stride, uint32_t row,
-                                              uint32_t c, const uint32_t (&w)[16]) {
-    uint32_t L[4][4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-        limb_transpose(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3], L[0][q], L[1][q],
-                       L[2][q], L[3][q]);
-    const uint32_t off = tc::sw128(row, 16 * c);
-#pragma unroll
-    for (int u = 0; u < 4; ++u) sts128(h + u * tile_stride, off, L[u][0], L[u][1], L[u][2], L[u][3]);
-}
-
-// H_d limb tiles: thread (warp w, lane L) builds rows 4 rg .. 4 rg + 3 of chunk c,
-// rg = 4 w + L / 8, c = L % 8 (conflict-free loads and swizzled stores).
-__device__ __forceinline__ void build_h(uint8_t* hbuf, const uint32_t* a_pad, int d) {
-    const int w = threadIdx.x >> 5, L = threadIdx.x & 31;
-    const int rg = 4 * w + (L >> 3), c = L & 7;
-    // rows r = 4 rg + k need a[i0 + k - t'], t' = 0..15, i0 = 128 d + 4 rg - 16 c:
-    // words a[i0 - 16 .. i0 + 3] (20, 16-byte aligned with the pad of 128)
-    const int i0 = 128 * d + 4 * rg - 16 * c;
-    const uint4* src = reinterpret_cast<const uint4*>(a_pad + TCM_APAD + i0 - 16);
-    uint32_t x[20];
-#pragma unroll
-    for (int q = 0; q < 5; ++q) {
-        const uint4 v = src[q];
-        x[4 * q] = v.x;
-        x[4 * q + 1] = v.y;
-        x[4 * q + 2] = v.z;
-        x[4 * q + 3] = v.w;
-    }
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        uint32_t wv[16];
-#pragma unroll
-        for (int t = 0; t < 16; ++t) wv[t] = x[16 + k - t];  // a[i0 + k - t]
-        put_row_chunk(hbuf, TILE, uint32_t(4 * rg + k), uint32_t(c), wv);
-    }
-}
-
-__device__ __forceinline__ void tmem_st32_zero(uint32_t taddr) {
-    asm volatile(
-        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
-        "{%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,"
-        "%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr),
-        "r"(0u)
-        : "memory");
-}
-
-__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
-                   "=r"(v[6]), "=r"(v[7])
-                 : "r"(taddr));
-}
+// MMM_TC_STATS builds: per-phase clock sums (CTA 0, thread 0) in tcm_stats
+__device__ long long tcm_stats[8];
 
 template <bool FAN>
 __global__ void __launch_bounds__(TCM_T, 1) tcmul_kernel(TcArgs g) {
@@ -175,7 +94,9 @@ __global__ void __launch_bounds__(TCM_T, 1) tcmul_kernel(TcArgs g) {
     uint32_t ph[2] = {0, 0};
     constexpr uint32_t ID_E = tc::idesc_u8(128, BROWS_E), ID_O = tc::idesc_u8(128, BROWS_O);
 
+    long long t_pro = 0, t_loop = 0, t_epi = 0, t_mmawait = 0, t0 = clock64(), t1;
     for (int64_t inst = blockIdx.x; inst < g.count; inst += gridDim.x) {
+        t0 = clock64();
         const uint32_t* a = g.A + inst * g.lda;
         const uint32_t* b = g.B + inst * g.ldb;
         // ---- stage a, build the B operand copies, zero the accumulator ----
@@ -211,6 +132,9 @@ __global__ void __launch_bounds__(TCM_T, 1) tcmul_kernel(TcArgs g) {
         tc::fence_before_sync();
         __syncthreads();
         tc::fence_after_sync();
+        t1 = clock64();
+        t_pro += t1 - t0;
+        t0 = t1;
 
         for (int d = 0; d < D; ++d) {
             const int buf = d & 1;
@@ -230,8 +154,10 @@ __global__ void __launch_bounds__(TCM_T, 1) tcmul_kernel(TcArgs g) {
             }
             if (d + 1 < D) {
                 if (d >= 1) {  // buffer (d+1)&1 was read by d-1's MMAs
+                    const long long tw = clock64();
                     tc::mbar_wait(&mbar[buf ^ 1], ph[buf ^ 1]);
                     ph[buf ^ 1] ^= 1;
+                    t_mmawait += clock64() - tw;
                 }
                 build_h(sH + (buf ^ 1) * HBUF, a_pad, d + 1);
                 tc::fence_async_smem();
@@ -252,6 +178,9 @@ __global__ void __launch_bounds__(TCM_T, 1) tcmul_kernel(TcArgs g) {
             }
         }
         tc::fence_after_sync();
+        t1 = clock64();
+        t_loop += t1 - t0;
+        t0 = t1;
         // ---- epilogue: warps w and w+4 share lanes 32 (w % 4) .. +31 ----
         {
             const int r = 32 * (warp & 3) + lane;
@@ -279,6 +208,13 @@ __global__ void __launch_bounds__(TCM_T, 1) tcmul_kernel(TcArgs g) {
         tc::fence_before_sync();
         __syncthreads();  // TMEM read before the next instance zeroes it
         tc::fence_after_sync();
+        t_epi += clock64() - t0;
+    }
+    if (blockIdx.x == 0 && tid == 0) {
+        tcm_stats[0] = t_pro;
+        tcm_stats[1] = t_loop;
+        tcm_stats[2] = t_epi;
+        tcm_stats[3] = t_mmawait;
     }
     __syncthreads();
     if (warp == 0) tc::tmem_free<512>(tbase);
@@ -320,6 +256,13 @@ void launch_tcmul_batched(const FieldParams& F, const uint32_t* A, int64_t lda, 
     const int blocks = int(std::min<int64_t>(count, sm_count()));
     kern<<<blocks, TCM_T, SMEM_BYTES, st>>>(g);
     check_launch("tcmul_kernel", dim3(blocks), dim3(TCM_T));
+    if (getenv("MMM_TC_STATS")) {
+        long long h[8];
+        MMM_CUDA(cudaMemcpyFromSymbolAsync(h, tcm_stats, sizeof(h), 0, cudaMemcpyDeviceToHost, st));
+        MMM_CUDA(cudaStreamSynchronize(st));
+        fprintf(stderr, "tcmul stats (CTA 0): prologue=%lld loop=%lld epilogue=%lld mma_wait=%lld cycles\n",
+                h[0], h[1], h[2], h[3]);
+    }
 }
 
 }  // namespace mmm_cu

@@ -91,3 +91,41 @@ def test_tc_product_fanout(cuda_lib, monkeypatch):
     want = mmm.mul_batched(A, A, P)
     for o in outs:
         assert np.array_equal(o.cpu().numpy().view(np.uint32), want)
+
+
+# ------------------------------------------------ tensor-core division ----
+@pytest.mark.parametrize("p", [P, 2147483647, 101, 7, 2])
+def test_tc_division_vs_oracle(cuda_lib, port, monkeypatch, p):
+    """csrc/tcdiv.cu (128 heads per step, remainder accumulated on the tensor
+    core) == oracle_divmod, including quotient lengths that are not multiples
+    of 128, mu = 1, 2-term divisors and degree drops over small fields."""
+    mmm = cuda_lib
+    monkeypatch.setenv("MMM_DIV_TC", "1")
+    rng = np.random.default_rng(77 + p % 1000)
+    shapes = [(8192, 4096), (8191, 4096), (5000, 3000), (4096, 4096), (4097, 4096), (8192, 2),
+              (300, 129), (1000, 999), (8192, 129), (130, 2), (6000, 700), (257, 128)]
+    for na, nb in shapes:
+        A = rng.integers(0, p, (2, na))
+        B = rng.integers(0, p, (2, nb))
+        B[:, -1] = np.maximum(B[:, -1], 1)
+        Q, R = mmm.divmod_batched(A, B, p)
+        for i in range(2):
+            wq, wr = port.divmod(A[i], B[i], p)
+            assert np.array_equal(np.trim_zeros(Q[i].astype(np.int64), "b"), wq), (p, na, nb, i)
+            assert np.array_equal(np.trim_zeros(R[i].astype(np.int64), "b"), wr), (p, na, nb, i)
+
+
+def test_tc_division_equals_cta_kernel(cuda_lib, monkeypatch):
+    """Many instances (the persistent grid walks the batch), strided rows:
+    tensor-core and CUDA-core division agree word for word."""
+    mmm = cuda_lib
+    rng = np.random.default_rng(8)
+    cnt, na, nb = 300, 8192, 4096
+    A = rng.integers(0, P, (cnt, na))
+    B = rng.integers(0, P, (cnt, nb))
+    B[:, -1] = np.maximum(B[:, -1], 1)
+    outs = []
+    for tc in ("1", "0"):
+        monkeypatch.setenv("MMM_DIV_TC", tc)
+        outs.append(mmm.divmod_batched(A, B, P))
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
