@@ -47,7 +47,7 @@ constexpr uint32_t D_OFF_BO = D_OFF_BE + BROWS_E * 128;
 constexpr uint32_t D_OFF_Q = D_OFF_BO + BROWS_O * 128;    // u32 Q (padded)
 constexpr uint32_t D_OFF_A = D_OFF_Q + TCD_QWORDS * 4;    // u32 a (as given)
 constexpr uint32_t D_OFF_SM = D_OFF_A + TCD_MAXA * 4;     // small arrays
-constexpr uint32_t D_SMALL = 128 * 5;                     // bp0, h, S, E, tmp
+constexpr uint32_t D_SMALL = 128 + 256 + 128 + 128 + 1024 + 128;  // bp0, h (padded), S, E, parts, tmp
 constexpr uint32_t D_SMEM_BYTES = D_OFF_SM + D_SMALL * 4 + 1024;
 
 struct TcDivArgs {
@@ -74,17 +74,59 @@ struct Acc {
     }
 };
 
-__device__ __forceinline__ uint64_t shfl_xor64(uint64_t v, int m) {
-    return __shfl_xor_sync(0xffffffffu, v, m);
+// Partial sums of y[i] = sum_{t<T} X[i - t] W[t] (i < n; n % 4 == 0, T % 16 == 0,
+// X 16-byte aligned and defined -- zero where the product has no term -- on
+// [-T, n)).  Thread (row group g: rows 4g..4g+3, t-part p: t in [16p, 16p+16))
+// keeps the four rows' X windows in registers and slides them 4 terms per
+// 16-byte load; W[t] is a broadcast.  part[p * n + i] = partial, reduced.
+__device__ __forceinline__ void toeplitz_partials(const uint32_t* X, const uint32_t* W, int n,
+                                                  int T, uint32_t* part, const FieldParams& F) {
+    const int ng = n >> 2, np = T >> 4;
+    const int tid = threadIdx.x;
+    if (tid >= ng * np) return;
+    const int g = tid % ng, p = tid / ng, r0 = 4 * g, t0 = 16 * p;
+    uint4 cv = *reinterpret_cast<const uint4*>(X + r0 - t0);
+    uint32_t cur[4] = {cv.x, cv.y, cv.z, cv.w};  // X[r0 - t + k]
+    uint64_t acc[4] = {0, 0, 0, 0};
+    const uint32_t ft = F.fold_terms;
+#pragma unroll
+    for (int jb = 0; jb < 4; ++jb) {
+        const int t = t0 + 4 * jb;
+        const uint4 nv = *reinterpret_cast<const uint4*>(X + r0 - t - 4);
+        const uint4 wv = *reinterpret_cast<const uint4*>(W + t);
+        const uint32_t z[8] = {nv.x, nv.y, nv.z, nv.w, cur[0], cur[1], cur[2], cur[3]};
+        const uint32_t w4[4] = {wv.x, wv.y, wv.z, wv.w};
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                acc[k] = mad_wide(z[4 + k - jj], w4[jj], acc[k]);
+                if (ft < 4) acc[k] = fold(acc[k], F);
+            }
+        }
+        if (ft >= 4 && ft < 16)
+#pragma unroll
+            for (int k = 0; k < 4; ++k) acc[k] = fold(acc[k], F);
+        cur[0] = nv.x;
+        cur[1] = nv.y;
+        cur[2] = nv.z;
+        cur[3] = nv.w;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) part[p * n + r0 + k] = reduce(acc[k], F);
 }
 
-// Sum the 4 sub-thread partials of a row pair (lanes 4m .. 4m+3), reduced.
-__device__ __forceinline__ uint32_t quad_reduce(Acc a, const FieldParams& F) {
-    uint64_t v = reduce(a.v, F);  // < p
-    v += shfl_xor64(v, 1);
-    v += shfl_xor64(v, 2);
+// y[i] = sum over the T/16 partials, mod p (threads i < n).
+__device__ __forceinline__ uint32_t partials_sum(const uint32_t* part, int n, int T, int i,
+                                                 const FieldParams& F) {
+    uint64_t v = 0;
+    for (int p = 0; p < (T >> 4); ++p) v += part[p * n + i];
     return reduce(v, F);
 }
+
+__device__ long long tcd_stats[8];
+#define TCD_T0() const long long _t0 = clock64()
+#define TCD_ACC(i) st[i] += clock64() - _t0
 
 template <bool FAN>
 __global__ void __launch_bounds__(TCD_T, 1) tcdiv_kernel(TcDivArgs g) {
@@ -97,10 +139,11 @@ __global__ void __launch_bounds__(TCD_T, 1) tcdiv_kernel(TcDivArgs g) {
     uint32_t* q_pad = reinterpret_cast<uint32_t*>(sm + D_OFF_Q);
     uint32_t* a_s = reinterpret_cast<uint32_t*>(sm + D_OFF_A);
     uint32_t* bp0 = reinterpret_cast<uint32_t*>(sm + D_OFF_SM);  // B'[0..128)
-    uint32_t* hs = bp0 + 128;                                     // B'^-1 mod X^128
+    uint32_t* hs = bp0 + 128 + 128;                               // B'^-1 mod X^128, 128 zeros before
     uint32_t* sS = hs + 128;                                      // block K of the sum
     uint32_t* sE = sS + 128;
-    uint32_t* tmp = sE + 128;
+    uint32_t* part = sE + 128;                                    // [8][128] partial sums
+    uint32_t* tmp = part + 1024;
     __shared__ uint64_t mbar;
     __shared__ uint32_t tslot;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -109,12 +152,11 @@ __global__ void __launch_bounds__(TCD_T, 1) tcdiv_kernel(TcDivArgs g) {
     const int mu = na - nb + 1, db = nb - 1;
     const int mB = (nb + 127) >> 7;
     const int Kq = (mu + 127) >> 7;  // quotient blocks; tiles d = 0 .. Kq
-    // row pair (m, 127 - m), sub-thread sub: terms t == sub (mod 4)
-    const int pm = tid >> 2, sub = tid & 3;
 
     for (uint32_t i = tid; i < (BROWS_E + BROWS_O) * 128 / 16; i += TCD_T)
         reinterpret_cast<uint4*>(sBE)[i] = make_uint4(0, 0, 0, 0);
     for (int i = tid; i < TCD_QWORDS; i += TCD_T) q_pad[i] = 0;
+    for (int i = tid; i < 128; i += TCD_T) hs[i - 128] = 0;
     if (warp == 0) tc::tmem_alloc<512>(&tslot);
     if (tid == 0) {
         tc::mbar_init(&mbar, 1);
@@ -128,9 +170,11 @@ __global__ void __launch_bounds__(TCD_T, 1) tcdiv_kernel(TcDivArgs g) {
     constexpr uint32_t ID_E = tc::idesc_u8(128, BROWS_E), ID_O = tc::idesc_u8(128, BROWS_O);
     const uint32_t lane_addr = tbase + (uint32_t(32 * (warp & 3)) << 16);
 
+    long long st[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     for (int64_t inst = blockIdx.x; inst < g.count; inst += gridDim.x) {
         const uint32_t* a = g.A + inst * g.lda;
         const uint32_t* b = g.B + inst * g.ldb;
+        long long tp = clock64();
         // ---- stage a; B' operand copies (rows 64 v + j [+1]); B'_0; zero TMEM ----
         for (int i = tid; i < na; i += TCD_T) a_s[i] = __ldg(a + i);
         for (int u = tid; u < mB * 8; u += TCD_T) {
@@ -159,10 +203,12 @@ __global__ void __launch_bounds__(TCD_T, 1) tcdiv_kernel(TcDivArgs g) {
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         }
         __syncthreads();
+        st[0] += clock64() - tp;
+        tp = clock64();
         // ---- h = B'^-1 mod X^128 by Newton doubling ----
         if (tid == 0) hs[0] = invmod(bp0[0], F);
         __syncthreads();
-        for (int k = 1; k < 128; k <<= 1) {
+        for (int k = 1; k < 16; k <<= 1) {
             // e[i] = sum_{m<k} B'[k+i-m] h[m]  (i < k): coefficients [k, 2k) of B' h_k
             if (tid < k) {
                 Acc e;
@@ -177,67 +223,73 @@ __global__ void __launch_bounds__(TCD_T, 1) tcdiv_kernel(TcDivArgs g) {
             }
             __syncthreads();
         }
+        for (int k = 16; k < 128; k <<= 1) {  // the same doubling with sliding products
+            toeplitz_partials(bp0 + k, hs, k, k, part, F);
+            __syncthreads();
+            if (tid < k) tmp[tid] = partials_sum(part, k, k, tid, F);
+            __syncthreads();
+            toeplitz_partials(hs, tmp, k, k, part, F);  // h[i-m], zero for i < m
+            __syncthreads();
+            if (tid < k) hs[k + tid] = negmod(partials_sum(part, k, k, tid, F), F);
+            __syncthreads();
+        }
 
+        st[1] += clock64() - tp;
         for (int K = 0; K <= Kq; ++K) {
             if (K >= 1) {
+                TCD_T0();
                 tc::mbar_wait(&mbar, ph);  // tile K-1 is in the planes
                 ph ^= 1;
                 tc::fence_after_sync();
+                TCD_ACC(2);
             }
             if (K < Kq) {
-                // ---- block K of the running sum, from TMEM (warps 0-3: row = lane) ----
+                TCD_T0();
+                // ---- block K of the running sum, from TMEM (warps 0-3: row = lane);
+                //      block K of Q cleared (U below reads it as zeros) ----
+                uint32_t* qk = q_pad + TCM_APAD + 128 * K;
                 if (warp < 4) {
                     uint32_t x[7];
 #pragma unroll
                     for (int s = 0; s < 7; ++s) x[s] = tmem_ld1(lane_addr + 64 * s + K);
                     tc::tmem_ld_wait();
                     sS[32 * warp + lane] = combine_planes(x, g.c_hi, F);
+                } else {
+                    qk[tid - 128] = 0;
                 }
                 __syncthreads();
-                // ---- E = A' - S - U(Q_{K-1}) B'_0, rows (pm, 127 - pm) ----
-                const uint32_t* qprev = q_pad + TCM_APAD + 128 * K - 128;  // block K-1
-                {
-                    Acc u1, u2;
-                    const int r1 = pm, r2 = 127 - pm;
-                    for (int t = r1 + 1 + ((sub - r1 - 1) & 3); t < 128; t += 4)
-                        u1.add(qprev[128 + r1 - t], bp0[t], F);
-                    for (int t = r2 + 1 + ((sub - r2 - 1) & 3); t < 128; t += 4)
-                        u2.add(qprev[128 + r2 - t], bp0[t], F);
-                    const uint32_t U1 = quad_reduce(u1, F), U2 = quad_reduce(u2, F);
-                    if (sub == 0) {
-                        const int k1 = 128 * K + r1, k2 = 128 * K + r2;
-                        const uint32_t a1 = k1 < na ? a_s[na - 1 - k1] : 0u;
-                        const uint32_t a2 = k2 < na ? a_s[na - 1 - k2] : 0u;
-                        sE[r1] = submod(submod(a1, sS[r1], F), U1, F);
-                        sE[r2] = submod(submod(a2, sS[r2], F), U2, F);
-                    }
+                // ---- U = (upper triangle of H_K) B'_0: the part of block K that
+                //      Q_{K-1} determines beyond the planes; E = A' - S - U ----
+                toeplitz_partials(qk, bp0, 128, 128, part, F);
+                __syncthreads();
+                if (tid < 128) {
+                    const int k1 = 128 * K + tid;
+                    const uint32_t a1 = k1 < na ? a_s[na - 1 - k1] : 0u;
+                    sE[tid] = submod(submod(a1, sS[tid], F), partials_sum(part, 128, 128, tid, F), F);
                 }
                 __syncthreads();
                 // ---- Q_K = E * h mod X^128 ----
-                {
-                    Acc s1, s2;
-                    const int i1 = pm, i2 = 127 - pm;
-                    for (int t = sub; t <= i1; t += 4) s1.add(sE[t], hs[i1 - t], F);
-                    for (int t = sub; t <= i2; t += 4) s2.add(sE[t], hs[i2 - t], F);
-                    const uint32_t Q1 = quad_reduce(s1, F), Q2 = quad_reduce(s2, F);
-                    if (sub == 0) {
-                        const int k1 = 128 * K + i1, k2 = 128 * K + i2;
-                        const uint32_t v1 = k1 < mu ? Q1 : 0u, v2 = k2 < mu ? Q2 : 0u;
-                        q_pad[TCM_APAD + k1] = v1;
-                        q_pad[TCM_APAD + k2] = v2;
-                        const int64_t qb = inst * g.ldq;
-                        if (k1 < mu) fan_store<FAN>(g.Q, qb + (mu - 1 - k1), v1);
-                        if (k2 < mu) fan_store<FAN>(g.Q, qb + (mu - 1 - k2), v2);
-                    }
+                toeplitz_partials(hs, sE, 128, 128, part, F);
+                __syncthreads();
+                if (tid < 128) {
+                    const int k1 = 128 * K + tid;
+                    const uint32_t v1 = k1 < mu ? partials_sum(part, 128, 128, tid, F) : 0u;
+                    qk[tid] = v1;
+                    if (k1 < mu) fan_store<FAN>(g.Q, inst * g.ldq + (mu - 1 - k1), v1);
                 }
                 __syncthreads();
+                TCD_ACC(3);
             }
             // ---- tile H_K (Q_K lower, Q_{K-1} upper) into the planes ----
+            {
+            TCD_T0();
             build_h(sH, q_pad, K);
             tc::fence_async_smem();
             tc::fence_before_sync();
             __syncthreads();
             tc::fence_after_sync();
+            TCD_ACC(4);
+            }
             if (tid == 0) {
                 const uint32_t hb = tc::smem_u32(sH);
                 const bool odd = K & 1;
@@ -253,6 +305,7 @@ __global__ void __launch_bounds__(TCD_T, 1) tcdiv_kernel(TcDivArgs g) {
                 tc::commit(&mbar);
             }
         }
+        tp = clock64();
         tc::mbar_wait(&mbar, ph);  // the last tile
         ph ^= 1;
         tc::fence_after_sync();
@@ -276,7 +329,10 @@ __global__ void __launch_bounds__(TCD_T, 1) tcdiv_kernel(TcDivArgs g) {
         tc::fence_before_sync();
         __syncthreads();  // TMEM read before the next instance zeroes it
         tc::fence_after_sync();
+        st[5] += clock64() - tp;
     }
+    if (blockIdx.x == 0 && tid == 0)
+        for (int i = 0; i < 8; ++i) tcd_stats[i] = st[i];
     __syncthreads();
     if (warp == 0) tc::tmem_free<512>(tbase);
 }
@@ -320,6 +376,13 @@ void launch_tcdiv_batched(const FieldParams& F, const uint32_t* A, int64_t lda, 
     const int blocks = int(std::min<int64_t>(count, sm_count()));
     kern<<<blocks, TCD_T, D_SMEM_BYTES, st>>>(g);
     check_launch("tcdiv_kernel", dim3(blocks), dim3(TCD_T));
+    if (getenv("MMM_TC_STATS")) {
+        long long h[8];
+        MMM_CUDA(cudaMemcpyFromSymbolAsync(h, tcd_stats, sizeof(h), 0, cudaMemcpyDeviceToHost, st));
+        MMM_CUDA(cudaStreamSynchronize(st));
+        fprintf(stderr, "tcdiv stats (CTA 0, thread 0): prologue=%lld newton=%lld mma_wait=%lld "
+                "head_solve=%lld build=%lld tail=%lld cycles\n", h[0], h[1], h[2], h[3], h[4], h[5]);
+    }
 }
 
 }  // namespace mmm_cu
