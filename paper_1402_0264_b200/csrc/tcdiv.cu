@@ -39,15 +39,14 @@ using namespace tct;
 
 constexpr int TCD_T = 256;
 constexpr int TCD_MAXA = 8192;
-constexpr int TCD_QWORDS = TCM_APAD + TCD_MAXA + 256;  // Q, padded like a_pad
+constexpr int TCD_QPAD = 256;                           // zero words before Q
+constexpr int TCD_QWORDS = TCD_QPAD + TCD_MAXA + 256;   // Q, padded
 // shared layout (bytes, 1024-aligned base)
-constexpr uint32_t D_OFF_H = 0;                           // one H buffer (4 limb tiles)
-constexpr uint32_t D_OFF_BE = D_OFF_H + HBUF;
-constexpr uint32_t D_OFF_BO = D_OFF_BE + BROWS_E * 128;
-constexpr uint32_t D_OFF_Q = D_OFF_BO + BROWS_O * 128;    // u32 Q (padded)
-constexpr uint32_t D_OFF_A = D_OFF_Q + TCD_QWORDS * 4;    // u32 a (as given)
-constexpr uint32_t D_OFF_SM = D_OFF_A + TCD_MAXA * 4;     // small arrays
-constexpr uint32_t D_SMALL = 128 + 256 + 128 + 128 + 1024 + 128;  // bp0, h (padded), S, E, parts, tmp
+constexpr uint32_t D_OFF_H = 0;                           // two H buffers (4 limb tiles each)
+constexpr uint32_t D_OFF_B = D_OFF_H + 2 * HBUF;          // B_PRE | 240 rows (tctile.cuh)
+constexpr uint32_t D_OFF_Q = D_OFF_B + B_BYTES;           // u32 Q (padded)
+constexpr uint32_t D_OFF_SM = D_OFF_Q + TCD_QWORDS * 4;   // small arrays
+constexpr uint32_t D_SMALL = 256 + 256 + 128 + 128 + 1024 + 128;  // B'[0..256), h (padded), S, E, parts, tmp
 constexpr uint32_t D_SMEM_BYTES = D_OFF_SM + D_SMALL * 4 + 1024;
 
 struct TcDivArgs {
@@ -116,6 +115,49 @@ __device__ __forceinline__ void toeplitz_partials(const uint32_t* X, const uint3
     for (int k = 0; k < 4; ++k) part[p * n + r0 + k] = reduce(acc[k], F);
 }
 
+// n = T = 128 rows / terms twice: part = partials of
+//   sum_{t<128} X[i - t] W[t]  +  sum_{t<128} X[i - 128 - t] W[128 + t]
+// (one 256-term Toeplitz product, X defined on [-256, 128)).
+__device__ __forceinline__ void toeplitz_partials_256(const uint32_t* X, const uint32_t* W,
+                                                      uint32_t* part, const FieldParams& F) {
+    const int tid = threadIdx.x;
+    const int g = tid & 31, p = tid >> 5, r0 = 4 * g;
+    uint64_t acc[4] = {0, 0, 0, 0};
+    const uint32_t ft = F.fold_terms;
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+        const uint32_t* Xh = X - 128 * half;
+        const uint32_t* Wh = W + 128 * half;
+        const int t0 = 16 * p;
+        const uint4 cv = *reinterpret_cast<const uint4*>(Xh + r0 - t0);
+        uint32_t cur[4] = {cv.x, cv.y, cv.z, cv.w};
+#pragma unroll
+        for (int jb = 0; jb < 4; ++jb) {
+            const int t = t0 + 4 * jb;
+            const uint4 nv = *reinterpret_cast<const uint4*>(Xh + r0 - t - 4);
+            const uint4 wv = *reinterpret_cast<const uint4*>(Wh + t);
+            const uint32_t z[8] = {nv.x, nv.y, nv.z, nv.w, cur[0], cur[1], cur[2], cur[3]};
+            const uint32_t w4[4] = {wv.x, wv.y, wv.z, wv.w};
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    acc[k] = mad_wide(z[4 + k - jj], w4[jj], acc[k]);
+                    if (ft < 4) acc[k] = fold(acc[k], F);
+                }
+            if (ft >= 4 && ft < 32)
+#pragma unroll
+                for (int k = 0; k < 4; ++k) acc[k] = fold(acc[k], F);
+            cur[0] = nv.x;
+            cur[1] = nv.y;
+            cur[2] = nv.z;
+            cur[3] = nv.w;
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) part[p * 128 + r0 + k] = reduce(acc[k], F);
+}
+
 // y[i] = sum over the T/16 partials, mod p (threads i < n).
 __device__ __forceinline__ uint32_t partials_sum(const uint32_t* part, int n, int T, int i,
                                                  const FieldParams& F) {
@@ -134,13 +176,12 @@ __global__ void __launch_bounds__(TCD_T, 1) tcdiv_kernel(TcDivArgs g) {
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
     uint8_t* sH = sm + D_OFF_H;
-    uint8_t* sBE = sm + D_OFF_BE;
-    uint8_t* sBO = sm + D_OFF_BO;
+    uint8_t* sBE = sm + D_OFF_B + B_PRE;
     uint32_t* q_pad = reinterpret_cast<uint32_t*>(sm + D_OFF_Q);
-    uint32_t* a_s = reinterpret_cast<uint32_t*>(sm + D_OFF_A);
-    uint32_t* bp0 = reinterpret_cast<uint32_t*>(sm + D_OFF_SM);  // B'[0..128)
-    uint32_t* hs = bp0 + 128 + 128;                               // B'^-1 mod X^128, 128 zeros before
-    uint32_t* sS = hs + 128;                                      // block K of the sum
+    uint32_t* qz = q_pad + TCD_QPAD;                               // Q[0] (Q[-256..-1] = 0)
+    uint32_t* bp01 = reinterpret_cast<uint32_t*>(sm + D_OFF_SM);  // B'[0..256)
+    uint32_t* hs = bp01 + 256 + 128;                              // B'^-1 mod X^128, 128 zeros before
+    uint32_t* sS = hs + 128;                                      // planes' block K+1
     uint32_t* sE = sS + 128;
     uint32_t* part = sE + 128;                                    // [8][128] partial sums
     uint32_t* tmp = part + 1024;
@@ -149,12 +190,12 @@ __global__ void __launch_bounds__(TCD_T, 1) tcdiv_kernel(TcDivArgs g) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const FieldParams F = g.Fp;
     const int na = g.na, nb = g.nb;
-    const int mu = na - nb + 1, db = nb - 1;
+    const int mu = na - nb + 1;
     const int mB = (nb + 127) >> 7;
     const int Kq = (mu + 127) >> 7;  // quotient blocks; tiles d = 0 .. Kq
 
-    for (uint32_t i = tid; i < (BROWS_E + BROWS_O) * 128 / 16; i += TCD_T)
-        reinterpret_cast<uint4*>(sBE)[i] = make_uint4(0, 0, 0, 0);
+    for (uint32_t i = tid; i < B_BYTES / 16; i += TCD_T)
+        reinterpret_cast<uint4*>(sm + D_OFF_B)[i] = make_uint4(0, 0, 0, 0);
     for (int i = tid; i < TCD_QWORDS; i += TCD_T) q_pad[i] = 0;
     for (int i = tid; i < 128; i += TCD_T) hs[i - 128] = 0;
     if (warp == 0) tc::tmem_alloc<512>(&tslot);
@@ -170,13 +211,28 @@ __global__ void __launch_bounds__(TCD_T, 1) tcdiv_kernel(TcDivArgs g) {
     constexpr uint32_t ID_E = tc::idesc_u8(128, BROWS_E), ID_O = tc::idesc_u8(128, BROWS_O);
     const uint32_t lane_addr = tbase + (uint32_t(32 * (warp & 3)) << 16);
 
+    // tile K into the planes from H buffer K & 1 (one thread)
+    auto issue = [&](int K) {
+        const uint32_t hb = tc::smem_u32(sH + (K & 1) * HBUF);
+        const bool odd = K & 1;
+        const uint32_t bb = tc::smem_u32(sBE) - (odd ? 128u : 0u);
+        const uint32_t idesc = odd ? ID_O : ID_E;
+        const uint32_t col = uint32_t(K & ~1);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                tc::mma_u8(tbase + 64 * u + col, tc::desc_sw128(hb + u * TILE + 32 * k),
+                           tc::desc_sw128(bb + 32 * k), idesc, 1u);
+        tc::commit(&mbar);
+    };
+
     long long st[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     for (int64_t inst = blockIdx.x; inst < g.count; inst += gridDim.x) {
         const uint32_t* a = g.A + inst * g.lda;
         const uint32_t* b = g.B + inst * g.ldb;
         long long tp = clock64();
-        // ---- stage a; B' operand copies (rows 64 v + j [+1]); B'_0; zero TMEM ----
-        for (int i = tid; i < na; i += TCD_T) a_s[i] = __ldg(a + i);
+        // ---- B' operand (rows 64 v + j), B'[0..256), zero TMEM, S_0 = 0 ----
         for (int u = tid; u < mB * 8; u += TCD_T) {
             const int j = u >> 3, c = u & 7;
             uint32_t wv[16];
@@ -191,12 +247,16 @@ __global__ void __launch_bounds__(TCD_T, 1) tcdiv_kernel(TcDivArgs g) {
                 limb_transpose(wv[4 * q], wv[4 * q + 1], wv[4 * q + 2], wv[4 * q + 3], L[0][q],
                                L[1][q], L[2][q], L[3][q]);
 #pragma unroll
-            for (int v = 0; v < 4; ++v) {
+            for (int v = 0; v < 4; ++v)
                 sts128(sBE, tc::sw128(64 * v + j, 16 * c), L[v][0], L[v][1], L[v][2], L[v][3]);
-                sts128(sBO, tc::sw128(64 * v + j + 1, 16 * c), L[v][0], L[v][1], L[v][2], L[v][3]);
-            }
         }
-        if (tid < 128) bp0[tid] = tid < nb ? __ldg(b + (nb - 1 - tid)) : 0u;
+        bp01[tid] = tid < nb ? __ldg(b + (nb - 1 - tid)) : 0u;
+        if (tid < 128) {
+            sS[tid] = 0;
+            qz[tid] = 0;  // Q block 0 (a previous instance's values)
+        }
+        // A' block 0 (rows r < 128)
+        uint32_t aK = (tid < 128 && tid < na) ? __ldg(a + (na - 1 - tid)) : 0u;
         if (warp < 4) {
 #pragma unroll
             for (int c0 = 0; c0 < 512; c0 += 32) tmem_st32_zero(lane_addr + c0);
@@ -206,13 +266,13 @@ __global__ void __launch_bounds__(TCD_T, 1) tcdiv_kernel(TcDivArgs g) {
         st[0] += clock64() - tp;
         tp = clock64();
         // ---- h = B'^-1 mod X^128 by Newton doubling ----
-        if (tid == 0) hs[0] = invmod(bp0[0], F);
+        if (tid == 0) hs[0] = invmod(bp01[0], F);
         __syncthreads();
         for (int k = 1; k < 16; k <<= 1) {
             // e[i] = sum_{m<k} B'[k+i-m] h[m]  (i < k): coefficients [k, 2k) of B' h_k
             if (tid < k) {
                 Acc e;
-                for (int m = 0; m < k; ++m) e.add(bp0[k + tid - m], hs[m], F);
+                for (int m = 0; m < k; ++m) e.add(bp01[k + tid - m], hs[m], F);
                 tmp[tid] = reduce(e.v, F);
             }
             __syncthreads();
@@ -224,7 +284,7 @@ __global__ void __launch_bounds__(TCD_T, 1) tcdiv_kernel(TcDivArgs g) {
             __syncthreads();
         }
         for (int k = 16; k < 128; k <<= 1) {  // the same doubling with sliding products
-            toeplitz_partials(bp0 + k, hs, k, k, part, F);
+            toeplitz_partials(bp01 + k, hs, k, k, part, F);
             __syncthreads();
             if (tid < k) tmp[tid] = partials_sum(part, k, k, tid, F);
             __syncthreads();
@@ -233,43 +293,27 @@ __global__ void __launch_bounds__(TCD_T, 1) tcdiv_kernel(TcDivArgs g) {
             if (tid < k) hs[k + tid] = negmod(partials_sum(part, k, k, tid, F), F);
             __syncthreads();
         }
-
         st[1] += clock64() - tp;
-        for (int K = 0; K <= Kq; ++K) {
-            if (K >= 1) {
+
+        // Step K: Q_K from block K of A' - sum_{I<K} Q_I X^(128 I) B', where the
+        // planes hold tiles <= K-2 (read into sS before tile K-1 was issued)
+        // and the two tiles K-1 (against B'_1) and K (against B'_0) that Q
+        // blocks < K determine come from one 256-term product on the CUDA
+        // cores; tile K-1 runs on the tensor core meanwhile.
+        for (int K = 0; K < Kq; ++K) {
+            uint32_t* qk = qz + 128 * K;  // Q block K (zero here)
+            {
                 TCD_T0();
-                tc::mbar_wait(&mbar, ph);  // tile K-1 is in the planes
-                ph ^= 1;
-                tc::fence_after_sync();
-                TCD_ACC(2);
-            }
-            if (K < Kq) {
-                TCD_T0();
-                // ---- block K of the running sum, from TMEM (warps 0-3: row = lane);
-                //      block K of Q cleared (U below reads it as zeros) ----
-                uint32_t* qk = q_pad + TCM_APAD + 128 * K;
-                if (warp < 4) {
-                    uint32_t x[7];
-#pragma unroll
-                    for (int s = 0; s < 7; ++s) x[s] = tmem_ld1(lane_addr + 64 * s + K);
-                    tc::tmem_ld_wait();
-                    sS[32 * warp + lane] = combine_planes(x, g.c_hi, F);
-                } else {
-                    qk[tid - 128] = 0;
-                }
-                __syncthreads();
-                // ---- U = (upper triangle of H_K) B'_0: the part of block K that
-                //      Q_{K-1} determines beyond the planes; E = A' - S - U ----
-                toeplitz_partials(qk, bp0, 128, 128, part, F);
+                toeplitz_partials_256(qk, bp01, part, F);
                 __syncthreads();
                 if (tid < 128) {
-                    const int k1 = 128 * K + tid;
-                    const uint32_t a1 = k1 < na ? a_s[na - 1 - k1] : 0u;
-                    sE[tid] = submod(submod(a1, sS[tid], F), partials_sum(part, 128, 128, tid, F), F);
+                    sE[tid] = submod(submod(aK, sS[tid], F), partials_sum(part, 128, 128, tid, F),
+                                     F);
+                    const int kn = 128 * (K + 1) + tid;  // prefetch A' block K+1
+                    aK = kn < na ? __ldg(a + (na - 1 - kn)) : 0u;
                 }
                 __syncthreads();
-                // ---- Q_K = E * h mod X^128 ----
-                toeplitz_partials(hs, sE, 128, 128, part, F);
+                toeplitz_partials(hs, sE, 128, 128, part, F);  // Q_K = E h mod X^128
                 __syncthreads();
                 if (tid < 128) {
                     const int k1 = 128 * K + tid;
@@ -280,36 +324,51 @@ __global__ void __launch_bounds__(TCD_T, 1) tcdiv_kernel(TcDivArgs g) {
                 __syncthreads();
                 TCD_ACC(3);
             }
-            // ---- tile H_K (Q_K lower, Q_{K-1} upper) into the planes ----
             {
-            TCD_T0();
-            build_h(sH, q_pad, K);
-            tc::fence_async_smem();
-            tc::fence_before_sync();
-            __syncthreads();
-            tc::fence_after_sync();
-            TCD_ACC(4);
+                TCD_T0();
+                build_h(sH + (K & 1) * HBUF, qz - TCM_APAD, K);  // tile K (Q_K, Q_{K-1})
+                tc::fence_async_smem();
+                TCD_ACC(4);
             }
-            if (tid == 0) {
-                const uint32_t hb = tc::smem_u32(sH);
-                const bool odd = K & 1;
-                const uint32_t bb = tc::smem_u32(odd ? sBO : sBE);
-                const uint32_t idesc = odd ? ID_O : ID_E;
-                const uint32_t col = uint32_t(K & ~1);
+            {
+                TCD_T0();
+                if (K >= 1) {  // tile K-1 done: the planes' block K+1 holds tiles <= K-1
+                    tc::mbar_wait(&mbar, ph);
+                    ph ^= 1;
+                }
+                tc::fence_after_sync();
+                if (warp < 4) {
+                    uint32_t x[7];
 #pragma unroll
-                for (int u = 0; u < 4; ++u)
-#pragma unroll
-                    for (int k = 0; k < 4; ++k)
-                        tc::mma_u8(tbase + 64 * u + col, tc::desc_sw128(hb + u * TILE + 32 * k),
-                                   tc::desc_sw128(bb + 32 * k), idesc, 1u);
-                tc::commit(&mbar);
+                    for (int s = 0; s < 7; ++s) x[s] = tmem_ld1(lane_addr + 64 * s + K + 1);
+                    tc::tmem_ld_wait();
+                    sS[32 * warp + lane] = combine_planes(x, g.c_hi, F);
+                } else {
+                    qk[tid] = 0;  // Q block K+1 (tid - 128 + 128)
+                }
+                tc::fence_before_sync();
+                __syncthreads();
+                tc::fence_after_sync();
+                TCD_ACC(2);
             }
+            if (tid == 0) issue(K);
         }
         tp = clock64();
-        tc::mbar_wait(&mbar, ph);  // the last tile
+        // ---- the last tile (Q_{Kq-1}'s upper triangle), then the remainder ----
+        build_h(sH + (Kq & 1) * HBUF, qz - TCM_APAD, Kq);
+        tc::fence_async_smem();
+        if (Kq >= 1) {  // every thread consumes tile Kq-1's phase (parity aliasing otherwise)
+            tc::mbar_wait(&mbar, ph);
+            ph ^= 1;
+        }
+        tc::fence_before_sync();
+        __syncthreads();
+        tc::fence_after_sync();
+        if (tid == 0) issue(Kq);
+        tc::mbar_wait(&mbar, ph);
         ph ^= 1;
         tc::fence_after_sync();
-        // ---- remainder: r[na-1-k] = A'[k] - (Q B')[k], k in [mu, na) ----
+        // r[na-1-k] = A'[k] - (Q B')[k], k in [mu, na)
         {
             const int r = 32 * (warp & 3) + lane;
             const int cfirst = mu >> 7, clast = (na - 1) >> 7;
@@ -322,7 +381,7 @@ __global__ void __launch_bounds__(TCD_T, 1) tcdiv_kernel(TcDivArgs g) {
                 const int k = 128 * c + r;
                 if (k >= mu && k < na) {
                     const uint32_t S = combine_planes(x, g.c_hi, F);
-                    fan_store<FAN>(g.R, rb + (na - 1 - k), submod(a_s[na - 1 - k], S, F));
+                    fan_store<FAN>(g.R, rb + (na - 1 - k), submod(__ldg(a + (na - 1 - k)), S, F));
                 }
             }
         }
@@ -380,7 +439,7 @@ void launch_tcdiv_batched(const FieldParams& F, const uint32_t* A, int64_t lda, 
         long long h[8];
         MMM_CUDA(cudaMemcpyFromSymbolAsync(h, tcd_stats, sizeof(h), 0, cudaMemcpyDeviceToHost, st));
         MMM_CUDA(cudaStreamSynchronize(st));
-        fprintf(stderr, "tcdiv stats (CTA 0, thread 0): prologue=%lld newton=%lld mma_wait=%lld "
+        fprintf(stderr, "tcdiv stats (CTA 0, thread 0): prologue=%lld newton=%lld wait+read=%lld "
                 "head_solve=%lld build=%lld tail=%lld cycles\n", h[0], h[1], h[2], h[3], h[4], h[5]);
     }
 }

@@ -65,8 +65,7 @@ __global__ void __launch_bounds__(TCM_T, 1) tcmul_kernel(TcArgs g) {
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
     uint8_t* sH = sm + OFF_H;
-    uint8_t* sBE = sm + OFF_BE;
-    uint8_t* sBO = sm + OFF_BO;
+    uint8_t* sBE = sm + OFF_B + B_PRE;
     uint32_t* a_pad = reinterpret_cast<uint32_t*>(sm + OFF_A);
     __shared__ uint64_t mbar[2];  // H buffer b's MMAs done
     __shared__ uint32_t tslot;
@@ -78,8 +77,8 @@ __global__ void __launch_bounds__(TCM_T, 1) tcmul_kernel(TcArgs g) {
     const int nc = (nf + 127) >> 7;               // output blocks
 
     // zero the B copies and the a pad once (data rows are rewritten per instance)
-    for (uint32_t i = tid; i < (BROWS_E + BROWS_O) * 128 / 16; i += TCM_T)
-        reinterpret_cast<uint4*>(sBE)[i] = make_uint4(0, 0, 0, 0);
+    for (uint32_t i = tid; i < B_BYTES / 16; i += TCM_T)
+        reinterpret_cast<uint4*>(sm + OFF_B)[i] = make_uint4(0, 0, 0, 0);
     for (int i = tid; i < TCM_AWORDS; i += TCM_T) a_pad[i] = 0;
     if (warp == 0) tc::tmem_alloc<512>(&tslot);
     if (tid == 0) {
@@ -118,7 +117,6 @@ __global__ void __launch_bounds__(TCM_T, 1) tcmul_kernel(TcArgs g) {
 #pragma unroll
             for (int v = 0; v < 4; ++v) {
                 sts128(sBE, tc::sw128(64 * v + j, 16 * c), L[v][0], L[v][1], L[v][2], L[v][3]);
-                sts128(sBO, tc::sw128(64 * v + j + 1, 16 * c), L[v][0], L[v][1], L[v][2], L[v][3]);
             }
         }
         if (warp < 4) {
@@ -141,7 +139,7 @@ __global__ void __launch_bounds__(TCM_T, 1) tcmul_kernel(TcArgs g) {
             if (tid == 0) {
                 const uint32_t hb = tc::smem_u32(sH + buf * HBUF);
                 const bool odd = d & 1;
-                const uint32_t bb = tc::smem_u32(odd ? sBO : sBE);
+                const uint32_t bb = tc::smem_u32(sBE) - (odd ? 128u : 0u);
                 const uint32_t idesc = odd ? ID_O : ID_E;
                 const uint32_t col = uint32_t(d & ~1);
 #pragma unroll

@@ -16,12 +16,19 @@ constexpr int TCM_APAD = 128;              // zero words before a (and after, to
 constexpr int TCM_AWORDS = TCM_APAD + TCM_MAXN + 256;
 constexpr uint32_t TILE = 128 * 128;       // one limb tile of H_d (bytes)
 constexpr uint32_t HBUF = 4 * TILE;        // four limb tiles
+// B operand: rows 64 v + j (limb v, block j < 32) of a 240-row region whose
+// preceding row is zero.  Even d: MMA N = 224 from the region's start; odd d:
+// N = 240 from one row earlier (descriptors may start at any 128-byte row: the
+// SWIZZLE_128B pattern follows absolute address bits, base_offset 0; measured
+// by tools/tc_i8_probe), i.e. every row one later -- the TMEM column offset
+// (which must be even) stays d & ~1.
 constexpr uint32_t BROWS_E = 224, BROWS_O = 240;
+constexpr uint32_t B_PRE = 1024;                         // keeps the region 1024-aligned
+constexpr uint32_t B_BYTES = B_PRE + BROWS_O * 128;
 // shared layout (bytes, from a 1024-aligned base)
 constexpr uint32_t OFF_H = 0;                            // 2 x HBUF
-constexpr uint32_t OFF_BE = OFF_H + 2 * HBUF;            // 224 rows
-constexpr uint32_t OFF_BO = OFF_BE + BROWS_E * 128;      // 240 rows
-constexpr uint32_t OFF_A = OFF_BO + BROWS_O * 128;       // u32 a, padded
+constexpr uint32_t OFF_B = OFF_H + 2 * HBUF;             // B_PRE | 240 rows
+constexpr uint32_t OFF_A = OFF_B + B_BYTES;              // u32 a, padded
 constexpr uint32_t SMEM_BYTES = OFF_A + TCM_AWORDS * 4 + 1024;
 
 

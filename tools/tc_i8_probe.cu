@@ -27,6 +27,8 @@ using namespace mmm_cu;
         }                                                                                  \
     } while (0)
 
+__device__ int g_shift = 0, g_bo = 0;
+
 template <int N>
 __global__ void __launch_bounds__(128) probe_kernel(const uint8_t* A, const uint8_t* B, int32_t* D,
                                                     int iters, int col_off) {
@@ -38,7 +40,10 @@ __global__ void __launch_bounds__(128) probe_kernel(const uint8_t* A, const uint
     __shared__ uint32_t tslot;
     const int tid = threadIdx.x, warp = tid >> 5;
     for (int i = tid; i < 128 * 128; i += 128) sA[tc::sw128(i >> 7, i & 127)] = A[i];
-    for (int i = tid; i < N * 128; i += 128) sB[tc::sw128(i >> 7, i & 127)] = B[i];
+    const int shift = g_shift;
+    for (int i = tid; i < (N + 8) * 128; i += 128) sB[i] = 0;
+    __syncthreads();
+    for (int i = tid; i < N * 128; i += 128) sB[tc::sw128((i >> 7) + shift, i & 127)] = B[i];
     tc::fence_async_smem();
     if (warp == 0) tc::tmem_alloc<512>(&tslot);
     if (tid == 0) {
@@ -55,7 +60,8 @@ __global__ void __launch_bounds__(128) probe_kernel(const uint8_t* A, const uint
         for (int it = 0; it < iters; ++it)
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-                tc::mma_u8(tbase + col_off, tc::desc_sw128(a0 + 32 * k), tc::desc_sw128(b0 + 32 * k), idesc,
+                tc::mma_u8(tbase + col_off, tc::desc_sw128(a0 + 32 * k),
+                           tc::desc_sw128(b0 + 128 * shift + 32 * k) | (uint64_t(g_bo & 7) << 49), idesc,
                            (it | k) != 0);
         tc::commit(&mbar);
     }
@@ -82,7 +88,7 @@ __global__ void __launch_bounds__(128) probe_kernel(const uint8_t* A, const uint
 
 template <int N>
 void run(int sms, int col_off = 0) {
-    const size_t smem = 1024 + 128 * 128 + N * 128;
+    const size_t smem = 1024 + 128 * 128 + (N + 8) * 128;
     CK(cudaFuncSetAttribute(probe_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     std::vector<uint8_t> A(128 * 128), B(N * 128);
     srand(7 + N);
@@ -140,6 +146,14 @@ void run(int sms, int col_off = 0) {
 int main(int argc, char** argv) {
     int sms = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+    if (argc > 2) {  // B operand starting `shift` rows into its swizzle atom, base_offset bo
+        int sh = atoi(argv[1]), bo = atoi(argv[2]);
+        CK(cudaMemcpyToSymbol(g_shift, &sh, sizeof(int)));
+        CK(cudaMemcpyToSymbol(g_bo, &bo, sizeof(int)));
+        printf("shift=%d bo=%d: ", sh, bo);
+        run<224>(sms, 2);
+        return 0;
+    }
     if (argc > 1) {  // one correctness case at a column offset
         run<224>(sms, atoi(argv[1]));
         return 0;
