@@ -171,7 +171,7 @@ __device__ long long tcd_stats[8];
 #define TCD_ACC(i) st[i] += clock64() - _t0
 
 template <bool FAN>
-__global__ void __launch_bounds__(TCD_T, 1) tcdiv_kernel(TcDivArgs g) {
+__global__ void __launch_bounds__(TCD_T + 32, 1) tcdiv_kernel(TcDivArgs g) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(TCD_T, 1) tcdiv_kernel(TcDivArgs g) {
     uint32_t* sE = sS + 128;
     uint32_t* part = sE + 128;                                    // [8][128] partial sums
     uint32_t* tmp = part + 1024;
-    __shared__ uint64_t mbar;
+    __shared__ uint64_t full[2], empty[2];
     __shared__ uint32_t tslot;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const FieldParams F = g.Fp;
@@ -194,205 +194,228 @@ __global__ void __launch_bounds__(TCD_T, 1) tcdiv_kernel(TcDivArgs g) {
     const int mB = (nb + 127) >> 7;
     const int Kq = (mu + 127) >> 7;  // quotient blocks; tiles d = 0 .. Kq
 
-    for (uint32_t i = tid; i < B_BYTES / 16; i += TCD_T)
+    for (uint32_t i = tid; i < B_BYTES / 16; i += TCD_T + 32)
         reinterpret_cast<uint4*>(sm + D_OFF_B)[i] = make_uint4(0, 0, 0, 0);
-    for (int i = tid; i < TCD_QWORDS; i += TCD_T) q_pad[i] = 0;
-    for (int i = tid; i < 128; i += TCD_T) hs[i - 128] = 0;
+    for (int i = tid; i < TCD_QWORDS; i += TCD_T + 32) q_pad[i] = 0;
+    for (int i = tid; i < 128; i += TCD_T + 32) hs[i - 128] = 0;
     if (warp == 0) tc::tmem_alloc<512>(&tslot);
     if (tid == 0) {
-        tc::mbar_init(&mbar, 1);
+        for (int b = 0; b < 2; ++b) {
+            tc::mbar_init(&full[b], 1);
+            tc::mbar_init(&empty[b], 1);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     tc::fence_before_sync();
     __syncthreads();
     tc::fence_after_sync();
     const uint32_t tbase = tslot;
-    uint32_t ph = 0;
-    constexpr uint32_t ID_E = tc::idesc_u8(128, BROWS_E), ID_O = tc::idesc_u8(128, BROWS_O);
-    const uint32_t lane_addr = tbase + (uint32_t(32 * (warp & 3)) << 16);
 
-    // tile K into the planes from H buffer K & 1 (one thread)
-    auto issue = [&](int K) {
-        const uint32_t hb = tc::smem_u32(sH + (K & 1) * HBUF);
-        const bool odd = K & 1;
-        const uint32_t bb = tc::smem_u32(sBE) - (odd ? 128u : 0u);
-        const uint32_t idesc = odd ? ID_O : ID_E;
-        const uint32_t col = uint32_t(K & ~1);
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-                tc::mma_u8(tbase + 64 * u + col, tc::desc_sw128(hb + u * TILE + 32 * k),
-                           tc::desc_sw128(bb + 32 * k), idesc, 1u);
-        tc::commit(&mbar);
-    };
-
-    long long st[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (int64_t inst = blockIdx.x; inst < g.count; inst += gridDim.x) {
-        const uint32_t* a = g.A + inst * g.lda;
-        const uint32_t* b = g.B + inst * g.ldb;
-        long long tp = clock64();
-        // ---- B' operand (rows 64 v + j), B'[0..256), zero TMEM, S_0 = 0 ----
-        for (int u = tid; u < mB * 8; u += TCD_T) {
-            const int j = u >> 3, c = u & 7;
-            uint32_t wv[16];
-#pragma unroll
-            for (int t = 0; t < 16; ++t) {
-                const int k = 128 * j + 16 * c + t;  // B' index
-                wv[t] = k < nb ? __ldg(b + (nb - 1 - k)) : 0u;
-            }
-            uint32_t L[4][4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-                limb_transpose(wv[4 * q], wv[4 * q + 1], wv[4 * q + 2], wv[4 * q + 3], L[0][q],
-                               L[1][q], L[2][q], L[3][q]);
-#pragma unroll
-            for (int v = 0; v < 4; ++v)
-                sts128(sBE, tc::sw128(64 * v + j, 16 * c), L[v][0], L[v][1], L[v][2], L[v][3]);
-        }
-        bp01[tid] = tid < nb ? __ldg(b + (nb - 1 - tid)) : 0u;
-        if (tid < 128) {
-            sS[tid] = 0;
-            qz[tid] = 0;  // Q block 0 (a previous instance's values)
-        }
-        // A' block 0 (rows r < 128)
-        uint32_t aK = (tid < 128 && tid < na) ? __ldg(a + (na - 1 - tid)) : 0u;
-        if (warp < 4) {
-#pragma unroll
-            for (int c0 = 0; c0 < 512; c0 += 32) tmem_st32_zero(lane_addr + c0);
-            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-        }
-        __syncthreads();
-        st[0] += clock64() - tp;
-        tp = clock64();
-        // ---- h = B'^-1 mod X^128 by Newton doubling ----
-        if (tid == 0) hs[0] = invmod(bp01[0], F);
-        __syncthreads();
-        for (int k = 1; k < 16; k <<= 1) {
-            // e[i] = sum_{m<k} B'[k+i-m] h[m]  (i < k): coefficients [k, 2k) of B' h_k
-            if (tid < k) {
-                Acc e;
-                for (int m = 0; m < k; ++m) e.add(bp01[k + tid - m], hs[m], F);
-                tmp[tid] = reduce(e.v, F);
-            }
-            __syncthreads();
-            if (tid < k) {  // h[k+i] = -sum_{m<=i} h[i-m] e[m]
-                Acc s;
-                for (int m = 0; m <= tid; ++m) s.add(hs[tid - m], tmp[m], F);
-                hs[k + tid] = negmod(reduce(s.v, F), F);
-            }
-            __syncthreads();
-        }
-        for (int k = 16; k < 128; k <<= 1) {  // the same doubling with sliding products
-            toeplitz_partials(bp01 + k, hs, k, k, part, F);
-            __syncthreads();
-            if (tid < k) tmp[tid] = partials_sum(part, k, k, tid, F);
-            __syncthreads();
-            toeplitz_partials(hs, tmp, k, k, part, F);  // h[i-m], zero for i < m
-            __syncthreads();
-            if (tid < k) hs[k + tid] = negmod(partials_sum(part, k, k, tid, F), F);
-            __syncthreads();
-        }
-        st[1] += clock64() - tp;
-
-        // Step K: Q_K from block K of A' - sum_{I<K} Q_I X^(128 I) B', where the
-        // planes hold tiles <= K-2 (read into sS before tile K-1 was issued)
-        // and the two tiles K-1 (against B'_1) and K (against B'_0) that Q
-        // blocks < K determine come from one 256-term product on the CUDA
-        // cores; tile K-1 runs on the tensor core meanwhile.
-        for (int K = 0; K < Kq; ++K) {
-            uint32_t* qk = qz + 128 * K;  // Q block K (zero here)
-            {
-                TCD_T0();
-                toeplitz_partials_256(qk, bp01, part, F);
-                __syncthreads();
-                if (tid < 128) {
-                    sE[tid] = submod(submod(aK, sS[tid], F), partials_sum(part, 128, 128, tid, F),
-                                     F);
-                    const int kn = 128 * (K + 1) + tid;  // prefetch A' block K+1
-                    aK = kn < na ? __ldg(a + (na - 1 - kn)) : 0u;
-                }
-                __syncthreads();
-                toeplitz_partials(hs, sE, 128, 128, part, F);  // Q_K = E h mod X^128
-                __syncthreads();
-                if (tid < 128) {
-                    const int k1 = 128 * K + tid;
-                    const uint32_t v1 = k1 < mu ? partials_sum(part, 128, 128, tid, F) : 0u;
-                    qk[tid] = v1;
-                    if (k1 < mu) fan_store<FAN>(g.Q, inst * g.ldq + (mu - 1 - k1), v1);
-                }
-                __syncthreads();
-                TCD_ACC(3);
-            }
-            {
-                TCD_T0();
-                build_h(sH + (K & 1) * HBUF, qz - TCM_APAD, K);  // tile K (Q_K, Q_{K-1})
-                tc::fence_async_smem();
-                TCD_ACC(4);
-            }
-            {
-                TCD_T0();
-                if (K >= 1) {  // tile K-1 done: the planes' block K+1 holds tiles <= K-1
-                    tc::mbar_wait(&mbar, ph);
-                    ph ^= 1;
-                }
+    if (warp == TCD_T / 32) {
+        // ---- MMA warp: tile K of each instance from buffer T & 1 ----
+        constexpr uint32_t ID_E = tc::idesc_u8(128, BROWS_E), ID_O = tc::idesc_u8(128, BROWS_O);
+        uint32_t fph[2] = {0, 0};
+        uint32_t T = 0;
+        for (int64_t inst = blockIdx.x; inst < g.count; inst += gridDim.x)
+            for (int K = 0; K <= Kq; ++K, ++T) {
+                const int b = T & 1;
+                tc::mbar_wait(&full[b], fph[b]);
+                fph[b] ^= 1;
                 tc::fence_after_sync();
-                if (warp < 4) {
+                if (lane == 0) {
+                    const uint32_t hb = tc::smem_u32(sH + b * HBUF);
+                    const bool odd = K & 1;
+                    const uint32_t bb = tc::smem_u32(sBE) - (odd ? 128u : 0u);
+                    const uint32_t idesc = odd ? ID_O : ID_E;
+                    const uint32_t col = uint32_t(K & ~1);
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+#pragma unroll
+                        for (int k = 0; k < 4; ++k)
+                            tc::mma_u8(tbase + 64 * u + col, tc::desc_sw128(hb + u * TILE + 32 * k),
+                                       tc::desc_sw128(bb + 32 * k), idesc, 1u);
+                    tc::commit(&empty[b]);
+                }
+                __syncwarp();
+            }
+    } else {
+        uint32_t eph[2] = {0, 0};
+        int pend[2] = {0, 0};
+        uint32_t T = 0;
+        auto free_buf = [&](int b) {
+            if (pend[b]) {
+                tc::mbar_wait(&empty[b], eph[b]);
+                eph[b] ^= 1;
+                --pend[b];
+            }
+        };
+        auto bar = [] { asm volatile("bar.sync 1, 256;" ::: "memory"); };
+        const uint32_t lane_addr = tbase + (uint32_t(32 * (warp & 3)) << 16);
+        long long st[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int64_t inst = blockIdx.x; inst < g.count; inst += gridDim.x) {
+            const uint32_t* a = g.A + inst * g.lda;
+            const uint32_t* b = g.B + inst * g.ldb;
+            long long tp = clock64();
+            // ---- B' operand (rows 64 v + j), B'[0..256), zero TMEM, S_0 = 0 ----
+            for (int u = tid; u < mB * 8; u += TCD_T) {
+                const int j = u >> 3, c = u & 7;
+                uint32_t wv[16];
+#pragma unroll
+                for (int t = 0; t < 16; ++t) {
+                    const int k = 128 * j + 16 * c + t;  // B' index
+                    wv[t] = k < nb ? __ldg(b + (nb - 1 - k)) : 0u;
+                }
+                uint32_t L[4][4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    limb_transpose(wv[4 * q], wv[4 * q + 1], wv[4 * q + 2], wv[4 * q + 3], L[0][q],
+                                   L[1][q], L[2][q], L[3][q]);
+#pragma unroll
+                for (int v = 0; v < 4; ++v)
+                    sts128(sBE, tc::sw128(64 * v + j, 16 * c), L[v][0], L[v][1], L[v][2], L[v][3]);
+            }
+            bp01[tid] = tid < nb ? __ldg(b + (nb - 1 - tid)) : 0u;
+            if (tid < 128) {
+                sS[tid] = 0;
+                qz[tid] = 0;  // Q block 0 (a previous instance's values)
+            }
+            uint32_t aK = (tid < 128 && tid < na) ? __ldg(a + (na - 1 - tid)) : 0u;  // A' block 0
+            if (warp < 4) {
+#pragma unroll
+                for (int c0 = 0; c0 < 512; c0 += 32) tmem_st32_zero(lane_addr + c0);
+                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            }
+            bar();
+            st[0] += clock64() - tp;
+            tp = clock64();
+            // ---- h = B'^-1 mod X^128 by Newton doubling ----
+            if (tid == 0) hs[0] = invmod(bp01[0], F);
+            bar();
+            for (int k = 1; k < 16; k <<= 1) {
+                // e[i] = sum_{m<k} B'[k+i-m] h[m]  (i < k): coefficients [k, 2k) of B' h_k
+                if (tid < k) {
+                    Acc e;
+                    for (int m = 0; m < k; ++m) e.add(bp01[k + tid - m], hs[m], F);
+                    tmp[tid] = reduce(e.v, F);
+                }
+                bar();
+                if (tid < k) {  // h[k+i] = -sum_{m<=i} h[i-m] e[m]
+                    Acc s;
+                    for (int m = 0; m <= tid; ++m) s.add(hs[tid - m], tmp[m], F);
+                    hs[k + tid] = negmod(reduce(s.v, F), F);
+                }
+                bar();
+            }
+            for (int k = 16; k < 128; k <<= 1) {  // the same doubling with sliding products
+                toeplitz_partials(bp01 + k, hs, k, k, part, F);
+                bar();
+                if (tid < k) tmp[tid] = partials_sum(part, k, k, tid, F);
+                bar();
+                toeplitz_partials(hs, tmp, k, k, part, F);  // h[i-m], zero for i < m
+                bar();
+                if (tid < k) hs[k + tid] = negmod(partials_sum(part, k, k, tid, F), F);
+                bar();
+            }
+            st[1] += clock64() - tp;
+
+            // Step K: Q_K from block K of A' - sum_{I<K} Q_I X^(128 I) B', where the
+            // planes hold tiles <= K-2 (read into sS before tile K-1 was handed
+            // off) and the tiles K-1 (against B'_1) and K (against B'_0) that Q
+            // blocks < K determine come from one 256-term product on the CUDA
+            // cores; the MMA warp runs tile K-1 meanwhile.
+            for (int K = 0; K < Kq; ++K, ++T) {
+                uint32_t* qk = qz + 128 * K;  // Q block K (zero here)
+                {
+                    TCD_T0();
+                    toeplitz_partials_256(qk, bp01, part, F);
+                    bar();
+                    if (tid < 128) {
+                        sE[tid] = submod(submod(aK, sS[tid], F),
+                                         partials_sum(part, 128, 128, tid, F), F);
+                        const int kn = 128 * (K + 1) + tid;  // prefetch A' block K+1
+                        aK = kn < na ? __ldg(a + (na - 1 - kn)) : 0u;
+                    }
+                    bar();
+                    toeplitz_partials(hs, sE, 128, 128, part, F);  // Q_K = E h mod X^128
+                    bar();
+                    if (tid < 128) {
+                        const int k1 = 128 * K + tid;
+                        const uint32_t v1 = k1 < mu ? partials_sum(part, 128, 128, tid, F) : 0u;
+                        qk[tid] = v1;
+                        if (k1 < mu) fan_store<FAN>(g.Q, inst * g.ldq + (mu - 1 - k1), v1);
+                    }
+                    bar();
+                    TCD_ACC(3);
+                }
+                {
+                    TCD_T0();
+                    free_buf(T & 1);
+                    build_h(sH + (T & 1) * HBUF, qz - TCM_APAD, K);  // tile K (Q_K, Q_{K-1})
+                    tc::fence_async_smem();
+                    TCD_ACC(4);
+                }
+                {
+                    TCD_T0();
+                    free_buf((T + 1) & 1);  // tile K-1 done: block K+1 holds tiles <= K-1
+                    tc::fence_after_sync();
+                    if (warp < 4) {
+                        uint32_t x[7];
+#pragma unroll
+                        for (int s = 0; s < 7; ++s) x[s] = tmem_ld1(lane_addr + 64 * s + K + 1);
+                        tc::tmem_ld_wait();
+                        sS[32 * warp + lane] = combine_planes(x, g.c_hi, F);
+                    } else {
+                        qk[tid] = 0;  // Q block K+1 (tid - 128 + 128)
+                    }
+                    tc::fence_before_sync();
+                    bar();
+                    if (tid == 0) tc::mbar_arrive(&full[T & 1]);
+                    ++pend[T & 1];
+                    TCD_ACC(2);
+                }
+            }
+            long long tq = clock64();
+            // ---- the last tile (Q_{Kq-1}'s upper triangle), then the remainder ----
+            free_buf(T & 1);
+            build_h(sH + (T & 1) * HBUF, qz - TCM_APAD, Kq);
+            tc::fence_async_smem();
+            tc::fence_before_sync();
+            bar();
+            if (tid == 0) tc::mbar_arrive(&full[T & 1]);
+            ++pend[T & 1];
+            ++T;
+            free_buf(0);
+            free_buf(1);
+            tc::fence_after_sync();
+            // r[na-1-k] = A'[k] - (Q B')[k], k in [mu, na)
+            {
+                const int r = 32 * (warp & 3) + lane;
+                const int cfirst = mu >> 7, clast = (na - 1) >> 7;
+                const int64_t rb = inst * g.ldr;
+                for (int c = cfirst + (warp >> 2); c <= clast; c += 2) {
                     uint32_t x[7];
 #pragma unroll
-                    for (int s = 0; s < 7; ++s) x[s] = tmem_ld1(lane_addr + 64 * s + K + 1);
+                    for (int s = 0; s < 7; ++s) x[s] = tmem_ld1(lane_addr + 64 * s + c);
                     tc::tmem_ld_wait();
-                    sS[32 * warp + lane] = combine_planes(x, g.c_hi, F);
-                } else {
-                    qk[tid] = 0;  // Q block K+1 (tid - 128 + 128)
-                }
-                tc::fence_before_sync();
-                __syncthreads();
-                tc::fence_after_sync();
-                TCD_ACC(2);
-            }
-            if (tid == 0) issue(K);
-        }
-        tp = clock64();
-        // ---- the last tile (Q_{Kq-1}'s upper triangle), then the remainder ----
-        build_h(sH + (Kq & 1) * HBUF, qz - TCM_APAD, Kq);
-        tc::fence_async_smem();
-        if (Kq >= 1) {  // every thread consumes tile Kq-1's phase (parity aliasing otherwise)
-            tc::mbar_wait(&mbar, ph);
-            ph ^= 1;
-        }
-        tc::fence_before_sync();
-        __syncthreads();
-        tc::fence_after_sync();
-        if (tid == 0) issue(Kq);
-        tc::mbar_wait(&mbar, ph);
-        ph ^= 1;
-        tc::fence_after_sync();
-        // r[na-1-k] = A'[k] - (Q B')[k], k in [mu, na)
-        {
-            const int r = 32 * (warp & 3) + lane;
-            const int cfirst = mu >> 7, clast = (na - 1) >> 7;
-            const int64_t rb = inst * g.ldr;
-            for (int c = cfirst + (warp >> 2); c <= clast; c += 2) {
-                uint32_t x[7];
-#pragma unroll
-                for (int s = 0; s < 7; ++s) x[s] = tmem_ld1(lane_addr + 64 * s + c);
-                tc::tmem_ld_wait();
-                const int k = 128 * c + r;
-                if (k >= mu && k < na) {
-                    const uint32_t S = combine_planes(x, g.c_hi, F);
-                    fan_store<FAN>(g.R, rb + (na - 1 - k), submod(__ldg(a + (na - 1 - k)), S, F));
+                    const int k = 128 * c + r;
+                    if (k >= mu && k < na) {
+                        const uint32_t S = combine_planes(x, g.c_hi, F);
+                        fan_store<FAN>(g.R, rb + (na - 1 - k),
+                                       submod(__ldg(a + (na - 1 - k)), S, F));
+                    }
                 }
             }
+            tc::fence_before_sync();
+            bar();  // TMEM read before the next instance zeroes it
+            tc::fence_after_sync();
+            st[5] += clock64() - tq;
         }
-        tc::fence_before_sync();
-        __syncthreads();  // TMEM read before the next instance zeroes it
-        tc::fence_after_sync();
-        st[5] += clock64() - tp;
+        if (blockIdx.x == 0 && tid == 0)
+            for (int i = 0; i < 8; ++i) tcd_stats[i] = st[i];
     }
-    if (blockIdx.x == 0 && tid == 0)
-        for (int i = 0; i < 8; ++i) tcd_stats[i] = st[i];
+    tc::fence_before_sync();
     __syncthreads();
+    tc::fence_after_sync();
     if (warp == 0) tc::tmem_free<512>(tbase);
 }
 
@@ -433,8 +456,8 @@ void launch_tcdiv_batched(const FieldParams& F, const uint32_t* A, int64_t lda, 
     MMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(D_SMEM_BYTES)));
     const int blocks = int(std::min<int64_t>(count, sm_count()));
-    kern<<<blocks, TCD_T, D_SMEM_BYTES, st>>>(g);
-    check_launch("tcdiv_kernel", dim3(blocks), dim3(TCD_T));
+    kern<<<blocks, TCD_T + 32, D_SMEM_BYTES, st>>>(g);
+    check_launch("tcdiv_kernel", dim3(blocks), dim3(TCD_T + 32));
     if (getenv("MMM_TC_STATS")) {
         long long h[8];
         MMM_CUDA(cudaMemcpyFromSymbolAsync(h, tcd_stats, sizeof(h), 0, cudaMemcpyDeviceToHost, st));

@@ -60,14 +60,14 @@ struct TcArgs {
 __device__ long long tcm_stats[8];
 
 template <bool FAN>
-__global__ void __launch_bounds__(TCM_T, 1) tcmul_kernel(TcArgs g) {
+__global__ void __launch_bounds__(TCM_T + 32, 1) tcmul_kernel(TcArgs g) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
     uint8_t* sH = sm + OFF_H;
     uint8_t* sBE = sm + OFF_B + B_PRE;
     uint32_t* a_pad = reinterpret_cast<uint32_t*>(sm + OFF_A);
-    __shared__ uint64_t mbar[2];  // H buffer b's MMAs done
+    __shared__ uint64_t full[2], empty[2];  // tile in buffer b built / its MMAs done
     __shared__ uint32_t tslot;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int na = g.na, nb = g.nb;
@@ -76,145 +76,154 @@ __global__ void __launch_bounds__(TCM_T, 1) tcmul_kernel(TcArgs g) {
     const int nf = na + nb - 1;
     const int nc = (nf + 127) >> 7;               // output blocks
 
-    // zero the B copies and the a pad once (data rows are rewritten per instance)
-    for (uint32_t i = tid; i < B_BYTES / 16; i += TCM_T)
+    // zero the B region and the a pad once (data rows are rewritten per instance)
+    for (uint32_t i = tid; i < B_BYTES / 16; i += TCM_T + 32)
         reinterpret_cast<uint4*>(sm + OFF_B)[i] = make_uint4(0, 0, 0, 0);
-    for (int i = tid; i < TCM_AWORDS; i += TCM_T) a_pad[i] = 0;
+    for (int i = tid; i < TCM_AWORDS; i += TCM_T + 32) a_pad[i] = 0;
     if (warp == 0) tc::tmem_alloc<512>(&tslot);
     if (tid == 0) {
-        tc::mbar_init(&mbar[0], 1);
-        tc::mbar_init(&mbar[1], 1);
+        for (int b = 0; b < 2; ++b) {
+            tc::mbar_init(&full[b], 1);
+            tc::mbar_init(&empty[b], 1);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     tc::fence_before_sync();
     __syncthreads();
     tc::fence_after_sync();
     const uint32_t tbase = tslot;
-    uint32_t ph[2] = {0, 0};
-    constexpr uint32_t ID_E = tc::idesc_u8(128, BROWS_E), ID_O = tc::idesc_u8(128, BROWS_O);
 
-    long long t_pro = 0, t_loop = 0, t_epi = 0, t_mmawait = 0, t0 = clock64(), t1;
-    for (int64_t inst = blockIdx.x; inst < g.count; inst += gridDim.x) {
-        t0 = clock64();
-        const uint32_t* a = g.A + inst * g.lda;
-        const uint32_t* b = g.B + inst * g.ldb;
-        // ---- stage a, build the B operand copies, zero the accumulator ----
-        for (int i = tid; i < na; i += TCM_T) a_pad[TCM_APAD + i] = __ldg(a + i);
-        // B rows: (v, j) -> E row 64 v + j, O row 64 v + j + 1; unit = (j, chunk c)
-        for (int u = tid; u < mB * 8; u += TCM_T) {
-            const int j = u >> 3, c = u & 7;
-            uint32_t wv[16];
+    if (warp == TCM_T / 32) {
+        // ---- MMA warp: tile after tile, buffer T & 1 (T counts tiles over instances) ----
+        constexpr uint32_t ID_E = tc::idesc_u8(128, BROWS_E), ID_O = tc::idesc_u8(128, BROWS_O);
+        uint32_t fph[2] = {0, 0};
+        uint32_t T = 0;
+        for (int64_t inst = blockIdx.x; inst < g.count; inst += gridDim.x)
+            for (int d = 0; d < D; ++d, ++T) {
+                const int b = T & 1;
+                tc::mbar_wait(&full[b], fph[b]);
+                fph[b] ^= 1;
+                tc::fence_after_sync();
+                if (lane == 0) {
+                    const uint32_t hb = tc::smem_u32(sH + b * HBUF);
+                    const bool odd = d & 1;
+                    const uint32_t bb = tc::smem_u32(sBE) - (odd ? 128u : 0u);
+                    const uint32_t idesc = odd ? ID_O : ID_E;
+                    const uint32_t col = uint32_t(d & ~1);
 #pragma unroll
-            for (int t = 0; t < 16; ++t) {
-                const int k = 128 * j + 16 * c + t;
-                wv[t] = k < nb ? __ldg(b + k) : 0u;
-            }
-            uint32_t L[4][4];
+                    for (int u = 0; u < 4; ++u)
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
-                limb_transpose(wv[4 * q], wv[4 * q + 1], wv[4 * q + 2], wv[4 * q + 3], L[0][q],
-                               L[1][q], L[2][q], L[3][q]);
-#pragma unroll
-            for (int v = 0; v < 4; ++v) {
-                sts128(sBE, tc::sw128(64 * v + j, 16 * c), L[v][0], L[v][1], L[v][2], L[v][3]);
-            }
-        }
-        if (warp < 4) {
-#pragma unroll
-            for (int c0 = 0; c0 < 512; c0 += 32) tmem_st32_zero(tbase + (uint32_t(warp * 32) << 16) + c0);
-            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-        }
-        __syncthreads();  // a staged
-        build_h(sH, a_pad, 0);
-        tc::fence_async_smem();
-        tc::fence_before_sync();
-        __syncthreads();
-        tc::fence_after_sync();
-        t1 = clock64();
-        t_pro += t1 - t0;
-        t0 = t1;
-
-        for (int d = 0; d < D; ++d) {
-            const int buf = d & 1;
-            if (tid == 0) {
-                const uint32_t hb = tc::smem_u32(sH + buf * HBUF);
-                const bool odd = d & 1;
-                const uint32_t bb = tc::smem_u32(sBE) - (odd ? 128u : 0u);
-                const uint32_t idesc = odd ? ID_O : ID_E;
-                const uint32_t col = uint32_t(d & ~1);
-#pragma unroll
-                for (int u = 0; u < 4; ++u)
-#pragma unroll
-                    for (int k = 0; k < 4; ++k)
-                        tc::mma_u8(tbase + 64 * u + col, tc::desc_sw128(hb + u * TILE + 32 * k),
-                                   tc::desc_sw128(bb + 32 * k), idesc, 1u);
-                tc::commit(&mbar[buf]);
-            }
-            if (d + 1 < D) {
-                if (d >= 1) {  // buffer (d+1)&1 was read by d-1's MMAs
-                    const long long tw = clock64();
-                    tc::mbar_wait(&mbar[buf ^ 1], ph[buf ^ 1]);
-                    ph[buf ^ 1] ^= 1;
-                    t_mmawait += clock64() - tw;
+                        for (int k = 0; k < 4; ++k)
+                            tc::mma_u8(tbase + 64 * u + col, tc::desc_sw128(hb + u * TILE + 32 * k),
+                                       tc::desc_sw128(bb + 32 * k), idesc, 1u);
+                    tc::commit(&empty[b]);
                 }
-                build_h(sH + (buf ^ 1) * HBUF, a_pad, d + 1);
+                __syncwarp();
+            }
+    } else {
+        // ---- 8 compute warps: operands in, tiles built, planes out ----
+        uint32_t eph[2] = {0, 0};
+        int pend[2] = {0, 0};  // handed-off tiles whose MMAs were not yet waited for
+        uint32_t T = 0;
+        auto free_buf = [&](int b) {
+            if (pend[b]) {
+                tc::mbar_wait(&empty[b], eph[b]);
+                eph[b] ^= 1;
+                --pend[b];
+            }
+        };
+        auto bar = [] { asm volatile("bar.sync 1, 256;" ::: "memory"); };
+        long long t_pro = 0, t_loop = 0, t_epi = 0, t_mmawait = 0, t0, t1;
+        for (int64_t inst = blockIdx.x; inst < g.count; inst += gridDim.x) {
+            t0 = clock64();
+            const uint32_t* a = g.A + inst * g.lda;
+            const uint32_t* b = g.B + inst * g.ldb;
+            for (int i = tid; i < na; i += TCM_T) a_pad[TCM_APAD + i] = __ldg(a + i);
+            // B rows 64 v + j; unit = (j, chunk c)
+            for (int u = tid; u < mB * 8; u += TCM_T) {
+                const int j = u >> 3, c = u & 7;
+                uint32_t wv[16];
+#pragma unroll
+                for (int t = 0; t < 16; ++t) {
+                    const int k = 128 * j + 16 * c + t;
+                    wv[t] = k < nb ? __ldg(b + k) : 0u;
+                }
+                uint32_t L[4][4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    limb_transpose(wv[4 * q], wv[4 * q + 1], wv[4 * q + 2], wv[4 * q + 3], L[0][q],
+                                   L[1][q], L[2][q], L[3][q]);
+#pragma unroll
+                for (int v = 0; v < 4; ++v)
+                    sts128(sBE, tc::sw128(64 * v + j, 16 * c), L[v][0], L[v][1], L[v][2], L[v][3]);
+            }
+            if (warp < 4) {
+#pragma unroll
+                for (int c0 = 0; c0 < 512; c0 += 32)
+                    tmem_st32_zero(tbase + (uint32_t(warp * 32) << 16) + c0);
+                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            }
+            bar();  // a staged
+            t1 = clock64();
+            t_pro += t1 - t0;
+            t0 = t1;
+            for (int d = 0; d < D; ++d, ++T) {
+                const int bb = T & 1;
+                const long long tw = clock64();
+                free_buf(bb);
+                t_mmawait += clock64() - tw;
+                build_h(sH + bb * HBUF, a_pad, d);
                 tc::fence_async_smem();
+                tc::fence_before_sync();
+                bar();
+                if (tid == 0) tc::mbar_arrive(&full[bb]);
+                ++pend[bb];
+            }
+            free_buf(0);  // every MMA of this instance is done
+            free_buf(1);
+            tc::fence_after_sync();
+            t1 = clock64();
+            t_loop += t1 - t0;
+            t0 = t1;
+            // ---- epilogue: warps w and w+4 share lanes 32 (w % 4) .. +31 ----
+            {
+                const int r = 32 * (warp & 3) + lane;
+                const int cbeg = (warp >> 2) * 32;
+                const uint32_t lane_addr = tbase + (uint32_t(32 * (warp & 3)) << 16);
+                const FieldParams& Fp = g.Fp;
+                const int64_t fb = inst * g.ldf;
+                for (int c0 = cbeg; c0 < cbeg + 32 && c0 < nc; c0 += 8) {
+                    uint32_t x[7][8];
+#pragma unroll
+                    for (int s = 0; s < 7; ++s) tmem_ld8(lane_addr + 64 * s + c0, x[s]);
+                    tc::tmem_ld_wait();
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        const int k = 128 * (c0 + e) + r;
+                        uint64_t v = uint64_t(x[0][e]) + (uint64_t(x[1][e]) << 8) +
+                                     (uint64_t(x[2][e]) << 16) + (uint64_t(x[3][e]) << 24);
+                        v += uint64_t(x[4][e]) * g.c_hi[0];
+                        v += uint64_t(x[5][e]) * g.c_hi[1];
+                        v += uint64_t(x[6][e]) * g.c_hi[2];
+                        if (k < nf) fan_store<FAN>(g.F, fb + k, reduce(v, Fp));
+                    }
+                }
             }
             tc::fence_before_sync();
-            __syncthreads();
+            bar();  // TMEM read before the next instance zeroes it
             tc::fence_after_sync();
+            t_epi += clock64() - t0;
         }
-        // drain: D-1's commit covers every MMA issued so far; D-2's commit (the
-        // other buffer, not waited in the loop) has completed too -- consume it
-        {
-            const int lb = (D - 1) & 1;
-            tc::mbar_wait(&mbar[lb], ph[lb]);
-            ph[lb] ^= 1;
-            if (D >= 2) {
-                tc::mbar_wait(&mbar[lb ^ 1], ph[lb ^ 1]);
-                ph[lb ^ 1] ^= 1;
-            }
+        if (blockIdx.x == 0 && tid == 0) {
+            tcm_stats[0] = t_pro;
+            tcm_stats[1] = t_loop;
+            tcm_stats[2] = t_epi;
+            tcm_stats[3] = t_mmawait;
         }
-        tc::fence_after_sync();
-        t1 = clock64();
-        t_loop += t1 - t0;
-        t0 = t1;
-        // ---- epilogue: warps w and w+4 share lanes 32 (w % 4) .. +31 ----
-        {
-            const int r = 32 * (warp & 3) + lane;
-            const int cbeg = (warp >> 2) * 32;
-            const uint32_t lane_addr = tbase + (uint32_t(32 * (warp & 3)) << 16);
-            const FieldParams& Fp = g.Fp;
-            const int64_t fb = inst * g.ldf;
-            for (int c0 = cbeg; c0 < cbeg + 32 && c0 < nc; c0 += 8) {
-                uint32_t x[7][8];
-#pragma unroll
-                for (int s = 0; s < 7; ++s) tmem_ld8(lane_addr + 64 * s + c0, x[s]);
-                tc::tmem_ld_wait();
-#pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    const int k = 128 * (c0 + e) + r;
-                    uint64_t v = uint64_t(x[0][e]) + (uint64_t(x[1][e]) << 8) +
-                                 (uint64_t(x[2][e]) << 16) + (uint64_t(x[3][e]) << 24);
-                    v += uint64_t(x[4][e]) * g.c_hi[0];
-                    v += uint64_t(x[5][e]) * g.c_hi[1];
-                    v += uint64_t(x[6][e]) * g.c_hi[2];
-                    if (k < nf) fan_store<FAN>(g.F, fb + k, reduce(v, Fp));
-                }
-            }
-        }
-        tc::fence_before_sync();
-        __syncthreads();  // TMEM read before the next instance zeroes it
-        tc::fence_after_sync();
-        t_epi += clock64() - t0;
     }
-    if (blockIdx.x == 0 && tid == 0) {
-        tcm_stats[0] = t_pro;
-        tcm_stats[1] = t_loop;
-        tcm_stats[2] = t_epi;
-        tcm_stats[3] = t_mmawait;
-    }
+    tc::fence_before_sync();
     __syncthreads();
+    tc::fence_after_sync();
     if (warp == 0) tc::tmem_free<512>(tbase);
 }
 
@@ -252,8 +261,8 @@ void launch_tcmul_batched(const FieldParams& F, const uint32_t* A, int64_t lda, 
     auto kern = Fo.n > 1 ? tcmul_kernel<true> : tcmul_kernel<false>;
     MMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES)));
     const int blocks = int(std::min<int64_t>(count, sm_count()));
-    kern<<<blocks, TCM_T, SMEM_BYTES, st>>>(g);
-    check_launch("tcmul_kernel", dim3(blocks), dim3(TCM_T));
+    kern<<<blocks, TCM_T + 32, SMEM_BYTES, st>>>(g);
+    check_launch("tcmul_kernel", dim3(blocks), dim3(TCM_T + 32));
     if (getenv("MMM_TC_STATS")) {
         long long h[8];
         MMM_CUDA(cudaMemcpyFromSymbolAsync(h, tcm_stats, sizeof(h), 0, cudaMemcpyDeviceToHost, st));
