@@ -225,6 +225,30 @@ def imad_line(macs, t, imad):
             "traffic": None}
 
 
+TC_PEAK = os.path.join(ROOT, "profiles", "tc_peak.json")
+
+
+def tensor_line(mod_macs, t, imad):
+    """Roofline entry for a tensor-core kernel doing `mod_macs` modular MACs
+    (16 u8 x u8 limb MACs each) in t s."""
+    try:
+        with open(TC_PEAK) as fh:
+            pk = json.load(fh)
+        peak, src = float(pk["u8_mac_per_s"]), pk["source"]
+    except (OSError, KeyError, ValueError):
+        peak, src = 2.25e15, "nominal (4.5 POPS dense int8)"
+    u8 = 16.0 * mod_macs
+    ach = u8 / t
+    return {"bound": "tensor", "achieved": ach / 1e12, "peak": peak / 1e12,
+            "unit": "T u8-MAC/s", "frac": ach / peak, "peak_source": src,
+            "peak_nominal": 2250.0, "frac_nominal": ach / 2.25e15,
+            "peak_nominal_source": "4.5 POPS dense int8 per B200 = 2.25e15 MAC/s",
+            "alg_u8_macs_per_launch": u8,
+            "modular_macs_per_s": mod_macs / t,
+            "vs_imad_wide_ceiling": (mod_macs / t) / (imad or 8.0647e12),
+            "traffic": None}
+
+
 def imad_rate():
     """Measured plain IMAD rate (profiles/peaks.json, tools/peaks.cu)."""
     try:
@@ -947,7 +971,7 @@ class BatchWork(_Sharded):
                                      if self.peer is not None else
                                      f"NCCL all-gather ({self.peer_note})")
 
-    def device_step(self, stream):
+    def _device_step(self, stream):
         k, n = self.hi - self.lo, self.n
         pe = getattr(self, "peer", None)
         if pe is not None:
@@ -955,7 +979,7 @@ class BatchWork(_Sharded):
             self.mmm.mul_batched_fanout_dev(P, self.dA.data_ptr(), n, n, self.dB.data_ptr(), n,
                                             n, k, pe.ptrs(0, lo * (2 * n - 1)), 2 * n - 1,
                                             s=self.s or 8, stream=stream)
-            self._mark("mul_kernel")
+            self._mark(self._mul_label)
             self.mmm.divmod_batched_fanout_dev(P, self.dC.data_ptr(), 2 * n, 2 * n,
                                                self.dD.data_ptr(), n, n, k,
                                                pe.ptrs(1, lo * (n + 1)), n + 1,
@@ -969,7 +993,7 @@ class BatchWork(_Sharded):
             return
         self.mmm.mul_batched_dev(P, self.dA.data_ptr(), n, n, self.dB.data_ptr(), n, n, k,
                                  self.dF.data_ptr(), 2 * n - 1, s=self.s or 8, stream=stream)
-        self._mark("mul_kernel")
+        self._mark(self._mul_label)
         self.mmm.divmod_batched_dev(P, self.dC.data_ptr(), 2 * n, 2 * n, self.dD.data_ptr(), n,
                                     n, k, self.dQ.data_ptr(), n + 1, self.dR.data_ptr(), n - 1,
                                     s=self.s or 64, stream=stream)
@@ -1017,27 +1041,44 @@ class BatchWork(_Sharded):
         if self.world == 1:
             assert self._digests(*out) == self.want
 
-    last_part = "div_cta_kernel"
+    def _kernels(self):
+        """Which kernels the dispatcher runs for cfg5 (csrc/mul.cu, divmod.cu):
+        the tensor-core ones unless MMM_MUL_TC / MMM_DIV_TC = 0."""
+        tm = os.environ.get("MMM_MUL_TC", "1") != "0"
+        td = os.environ.get("MMM_DIV_TC", "1") != "0"
+        return ("tcmul_kernel" if tm else "mul_kernel"), ("tcdiv_kernel" if td else "div_cta_kernel")
+
+    @property
+    def last_part(self):
+        return self._kernels()[1]
+
+    def device_step(self, stream):
+        self._mul_label = self._kernels()[0]
+        self._device_step(stream)
 
     def roofline(self, t_step, hbm, imad, parts=None):
         """Per kernel (CUDA events between the two launches of each step):
         algorithmic modular MACs of this rank's share (mul: n^2 per product;
-        div: (n+1) n per division, SURVEY §8d) over the kernel's mean time;
-        the dominant kernel is the headline.  With a gather, it rides in the
-        division's segment (the barrier after it)."""
+        div: (n+1) n per division) over the kernel's mean time.
+        Tensor-core kernels are measured in u8 MACs -- 16 limb products per
+        modular MAC -- against the measured kind::i8 UMMA rate; the modular
+        rate is also given against the IMAD.WIDE ceiling of the CUDA-core
+        kernels.  The dominant kernel is the headline.  With a gather, it
+        rides in the division's segment (the barrier after it)."""
         k, n = self.hi - self.lo, self.n
-        work = {"mul_kernel": float(k) * n * n, "div_cta_kernel": float(k) * (n + 1) * n}
-        parts = parts or {"mul_kernel+div_cta_kernel": t_step}
-        if "mul_kernel+div_cta_kernel" in parts:
-            work = {"mul_kernel+div_cta_kernel": sum(work.values())}
+        km, kd = self._kernels()
+        work = {km: float(k) * n * n, kd: float(k) * (n + 1) * n}
+        parts = parts or {km + "+" + kd: t_step}
+        if km + "+" + kd in parts:
+            work = {km + "+" + kd: sum(work.values())}
         out = {}
         for name, t in parts.items():
-            out[name] = imad_line(work[name], t, imad)
+            out[name] = (tensor_line(work[name], t, imad) if name.startswith("tc")
+                         else imad_line(work[name], t, imad))
             out[name]["ms"] = t * 1e3
         dom = max(parts, key=lambda x: parts[x])
         r = dict(out[dom])
-        r.update(kernel=dom, parts=out, alg_macs_per_launch=work[dom],
-                 alg_unit="modular MACs (one IMAD.WIDE.U32 each)")
+        r.update(kernel=dom, parts=out, alg_modular_macs_per_launch=work[dom])
         return r
 
     def cpu_ref(self, orc):

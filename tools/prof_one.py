@@ -25,7 +25,8 @@ def main():
     torch.cuda.set_device(0)
     import paper_1402_0264_b200 as mmm
     mmm.load()
-    w = bench.WORKLOADS[args.workload](args.s)
+    w = bench.WORKLOADS[args.workload](args.s, bench.OursGen(42))
+    w.attach(mmm)
     if getattr(w, "sharded", False):
         w.bind(bench.Dist("ours"))
     w.device_setup()

@@ -47,7 +47,7 @@ def time_ms(w, reps):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r1_s_sweep.csv"))
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r2_s_sweep.csv"))
     ap.add_argument("--reps", type=int, default=5)
     args = ap.parse_args()
     import torch
@@ -58,7 +58,9 @@ def main():
     def sweep(app, variant, name, svals, model, steps):
         got = []
         for s in svals:
-            w = bench.WORKLOADS[name](s)
+            import paper_1402_0264_b200 as mmm
+            w = bench.WORKLOADS[name](s, bench.OursGen(42))
+            w.attach(mmm)
             w.device_setup()
             ms = time_ms(w, args.reps)
             n, m, t = model(w, s)
