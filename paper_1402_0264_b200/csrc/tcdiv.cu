@@ -336,6 +336,8 @@ __global__ void __launch_bounds__(TCD_T + 32, 1) tcdiv_kernel(TcDivArgs g) {
                         aK = kn < na ? __ldg(a + (na - 1 - kn)) : 0u;
                     }
                     bar();
+                    TCD_ACC(3);
+                    const long long _t1 = clock64();
                     toeplitz_partials(hs, sE, 128, 128, part, F);  // Q_K = E h mod X^128
                     bar();
                     if (tid < 128) {
@@ -345,7 +347,7 @@ __global__ void __launch_bounds__(TCD_T + 32, 1) tcdiv_kernel(TcDivArgs g) {
                         if (k1 < mu) fan_store<FAN>(g.Q, inst * g.ldq + (mu - 1 - k1), v1);
                     }
                     bar();
-                    TCD_ACC(3);
+                    st[6] += clock64() - _t1;
                 }
                 {
                     TCD_T0();
@@ -463,7 +465,7 @@ void launch_tcdiv_batched(const FieldParams& F, const uint32_t* A, int64_t lda, 
         MMM_CUDA(cudaMemcpyFromSymbolAsync(h, tcd_stats, sizeof(h), 0, cudaMemcpyDeviceToHost, st));
         MMM_CUDA(cudaStreamSynchronize(st));
         fprintf(stderr, "tcdiv stats (CTA 0, thread 0): prologue=%lld newton=%lld wait+read=%lld "
-                "head_solve=%lld build=%lld tail=%lld cycles\n", h[0], h[1], h[2], h[3], h[4], h[5]);
+                "corr+E=%lld build=%lld tail=%lld Qsolve=%lld cycles\n", h[0], h[1], h[2], h[3], h[4], h[5], h[6]);
     }
 }
 

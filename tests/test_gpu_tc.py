@@ -129,3 +129,29 @@ def test_tc_division_equals_cta_kernel(cuda_lib, monkeypatch):
         monkeypatch.setenv("MMM_DIV_TC", tc)
         outs.append(mmm.divmod_batched(A, B, P))
     assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+
+
+def test_tc_division_fanout(cuda_lib, port, monkeypatch):
+    """The tensor-core division's fan-out epilogue (q and r into every pointer
+    of a set, as the sharded cfg5 gather uses it)."""
+    import torch
+    mmm = cuda_lib
+    monkeypatch.setenv("MMM_DIV_TC", "1")
+    rng = np.random.default_rng(12)
+    cnt, na, nb = 5, 3000, 1300
+    A = rng.integers(0, P, (cnt, na)).astype(np.uint32)
+    B = rng.integers(1, P, (cnt, nb)).astype(np.uint32)
+    dA = torch.from_numpy(A.view(np.int32)).cuda()
+    dB = torch.from_numpy(B.view(np.int32)).cuda()
+    lq, lr = na - nb + 1, nb - 1
+    qs = [torch.zeros((cnt, lq), dtype=torch.int32, device="cuda") for _ in range(3)]
+    rs = [torch.zeros((cnt, lr), dtype=torch.int32, device="cuda") for _ in range(3)]
+    mmm.divmod_batched_fanout_dev(P, dA.data_ptr(), na, na, dB.data_ptr(), nb, nb, cnt,
+                                  [q.data_ptr() for q in qs], lq, [r.data_ptr() for r in rs], lr,
+                                  stream=torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    for i in range(cnt):
+        wq, wr = port.divmod(A[i], B[i], P)
+        for q, r in zip(qs, rs):
+            assert np.array_equal(np.trim_zeros(q[i].cpu().numpy().view(np.uint32).astype(np.int64), "b"), wq)
+            assert np.array_equal(np.trim_zeros(r[i].cpu().numpy().view(np.uint32).astype(np.int64), "b"), wr)
