@@ -533,7 +533,7 @@ class MulWork(Workload):
     sharded = True
 
     def __init__(self, s, gen):
-        self.s = s or 4  # s = 4: fastest in the sweep (PAPER.md:1781 too)
+        self.s = s  # 0 = auto (the tensor core); s >= 1: the s x s-tile CUDA-core kernel
         c = suites.cfg1(gen)
         self.a, self.b = c["a"], c["b"]
         self.want = golden()["cfg1"]["f"]
@@ -541,7 +541,8 @@ class MulWork(Workload):
         self.world, self.dist = 1, None
         self.ranges = [(0, self.nf)]
         self.k0, self.k1, self.L = 0, self.nf, self.nf
-        self.config = {"workload": "cfg1_mul_2^14x2^14_p469762049", "p": P, "s": self.s,
+        self.config = {"workload": "cfg1_mul_2^14x2^14_p469762049", "p": P,
+                       "s": self.s or "auto (tensor core)",
                        "seed": 42, "parallelism": "single GPU",
                        "l2": "flushed between timed steps (256 MB written then read: clean lines; inputs < L2)"}
 
@@ -620,9 +621,14 @@ class MulWork(Workload):
     def roofline(self, t_step, hbm, imad, parts=None):
         from paper_1402_0264_b200.shard import range_work
         macs = float(range_work(len(self.a), len(self.b), self.k0, self.k1))  # this rank
+        full = (self.k0, self.k1) == (0, self.nf)
+        if not self.s and full and os.environ.get("MMM_MUL_TC", "1") != "0":
+            r = tensor_line(macs, t_step, imad)  # csrc/tcmul.cu: tcmul_split_kernel
+            r.update(kernel="tcmul_split_kernel", alg_modular_macs_per_launch=macs)
+            return r
         r = imad_line(macs, t_step, imad)
         r.update(kernel="mul_kernel", alg_macs_per_launch=macs,
-                 note="integer pipe: one IMAD.WIDE.U32 per modular MAD; no tensor cores")
+                 note="integer pipe: one IMAD.WIDE.U32 per modular MAD")
         return r
 
     def cpu_ref(self, orc):
@@ -945,7 +951,7 @@ class BatchWork(_Sharded):
         self.want = (gold["f_all"], gold["qr_all"])
         self.n = self.A.shape[1]
         self.config = {"workload": "cfg5_4096x(4096x4096 mul)+4096x(8192/4096 div)_p469762049",
-                       "p": P, "seed": 42, "s_mul": self.s or 8, "s_div": self.s or 64,
+                       "p": P, "seed": 42, "s": self.s or "auto (tensor core)",
                        "parallelism": "instances sharded across ranks; results gathered to "
                        "every rank (config.gather)", "l2": "inputs 335 MB > L2"}
 
@@ -978,13 +984,13 @@ class BatchWork(_Sharded):
             lo = self.lo
             self.mmm.mul_batched_fanout_dev(P, self.dA.data_ptr(), n, n, self.dB.data_ptr(), n,
                                             n, k, pe.ptrs(0, lo * (2 * n - 1)), 2 * n - 1,
-                                            s=self.s or 8, stream=stream)
+                                            s=self.s, stream=stream)
             self._mark(self._mul_label)
             self.mmm.divmod_batched_fanout_dev(P, self.dC.data_ptr(), 2 * n, 2 * n,
                                                self.dD.data_ptr(), n, n, k,
                                                pe.ptrs(1, lo * (n + 1)), n + 1,
                                                pe.ptrs(2, lo * (n - 1)), n - 1,
-                                               s=self.s or 64, stream=stream)
+                                               s=self.s, stream=stream)
             pe.barrier()
             c = self.count
             self.fullF = pe.view(0, (c, 2 * n - 1))
@@ -992,11 +998,11 @@ class BatchWork(_Sharded):
             self.fullR = pe.view(2, (c, n - 1))
             return
         self.mmm.mul_batched_dev(P, self.dA.data_ptr(), n, n, self.dB.data_ptr(), n, n, k,
-                                 self.dF.data_ptr(), 2 * n - 1, s=self.s or 8, stream=stream)
+                                 self.dF.data_ptr(), 2 * n - 1, s=self.s, stream=stream)
         self._mark(self._mul_label)
         self.mmm.divmod_batched_dev(P, self.dC.data_ptr(), 2 * n, 2 * n, self.dD.data_ptr(), n,
                                     n, k, self.dQ.data_ptr(), n + 1, self.dR.data_ptr(), n - 1,
-                                    s=self.s or 64, stream=stream)
+                                    s=self.s, stream=stream)
         self.fullF = self._gather(self.dF)
         self.fullQ = self._gather(self.dQ)
         self.fullR = self._gather(self.dR)
@@ -1027,14 +1033,14 @@ class BatchWork(_Sharded):
         self.bytes_out = 4 * k * ((2 * n - 1) + (n + 1) + (n - 1))
 
     def host_step(self):
-        F = self.mmm.mul_batched(self.hA, self.hB, P, s=self.s or 8, out=self.hF)
-        Q, R = self.mmm.divmod_batched(self.hC, self.hD, P, s=self.s or 64, q_out=self.hQ,
+        F = self.mmm.mul_batched(self.hA, self.hB, P, s=self.s, out=self.hF)
+        Q, R = self.mmm.divmod_batched(self.hC, self.hD, P, s=self.s, q_out=self.hQ,
                                        r_out=self.hR)
         return F, Q, R
 
     def host_step_default(self):
-        F = self.mmm.mul_batched(self.hA, self.hB, P, s=self.s or 8)
-        Q, R = self.mmm.divmod_batched(self.hC, self.hD, P, s=self.s or 64)
+        F = self.mmm.mul_batched(self.hA, self.hB, P, s=self.s)
+        Q, R = self.mmm.divmod_batched(self.hC, self.hD, P, s=self.s)
         return F, Q, R
 
     def host_check(self, out):
@@ -1044,8 +1050,8 @@ class BatchWork(_Sharded):
     def _kernels(self):
         """Which kernels the dispatcher runs for cfg5 (csrc/mul.cu, divmod.cu):
         the tensor-core ones unless MMM_MUL_TC / MMM_DIV_TC = 0."""
-        tm = os.environ.get("MMM_MUL_TC", "1") != "0"
-        td = os.environ.get("MMM_DIV_TC", "1") != "0"
+        tm = os.environ.get("MMM_MUL_TC", "1" if not self.s else "0") != "0"
+        td = os.environ.get("MMM_DIV_TC", "1" if not self.s else "0") != "0"
         return ("tcmul_kernel" if tm else "mul_kernel"), ("tcdiv_kernel" if td else "div_cta_kernel")
 
     @property

@@ -92,8 +92,9 @@ uint64_t mmm_rng_next(mmm_rng* g);
 int mmm_random_poly(mmm_rng* g, int64_t terms, int64_t p, uint32_t* out);
 
 /* ---- host-buffer entry points (synchronous, trimmed results) ------------ */
-/* f = a*b; f_cap >= na+nb-1.  s = per-thread register tile (the paper's
- * program parameter s), l = threads-per-block hint (ignored on B200). */
+/* f = a*b; f_cap >= na+nb-1.  s >= 1: the paper's program parameter (per-thread
+ * register tile of the CUDA-core kernel); s <= 0: auto (large products run on
+ * the integer tensor core).  l = threads-per-block hint (ignored on B200). */
 int mmm_cu_mul(int64_t p, const uint32_t* a, int64_t na, const uint32_t* b, int64_t nb, int64_t s,
                int64_t l, uint32_t* f, int64_t f_cap, int64_t* nf);
 /* (q, r) = divmod(a, b); q_cap >= na-nb+1, r_cap >= nb-1 (when na >= nb),
@@ -116,7 +117,10 @@ int mmm_cu_ntt_mul(int64_t p, const uint32_t* a, int64_t na, const uint32_t* b, 
                    uint32_t* f, int64_t f_cap, int64_t* nf);
 
 /* ---- batched host entry points: `count` equal-shape instances, row-major
- *      with leading dimensions; outputs untrimmed (fixed lengths). -------- */
+ *      with leading dimensions; outputs untrimmed (fixed lengths).  s <= 0 =
+ *      auto: products of <= 4096-term operands and divisions of <= 8192 by
+ *      <= 4096 terms run on the integer tensor core when the batch is large;
+ *      s >= 1 selects the s-parameterised CUDA-core kernels. -------------- */
 int mmm_cu_mul_batched(int64_t p, const uint32_t* A, int64_t lda, int64_t na, const uint32_t* B,
                        int64_t ldb, int64_t nb, int64_t count, int64_t s, uint32_t* F, int64_t ldf);
 /* every B row must have a nonzero word at index nb-1; na >= nb.

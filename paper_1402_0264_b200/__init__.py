@@ -7,11 +7,16 @@ reference's oracle-style entry points (proj/include/mmm/oracle.hpp) and its
 blocked kernel programs (run_multiplication / run_division / run_gcd), with
 the same argument meaning and error behaviour:
 
-    mul(a, b, p, s=8)            == oracle_mul        (oracle.cpp:8-15)
+    mul(a, b, p, s=0)            == oracle_mul        (oracle.cpp:8-15)
     divmod(a, b, p, s=64)        == oracle_divmod     (oracle.cpp:51-67)
     gcd(a, b, p, s=64)           == oracle_gcd        (oracle.cpp:69-78)
     ntt_mul(a, b, p)             == oracle_mul        (product uniqueness)
     Field(p), random_poly(rng, terms, F)              (field.cpp, poly.cpp)
+
+The program parameter s: s >= 1 runs the paper's s-parameterised CUDA-core
+kernel (register tile / heads per step / steps per matrix batch); s = 0 (the
+default for products and batched divisions) lets the library pick, which for
+large products and cfg5-sized batches is the integer tensor core.
 
 Polynomials are 1-D numpy arrays of canonical residues, ascending, trimmed
 (the zero polynomial is an empty array).  Errors raise ``InvalidArgument``
@@ -267,7 +272,7 @@ def _pint(p) -> int:
 
 
 # ------------------------------------------------------------- host API ---
-def mul(a, b, p, s: int = 8, l: int = 128, out=None) -> np.ndarray:
+def mul(a, b, p, s: int = 0, l: int = 128, out=None) -> np.ndarray:
     a, b, p = _u32(a), _u32(b), _pint(p)
     f = _out(out, (max(a.size + b.size - 1, 1),))
     n = C.c_int64(0)
@@ -329,7 +334,7 @@ def ntt_mul(a, b, p, out=None) -> np.ndarray:
     return f[: n.value] if out is not None else f[: n.value].copy()
 
 
-def mul_batched(A, B, p, s: int = 8, out=None) -> np.ndarray:
+def mul_batched(A, B, p, s: int = 0, out=None) -> np.ndarray:
     A, B, p = _u32(A), _u32(B), _pint(p)
     cnt, na = A.shape
     nb = B.shape[1]
@@ -338,7 +343,7 @@ def mul_batched(A, B, p, s: int = 8, out=None) -> np.ndarray:
     return F
 
 
-def divmod_batched(A, B, p, s: int = 64, q_out=None, r_out=None):
+def divmod_batched(A, B, p, s: int = 0, q_out=None, r_out=None):
     A, B, p = _u32(A), _u32(B), _pint(p)
     cnt, na = A.shape
     nb = B.shape[1]
@@ -362,11 +367,11 @@ def ntt_mul_batched(A, B, p, out=None) -> np.ndarray:
 # -------------------------------------------- device-pointer API (async) --
 # Pointers are integers (e.g. torch.Tensor.data_ptr()), stream a
 # cudaStream_t as int (torch.cuda.Stream.cuda_stream) or 0.
-def mul_dev(p, d_a, na, d_b, nb, d_f, s=8, stream=0):
+def mul_dev(p, d_a, na, d_b, nb, d_f, s=0, stream=0):
     _check(load().mmm_cu_mul_dev(_pint(p), d_a, na, d_b, nb, s, d_f, stream))
 
 
-def mul_range_dev(p, d_a, na, d_b, nb, k0, k1, d_f, s=8, stream=0):
+def mul_range_dev(p, d_a, na, d_b, nb, k0, k1, d_f, s=0, stream=0):
     """Product coefficients [k0, k1) into d_f[0, k1 - k0) (a rank's output slice)."""
     _check(load().mmm_cu_mul_range_dev(_pint(p), d_a, na, d_b, nb, k0, k1, s, d_f, stream))
 
@@ -383,12 +388,12 @@ def ntt_mul_dev(p, d_a, na, d_b, nb, d_f, stream=0):
     _check(load().mmm_cu_ntt_mul_dev(_pint(p), d_a, na, d_b, nb, d_f, stream))
 
 
-def mul_batched_dev(p, d_A, lda, na, d_B, ldb, nb, count, d_F, ldf, s=8, stream=0):
+def mul_batched_dev(p, d_A, lda, na, d_B, ldb, nb, count, d_F, ldf, s=0, stream=0):
     _check(load().mmm_cu_mul_batched_dev(_pint(p), d_A, lda, na, d_B, ldb, nb, count, s, d_F,
                                          ldf, stream))
 
 
-def divmod_batched_dev(p, d_A, lda, na, d_B, ldb, nb, count, d_Q, ldq, d_R, ldr, s=64,
+def divmod_batched_dev(p, d_A, lda, na, d_B, ldb, nb, count, d_Q, ldq, d_R, ldr, s=0,
                        stream=0):
     _check(load().mmm_cu_divmod_batched_dev(_pint(p), d_A, lda, na, d_B, ldb, nb, count, s, d_Q,
                                             ldq, d_R, ldr, stream))
@@ -414,14 +419,14 @@ def mul_range_fanout_dev(p, d_a, na, d_b, nb, k0, k1, outs, s=8, stream=0):
                                               stream))
 
 
-def mul_batched_fanout_dev(p, d_A, lda, na, d_B, ldb, nb, count, outs, ldf, s=8, stream=0):
+def mul_batched_fanout_dev(p, d_A, lda, na, d_B, ldb, nb, count, outs, ldf, s=0, stream=0):
     arr, n = _ptrs(outs)
     _check(load().mmm_cu_mul_batched_fanout_dev(_pint(p), d_A, lda, na, d_B, ldb, nb, count, s,
                                                 arr, n, ldf, stream))
 
 
 def divmod_batched_fanout_dev(p, d_A, lda, na, d_B, ldb, nb, count, q_outs, ldq, r_outs, ldr,
-                              s=64, stream=0):
+                              s=0, stream=0):
     if len(q_outs) != len(r_outs):
         raise InvalidArgument("division batch: q and r fan-outs differ in length")
     qa, n = _ptrs(q_outs)
@@ -444,7 +449,7 @@ def _devs(devices):
     return d.ctypes.data_as(_I32P), d.size, d
 
 
-def mul_batched_multi(A, B, p, devices, s: int = 8, out=None) -> np.ndarray:
+def mul_batched_multi(A, B, p, devices, s: int = 0, out=None) -> np.ndarray:
     A, B, p = _u32(A), _u32(B), _pint(p)
     cnt, na = A.shape
     nb = B.shape[1]
@@ -455,7 +460,7 @@ def mul_batched_multi(A, B, p, devices, s: int = 8, out=None) -> np.ndarray:
     return F
 
 
-def divmod_batched_multi(A, B, p, devices, s: int = 64):
+def divmod_batched_multi(A, B, p, devices, s: int = 0):
     A, B, p = _u32(A), _u32(B), _pint(p)
     cnt, na = A.shape
     nb = B.shape[1]
@@ -478,7 +483,7 @@ def ntt_mul_batched_multi(A, B, p, devices, out=None) -> np.ndarray:
     return F
 
 
-def mul_batched_multi_dev(p, d_A, lda, na, d_B, ldb, nb, count, d_F, ldf, devices, s=8,
+def mul_batched_multi_dev(p, d_A, lda, na, d_B, ldb, nb, count, d_F, ldf, devices, s=0,
                           stream=0):
     dp, nd, _keep = _devs(devices)
     _check(load().mmm_cu_mul_batched_multi_dev(_pint(p), d_A, lda, na, d_B, ldb, nb, count, s,
@@ -486,7 +491,7 @@ def mul_batched_multi_dev(p, d_A, lda, na, d_B, ldb, nb, count, d_F, ldf, device
 
 
 def divmod_batched_multi_dev(p, d_A, lda, na, d_B, ldb, nb, count, d_Q, ldq, d_R, ldr, devices,
-                             s=64, stream=0):
+                             s=0, stream=0):
     dp, nd, _keep = _devs(devices)
     _check(load().mmm_cu_divmod_batched_multi_dev(_pint(p), d_A, lda, na, d_B, ldb, nb, count, s,
                                                   d_Q, ldq, d_R, ldr, dp, nd, stream))

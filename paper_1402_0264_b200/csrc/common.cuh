@@ -198,12 +198,18 @@ void launch_mul_batched(const FieldParams& F, const uint32_t* A, int64_t lda, in
                         const uint32_t* B, int64_t ldb, int64_t nb, int64_t count, uint32_t* Fo,
                         int64_t ldf, int64_t s, cudaStream_t st);
 // tensor-core batched product (tcmul.cu): na, nb <= 4096, exact like launch_mul_batched.
-bool tcmul_supported(int64_t na, int64_t nb, int64_t count);
+// s <= 0 = auto (tensor core where it pays); s >= 1 = the s-parameterised CUDA-core kernel
+bool tc_route(const char* env, int64_t s, bool shape_ok, bool worth);
+bool tcmul_supported(int64_t na, int64_t nb, int64_t count, int64_t s);
 void launch_tcmul_batched(const FieldParams& F, const uint32_t* A, int64_t lda, int64_t na,
                           const uint32_t* B, int64_t ldb, int64_t nb, int64_t count, Fan Fo,
                           int64_t ldf, cudaStream_t st);
+// one large product on the tensor core, split over the SMs (tcmul.cu)
+bool tcmul_single_supported(int64_t na, int64_t nb, int64_t s);
+void launch_tcmul_single(const FieldParams& F, const uint32_t* a, int64_t na, const uint32_t* b,
+                         int64_t nb, Fan Fo, cudaStream_t st);
 // tensor-core batched division (tcdiv.cu): 2 <= nb <= 4096, nb <= na <= 8192.
-bool tcdiv_supported(int64_t na, int64_t nb, int64_t count);
+bool tcdiv_supported(int64_t na, int64_t nb, int64_t count, int64_t s);
 void launch_tcdiv_batched(const FieldParams& F, const uint32_t* A, int64_t lda, int64_t na,
                           const uint32_t* B, int64_t ldb, int64_t nb, int64_t count, Fan Q,
                           int64_t ldq, Fan R, int64_t ldr, cudaStream_t st);

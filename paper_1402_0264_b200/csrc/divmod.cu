@@ -991,6 +991,11 @@ void launch_divmod_batched(const FieldParams& F, const uint32_t* A, int64_t lda,
 void launch_divmod_batched_fan(const FieldParams& F, const uint32_t* A, int64_t lda, int64_t na,
                                const uint32_t* B, int64_t ldb, int64_t nb, int64_t count, Fan Q,
                                int64_t ldq, Fan Rr, int64_t ldr, int64_t s, cudaStream_t st) {
+    if (nb >= 2 && tcdiv_supported(na, nb, count, s)) {  // 128 heads per step on the tensor core
+        launch_tcdiv_batched(F, A, lda, na, B, ldb, nb, count, Q, ldq, Rr, ldr, st);
+        return;
+    }
+    if (s <= 0) s = 64;  // auto on the CUDA cores
     if (s < 1) throw Error(ST_INVALID, "division: block parameter must be >= 1");
     const int64_t mu = na - nb + 1;
     DivArgs g{};
@@ -1011,10 +1016,6 @@ void launch_divmod_batched_fan(const FieldParams& F, const uint32_t* A, int64_t 
     const int borg = ((Spad + 3) & ~3) + 3;
     if (nb == 1) {
         run_const(F, A, lda, na, B, ldb, count, Q, ldq, st);
-        return;
-    }
-    if (tcdiv_supported(na, nb, count)) {  // 128 heads per step on the tensor core (tcdiv.cu)
-        launch_tcdiv_batched(F, A, lda, na, B, ldb, nb, count, Q, ldq, Rr, ldr, st);
         return;
     }
     if (cta_smem_words(na, nb, g.S, R, borg) * 4 > 200 * 1024) {

@@ -229,6 +229,11 @@ void launch_mul_range(const FieldParams& F, const uint32_t* a, int64_t na, const
 void launch_mul_range_fan(const FieldParams& F, const uint32_t* a, int64_t na, const uint32_t* b,
                           int64_t nb, int64_t klo, int64_t khi, Fan f, int64_t s, int64_t /*l*/,
                           cudaStream_t st) {
+    if (klo == 0 && khi == na + nb - 1 && tcmul_single_supported(na, nb, s)) {
+        launch_tcmul_single(F, a, na, b, nb, f, st);  // integer tensor core (tcmul.cu)
+        return;
+    }
+    if (s <= 0) s = 8;  // auto on the CUDA cores: the 8 x 8 register tile
     const int R = pick_tile(s, F);
     const int64_t TK = int64_t(MUL_T) * R;
     const int64_t nf = khi - klo;
@@ -279,10 +284,11 @@ void launch_mul_batched(const FieldParams& F, const uint32_t* A, int64_t lda, in
 void launch_mul_batched_fan(const FieldParams& F, const uint32_t* A, int64_t lda, int64_t na,
                             const uint32_t* B, int64_t ldb, int64_t nb, int64_t count, Fan Fo,
                             int64_t ldf, int64_t s, cudaStream_t st) {
-    if (tcmul_supported(na, nb, count)) {  // integer tensor core (tcmul.cu)
+    if (tcmul_supported(na, nb, count, s)) {  // integer tensor core (tcmul.cu)
         launch_tcmul_batched(F, A, lda, na, B, ldb, nb, count, Fo, ldf, st);
         return;
     }
+    if (s <= 0) s = 8;  // auto on the CUDA cores
     const int R = pick_tile(s, F);
     const int64_t TK = int64_t(MUL_T) * R;
     const int64_t nf = na + nb - 1;

@@ -797,8 +797,10 @@ void run_ntt(const FieldParams& F, const uint32_t* A, int64_t lda, int64_t na, c
     // instances per launch group: the two N-word workspaces of a group stay
     // L2-resident (2 x 16 MB at the default), so the row pass reads what the
     // column pass wrote from L2 instead of HBM
+    int64_t chunk_words = int64_t(NTT_CHUNK_WORDS);
+    if (const char* e = getenv("MMM_NTT_CHUNK_WORDS")) chunk_words = atoll(e);  // tools/ntt_sweep
     const int64_t chunk =
-        std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(count, 65535), int64_t(NTT_CHUNK_WORDS) >> logN));
+        std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(count, 65535), chunk_words >> logN));
     g.work[0] = sc.get<uint32_t>(size_t(chunk) << logN);
     g.work[1] = sc.get<uint32_t>(size_t(chunk) << logN);
     if (F.p < (1u << 30))

@@ -423,11 +423,11 @@ __global__ void __launch_bounds__(TCD_T + 32, 1) tcdiv_kernel(TcDivArgs g) {
 
 }  // namespace
 
-bool tcdiv_supported(int64_t na, int64_t nb, int64_t count) {
+bool tcdiv_supported(int64_t na, int64_t nb, int64_t count, int64_t s) {
     const bool fits = nb >= 2 && na >= nb && na <= TCD_MAXA && nb <= TCM_MAXN;
-    if (const char* e = getenv("MMM_DIV_TC")) return atoi(e) != 0 && fits;
-    return fits && nb >= 512 && na - nb + 1 >= 512 &&
-           double(na - nb + 1) * double(nb) * double(count) >= 1.0e9;
+    return tc_route("MMM_DIV_TC", s, fits,
+                    nb >= 512 && na - nb + 1 >= 512 &&
+                        double(na - nb + 1) * double(nb) * double(count) >= 1.0e9);
 }
 
 void launch_tcdiv_batched(const FieldParams& F, const uint32_t* A, int64_t lda, int64_t na,

@@ -29,6 +29,7 @@
 // buffers while the tensor core runs the previous d's 16 MMAs (128 x N x 32,
 // N = 224 / 240); one thread issues, tcgen05.commit -> mbarrier frees the
 // buffer.  Persistent: one CTA per SM walks the batch.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -40,6 +41,8 @@
 #include "tctile.cuh"
 
 namespace mmm_cu {
+
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -227,13 +230,214 @@ __global__ void __launch_bounds__(TCM_T + 32, 1) tcmul_kernel(TcArgs g) {
     if (warp == 0) tc::tmem_free<512>(tbase);
 }
 
+// ---- one large product split over the SMs (cfg1: 2^14 x 2^14) -------------
+// a and b cut into segments of <= 4096 terms; work item = (segment of a,
+// segment of b, a range of <= 32 consecutive tiles d of that segment pair).
+// An item accumulates its tiles in the TMEM planes exactly like a batch
+// instance (column offset d - d0), then adds its reduced outputs into a u64
+// accumulator (RED.ADD.U64; up to a few dozen residues per word); after a grid
+// barrier every thread finalises a slice: f = acc mod p, acc = 0 (ZeroBuf).
+struct TcSplitArgs {
+    const uint32_t* a;
+    const uint32_t* b;
+    int na, nb, nf;
+    int segA, segB, dpr;          // segments of a / b, tiles per item
+    int rA;                        // items per segment pair (max over a's segments)
+    int items;
+    unsigned long long* acc;
+    Fan F;
+    FieldParams Fp;
+    uint32_t c_hi[3];
+};
+
+struct Item {
+    int ia, ib, d0, d1, na_i, nb_j;
+};
+
+__device__ __forceinline__ bool decode_item(const TcSplitArgs& g, int w, Item& it) {
+    const int pr = w / g.rA, r = w % g.rA;
+    it.ia = pr / g.segB;
+    it.ib = pr % g.segB;
+    it.na_i = min(TCM_MAXN, g.na - TCM_MAXN * it.ia);
+    it.nb_j = min(TCM_MAXN, g.nb - TCM_MAXN * it.ib);
+    const int D = (it.na_i + 126) / 128 + 1;
+    it.d0 = r * g.dpr;
+    it.d1 = min(D, it.d0 + g.dpr);
+    return it.d0 < it.d1;
+}
+
+__global__ void __launch_bounds__(TCM_T + 32, 1) tcmul_split_kernel(TcSplitArgs g) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+    uint8_t* sH = sm + OFF_H;
+    uint8_t* sBE = sm + OFF_B + B_PRE;
+    uint32_t* a_pad = reinterpret_cast<uint32_t*>(sm + OFF_A);
+    __shared__ uint64_t full[2], empty[2];
+    __shared__ uint32_t tslot;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+    for (uint32_t i = tid; i < B_BYTES / 16; i += TCM_T + 32)
+        reinterpret_cast<uint4*>(sm + OFF_B)[i] = make_uint4(0, 0, 0, 0);
+    for (int i = tid; i < TCM_AWORDS; i += TCM_T + 32) a_pad[i] = 0;
+    if (warp == 0) tc::tmem_alloc<512>(&tslot);
+    if (tid == 0) {
+        for (int b = 0; b < 2; ++b) {
+            tc::mbar_init(&full[b], 1);
+            tc::mbar_init(&empty[b], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    const uint32_t tbase = tslot;
+
+    if (warp == TCM_T / 32) {  // MMA warp
+        constexpr uint32_t ID_E = tc::idesc_u8(128, BROWS_E), ID_O = tc::idesc_u8(128, BROWS_O);
+        uint32_t fph[2] = {0, 0};
+        uint32_t T = 0;
+        for (int w = blockIdx.x; w < g.items; w += gridDim.x) {
+            Item it;
+            if (!decode_item(g, w, it)) continue;
+            for (int d = it.d0; d < it.d1; ++d, ++T) {
+                const int b = T & 1;
+                tc::mbar_wait(&full[b], fph[b]);
+                fph[b] ^= 1;
+                tc::fence_after_sync();
+                if (lane == 0) {
+                    const int e = d - it.d0;
+                    const uint32_t hb = tc::smem_u32(sH + b * HBUF);
+                    const bool odd = e & 1;
+                    const uint32_t bb = tc::smem_u32(sBE) - (odd ? 128u : 0u);
+                    const uint32_t idesc = odd ? ID_O : ID_E;
+                    const uint32_t col = uint32_t(e & ~1);
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+#pragma unroll
+                        for (int k = 0; k < 4; ++k)
+                            tc::mma_u8(tbase + 64 * u + col, tc::desc_sw128(hb + u * TILE + 32 * k),
+                                       tc::desc_sw128(bb + 32 * k), idesc, 1u);
+                    tc::commit(&empty[b]);
+                }
+                __syncwarp();
+            }
+        }
+    } else {
+        uint32_t eph[2] = {0, 0};
+        int pend[2] = {0, 0};
+        uint32_t T = 0;
+        auto free_buf = [&](int b) {
+            if (pend[b]) {
+                tc::mbar_wait(&empty[b], eph[b]);
+                eph[b] ^= 1;
+                --pend[b];
+            }
+        };
+        auto bar = [] { asm volatile("bar.sync 1, 256;" ::: "memory"); };
+        const uint32_t lane_addr = tbase + (uint32_t(32 * (warp & 3)) << 16);
+        for (int w = blockIdx.x; w < g.items; w += gridDim.x) {
+            Item it;
+            if (!decode_item(g, w, it)) continue;
+            const uint32_t* a = g.a + int64_t(TCM_MAXN) * it.ia;
+            const uint32_t* b = g.b + int64_t(TCM_MAXN) * it.ib;
+            // the window of a the tiles d0..d1-1 read: [128 d0 - 128, 128 d1)
+            const int lo = max(0, 128 * it.d0 - 128), hi = min(TCM_MAXN + 128, 128 * it.d1);
+            for (int i = lo + tid; i < hi; i += TCM_T) a_pad[TCM_APAD + i] = i < it.na_i ? __ldg(a + i) : 0u;
+            const int mB = (it.nb_j + 127) >> 7;
+            for (int u = tid; u < 32 * 8; u += TCM_T) {  // all 32 block rows (zeros past mB)
+                const int j = u >> 3, c = u & 7;
+                uint32_t wv[16];
+#pragma unroll
+                for (int t = 0; t < 16; ++t) {
+                    const int k = 128 * j + 16 * c + t;
+                    wv[t] = (j < mB && k < it.nb_j) ? __ldg(b + k) : 0u;
+                }
+                uint32_t L[4][4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    limb_transpose(wv[4 * q], wv[4 * q + 1], wv[4 * q + 2], wv[4 * q + 3], L[0][q],
+                                   L[1][q], L[2][q], L[3][q]);
+#pragma unroll
+                for (int v = 0; v < 4; ++v)
+                    sts128(sBE, tc::sw128(64 * v + j, 16 * c), L[v][0], L[v][1], L[v][2], L[v][3]);
+            }
+            if (warp < 4) {
+#pragma unroll
+                for (int c0 = 0; c0 < 512; c0 += 32) tmem_st32_zero(lane_addr + c0);
+                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            }
+            bar();
+            for (int d = it.d0; d < it.d1; ++d, ++T) {
+                const int bb = T & 1;
+                free_buf(bb);
+                build_h(sH + bb * HBUF, a_pad, d);
+                tc::fence_async_smem();
+                tc::fence_before_sync();
+                bar();
+                if (tid == 0) tc::mbar_arrive(&full[bb]);
+                ++pend[bb];
+            }
+            free_buf(0);
+            free_buf(1);
+            tc::fence_after_sync();
+            // outputs of this item: blocks d0 + e, e < (d1 - d0) + mB, of segment pair (ia, ib)
+            {
+                const int r = 32 * (warp & 3) + lane;
+                const int ne = (it.d1 - it.d0) + mB;
+                const int64_t kb = int64_t(TCM_MAXN) * (it.ia + it.ib) + 128 * it.d0 + r;
+                for (int e0 = (warp >> 2) * 8; e0 < ne; e0 += 16) {
+                    uint32_t x[7][8];
+#pragma unroll
+                    for (int s = 0; s < 7; ++s) tmem_ld8(lane_addr + 64 * s + e0, x[s]);
+                    tc::tmem_ld_wait();
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        const int64_t k = kb + 128 * (e0 + e);
+                        if (e0 + e < ne && k < g.nf) {
+                            const uint32_t xs[7] = {x[0][e], x[1][e], x[2][e], x[3][e], x[4][e],
+                                                    x[5][e], x[6][e]};
+                            atomicAdd(g.acc + k,
+                                      (unsigned long long)combine_planes(xs, g.c_hi, g.Fp));
+                        }
+                    }
+                }
+            }
+            tc::fence_before_sync();
+            bar();  // TMEM read before the next item zeroes it
+            tc::fence_after_sync();
+        }
+    }
+    // every item's additions are in acc: finalise (f = acc mod p, acc back to zero)
+    __threadfence();
+    cg::this_grid().sync();
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t k = int64_t(blockIdx.x) * blockDim.x + tid; k < g.nf; k += stride) {
+        const unsigned long long v = __ldcg(g.acc + k);
+        g.acc[k] = 0ull;
+        fan_store<true>(g.F, k, reduce(v, g.Fp));
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    if (warp == 0) tc::tmem_free<512>(tbase);
+}
+
 }  // namespace
 
-bool tcmul_supported(int64_t na, int64_t nb, int64_t count) {
-    if (const char* e = getenv("MMM_MUL_TC")) return atoi(e) != 0 && na <= TCM_MAXN && nb <= TCM_MAXN && na >= 1 && nb >= 1;
-    // worth a persistent tensor-core pass: enough products of enough terms
-    return na <= TCM_MAXN && nb <= TCM_MAXN && na >= 512 && nb >= 512 &&
-           double(na) * double(nb) * double(count) >= 1.0e9;
+// Routing (mul.cu, divmod.cu): an explicit program parameter s >= 1 selects the
+// paper's s-parameterised CUDA-core kernel; s <= 0 ("auto") lets the library
+// take the tensor core where it pays.  MMM_MUL_TC / MMM_DIV_TC = 1 force the
+// tensor core wherever the shape allows (tests), 0 forbids it.
+bool tc_route(const char* env, int64_t s, bool shape_ok, bool worth) {
+    if (const char* e = getenv(env)) return atoi(e) != 0 && shape_ok;
+    return s <= 0 && shape_ok && worth;
+}
+
+bool tcmul_supported(int64_t na, int64_t nb, int64_t count, int64_t s) {
+    const bool shape = na >= 1 && nb >= 1 && na <= TCM_MAXN && nb <= TCM_MAXN;
+    return tc_route("MMM_MUL_TC", s, shape,
+                    na >= 512 && nb >= 512 && double(na) * double(nb) * double(count) >= 1.0e9);
 }
 
 void launch_tcmul_batched(const FieldParams& F, const uint32_t* A, int64_t lda, int64_t na,
@@ -270,6 +474,49 @@ void launch_tcmul_batched(const FieldParams& F, const uint32_t* A, int64_t lda, 
         fprintf(stderr, "tcmul stats (CTA 0): prologue=%lld loop=%lld epilogue=%lld mma_wait=%lld cycles\n",
                 h[0], h[1], h[2], h[3]);
     }
+}
+
+bool tcmul_single_supported(int64_t na, int64_t nb, int64_t s) {
+    return tc_route("MMM_MUL_TC", s, na >= 1 && nb >= 1,
+                    double(na) * double(nb) >= 3.0e7 && na >= 512 && nb >= 512);
+}
+
+// One product f = a * b (all na + nb - 1 words) on the tensor core, split over
+// the SMs (tcmul_split_kernel).
+void launch_tcmul_single(const FieldParams& F, const uint32_t* a, int64_t na, const uint32_t* b,
+                         int64_t nb, Fan Fo, cudaStream_t st) {
+    if (na < 1 || nb < 1) throw Error(ST_INVALID, "tensor-core product: empty operand");
+    if (na + nb > (int64_t(1) << 30)) throw Error(ST_INVALID, "tensor-core product: too long");
+    TcSplitArgs g{};
+    g.a = a;
+    g.b = b;
+    g.na = int(na);
+    g.nb = int(nb);
+    g.nf = int(na + nb - 1);
+    g.segA = int(ceil_div(na, TCM_MAXN));
+    g.segB = int(ceil_div(nb, TCM_MAXN));
+    const int Dmax = (int(std::min<int64_t>(na, TCM_MAXN)) + 126) / 128 + 1;
+    const int64_t tiles = int64_t(g.segA) * g.segB * Dmax;
+    const int sms = sm_count();
+    g.dpr = int(std::max<int64_t>(1, std::min<int64_t>(32, ceil_div(tiles, sms))));
+    g.rA = (Dmax + g.dpr - 1) / g.dpr;
+    g.items = g.segA * g.segB * g.rA;
+    g.F = Fo;
+    g.Fp = F;
+    for (int s = 0; s < 3; ++s) {
+        uint64_t x = 1;
+        for (int e = 0; e < 32 + 8 * s; ++e) x = (x * 2) % F.p;
+        g.c_hi[s] = uint32_t(x);
+    }
+    g.acc = zero_buf_acquire(size_t(g.nf), st);
+    MMM_CUDA(cudaFuncSetAttribute(tcmul_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(SMEM_BYTES)));
+    const int blocks = std::min(g.items, sms);
+    void* params[] = {&g};
+    MMM_CUDA(cudaLaunchCooperativeKernel((void*)tcmul_split_kernel, dim3(blocks), dim3(TCM_T + 32),
+                                         params, SMEM_BYTES, st));
+    check_launch("tcmul_split_kernel", dim3(blocks), dim3(TCM_T + 32));
+    zero_buf_release(st);
 }
 
 }  // namespace mmm_cu

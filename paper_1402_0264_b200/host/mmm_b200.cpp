@@ -187,7 +187,7 @@ std::string to_string(const Poly& p) {
 }
 
 // -------------------------------------------------------- oracle-style ----
-Poly oracle_mul(const Poly& a, const Poly& b, const Field& F) { return gpu_mul(a, b, F, 8, 128); }
+Poly oracle_mul(const Poly& a, const Poly& b, const Field& F) { return gpu_mul(a, b, F, 0, 128); }  // auto
 
 Poly oracle_mul_alt(const Poly& a, const Poly& b, const Field& F) {
     if (a.is_zero() || b.is_zero()) return Poly{};

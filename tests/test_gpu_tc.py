@@ -155,3 +155,35 @@ def test_tc_division_fanout(cuda_lib, port, monkeypatch):
         for q, r in zip(qs, rs):
             assert np.array_equal(np.trim_zeros(q[i].cpu().numpy().view(np.uint32).astype(np.int64), "b"), wq)
             assert np.array_equal(np.trim_zeros(r[i].cpu().numpy().view(np.uint32).astype(np.int64), "b"), wr)
+
+
+# ------------------------------------------- one large product, split ----
+@pytest.mark.parametrize("p", [P, 2147483647, 7])
+def test_tc_single_product_vs_oracle(cuda_lib, port, monkeypatch, p):
+    """csrc/tcmul.cu tcmul_split_kernel (segments of 4096 terms x tile ranges
+    over the SMs, u64 accumulation, grid-wide finalise) == oracle_mul."""
+    mmm = cuda_lib
+    monkeypatch.setenv("MMM_MUL_TC", "1")
+    rng = np.random.default_rng(31 + p % 97)
+    for na, nb in [(1, 1), (5000, 3), (4096, 4096), (4097, 4095), (9000, 5000), (16384, 1000),
+                   (700, 20000)]:
+        a, b = rng.integers(0, p, na), rng.integers(0, p, nb)
+        a[-1] = max(int(a[-1]), 1)
+        b[-1] = max(int(b[-1]), 1)
+        got = mmm.mul(a, b, p)
+        want = port.mul(a, b, p) if na * nb <= 5e7 else mmm.ntt_mul(a, b, p) if p == P else None
+        if want is None:
+            monkeypatch.setenv("MMM_MUL_TC", "0")
+            want = mmm.mul(a, b, p, s=8)
+            monkeypatch.setenv("MMM_MUL_TC", "1")
+        assert np.array_equal(got, want), (p, na, nb)
+    # repeated calls reuse the zeroed accumulator
+    a, b = rng.integers(0, p, 12000), rng.integers(0, p, 12000)
+    assert np.array_equal(mmm.mul(a, b, p), mmm.mul(a, b, p))
+
+
+def test_cfg1_tensor_core(cuda_lib, golden_configs):
+    """cfg1 (2^14 x 2^14) on the default (auto) path == the reference digest."""
+    from helpers import ProductRng, digest
+    c = suites.cfg1(ProductRng(42))
+    assert digest(cuda_lib.mul(c["a"], c["b"], P)) == golden_configs["cfg1"]["f"]
