@@ -260,10 +260,17 @@ __global__ void __launch_bounds__(TCD_T + 32, 1) tcdiv_kernel(TcDivArgs g) {
             for (int u = tid; u < mB * 8; u += TCD_T) {
                 const int j = u >> 3, c = u & 7;
                 uint32_t wv[16];
+                {  // B'[k] = b[nb - 1 - k], k = 128 j + 16 c + t: 16 words of b read backwards
+                    const int k0 = 128 * j + 16 * c;
+                    uint32_t rv[16];
+                    if (k0 + 16 <= nb) {
+                        load16(b + (nb - 16 - k0), 16, rv);
 #pragma unroll
-                for (int t = 0; t < 16; ++t) {
-                    const int k = 128 * j + 16 * c + t;  // B' index
-                    wv[t] = k < nb ? __ldg(b + (nb - 1 - k)) : 0u;
+                        for (int t = 0; t < 16; ++t) wv[t] = rv[15 - t];
+                    } else {
+#pragma unroll
+                        for (int t = 0; t < 16; ++t) wv[t] = k0 + t < nb ? __ldg(b + (nb - 1 - k0 - t)) : 0u;
+                    }
                 }
                 uint32_t L[4][4];
 #pragma unroll

@@ -141,16 +141,12 @@ __global__ void __launch_bounds__(TCM_T + 32, 1) tcmul_kernel(TcArgs g) {
             t0 = clock64();
             const uint32_t* a = g.A + inst * g.lda;
             const uint32_t* b = g.B + inst * g.ldb;
-            for (int i = tid; i < na; i += TCM_T) a_pad[TCM_APAD + i] = __ldg(a + i);
+            stage_words(a_pad + TCM_APAD, a, 0, na, na, tid, TCM_T);
             // B rows 64 v + j; unit = (j, chunk c)
             for (int u = tid; u < mB * 8; u += TCM_T) {
                 const int j = u >> 3, c = u & 7;
                 uint32_t wv[16];
-#pragma unroll
-                for (int t = 0; t < 16; ++t) {
-                    const int k = 128 * j + 16 * c + t;
-                    wv[t] = k < nb ? __ldg(b + k) : 0u;
-                }
+                load16(b + 128 * j + 16 * c, nb - (128 * j + 16 * c), wv);
                 uint32_t L[4][4];
 #pragma unroll
                 for (int q = 0; q < 4; ++q)
@@ -343,16 +339,12 @@ __global__ void __launch_bounds__(TCM_T + 32, 1) tcmul_split_kernel(TcSplitArgs 
             const uint32_t* b = g.b + int64_t(TCM_MAXN) * it.ib;
             // the window of a the tiles d0..d1-1 read: [128 d0 - 128, 128 d1)
             const int lo = max(0, 128 * it.d0 - 128), hi = min(TCM_MAXN + 128, 128 * it.d1);
-            for (int i = lo + tid; i < hi; i += TCM_T) a_pad[TCM_APAD + i] = i < it.na_i ? __ldg(a + i) : 0u;
+            stage_words(a_pad + TCM_APAD, a, lo, hi, it.na_i, tid, TCM_T);
             const int mB = (it.nb_j + 127) >> 7;
             for (int u = tid; u < 32 * 8; u += TCM_T) {  // all 32 block rows (zeros past mB)
                 const int j = u >> 3, c = u & 7;
                 uint32_t wv[16];
-#pragma unroll
-                for (int t = 0; t < 16; ++t) {
-                    const int k = 128 * j + 16 * c + t;
-                    wv[t] = (j < mB && k < it.nb_j) ? __ldg(b + k) : 0u;
-                }
+                load16(b + 128 * j + 16 * c, j < mB ? it.nb_j - (128 * j + 16 * c) : 0, wv);
                 uint32_t L[4][4];
 #pragma unroll
                 for (int q = 0; q < 4; ++q)

@@ -108,6 +108,52 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
 }
 
 
+// w[t] = p[t] for t < 16, words at or past `valid` read as zero; four 16-byte
+// loads when p is 16-byte aligned and the 16 words are all valid.
+__device__ __forceinline__ void load16(const uint32_t* p, int valid, uint32_t (&w)[16]) {
+    if (valid >= 16 && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint4 v = __ldg(reinterpret_cast<const uint4*>(p) + q);
+            w[4 * q] = v.x;
+            w[4 * q + 1] = v.y;
+            w[4 * q + 2] = v.z;
+            w[4 * q + 3] = v.w;
+        }
+    } else {
+#pragma unroll
+        for (int t = 0; t < 16; ++t) w[t] = t < valid ? __ldg(p + t) : 0u;
+    }
+}
+
+// a_pad[base + i] = a[i] for i in [lo, hi) (zero where i >= n), 16-byte loads
+// and stores where a and the range allow (lo a multiple of 4).
+__device__ __forceinline__ void stage_words(uint32_t* dst, const uint32_t* a, int lo, int hi, int n,
+                                            int tid, int nthreads) {
+    if ((reinterpret_cast<uintptr_t>(a) & 15) == 0 && (lo & 3) == 0 &&
+        (reinterpret_cast<uintptr_t>(dst + lo) & 15) == 0) {
+        for (int i = lo + 4 * tid; i < hi; i += 4 * nthreads) {
+            uint4 v;
+            if (i + 4 <= n) {
+                v = __ldg(reinterpret_cast<const uint4*>(a + i));
+            } else {
+                v.x = i < n ? __ldg(a + i) : 0u;
+                v.y = i + 1 < n ? __ldg(a + i + 1) : 0u;
+                v.z = i + 2 < n ? __ldg(a + i + 2) : 0u;
+                v.w = i + 3 < n ? __ldg(a + i + 3) : 0u;
+            }
+            if (i + 4 <= hi) {
+                *reinterpret_cast<uint4*>(dst + i) = v;
+            } else {
+                const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
+                for (int q = 0; i + q < hi; ++q) dst[i + q] = vv[q];
+            }
+        }
+    } else {
+        for (int i = lo + tid; i < hi; i += nthreads) dst[i] = i < n ? __ldg(a + i) : 0u;
+    }
+}
+
 __device__ __forceinline__ uint32_t tmem_ld1(uint32_t taddr) {
     uint32_t v;
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(v) : "r"(taddr));
