@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(TCD_T + 32, 1) tcdiv_kernel(TcDivArgs g) {
     uint32_t* sE = sS + 128;
     uint32_t* part = sE + 128;                                    // [8][128] partial sums
     uint32_t* tmp = part + 1024;
-    __shared__ uint64_t full[2], empty[2], half[2];  // tile built / MMAs done / upper part built
+    __shared__ uint64_t full[2], empty[2];
     __shared__ uint32_t tslot;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const FieldParams F = g.Fp;
@@ -203,7 +203,6 @@ __global__ void __launch_bounds__(TCD_T + 32, 1) tcdiv_kernel(TcDivArgs g) {
         for (int b = 0; b < 2; ++b) {
             tc::mbar_init(&full[b], 1);
             tc::mbar_init(&empty[b], 1);
-            tc::mbar_init(&half[b], 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -215,26 +214,9 @@ __global__ void __launch_bounds__(TCD_T + 32, 1) tcdiv_kernel(TcDivArgs g) {
     if (warp == TCD_T / 32) {
         // ---- MMA warp: tile K of each instance from buffer T & 1 ----
         constexpr uint32_t ID_E = tc::idesc_u8(128, BROWS_E), ID_O = tc::idesc_u8(128, BROWS_O);
-        // Between issues it builds the strictly-upper units of the next tile
-        // (they read only the previous quotient block) into the free buffer, so
-        // the compute warps build only the band on and below the diagonal.
-        uint32_t fph[2] = {0, 0}, eph[2] = {0, 0};
-        int issued[2] = {0, 0};  // tiles issued on buffer b whose completion we did not wait for
+        uint32_t fph[2] = {0, 0};
         uint32_t T = 0;
-        auto upper = [&](int K, uint32_t Tk) {  // tile K's upper units into buffer Tk & 1
-            const int b = Tk & 1;
-            if (issued[b]) {  // the buffer's previous tile (Tk - 2) must be done
-                tc::mbar_wait(&empty[b], eph[b]);
-                eph[b] ^= 1;
-                --issued[b];
-            }
-            build_h_upper_warp(sH + b * HBUF, qz - TCM_APAD, K, lane);
-            tc::fence_async_smem();
-            __syncwarp();
-            if (lane == 0) tc::mbar_arrive(&half[b]);
-        };
-        for (int64_t inst = blockIdx.x; inst < g.count; inst += gridDim.x) {
-            upper(0, T);  // reads Q[-128..-1] = 0
+        for (int64_t inst = blockIdx.x; inst < g.count; inst += gridDim.x)
             for (int K = 0; K <= Kq; ++K, ++T) {
                 const int b = T & 1;
                 tc::mbar_wait(&full[b], fph[b]);
@@ -255,20 +237,9 @@ __global__ void __launch_bounds__(TCD_T + 32, 1) tcdiv_kernel(TcDivArgs g) {
                     tc::commit(&empty[b]);
                 }
                 __syncwarp();
-                ++issued[b];
-                if (K < Kq) upper(K + 1, T + 1);  // Q_K is in q_pad (published with full)
             }
-            // the instance's last two tiles complete before the compute warps'
-            // epilogue reads the planes; settle their phases here too
-            for (int b = 0; b < 2; ++b)
-                while (issued[b]) {
-                    tc::mbar_wait(&empty[b], eph[b]);
-                    eph[b] ^= 1;
-                    --issued[b];
-                }
-        }
     } else {
-        uint32_t eph[2] = {0, 0}, hph[2] = {0, 0};
+        uint32_t eph[2] = {0, 0};
         int pend[2] = {0, 0};
         uint32_t T = 0;
         auto free_buf = [&](int b) {
@@ -388,9 +359,7 @@ __global__ void __launch_bounds__(TCD_T + 32, 1) tcdiv_kernel(TcDivArgs g) {
                 {
                     TCD_T0();
                     free_buf(T & 1);
-                    tc::mbar_wait(&half[T & 1], hph[T & 1]);  // the MMA warp built the upper units
-                    hph[T & 1] ^= 1;
-                    build_h(sH + (T & 1) * HBUF, qz - TCM_APAD, K, 1);  // the band (Q_K, Q_{K-1})
+                    build_h(sH + (T & 1) * HBUF, qz - TCM_APAD, K);  // tile K (Q_K, Q_{K-1})
                     tc::fence_async_smem();
                     TCD_ACC(4);
                 }
@@ -417,9 +386,7 @@ __global__ void __launch_bounds__(TCD_T + 32, 1) tcdiv_kernel(TcDivArgs g) {
             long long tq = clock64();
             // ---- the last tile (Q_{Kq-1}'s upper triangle), then the remainder ----
             free_buf(T & 1);
-            tc::mbar_wait(&half[T & 1], hph[T & 1]);
-            hph[T & 1] ^= 1;
-            build_h(sH + (T & 1) * HBUF, qz - TCM_APAD, Kq, 1);
+            build_h(sH + (T & 1) * HBUF, qz - TCM_APAD, Kq);
             tc::fence_async_smem();
             tc::fence_before_sync();
             bar();

@@ -64,12 +64,13 @@ __device__ __forceinline__ void put_row_chunk(uint8_t* h, uint32_t tile_stride, 
     for (int u = 0; u < 4; ++u) sts128(h + u * tile_stride, off, L[u][0], L[u][1], L[u][2], L[u][3]);
 }
 
-// Rows 4 rg .. 4 rg + 3, chunk c (elements t in [16c, 16c+16)) of the four limb
-// tiles of H_d: row r = 4 rg + k needs a[i0 + k - t'], t' = 0..15,
-// i0 = 128 d + 4 rg - 16 c: words a[i0 - 16 .. i0 + 3] (20, 16-byte aligned
-// with the pad of 128).
-__device__ __forceinline__ void build_unit(uint8_t* hbuf, const uint32_t* a_pad, int d, int rg,
-                                           int c) {
+// H_d limb tiles: thread (warp w, lane L) builds rows 4 rg .. 4 rg + 3 of chunk c,
+// rg = 4 w + L / 8, c = L % 8 (conflict-free loads and swizzled stores).
+__device__ __forceinline__ void build_h(uint8_t* hbuf, const uint32_t* a_pad, int d) {
+    const int w = threadIdx.x >> 5, L = threadIdx.x & 31;
+    const int rg = 4 * w + (L >> 3), c = L & 7;
+    // rows r = 4 rg + k need a[i0 + k - t'], t' = 0..15, i0 = 128 d + 4 rg - 16 c:
+    // words a[i0 - 16 .. i0 + 3] (20, 16-byte aligned with the pad of 128)
     const int i0 = 128 * d + 4 * rg - 16 * c;
     const uint4* src = reinterpret_cast<const uint4*>(a_pad + TCM_APAD + i0 - 16);
     uint32_t x[20];
@@ -87,34 +88,6 @@ __device__ __forceinline__ void build_unit(uint8_t* hbuf, const uint32_t* a_pad,
 #pragma unroll
         for (int t = 0; t < 16; ++t) wv[t] = x[16 + k - t];  // a[i0 + k - t]
         put_row_chunk(hbuf, TILE, uint32_t(4 * rg + k), uint32_t(c), wv);
-    }
-}
-
-// H_d limb tiles: thread (warp w, lane L) builds rows 4 rg .. 4 rg + 3 of chunk c,
-// rg = 4 w + L / 8, c = L % 8 (conflict-free loads and swizzled stores).
-// part: 0 = all units; 1 = only the units on or below the diagonal band
-// (c <= rg / 4: some t <= r), the ones whose upper neighbours another warp builds.
-__device__ __forceinline__ void build_h(uint8_t* hbuf, const uint32_t* a_pad, int d, int part = 0) {
-    const int w = threadIdx.x >> 5, L = threadIdx.x & 31;
-    const int rg = 4 * w + (L >> 3), c = L & 7;
-    if (part == 1 && c > (rg >> 2)) return;
-    build_unit(hbuf, a_pad, d, rg, c);
-}
-
-// The 112 units strictly above the diagonal band (c > rg / 4: every t > r),
-// built by one warp (lane = the warp's lane): unit i -> (rg, c) through the
-// groups q = rg / 4, which hold 4 (7 - q) units each.
-__device__ __forceinline__ void build_h_upper_warp(uint8_t* hbuf, const uint32_t* a_pad, int d,
-                                                   int lane) {
-    for (int i = lane; i < 112; i += 32) {
-        int q = 0, base = 0;
-        while (base + 4 * (7 - q) <= i) {
-            base += 4 * (7 - q);
-            ++q;
-        }
-        const int off = i - base, per = 7 - q;
-        const int rg = 4 * q + off / per, c = q + 1 + off % per;
-        build_unit(hbuf, a_pad, d, rg, c);
     }
 }
 
