@@ -178,6 +178,17 @@ def ntt_mul_sharded(mmm, p, d_a, na, d_b, nb, d_f, dist, world: int, rank: int, 
     NCCL over NVLink.  d_a, d_b: replicated int32 device tensors."""
     import torch
 
+    # every step -- phase kernels, block packing, collectives -- on the caller's
+    # stream, in order (torch ops and NCCL calls follow the current stream)
+    ext = torch.cuda.ExternalStream(stream, device=d_a.device) if stream else \
+        torch.cuda.current_stream(d_a.device)
+    with torch.cuda.stream(ext):
+        return _ntt_mul_sharded(mmm, p, d_a, na, d_b, nb, d_f, dist, world, rank, ext.cuda_stream)
+
+
+def _ntt_mul_sharded(mmm, p, d_a, na, d_b, nb, d_f, dist, world, rank, stream):
+    import torch
+
     nf = na + nb - 1
     n1, n2 = mmm.ntt_shape(p, nf)
     sh = NttShards(n1, n2, world)
