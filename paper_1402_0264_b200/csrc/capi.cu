@@ -200,15 +200,29 @@ using namespace mmm_cu;
 
 namespace {
 
-// Field::Field (field.cpp:10-25).
+// Field::Field (field.cpp:10-25).  The trial-division primality test costs
+// ~70 us on the host for a 29-bit p; the calling thread remembers the last
+// few primes it validated, so repeated calls (the bench's steps, a batch of
+// small products) pay it once.
 FieldParams field_or_throw(int64_t p) {
+    struct Seen {
+        int64_t p = 0;
+        FieldParams F{};
+    };
+    thread_local Seen seen[8];
+    thread_local int next_slot = 0;
+    for (const Seen& e : seen)
+        if (e.p == p && p != 0) return e.F;
     if (p < 2 || p >= (int64_t(1) << 31))
         throw Error(ST_INVALID, "field: p must satisfy 2 <= p < 2^31, got " + std::to_string(p));
     bool prime = p == 2 || (p % 2 != 0);
     for (int64_t d = 3; prime && d * d <= p; d += 2)
         if (p % d == 0) prime = false;
     if (!prime) throw Error(ST_INVALID, "field: p must be prime, got " + std::to_string(p));
-    return make_field(uint32_t(p));
+    const FieldParams F = make_field(uint32_t(p));
+    seen[next_slot] = {p, F};
+    next_slot = (next_slot + 1) % 8;
+    return F;
 }
 
 // validate_coeffs (run_util.hpp:24-29).

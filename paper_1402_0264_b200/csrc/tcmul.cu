@@ -332,9 +332,11 @@ __global__ void __launch_bounds__(TCM_T + 32, 1) tcmul_split_kernel(TcSplitArgs 
         };
         auto bar = [] { asm volatile("bar.sync 1, 256;" ::: "memory"); };
         const uint32_t lane_addr = tbase + (uint32_t(32 * (warp & 3)) << 16);
+        long long t0 = clock64(), sp[4] = {0, 0, 0, 0};
         for (int w = blockIdx.x; w < g.items; w += gridDim.x) {
             Item it;
             if (!decode_item(g, w, it)) continue;
+            const long long ti = clock64();
             const uint32_t* a = g.a + int64_t(TCM_MAXN) * it.ia;
             const uint32_t* b = g.b + int64_t(TCM_MAXN) * it.ib;
             // the window of a the tiles d0..d1-1 read: [128 d0 - 128, 128 d1)
@@ -360,6 +362,8 @@ __global__ void __launch_bounds__(TCM_T + 32, 1) tcmul_split_kernel(TcSplitArgs 
                 asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             }
             bar();
+            const long long tl = clock64();
+            sp[0] += tl - ti;
             for (int d = it.d0; d < it.d1; ++d, ++T) {
                 const int bb = T & 1;
                 free_buf(bb);
@@ -373,6 +377,8 @@ __global__ void __launch_bounds__(TCM_T + 32, 1) tcmul_split_kernel(TcSplitArgs 
             free_buf(0);
             free_buf(1);
             tc::fence_after_sync();
+            const long long te = clock64();
+            sp[1] += te - tl;
             // outputs of this item: blocks d0 + e, e < (d1 - d0) + mB, of segment pair (ia, ib)
             {
                 const int r = 32 * (warp & 3) + lane;
@@ -398,6 +404,13 @@ __global__ void __launch_bounds__(TCM_T + 32, 1) tcmul_split_kernel(TcSplitArgs 
             tc::fence_before_sync();
             bar();  // TMEM read before the next item zeroes it
             tc::fence_after_sync();
+            sp[2] += clock64() - te;
+        }
+        if (blockIdx.x == 0 && tid == 0) {
+            tcm_stats[4] = sp[0];
+            tcm_stats[5] = sp[1];
+            tcm_stats[6] = sp[2];
+            tcm_stats[7] = clock64() - t0;
         }
     }
     // every item's additions are in acc: finalise (f = acc mod p, acc back to zero)
@@ -509,6 +522,13 @@ void launch_tcmul_single(const FieldParams& F, const uint32_t* a, int64_t na, co
                                          params, SMEM_BYTES, st));
     check_launch("tcmul_split_kernel", dim3(blocks), dim3(TCM_T + 32));
     zero_buf_release(st);
+    if (getenv("MMM_TC_STATS")) {
+        long long h[8];
+        MMM_CUDA(cudaMemcpyFromSymbolAsync(h, tcm_stats, sizeof(h), 0, cudaMemcpyDeviceToHost, st));
+        MMM_CUDA(cudaStreamSynchronize(st));
+        fprintf(stderr, "tcmul_split stats (CTA 0): items=%d per_item_tiles=%d stage+B=%lld tiles=%lld "
+                "epilogue=%lld total_to_sync=%lld cycles\n", g.items, g.dpr, h[4], h[5], h[6], h[7]);
+    }
 }
 
 }  // namespace mmm_cu
