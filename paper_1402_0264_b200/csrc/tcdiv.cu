@@ -37,7 +37,9 @@ namespace {
 
 using namespace tct;
 
-constexpr int TCD_T = 256;
+constexpr int TCD_T = 256;    // compute warps 0-7: the per-step solve
+constexpr int TCD_BLD = 128;  // builder warps 8-11: the tiles
+constexpr int TCD_ALL = TCD_T + TCD_BLD + 32;  // + the MMA warp
 constexpr int TCD_MAXA = 8192;
 constexpr int TCD_QPAD = 256;                           // zero words before Q
 constexpr int TCD_QWORDS = TCD_QPAD + TCD_MAXA + 256;   // Q, padded
@@ -171,7 +173,7 @@ __device__ long long tcd_stats[8];
 #define TCD_ACC(i) st[i] += clock64() - _t0
 
 template <bool FAN>
-__global__ void __launch_bounds__(TCD_T + 32, 1) tcdiv_kernel(TcDivArgs g) {
+__global__ void __launch_bounds__(TCD_T + TCD_BLD + 32, 1) tcdiv_kernel(TcDivArgs g) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -185,7 +187,7 @@ __global__ void __launch_bounds__(TCD_T + 32, 1) tcdiv_kernel(TcDivArgs g) {
     uint32_t* sE = sS + 128;
     uint32_t* part = sE + 128;                                    // [8][128] partial sums
     uint32_t* tmp = part + 1024;
-    __shared__ uint64_t full[2], empty[2];
+    __shared__ uint64_t full[2], empty[2], qready[2], built[2];
     __shared__ uint32_t tslot;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const FieldParams F = g.Fp;
@@ -194,15 +196,17 @@ __global__ void __launch_bounds__(TCD_T + 32, 1) tcdiv_kernel(TcDivArgs g) {
     const int mB = (nb + 127) >> 7;
     const int Kq = (mu + 127) >> 7;  // quotient blocks; tiles d = 0 .. Kq
 
-    for (uint32_t i = tid; i < B_BYTES / 16; i += TCD_T + 32)
+    for (uint32_t i = tid; i < B_BYTES / 16; i += TCD_ALL)
         reinterpret_cast<uint4*>(sm + D_OFF_B)[i] = make_uint4(0, 0, 0, 0);
-    for (int i = tid; i < TCD_QWORDS; i += TCD_T + 32) q_pad[i] = 0;
-    for (int i = tid; i < 128; i += TCD_T + 32) hs[i - 128] = 0;
+    for (int i = tid; i < TCD_QWORDS; i += TCD_ALL) q_pad[i] = 0;
+    for (int i = tid; i < 128; i += TCD_ALL) hs[i - 128] = 0;
     if (warp == 0) tc::tmem_alloc<512>(&tslot);
     if (tid == 0) {
         for (int b = 0; b < 2; ++b) {
             tc::mbar_init(&full[b], 1);
             tc::mbar_init(&empty[b], 1);
+            tc::mbar_init(&qready[b], 1);
+            tc::mbar_init(&built[b], 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -211,7 +215,30 @@ __global__ void __launch_bounds__(TCD_T + 32, 1) tcdiv_kernel(TcDivArgs g) {
     tc::fence_after_sync();
     const uint32_t tbase = tslot;
 
-    if (warp == TCD_T / 32) {
+    if (warp >= TCD_T / 32 && warp < (TCD_T + TCD_BLD) / 32) {
+        // ---- builder warps: tile K (Q_K lower, Q_{K-1} upper) into buffer T & 1,
+        //      while the compute warps run the next step's correction product ----
+        const int bt = tid - TCD_T;
+        uint32_t qph[2] = {0, 0}, eph[2] = {0, 0};
+        uint32_t T = 0;
+        for (int64_t inst = blockIdx.x; inst < g.count; inst += gridDim.x)
+            for (int K = 0; K <= Kq; ++K, ++T) {
+                const int b = T & 1;
+                tc::mbar_wait(&qready[b], qph[b]);  // Q_K (and Q_{K-1}) published
+                qph[b] ^= 1;
+                if (T >= 2) {  // the buffer's previous tile (T - 2) is done
+                    tc::mbar_wait(&empty[b], eph[b]);
+                    eph[b] ^= 1;
+                }
+                const int wb = bt >> 5, L = bt & 31;
+#pragma unroll
+                for (int i = 0; i < 2; ++i)
+                    build_unit(sH + b * HBUF, qz - TCM_APAD, K, 4 * (wb + 4 * i) + (L >> 3), L & 7);
+                tc::fence_async_smem();
+                asm volatile("bar.sync 2, 128;" ::: "memory");
+                if (bt == 0) tc::mbar_arrive(&built[b]);
+            }
+    } else if (warp == (TCD_T + TCD_BLD) / 32) {
         // ---- MMA warp: tile K of each instance from buffer T & 1 ----
         constexpr uint32_t ID_E = tc::idesc_u8(128, BROWS_E), ID_O = tc::idesc_u8(128, BROWS_O);
         uint32_t fph[2] = {0, 0};
@@ -239,7 +266,7 @@ __global__ void __launch_bounds__(TCD_T + 32, 1) tcdiv_kernel(TcDivArgs g) {
                 __syncwarp();
             }
     } else {
-        uint32_t eph[2] = {0, 0};
+        uint32_t eph[2] = {0, 0}, bph[2] = {0, 0};
         int pend[2] = {0, 0};
         uint32_t T = 0;
         auto free_buf = [&](int b) {
@@ -330,17 +357,20 @@ __global__ void __launch_bounds__(TCD_T + 32, 1) tcdiv_kernel(TcDivArgs g) {
             // off) and the tiles K-1 (against B'_1) and K (against B'_0) that Q
             // blocks < K determine come from one 256-term product on the CUDA
             // cores; the MMA warp runs tile K-1 meanwhile.
+            // corr_0 = 0 (no quotient block yet)
+            for (int i = tid; i < 1024; i += TCD_T) part[i] = 0;
+            bar();
             for (int K = 0; K < Kq; ++K, ++T) {
                 uint32_t* qk = qz + 128 * K;  // Q block K (zero here)
                 {
                     TCD_T0();
-                    toeplitz_partials_256(qk, bp01, part, F);
-                    bar();
-                    if (tid < 128) {
+                    if (tid < 128) {  // E = A' - S - corr (partials of the previous step)
                         sE[tid] = submod(submod(aK, sS[tid], F),
                                          partials_sum(part, 128, 128, tid, F), F);
                         const int kn = 128 * (K + 1) + tid;  // prefetch A' block K+1
                         aK = kn < na ? __ldg(a + (na - 1 - kn)) : 0u;
+                    } else {
+                        qk[tid] = 0;  // Q block K+1 (tid - 128 + 128): zero for corr_{K+1}
                     }
                     bar();
                     TCD_ACC(3);
@@ -354,13 +384,14 @@ __global__ void __launch_bounds__(TCD_T + 32, 1) tcdiv_kernel(TcDivArgs g) {
                         if (k1 < mu) fan_store<FAN>(g.Q, inst * g.ldq + (mu - 1 - k1), v1);
                     }
                     bar();
+                    if (tid == 0) tc::mbar_arrive(&qready[T & 1]);  // the builders take tile K
                     st[6] += clock64() - _t1;
                 }
                 {
                     TCD_T0();
-                    free_buf(T & 1);
-                    build_h(sH + (T & 1) * HBUF, qz - TCM_APAD, K);  // tile K (Q_K, Q_{K-1})
-                    tc::fence_async_smem();
+                    // corr_{K+1}: the tiles K (against B'_1) and K+1 (upper, against
+                    // B'_0) that Q blocks <= K determine -- while tile K is built
+                    if (K + 1 < Kq) toeplitz_partials_256(qk + 128, bp01, part, F);
                     TCD_ACC(4);
                 }
                 {
@@ -373,24 +404,26 @@ __global__ void __launch_bounds__(TCD_T + 32, 1) tcdiv_kernel(TcDivArgs g) {
                         for (int s = 0; s < 7; ++s) x[s] = tmem_ld1(lane_addr + 64 * s + K + 1);
                         tc::tmem_ld_wait();
                         sS[32 * warp + lane] = combine_planes(x, g.c_hi, F);
-                    } else {
-                        qk[tid] = 0;  // Q block K+1 (tid - 128 + 128)
                     }
                     tc::fence_before_sync();
                     bar();
-                    if (tid == 0) tc::mbar_arrive(&full[T & 1]);
+                    if (tid == 0) {
+                        tc::mbar_wait(&built[T & 1], bph[T & 1]);
+                        tc::mbar_arrive(&full[T & 1]);
+                    }
+                    bph[T & 1] ^= 1;
                     ++pend[T & 1];
                     TCD_ACC(2);
                 }
             }
             long long tq = clock64();
             // ---- the last tile (Q_{Kq-1}'s upper triangle), then the remainder ----
-            free_buf(T & 1);
-            build_h(sH + (T & 1) * HBUF, qz - TCM_APAD, Kq);
-            tc::fence_async_smem();
-            tc::fence_before_sync();
-            bar();
-            if (tid == 0) tc::mbar_arrive(&full[T & 1]);
+            if (tid == 0) {
+                tc::mbar_arrive(&qready[T & 1]);
+                tc::mbar_wait(&built[T & 1], bph[T & 1]);
+                tc::mbar_arrive(&full[T & 1]);
+            }
+            bph[T & 1] ^= 1;
             ++pend[T & 1];
             ++T;
             free_buf(0);
@@ -465,8 +498,8 @@ void launch_tcdiv_batched(const FieldParams& F, const uint32_t* A, int64_t lda, 
     MMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(D_SMEM_BYTES)));
     const int blocks = int(std::min<int64_t>(count, sm_count()));
-    kern<<<blocks, TCD_T + 32, D_SMEM_BYTES, st>>>(g);
-    check_launch("tcdiv_kernel", dim3(blocks), dim3(TCD_T + 32));
+    kern<<<blocks, TCD_ALL, D_SMEM_BYTES, st>>>(g);
+    check_launch("tcdiv_kernel", dim3(blocks), dim3(TCD_ALL));
     if (getenv("MMM_TC_STATS")) {
         long long h[8];
         MMM_CUDA(cudaMemcpyFromSymbolAsync(h, tcd_stats, sizeof(h), 0, cudaMemcpyDeviceToHost, st));

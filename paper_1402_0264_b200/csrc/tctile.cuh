@@ -64,13 +64,12 @@ __device__ __forceinline__ void put_row_chunk(uint8_t* h, uint32_t tile_stride, 
     for (int u = 0; u < 4; ++u) sts128(h + u * tile_stride, off, L[u][0], L[u][1], L[u][2], L[u][3]);
 }
 
-// H_d limb tiles: thread (warp w, lane L) builds rows 4 rg .. 4 rg + 3 of chunk c,
-// rg = 4 w + L / 8, c = L % 8 (conflict-free loads and swizzled stores).
-__device__ __forceinline__ void build_h(uint8_t* hbuf, const uint32_t* a_pad, int d) {
-    const int w = threadIdx.x >> 5, L = threadIdx.x & 31;
-    const int rg = 4 * w + (L >> 3), c = L & 7;
-    // rows r = 4 rg + k need a[i0 + k - t'], t' = 0..15, i0 = 128 d + 4 rg - 16 c:
-    // words a[i0 - 16 .. i0 + 3] (20, 16-byte aligned with the pad of 128)
+// Rows 4 rg .. 4 rg + 3, chunk c (elements t in [16c, 16c+16)) of the four limb
+// tiles of H_d: row r = 4 rg + k needs a[i0 + k - t'], t' = 0..15,
+// i0 = 128 d + 4 rg - 16 c: words a[i0 - 16 .. i0 + 3] (20, 16-byte aligned
+// with the pad of 128).
+__device__ __forceinline__ void build_unit(uint8_t* hbuf, const uint32_t* a_pad, int d, int rg,
+                                           int c) {
     const int i0 = 128 * d + 4 * rg - 16 * c;
     const uint4* src = reinterpret_cast<const uint4*>(a_pad + TCM_APAD + i0 - 16);
     uint32_t x[20];
@@ -89,6 +88,14 @@ __device__ __forceinline__ void build_h(uint8_t* hbuf, const uint32_t* a_pad, in
         for (int t = 0; t < 16; ++t) wv[t] = x[16 + k - t];  // a[i0 + k - t]
         put_row_chunk(hbuf, TILE, uint32_t(4 * rg + k), uint32_t(c), wv);
     }
+}
+
+// H_d limb tiles by 256 threads: thread (warp w, lane L) builds rows
+// 4 rg .. 4 rg + 3 of chunk c, rg = 4 w + L / 8, c = L % 8 (conflict-free loads
+// and swizzled stores).
+__device__ __forceinline__ void build_h(uint8_t* hbuf, const uint32_t* a_pad, int d) {
+    const int w = threadIdx.x >> 5, L = threadIdx.x & 31;
+    build_unit(hbuf, a_pad, d, 4 * w + (L >> 3), L & 7);
 }
 
 __device__ __forceinline__ void tmem_st32_zero(uint32_t taddr) {
