@@ -48,7 +48,8 @@ constexpr uint32_t D_OFF_H = 0;                           // two H buffers (4 li
 constexpr uint32_t D_OFF_B = D_OFF_H + 2 * HBUF;          // B_PRE | 240 rows (tctile.cuh)
 constexpr uint32_t D_OFF_Q = D_OFF_B + B_BYTES;           // u32 Q (padded)
 constexpr uint32_t D_OFF_SM = D_OFF_Q + TCD_QWORDS * 4;   // small arrays
-constexpr uint32_t D_SMALL = 256 + 256 + 128 + 128 + 1024 + 128;  // B'[0..256), h (padded), S, E, parts, tmp
+constexpr uint32_t D_SMALL = 256 + 2 * 256 + 128 + 128 + 1024 + 128 + 256 + 1024 + 128;
+// B'[0..256), h ping-pong (each: 128 zeros, h), S, E, parts, tmp | builders: B'[0..256), parts, tmp
 constexpr uint32_t D_SMEM_BYTES = D_OFF_SM + D_SMALL * 4 + 1024;
 
 struct TcDivArgs {
@@ -81,9 +82,10 @@ struct Acc {
 // keeps the four rows' X windows in registers and slides them 4 terms per
 // 16-byte load; W[t] is a broadcast.  part[p * n + i] = partial, reduced.
 __device__ __forceinline__ void toeplitz_partials(const uint32_t* X, const uint32_t* W, int n,
-                                                  int T, uint32_t* part, const FieldParams& F) {
+                                                  int T, uint32_t* part, const FieldParams& F,
+                                                  int tid = -1) {
     const int ng = n >> 2, np = T >> 4;
-    const int tid = threadIdx.x;
+    if (tid < 0) tid = threadIdx.x;
     if (tid >= ng * np) return;
     const int g = tid % ng, p = tid / ng, r0 = 4 * g, t0 = 16 * p;
     uint4 cv = *reinterpret_cast<const uint4*>(X + r0 - t0);
@@ -168,6 +170,41 @@ __device__ __forceinline__ uint32_t partials_sum(const uint32_t* part, int n, in
     return reduce(v, F);
 }
 
+// h = B'^-1 mod X^128 by Newton doubling (h_{2k} = h_k - X^k (h_k e mod X^k),
+// e = coefficients [k, 2k) of B' h_k), by the `nt` threads of a group (local id
+// ltid) synchronised by `sync`.  bp: B'[0..256); hs: 128 zeros before h.
+template <class Sync>
+__device__ __forceinline__ void newton_inverse(const uint32_t* bp, uint32_t* hs, uint32_t* part,
+                                               uint32_t* tmp, int ltid, const FieldParams& F,
+                                               Sync sync) {
+    if (ltid == 0) hs[0] = invmod(bp[0], F);
+    sync();
+    for (int k = 1; k < 16; k <<= 1) {
+        if (ltid < k) {
+            Acc e;
+            for (int m = 0; m < k; ++m) e.add(bp[k + ltid - m], hs[m], F);
+            tmp[ltid] = reduce(e.v, F);
+        }
+        sync();
+        if (ltid < k) {
+            Acc q;
+            for (int m = 0; m <= ltid; ++m) q.add(hs[ltid - m], tmp[m], F);
+            hs[k + ltid] = negmod(reduce(q.v, F), F);
+        }
+        sync();
+    }
+    for (int k = 16; k < 128; k <<= 1) {  // the same doubling with sliding products
+        toeplitz_partials(bp + k, hs, k, k, part, F, ltid);
+        sync();
+        if (ltid < k) tmp[ltid] = partials_sum(part, k, k, ltid, F);
+        sync();
+        toeplitz_partials(hs, tmp, k, k, part, F, ltid);  // h[i-m], zero for i < m
+        sync();
+        if (ltid < k) hs[k + ltid] = negmod(partials_sum(part, k, k, ltid, F), F);
+        sync();
+    }
+}
+
 __device__ long long tcd_stats[8];
 #define TCD_T0() const long long _t0 = clock64()
 #define TCD_ACC(i) st[i] += clock64() - _t0
@@ -182,12 +219,15 @@ __global__ void __launch_bounds__(TCD_T + TCD_BLD + 32, 1) tcdiv_kernel(TcDivArg
     uint32_t* q_pad = reinterpret_cast<uint32_t*>(sm + D_OFF_Q);
     uint32_t* qz = q_pad + TCD_QPAD;                               // Q[0] (Q[-256..-1] = 0)
     uint32_t* bp01 = reinterpret_cast<uint32_t*>(sm + D_OFF_SM);  // B'[0..256)
-    uint32_t* hs = bp01 + 256 + 128;                              // B'^-1 mod X^128, 128 zeros before
-    uint32_t* sS = hs + 128;                                      // planes' block K+1
+    uint32_t* hsp = bp01 + 256;                                   // [2][256]: 128 zeros, then h
+    uint32_t* sS = hsp + 512;                                     // planes' block K+1
     uint32_t* sE = sS + 128;
     uint32_t* part = sE + 128;                                    // [8][128] partial sums
     uint32_t* tmp = part + 1024;
-    __shared__ uint64_t full[2], empty[2], qready[2], built[2];
+    uint32_t* bpB = tmp + 128;                                    // builders: next B'[0..256)
+    uint32_t* partB = bpB + 256;
+    uint32_t* tmpB = partB + 1024;
+    __shared__ uint64_t full[2], empty[2], qready[2], built[2], hready;
     __shared__ uint32_t tslot;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const FieldParams F = g.Fp;
@@ -199,7 +239,10 @@ __global__ void __launch_bounds__(TCD_T + TCD_BLD + 32, 1) tcdiv_kernel(TcDivArg
     for (uint32_t i = tid; i < B_BYTES / 16; i += TCD_ALL)
         reinterpret_cast<uint4*>(sm + D_OFF_B)[i] = make_uint4(0, 0, 0, 0);
     for (int i = tid; i < TCD_QWORDS; i += TCD_ALL) q_pad[i] = 0;
-    for (int i = tid; i < 128; i += TCD_ALL) hs[i - 128] = 0;
+    for (int i = tid; i < 128; i += TCD_ALL) {
+        hsp[i] = 0;
+        hsp[256 + i] = 0;
+    }
     if (warp == 0) tc::tmem_alloc<512>(&tslot);
     if (tid == 0) {
         for (int b = 0; b < 2; ++b) {
@@ -208,6 +251,7 @@ __global__ void __launch_bounds__(TCD_T + TCD_BLD + 32, 1) tcdiv_kernel(TcDivArg
             tc::mbar_init(&qready[b], 1);
             tc::mbar_init(&built[b], 1);
         }
+        tc::mbar_init(&hready, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     tc::fence_before_sync();
@@ -218,10 +262,23 @@ __global__ void __launch_bounds__(TCD_T + TCD_BLD + 32, 1) tcdiv_kernel(TcDivArg
     if (warp >= TCD_T / 32 && warp < (TCD_T + TCD_BLD) / 32) {
         // ---- builder warps: tile K (Q_K lower, Q_{K-1} upper) into buffer T & 1,
         //      while the compute warps run the next step's correction product ----
+        // They also compute h = B'^-1 mod X^128 of the instance after the
+        // current one while the compute warps finish it (the first instance:
+        // up front), into the other half of the h ping-pong.
         const int bt = tid - TCD_T;
         uint32_t qph[2] = {0, 0}, eph[2] = {0, 0};
         uint32_t T = 0;
-        for (int64_t inst = blockIdx.x; inst < g.count; inst += gridDim.x)
+        auto bsync = [] { asm volatile("bar.sync 2, 128;" ::: "memory"); };
+        auto inverse_of = [&](int64_t which, int slot) {
+            const uint32_t* bb = g.B + which * g.ldb;
+            for (int t = bt; t < 256; t += TCD_BLD) bpB[t] = t < nb ? __ldg(bb + (nb - 1 - t)) : 0u;
+            bsync();
+            newton_inverse(bpB, hsp + 256 * slot + 128, partB, tmpB, bt, F, bsync);
+            if (bt == 0) tc::mbar_arrive(&hready);
+        };
+        int ip = 0;
+        for (int64_t inst = blockIdx.x; inst < g.count; inst += gridDim.x, ++ip) {
+            if (ip == 0) inverse_of(inst, 0);
             for (int K = 0; K <= Kq; ++K, ++T) {
                 const int b = T & 1;
                 tc::mbar_wait(&qready[b], qph[b]);  // Q_K (and Q_{K-1}) published
@@ -235,9 +292,11 @@ __global__ void __launch_bounds__(TCD_T + TCD_BLD + 32, 1) tcdiv_kernel(TcDivArg
                 for (int i = 0; i < 2; ++i)
                     build_unit(sH + b * HBUF, qz - TCM_APAD, K, 4 * (wb + 4 * i) + (L >> 3), L & 7);
                 tc::fence_async_smem();
-                asm volatile("bar.sync 2, 128;" ::: "memory");
+                bsync();
                 if (bt == 0) tc::mbar_arrive(&built[b]);
             }
+            if (inst + gridDim.x < g.count) inverse_of(inst + gridDim.x, (ip + 1) & 1);
+        }
     } else if (warp == (TCD_T + TCD_BLD) / 32) {
         // ---- MMA warp: tile K of each instance from buffer T & 1 ----
         constexpr uint32_t ID_E = tc::idesc_u8(128, BROWS_E), ID_O = tc::idesc_u8(128, BROWS_O);
@@ -266,8 +325,9 @@ __global__ void __launch_bounds__(TCD_T + TCD_BLD + 32, 1) tcdiv_kernel(TcDivArg
                 __syncwarp();
             }
     } else {
-        uint32_t eph[2] = {0, 0}, bph[2] = {0, 0};
+        uint32_t eph[2] = {0, 0}, bph[2] = {0, 0}, hph = 0;
         int pend[2] = {0, 0};
+        int ip = 0;
         uint32_t T = 0;
         auto free_buf = [&](int b) {
             if (pend[b]) {
@@ -279,7 +339,7 @@ __global__ void __launch_bounds__(TCD_T + TCD_BLD + 32, 1) tcdiv_kernel(TcDivArg
         auto bar = [] { asm volatile("bar.sync 1, 256;" ::: "memory"); };
         const uint32_t lane_addr = tbase + (uint32_t(32 * (warp & 3)) << 16);
         long long st[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        for (int64_t inst = blockIdx.x; inst < g.count; inst += gridDim.x) {
+        for (int64_t inst = blockIdx.x; inst < g.count; inst += gridDim.x, ++ip) {
             const uint32_t* a = g.A + inst * g.lda;
             const uint32_t* b = g.B + inst * g.ldb;
             long long tp = clock64();
@@ -322,34 +382,10 @@ __global__ void __launch_bounds__(TCD_T + TCD_BLD + 32, 1) tcdiv_kernel(TcDivArg
             bar();
             st[0] += clock64() - tp;
             tp = clock64();
-            // ---- h = B'^-1 mod X^128 by Newton doubling ----
-            if (tid == 0) hs[0] = invmod(bp01[0], F);
-            bar();
-            for (int k = 1; k < 16; k <<= 1) {
-                // e[i] = sum_{m<k} B'[k+i-m] h[m]  (i < k): coefficients [k, 2k) of B' h_k
-                if (tid < k) {
-                    Acc e;
-                    for (int m = 0; m < k; ++m) e.add(bp01[k + tid - m], hs[m], F);
-                    tmp[tid] = reduce(e.v, F);
-                }
-                bar();
-                if (tid < k) {  // h[k+i] = -sum_{m<=i} h[i-m] e[m]
-                    Acc s;
-                    for (int m = 0; m <= tid; ++m) s.add(hs[tid - m], tmp[m], F);
-                    hs[k + tid] = negmod(reduce(s.v, F), F);
-                }
-                bar();
-            }
-            for (int k = 16; k < 128; k <<= 1) {  // the same doubling with sliding products
-                toeplitz_partials(bp01 + k, hs, k, k, part, F);
-                bar();
-                if (tid < k) tmp[tid] = partials_sum(part, k, k, tid, F);
-                bar();
-                toeplitz_partials(hs, tmp, k, k, part, F);  // h[i-m], zero for i < m
-                bar();
-                if (tid < k) hs[k + tid] = negmod(partials_sum(part, k, k, tid, F), F);
-                bar();
-            }
+            // ---- h = B'^-1 mod X^128: computed by the builder warps ----
+            tc::mbar_wait(&hready, hph);
+            hph ^= 1;
+            const uint32_t* hs = hsp + 256 * (ip & 1) + 128;
             st[1] += clock64() - tp;
 
             // Step K: Q_K from block K of A' - sum_{I<K} Q_I X^(128 I) B', where the
@@ -429,21 +465,25 @@ __global__ void __launch_bounds__(TCD_T + TCD_BLD + 32, 1) tcdiv_kernel(TcDivArg
             free_buf(0);
             free_buf(1);
             tc::fence_after_sync();
-            // r[na-1-k] = A'[k] - (Q B')[k], k in [mu, na)
+            // r[na-1-k] = A'[k] - (Q B')[k], k in [mu, na): 8 blocks per TMEM load
             {
                 const int r = 32 * (warp & 3) + lane;
                 const int cfirst = mu >> 7, clast = (na - 1) >> 7;
                 const int64_t rb = inst * g.ldr;
-                for (int c = cfirst + (warp >> 2); c <= clast; c += 2) {
-                    uint32_t x[7];
+                for (int c0 = cfirst + 8 * (warp >> 2); c0 <= clast; c0 += 16) {
+                    uint32_t x[7][8];
 #pragma unroll
-                    for (int s = 0; s < 7; ++s) x[s] = tmem_ld1(lane_addr + 64 * s + c);
+                    for (int s = 0; s < 7; ++s) tmem_ld8(lane_addr + 64 * s + c0, x[s]);
                     tc::tmem_ld_wait();
-                    const int k = 128 * c + r;
-                    if (k >= mu && k < na) {
-                        const uint32_t S = combine_planes(x, g.c_hi, F);
-                        fan_store<FAN>(g.R, rb + (na - 1 - k),
-                                       submod(__ldg(a + (na - 1 - k)), S, F));
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        const int k = 128 * (c0 + e) + r;
+                        if (k >= mu && k < na) {
+                            const uint32_t xs[7] = {x[0][e], x[1][e], x[2][e], x[3][e], x[4][e],
+                                                    x[5][e], x[6][e]};
+                            fan_store<FAN>(g.R, rb + (na - 1 - k),
+                                           submod(__ldg(a + (na - 1 - k)), combine_planes(xs, g.c_hi, F), F));
+                        }
                     }
                 }
             }
