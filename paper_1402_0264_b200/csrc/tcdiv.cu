@@ -173,13 +173,15 @@ __device__ __forceinline__ uint32_t partials_sum(const uint32_t* part, int n, in
 // h = B'^-1 mod X^128 by Newton doubling (h_{2k} = h_k - X^k (h_k e mod X^k),
 // e = coefficients [k, 2k) of B' h_k), by the `nt` threads of a group (local id
 // ltid) synchronised by `sync`.  bp: B'[0..256); hs: 128 zeros before h.
+// One doubling h_k -> h_{2k} (k = 1, 2, ..., 64; h[0] set before k = 1) by the
+// `nt` threads of a group (local id ltid) synchronised by `sync`:
+// h_{2k} = h_k - X^k (h_k e mod X^k), e = coefficients [k, 2k) of B' h_k.
+// bp: B'[0..256); hs: 128 zeros before h.
 template <class Sync>
-__device__ __forceinline__ void newton_inverse(const uint32_t* bp, uint32_t* hs, uint32_t* part,
-                                               uint32_t* tmp, int ltid, const FieldParams& F,
-                                               Sync sync) {
-    if (ltid == 0) hs[0] = invmod(bp[0], F);
-    sync();
-    for (int k = 1; k < 16; k <<= 1) {
+__device__ __forceinline__ void newton_step(const uint32_t* bp, uint32_t* hs, uint32_t* part,
+                                            uint32_t* tmp, int ltid, const FieldParams& F, int k,
+                                            Sync sync) {
+    if (k < 16) {
         if (ltid < k) {
             Acc e;
             for (int m = 0; m < k; ++m) e.add(bp[k + ltid - m], hs[m], F);
@@ -192,17 +194,16 @@ __device__ __forceinline__ void newton_inverse(const uint32_t* bp, uint32_t* hs,
             hs[k + ltid] = negmod(reduce(q.v, F), F);
         }
         sync();
+        return;
     }
-    for (int k = 16; k < 128; k <<= 1) {  // the same doubling with sliding products
-        toeplitz_partials(bp + k, hs, k, k, part, F, ltid);
-        sync();
-        if (ltid < k) tmp[ltid] = partials_sum(part, k, k, ltid, F);
-        sync();
-        toeplitz_partials(hs, tmp, k, k, part, F, ltid);  // h[i-m], zero for i < m
-        sync();
-        if (ltid < k) hs[k + ltid] = negmod(partials_sum(part, k, k, ltid, F), F);
-        sync();
-    }
+    toeplitz_partials(bp + k, hs, k, k, part, F, ltid);  // sliding products
+    sync();
+    if (ltid < k) tmp[ltid] = partials_sum(part, k, k, ltid, F);
+    sync();
+    toeplitz_partials(hs, tmp, k, k, part, F, ltid);  // h[i-m], zero for i < m
+    sync();
+    if (ltid < k) hs[k + ltid] = negmod(partials_sum(part, k, k, ltid, F), F);
+    sync();
 }
 
 __device__ long long tcd_stats[8];
@@ -269,16 +270,26 @@ __global__ void __launch_bounds__(TCD_T + TCD_BLD + 32, 1) tcdiv_kernel(TcDivArg
         uint32_t qph[2] = {0, 0}, eph[2] = {0, 0};
         uint32_t T = 0;
         auto bsync = [] { asm volatile("bar.sync 2, 128;" ::: "memory"); };
-        auto inverse_of = [&](int64_t which, int slot) {
+        // B'[0..256) of instance `which` into bpB and h[0] of its inverse
+        auto inverse_begin = [&](int64_t which, uint32_t* hsn) {
             const uint32_t* bb = g.B + which * g.ldb;
             for (int t = bt; t < 256; t += TCD_BLD) bpB[t] = t < nb ? __ldg(bb + (nb - 1 - t)) : 0u;
             bsync();
-            newton_inverse(bpB, hsp + 256 * slot + 128, partB, tmpB, bt, F, bsync);
-            if (bt == 0) tc::mbar_arrive(&hready);
+            if (bt == 0) hsn[0] = invmod(bpB[0], F);
+            bsync();
         };
         int ip = 0;
         for (int64_t inst = blockIdx.x; inst < g.count; inst += gridDim.x, ++ip) {
-            if (ip == 0) inverse_of(inst, 0);
+            uint32_t* hsn = hsp + 256 * ((ip + 1) & 1) + 128;  // the next instance's h
+            const bool next = inst + gridDim.x < g.count;
+            if (ip == 0) {  // the first instance's inverse, up front
+                uint32_t* hs0 = hsp + 128;
+                inverse_begin(inst, hs0);
+                for (int k = 1; k < 128; k <<= 1) newton_step(bpB, hs0, partB, tmpB, bt, F, k, bsync);
+                if (bt == 0) tc::mbar_arrive(&hready);
+            }
+            if (next) inverse_begin(inst + gridDim.x, hsn);
+            int kn = 1;  // the next instance's Newton: one doubling after each tile
             for (int K = 0; K <= Kq; ++K, ++T) {
                 const int b = T & 1;
                 tc::mbar_wait(&qready[b], qph[b]);  // Q_K (and Q_{K-1}) published
@@ -294,8 +305,16 @@ __global__ void __launch_bounds__(TCD_T + TCD_BLD + 32, 1) tcdiv_kernel(TcDivArg
                 tc::fence_async_smem();
                 bsync();
                 if (bt == 0) tc::mbar_arrive(&built[b]);
+                if (next && kn < 128) {
+                    newton_step(bpB, hsn, partB, tmpB, bt, F, kn, bsync);
+                    kn <<= 1;
+                    if (kn == 128 && bt == 0) tc::mbar_arrive(&hready);
+                }
             }
-            if (inst + gridDim.x < g.count) inverse_of(inst + gridDim.x, (ip + 1) & 1);
+            if (next && kn < 128) {  // short instances: finish the doublings
+                for (; kn < 128; kn <<= 1) newton_step(bpB, hsn, partB, tmpB, bt, F, kn, bsync);
+                if (bt == 0) tc::mbar_arrive(&hready);
+            }
         }
     } else if (warp == (TCD_T + TCD_BLD) / 32) {
         // ---- MMA warp: tile K of each instance from buffer T & 1 ----
