@@ -42,6 +42,13 @@ __host__ __device__ constexpr uint32_t idesc_u8(int M, int N) {
            | (uint32_t(M >> 4) << 24);  // m_dim
 }
 
+// The first 1024-aligned byte of a dynamic shared-memory array, by pointer
+// arithmetic on the array itself: a round trip through an integer would make
+// every access through the result a generic LD/ST instead of LDS/STS.
+__device__ __forceinline__ uint8_t* align_smem_1024(uint8_t* raw) {
+    return raw + ((1024u - (smem_u32(raw) & 1023u)) & 1023u);
+}
+
 // D[tmem] (+)= A[smem] . B[smem]^T, issued by one thread.
 __device__ __forceinline__ void mma_u8(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
                                        uint32_t accumulate) {

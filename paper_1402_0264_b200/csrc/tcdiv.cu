@@ -213,8 +213,7 @@ __device__ long long tcd_stats[8];
 template <bool FAN>
 __global__ void __launch_bounds__(TCD_T + TCD_BLD + 32, 1) tcdiv_kernel(TcDivArgs g) {
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+    uint8_t* sm = tc::align_smem_1024(smem_raw);
     uint8_t* sH = sm + D_OFF_H;
     uint8_t* sBE = sm + D_OFF_B + B_PRE;
     uint32_t* q_pad = reinterpret_cast<uint32_t*>(sm + D_OFF_Q);

@@ -35,15 +35,21 @@ idx = {h: i for i, h in enumerate(hdr)}
 data = rows[2:]
 base = min(int(r[idx["Address"]], 16) for r in data)
 S, X = "Warp Stall Sampling (All Samples)", "L1 Wavefronts Shared Excessive"
-agg, exc = {}, {}
+REASONS = [h for h in hdr if h.startswith("stall_") and "Not Issued" not in h]
+agg, exc, why = {}, {}, {}
 for r in data:
     k = off2line.get(int(r[idx["Address"]], 16) - base, ("?", 0))
     agg[k] = agg.get(k, 0) + float(r[idx[S]] or 0)
     exc[k] = exc.get(k, 0) + float(r[idx[X]] or 0)
+    w = why.setdefault(k, {})
+    for h in REASONS:
+        w[h] = w.get(h, 0) + float(r[idx[h]] or 0)
 tot = sum(agg.values())
 print(f"stall samples {tot:.0f}")
 for k, v in sorted(agg.items(), key=lambda x: -x[1])[:top]:
-    print(f"  {k[0]}:{k[1]:5d}  {v:8.0f}  {100 * v / tot:5.1f}%")
+    rs = sorted(why[k].items(), key=lambda x: -x[1])[:3]
+    rtxt = " ".join(f"{h[6:]}={100 * c / max(v, 1):.0f}%" for h, c in rs if c)
+    print(f"  {k[0]}:{k[1]:5d}  {v:8.0f}  {100 * v / tot:5.1f}%  {rtxt}")
 print("excessive shared wavefronts")
 for k, v in sorted(exc.items(), key=lambda x: -x[1])[:10]:
     if v:
