@@ -72,6 +72,16 @@ __device__ __forceinline__ uint32_t reduce(uint64_t x, const FieldParams& F) {
     return redc(uint64_t(y) * F.r2, F);
 }
 
+// reduce() for odd p known at compile time of the caller (no p = 2 branch)
+__device__ __forceinline__ uint32_t reduce_odd(uint64_t x, const FieldParams& F) {
+    uint32_t y = redc(fold(x, F), F);
+    return redc(uint64_t(y) * F.r2, F);
+}
+template <bool ODD>
+__device__ __forceinline__ uint32_t reduce_t(uint64_t x, const FieldParams& F) {
+    return ODD ? reduce_odd(x, F) : reduce(x, F);
+}
+
 __device__ __forceinline__ uint32_t mulmod(uint32_t a, uint32_t b, const FieldParams& F) {
     return reduce(uint64_t(a) * b, F);
 }

@@ -39,7 +39,7 @@ using namespace tct;
 
 constexpr int TCD_T = 256;    // compute warps 0-7: the per-step solve
 constexpr int TCD_BLD = 128;  // builder warps 8-11: the tiles
-constexpr int TCD_ALL = TCD_T + TCD_BLD + 32;  // + the MMA warp
+constexpr int TCD_ALL = TCD_T + TCD_BLD;  // twelve warps: three per SMSP, up to 168 registers
 constexpr int TCD_MAXA = 8192;
 constexpr int TCD_QPAD = 256;                           // zero words before Q
 constexpr int TCD_QWORDS = TCD_QPAD + TCD_MAXA + 256;   // Q, padded
@@ -48,8 +48,9 @@ constexpr uint32_t D_OFF_H = 0;                           // two H buffers (4 li
 constexpr uint32_t D_OFF_B = D_OFF_H + 2 * HBUF;          // B_PRE | 240 rows (tctile.cuh)
 constexpr uint32_t D_OFF_Q = D_OFF_B + B_BYTES;           // u32 Q (padded)
 constexpr uint32_t D_OFF_SM = D_OFF_Q + TCD_QWORDS * 4;   // small arrays
-constexpr uint32_t D_SMALL = 256 + 2 * 256 + 128 + 128 + 1024 + 128 + 256 + 1024 + 128;
-// B'[0..256), h ping-pong (each: 128 zeros, h), S, E, parts, tmp | builders: B'[0..256), parts, tmp
+constexpr uint32_t D_SMALL = 256 + 2 * 256 + 128 + 128 + 1024 + 128 + 256 + 1024 + 128 + 256 + 128 + 1024;
+// B'[0..256), h ping-pong (each: 128 zeros, h), S, E, parts, tmp | builders: B'[0..256), parts,
+// tmp, B'[128..256) + 128 zeros, the late correction of the next block, its partials [8][128]
 constexpr uint32_t D_SMEM_BYTES = D_OFF_SM + D_SMALL * 4 + 1024;
 
 struct TcDivArgs {
@@ -81,6 +82,8 @@ struct Acc {
 // [-T, n)).  Thread (row group g: rows 4g..4g+3, t-part p: t in [16p, 16p+16))
 // keeps the four rows' X windows in registers and slides them 4 terms per
 // 16-byte load; W[t] is a broadcast.  part[p * n + i] = partial, reduced.
+// FAST: odd p with fold_terms >= 16 (no folds inside the 16-term blocks, no p = 2 branch).
+template <bool FAST = false>
 __device__ __forceinline__ void toeplitz_partials(const uint32_t* X, const uint32_t* W, int n,
                                                   int T, uint32_t* part, const FieldParams& F,
                                                   int tid = -1) {
@@ -104,10 +107,10 @@ __device__ __forceinline__ void toeplitz_partials(const uint32_t* X, const uint3
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 acc[k] = mad_wide(z[4 + k - jj], w4[jj], acc[k]);
-                if (ft < 4) acc[k] = fold(acc[k], F);
+                if (!FAST && ft < 4) acc[k] = fold(acc[k], F);
             }
         }
-        if (ft >= 4 && ft < 16)
+        if (!FAST && ft >= 4 && ft < 16)
 #pragma unroll
             for (int k = 0; k < 4; ++k) acc[k] = fold(acc[k], F);
         cur[0] = nv.x;
@@ -116,7 +119,7 @@ __device__ __forceinline__ void toeplitz_partials(const uint32_t* X, const uint3
         cur[3] = nv.w;
     }
 #pragma unroll
-    for (int k = 0; k < 4; ++k) part[p * n + r0 + k] = reduce(acc[k], F);
+    for (int k = 0; k < 4; ++k) part[p * n + r0 + k] = reduce_t<FAST>(acc[k], F);
 }
 
 // n = T = 128 rows / terms twice: part = partials of
@@ -163,11 +166,12 @@ __device__ __forceinline__ void toeplitz_partials_256(const uint32_t* X, const u
 }
 
 // y[i] = sum over the T/16 partials, mod p (threads i < n).
+template <bool FAST = false>
 __device__ __forceinline__ uint32_t partials_sum(const uint32_t* part, int n, int T, int i,
                                                  const FieldParams& F) {
     uint64_t v = 0;
     for (int p = 0; p < (T >> 4); ++p) v += part[p * n + i];
-    return reduce(v, F);
+    return reduce_t<FAST>(v, F);
 }
 
 // h = B'^-1 mod X^128 by Newton doubling (h_{2k} = h_k - X^k (h_k e mod X^k),
@@ -206,12 +210,18 @@ __device__ __forceinline__ void newton_step(const uint32_t* bp, uint32_t* hs, ui
     sync();
 }
 
-__device__ long long tcd_stats[8];
-#define TCD_T0() const long long _t0 = clock64()
-#define TCD_ACC(i) st[i] += clock64() - _t0
+__device__ long long tcd_stats[16];
+// Phase clocks (CTA 0) for tuning: build with -DTCD_STATS=1 and run with MMM_TC_STATS=1.
+#ifndef TCD_STATS
+#define TCD_STATS 0
+#endif
+__device__ __forceinline__ long long tcd_clock() { return TCD_STATS ? clock64() : 0; }
+#define TCD_T0() const long long _t0 = tcd_clock()
+#define TCD_ACC(i) \
+    if (TCD_STATS) st[i] += clock64() - _t0
 
-template <bool FAN>
-__global__ void __launch_bounds__(TCD_T + TCD_BLD + 32, 1) tcdiv_kernel(TcDivArgs g) {
+template <bool FAN, bool FAST>
+__global__ void __maxnreg__(168) tcdiv_kernel(TcDivArgs g) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* sm = tc::align_smem_1024(smem_raw);
     uint8_t* sH = sm + D_OFF_H;
@@ -227,7 +237,11 @@ __global__ void __launch_bounds__(TCD_T + TCD_BLD + 32, 1) tcdiv_kernel(TcDivArg
     uint32_t* bpB = tmp + 128;                                    // builders: next B'[0..256)
     uint32_t* partB = bpB + 256;
     uint32_t* tmpB = partB + 1024;
-    __shared__ uint64_t full[2], empty[2], qready[2], built[2], hready;
+    uint32_t* bnc = tmpB + 128;  // B'[128..256), then 128 zeros
+    uint32_t* lateb = bnc + 256;  // L_{K+1} (see step K)
+    uint32_t* partL = lateb + 128;  // [8][128] partials of L_{K+2}
+    __shared__ uint64_t full[2], empty[2], qready[2], hready;
+    __shared__ long long issue_ts[2];
     __shared__ uint32_t tslot;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const FieldParams F = g.Fp;
@@ -249,7 +263,6 @@ __global__ void __launch_bounds__(TCD_T + TCD_BLD + 32, 1) tcdiv_kernel(TcDivArg
             tc::mbar_init(&full[b], 1);
             tc::mbar_init(&empty[b], 1);
             tc::mbar_init(&qready[b], 1);
-            tc::mbar_init(&built[b], 1);
         }
         tc::mbar_init(&hready, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -266,7 +279,9 @@ __global__ void __launch_bounds__(TCD_T + TCD_BLD + 32, 1) tcdiv_kernel(TcDivArg
         // current one while the compute warps finish it (the first instance:
         // up front), into the other half of the h ping-pong.
         const int bt = tid - TCD_T;
-        uint32_t qph[2] = {0, 0}, eph[2] = {0, 0};
+        uint32_t qph[2] = {0, 0}, eph[2] = {0, 0}, fph[2] = {0, 0};
+        long long bst[4] = {0, 0, 0, 0};
+        constexpr uint32_t ID_E = tc::idesc_u8(128, BROWS_E), ID_O = tc::idesc_u8(128, BROWS_O);
         uint32_t T = 0;
         auto bsync = [] { asm volatile("bar.sync 2, 128;" ::: "memory"); };
         // B'[0..256) of instance `which` into bpB and h[0] of its inverse
@@ -291,42 +306,28 @@ __global__ void __launch_bounds__(TCD_T + TCD_BLD + 32, 1) tcdiv_kernel(TcDivArg
             int kn = 1;  // the next instance's Newton: one doubling after each tile
             for (int K = 0; K <= Kq; ++K, ++T) {
                 const int b = T & 1;
+                long long tb = tcd_clock();
                 tc::mbar_wait(&qready[b], qph[b]);  // Q_K (and Q_{K-1}) published
                 qph[b] ^= 1;
                 if (T >= 2) {  // the buffer's previous tile (T - 2) is done
                     tc::mbar_wait(&empty[b], eph[b]);
                     eph[b] ^= 1;
                 }
+                bst[0] += tcd_clock() - tb;
+                tb = tcd_clock();
                 const int wb = bt >> 5, L = bt & 31;
 #pragma unroll
                 for (int i = 0; i < 2; ++i)
                     build_unit(sH + b * HBUF, qz - TCM_APAD, K, 4 * (wb + 4 * i) + (L >> 3), L & 7);
                 tc::fence_async_smem();
                 bsync();
-                if (bt == 0) tc::mbar_arrive(&built[b]);
-                if (next && kn < 128) {
-                    newton_step(bpB, hsn, partB, tmpB, bt, F, kn, bsync);
-                    kn <<= 1;
-                    if (kn == 128 && bt == 0) tc::mbar_arrive(&hready);
-                }
-            }
-            if (next && kn < 128) {  // short instances: finish the doublings
-                for (; kn < 128; kn <<= 1) newton_step(bpB, hsn, partB, tmpB, bt, F, kn, bsync);
-                if (bt == 0) tc::mbar_arrive(&hready);
-            }
-        }
-    } else if (warp == (TCD_T + TCD_BLD) / 32) {
-        // ---- MMA warp: tile K of each instance from buffer T & 1 ----
-        constexpr uint32_t ID_E = tc::idesc_u8(128, BROWS_E), ID_O = tc::idesc_u8(128, BROWS_O);
-        uint32_t fph[2] = {0, 0};
-        uint32_t T = 0;
-        for (int64_t inst = blockIdx.x; inst < g.count; inst += gridDim.x)
-            for (int K = 0; K <= Kq; ++K, ++T) {
-                const int b = T & 1;
-                tc::mbar_wait(&full[b], fph[b]);
-                fph[b] ^= 1;
-                tc::fence_after_sync();
-                if (lane == 0) {
+                bst[1] += tcd_clock() - tb;
+                tb = tcd_clock();
+                if (bt == 0) {
+                    // tile K's MMAs, once the compute warps have read block K+1 of the
+                    // planes (tile K must not land before that read)
+                    tc::mbar_wait(&full[b], fph[b]);
+                    tc::fence_after_sync();
                     const uint32_t hb = tc::smem_u32(sH + b * HBUF);
                     const bool odd = K & 1;
                     const uint32_t bb = tc::smem_u32(sBE) - (odd ? 128u : 0u);
@@ -339,15 +340,31 @@ __global__ void __launch_bounds__(TCD_T + TCD_BLD + 32, 1) tcdiv_kernel(TcDivArg
                             tc::mma_u8(tbase + 64 * u + col, tc::desc_sw128(hb + u * TILE + 32 * k),
                                        tc::desc_sw128(bb + 32 * k), idesc, 1u);
                     tc::commit(&empty[b]);
+                    issue_ts[b] = tcd_clock();
                 }
-                __syncwarp();
+                fph[b] ^= 1;
+                bst[2] += tcd_clock() - tb;
+                tb = tcd_clock();
+                if (next && kn < 128) {
+                    newton_step(bpB, hsn, partB, tmpB, bt, F, kn, bsync);
+                    kn <<= 1;
+                    if (kn == 128 && bt == 0) tc::mbar_arrive(&hready);
+                }
+                bst[3] += tcd_clock() - tb;
             }
+            if (next && kn < 128) {  // short instances: finish the doublings
+                for (; kn < 128; kn <<= 1) newton_step(bpB, hsn, partB, tmpB, bt, F, kn, bsync);
+                if (bt == 0) tc::mbar_arrive(&hready);
+            }
+        }
+        if (blockIdx.x == 0 && bt == 0)
+            for (int i = 0; i < 4; ++i) tcd_stats[8 + i] = bst[i];
     } else {
-        uint32_t eph[2] = {0, 0}, bph[2] = {0, 0}, hph = 0;
+        uint32_t eph[2] = {0, 0}, hph = 0;
         int pend[2] = {0, 0};
         int ip = 0;
         uint32_t T = 0;
-        auto free_buf = [&](int b) {
+        auto free_buf = [&](int b) {  // the tile handed off in buffer b is done
             if (pend[b]) {
                 tc::mbar_wait(&empty[b], eph[b]);
                 eph[b] ^= 1;
@@ -356,11 +373,11 @@ __global__ void __launch_bounds__(TCD_T + TCD_BLD + 32, 1) tcdiv_kernel(TcDivArg
         };
         auto bar = [] { asm volatile("bar.sync 1, 256;" ::: "memory"); };
         const uint32_t lane_addr = tbase + (uint32_t(32 * (warp & 3)) << 16);
-        long long st[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        long long st[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
         for (int64_t inst = blockIdx.x; inst < g.count; inst += gridDim.x, ++ip) {
             const uint32_t* a = g.A + inst * g.lda;
             const uint32_t* b = g.B + inst * g.ldb;
-            long long tp = clock64();
+            long long tp = tcd_clock();
             // ---- B' operand (rows 64 v + j), B'[0..256), zero TMEM, S_0 = 0 ----
             for (int u = tid; u < mB * 8; u += TCD_T) {
                 const int j = u >> 3, c = u & 7;
@@ -387,6 +404,7 @@ __global__ void __launch_bounds__(TCD_T + TCD_BLD + 32, 1) tcdiv_kernel(TcDivArg
                     sts128(sBE, tc::sw128(64 * v + j, 16 * c), L[v][0], L[v][1], L[v][2], L[v][3]);
             }
             bp01[tid] = tid < nb ? __ldg(b + (nb - 1 - tid)) : 0u;
+            bnc[tid] = (tid < 128 && 128 + tid < nb) ? __ldg(b + (nb - 129 - tid)) : 0u;
             if (tid < 128) {
                 sS[tid] = 0;
                 qz[tid] = 0;  // Q block 0 (a previous instance's values)
@@ -398,97 +416,232 @@ __global__ void __launch_bounds__(TCD_T + TCD_BLD + 32, 1) tcdiv_kernel(TcDivArg
                 asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             }
             bar();
-            st[0] += clock64() - tp;
-            tp = clock64();
+            st[0] += tcd_clock() - tp;
+            tp = tcd_clock();
             // ---- h = B'^-1 mod X^128: computed by the builder warps ----
             tc::mbar_wait(&hready, hph);
             hph ^= 1;
             const uint32_t* hs = hsp + 256 * (ip & 1) + 128;
-            st[1] += clock64() - tp;
+            st[1] += tcd_clock() - tp;
+            tp = tcd_clock();
 
-            // Step K: Q_K from block K of A' - sum_{I<K} Q_I X^(128 I) B', where the
-            // planes hold tiles <= K-2 (read into sS before tile K-1 was handed
-            // off) and the tiles K-1 (against B'_1) and K (against B'_0) that Q
-            // blocks < K determine come from one 256-term product on the CUDA
-            // cores; the MMA warp runs tile K-1 meanwhile.
-            // corr_0 = 0 (no quotient block yet)
-            for (int i = tid; i < 1024; i += TCD_T) part[i] = 0;
+            // ---- the step matrix M = T_h T_B1 (see the header), negated, into registers ----
+            // u[r] = M[r][0] = sum_{t <= r} h[r - t] B'[128 + t]
+            // (FAST: M is kept in Montgomery form, M 2^32 mod p, so that each entry and
+            // each phase-A partial costs one REDC: the walk runs on B' 2^64 mod p)
+            toeplitz_partials<FAST>(hs, bnc, 128, 128, part, F);
+            uint32_t* bw = sE;  // B'[k] (2^64 mod p when FAST), k < 128
+            if (tid < 128) bw[tid] = FAST ? reduce_odd(uint64_t(bp01[tid]) * F.r2, F) : bp01[tid];
             bar();
+            if (tid < 128) {
+                const uint32_t u = partials_sum<FAST>(part, 128, 128, tid, F);
+                tmp[tid] = FAST ? reduce_odd(uint64_t(u) * F.r2, F) : u;
+            }
+            bar();
+            {
+                // diagonal r - m = dl of M, walked from its first entry with
+                // M[r][m] = M[r-1][m-1] + h[r] B'[128 - m]; stored as p - M, rows of 129 words
+                uint32_t* Mst = reinterpret_cast<uint32_t*>(sH);
+                const int dl = tid - 127;
+                if (dl < 128) {
+                    int r = dl >= 0 ? dl : 0, m = dl >= 0 ? 0 : -dl;
+                    uint64_t acc = dl >= 0 ? uint64_t(tmp[dl]) : uint64_t(hs[0]) * bw[128 + dl];
+                    uint32_t since = 1;
+                    auto out = [&](uint64_t x) {
+                        return negmod(FAST ? redc(fold(x, F), F) : reduce(x, F), F);
+                    };
+                    Mst[r * 129 + m] = out(acc);
+#pragma unroll 4
+                    for (++r, ++m; r < 128 && m < 128; ++r, ++m) {
+                        if (++since > F.fold_terms) {
+                            acc = fold(acc, F);
+                            since = 1;
+                        }
+                        acc = mad_wide(hs[r], bw[128 - m], acc);
+                        Mst[r * 129 + m] = out(acc);
+                    }
+                }
+            }
+            bar();
+            // thread (row group gq: rows 4 gq..4 gq+3, term part pq: terms 16 pq..16 pq+15)
+            const int gq = tid & 31, pq = tid >> 5;
+            uint32_t mneg[4][16], hw[19];
+            {
+                const uint32_t* Mst = reinterpret_cast<const uint32_t*>(sH);
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) mneg[k][j] = Mst[(4 * gq + k) * 129 + 16 * pq + j];
+#pragma unroll
+                for (int i = 0; i < 19; ++i) hw[i] = hs[4 * gq - 16 * pq - 15 + i];  // zeros before h
+            }
+            if (tid < 128) {  // Z_0 = A'_0 (no planes, no corrections yet)
+                sS[tid] = aK;
+                const int kn = 128 + tid;  // prefetch A' block 1
+                aK = kn < na ? __ldg(a + (na - 1 - kn)) : 0u;
+            }
+            bar();  // M read (the builders reuse the H buffers), Z_0 in place
+            st[3] += tcd_clock() - tp;
+
+            // Step K: Q_K = T_h Z_K - M Q_{K-1} with Z_K = A'_K - S_K - L_K in sS (the
+            // planes hold tiles <= K-2, L_K = Q_{K-2}'s terms outside them, from the
+            // builder warps).  -M Q_{K-1} (phase A) is formed as soon as Q_{K-1} is
+            // out, T_h Z_K (phase B) once S_K has been read: 64 MACs per thread each.
+            uint32_t pm[4] = {0, 0, 0, 0};  // this thread's partials of -M Q_{K-1}
+            const uint32_t ft = F.fold_terms;
             for (int K = 0; K < Kq; ++K, ++T) {
-                uint32_t* qk = qz + 128 * K;  // Q block K (zero here)
+                uint32_t* qk = qz + 128 * K;  // Q block K
                 {
                     TCD_T0();
-                    if (tid < 128) {  // E = A' - S - corr (partials of the previous step)
-                        sE[tid] = submod(submod(aK, sS[tid], F),
-                                         partials_sum(part, 128, 128, tid, F), F);
-                        const int kn = 128 * (K + 1) + tid;  // prefetch A' block K+1
-                        aK = kn < na ? __ldg(a + (na - 1 - kn)) : 0u;
-                    } else {
-                        qk[tid] = 0;  // Q block K+1 (tid - 128 + 128): zero for corr_{K+1}
+                    uint32_t z[16];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const uint4 zv = *reinterpret_cast<const uint4*>(sS + 16 * pq + 4 * i);
+                        z[4 * i] = zv.x; z[4 * i + 1] = zv.y; z[4 * i + 2] = zv.z; z[4 * i + 3] = zv.w;
                     }
+                    uint64_t a1[4] = {0, 0, 0, 0};
+#ifndef TCD_NOMV
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            a1[k] = mad_wide(hw[k - j + 15], z[j], a1[k]);  // h[4gq + k - (16pq + j)]
+                            if (!FAST && ft < 4) a1[k] = fold(a1[k], F);
+                        }
+                        if (!FAST && ft >= 4 && ft < 16 && (j & 3) == 3)
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) a1[k] = fold(a1[k], F);
+                    }
+#endif
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        part[pq * 128 + 4 * gq + k] = reduce_t<FAST>(a1[k], F) + pm[k];
                     bar();
-                    TCD_ACC(3);
-                    const long long _t1 = clock64();
-                    toeplitz_partials(hs, sE, 128, 128, part, F);  // Q_K = E h mod X^128
-                    bar();
+                    TCD_ACC(6);
+                }
+                {
+                    TCD_T0();
                     if (tid < 128) {
                         const int k1 = 128 * K + tid;
-                        const uint32_t v1 = k1 < mu ? partials_sum(part, 128, 128, tid, F) : 0u;
+                        const uint32_t v1 = k1 < mu ? partials_sum<FAST>(part, 128, 128, tid, F) : 0u;
                         qk[tid] = v1;
                         if (k1 < mu) fan_store<FAN>(g.Q, inst * g.ldq + (mu - 1 - k1), v1);
+                    } else {
+                        qk[tid] = 0;  // Q block K+1: zero until solved (the last tile reads it)
+                        if (K >= 1 && K + 1 < Kq)  // L_{K+1} from phase A of step K-1
+                            lateb[tid - 128] = partials_sum<FAST>(partL, 128, 128, tid - 128, F);
                     }
                     bar();
                     if (tid == 0) tc::mbar_arrive(&qready[T & 1]);  // the builders take tile K
-                    st[6] += clock64() - _t1;
-                }
-                {
-                    TCD_T0();
-                    // corr_{K+1}: the tiles K (against B'_1) and K+1 (upper, against
-                    // B'_0) that Q blocks <= K determine -- while tile K is built
-                    if (K + 1 < Kq) toeplitz_partials_256(qk + 128, bp01, part, F);
                     TCD_ACC(4);
                 }
+                if (K + 1 < Kq) {  // phase A of step K+1: -M Q_K
+                    TCD_T0();
+                    uint32_t q[16];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const uint4 qv = *reinterpret_cast<const uint4*>(qk + 16 * pq + 4 * i);
+                        q[4 * i] = qv.x; q[4 * i + 1] = qv.y; q[4 * i + 2] = qv.z; q[4 * i + 3] = qv.w;
+                    }
+                    // L window: X[j] = B'[256 + j] for j < 0 (bnc + 128), zero for j >= 0;
+                    // lw[i] = X[4 gq - 16 pq - 16 + i]
+                    uint32_t lw[20];
+#pragma unroll
+                    for (int i = 0; i < 5; ++i) {
+                        const uint4 v = *reinterpret_cast<const uint4*>(bnc + 128 + 4 * gq - 16 * pq - 16 + 4 * i);
+                        lw[4 * i] = v.x; lw[4 * i + 1] = v.y; lw[4 * i + 2] = v.z; lw[4 * i + 3] = v.w;
+                    }
+                    uint64_t a2[4] = {0, 0, 0, 0}, a3[4] = {0, 0, 0, 0};
+#ifndef TCD_NOMV
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            a2[k] = mad_wide(mneg[k][j], q[j], a2[k]);
+                            a3[k] = mad_wide(lw[k - j + 16], q[j], a3[k]);  // L_{K+2}: Q_K's late terms
+                            if (!FAST && ft < 4) {
+                                a2[k] = fold(a2[k], F);
+                                a3[k] = fold(a3[k], F);
+                            }
+                        }
+                        if (!FAST && ft >= 4 && ft < 16 && (j & 3) == 3)
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) {
+                                a2[k] = fold(a2[k], F);
+                                a3[k] = fold(a3[k], F);
+                            }
+                    }
+#endif
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        pm[k] = FAST ? redc(fold(a2[k], F), F) : reduce(a2[k], F);  // M: Montgomery
+                        partL[pq * 128 + 4 * gq + k] = reduce_t<FAST>(a3[k], F);
+                    }
+                    TCD_ACC(7);
+                }
                 {
                     TCD_T0();
-                    free_buf((T + 1) & 1);  // tile K-1 done: block K+1 holds tiles <= K-1
-                    tc::fence_after_sync();
-                    if (warp < 4) {
-                        uint32_t x[7];
+                    // Z_{K+1} = A'_{K+1} - S_{K+1} - L_{K+1}: S from the planes once tile
+                    // K-1 is done (block K+1 then holds tiles <= K-1)
+                    // (tile K-1 is waited for at every step, the last one too: a
+                    // parity wait must never fall two phases behind its mbarrier)
+                    {
+                        const long long tw = tcd_clock();
+                        free_buf((T + 1) & 1);
+                        const long long te = tcd_clock();
+                        st[9] += te - tw;                              // waited for tile K-1
+                        if (K > 0) st[10] += te - issue_ts[(T + 1) & 1];  // its issue -> seen done
+                    }
+                    if (K + 1 < Kq) {
+                        tc::fence_after_sync();
+                        if (warp < 4) {
+                            uint32_t x[7];
 #pragma unroll
-                        for (int s = 0; s < 7; ++s) x[s] = tmem_ld1(lane_addr + 64 * s + K + 1);
-                        tc::tmem_ld_wait();
-                        sS[32 * warp + lane] = combine_planes(x, g.c_hi, F);
+                            for (int s = 0; s < 7; ++s) x[s] = tmem_ld1(lane_addr + 64 * s + K + 1);
+                            tc::tmem_ld_wait();
+                            uint32_t zz = submod(aK, combine_planes(x, g.c_hi, F), F);
+                            if (K + 1 >= 2) zz = submod(zz, lateb[tid], F);
+                            sS[tid] = zz;
+                            const int kn = 128 * (K + 2) + tid;  // prefetch A' block K+2
+                            aK = kn < na ? __ldg(a + (na - 1 - kn)) : 0u;
+                        }
+                        tc::fence_before_sync();
                     }
-                    tc::fence_before_sync();
                     bar();
-                    if (tid == 0) {
-                        tc::mbar_wait(&built[T & 1], bph[T & 1]);
-                        tc::mbar_arrive(&full[T & 1]);
-                    }
-                    bph[T & 1] ^= 1;
+                    if (tid == 0) tc::mbar_arrive(&full[T & 1]);  // the builders may issue tile K
                     ++pend[T & 1];
                     TCD_ACC(2);
                 }
             }
-            long long tq = clock64();
+            long long tq = tcd_clock();
             // ---- the last tile (Q_{Kq-1}'s upper triangle), then the remainder ----
             if (tid == 0) {
                 tc::mbar_arrive(&qready[T & 1]);
-                tc::mbar_wait(&built[T & 1], bph[T & 1]);
                 tc::mbar_arrive(&full[T & 1]);
             }
-            bph[T & 1] ^= 1;
             ++pend[T & 1];
             ++T;
-            free_buf(0);
-            free_buf(1);
-            tc::fence_after_sync();
-            // r[na-1-k] = A'[k] - (Q B')[k], k in [mu, na): 8 blocks per TMEM load
+            // r[na-1-k] = A'[k] - (Q B')[k], k in [mu, na): 8 blocks per TMEM load, the
+            // dividend words loaded while the last tiles run (blocks < 64: <= 4 rounds)
             {
                 const int r = 32 * (warp & 3) + lane;
                 const int cfirst = mu >> 7, clast = (na - 1) >> 7;
                 const int64_t rb = inst * g.ldr;
-                for (int c0 = cfirst + 8 * (warp >> 2); c0 <= clast; c0 += 16) {
+                uint32_t av[4][8];
+#pragma unroll
+                for (int it = 0; it < 4; ++it)
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        const int k = 128 * (cfirst + 8 * (warp >> 2) + 16 * it + e) + r;
+                        av[it][e] = (k >= mu && k < na) ? __ldg(a + (na - 1 - k)) : 0u;
+                    }
+                free_buf(0);
+                free_buf(1);
+                tc::fence_after_sync();
+#pragma unroll
+                for (int it = 0; it < 4; ++it) {
+                    const int c0 = cfirst + 8 * (warp >> 2) + 16 * it;
+                    if (c0 > clast) break;
                     uint32_t x[7][8];
 #pragma unroll
                     for (int s = 0; s < 7; ++s) tmem_ld8(lane_addr + 64 * s + c0, x[s]);
@@ -500,7 +653,7 @@ __global__ void __launch_bounds__(TCD_T + TCD_BLD + 32, 1) tcdiv_kernel(TcDivArg
                             const uint32_t xs[7] = {x[0][e], x[1][e], x[2][e], x[3][e], x[4][e],
                                                     x[5][e], x[6][e]};
                             fan_store<FAN>(g.R, rb + (na - 1 - k),
-                                           submod(__ldg(a + (na - 1 - k)), combine_planes(xs, g.c_hi, F), F));
+                                           submod(av[it][e], combine_planes(xs, g.c_hi, F), F));
                         }
                     }
                 }
@@ -508,10 +661,14 @@ __global__ void __launch_bounds__(TCD_T + TCD_BLD + 32, 1) tcdiv_kernel(TcDivArg
             tc::fence_before_sync();
             bar();  // TMEM read before the next instance zeroes it
             tc::fence_after_sync();
-            st[5] += clock64() - tq;
+            st[5] += tcd_clock() - tq;
         }
         if (blockIdx.x == 0 && tid == 0)
             for (int i = 0; i < 8; ++i) tcd_stats[i] = st[i];
+        if (blockIdx.x == 0 && tid == 0) {
+            tcd_stats[12] = st[9];
+            tcd_stats[13] = st[10];
+        }
     }
     tc::fence_before_sync();
     __syncthreads();
@@ -552,18 +709,21 @@ void launch_tcdiv_batched(const FieldParams& F, const uint32_t* A, int64_t lda, 
         for (int e = 0; e < 32 + 8 * s; ++e) x = (x * 2) % F.p;
         g.c_hi[s] = uint32_t(x);
     }
-    auto kern = (Q.n > 1 || R.n > 1) ? tcdiv_kernel<true> : tcdiv_kernel<false>;
+    const bool fan = Q.n > 1 || R.n > 1, fast = F.odd && F.fold_terms >= 16;
+    auto kern = fan ? (fast ? tcdiv_kernel<true, true> : tcdiv_kernel<true, false>)
+                    : (fast ? tcdiv_kernel<false, true> : tcdiv_kernel<false, false>);
     MMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(D_SMEM_BYTES)));
     const int blocks = int(std::min<int64_t>(count, sm_count()));
     kern<<<blocks, TCD_ALL, D_SMEM_BYTES, st>>>(g);
     check_launch("tcdiv_kernel", dim3(blocks), dim3(TCD_ALL));
     if (getenv("MMM_TC_STATS")) {
-        long long h[8];
+        long long h[16];
         MMM_CUDA(cudaMemcpyFromSymbolAsync(h, tcd_stats, sizeof(h), 0, cudaMemcpyDeviceToHost, st));
         MMM_CUDA(cudaStreamSynchronize(st));
-        fprintf(stderr, "tcdiv stats (CTA 0, thread 0): prologue=%lld newton=%lld wait+read=%lld "
-                "corr+E=%lld build=%lld tail=%lld Qsolve=%lld cycles\n", h[0], h[1], h[2], h[3], h[4], h[5], h[6]);
+        fprintf(stderr, "tcdiv stats (CTA 0, thread 0): prologue=%lld h_wait=%lld tmem+Z=%lld "
+                "M=%lld Qsum=%lld tail=%lld MV_B=%lld MV_A=%lld cycles | builders: wait_q=%lld build=%lld issue=%lld newton+late=%lld | mma_wait=%lld issue_to_done=%lld\n",
+                h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7], h[8], h[9], h[10], h[11], h[12], h[13]);
     }
 }
 
