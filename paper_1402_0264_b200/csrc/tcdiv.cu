@@ -440,25 +440,40 @@ __global__ void __maxnreg__(168) tcdiv_kernel(TcDivArgs g) {
             bar();
             {
                 // diagonal r - m = dl of M, walked from its first entry with
-                // M[r][m] = M[r-1][m-1] + h[r] B'[128 - m]; stored as p - M, rows of 129 words
+                // M[r][m] = M[r-1][m-1] + h[r] B'[128 - m]; stored as p - M, rows of 128
+                // words, word groups of 4 XOR-swizzled by the row group (conflict-free
+                // 16-byte reads below)
                 uint32_t* Mst = reinterpret_cast<uint32_t*>(sH);
                 const int dl = tid - 127;
                 if (dl < 128) {
                     int r = dl >= 0 ? dl : 0, m = dl >= 0 ? 0 : -dl;
                     uint64_t acc = dl >= 0 ? uint64_t(tmp[dl]) : uint64_t(hs[0]) * bw[128 + dl];
-                    uint32_t since = 1;
                     auto out = [&](uint64_t x) {
                         return negmod(FAST ? redc(fold(x, F), F) : reduce(x, F), F);
                     };
-                    Mst[r * 129 + m] = out(acc);
-#pragma unroll 4
-                    for (++r, ++m; r < 128 && m < 128; ++r, ++m) {
+                    auto at = [](int r, int m) { return r * 128 + (m ^ (((r >> 2) & 7) << 2)); };
+                    Mst[at(r, m)] = out(acc);
+                    const int len = 128 - (dl >= 0 ? dl : -dl);  // entries on this diagonal
+                    int i = 1;
+                    if (FAST) {  // fold_terms >= 16: fold, 16 terms, fold, ... (pipelined)
+                        acc = fold(acc, F);
+                        for (; i + 16 <= len; i += 16) {
+#pragma unroll
+                            for (int q = 0; q < 16; ++q) {
+                                acc = mad_wide(hs[r + i + q], bw[128 - (m + i + q)], acc);
+                                Mst[at(r + i + q, m + i + q)] = out(acc);
+                            }
+                            acc = fold(acc, F);
+                        }
+                    }
+                    uint32_t since = 1;
+                    for (; i < len; ++i) {
                         if (++since > F.fold_terms) {
                             acc = fold(acc, F);
                             since = 1;
                         }
-                        acc = mad_wide(hs[r], bw[128 - m], acc);
-                        Mst[r * 129 + m] = out(acc);
+                        acc = mad_wide(hs[r + i], bw[128 - (m + i)], acc);
+                        Mst[at(r + i, m + i)] = out(acc);
                     }
                 }
             }
@@ -471,7 +486,14 @@ __global__ void __maxnreg__(168) tcdiv_kernel(TcDivArgs g) {
 #pragma unroll
                 for (int k = 0; k < 4; ++k)
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) mneg[k][j] = Mst[(4 * gq + k) * 129 + 16 * pq + j];
+                    for (int jj = 0; jj < 4; ++jj) {
+                        const uint4 v = *reinterpret_cast<const uint4*>(
+                            Mst + (4 * gq + k) * 128 + ((16 * pq + 4 * jj) ^ ((gq & 7) << 2)));
+                        mneg[k][4 * jj] = v.x;
+                        mneg[k][4 * jj + 1] = v.y;
+                        mneg[k][4 * jj + 2] = v.z;
+                        mneg[k][4 * jj + 3] = v.w;
+                    }
 #pragma unroll
                 for (int i = 0; i < 19; ++i) hw[i] = hs[4 * gq - 16 * pq - 15 + i];  // zeros before h
             }
