@@ -35,8 +35,8 @@ namespace {
 constexpr int MAX_DEV = 64;
 struct DevState {
     cudaStream_t stream = nullptr;
-    cudaStream_t aux[2] = {nullptr, nullptr};  // the batch pipeline's copy/compute lanes
-    cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+    cudaStream_t aux[3] = {nullptr, nullptr, nullptr};  // the batch pipeline: H2D, kernels, D2H
+    cudaEvent_t ev[16] = {};
     Arena arena;
     ZeroBuf zero;
     bool used = false;
@@ -289,15 +289,16 @@ uint32_t* pinned_stage(size_t bytes) {
 cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 
 // ---- pipelined batches (host buffers) --------------------------------------
-// A batched host call streams its instances through the GPU in chunks on two
-// lanes: chunk k's H2D, coefficient check, kernels and D2H are ordered on lane
-// k % 2, so chunk k+1's copies overlap chunk k's kernels (and the copy engines
-// run both directions at once).  The canonical-coefficient check
-// (run_util.hpp:24-29) runs on the device as each chunk lands -- the host scan
-// of a cfg5 batch (335 MB) cost more than its transfer -- and is reported after
-// the join (outputs are then unspecified, as for any failed call).  D2H of
-// chunk k is issued after chunk k+1's H2D and kernels, so pageable (blocking)
-// copies still overlap.
+// A batched host call streams its instances through the GPU in chunks over
+// three streams -- copies in, kernels, copies out -- and a ring of device
+// slots: chunk k's H2D waits only for the D2H that last used its slot, its
+// kernels for its H2D, its D2H for its kernels, so the copy engines run both
+// directions while the SMs work on the chunk in between.  The canonical-
+// coefficient check (run_util.hpp:24-29) runs on the device as each chunk
+// lands -- the host scan of a cfg5 batch (335 MB) cost more than its transfer
+// -- and is reported after the join (outputs are then unspecified, as for any
+// failed call).  D2H of chunk k is issued after chunk k+1's H2D and kernels,
+// so pageable (blocking) copies still overlap.
 struct HostIn {
     const uint32_t* p;
     int64_t ld, n;
@@ -308,6 +309,8 @@ struct HostOut {
     int64_t ld, n;
 };
 
+constexpr int PIPE_SLOTS = 3;
+
 template <class Launch>
 void pipelined_batch(const FieldParams& F, int64_t count, std::vector<HostIn> ins,
                      std::vector<HostOut> outs, Launch launch) {
@@ -317,56 +320,68 @@ void pipelined_batch(const FieldParams& F, int64_t count, std::vector<HostIn> in
         if (!a) MMM_CUDA(cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking));
     for (auto& e : ds.ev)
         if (!e) MMM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    const cudaStream_t sH = ds.aux[0], sK = ds.aux[1], sD = ds.aux[2];
+    cudaEvent_t* evIn = ds.ev + 1;                // [slot]: chunk's inputs landed
+    cudaEvent_t* evOut = evIn + PIPE_SLOTS;       // [slot]: chunk's kernels done
+    cudaEvent_t* evFree = evOut + PIPE_SLOTS;     // [slot]: chunk's results copied out
     int64_t row_words = 0;
     for (auto& i : ins) row_words += i.n;
     for (auto& o : outs) row_words += o.n;
-    // chunks of >= 2 waves of one CTA per SM and >= 4 MB, about 8 per call
-    int64_t chunk = std::max<int64_t>(ceil_div(count, 8), 2LL * sm_count());
-    chunk = std::max<int64_t>(chunk, ceil_div(int64_t(4) << 20, 4 * std::max<int64_t>(row_words, 1)));
+    // about 16 chunks per call, each a whole number of CTA rounds (one CTA per SM)
+    // and >= 2 MB
+    const int64_t sms = sm_count();
+    int64_t chunk = ceil_div(ceil_div(count, 16), sms) * sms;
+    chunk = std::max<int64_t>(chunk, ceil_div(int64_t(2) << 20, 4 * std::max<int64_t>(row_words, 1)));
     chunk = std::min<int64_t>(chunk, count);
     const int64_t nchunks = ceil_div(count, chunk);
-    const int lanes = nchunks > 1 ? 2 : 1;
+    const int slots = int(std::min<int64_t>(PIPE_SLOTS, nchunks));
     uint32_t* stage = pinned_stage(ins.size() * 4 + 16);
     {
         Scratch sc(st0);
-        std::vector<uint32_t*> din[2], dout[2];
-        for (int l = 0; l < lanes; ++l) {
+        std::vector<uint32_t*> din[PIPE_SLOTS], dout[PIPE_SLOTS];
+        for (int l = 0; l < slots; ++l) {
             for (auto& i : ins) din[l].push_back(sc.get<uint32_t>(size_t(chunk * i.n)));
             for (auto& o : outs) dout[l].push_back(sc.get<uint32_t>(size_t(chunk * std::max<int64_t>(o.n, 1))));
         }
         unsigned* flags = sc.get<unsigned>(ins.size());
         MMM_CUDA(cudaMemsetAsync(flags, 0, ins.size() * sizeof(unsigned), st0));
         MMM_CUDA(cudaEventRecord(ds.ev[0], st0));  // fork: scratch and flags ready
-        for (int l = 0; l < lanes; ++l) MMM_CUDA(cudaStreamWaitEvent(ds.aux[l], ds.ev[0], 0));
+        for (cudaStream_t a : {sH, sK, sD}) MMM_CUDA(cudaStreamWaitEvent(a, ds.ev[0], 0));
         auto d2h = [&](int64_t k) {
-            const int l = int(k % lanes);
+            const int l = int(k % slots);
             const int64_t c0 = k * chunk, c = std::min(chunk, count - c0);
+            MMM_CUDA(cudaStreamWaitEvent(sD, evOut[l], 0));
             for (size_t j = 0; j < outs.size(); ++j)
                 if (outs[j].n)
                     MMM_CUDA(cudaMemcpy2DAsync(outs[j].p + c0 * outs[j].ld, size_t(outs[j].ld) * 4,
                                                dout[l][j], size_t(outs[j].n) * 4,
                                                size_t(outs[j].n) * 4, size_t(c),
-                                               cudaMemcpyDeviceToHost, ds.aux[l]));
+                                               cudaMemcpyDeviceToHost, sD));
+            MMM_CUDA(cudaEventRecord(evFree[l], sD));
         };
         for (int64_t k = 0; k < nchunks; ++k) {
-            const int l = int(k % lanes);
-            const cudaStream_t st = ds.aux[l];
+            const int l = int(k % slots);
             const int64_t c0 = k * chunk, c = std::min(chunk, count - c0);
-            for (size_t j = 0; j < ins.size(); ++j) {
+            if (k >= slots) MMM_CUDA(cudaStreamWaitEvent(sH, evFree[l], 0));  // slot drained
+            for (size_t j = 0; j < ins.size(); ++j)
                 MMM_CUDA(cudaMemcpy2DAsync(din[l][j], size_t(ins[j].n) * 4, ins[j].p + c0 * ins[j].ld,
                                            size_t(ins[j].ld) * 4, size_t(ins[j].n) * 4, size_t(c),
-                                           cudaMemcpyHostToDevice, st));
+                                           cudaMemcpyHostToDevice, sH));
+            MMM_CUDA(cudaEventRecord(evIn[l], sH));
+            MMM_CUDA(cudaStreamWaitEvent(sK, evIn[l], 0));
+            for (size_t j = 0; j < ins.size(); ++j) {
                 const unsigned blocks = unsigned(std::min<int64_t>(c, 4LL * sm_count()));
-                check_rows_kernel<<<blocks, 256, 0, st>>>(din[l][j], c, ins[j].n, F.p, flags + j);
+                check_rows_kernel<<<blocks, 256, 0, sK>>>(din[l][j], c, ins[j].n, F.p, flags + j);
                 check_launch("check_rows_kernel", dim3(blocks), dim3(256));
             }
-            launch(din[l], dout[l], c, st);
+            launch(din[l], dout[l], c, sK);
+            MMM_CUDA(cudaEventRecord(evOut[l], sK));
             if (k > 0) d2h(k - 1);
         }
         d2h(nchunks - 1);
-        for (int l = 0; l < lanes; ++l) {  // join before the scratch is released
-            MMM_CUDA(cudaEventRecord(ds.ev[1 + l], ds.aux[l]));
-            MMM_CUDA(cudaStreamWaitEvent(st0, ds.ev[1 + l], 0));
+        for (int a = 0; a < 3; ++a) {  // join before the scratch is released
+            MMM_CUDA(cudaEventRecord(ds.ev[13 + a], ds.aux[a]));
+            MMM_CUDA(cudaStreamWaitEvent(st0, ds.ev[13 + a], 0));
         }
         MMM_CUDA(cudaMemcpyAsync(stage, flags, ins.size() * sizeof(unsigned),
                                  cudaMemcpyDeviceToHost, st0));
