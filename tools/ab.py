@@ -33,7 +33,7 @@ if w == "batch":
     calls["mul"] = lambda: mmm.mul_batched_dev(P, A.data_ptr(), n, n, B.data_ptr(), n, n, k, F.data_ptr(), 2 * n - 1, stream=st)
     calls["div"] = lambda: mmm.divmod_batched_dev(P, Cd.data_ptr(), 2 * n, 2 * n, D.data_ptr(), n, n, k, Q.data_ptr(), n + 1, R.data_ptr(), n - 1, stream=st)
 elif w in ("ntt", "ntt_batch"):
-    n, k = (1 << 20, 1) if w == "ntt" else (1 << 16, 256)
+    n, k = (1 << 20, 1) if w == "ntt" else (1 << 15, 256)  # cfg4: 2^21 product; 256 x 2^16 transforms
     A, B = draw(k, n), draw(k, n)
     F = torch.empty((k, 2 * n - 1), dtype=torch.int32, device="cuda")
     if k == 1:
