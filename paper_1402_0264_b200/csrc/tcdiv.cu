@@ -13,14 +13,30 @@
 // same arithmetic: a zero head gives a zero quotient word).
 //
 // The running product sum_I Q_I X^(128 I) B' is the block-Toeplitz GEMM of
-// tcmul.cu with Q on the Toeplitz side: after step K the tensor core adds
-// tile H_K (built from Q_K and Q_{K-1}) times all of B' into the seven TMEM
-// limb planes.  Step K+1 reads block K+1 of that sum back from TMEM (one
-// column per plane), adds the part of tile H_{K+1} that Q_K already
-// determines (its upper triangle against B'_0, on the CUDA cores), and solves
-// the 128 x 128 triangular system for Q_{K+1} (the CUDA cores again).  After
+// tcmul.cu with Q on the Toeplitz side: tile H_K (Q_K below the diagonal,
+// Q_{K-1} above) times all of B' goes into the seven TMEM limb planes.  The
+// tensor core runs two tiles behind the chain, so when block K is read back
+// (S_K) the planes hold tiles <= K-2 and the rest of block K is on the CUDA
+// cores:  E_K = A'_K - S_K - T_B1 Q_{K-1} - L_K,  with
+//   T_B1[r][m] = B'[128 + r - m]   (Q_{K-1}'s terms in block K: tile K-1's
+//                                   lower part against B'_1, tile K's upper
+//                                   part against B'_0),
+//   L_K[r] = sum_{m > r} Q_{K-2}[m] B'[256 + r - m]   (tile K-1's upper part
+//                                   against B'_1: Q_{K-2}'s late terms).
+// With Z_K = A'_K - S_K - L_K that is one product per step on the chain:
+//   Q_K = T_h Z_K - M Q_{K-1},   M = T_h T_B1   (T_h: lower-triangular
+//   Toeplitz of h), where -M (128 x 128, per instance) sits in the compute
+// threads' registers -- M[r][m] = M[r-1][m-1] + h[r] B'[128 - m] builds it in
+// one diagonal walk per instance -- and -M Q_{K-1} plus L_{K+1} (phase A) run
+// as soon as Q_{K-1} is out, T_h Z_K (phase B) once S_K has been read.  After
 // the last block one more tile completes Q B' and the remainder comes out of
-// TMEM in one pass.  Shapes: na <= 8192, nb <= 4096 (cfg5: 8192 / 4096 terms).
+// TMEM in one pass.  Warps: 8 compute (the chain, the planes' reads, the
+// remainder), 4 builders (tiles; one lane issues each tile's 16 UMMAs once the
+// compute warps have read the block the tile would disturb; the next
+// instance's h by Newton).  Shapes: na <= 8192, nb <= 4096 (cfg5: 8192 / 4096).
+// (Measured alternatives, tools/ab.py on cfg5: L on the builder warps 3.44 ms
+// vs 2.82 ms here -- the builders then bound the step; a dedicated MMA warp
+// needs 13 warps, i.e. <= 128 registers, too few for M in registers.)
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -37,7 +53,7 @@ namespace {
 
 using namespace tct;
 
-constexpr int TCD_T = 256;    // compute warps 0-7: the per-step solve
+constexpr int TCD_T = 256;    // compute warps 0-7: the chain
 constexpr int TCD_BLD = 128;  // builder warps 8-11: the tiles
 constexpr int TCD_ALL = TCD_T + TCD_BLD;  // twelve warps: three per SMSP, up to 168 registers
 constexpr int TCD_MAXA = 8192;
@@ -49,8 +65,8 @@ constexpr uint32_t D_OFF_B = D_OFF_H + 2 * HBUF;          // B_PRE | 240 rows (t
 constexpr uint32_t D_OFF_Q = D_OFF_B + B_BYTES;           // u32 Q (padded)
 constexpr uint32_t D_OFF_SM = D_OFF_Q + TCD_QWORDS * 4;   // small arrays
 constexpr uint32_t D_SMALL = 256 + 2 * 256 + 128 + 128 + 1024 + 128 + 256 + 1024 + 128 + 256 + 128 + 1024;
-// B'[0..256), h ping-pong (each: 128 zeros, h), S, E, parts, tmp | builders: B'[0..256), parts,
-// tmp, B'[128..256) + 128 zeros, the late correction of the next block, its partials [8][128]
+// B'[0..256), h ping-pong (each: 128 zeros, h), Z, B' (Montgomery), parts, tmp | builders:
+// B'[0..256), parts, tmp | B'[128..256) + 128 zeros, L_{K+1}, L_{K+2}'s partials [8][128]
 constexpr uint32_t D_SMEM_BYTES = D_OFF_SM + D_SMALL * 4 + 1024;
 
 struct TcDivArgs {
@@ -120,49 +136,6 @@ __device__ __forceinline__ void toeplitz_partials(const uint32_t* X, const uint3
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k) part[p * n + r0 + k] = reduce_t<FAST>(acc[k], F);
-}
-
-// n = T = 128 rows / terms twice: part = partials of
-//   sum_{t<128} X[i - t] W[t]  +  sum_{t<128} X[i - 128 - t] W[128 + t]
-// (one 256-term Toeplitz product, X defined on [-256, 128)).
-__device__ __forceinline__ void toeplitz_partials_256(const uint32_t* X, const uint32_t* W,
-                                                      uint32_t* part, const FieldParams& F) {
-    const int tid = threadIdx.x;
-    const int g = tid & 31, p = tid >> 5, r0 = 4 * g;
-    uint64_t acc[4] = {0, 0, 0, 0};
-    const uint32_t ft = F.fold_terms;
-#pragma unroll
-    for (int half = 0; half < 2; ++half) {
-        const uint32_t* Xh = X - 128 * half;
-        const uint32_t* Wh = W + 128 * half;
-        const int t0 = 16 * p;
-        const uint4 cv = *reinterpret_cast<const uint4*>(Xh + r0 - t0);
-        uint32_t cur[4] = {cv.x, cv.y, cv.z, cv.w};
-#pragma unroll
-        for (int jb = 0; jb < 4; ++jb) {
-            const int t = t0 + 4 * jb;
-            const uint4 nv = *reinterpret_cast<const uint4*>(Xh + r0 - t - 4);
-            const uint4 wv = *reinterpret_cast<const uint4*>(Wh + t);
-            const uint32_t z[8] = {nv.x, nv.y, nv.z, nv.w, cur[0], cur[1], cur[2], cur[3]};
-            const uint32_t w4[4] = {wv.x, wv.y, wv.z, wv.w};
-#pragma unroll
-            for (int jj = 0; jj < 4; ++jj)
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    acc[k] = mad_wide(z[4 + k - jj], w4[jj], acc[k]);
-                    if (ft < 4) acc[k] = fold(acc[k], F);
-                }
-            if (ft >= 4 && ft < 32)
-#pragma unroll
-                for (int k = 0; k < 4; ++k) acc[k] = fold(acc[k], F);
-            cur[0] = nv.x;
-            cur[1] = nv.y;
-            cur[2] = nv.z;
-            cur[3] = nv.w;
-        }
-    }
-#pragma unroll
-    for (int k = 0; k < 4; ++k) part[p * 128 + r0 + k] = reduce(acc[k], F);
 }
 
 // y[i] = sum over the T/16 partials, mod p (threads i < n).

@@ -14,7 +14,7 @@ cap() {  # name workload kernel-regex count [extra args]
 cap tcmul batch tcmul 1
 cap tcdiv batch tcdiv 1
 cap gcd gcd gcd_kernel 1
-cap mul mul mul_kernel 1
+cap mul mul tcmul_split 1
 cap div div div_pipe 1
 cap ntt ntt ntt_ 3
 cap ntt_batch ntt_batch ntt_ 3
