@@ -58,7 +58,10 @@ def main():
     for f in os.listdir(src):
         if f.endswith("_brief.txt"):
             shutil.copy(os.path.join(src, f), os.path.join(PROF, f"{tag}_{f}"))
-    # s sweep + per-s counters
+    # s sweep + per-s counters (rounds that re-ran it)
+    if not os.path.exists(os.path.join(src, "s_sweep.csv")):
+        print("traffic:", json.dumps(traffic, indent=1)[:1500])
+        return
     sweep = list(csv.DictReader(open(os.path.join(src, "s_sweep.csv"))))
     cols = ["ncu_time_us", "inst_issued", "fmaheavy_inst", "fmaheavy_busy_pct", "issue_active_pct",
             "dram_read_B", "dram_write_B", "dram_GBps", "l2_bytes"]
