@@ -333,7 +333,18 @@ void pipelined_batch(const FieldParams& F, int64_t count, std::vector<HostIn> in
     int64_t chunk = ceil_div(ceil_div(count, 16), sms) * sms;
     chunk = std::max<int64_t>(chunk, ceil_div(int64_t(2) << 20, 4 * std::max<int64_t>(row_words, 1)));
     chunk = std::min<int64_t>(chunk, count);
-    const int64_t nchunks = ceil_div(count, chunk);
+    // the first and last chunks are one CTA round when the batch allows: the first H2D
+    // and the last kernels + D2H are the pipeline's unoverlapped fill and drain
+    std::vector<int64_t> cuts{0};
+    {
+        const int64_t edge = std::min(chunk, sms);
+        const bool ramp = count >= 2 * edge + 2 * chunk;
+        if (ramp) cuts.push_back(edge);
+        const int64_t body_end = ramp ? count - edge : count;
+        while (cuts.back() < body_end) cuts.push_back(std::min(body_end, cuts.back() + chunk));
+        if (ramp) cuts.push_back(count);
+    }
+    const int64_t nchunks = int64_t(cuts.size()) - 1;
     const int slots = int(std::min<int64_t>(PIPE_SLOTS, nchunks));
     uint32_t* stage = pinned_stage(ins.size() * 4 + 16);
     {
@@ -349,7 +360,7 @@ void pipelined_batch(const FieldParams& F, int64_t count, std::vector<HostIn> in
         for (cudaStream_t a : {sH, sK, sD}) MMM_CUDA(cudaStreamWaitEvent(a, ds.ev[0], 0));
         auto d2h = [&](int64_t k) {
             const int l = int(k % slots);
-            const int64_t c0 = k * chunk, c = std::min(chunk, count - c0);
+            const int64_t c0 = cuts[k], c = cuts[k + 1] - c0;
             MMM_CUDA(cudaStreamWaitEvent(sD, evOut[l], 0));
             for (size_t j = 0; j < outs.size(); ++j)
                 if (outs[j].n)
@@ -361,7 +372,7 @@ void pipelined_batch(const FieldParams& F, int64_t count, std::vector<HostIn> in
         };
         for (int64_t k = 0; k < nchunks; ++k) {
             const int l = int(k % slots);
-            const int64_t c0 = k * chunk, c = std::min(chunk, count - c0);
+            const int64_t c0 = cuts[k], c = cuts[k + 1] - c0;
             if (k >= slots) MMM_CUDA(cudaStreamWaitEvent(sH, evFree[l], 0));  // slot drained
             for (size_t j = 0; j < ins.size(); ++j)
                 MMM_CUDA(cudaMemcpy2DAsync(din[l][j], size_t(ins[j].n) * 4, ins[j].p + c0 * ins[j].ld,
