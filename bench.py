@@ -1189,7 +1189,9 @@ def run_ours(args, dist):
         for _ in range(n_def):
             work.host_step_default()
         e2e["default_out_ms_per_step"] = (time.perf_counter() - t0) / n_def * 1e3
-        e2e["default_out_note"] = "same call with out=None (library-allocated pageable results)"
+        e2e["default_out_note"] = ("same call with out=None: results in page-locked memory from "
+                                   "the library's pool (mmm_cu_host_alloc), reused once the "
+                                   "previous step's arrays are dropped")
 
     hbm, src, imad = peaks()
     roof = work.roofline(t_step, hbm, imad, parts=parts)

@@ -78,6 +78,15 @@ int mmm_cu_release_scratch(void);
  * synchronising every device.  No other thread may have calls in flight. */
 int mmm_cu_release_all(void);
 
+/* Page-locked host memory for results (process-wide pool): a buffer handed
+ * back with mmm_cu_host_free() is kept and reused by the next request of the
+ * same rounded size, so a caller that allocates its batched results this way
+ * gets full-speed device-to-host copies without paying for page-locking on
+ * every call.  Up to 2 GB of freed buffers are kept; mmm_cu_release_all()
+ * returns them to the system. */
+int mmm_cu_host_alloc(size_t bytes, void** out);
+int mmm_cu_host_free(void* p);
+
 /* ---- field and inputs (host) ------------------------------------------- */
 int mmm_field_check(int64_t p);
 /* a^-1 mod p in *out; MMM_DOMAIN_ERROR for a == 0 (Field::inv, field.cpp:27-42). */

@@ -28,6 +28,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import weakref
 from typing import Optional
 
 import numpy as np
@@ -89,6 +90,8 @@ SIGNATURES = {
     "mmm_cu_release_scratch": (C.c_int, []),
     "mmm_cu_last_schedule": (C.c_int, [C.POINTER(KernelRec), C.c_int32, _I32P]),
     "mmm_cu_release_all": (C.c_int, []),
+    "mmm_cu_host_alloc": (C.c_int, [C.c_size_t, C.POINTER(C.c_void_p)]),
+    "mmm_cu_host_free": (C.c_int, [_VP]),
     "mmm_field_check": (C.c_int, [_I64]),
     "mmm_field_inv": (C.c_int, [_I64, _I64, _I64P]),
     "mmm_rng_create": (_VP, [C.c_uint64]),
@@ -267,6 +270,29 @@ def _out(out, shape):
     return out
 
 
+def _host_free(ptr: int) -> None:
+    try:
+        if _lib is not None:
+            _lib.mmm_cu_host_free(C.c_void_p(ptr))
+    except Exception:  # interpreter teardown
+        pass
+
+
+def _pinned_out(out, shape):
+    """A batched call's results: the caller's array, or page-locked memory from
+    the library's pool (mmm_cu_host_alloc), so the device-to-host copies run at
+    link speed; the buffer goes back to the pool when the array and every view
+    of it are gone.  Every word is written by the call."""
+    if out is not None:
+        return _out(out, shape)
+    n = int(np.prod(shape))
+    ptr = C.c_void_p()
+    _check(load().mmm_cu_host_alloc(max(n, 1) * 4, C.byref(ptr)))
+    buf = (C.c_uint32 * max(n, 1)).from_address(ptr.value)
+    weakref.finalize(buf, _host_free, ptr.value)
+    return np.frombuffer(buf, dtype=np.uint32, count=n).reshape(shape)
+
+
 def _pint(p) -> int:
     return p.p() if isinstance(p, Field) else int(p)
 
@@ -338,7 +364,7 @@ def mul_batched(A, B, p, s: int = 0, out=None) -> np.ndarray:
     A, B, p = _u32(A), _u32(B), _pint(p)
     cnt, na = A.shape
     nb = B.shape[1]
-    F = _out(out, (cnt, na + nb - 1))
+    F = _pinned_out(out, (cnt, na + nb - 1))
     _check(load().mmm_cu_mul_batched(p, _p(A), na, na, _p(B), nb, nb, cnt, s, _p(F), F.shape[1]))
     return F
 
@@ -347,8 +373,8 @@ def divmod_batched(A, B, p, s: int = 0, q_out=None, r_out=None):
     A, B, p = _u32(A), _u32(B), _pint(p)
     cnt, na = A.shape
     nb = B.shape[1]
-    Q = _out(q_out, (cnt, na - nb + 1))
-    R = _out(r_out, (cnt, max(nb - 1, 1)))
+    Q = _pinned_out(q_out, (cnt, na - nb + 1))
+    R = _pinned_out(r_out, (cnt, max(nb - 1, 1)))
     _check(load().mmm_cu_divmod_batched(p, _p(A), na, na, _p(B), nb, nb, cnt, s, _p(Q),
                                         Q.shape[1], _p(R), R.shape[1]))
     return Q, R[:, : nb - 1]
@@ -358,7 +384,7 @@ def ntt_mul_batched(A, B, p, out=None) -> np.ndarray:
     A, B, p = _u32(A), _u32(B), _pint(p)
     cnt, na = A.shape
     nb = B.shape[1]
-    F = _out(out, (cnt, na + nb - 1))
+    F = _pinned_out(out, (cnt, na + nb - 1))
     _check(load().mmm_cu_ntt_mul_batched(p, _p(A), na, na, _p(B), nb, nb, cnt, _p(F),
                                          F.shape[1]))
     return F

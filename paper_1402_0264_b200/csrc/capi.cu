@@ -426,8 +426,71 @@ int mmm_cu_release_scratch(void) {
     return guarded([&] { t_state.release(); });
 }
 
+// ---- pinned result pool ------------------------------------------------
+namespace {
+struct HostPool {
+    std::mutex mu;
+    std::multimap<size_t, void*> free_;     // rounded size -> buffer
+    std::map<void*, size_t> live;           // buffer -> rounded size
+    size_t cached = 0;
+    static constexpr size_t CAP = size_t(2) << 30;
+    static size_t round(size_t b) {  // 1 MB granularity (few distinct sizes per workload)
+        const size_t g = size_t(1) << 20;
+        return std::max(g, (b + g - 1) / g * g);
+    }
+    void drain() {
+        std::lock_guard<std::mutex> lk(mu);
+        for (auto& kv : free_) cudaFreeHost(kv.second);
+        free_.clear();
+        cached = 0;
+    }
+} g_hostpool;
+}  // namespace
+
+int mmm_cu_host_alloc(size_t bytes, void** out) {
+    return guarded([&] {
+        if (!out) throw Error(ST_INVALID, "mmm_cu_host_alloc: null out");
+        const size_t n = HostPool::round(bytes);
+        {
+            std::lock_guard<std::mutex> lk(g_hostpool.mu);
+            auto it = g_hostpool.free_.find(n);
+            if (it != g_hostpool.free_.end()) {
+                *out = it->second;
+                g_hostpool.cached -= n;
+                g_hostpool.free_.erase(it);
+                g_hostpool.live[*out] = n;
+                return;
+            }
+        }
+        void* p = nullptr;
+        MMM_CUDA(cudaMallocHost(&p, n));
+        std::lock_guard<std::mutex> lk(g_hostpool.mu);
+        g_hostpool.live[p] = n;
+        *out = p;
+    });
+}
+
+int mmm_cu_host_free(void* p) {
+    return guarded([&] {
+        if (!p) return;
+        std::lock_guard<std::mutex> lk(g_hostpool.mu);
+        auto it = g_hostpool.live.find(p);
+        if (it == g_hostpool.live.end())
+            throw Error(ST_INVALID, "mmm_cu_host_free: not a buffer from mmm_cu_host_alloc");
+        const size_t n = it->second;
+        g_hostpool.live.erase(it);
+        if (g_hostpool.cached + n <= HostPool::CAP) {
+            g_hostpool.free_.emplace(n, p);
+            g_hostpool.cached += n;
+        } else {
+            MMM_CUDA(cudaFreeHost(p));
+        }
+    });
+}
+
 int mmm_cu_release_all(void) {
     return guarded([&] {
+        g_hostpool.drain();
         int n = 0, cur = 0;
         MMM_CUDA(cudaGetDevice(&cur));
         MMM_CUDA(cudaGetDeviceCount(&n));

@@ -117,3 +117,14 @@ def test_no_cpu_fallback_without_gpu():
                lambda: mmm.ntt_mul([1, 2], [3, 4], 469762049)):
         with pytest.raises(mmm.CudaError):
             fn()
+
+
+def test_host_free_rejects_foreign_pointers():
+    """mmm_cu_host_free only takes buffers from mmm_cu_host_alloc (no CUDA call
+    is made for a foreign pointer, so this runs without a GPU)."""
+    import ctypes
+    mmm = pytest.importorskip("paper_1402_0264_b200")
+    lib = mmm.load()
+    bogus = (ctypes.c_uint32 * 4)()
+    assert lib.mmm_cu_host_free(ctypes.addressof(bogus)) == mmm.InvalidArgument.status
+    assert lib.mmm_cu_host_free(None) == 0

@@ -274,6 +274,48 @@ def test_out_arrays_dirty_and_rejected(cuda_lib, port):
         mmm.mul(A[0], B[0], P, out=np.zeros(10, np.uint32))
 
 
+def test_default_results_from_the_pinned_pool(cuda_lib, port):
+    """out=None on a batched call: results in page-locked memory from the
+    library's pool (mmm_cu_host_alloc), every word written, the buffer reused
+    once the previous result (and its views) are dropped; mmm_cu_host_free of
+    anything else is rejected."""
+    import ctypes
+    import gc
+    mmm = cuda_lib
+    rng = np.random.default_rng(43)
+    A, B = rng.integers(0, P, (7, 900)), rng.integers(0, P, (7, 500))
+    B[:, -1] = np.maximum(B[:, -1], 1)
+    want = [port.mul(A[i], B[i], P) for i in range(7)]
+    F = mmm.mul_batched(A, B, P)
+    assert F.shape == (7, 1399) and all(np.array_equal(F[i], want[i]) for i in range(7))
+    addr = F.ctypes.data
+    view = F[3]  # keeps the first buffer alive
+    del F
+    gc.collect()
+    G = mmm.mul_batched(A, B, P)  # the first buffer is still held by `view`
+    assert G.ctypes.data != addr and np.array_equal(view, want[3])
+    del view, G
+    gc.collect()
+    H = mmm.ntt_mul_batched(A, B, P)
+    assert all(np.array_equal(H[i], want[i]) for i in range(7))
+    lib = mmm.load()  # a freed buffer comes back for the next request of its size
+    size = (37 << 20) + 5
+    p1, p2 = ctypes.c_void_p(), ctypes.c_void_p()
+    assert lib.mmm_cu_host_alloc(size, ctypes.byref(p1)) == 0 and p1.value
+    assert lib.mmm_cu_host_free(p1) == 0
+    assert lib.mmm_cu_host_alloc(size, ctypes.byref(p2)) == 0 and p2.value == p1.value
+    assert lib.mmm_cu_host_free(p2) == 0
+    A2 = rng.integers(0, P, (7, 1000))
+    A2[:, -1] = np.maximum(A2[:, -1], 1)
+    Q, R = mmm.divmod_batched(A2, B, P)
+    for i in range(7):
+        wq, wr = port.divmod(A2[i], B[i], P)
+        assert np.array_equal(np.trim_zeros(Q[i], "b"), wq)
+        assert np.array_equal(np.trim_zeros(R[i], "b"), wr)
+    bogus = (ctypes.c_uint32 * 4)()
+    assert mmm.load().mmm_cu_host_free(ctypes.addressof(bogus)) == mmm.InvalidArgument.status
+
+
 def test_last_schedule_reports_the_launches(cuda_lib, port):
     """mmm_cu_last_schedule: the kernels of the thread's last host call (what
     the drop-in's SimReport.kernels and N/L/K are built from)."""
