@@ -194,6 +194,16 @@ __global__ void check_rows_kernel(const uint32_t* __restrict__ d, int64_t rows, 
     if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1u);
 }
 
+// validate_coeffs (run_util.hpp:24-29) for one operand where it landed
+__global__ void check_flat_kernel(const uint32_t* __restrict__ d, int64_t n, uint32_t p,
+                                  unsigned* flag) {
+    unsigned bad = 0;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x)
+        bad |= __ldg(d + i) >= p;
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1u);
+}
+
 }  // namespace mmm_cu
 
 using namespace mmm_cu;
@@ -225,10 +235,14 @@ FieldParams field_or_throw(int64_t p) {
     return F;
 }
 
-// validate_coeffs (run_util.hpp:24-29).
-void check_canonical(const uint32_t* c, int64_t n, uint32_t p, const char* who) {
+void check_operand(const uint32_t* c, int64_t n, const char* who) {
     if (n < 0) throw Error(ST_INVALID, std::string(who) + ": negative length");
     if (n > 0 && c == nullptr) throw Error(ST_INVALID, std::string(who) + ": null pointer");
+}
+
+// validate_coeffs (run_util.hpp:24-29).
+void check_canonical(const uint32_t* c, int64_t n, uint32_t p, const char* who) {
+    check_operand(c, n, who);
     // blockwise maximum without an early exit, so the scan vectorises (the
     // branchy per-word test was most of the host time of a large e2e call)
     for (int64_t i0 = 0; i0 < n; i0 += 8192) {
@@ -284,6 +298,66 @@ uint32_t* pinned_stage(size_t bytes) {
         buf = {p, n};
     }
     return static_cast<uint32_t*>(buf.first);
+}
+
+// Single host calls with large operands (> 2^18 words together)
+// validate them on the device, where they land (a host scan of a 2^20-term
+// operand cost more than its copy): one flag per operand, read back with the
+// results and reported after the synchronisation (outputs are then
+// unspecified, as for any failed call).  Any other error the call raises
+// first re-runs the host scan, so a non-canonical operand is still reported
+// ahead of it, as validate_coeffs comes first in the reference.  Smaller
+// operands are scanned on the host up front (errors before any device work).
+constexpr int64_t DEV_CHECK_WORDS = int64_t(1) << 18;
+struct DevCheck {
+    unsigned* flags = nullptr;
+    const char* who[2] = {nullptr, nullptr};
+    int n = 0;
+    cudaStream_t st;
+    DevCheck(Scratch& sc, cudaStream_t s) : st(s) {
+        flags = sc.get<unsigned>(2);
+        MMM_CUDA(cudaMemsetAsync(flags, 0, 2 * sizeof(unsigned), st));
+    }
+    void add(const uint32_t* d, int64_t len, uint32_t p, const char* w) {
+        if (len > 0) {
+            const unsigned blocks = unsigned(std::min<int64_t>(ceil_div(len, 2048), 2LL * sm_count()));
+            check_flat_kernel<<<blocks, 256, 0, st>>>(d, len, p, flags + n);
+            note_launch();  // counted, but not part of the program's schedule (SimReport)
+            cuda_check(cudaGetLastError(), "check_flat_kernel");
+        }
+        who[n++] = w;
+    }
+    uint32_t* stage() {  // the flags' copy, with the results
+        uint32_t* h = pinned_stage(16);
+        MMM_CUDA(cudaMemcpyAsync(h, flags, 2 * sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+        return h;
+    }
+    void report(const uint32_t* h) const {  // after the synchronisation
+        for (int i = 0; i < n; ++i)
+            if (h[i])
+                throw Error(ST_INVALID,
+                            std::string(who[i]) + ": coefficients must be canonical field elements");
+    }
+};
+
+// A single host call's device part: both operands uploaded and checked where
+// they land, `body` launches the kernels and queues the result copies, one
+// synchronisation, then the check's verdict.
+template <class Body>
+void checked_call(cudaStream_t st, bool dev_check, uint32_t p, const uint32_t* a, int64_t na,
+                  const char* wa, const uint32_t* b, int64_t nb, const char* wb, Body body) {
+    Scratch sc(st);
+    const uint32_t* da = to_device(sc, a, na);
+    const uint32_t* db = to_device(sc, b, nb);
+    DevCheck chk(sc, st);
+    if (dev_check) {  // (else the caller scanned on the host)
+        chk.add(da, na, p, wa);
+        chk.add(db, nb, p, wb);
+    }
+    body(sc, da, db);
+    const uint32_t* h = chk.stage();
+    sync(st);
+    chk.report(h);
 }
 
 cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
@@ -557,23 +631,37 @@ int mmm_cu_mul(int64_t p, const uint32_t* a, int64_t na, const uint32_t* b, int6
     return guarded([&] {
         schedule_reset();
         const FieldParams F = field_or_throw(p);
-        check_canonical(a, na, F.p, "multiplication first operand");
-        check_canonical(b, nb, F.p, "multiplication second operand");
+        const char* wa = "multiplication first operand";
+        const char* wb = "multiplication second operand";
+        check_operand(a, na, wa);
+        check_operand(b, nb, wb);
+        const int64_t na0 = na, nb0 = nb;
+        auto host_scan = [&] {
+            check_canonical(a, na0, F.p, wa);
+            check_canonical(b, nb0, F.p, wb);
+        };
+        const bool scanned = na0 + nb0 <= DEV_CHECK_WORDS;
+        if (scanned) host_scan();
+        *nf = 0;
         na = trimmed_len(a, na);
         nb = trimmed_len(b, nb);
-        *nf = 0;
-        if (na == 0 || nb == 0) return;  // oracle.cpp:9
-        need_cap(f_cap, na + nb - 1, "multiplication");
-        cudaStream_t st = thread_stream();
-        {
-            Scratch sc(st);
-            const uint32_t* da = to_device(sc, a, na);
-            const uint32_t* db = to_device(sc, b, nb);
-            uint32_t* df = sc.get<uint32_t>(size_t(na + nb - 1));
-            launch_mul(F, da, na, db, nb, df, s, l, st);
-            to_host(f, df, na + nb - 1, st);
+        if (na == 0 || nb == 0) {  // oracle.cpp:9
+            host_scan();
+            return;
         }
-        sync(st);
+        try {
+            need_cap(f_cap, na + nb - 1, "multiplication");
+        } catch (Error&) {
+            host_scan();
+            throw;
+        }
+        cudaStream_t st = thread_stream();
+        checked_call(st, !scanned, F.p, a, na, wa, b, nb, wb,
+                     [&](Scratch& sc, const uint32_t* da, const uint32_t* db) {
+                         uint32_t* df = sc.get<uint32_t>(size_t(na + nb - 1));
+                         launch_mul(F, da, na, db, nb, df, s, l, st);
+                         to_host(f, df, na + nb - 1, st);
+                     });
         *nf = trimmed_len(f, na + nb - 1);
     });
 }
@@ -754,33 +842,45 @@ int mmm_cu_divmod(int64_t p, const uint32_t* a, int64_t na, const uint32_t* b, i
     return guarded([&] {
         schedule_reset();
         const FieldParams F = field_or_throw(p);
-        check_canonical(a, na, F.p, "division dividend");
-        check_canonical(b, nb, F.p, "division divisor");
+        const char* wa = "division dividend";
+        const char* wb = "division divisor";
+        check_operand(a, na, wa);
+        check_operand(b, nb, wb);
+        const int64_t na0 = na;
+        auto host_scan = [&] {  // the paths below that raise or return before the device
+            check_canonical(a, na0, F.p, wa);
+            check_canonical(b, nb, F.p, wb);
+        };
+        const bool scanned = na0 + nb <= DEV_CHECK_WORDS;
+        if (scanned) host_scan();
         *nq = *nr = 0;
         // oracle.cpp:52-55: b is used as given; a is trimmed.
-        if (nb == 0) throw Error(ST_DOMAIN, "divmod: division by the zero polynomial");
-        na = trimmed_len(a, na);
-        if (na < nb) {
-            need_cap(r_cap, na, "division remainder");
-            if (na) std::memcpy(r, a, size_t(na) * 4);
-            *nr = na;
-            return;
+        try {
+            if (nb == 0) throw Error(ST_DOMAIN, "divmod: division by the zero polynomial");
+            na = trimmed_len(a, na);
+            if (na < nb) {
+                host_scan();
+                need_cap(r_cap, na, "division remainder");
+                if (na) std::memcpy(r, a, size_t(na) * 4);
+                *nr = na;
+                return;
+            }
+            if (b[nb - 1] == 0) throw Error(ST_DOMAIN, "field: inverse of zero");
+            need_cap(q_cap, na - nb + 1, "division quotient");
+            need_cap(r_cap, nb - 1, "division remainder");
+        } catch (Error&) {
+            host_scan();
+            throw;
         }
-        if (b[nb - 1] == 0) throw Error(ST_DOMAIN, "field: inverse of zero");
-        need_cap(q_cap, na - nb + 1, "division quotient");
-        need_cap(r_cap, nb - 1, "division remainder");
         cudaStream_t st = thread_stream();
-        {
-            Scratch sc(st);
-            const uint32_t* da = to_device(sc, a, na);
-            const uint32_t* db = to_device(sc, b, nb);
-            uint32_t* dq = sc.get<uint32_t>(size_t(na - nb + 1));
-            uint32_t* dr = sc.get<uint32_t>(size_t(nb));
-            launch_divmod(F, da, na, db, nb, dq, dr, s, st);
-            to_host(q, dq, na - nb + 1, st);
-            to_host(r, dr, nb - 1, st);
-        }
-        sync(st);
+        checked_call(st, !scanned, F.p, a, na, wa, b, nb, wb,
+                     [&](Scratch& sc, const uint32_t* da, const uint32_t* db) {
+                         uint32_t* dq = sc.get<uint32_t>(size_t(na - nb + 1));
+                         uint32_t* dr = sc.get<uint32_t>(size_t(nb));
+                         launch_divmod(F, da, na, db, nb, dq, dr, s, st);
+                         to_host(q, dq, na - nb + 1, st);
+                         to_host(r, dr, nb - 1, st);
+                     });
         *nq = trimmed_len(q, na - nb + 1);
         *nr = trimmed_len(r, nb - 1);
     });
@@ -815,32 +915,44 @@ int mmm_cu_divmod_fast(int64_t p, const uint32_t* a, int64_t na, const uint32_t*
     return guarded([&] {  // validation and results exactly as mmm_cu_divmod
         schedule_reset();
         const FieldParams F = field_or_throw(p);
-        check_canonical(a, na, F.p, "division dividend");
-        check_canonical(b, nb, F.p, "division divisor");
+        const char* wa = "division dividend";
+        const char* wb = "division divisor";
+        check_operand(a, na, wa);
+        check_operand(b, nb, wb);
+        const int64_t na0 = na;
+        auto host_scan = [&] {  // the paths below that raise or return before the device
+            check_canonical(a, na0, F.p, wa);
+            check_canonical(b, nb, F.p, wb);
+        };
+        const bool scanned = na0 + nb <= DEV_CHECK_WORDS;
+        if (scanned) host_scan();
         *nq = *nr = 0;
-        if (nb == 0) throw Error(ST_DOMAIN, "divmod: division by the zero polynomial");
-        na = trimmed_len(a, na);
-        if (na < nb) {
-            need_cap(r_cap, na, "division remainder");
-            if (na) std::memcpy(r, a, size_t(na) * 4);
-            *nr = na;
-            return;
+        try {
+            if (nb == 0) throw Error(ST_DOMAIN, "divmod: division by the zero polynomial");
+            na = trimmed_len(a, na);
+            if (na < nb) {
+                host_scan();
+                need_cap(r_cap, na, "division remainder");
+                if (na) std::memcpy(r, a, size_t(na) * 4);
+                *nr = na;
+                return;
+            }
+            if (b[nb - 1] == 0) throw Error(ST_DOMAIN, "field: inverse of zero");
+            need_cap(q_cap, na - nb + 1, "division quotient");
+            need_cap(r_cap, nb - 1, "division remainder");
+        } catch (Error&) {
+            host_scan();
+            throw;
         }
-        if (b[nb - 1] == 0) throw Error(ST_DOMAIN, "field: inverse of zero");
-        need_cap(q_cap, na - nb + 1, "division quotient");
-        need_cap(r_cap, nb - 1, "division remainder");
         cudaStream_t st = thread_stream();
-        {
-            Scratch sc(st);
-            const uint32_t* da = to_device(sc, a, na);
-            const uint32_t* db = to_device(sc, b, nb);
-            uint32_t* dq = sc.get<uint32_t>(size_t(na - nb + 1));
-            uint32_t* dr = sc.get<uint32_t>(size_t(nb));
-            launch_divmod_fast(F, da, na, db, nb, dq, dr, st);
-            to_host(q, dq, na - nb + 1, st);
-            to_host(r, dr, nb - 1, st);
-        }
-        sync(st);
+        checked_call(st, !scanned, F.p, a, na, wa, b, nb, wb,
+                     [&](Scratch& sc, const uint32_t* da, const uint32_t* db) {
+                         uint32_t* dq = sc.get<uint32_t>(size_t(na - nb + 1));
+                         uint32_t* dr = sc.get<uint32_t>(size_t(nb));
+                         launch_divmod_fast(F, da, na, db, nb, dq, dr, st);
+                         to_host(q, dq, na - nb + 1, st);
+                         to_host(r, dr, nb - 1, st);
+                     });
         *nq = trimmed_len(q, na - nb + 1);
         *nr = trimmed_len(r, nb - 1);
     });
@@ -957,25 +1069,39 @@ int mmm_cu_ntt_mul(int64_t p, const uint32_t* a, int64_t na, const uint32_t* b, 
     return guarded([&] {
         schedule_reset();
         const FieldParams F = field_or_throw(p);
-        check_canonical(a, na, F.p, "ntt first operand");
-        check_canonical(b, nb, F.p, "ntt second operand");
+        const char* wa = "ntt first operand";
+        const char* wb = "ntt second operand";
+        check_operand(a, na, wa);
+        check_operand(b, nb, wb);
+        const int64_t na0 = na, nb0 = nb;
+        auto host_scan = [&] {
+            check_canonical(a, na0, F.p, wa);
+            check_canonical(b, nb0, F.p, wb);
+        };
+        const bool scanned = na0 + nb0 <= DEV_CHECK_WORDS;
+        if (scanned) host_scan();
+        *nf = 0;
         na = trimmed_len(a, na);
         nb = trimmed_len(b, nb);
-        *nf = 0;
-        if (na == 0 || nb == 0) return;
-        if (!ntt_supported(F.p, na + nb - 1))
-            throw Error(ST_INVALID, "ntt: p has no 2-adic root of unity of the needed order");
-        need_cap(f_cap, na + nb - 1, "ntt");
-        cudaStream_t st = thread_stream();
-        {
-            Scratch sc(st);
-            const uint32_t* da = to_device(sc, a, na);
-            const uint32_t* db = to_device(sc, b, nb);
-            uint32_t* df = sc.get<uint32_t>(size_t(na + nb - 1));
-            launch_ntt_mul(F, da, na, db, nb, df, st);
-            to_host(f, df, na + nb - 1, st);
+        if (na == 0 || nb == 0) {
+            host_scan();
+            return;
         }
-        sync(st);
+        try {
+            if (!ntt_supported(F.p, na + nb - 1))
+                throw Error(ST_INVALID, "ntt: p has no 2-adic root of unity of the needed order");
+            need_cap(f_cap, na + nb - 1, "ntt");
+        } catch (Error&) {
+            host_scan();
+            throw;
+        }
+        cudaStream_t st = thread_stream();
+        checked_call(st, !scanned, F.p, a, na, wa, b, nb, wb,
+                     [&](Scratch& sc, const uint32_t* da, const uint32_t* db) {
+                         uint32_t* df = sc.get<uint32_t>(size_t(na + nb - 1));
+                         launch_ntt_mul(F, da, na, db, nb, df, st);
+                         to_host(f, df, na + nb - 1, st);
+                     });
         *nf = trimmed_len(f, na + nb - 1);
     });
 }

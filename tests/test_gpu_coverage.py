@@ -316,6 +316,38 @@ def test_default_results_from_the_pinned_pool(cuda_lib, port):
     assert mmm.load().mmm_cu_host_free(ctypes.addressof(bogus)) == mmm.InvalidArgument.status
 
 
+def test_large_operands_validated_on_the_device(cuda_lib):
+    """Single calls with operands past 2^18 words check canonical coefficients on
+    the device (after the copy) and still raise InvalidArgument -- also when the
+    bad word sits under trailing zeros that trimming drops below the threshold,
+    and ahead of a domain error (validate_coeffs comes first,
+    run_util.hpp:24-29)."""
+    mmm = cuda_lib
+    rng = np.random.default_rng(61)
+    big = rng.integers(0, P, 300_000).astype(np.uint32)
+    big[-1] = 5
+    bad = big.copy()
+    bad[12345] = P  # one word equal to p
+    small = rng.integers(0, P, 3_000).astype(np.uint32)
+    small[-1] = 7
+    for fn in (lambda: mmm.mul(bad, small, P), lambda: mmm.mul(small, bad, P),
+               lambda: mmm.ntt_mul(bad, small, P), lambda: mmm.divmod(bad, small, P, s=64),
+               lambda: mmm.divmod_fast(bad, small, P), lambda: mmm.divmod(big, np.append(small[:-1], P), P)):
+        with pytest.raises(mmm.InvalidArgument):
+            fn()
+    hidden = np.zeros(300_000, np.uint32)  # 1000 words after trimming, 300k before
+    hidden[:1000] = rng.integers(0, P, 1000)
+    hidden[999] = 3
+    hidden[10] = P + 1
+    with pytest.raises(mmm.InvalidArgument):
+        mmm.mul(hidden, small, P)
+    zero_lead = np.append(small[:-1], 0).astype(np.uint32)  # divisor lead 0: a domain error ...
+    with pytest.raises(mmm.InvalidArgument):  # ... but the dividend is checked first
+        mmm.divmod(bad, zero_lead, P)
+    f = mmm.mul(big, small, P)  # the valid operands still go through
+    assert f.size == big.size + small.size - 1
+
+
 def test_last_schedule_reports_the_launches(cuda_lib, port):
     """mmm_cu_last_schedule: the kernels of the thread's last host call (what
     the drop-in's SimReport.kernels and N/L/K are built from)."""
