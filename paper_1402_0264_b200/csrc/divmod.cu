@@ -261,10 +261,15 @@ __global__ void __launch_bounds__(DIV_T) div_grid_kernel(DivArgs g, int64_t seg)
 #else
 #define PIPE_CONV(x) x
 #endif
+// Bulk lag (steps the head absorbs): the kernel is instantiated for the split
+// head's lag (DIV_PIPE_L, 2: best measured for it) and the M-form head's
+// (DIV_PIPE_LM, 4: its cheaper steps leave room for a longer hand-off).
 #ifndef DIV_PIPE_L
 #define DIV_PIPE_L 2
 #endif
-constexpr int PIPE_L = DIV_PIPE_L;  // bulk lag (steps) the head absorbs
+#ifndef DIV_PIPE_LM
+#define DIV_PIPE_LM 4
+#endif
 #ifndef DIV_PIPE_CT
 #define DIV_PIPE_CT 256
 #endif
@@ -287,6 +292,7 @@ struct PipeArgs {
     unsigned* progress;     // per bulk CTA: steps applied to all of its blocks
     long long* stats;       // optional (MMM_DIV_STATS): cycle counters
     bool b_smem;            // bulk CTAs hold all of b in shared memory
+    bool mform;             // head: pipe_head_m (S = 128, odd p, fold_terms >= 16)
 };
 
 namespace {
@@ -406,8 +412,9 @@ __device__ __forceinline__ void tiled_sum(int NQ, int P, uint32_t* red, Item ite
 #ifndef DIV_PIPE_AW
 #define DIV_PIPE_AW 4
 #endif
+template <int L>
 __device__ void pipe_head_split(const PipeArgs& g, uint32_t* sm, int nbulk) {
-    constexpr int L = PIPE_L, LR = PIPE_L + 1, CT = PIPE_CT;
+    constexpr int LR = L + 1, CT = PIPE_CT;
     constexpr int AT = 32 * DIV_PIPE_AW, BT = CT - AT;
     static_assert(L >= 1 && AT > 0 && BT > 0, "pipe_head_split: both groups non-empty");
     constexpr int BAR_A = 1, BAR_B = 2, BAR_LAM = 3, BAR_ENT = 5, BAR_STG = 7;
@@ -603,6 +610,316 @@ __device__ void pipe_head_split(const PipeArgs& g, uint32_t* sm, int nbulk) {
     }
 }
 
+// pipe_head_m: the head with one product per step on its chain (S = 128).
+// With Z_j = step j's heads before step j-1's update (steps <= j-2 applied)
+// and the step's negated lambdas nl_j = -lambda_j,
+//   lambda_j = T_h Z_j + Mb nl_{j-1},
+//   Mb[r][k] = sum_{t <= r} h[r - t] b[db - S - t + k]   (T_h: lower-triangular
+//   Toeplitz of h; Mb: step j-1's update of step j's heads, solved by T_h),
+// and Z_{j+2} is exactly step j's entering words (positions [2S, 3S) below
+// step j's top, steps <= j applied).  So the old chain -- lambda_j, then the
+// window update that forms step j+1's heads -- becomes one pass: Mb sits in
+// the compute threads' registers (a 4 x 16 block each, Montgomery form, built
+// once by a diagonal walk Mb[r][k] = Mb[r-1][k-1] + h[r] b[db - S + k]), the
+// window is never materialised, and after the last step the top 2S remainder
+// words are formed from the last Z's and lambdas.  All eight compute warps run
+// the chain and then the entering words; the control warp stages as before.
+constexpr int PIPE_HS_OFF = 16384;  // head: h computed here (words; the head layout ends below)
+constexpr int MF_S = 128;
+constexpr int MST_OFF = PIPE_HS_OFF + 512;  // the walk's staging of Mb (S x S words)
+template <int L>
+__device__ void pipe_head_m(const PipeArgs& g, uint32_t* sm, int nbulk) {
+    constexpr int S = MF_S, LR = L + 1, CT = PIPE_CT, WH = 2 * S;
+    constexpr int logS = 7;
+    static_assert(CT == 256 && L >= 2 && L <= 4, "pipe_head_m: eight compute warps, lag 2..4");
+    constexpr int BAR_C = 1, BAR_LAM = 3, BAR_STG = 7;  // LAM / STG by step parity
+    constexpr int MB = (L + 2) * S + 16;
+    const FieldParams F = g.F;
+    const int tid = threadIdx.x;
+    const int64_t na = g.na, db = g.nb - 1;
+    const int64_t J = (na - db + S - 1) / S;
+    const bool control = tid >= CT;
+    uint32_t* hz = sm;                // hz[S + m] = h[m], zeros around
+    uint32_t* lamh = hz + 2 * S + 8;  // LR x S negated lambdas, ring by step
+    uint32_t* stage = lamh + LR * S;  // 2 x S entering words (control warp)
+    uint32_t* bt3 = stage + 2 * S;    // bt3[3 + m] = b[db - m]
+    uint32_t* Zr = bt3 + MB;          // 3 x S: Z_j in slot j % 3
+    uint32_t* part = Zr + 3 * S;      // 8 x S chain partials
+    uint32_t* red = part + 8 * S;     // tiled_sum partials (8 x 4 x 32)
+    uint32_t* tmpu = red + 1024;      // S
+    uint32_t* bw = tmpu + S;          // S: b[db - S + k] 2^64 mod p
+    uint32_t* bx = bw + S;            // bx[m] = b[db - m], m < (L+2) S (16-byte aligned windows)
+    uint32_t* Mst = sm + MST_OFF;
+    for (int m = tid; m < 2 * S + 8; m += PIPE_T) {
+        const int j = m - S;
+        hz[m] = (j >= 0 && j < S) ? __ldcg(g.h_glob + j) : 0u;
+    }
+    for (int m = tid; m < MB; m += PIPE_T) {
+        const int64_t x = db - (m - 3);
+        bt3[m] = (m >= 3 && x >= 0) ? g.b[x] : 0u;
+        if (m >= 3 && m < (L + 2) * S + 3) bx[m - 3] = (x >= 0) ? g.b[x] : 0u;
+    }
+    for (int m = tid; m < LR * S; m += PIPE_T) lamh[m] = 0u;
+    {  // Z_0 and Z_1: the top 2S words, no step applied
+        const int64_t i0 = na - 1;
+        for (int t = tid; t < WH; t += PIPE_T) {
+            const int64_t x = i0 - t;
+            Zr[t] = x >= 0 ? __ldcg(g.A + x) : 0u;  // slot 0 = Z_0, slot 1 = Z_1
+        }
+    }
+    long long c_poll = 0;
+    auto stage_entering = [&](int64_t jj) {  // as in pipe_head_split
+        const int64_t hi = pipe_i(na, db, S, jj) - WH, lo = pipe_i(na, db, S, jj + 1) - WH + 1;
+        if (hi < 0 || hi < lo) return;
+        const int lane = tid & 31;
+        const int64_t need = jj - L + 1;
+        if (need > 0) {  // the whole warp polls the owners of both ends
+            const int64_t x = (lane & 1) == 0 ? (lo > 0 ? lo : 0) : hi;
+            const unsigned* pw = g.progress + int((x / PIPE_B) % nbulk);
+            const long long cp = clock64();
+#ifndef PIPE_DBG_NOSPIN  // timing experiments: no wait for the bulk (wrong results)
+            while (__any_sync(0xffffffffu, ld_relaxed_gpu(pw) < unsigned(need))) {
+            }
+            (void)spin_until_geq(pw, unsigned(need));  // the acquiring load
+#endif
+            c_poll += clock64() - cp;
+        }
+        __syncwarp();
+        uint32_t* st = stage + (jj & 1) * S;
+        for (int64_t x = lo + lane; x <= hi; x += 32) st[x - lo] = x >= 0 ? __ldcg(g.A + x) : 0u;
+    };
+    if (control) stage_entering(0);
+    __syncthreads();
+    long long c_loop = clock64(), c_mv = 0, c_ent = 0, c_wait = 0, c_build = 0, c_ts = 0;
+    if (control) {
+        for (int64_t j = 0; j < J; ++j) {
+            bar_sync_n(BAR_LAM + int(j & 1), PIPE_T);
+            if (j + 1 < J) {
+                stage_entering(j + 1);
+                bar_arrive_n(BAR_STG + int((j + 1) & 1), PIPE_T);
+            }
+        }
+    } else {
+        const long long cb = clock64();
+        // ---- Mb in Montgomery form (x 2^32), by a diagonal walk through Mst ----
+        if (tid < S) {
+            bw[tid] = reduce_odd(uint64_t(bt3[3 + S - tid]) * F.r2, F);  // b[db - S + k] R^2
+            uint64_t u = 0;  // Mb[r][0] = sum_{t <= r} h[r - t] b[db - S - t]
+            uint32_t since = 0;
+            for (int t = 0; t <= tid; ++t) {
+                if (++since > F.fold_terms) {
+                    u = fold(u, F);
+                    since = 1;
+                }
+                u = mad_wide(hz[S + tid - t], bt3[3 + S + t], u);
+            }
+            tmpu[tid] = reduce_odd(uint64_t(reduce_odd(u, F)) * F.r2, F);
+        }
+        bar_sync_n(BAR_C, CT);
+        auto at = [](int r, int k) { return r * S + (k ^ (((r >> 2) & 7) << 2)); };
+        {
+            const int dl = tid - 127;
+            if (dl < 128) {
+                const int r = dl >= 0 ? dl : 0, k = dl >= 0 ? 0 : -dl;
+                uint64_t acc = dl >= 0 ? uint64_t(tmpu[dl]) : uint64_t(hz[S]) * bw[k];
+                Mst[at(r, k)] = redc(fold(acc, F), F);
+                const int len = 128 - (dl >= 0 ? dl : -dl);
+                acc = fold(acc, F);
+                int i = 1;
+                for (; i + 16 <= len; i += 16) {
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) {
+                        acc = mad_wide(hz[S + r + i + q], bw[k + i + q], acc);
+                        Mst[at(r + i + q, k + i + q)] = redc(fold(acc, F), F);
+                    }
+                    acc = fold(acc, F);
+                }
+                for (; i < len; ++i) {
+                    acc = mad_wide(hz[S + r + i], bw[k + i], acc);
+                    Mst[at(r + i, k + i)] = redc(fold(acc, F), F);
+                }
+            }
+        }
+        bar_sync_n(BAR_C, CT);
+        const int gq = tid & 31, pq = tid >> 5;
+        uint32_t mm[4][16], hw[19];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) {
+                const uint4 w4 = *reinterpret_cast<const uint4*>(
+                    Mst + (4 * gq + k) * S + ((16 * pq + 4 * jj) ^ ((gq & 7) << 2)));
+                mm[k][4 * jj] = w4.x;
+                mm[k][4 * jj + 1] = w4.y;
+                mm[k][4 * jj + 2] = w4.z;
+                mm[k][4 * jj + 3] = w4.w;
+            }
+#pragma unroll
+        for (int i = 0; i < 19; ++i) hw[i] = hz[S + 4 * gq - 16 * pq - 15 + i];
+        bar_sync_n(BAR_C, CT);
+        c_build = clock64() - cb;
+        // ring slots kept incrementally (no 64-bit modulo per step): Z by j % 3, the
+        // lambda history by j % LR
+        int r0 = 0, l0 = 0;
+        for (int64_t j = 0; j < J; ++j, r0 = r0 == 2 ? 0 : r0 + 1, l0 = l0 == LR - 1 ? 0 : l0 + 1) {
+            const int rp2 = r0 == 0 ? 2 : r0 - 1;                   // (j + 2) % 3
+            const int lm1 = l0 == 0 ? LR - 1 : l0 - 1;              // (j - 1) % LR
+            const int64_t i = pipe_i(na, db, S, j), inext = pipe_i(na, db, S, j + 1);
+            const int v = int(i - inext);
+            const long long p0 = clock64();
+            // ---- the chain: lambda_j = T_h Z_j + Mb nl_{j-1} ----
+            {
+                const uint32_t* zj = Zr + r0 * S + 16 * pq;
+                const uint32_t* np = lamh + lm1 * S + 16 * pq;  // zeros at j = 0
+                uint32_t z[16], q[16];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const uint4 zv = *reinterpret_cast<const uint4*>(zj + 4 * c);
+                    const uint4 qv = *reinterpret_cast<const uint4*>(np + 4 * c);
+                    z[4 * c] = zv.x; z[4 * c + 1] = zv.y; z[4 * c + 2] = zv.z; z[4 * c + 3] = zv.w;
+                    q[4 * c] = qv.x; q[4 * c + 1] = qv.y; q[4 * c + 2] = qv.z; q[4 * c + 3] = qv.w;
+                }
+                uint64_t a1[4] = {0, 0, 0, 0}, a2[4] = {0, 0, 0, 0};
+#pragma unroll
+                for (int jj = 0; jj < 16; ++jj)
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        a1[k] = mad_wide(hw[k - jj + 15], z[jj], a1[k]);
+                        a2[k] = mad_wide(mm[k][jj], q[jj], a2[k]);
+                    }
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    part[pq * S + 4 * gq + k] = reduce_odd(a1[k], F) + redc(fold(a2[k], F), F);
+            }
+            bar_sync_n(BAR_C, CT);
+            if (tid < S) {
+                uint64_t sum = 0;
+#pragma unroll
+                for (int pp = 0; pp < 8; ++pp) sum += part[pp * S + tid];
+                const uint32_t lam = reduce_odd(sum, F);
+                const int k = tid;
+                const uint32_t nl = k < v ? negmod(lam, F) : 0u;
+                if (k < v) {
+                    g.q[i - db - k] = lam;
+                    pipe_st_tag(g.lam_t + j * S + k, nl, unsigned(j + 1));
+                }
+                lamh[l0 * S + k] = nl;
+            }
+            bar_sync_n(BAR_C, CT);
+            bar_arrive_n(BAR_LAM + int(j & 1), PIPE_T);
+            const long long p1 = clock64();
+            c_mv += p1 - p0;
+            if (j >= 1) bar_sync_n(BAR_STG + int(j & 1), PIPE_T);  // E_j staged
+            const long long p2 = clock64();
+            c_wait += p2 - p1;
+            // ---- entering_j -> Z_{j+2}: stage + steps j - 1 .. j ----
+            // value[tt] = st + sum_{d<L} sum_k nl_{j-d}[k] b[db - (2S + tt + dS - k)]: thread
+            // (gq, pq) takes rows 4gq..4gq+3 and the 16 L combined terms c in
+            // [16 L pq, +16 L) (c = dS + k), b in a sliding register window (16-byte loads
+            // from bx), 16 terms per chunk
+            {
+                uint64_t acc[4] = {0, 0, 0, 0};
+#pragma unroll
+                for (int hh = 0; hh < L; ++hh) {
+                    const int c = 16 * L * pq + 16 * hh, d = c >> logS, k0 = c & (S - 1);
+                    const int ld = l0 - d < 0 ? l0 - d + LR : l0 - d;  // (j - d) % LR
+                    const uint32_t* X = bx + 2 * S + d * S;           // X[i] = b[db - 2S - dS - i]
+                    const uint32_t* W = lamh + ld * S + k0;           // nl_{j-d}[k0 ..]
+                    uint32_t xw[20], wv[16];  // xw[i] = X[4gq - k0 - 16 + i]
+#pragma unroll
+                    for (int q4 = 0; q4 < 5; ++q4) {
+                        const uint4 t4 = *reinterpret_cast<const uint4*>(X + 4 * gq - k0 - 16 + 4 * q4);
+                        xw[4 * q4] = t4.x; xw[4 * q4 + 1] = t4.y; xw[4 * q4 + 2] = t4.z; xw[4 * q4 + 3] = t4.w;
+                    }
+#pragma unroll
+                    for (int q4 = 0; q4 < 4; ++q4) {
+                        const uint4 t4 = *reinterpret_cast<const uint4*>(W + 4 * q4);
+                        wv[4 * q4] = t4.x; wv[4 * q4 + 1] = t4.y; wv[4 * q4 + 2] = t4.z; wv[4 * q4 + 3] = t4.w;
+                    }
+#pragma unroll
+                    for (int jj = 0; jj < 16; ++jj)
+#pragma unroll
+                        for (int k = 0; k < 4; ++k)  // X[4gq + k - (k0 + jj)]
+                            acc[k] = mad_wide(xw[k - jj + 16], wv[jj], acc[k]);
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) acc[k] = fold(acc[k], F);  // 16 terms per chunk
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k) part[pq * S + 4 * gq + k] = reduce_odd(acc[k], F);
+                bar_sync_n(BAR_C, CT);
+                if (tid < S) {
+                    const int tt = tid;
+                    uint64_t sum = 0;
+#pragma unroll
+                    for (int pp = 0; pp < 8; ++pp) sum += part[pp * S + tt];
+                    const uint32_t add = reduce_odd(sum, F);
+                    const uint32_t* st = stage + (j & 1) * S;
+                    const int64_t x = i - WH - tt;
+                    if (tt < v) Zr[rp2 * S + tt] = x >= 0 ? addmod(st[v - 1 - tt], add, F) : 0u;
+                }
+            }
+            c_ts += clock64() - p2;
+            bar_sync_n(BAR_C, CT);
+            c_ent += clock64() - p2;
+        }
+        // ---- the top 2S remainder words below the last heads (x = db - 1 - t) ----
+        // t < S - v: Z_{J-1}[t + v] + steps J-2, J-1;  t < 2S - v: Z_J[t - S + v] + step
+        // J-1;  else Z_{J+1}[t - 2S + v] (every step applied)
+        {
+            const int64_t iJ1 = pipe_i(na, db, S, J - 1);
+            const int v = int(iJ1 - (db - 1));
+            const int t = tid;  // 2S outputs, one per compute thread
+            const int64_t x = db - 1 - t;
+            const uint32_t* n1 = lamh + int((J - 1) % LR) * S;  // (zero-initialised slots:
+            const uint32_t* n2 = lamh + int((J - 2) % LR) * S;  //  J >= 3 here)
+            auto bb = [&](int m) { return m < 0 ? 0u : bt3[3 + m]; };  // b[db - m]
+            uint32_t base;
+            int steps;
+            if (t < S - v) {
+                base = Zr[int((J - 1) % 3) * S + t + v];
+                steps = 2;
+            } else if (t < 2 * S - v) {
+                base = Zr[int(J % 3) * S + t - S + v];
+                steps = 1;
+            } else {
+                base = Zr[int((J + 1) % 3) * S + t - 2 * S + v];
+                steps = 0;
+            }
+            uint64_t acc = 0;
+            uint32_t since = 0;
+            if (steps >= 1)
+                for (int kk = 0; kk < S; ++kk) {  // step J-1: b[db - (t + v) + kk]
+                    if (++since > F.fold_terms) {
+                        acc = fold(acc, F);
+                        since = 1;
+                    }
+                    acc = mad_wide(n1[kk], bb(t + v - kk), acc);
+                }
+            if (steps >= 2)
+                for (int kk = 0; kk < S; ++kk) {  // step J-2: b[db - (t + v + S) + kk]
+                    if (++since > F.fold_terms) {
+                        acc = fold(acc, F);
+                        since = 1;
+                    }
+                    acc = mad_wide(n2[kk], bb(t + v + S - kk), acc);
+                }
+            if (x >= 0) __stcg(g.A + x, addmod(base, reduce_odd(acc, F), F));
+        }
+    }
+    if (g.stats && tid == 0) {
+        g.stats[0] = J;
+        g.stats[1] = clock64() - c_loop;
+        g.stats[8] = c_mv;
+        g.stats[9] = c_build;
+        g.stats[10] = c_ent;
+        g.stats[11] = c_wait;
+        g.stats[3] = c_ts;
+    }
+    if (g.stats && tid == CT) g.stats[4] = c_poll;
+    if (g.stats && tid == 33) g.stats[2] = c_ts;
+    __syncthreads();
+}
+
 // Bulk shared layout (words): lam [PIPE_MAXB * S + 4] | bw [PIPE_B + S + 8,
 // padded] | bz [nb + 2 * PIPE_PADB] when the whole divisor fits (g.b_smem):
 // bz[PIPE_PADB + x] = b[x], zero outside [0, db], loaded once per launch, so
@@ -613,7 +930,6 @@ __host__ __device__ constexpr int64_t pipe_bulk_words(int S, int64_t nb, bool b_
            (b_smem ? nb + 2 * PIPE_PADB : 0);
 }
 
-constexpr int PIPE_HS_OFF = 16384;  // head: h computed here (words; the head layout ends below)
 
 __device__ void pipe_bulk_load_b(const PipeArgs& g, uint32_t* sm) {
     if (!g.b_smem) return;
@@ -626,8 +942,8 @@ __device__ void pipe_bulk_load_b(const PipeArgs& g, uint32_t* sm) {
     }
 }
 
+template <int L>
 __device__ void pipe_bulk(const PipeArgs& g, uint32_t* sm, int nbulk, int me) {
-    constexpr int L = PIPE_L;
     const FieldParams F = g.F;
     const int S = g.S, tid = threadIdx.x, WH = 2 * S;
     const int64_t na = g.na, db = g.nb - 1;
@@ -736,6 +1052,7 @@ __device__ void pipe_bulk(const PipeArgs& g, uint32_t* sm, int nbulk, int me) {
     }
 }
 
+template <int L>
 __global__ void __launch_bounds__(PIPE_T, 1) div_pipe_kernel(PipeArgs g) {
     extern __shared__ __align__(16) uint32_t smem[];
     cg::grid_group grid = cg::this_grid();
@@ -756,10 +1073,12 @@ __global__ void __launch_bounds__(PIPE_T, 1) div_pipe_kernel(PipeArgs g) {
     }
     grid.sync();
     const int nbulk = gridDim.x - 1;
-    if (blockIdx.x == 0)
-        pipe_head_split(g, smem, nbulk);
+    if (blockIdx.x == 0 && g.mform)
+        pipe_head_m<L>(g, smem, nbulk);
+    else if (blockIdx.x == 0)
+        pipe_head_split<L>(g, smem, nbulk);
     else
-        pipe_bulk(g, smem, nbulk, blockIdx.x - 1);
+        pipe_bulk<L>(g, smem, nbulk, blockIdx.x - 1);
     grid.sync();
     for (int64_t x = int64_t(blockIdx.x) * PIPE_T + threadIdx.x; x < db;
          x += int64_t(gridDim.x) * PIPE_T)
@@ -883,7 +1202,10 @@ void run_pipe(const DivArgs& d, int64_t s, cudaStream_t st) {
     g.nb = d.nb;
     g.S = S;
     g.F = d.F;
-    const int L = PIPE_L;
+    const int64_t Jm = (d.na - (d.nb - 1) + S - 1) / S;
+    g.mform = S == MF_S && d.F.odd && d.F.fold_terms >= 16 && Jm >= 3 && !getenv("MMM_DIV_PIPE_OLD");
+    const int L = g.mform ? DIV_PIPE_LM : DIV_PIPE_L;
+    auto kern = g.mform ? div_pipe_kernel<DIV_PIPE_LM> : div_pipe_kernel<DIV_PIPE_L>;
     const int horg = pipe_horg(S);
     const size_t head =
         size_t(((horg + S + 8 + 3) & ~3) + S + (L + 1) * S + 4 * S + 2 * S + (L + 2) * S + 16 + 4 * PIPE_CT);
@@ -891,12 +1213,12 @@ void run_pipe(const DivArgs& d, int64_t s, cudaStream_t st) {
     const size_t bulk = size_t(pipe_bulk_words(S, d.nb, g.b_smem));
     // more than half an SM's shared memory: one CTA per SM, so no bulk CTA
     // shares (and takes issue slots from) the head's SM
-    const size_t bytes = std::max<size_t>(std::max(std::max(head, bulk), size_t(PIPE_HS_OFF + S)) * 4,
-                                          120 * 1024);
-    MMM_CUDA(cudaFuncSetAttribute(div_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  int(bytes)));
+    const size_t head_m = g.mform ? size_t(MST_OFF + MF_S * MF_S) : 0;
+    const size_t bytes = std::max<size_t>(
+        std::max(std::max(std::max(head, bulk), head_m), size_t(PIPE_HS_OFF + S)) * 4, 120 * 1024);
+    MMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
     int per_sm = 0;
-    MMM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, div_pipe_kernel, PIPE_T, bytes));
+    MMM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, PIPE_T, bytes));
     if (per_sm < 1) throw Error(ST_SIM, "division: pipelined grid does not fit");
     // one CTA per SM (the head's SM to itself), no more bulk CTAs than blocks
     const int blocks = int(std::min<int64_t>(sm_count(), 1 + ceil_div(d.na, PIPE_B)));
@@ -914,8 +1236,8 @@ void run_pipe(const DivArgs& d, int64_t s, cudaStream_t st) {
         MMM_CUDA(cudaMemsetAsync(g.stats, 0, 12 * sizeof(long long), st));
     }
     void* params[] = {&g};
-    MMM_CUDA(cudaLaunchCooperativeKernel((void*)div_pipe_kernel, dim3(unsigned(blocks)),
-                                         dim3(PIPE_T), params, bytes, st));
+    MMM_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3(unsigned(blocks)), dim3(PIPE_T), params,
+                                         bytes, st));
     check_launch("div_pipe_kernel", dim3(unsigned(blocks)), dim3(PIPE_T));
     if (want_stats) {
         long long h[12];
