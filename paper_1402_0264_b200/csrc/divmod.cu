@@ -926,14 +926,14 @@ __device__ void pipe_head_m(const PipeArgs& g, uint32_t* sm, int nbulk) {
 // a step's b window is a shared-memory copy instead of an L2 round trip.
 constexpr int PIPE_PADB = PIPE_B + 264;
 __host__ __device__ constexpr int64_t pipe_bulk_words(int S, int64_t nb, bool b_smem) {
-    return int64_t(PIPE_MAXB) * S + 4 + ((PIPE_B + S + 8 + 3) & ~3) +
+    return int64_t(PIPE_MAXB) * S + 4 + ((PIPE_B + S + 8 + 3) & ~3) + 4 * PIPE_B +
            (b_smem ? nb + 2 * PIPE_PADB : 0);
 }
 
 
 __device__ void pipe_bulk_load_b(const PipeArgs& g, uint32_t* sm) {
     if (!g.b_smem) return;
-    uint32_t* bz = sm + PIPE_MAXB * g.S + 4 + ((PIPE_B + g.S + 8 + 3) & ~3);
+    uint32_t* bz = sm + PIPE_MAXB * g.S + 4 + ((PIPE_B + g.S + 8 + 3) & ~3) + 4 * PIPE_B;
     const int64_t n = g.nb + 2 * PIPE_PADB, db = g.nb - 1;
 #pragma unroll 8
     for (int64_t y = threadIdx.x; y < n; y += PIPE_T) {
@@ -951,15 +951,18 @@ __device__ void pipe_bulk(const PipeArgs& g, uint32_t* sm, int nbulk, int me) {
     const int64_t nblocks = (na + PIPE_B - 1) / PIPE_B;  // every position below the heads
     uint32_t* lam = sm;                          // per step of the pass: S reversed negated lambdas
     uint32_t* bw = lam + PIPE_MAXB * S + 4;      // b window: PIPE_B + S + 8 words
-    uint32_t* bz = bw + ((PIPE_B + S + 8 + 3) & ~3);
+    uint32_t* red = bw + ((PIPE_B + S + 8 + 3) & ~3);  // 4 parts x PIPE_B partial sums
+    uint32_t* bz = red + 4 * PIPE_B;
     const bool b_smem = g.b_smem;  // bz loaded by pipe_bulk_load_b before the grid barrier
     __shared__ unsigned pub_s;
     // 4 positions per thread, 4 parts over the step's terms: PIPE_B/4 x 4 = the
-    // first PIPE_B threads (whole warps; the ninth warp only stages and syncs)
+    // first PIPE_B threads (whole warps; the ninth warp only stages and syncs).
+    // A warp's lanes hold consecutive quads of one part (16-byte window reads of
+    // consecutive words: no bank conflicts); the parts meet in shared memory.
     static_assert(PIPE_B == PIPE_CT, "pipe_bulk: one quad x part per compute thread");
     const bool worker = tid < PIPE_B;
-    const int part = tid & 3, qd = tid >> 2;
-    long long c_wait = 0, c_work = 0, passes = 0;
+    const int part = tid / (PIPE_B / 4), qd = tid % (PIPE_B / 4);
+    long long c_wait = 0, c_work = 0, passes = 0, c_rel = 0, c_lam = 0;
     int64_t k = 0;
     while (k < J) {
         const long long tw = clock64();
@@ -976,6 +979,7 @@ __device__ void pipe_bulk(const PipeArgs& g, uint32_t* sm, int nbulk, int me) {
         c_wait += tb - tw;
         ++passes;
         const int64_t kend = min(int64_t(pub_s), k + int64_t(PIPE_MAXB));
+        const long long tl = clock64();
         // the pass's lambdas, once for all blocks: lam[(kk - k) * S + u] = nl_{v-1-u}
         for (int64_t kk = k; kk < kend; ++kk) {
             const int64_t ik = pipe_i(na, db, S, kk);
@@ -986,14 +990,14 @@ __device__ void pipe_bulk(const PipeArgs& g, uint32_t* sm, int nbulk, int me) {
                 lk[u] = kp >= 0 ? pipe_ld_tag(g.lam_t + kk * S + kp, unsigned(kk + 1)) : 0u;
             }
         }
+        if (tid == 0) c_lam += clock64() - tl;
         for (int64_t beta = me; beta < nblocks; beta += nbulk) {
             const int64_t blo = beta * PIPE_B, bhi = min(blo + int64_t(PIPE_B), na);
             const int64_t x0 = blo + 4 * qd;
-            const int64_t x = x0 + part;
-            // this thread's stored position, loaded ahead: only this CTA writes it
-            const uint32_t a_old = (worker && x < bhi) ? __ldcg(g.A + x) : 0u;
+            // this thread's stored position (blo + tid), loaded ahead: only this CTA writes it
+            const uint32_t a_old = (worker && blo + tid < bhi) ? __ldcg(g.A + blo + tid) : 0u;
             uint64_t acc[4] = {0, 0, 0, 0};  // sum of per-step canonical partials
-            bool touched = false, mine = false;  // mine: x0 + part got a step (store it)
+            bool touched = false;
             for (int64_t kk = k; kk < kend; ++kk) {
                 const int64_t ik = pipe_i(na, db, S, kk);
                 const int64_t v = ik - pipe_i(na, db, S, kk + 1);
@@ -1001,7 +1005,6 @@ __device__ void pipe_bulk(const PipeArgs& g, uint32_t* sm, int nbulk, int me) {
                 const int64_t top = min(pipe_i(na, db, S, kk + L) - int64_t(WH), ik - v);
                 if (bhi - 1 < xlo || blo > top) continue;  // uniform over the CTA
                 touched = true;
-                if (x >= xlo && x <= top) mine = true;
                 const int vp = int((v + 3) & ~3);
                 __syncthreads();  // previous step's window consumed (and the pass's lambdas in)
                 const int64_t bwlo = blo - ik + db + v - vp;  // bw[y] = b[bwlo + y]
@@ -1029,19 +1032,37 @@ __device__ void pipe_bulk(const PipeArgs& g, uint32_t* sm, int nbulk, int me) {
                     }
                 }
             }
-            if (!touched || !worker) continue;
-            uint32_t add[4];
-            quad_reduce(acc, 4, add, F);
-            const uint32_t ad = part == 0 ? add[0] : part == 1 ? add[1] : part == 2 ? add[2] : add[3];
-            // store only positions a step updated: the rest may belong to the
-            // head, whose final window must not be overwritten by a late pass
-            if (mine && x < bhi) __stcg(g.A + x, addmod(a_old, ad, F));
+            if (!touched) continue;  // (uniform over the CTA)
+            if (worker)
+#pragma unroll
+                for (int r = 0; r < 4; ++r) red[part * PIPE_B + 4 * qd + r] = reduce(acc[r], F);
+            __syncthreads();
+            if (worker) {
+                // position blo + tid: the four parts' sums; store only positions a step
+                // updated (the rest may belong to the head, whose final words must not
+                // be overwritten by a late pass)
+                const int64_t xp = blo + tid;
+                bool upd = false;
+                for (int64_t kk = k; kk < kend; ++kk) {
+                    const int64_t ik = pipe_i(na, db, S, kk);
+                    const int64_t v = ik - pipe_i(na, db, S, kk + 1);
+                    const int64_t top = min(pipe_i(na, db, S, kk + L) - int64_t(WH), ik - v);
+                    if (xp >= ik - v + 1 - db && xp <= top) upd = true;
+                }
+                if (upd && xp < bhi) {
+                    const uint64_t sum = uint64_t(red[tid]) + red[PIPE_B + tid] +
+                                         red[2 * PIPE_B + tid] + red[3 * PIPE_B + tid];
+                    __stcg(g.A + xp, addmod(a_old, reduce(sum, F), F));
+                }
+            }
         }
         __syncthreads();
+        const long long tr = clock64();
         if (tid == 0) {
             pipe_sc_fence();
             pipe_st_release(g.progress + me, unsigned(kend));
         }
+        c_rel += clock64() - tr;
         c_work += clock64() - tb;
         k = kend;
     }
@@ -1049,6 +1070,8 @@ __device__ void pipe_bulk(const PipeArgs& g, uint32_t* sm, int nbulk, int me) {
         g.stats[5] = c_wait;
         g.stats[6] = c_work;
         g.stats[7] = passes;
+        g.stats[12] = c_rel;
+        g.stats[13] = c_lam;
     }
 }
 
@@ -1232,23 +1255,23 @@ void run_pipe(const DivArgs& d, int64_t s, cudaStream_t st) {
     MMM_CUDA(cudaMemsetAsync(g.lam_t, 0, size_t(J) * S * sizeof(uint64_t), st));
     const bool want_stats = getenv("MMM_DIV_STATS") != nullptr;
     if (want_stats) {
-        g.stats = sc.get<long long>(12);
-        MMM_CUDA(cudaMemsetAsync(g.stats, 0, 12 * sizeof(long long), st));
+        g.stats = sc.get<long long>(16);
+        MMM_CUDA(cudaMemsetAsync(g.stats, 0, 16 * sizeof(long long), st));
     }
     void* params[] = {&g};
     MMM_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3(unsigned(blocks)), dim3(PIPE_T), params,
                                          bytes, st));
     check_launch("div_pipe_kernel", dim3(unsigned(blocks)), dim3(PIPE_T));
     if (want_stats) {
-        long long h[12];
+        long long h[16];
         MMM_CUDA(cudaMemcpyAsync(h, g.stats, sizeof(h), cudaMemcpyDeviceToHost, st));
         MMM_CUDA(cudaStreamSynchronize(st));
         fprintf(stderr,
                 "div pipe stats: S=%d blocks=%d steps=%lld head_loop=%lld ctl_stage=%lld "
                 "B_wait=%lld (ctl poll=%lld) | hd+lambda=%lld (waitA=%lld) window=%lld "
-                "entering=%lld | bulk0 wait=%lld work=%lld passes=%lld\n",
+                "entering=%lld | bulk0 wait=%lld work=%lld passes=%lld release=%lld lambdas=%lld\n",
                 S, blocks, h[0], h[1], h[2], h[3], h[4], h[8], h[11], h[9], h[10], h[5], h[6],
-                h[7]);
+                h[7], h[12], h[13]);
     }
 }
 
