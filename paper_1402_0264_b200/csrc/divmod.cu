@@ -991,6 +991,7 @@ __device__ void pipe_bulk(const PipeArgs& g, uint32_t* sm, int nbulk, int me) {
             }
         }
         if (tid == 0) c_lam += clock64() - tl;
+        __syncthreads();  // the pass's lambdas in
         for (int64_t beta = me; beta < nblocks; beta += nbulk) {
             const int64_t blo = beta * PIPE_B, bhi = min(blo + int64_t(PIPE_B), na);
             const int64_t x0 = blo + 4 * qd;
@@ -1006,24 +1007,30 @@ __device__ void pipe_bulk(const PipeArgs& g, uint32_t* sm, int nbulk, int me) {
                 if (bhi - 1 < xlo || blo > top) continue;  // uniform over the CTA
                 touched = true;
                 const int vp = int((v + 3) & ~3);
-                __syncthreads();  // previous step's window consumed (and the pass's lambdas in)
-                const int64_t bwlo = blo - ik + db + v - vp;  // bw[y] = b[bwlo + y]
-                if (b_smem) {
-                    for (int y = tid; y < PIPE_B + vp + 8; y += PIPE_T) bw[y] = bz[PIPE_PADB + bwlo + y];
-                } else {
-                    for (int y = tid; y < PIPE_B + vp + 8; y += PIPE_T) {
-                        const int64_t bx = bwlo + y;
-                        bw[y] = (bx >= 0 && bx <= db) ? __ldcg(g.b + bx) : 0u;
+                const int64_t bwlo = blo - ik + db + v - vp;  // window[y] = b[bwlo + y]
+                // b in shared memory at the window's alignment: read it in place (no copy,
+                // no barrier); otherwise stage the window
+                const bool direct = b_smem && ((PIPE_PADB + bwlo) & 3) == 0;
+                const uint32_t* win = direct ? bz + PIPE_PADB + bwlo : bw;
+                if (!direct) {
+                    __syncthreads();  // previous step's window consumed
+                    if (b_smem) {
+                        for (int y = tid; y < PIPE_B + vp + 8; y += PIPE_T) bw[y] = bz[PIPE_PADB + bwlo + y];
+                    } else {
+                        for (int y = tid; y < PIPE_B + vp + 8; y += PIPE_T) {
+                            const int64_t bx = bwlo + y;
+                            bw[y] = (bx >= 0 && bx <= db) ? __ldcg(g.b + bx) : 0u;
+                        }
                     }
+                    __syncthreads();
                 }
-                __syncthreads();
                 // part's terms: [u0, u0 + n), multiples of 4
                 const int span = ((vp / 4 + 3) & ~3) > 4 ? ((vp / 4 + 3) & ~3) : 4;
                 const int u0 = part * span;
                 if (worker && u0 < vp) {
                     uint64_t pa[4] = {0, 0, 0, 0};
                     uint32_t since = 0;
-                    conv_accumulate4_fast(pa, lam + (kk - k) * S + u0, min(span, vp - u0) / 4, bw,
+                    conv_accumulate4_fast(pa, lam + (kk - k) * S + u0, min(span, vp - u0) / 4, win,
                                           4 * qd + vp - 1 - u0, since, F);
 #pragma unroll
                     for (int r = 0; r < 4; ++r) {
