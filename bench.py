@@ -691,7 +691,8 @@ class DivWork(Workload):
                 "alg_bytes_per_launch": alg,
                 "imad_frac": self.units() / t_step / (imad or 8.0647e12),
                 "binding": f"{-(-self.nq // self.s)} dependent steps of s={self.s} heads "
-                           "(pipelined head CTA for s >= 32)"}
+                           "(pipelined head CTA for s >= 32; at s = 128 one product per step "
+                           "on the head, bound by the head -> bulk -> head hand-off)"}
 
     def cpu_ref(self, orc):
         a, b = self.a.astype(np.int64), self.b.astype(np.int64)
