@@ -1052,6 +1052,9 @@ __device__ void window_from_global(uint32_t* win, const uint64_t* Z, unsigned ta
 #ifndef GCD_BUILD_PARTS
 #define GCD_BUILD_PARTS 4  // 8 (warp 7 builds, publishes after) measured 15 % slower
 #endif
+#ifndef GCD_PUB_FIRST
+#define GCD_PUB_FIRST 1  // 8 parts: warp 7 publishes the meta words before its part
+#endif
 constexpr int BUILD_PARTS = GCD_BUILD_PARTS;
 static_assert(2 * (W1 / 4) == 32, "window builder: one (window, quad) per lane");
 static_assert(BUILD_PARTS <= GCD_T / 32, "window builder: one part per warp");
@@ -1233,8 +1236,11 @@ __device__ int head_cta(const GcdArgs& g, BatchMeta& ctl, StepLog* log, uint32_t
         }
         // next windows, top-aligned, from S_j and the batch matrix (with 8
         // parts warp 7 builds first and publishes after: the bulk has slack)
+        if (g.stats && threadIdx.x == 0) hx[0] += clock64() - t0;
+        if (BUILD_PARTS == 8 && GCD_PUB_FIRST && warp == 7) publish();
         if (warp < BUILD_PARTS) build_window_part(warp, red, Ps, hi_s, topA, topB, F);
-        if (BUILD_PARTS == 8 && warp == 7) publish();
+        if (g.stats && threadIdx.x == 0) hx[1] += clock64() - t0;
+        if (BUILD_PARTS == 8 && !GCD_PUB_FIRST && warp == 7) publish();
         if (g.stats && (g.dbg & 4)) {  // timing experiment: the same part again (warm)
             if (warp < BUILD_PARTS) build_window_part(warp, red, Ps, hi_s, topA, topB, F);
             if (threadIdx.x == 0) hx[3] += clock64() - t0;
@@ -1626,7 +1632,7 @@ void launch_gcd(const FieldParams& F, const uint32_t* a, int64_t na, const uint3
                 blocks, h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7], h[8], h[9]);
         fprintf(stderr,
                 "gcd latency: bulk0_seen_ns=%lld bulk0_warp_seen_ns=%lld bulk0_switch_ns=%lld "
-                "bulk0_barrier_ns=%lld spins=%lld head_prefetch_seen_ns=%lld (%lld) bulkLast_seen_ns=%lld replay_loop_exit_cyc=%lld bulkLast_done_ns=%lld fb_check=%lld fb_bar=%lld da0s=%lld unused=%lld\n",
+                "bulk0_barrier_ns=%lld spins=%lld head_prefetch_seen_ns=%lld (%lld) bulkLast_seen_ns=%lld replay_loop_exit_cyc=%lld bulkLast_done_ns=%lld build_start=%lld build_part_done=%lld windows_ready=%lld warm_rebuild=%lld\n",
                 h[12], h[13], h[14], h[15], h[16], h[17], h[19], h[18], h[10], h[20], h[21], h[22], h[23], h[24]);
     }
 }
