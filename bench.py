@@ -431,6 +431,8 @@ class GcdWork(Workload):
         self.steps_, self.updates, self.ng = gold["steps"], gold["updates"], gold["deg_g"] + 1
         self.config = {"workload": "cfg2_gcd_deg12288_deg12287_p469762049", "p": P,
                        "deg_a": len(self.a) - 1, "deg_b": len(self.b) - 1, "s": self.s,
+                       "s_effective": "61.6 eliminations per batch for s >= 64 (16384 in 266 batches, "
+                                      "MMM_GCD_STATS): the 64-word update matrix caps a batch",
                        "eliminations": self.steps_, "seed": 42, "parallelism": "replicas",
                        "l2": "flushed between timed steps (256 MB written then read: clean lines; inputs < L2)"}
 

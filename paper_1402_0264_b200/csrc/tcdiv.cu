@@ -27,8 +27,13 @@
 //   Q_K = T_h Z_K - M Q_{K-1},   M = T_h T_B1   (T_h: lower-triangular
 //   Toeplitz of h), where -M (128 x 128, per instance) sits in the compute
 // threads' registers -- M[r][m] = M[r-1][m-1] + h[r] B'[128 - m] builds it in
-// one diagonal walk per instance -- and -M Q_{K-1} plus L_{K+1} (phase A) run
-// as soon as Q_{K-1} is out, T_h Z_K (phase B) once S_K has been read.  After
+// one diagonal walk per instance -- and -M Q_{K-1} (phase A) runs as soon as
+// Q_{K-1} is out, T_h Z_K (phase B) once S_K has been read.  T_h is lower
+// triangular and L's matrix U (L_{K+1} = U Q_{K-1}) strictly upper, so the
+// two share one 128 x 128 pass: a thread whose 4 x 16 block lies above the
+// diagonal runs phase B's instruction stream on (B', Q_{K-1}) instead of
+// (h, Z_K); only the diagonal blocks' upper halves (<= 15 terms per row) are
+// formed separately (8 MACs per thread in phase A).  After
 // the last block one more tile completes Q B' and the remainder comes out of
 // TMEM in one pass.  Warps: 8 compute (the chain, the planes' reads, the
 // remainder), 4 builders (tiles; one lane issues each tile's 16 UMMAs once the
@@ -54,8 +59,9 @@ namespace {
 using namespace tct;
 
 constexpr int TCD_T = 256;    // compute warps 0-7: the chain
-constexpr int TCD_BLD = 128;  // builder warps 8-11: the tiles
-constexpr int TCD_ALL = TCD_T + TCD_BLD;  // twelve warps: three per SMSP, up to 168 registers
+constexpr int TCD_BLD = 96;   // builder warps 8-10: the tiles
+constexpr int TCD_ALL = TCD_T + TCD_BLD + 32;  // + warp 11: one lane issues the tiles' UMMAs
+                                                // (twelve warps: three per SMSP, up to 168 registers)
 constexpr int TCD_MAXA = 8192;
 constexpr int TCD_QPAD = 256;                           // zero words before Q
 constexpr int TCD_QWORDS = TCD_QPAD + TCD_MAXA + 256;   // Q, padded
@@ -213,8 +219,8 @@ __global__ void __maxnreg__(168) tcdiv_kernel(TcDivArgs g) {
     uint32_t* bnc = tmpB + 128;  // B'[128..256), then 128 zeros
     uint32_t* lateb = bnc + 256;  // L_{K+1} (see step K)
     uint32_t* partL = lateb + 128;  // [8][128] partials of L_{K+2}
-    __shared__ uint64_t full[2], empty[2], qready[2], hready;
-    __shared__ long long issue_ts[2];
+    __shared__ uint64_t full[2], empty[2], qready[2], built[2], hready;
+    __shared__ long long issue_ts[2], full_ts[2];
     __shared__ uint32_t tslot;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const FieldParams F = g.Fp;
@@ -234,6 +240,7 @@ __global__ void __maxnreg__(168) tcdiv_kernel(TcDivArgs g) {
     if (tid == 0) {
         for (int b = 0; b < 2; ++b) {
             tc::mbar_init(&full[b], 1);
+            tc::mbar_init(&built[b], 1);
             tc::mbar_init(&empty[b], 1);
             tc::mbar_init(&qready[b], 1);
         }
@@ -252,11 +259,10 @@ __global__ void __maxnreg__(168) tcdiv_kernel(TcDivArgs g) {
         // current one while the compute warps finish it (the first instance:
         // up front), into the other half of the h ping-pong.
         const int bt = tid - TCD_T;
-        uint32_t qph[2] = {0, 0}, eph[2] = {0, 0}, fph[2] = {0, 0};
+        uint32_t qph[2] = {0, 0}, eph[2] = {0, 0};
         long long bst[4] = {0, 0, 0, 0};
-        constexpr uint32_t ID_E = tc::idesc_u8(128, BROWS_E), ID_O = tc::idesc_u8(128, BROWS_O);
         uint32_t T = 0;
-        auto bsync = [] { asm volatile("bar.sync 2, 128;" ::: "memory"); };
+        auto bsync = [] { asm volatile("bar.sync 2, %0;" ::"n"(TCD_BLD) : "memory"); };
         // B'[0..256) of instance `which` into bpB and h[0] of its inverse
         auto inverse_begin = [&](int64_t which, uint32_t* hsn) {
             const uint32_t* bb = g.B + which * g.ldb;
@@ -289,17 +295,59 @@ __global__ void __maxnreg__(168) tcdiv_kernel(TcDivArgs g) {
                 bst[0] += tcd_clock() - tb;
                 tb = tcd_clock();
                 const int wb = bt >> 5, L = bt & 31;
-#pragma unroll
-                for (int i = 0; i < 2; ++i)
-                    build_unit(sH + b * HBUF, qz - TCM_APAD, K, 4 * (wb + 4 * i) + (L >> 3), L & 7);
+                // eight warp-units of 4 row groups x 8 chunks over the builder warps
+                for (int wu = wb; wu < 8; wu += TCD_BLD / 32)
+                    build_unit(sH + b * HBUF, qz - TCM_APAD, K, 4 * wu + (L >> 3), L & 7);
                 tc::fence_async_smem();
                 bsync();
                 bst[1] += tcd_clock() - tb;
                 tb = tcd_clock();
-                if (bt == 0) {
-                    // tile K's MMAs, once the compute warps have read block K+1 of the
-                    // planes (tile K must not land before that read)
+                if (bt == 0) tc::mbar_arrive(&built[b]);  // warp 11 issues tile K
+                bst[2] += tcd_clock() - tb;
+                tb = tcd_clock();
+                if (next && kn < 128) {
+                    newton_step(bpB, hsn, partB, tmpB, bt, F, kn, bsync);
+                    kn <<= 1;
+                    if (kn == 128 && bt == 0) tc::mbar_arrive(&hready);
+                }
+                bst[3] += tcd_clock() - tb;
+            }
+            if (next && kn < 128) {  // short instances: finish the doublings
+                for (; kn < 128; kn <<= 1) newton_step(bpB, hsn, partB, tmpB, bt, F, kn, bsync);
+                if (bt == 0) tc::mbar_arrive(&hready);
+            }
+        }
+        if (blockIdx.x == 0 && bt == 0) {
+            tcd_stats[8] = bst[0];
+            tcd_stats[9] = bst[1];
+            tcd_stats[11] = bst[3];
+        }
+    } else if (warp == (TCD_T + TCD_BLD) / 32) {
+        // ---- warp 11, one lane: tile K's 16 UMMAs once the builders have written it
+        //      and the compute warps have read block K+1 of the planes (tile K must
+        //      not land before that read).  The issue blocks while the tensor core's
+        //      queue is full (~1.8k cycles per tile), which is why it is not a
+        //      builder lane: the builders' Newton steps and next tile would wait. ----
+        if (lane == 0) {
+            constexpr uint32_t ID_E = tc::idesc_u8(128, BROWS_E), ID_O = tc::idesc_u8(128, BROWS_O);
+            uint32_t fph[2] = {0, 0}, bph[2] = {0, 0};
+            uint32_t T = 0;
+            long long mst[3] = {0, 0, 0};
+            for (int64_t inst = blockIdx.x; inst < g.count; inst += gridDim.x)
+                for (int K = 0; K <= Kq; ++K, ++T) {
+                    const int b = T & 1;
+                    long long tb = tcd_clock();
+                    tc::mbar_wait(&built[b], bph[b]);
+                    bph[b] ^= 1;
+                    mst[0] += tcd_clock() - tb;
+                    tb = tcd_clock();
                     tc::mbar_wait(&full[b], fph[b]);
+                    fph[b] ^= 1;
+                    if (TCD_STATS) {
+                        const long long tn = clock64();
+                        mst[1] += tn - tb;          // waited for the planes' read
+                        mst[2] += tn - full_ts[b];  // its arrive -> seen here
+                    }
                     tc::fence_after_sync();
                     const uint32_t hb = tc::smem_u32(sH + b * HBUF);
                     const bool odd = K & 1;
@@ -315,23 +363,13 @@ __global__ void __maxnreg__(168) tcdiv_kernel(TcDivArgs g) {
                     tc::commit(&empty[b]);
                     issue_ts[b] = tcd_clock();
                 }
-                fph[b] ^= 1;
-                bst[2] += tcd_clock() - tb;
-                tb = tcd_clock();
-                if (next && kn < 128) {
-                    newton_step(bpB, hsn, partB, tmpB, bt, F, kn, bsync);
-                    kn <<= 1;
-                    if (kn == 128 && bt == 0) tc::mbar_arrive(&hready);
-                }
-                bst[3] += tcd_clock() - tb;
-            }
-            if (next && kn < 128) {  // short instances: finish the doublings
-                for (; kn < 128; kn <<= 1) newton_step(bpB, hsn, partB, tmpB, bt, F, kn, bsync);
-                if (bt == 0) tc::mbar_arrive(&hready);
+            if (blockIdx.x == 0) {
+                tcd_stats[10] = mst[0];
+                tcd_stats[14] = mst[1];
+                tcd_stats[15] = mst[2];
             }
         }
-        if (blockIdx.x == 0 && bt == 0)
-            for (int i = 0; i < 4; ++i) tcd_stats[8 + i] = bst[i];
+        __syncwarp();
     } else {
         uint32_t eph[2] = {0, 0}, hph = 0;
         int pend[2] = {0, 0};
@@ -453,7 +491,11 @@ __global__ void __maxnreg__(168) tcdiv_kernel(TcDivArgs g) {
             bar();
             // thread (row group gq: rows 4 gq..4 gq+3, term part pq: terms 16 pq..16 pq+15)
             const int gq = tid & 31, pq = tid >> 5;
-            uint32_t mneg[4][16], hw[19];
+            const bool upper = pq > (gq >> 2);  // block (rows 4gq.., terms 16pq..) above the diagonal
+            // the diagonal blocks' strictly upper halves of U (phase A): thread = (row dr,
+            // half dh of the block's 16 terms), window xw[j] = X[dr - (dt0 + j)]
+            const int dr = tid >> 1, dh = tid & 1, dt0 = 16 * (dr >> 4) + 8 * dh;
+            uint32_t mneg[4][16], hw[19], xw[8];
             {
                 const uint32_t* Mst = reinterpret_cast<const uint32_t*>(sH);
 #pragma unroll
@@ -467,8 +509,14 @@ __global__ void __maxnreg__(168) tcdiv_kernel(TcDivArgs g) {
                         mneg[k][4 * jj + 2] = v.z;
                         mneg[k][4 * jj + 3] = v.w;
                     }
+                // this thread's Toeplitz window for the merged phase B (see step K):
+                // lower and diagonal blocks take h (zeros before it), strictly upper
+                // blocks X[j] = B'[256 + j] for j < 0, zero for j >= 0 (bnc + 128)
+                const uint32_t* wsrc = upper ? bnc + 128 : hs;
 #pragma unroll
-                for (int i = 0; i < 19; ++i) hw[i] = hs[4 * gq - 16 * pq - 15 + i];  // zeros before h
+                for (int i = 0; i < 19; ++i) hw[i] = wsrc[4 * gq - 16 * pq - 15 + i];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) xw[j] = bnc[128 + dr - dt0 - j];
             }
             if (tid < 128) {  // Z_0 = A'_0 (no planes, no corrections yet)
                 sS[tid] = aK;
@@ -480,18 +528,25 @@ __global__ void __maxnreg__(168) tcdiv_kernel(TcDivArgs g) {
 
             // Step K: Q_K = T_h Z_K - M Q_{K-1} with Z_K = A'_K - S_K - L_K in sS (the
             // planes hold tiles <= K-2, L_K = Q_{K-2}'s terms outside them, from the
-            // builder warps).  -M Q_{K-1} (phase A) is formed as soon as Q_{K-1} is
-            // out, T_h Z_K (phase B) once S_K has been read: 64 MACs per thread each.
+            // compute warps' upper-block threads in phase B).  -M Q_{K-1} (phase A) is
+            // formed as soon as Q_{K-1} is out, T_h Z_K and U Q_{K-1} (phase B) once S_K
+            // has been read: 64 MACs per thread each.
             uint32_t pm[4] = {0, 0, 0, 0};  // this thread's partials of -M Q_{K-1}
             const uint32_t ft = F.fold_terms;
             for (int K = 0; K < Kq; ++K, ++T) {
                 uint32_t* qk = qz + 128 * K;  // Q block K
                 {
                     TCD_T0();
+                    // T_h is lower triangular and L's matrix strictly upper: a thread whose
+                    // block lies above the diagonal has no T_h Z_K terms and forms its
+                    // part of L_{K+1} = U Q_{K-1} instead (same instruction stream, its
+                    // window holds B' and its vector is Q_{K-1}); the diagonal blocks'
+                    // L halves come from the previous step's phase A.
+                    const uint32_t* vsrc = upper ? qk - 128 : sS;
                     uint32_t z[16];
 #pragma unroll
                     for (int i = 0; i < 4; ++i) {
-                        const uint4 zv = *reinterpret_cast<const uint4*>(sS + 16 * pq + 4 * i);
+                        const uint4 zv = *reinterpret_cast<const uint4*>(vsrc + 16 * pq + 4 * i);
                         z[4 * i] = zv.x; z[4 * i + 1] = zv.y; z[4 * i + 2] = zv.z; z[4 * i + 3] = zv.w;
                     }
                     uint64_t a1[4] = {0, 0, 0, 0};
@@ -509,8 +564,11 @@ __global__ void __maxnreg__(168) tcdiv_kernel(TcDivArgs g) {
                     }
 #endif
 #pragma unroll
-                    for (int k = 0; k < 4; ++k)
-                        part[pq * 128 + 4 * gq + k] = reduce_t<FAST>(a1[k], F) + pm[k];
+                    for (int k = 0; k < 4; ++k) {
+                        const uint32_t rk = reduce_t<FAST>(a1[k], F);
+                        part[pq * 128 + 4 * gq + k] = (upper ? 0u : rk) + pm[k];
+                        if (upper) partL[pq * 128 + 4 * gq + k] = rk;
+                    }
                     bar();
                     TCD_ACC(6);
                 }
@@ -523,8 +581,13 @@ __global__ void __maxnreg__(168) tcdiv_kernel(TcDivArgs g) {
                         if (k1 < mu) fan_store<FAN>(g.Q, inst * g.ldq + (mu - 1 - k1), v1);
                     } else {
                         qk[tid] = 0;  // Q block K+1: zero until solved (the last tile reads it)
-                        if (K >= 1 && K + 1 < Kq)  // L_{K+1} from phase A of step K-1
-                            lateb[tid - 128] = partials_sum<FAST>(partL, 128, 128, tid - 128, F);
+                        if (K >= 1 && K + 1 < Kq) {  // L_{K+1} = U Q_{K-1}, row i
+                            const int i = tid - 128, pd = i >> 4;
+                            uint64_t v = partL[i];  // the diagonal block's part (step K-1's phase A)
+#pragma unroll
+                            for (int p = 1; p < 8; ++p) v += p > pd ? partL[p * 128 + i] : 0u;  // blocks above
+                            lateb[i] = reduce_t<FAST>(v, F);
+                        }
                     }
                     bar();
                     if (tid == 0) tc::mbar_arrive(&qready[T & 1]);  // the builders take tile K
@@ -538,39 +601,39 @@ __global__ void __maxnreg__(168) tcdiv_kernel(TcDivArgs g) {
                         const uint4 qv = *reinterpret_cast<const uint4*>(qk + 16 * pq + 4 * i);
                         q[4 * i] = qv.x; q[4 * i + 1] = qv.y; q[4 * i + 2] = qv.z; q[4 * i + 3] = qv.w;
                     }
-                    // L window: X[j] = B'[256 + j] for j < 0 (bnc + 128), zero for j >= 0;
-                    // lw[i] = X[4 gq - 16 pq - 16 + i]
-                    uint32_t lw[20];
+                    uint64_t a2[4] = {0, 0, 0, 0};
+                    // the diagonal blocks of U Q_K (L_{K+2}), 8 terms per thread
+                    uint64_t ad = 0;
+                    {
+                        const uint4 d0 = *reinterpret_cast<const uint4*>(qk + dt0);
+                        const uint4 d1 = *reinterpret_cast<const uint4*>(qk + dt0 + 4);
+                        const uint32_t dq[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
 #pragma unroll
-                    for (int i = 0; i < 5; ++i) {
-                        const uint4 v = *reinterpret_cast<const uint4*>(bnc + 128 + 4 * gq - 16 * pq - 16 + 4 * i);
-                        lw[4 * i] = v.x; lw[4 * i + 1] = v.y; lw[4 * i + 2] = v.z; lw[4 * i + 3] = v.w;
+                        for (int j = 0; j < 8; ++j) {
+                            ad = mad_wide(xw[j], dq[j], ad);
+                            if (!FAST && ft < 8) ad = fold(ad, F);
+                        }
                     }
-                    uint64_t a2[4] = {0, 0, 0, 0}, a3[4] = {0, 0, 0, 0};
 #ifndef TCD_NOMV
 #pragma unroll
                     for (int j = 0; j < 16; ++j) {
 #pragma unroll
                         for (int k = 0; k < 4; ++k) {
                             a2[k] = mad_wide(mneg[k][j], q[j], a2[k]);
-                            a3[k] = mad_wide(lw[k - j + 16], q[j], a3[k]);  // L_{K+2}: Q_K's late terms
-                            if (!FAST && ft < 4) {
-                                a2[k] = fold(a2[k], F);
-                                a3[k] = fold(a3[k], F);
-                            }
+                            if (!FAST && ft < 4) a2[k] = fold(a2[k], F);
                         }
                         if (!FAST && ft >= 4 && ft < 16 && (j & 3) == 3)
 #pragma unroll
-                            for (int k = 0; k < 4; ++k) {
-                                a2[k] = fold(a2[k], F);
-                                a3[k] = fold(a3[k], F);
-                            }
+                            for (int k = 0; k < 4; ++k) a2[k] = fold(a2[k], F);
                     }
 #endif
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) {
+                    for (int k = 0; k < 4; ++k)
                         pm[k] = FAST ? redc(fold(a2[k], F), F) : reduce(a2[k], F);  // M: Montgomery
-                        partL[pq * 128 + 4 * gq + k] = reduce_t<FAST>(a3[k], F);
+                    {
+                        uint32_t dv = reduce_t<FAST>(ad, F);
+                        dv += __shfl_xor_sync(0xffffffffu, dv, 1);  // the row's two halves (< 2p)
+                        if (!dh) partL[dr] = dv;
                     }
                     TCD_ACC(7);
                 }
@@ -603,7 +666,10 @@ __global__ void __maxnreg__(168) tcdiv_kernel(TcDivArgs g) {
                         tc::fence_before_sync();
                     }
                     bar();
-                    if (tid == 0) tc::mbar_arrive(&full[T & 1]);  // the builders may issue tile K
+                    if (tid == 0) {
+                        if (TCD_STATS) full_ts[T & 1] = clock64();
+                        tc::mbar_arrive(&full[T & 1]);  // warp 11 may issue tile K
+                    }
                     ++pend[T & 1];
                     TCD_ACC(2);
                 }
@@ -611,6 +677,7 @@ __global__ void __maxnreg__(168) tcdiv_kernel(TcDivArgs g) {
             long long tq = tcd_clock();
             // ---- the last tile (Q_{Kq-1}'s upper triangle), then the remainder ----
             if (tid == 0) {
+                if (TCD_STATS) full_ts[T & 1] = clock64();
                 tc::mbar_arrive(&qready[T & 1]);
                 tc::mbar_arrive(&full[T & 1]);
             }
@@ -717,8 +784,8 @@ void launch_tcdiv_batched(const FieldParams& F, const uint32_t* A, int64_t lda, 
         MMM_CUDA(cudaMemcpyFromSymbolAsync(h, tcd_stats, sizeof(h), 0, cudaMemcpyDeviceToHost, st));
         MMM_CUDA(cudaStreamSynchronize(st));
         fprintf(stderr, "tcdiv stats (CTA 0, thread 0): prologue=%lld h_wait=%lld tmem+Z=%lld "
-                "M=%lld Qsum=%lld tail=%lld MV_B=%lld MV_A=%lld cycles | builders: wait_q=%lld build=%lld issue=%lld newton+late=%lld | mma_wait=%lld issue_to_done=%lld\n",
-                h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7], h[8], h[9], h[10], h[11], h[12], h[13]);
+                "M=%lld Qsum=%lld tail=%lld MV_B=%lld MV_A=%lld cycles | builders: wait_q=%lld build=%lld (issuer: wait_built=%lld) newton=%lld | mma_wait=%lld issue_to_done=%lld | issuer: full_wait=%lld full_arrive_to_seen=%lld\n",
+                h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7], h[8], h[9], h[10], h[11], h[12], h[13], h[14], h[15]);
     }
 }
 
