@@ -239,7 +239,7 @@ __global__ void __maxnreg__(168) tcdiv_kernel(TcDivArgs g) {
     if (warp == 0) tc::tmem_alloc<512>(&tslot);
     if (tid == 0) {
         for (int b = 0; b < 2; ++b) {
-            tc::mbar_init(&full[b], 1);
+            tc::mbar_init(&full[b], 4);  // compute warps 0-3, once their rows are read
             tc::mbar_init(&built[b], 1);
             tc::mbar_init(&empty[b], 1);
             tc::mbar_init(&qready[b], 1);
@@ -297,7 +297,7 @@ __global__ void __maxnreg__(168) tcdiv_kernel(TcDivArgs g) {
                 const int wb = bt >> 5, L = bt & 31;
                 // eight warp-units of 4 row groups x 8 chunks over the builder warps
                 for (int wu = wb; wu < 8; wu += TCD_BLD / 32)
-                    build_unit(sH + b * HBUF, qz - TCM_APAD, K, 4 * wu + (L >> 3), L & 7);
+                    build_unit<true>(sH + b * HBUF, qz - TCM_APAD, K, 4 * wu + (L >> 3), L & 7);
                 tc::fence_async_smem();
                 bsync();
                 bst[1] += tcd_clock() - tb;
@@ -492,6 +492,7 @@ __global__ void __maxnreg__(168) tcdiv_kernel(TcDivArgs g) {
             // thread (row group gq: rows 4 gq..4 gq+3, term part pq: terms 16 pq..16 pq+15)
             const int gq = tid & 31, pq = tid >> 5;
             const bool upper = pq > (gq >> 2);  // block (rows 4gq.., terms 16pq..) above the diagonal
+            const int qx = (pq >> 1) & 3;       // slot swizzle of Q's words 16 pq .. 16 pq + 15
             // the diagonal blocks' strictly upper halves of U (phase A): thread = (row dr,
             // half dh of the block's 16 terms), window xw[j] = X[dr - (dt0 + j)]
             const int dr = tid >> 1, dh = tid & 1, dt0 = 16 * (dr >> 4) + 8 * dh;
@@ -546,7 +547,7 @@ __global__ void __maxnreg__(168) tcdiv_kernel(TcDivArgs g) {
                     uint32_t z[16];
 #pragma unroll
                     for (int i = 0; i < 4; ++i) {
-                        const uint4 zv = *reinterpret_cast<const uint4*>(vsrc + 16 * pq + 4 * i);
+                        const uint4 zv = *reinterpret_cast<const uint4*>(vsrc + 16 * pq + 4 * (i ^ (upper ? qx : 0)));
                         z[4 * i] = zv.x; z[4 * i + 1] = zv.y; z[4 * i + 2] = zv.z; z[4 * i + 3] = zv.w;
                     }
                     uint64_t a1[4] = {0, 0, 0, 0};
@@ -577,7 +578,7 @@ __global__ void __maxnreg__(168) tcdiv_kernel(TcDivArgs g) {
                     if (tid < 128) {
                         const int k1 = 128 * K + tid;
                         const uint32_t v1 = k1 < mu ? partials_sum<FAST>(part, 128, 128, tid, F) : 0u;
-                        qk[tid] = v1;
+                        qk[swz_word(tid)] = v1;  // Q is stored slot-swizzled (tctile.cuh, build_unit)
                         if (k1 < mu) fan_store<FAN>(g.Q, inst * g.ldq + (mu - 1 - k1), v1);
                     } else {
                         qk[tid] = 0;  // Q block K+1: zero until solved (the last tile reads it)
@@ -598,15 +599,15 @@ __global__ void __maxnreg__(168) tcdiv_kernel(TcDivArgs g) {
                     uint32_t q[16];
 #pragma unroll
                     for (int i = 0; i < 4; ++i) {
-                        const uint4 qv = *reinterpret_cast<const uint4*>(qk + 16 * pq + 4 * i);
+                        const uint4 qv = *reinterpret_cast<const uint4*>(qk + 16 * pq + 4 * (i ^ qx));
                         q[4 * i] = qv.x; q[4 * i + 1] = qv.y; q[4 * i + 2] = qv.z; q[4 * i + 3] = qv.w;
                     }
                     uint64_t a2[4] = {0, 0, 0, 0};
                     // the diagonal blocks of U Q_K (L_{K+2}), 8 terms per thread
                     uint64_t ad = 0;
                     {
-                        const uint4 d0 = *reinterpret_cast<const uint4*>(qk + dt0);
-                        const uint4 d1 = *reinterpret_cast<const uint4*>(qk + dt0 + 4);
+                        const uint4 d0 = *reinterpret_cast<const uint4*>(qk + swz_word(dt0));
+                        const uint4 d1 = *reinterpret_cast<const uint4*>(qk + swz_word(dt0 + 4));
                         const uint32_t dq[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
 #pragma unroll
                         for (int j = 0; j < 8; ++j) {
@@ -650,6 +651,17 @@ __global__ void __maxnreg__(168) tcdiv_kernel(TcDivArgs g) {
                         st[9] += te - tw;                              // waited for tile K-1
                         if (K > 0) st[10] += te - issue_ts[(T + 1) & 1];  // its issue -> seen done
                     }
+                    // warp 11 may issue tile K as soon as block K+1 is in registers (the
+                    // planes' rows of warps 0-3): full[] counts those four warps, so the
+                    // tensor core restarts while Z_{K+1} is still being formed
+                    auto release_tile = [&] {
+                        tc::fence_before_sync();
+                        __syncwarp();
+                        if (lane == 0) {
+                            if (TCD_STATS && tid == 0) full_ts[T & 1] = clock64();
+                            tc::mbar_arrive(&full[T & 1]);
+                        }
+                    };
                     if (K + 1 < Kq) {
                         tc::fence_after_sync();
                         if (warp < 4) {
@@ -657,6 +669,7 @@ __global__ void __maxnreg__(168) tcdiv_kernel(TcDivArgs g) {
 #pragma unroll
                             for (int s = 0; s < 7; ++s) x[s] = tmem_ld1(lane_addr + 64 * s + K + 1);
                             tc::tmem_ld_wait();
+                            release_tile();
                             uint32_t zz = submod(aK, combine_planes(x, g.c_hi, F), F);
                             if (K + 1 >= 2) zz = submod(zz, lateb[tid], F);
                             sS[tid] = zz;
@@ -664,12 +677,10 @@ __global__ void __maxnreg__(168) tcdiv_kernel(TcDivArgs g) {
                             aK = kn < na ? __ldg(a + (na - 1 - kn)) : 0u;
                         }
                         tc::fence_before_sync();
+                    } else if (warp < 4) {
+                        release_tile();
                     }
                     bar();
-                    if (tid == 0) {
-                        if (TCD_STATS) full_ts[T & 1] = clock64();
-                        tc::mbar_arrive(&full[T & 1]);  // warp 11 may issue tile K
-                    }
                     ++pend[T & 1];
                     TCD_ACC(2);
                 }
@@ -679,8 +690,8 @@ __global__ void __maxnreg__(168) tcdiv_kernel(TcDivArgs g) {
             if (tid == 0) {
                 if (TCD_STATS) full_ts[T & 1] = clock64();
                 tc::mbar_arrive(&qready[T & 1]);
-                tc::mbar_arrive(&full[T & 1]);
             }
+            if (warp < 4 && lane == 0) tc::mbar_arrive(&full[T & 1]);
             ++pend[T & 1];
             ++T;
             // r[na-1-k] = A'[k] - (Q B')[k], k in [mu, na): 8 blocks per TMEM load, the

@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(TCM_T + 32, 1) tcmul_kernel(TcArgs g) {
             t0 = clock64();
             const uint32_t* a = g.A + inst * g.lda;
             const uint32_t* b = g.B + inst * g.ldb;
-            stage_words(a_pad + TCM_APAD, a, 0, na, na, tid, TCM_T);
+            stage_words<true>(a_pad + TCM_APAD, a, 0, na, na, tid, TCM_T);
             // B rows 64 v + j; unit = (j, chunk c)
             for (int u = tid; u < mB * 8; u += TCM_T) {
                 const int j = u >> 3, c = u & 7;
@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(TCM_T + 32, 1) tcmul_kernel(TcArgs g) {
                 const long long tw = clock64();
                 free_buf(bb);
                 t_mmawait += clock64() - tw;
-                build_h(sH + bb * HBUF, a_pad, d);
+                build_h<true>(sH + bb * HBUF, a_pad, d);
                 tc::fence_async_smem();
                 tc::fence_before_sync();
                 bar();
@@ -343,7 +343,7 @@ __global__ void __launch_bounds__(TCM_T + 32, 1) tcmul_split_kernel(TcSplitArgs 
             const uint32_t* b = g.b + int64_t(TCM_MAXN) * it.ib;
             // the window of a the tiles d0..d1-1 read: [128 d0 - 128, 128 d1)
             const int lo = max(0, 128 * it.d0 - 128), hi = min(TCM_MAXN + 128, 128 * it.d1);
-            stage_words(a_pad + TCM_APAD, a, lo, hi, it.na_i, tid, TCM_T);
+            stage_words<true>(a_pad + TCM_APAD, a, lo, hi, it.na_i, tid, TCM_T);
             const int mB = (it.nb_j + 127) >> 7;
             for (int u = tid; u < 32 * 8; u += TCM_T) {  // all 32 block rows (zeros past mB)
                 const int j = u >> 3, c = u & 7;
@@ -369,7 +369,7 @@ __global__ void __launch_bounds__(TCM_T + 32, 1) tcmul_split_kernel(TcSplitArgs 
             for (int d = it.d0; d < it.d1; ++d, ++T) {
                 const int bb = T & 1;
                 free_buf(bb);
-                build_h(sH + bb * HBUF, a_pad, d);
+                build_h<true>(sH + bb * HBUF, a_pad, d);
                 tc::fence_async_smem();
                 tc::fence_before_sync();
                 bar();

@@ -68,14 +68,22 @@ __device__ __forceinline__ void put_row_chunk(uint8_t* h, uint32_t tile_stride, 
 // tiles of H_d: row r = 4 rg + k needs a[i0 + k - t'], t' = 0..15,
 // i0 = 128 d + 4 rg - 16 c: words a[i0 - 16 .. i0 + 3] (20, 16-byte aligned
 // with the pad of 128).
+// SWZ: the words are stored with swz_word() (a_pad 128-word aligned): the eight
+// lanes of a quarter-warp (one row group, chunks 0..7) read 16-byte slots 64
+// bytes apart, a 4-way bank conflict in the plain layout (measured: 12 excess
+// wavefronts per load), none with the slots of each 128-byte line XORed by the
+// line index.
+__device__ __forceinline__ int swz_word(int w) { return w ^ (((w >> 5) & 3) << 2); }
+template <bool SWZ = false>
 __device__ __forceinline__ void build_unit(uint8_t* hbuf, const uint32_t* a_pad, int d, int rg,
                                            int c) {
     const int i0 = 128 * d + 4 * rg - 16 * c;
-    const uint4* src = reinterpret_cast<const uint4*>(a_pad + TCM_APAD + i0 - 16);
+    const int w0 = TCM_APAD + i0 - 16;
+    const uint4* src = reinterpret_cast<const uint4*>(a_pad + w0);
     uint32_t x[20];
 #pragma unroll
     for (int q = 0; q < 5; ++q) {
-        const uint4 v = src[q];
+        const uint4 v = SWZ ? *reinterpret_cast<const uint4*>(a_pad + swz_word(w0 + 4 * q)) : src[q];
         x[4 * q] = v.x;
         x[4 * q + 1] = v.y;
         x[4 * q + 2] = v.z;
@@ -93,9 +101,10 @@ __device__ __forceinline__ void build_unit(uint8_t* hbuf, const uint32_t* a_pad,
 // H_d limb tiles by 256 threads: thread (warp w, lane L) builds rows
 // 4 rg .. 4 rg + 3 of chunk c, rg = 4 w + L / 8, c = L % 8 (conflict-free loads
 // and swizzled stores).
+template <bool SWZ = false>
 __device__ __forceinline__ void build_h(uint8_t* hbuf, const uint32_t* a_pad, int d) {
     const int w = threadIdx.x >> 5, L = threadIdx.x & 31;
-    build_unit(hbuf, a_pad, d, 4 * w + (L >> 3), L & 7);
+    build_unit<SWZ>(hbuf, a_pad, d, 4 * w + (L >> 3), L & 7);
 }
 
 __device__ __forceinline__ void tmem_st32_zero(uint32_t taddr) {
@@ -135,6 +144,8 @@ __device__ __forceinline__ void load16(const uint32_t* p, int valid, uint32_t (&
 
 // a_pad[base + i] = a[i] for i in [lo, hi) (zero where i >= n), 16-byte loads
 // and stores where a and the range allow (lo a multiple of 4).
+// SWZ: stored with swz_word() (dst a multiple of 128 words past the swizzle's origin).
+template <bool SWZ = false>
 __device__ __forceinline__ void stage_words(uint32_t* dst, const uint32_t* a, int lo, int hi, int n,
                                             int tid, int nthreads) {
     if ((reinterpret_cast<uintptr_t>(a) & 15) == 0 && (lo & 3) == 0 &&
@@ -149,15 +160,17 @@ __device__ __forceinline__ void stage_words(uint32_t* dst, const uint32_t* a, in
                 v.z = i + 2 < n ? __ldg(a + i + 2) : 0u;
                 v.w = i + 3 < n ? __ldg(a + i + 3) : 0u;
             }
+            const int is = SWZ ? swz_word(i) : i;
             if (i + 4 <= hi) {
-                *reinterpret_cast<uint4*>(dst + i) = v;
+                *reinterpret_cast<uint4*>(dst + is) = v;
             } else {
                 const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
-                for (int q = 0; i + q < hi; ++q) dst[i + q] = vv[q];
+                for (int q = 0; i + q < hi; ++q) dst[is + q] = vv[q];
             }
         }
     } else {
-        for (int i = lo + tid; i < hi; i += nthreads) dst[i] = i < n ? __ldg(a + i) : 0u;
+        for (int i = lo + tid; i < hi; i += nthreads)
+            dst[SWZ ? swz_word(i) : i] = i < n ? __ldg(a + i) : 0u;
     }
 }
 
