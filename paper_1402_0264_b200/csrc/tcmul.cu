@@ -65,9 +65,11 @@ __device__ long long tcm_stats[8];
 template <bool FAN>
 __global__ void __launch_bounds__(TCM_T + 32, 1) tcmul_kernel(TcArgs g) {
     extern __shared__ uint8_t smem_raw[];
-    // Aligned through an integer on purpose: the tile build then uses generic
-    // ST/LD, measured 6% faster here than LDS/STS (tools/ab.py, 1.42 vs 1.51 ms
-    // for cfg5's products); tcdiv is the other way round (tc::align_smem_1024).
+    // Aligned through an integer: the tile build then uses generic ST/LD, which
+    // measured 6% faster here than LDS/STS while the build's loads were bank
+    // conflicted (1.42 vs 1.51 ms for cfg5's products) and the same since the
+    // Toeplitz words are stored slot-swizzled (1.157 ms either way: the tile
+    // stream runs at the tensor core's rate); tcdiv uses tc::align_smem_1024.
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
     uint8_t* sH = sm + OFF_H;
