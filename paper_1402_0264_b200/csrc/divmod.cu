@@ -515,7 +515,14 @@ __device__ void pipe_head_split(const PipeArgs& g, uint32_t* sm, int nbulk) {
             bar_arrive_n(BAR_LAM + int(j & 1), PIPE_T);
             const long long p1 = clock64();
             c_lam += p1 - p0;
-            if (j >= 1) bar_sync_n(BAR_ENT + int((j - 1) & 1), CT);  // E_{j-1} complete
+            // E_{j-1} complete; either barrier also orders group A's lambda stores (lj)
+            // before the window pass reads them -- at j = 0 nothing else did, and a
+            // delayed warp (another kernel sharing the SM) then updated the window with
+            // stale zeros: step 0's quotient right, every later word wrong
+            if (j >= 1)
+                bar_sync_n(BAR_ENT + int((j - 1) & 1), CT);
+            else
+                bar_sync_n(BAR_A, AT);
             const long long p2 = clock64();
             c_wait += p2 - p1;
             // window (t in [v, WH)): step j
@@ -1062,6 +1069,9 @@ __device__ void pipe_bulk(const PipeArgs& g, uint32_t* sm, int nbulk, int me) {
                     __stcg(g.A + xp, addmod(a_old, reduce(sum, F), F));
                 }
             }
+            // the partial sums are read: the next block's may be written (with b read
+            // in place nothing else separates the two; uniform over the CTA)
+            if (beta + nbulk < nblocks) __syncthreads();
         }
         __syncthreads();
         const long long tr = clock64();

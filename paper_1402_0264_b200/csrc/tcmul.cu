@@ -142,16 +142,52 @@ __global__ void __launch_bounds__(TCM_T + 32, 1) tcmul_kernel(TcArgs g) {
         };
         auto bar = [] { asm volatile("bar.sync 1, 256;" ::: "memory"); };
         long long t_pro = 0, t_loop = 0, t_epi = 0, t_mmawait = 0, t0, t1;
+        // Rows whose words can be moved as whole 16-byte groups: each thread then holds
+        // the next instance's share of a and b (4 + 4 groups) in registers, loaded while
+        // the current instance's tiles run, so the prologue does not wait for HBM.
+        const bool pre_ok = (reinterpret_cast<uintptr_t>(g.A) & 15) == 0 &&
+                            (reinterpret_cast<uintptr_t>(g.B) & 15) == 0 && (g.lda & 3) == 0 &&
+                            (g.ldb & 3) == 0 && (na & 3) == 0 && (nb & 3) == 0;
+        uint4 pa[4], pb[4];
+        auto prefetch_rows = [&](int64_t which) {
+            const uint32_t* a = g.A + which * g.lda;
+            const uint32_t* b = g.B + which * g.ldb;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int ia = 4 * tid + 4 * TCM_T * q, ib = 16 * tid + 4 * q;
+                pa[q] = ia < na ? __ldg(reinterpret_cast<const uint4*>(a + ia)) : make_uint4(0, 0, 0, 0);
+                pb[q] = ib < nb ? __ldg(reinterpret_cast<const uint4*>(b + ib)) : make_uint4(0, 0, 0, 0);
+            }
+        };
+        if (pre_ok && int64_t(blockIdx.x) < g.count) prefetch_rows(blockIdx.x);
         for (int64_t inst = blockIdx.x; inst < g.count; inst += gridDim.x) {
             t0 = clock64();
             const uint32_t* a = g.A + inst * g.lda;
             const uint32_t* b = g.B + inst * g.ldb;
-            stage_words<true>(a_pad + TCM_APAD, a, 0, na, na, tid, TCM_T);
+            if (pre_ok) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int ia = 4 * tid + 4 * TCM_T * q;
+                    if (ia < na) *reinterpret_cast<uint4*>(a_pad + TCM_APAD + swz_word(ia)) = pa[q];
+                }
+            } else {
+                stage_words<true>(a_pad + TCM_APAD, a, 0, na, na, tid, TCM_T);
+            }
             // B rows 64 v + j; unit = (j, chunk c)
             for (int u = tid; u < mB * 8; u += TCM_T) {
                 const int j = u >> 3, c = u & 7;
                 uint32_t wv[16];
-                load16(b + 128 * j + 16 * c, nb - (128 * j + 16 * c), wv);
+                if (pre_ok) {  // u == tid: words b[16 u .. 16 u + 15]
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        wv[4 * q] = pb[q].x;
+                        wv[4 * q + 1] = pb[q].y;
+                        wv[4 * q + 2] = pb[q].z;
+                        wv[4 * q + 3] = pb[q].w;
+                    }
+                } else {
+                    load16(b + 128 * j + 16 * c, nb - (128 * j + 16 * c), wv);
+                }
                 uint32_t L[4][4];
 #pragma unroll
                 for (int q = 0; q < 4; ++q)
@@ -161,6 +197,7 @@ __global__ void __launch_bounds__(TCM_T + 32, 1) tcmul_kernel(TcArgs g) {
                 for (int v = 0; v < 4; ++v)
                     sts128(sBE, tc::sw128(64 * v + j, 16 * c), L[v][0], L[v][1], L[v][2], L[v][3]);
             }
+            if (pre_ok && inst + gridDim.x < g.count) prefetch_rows(inst + gridDim.x);
             if (warp < 4) {
 #pragma unroll
                 for (int c0 = 0; c0 < 512; c0 += 32)

@@ -216,11 +216,23 @@ def test_scratch_across_streams_and_threads(cuda_lib, port):
 
     def worker(k):
         try:
-            for a, b, (wq, wr) in cases[k:] + cases[:k]:
+            for i, (a, b, (wq, wr)) in enumerate(cases[k:] + cases[:k]):
                 q, r = mmm.divmod(a, b, P, s=64)
-                assert np.array_equal(q, wq) and np.array_equal(r, wr)
-                assert np.array_equal(mmm.mul(a[:3000], b[:2000], P),
-                                      port.mul(a[:3000], b[:2000], P))
+                if not (np.array_equal(q, wq) and np.array_equal(r, wr)):
+                    dq = np.nonzero(q != wq)[0] if len(q) == len(wq) else np.array([-1])
+                    dr = np.nonzero(r != wr)[0] if len(r) == len(wr) else np.array([-1])
+                    q2, r2 = mmm.divmod(a, b, P, s=64)  # diagnostics: transient or not
+                    again = np.array_equal(q2, wq) and np.array_equal(r2, wr)
+                    same_a = np.array_equal(r, a[: len(r)]) if len(r) <= len(a) else None
+                    raise AssertionError(f"thread {k} call {i}: divmod differs: q {len(q)}/{len(wq)} at "
+                                         f"{dq[:4]}..{dq[-4:]} ({len(dq)}), r {len(r)}/{len(wr)} at "
+                                         f"{dr[:4]}..{dr[-4:]} ({len(dr)}); retry ok={again}; "
+                                         f"r==a[:nr] {same_a}; q[-66:-62]={q[-66:-62]} want {wq[-66:-62]}; "
+                                         f"r[:3]={r[:3]} want {wr[:3]} a[:3]={a[:3]}")
+                m, wm = mmm.mul(a[:3000], b[:2000], P), port.mul(a[:3000], b[:2000], P)
+                if not np.array_equal(m, wm):
+                    dm = np.nonzero(m != wm)[0] if len(m) == len(wm) else np.array([-1])
+                    raise AssertionError(f"thread {k}: mul differs at {dm[:4]}..{dm[-4:]} ({len(dm)})")
             mmm.release_scratch()
         except Exception as e:  # noqa: BLE001
             errs.append(e)
