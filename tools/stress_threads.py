@@ -22,9 +22,30 @@ cases = []
 for _ in range(4):
     a, b = rand(20000), rand(9000)
     cases.append((a, b, port.divmod(a, b, P), port.mul(a[:3000], b[:2000], P)))
+gcases = []
+if mode == "gcd":
+    for _ in range(2):
+        gg, u, v = rand(1200), rand(2400), rand(2399)
+        ga, gb = port.mul(gg, u, P), port.mul(gg, v, P)
+        gcases.append((ga, gb, port.gcd(ga, gb, P)))
 bad = []
 def worker(k, rd):
     try:
+        if mode == "gcd":  # two threads run GCDs, two run products and divisions beside them
+            for i in range(3):
+                if k < 2:
+                    ga, gb, wg = gcases[(k + i) % 2]
+                    got = mmm.gcd(ga, gb, P, s=s)
+                    if not np.array_equal(got, wg):
+                        bad.append(("gcd", rd, k, i, len(got), len(wg)))
+                else:
+                    a, b, (wq, wr), wm = cases[(k + i) % 4]
+                    if not np.array_equal(mmm.mul(a[:3000], b[:2000], P), wm):
+                        bad.append(("mul-beside-gcd", rd, k, i))
+                    q, r = mmm.divmod(a, b, P, s=128)
+                    if not (np.array_equal(q, wq) and np.array_equal(r, wr)):
+                        bad.append(("div-beside-gcd", rd, k, i))
+            return
         for i, (a, b, (wq, wr), wm) in enumerate(cases[k:] + cases[:k]):
             if mode in ("both", "div"):
                 q, r = mmm.divmod(a, b, P, s=s)
