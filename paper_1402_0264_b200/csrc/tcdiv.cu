@@ -36,12 +36,15 @@
 // formed separately (8 MACs per thread in phase A).  After
 // the last block one more tile completes Q B' and the remainder comes out of
 // TMEM in one pass.  Warps: 8 compute (the chain, the planes' reads, the
-// remainder), 4 builders (tiles; one lane issues each tile's 16 UMMAs once the
-// compute warps have read the block the tile would disturb; the next
-// instance's h by Newton).  Shapes: na <= 8192, nb <= 4096 (cfg5: 8192 / 4096).
-// (Measured alternatives, tools/ab.py on cfg5: L on the builder warps 3.44 ms
-// vs 2.82 ms here -- the builders then bound the step; a dedicated MMA warp
-// needs 13 warps, i.e. <= 128 registers, too few for M in registers.)
+// remainder), 3 builders (tiles; the next instance's h by Newton) and one
+// issuer (warp 11, one lane: each tile's 16 UMMAs once the tile is written and
+// the compute warps have read the block it would disturb -- the issues block
+// ~1.8k cycles per tile on the tensor core's queue, which stalled the builders
+// while a builder lane issued).  Shapes: na <= 8192, nb <= 4096 (cfg5).
+// (Measured alternatives, tools/ab.py on cfg5: L on the builder
+// warps 3.44 ms; a 13th warp puts four warps on one SMSP, i.e. <= 128
+// registers, too few for M in registers; polling hand-offs, a tile build split
+// at the diagonal, byte-window tile rows: all slower than the 2.46 ms here.)
 #include <cuda_runtime.h>
 
 #include <algorithm>
